@@ -1,0 +1,398 @@
+"""TEST INFRASTRUCTURE ONLY -- ctypes view of the CPU oracle (xconv_oracle.cpp).
+
+The oracle is a double-precision restatement of the reference 2D path
+(/root/reference/proj/include/xconv/*.hpp, see the citations in
+xconv_oracle.cpp).  Only tests/, __graft_entry__.smoke() and bench.py's CPU
+baseline legs import this module; the product package never does.
+
+Grids are numpy arrays indexed [y, x] (the reference's values(y, x)).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "build", "liboracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with its Makefile (gcc/g++ only)."""
+    if force or not os.path.exists(_LIB_PATH):
+        subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return _LIB_PATH
+
+
+class _OrFilter(C.Structure):
+    _fields_ = [
+        ("group", C.c_int), ("K", C.c_int), ("nc", C.c_int),
+        ("ks", C.POINTER(C.c_int)), ("comps", C.POINTER(C.c_double)),
+        ("n_radii", C.c_int), ("n_angles", C.c_int),
+        ("r_max", C.c_double), ("r_min", C.c_double), ("r_domain", C.c_double),
+    ]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            build()
+        L = C.CDLL(_LIB_PATH)
+        L.or_last_error.restype = C.c_char_p
+        L.or_rng_new.restype = C.c_void_p
+        L.or_rng_new.argtypes = [C.c_uint64]
+        L.or_rng_free.argtypes = [C.c_void_p]
+        L.or_rng_next.restype = C.c_uint64
+        L.or_rng_next.argtypes = [C.c_void_p]
+        L.or_rng_uniform.restype = C.c_double
+        L.or_rng_uniform.argtypes = [C.c_void_p, C.c_double, C.c_double]
+        for name in ("or_random_field", "or_random_smooth_filter", "or_annular_filter",
+                     "or_random_rotation_field", "or_random_scale_field"):
+            getattr(L, name).restype = None
+        _lib = L
+    return _lib
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _ip(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_int))
+
+
+def _c128(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.complex128))
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _check(rc: int):
+    if rc == 2:
+        raise ValueError(lib().or_last_error().decode())
+    if rc != 0:
+        raise RuntimeError(lib().or_last_error().decode())
+
+
+@dataclass
+class Filter:
+    """FreqFilter2 (freq_filter.hpp:21-46); comps is (n_rows, nc) complex."""
+    group: int
+    K: int
+    ks: np.ndarray
+    comps: np.ndarray
+    n_radii: int
+    n_angles: int
+    r_max: float
+    r_min: float = 0.0
+    r_domain: float = 0.0
+    _keep: list = field(default_factory=list, repr=False)
+
+    def n_components(self) -> int:
+        return len(self.ks)
+
+    def index_of(self, k: int) -> int:
+        return int(np.nonzero(np.asarray(self.ks) == k)[0][0])
+
+    def domain_top(self) -> float:
+        return self.r_domain if self.r_domain > 0 else self.r_max
+
+    def omega(self) -> float:
+        return 2.0 * np.pi / np.log(self.domain_top() / self.r_min)
+
+
+def _cfilter(F) -> _OrFilter:
+    ks = np.ascontiguousarray(np.asarray(F.ks, dtype=np.int32))
+    comps = _c128(F.comps)
+    s = _OrFilter(int(F.group), int(F.K), len(ks), _ip(ks), _dp(comps.view(np.float64)),
+                  int(F.n_radii), int(F.n_angles), float(F.r_max), float(F.r_min),
+                  float(F.r_domain))
+    s._keep = (ks, comps)  # keep buffers alive
+    return s
+
+
+# ----------------------------------------------------------------- FFT layer
+
+def next_fast_size(n: int) -> int:
+    return lib().or_next_fast_size(int(n))
+
+
+def fft2(a, inverse=False) -> np.ndarray:
+    a = _c128(a).copy()
+    lib().or_fft2(_dp(a.view(np.float64)), a.shape[0], a.shape[1], int(inverse))
+    return a
+
+
+def filter2_fft(sig, filt, fcx, fcy, correlate, periodic=False) -> np.ndarray:
+    sig, filt = _c128(sig), _c128(filt)
+    out = np.zeros_like(sig)
+    lib().or_filter2_fft(_dp(sig.view(np.float64)), sig.shape[0], sig.shape[1],
+                         _dp(filt.view(np.float64)), filt.shape[0], filt.shape[1],
+                         int(fcx), int(fcy), int(correlate), int(periodic),
+                         _dp(out.view(np.float64)))
+    return out
+
+
+def correlate_direct(H, F, fcx, fcy) -> np.ndarray:
+    H, F = _c128(H), _c128(F)
+    out = np.zeros_like(H)
+    lib().or_correlate_direct(_dp(H.view(np.float64)), H.shape[0], H.shape[1],
+                              _dp(F.view(np.float64)), F.shape[0], F.shape[1], fcx, fcy,
+                              _dp(out.view(np.float64)))
+    return out
+
+
+def convolve_direct(H, F, fcx, fcy) -> np.ndarray:
+    H, F = _c128(H), _c128(F)
+    out = np.zeros_like(H)
+    lib().or_convolve_direct(_dp(H.view(np.float64)), H.shape[0], H.shape[1],
+                             _dp(F.view(np.float64)), F.shape[0], F.shape[1], fcx, fcy,
+                             _dp(out.view(np.float64)))
+    return out
+
+
+# ----------------------------------------------------------- decomposition
+
+def decompose_rotation2(filt, cx, cy, K, n_radii, n_angles, r_max) -> Filter:
+    filt = _c128(filt)
+    nc_max = 2 * (K // 2) + 1
+    ks = np.zeros(nc_max, np.int32)
+    comps = np.zeros((max(n_radii, 1), nc_max), np.complex128)
+    nc = C.c_int(0)
+    _check(lib().or_decompose_rotation2(
+        _dp(filt.view(np.float64)), filt.shape[1], filt.shape[0], C.c_double(cx),
+        C.c_double(cy), int(K), int(n_radii), int(n_angles), C.c_double(r_max), _ip(ks),
+        _dp(comps.view(np.float64)), C.byref(nc)))
+    return Filter(0, K, ks[: nc.value].copy(), comps[:, : nc.value].copy(), n_radii,
+                  n_angles, float(r_max))
+
+
+def decompose_scale2(filt, cx, cy, K, n_radii, n_angles, r_min, r_max,
+                     r_domain=0.0) -> Filter:
+    filt = _c128(filt)
+    nc_max = 2 * (K // 2) + 1
+    ks = np.zeros(nc_max, np.int32)
+    comps = np.zeros((max(n_angles, 1), nc_max), np.complex128)
+    nc = C.c_int(0)
+    _check(lib().or_decompose_scale2(
+        _dp(filt.view(np.float64)), filt.shape[1], filt.shape[0], C.c_double(cx),
+        C.c_double(cy), int(K), int(n_radii), int(n_angles), C.c_double(r_min),
+        C.c_double(r_max), C.c_double(r_domain), _ip(ks), _dp(comps.view(np.float64)),
+        C.byref(nc)))
+    D = r_domain if r_domain > 0 else r_max
+    return Filter(1, K, ks[: nc.value].copy(), comps[:, : nc.value].copy(), n_radii,
+                  n_angles, float(r_max), float(r_min), float(D))
+
+
+def component_value(F, ci, r, theta) -> complex:
+    out = np.zeros(2)
+    lib().or_component_value(C.byref(_cfilter(F)), int(ci), C.c_double(r),
+                             C.c_double(theta), _dp(out))
+    return complex(out[0], out[1])
+
+
+def render_component(F, ci, width, height, cx, cy) -> np.ndarray:
+    out = np.zeros((height, width), np.complex128)
+    lib().or_render_component(C.byref(_cfilter(F)), int(ci), int(width), int(height),
+                              C.c_double(cx), C.c_double(cy), _dp(out.view(np.float64)))
+    return out
+
+
+def inner_dc_value(F) -> complex:
+    out = np.zeros(2)
+    lib().or_inner_dc_value(C.byref(_cfilter(F)), _dp(out))
+    return complex(out[0], out[1])
+
+
+def reconstruct(F, width, height, cx, cy, subset=None) -> np.ndarray:
+    out = np.zeros((height, width), np.complex128)
+    sub = None if subset is None else np.ascontiguousarray(np.asarray(subset, np.int32))
+    lib().or_reconstruct(C.byref(_cfilter(F)), int(width), int(height), C.c_double(cx),
+                         C.c_double(cy), None if sub is None else _ip(sub),
+                         -1 if sub is None else len(sub), _dp(out.view(np.float64)))
+    return out
+
+
+def synthesize_polar(F, subset=None) -> np.ndarray:
+    out = np.zeros((F.n_radii, F.n_angles), np.complex128)
+    sub = None if subset is None else np.ascontiguousarray(np.asarray(subset, np.int32))
+    lib().or_synthesize_polar(C.byref(_cfilter(F)), None if sub is None else _ip(sub),
+                              -1 if sub is None else len(sub), _dp(out.view(np.float64)))
+    return out
+
+
+# ------------------------------------------------------------------ engine
+
+def _xfast(mode, H, kind, param, F, components, periodic, nthreads):
+    H = _c128(H)
+    param = _f64(param)
+    assert param.shape == H.shape
+    out = np.zeros_like(H)
+    ops = C.c_longlong(0)
+    secs = np.zeros(4)
+    comp = None if not components else np.ascontiguousarray(np.asarray(components, np.int32))
+    _check(lib().or_xfast(int(mode), _dp(H.view(np.float64)), H.shape[0], H.shape[1],
+                          int(kind), _dp(param), C.byref(_cfilter(F)),
+                          None if comp is None else _ip(comp),
+                          0 if comp is None else len(comp), int(periodic),
+                          _dp(out.view(np.float64)), C.byref(ops), _dp(secs),
+                          int(nthreads)))
+    return out, ops.value, dict(zip(("render", "fft", "combine", "premultiply"), secs))
+
+
+def xcorr_fast(H, kind, param, F, components=None, periodic=False, nthreads=1):
+    """engine.hpp:286-326. Returns (output, standard_ops, seconds)."""
+    return _xfast(0, H, kind, param, F, components, periodic, nthreads)
+
+
+def xconv_fast(H, kind, param, F, components=None, periodic=False, nthreads=1):
+    """engine.hpp:331-373. Returns (output, standard_ops, seconds)."""
+    return _xfast(1, H, kind, param, F, components, periodic, nthreads)
+
+
+def smooth_adaptive(H, kind, param, F, normalize_signal=True, nthreads=1):
+    """engine.hpp:385-419. Returns (output_real, standard_ops, clamped_pixels)."""
+    H = _c128(H)
+    param = _f64(param)
+    out = np.zeros(H.shape, np.float64)
+    ops = C.c_longlong(0)
+    cl = C.c_int(0)
+    _check(lib().or_smooth_adaptive(_dp(H.view(np.float64)), H.shape[0], H.shape[1],
+                                    int(kind), _dp(param), C.byref(_cfilter(F)),
+                                    int(normalize_signal), _dp(out), C.byref(ops),
+                                    C.byref(cl), int(nthreads)))
+    return out, ops.value, cl.value
+
+
+def _brute(mode, H, kind, param, F, eps, table_radii, table_angles):
+    H = _c128(H)
+    param = _f64(param)
+    out = np.zeros_like(H)
+    _check(lib().or_xbrute(int(mode), _dp(H.view(np.float64)), H.shape[0], H.shape[1],
+                           int(kind), _dp(param), C.byref(_cfilter(F)), C.c_double(eps),
+                           int(table_radii), int(table_angles), _dp(out.view(np.float64))))
+    return out
+
+
+def xcorr_brute(H, kind, param, F, eps=0.0, table_radii=0, table_angles=0):
+    return _brute(0, H, kind, param, F, eps, table_radii, table_angles)
+
+
+def xconv_brute(H, kind, param, F, eps=0.0, table_radii=0, table_angles=0):
+    return _brute(1, H, kind, param, F, eps, table_radii, table_angles)
+
+
+def spectral_oracle(mode, H, kind, param, F):
+    H = _c128(H)
+    param = _f64(param)
+    out = np.zeros_like(H)
+    _check(lib().or_spectral_oracle(int(mode), _dp(H.view(np.float64)), H.shape[0],
+                                    H.shape[1], int(kind), _dp(param), C.byref(_cfilter(F)),
+                                    _dp(out.view(np.float64))))
+    return out
+
+
+def find_peaks(resp, radius, threshold_frac=0.5, max_out=1 << 16):
+    resp = _f64(resp)
+    xs = np.zeros(max_out, np.int32)
+    ys = np.zeros(max_out, np.int32)
+    vals = np.zeros(max_out)
+    n = lib().or_find_peaks(_dp(resp), resp.shape[0], resp.shape[1], C.c_double(radius),
+                            C.c_double(threshold_frac), _ip(xs), _ip(ys), _dp(vals), max_out)
+    n = min(n, max_out)
+    return [(int(xs[i]), int(ys[i]), float(vals[i])) for i in range(n)]
+
+
+def gaussian_blur(img, sigma) -> np.ndarray:
+    img = _f64(img)
+    out = np.zeros_like(img)
+    lib().or_gaussian_blur(_dp(img), img.shape[0], img.shape[1], C.c_double(sigma), _dp(out))
+    return out
+
+
+def gradient(img):
+    img = _f64(img)
+    mag = np.zeros_like(img)
+    d = np.zeros_like(img)
+    lib().or_gradient(_dp(img), img.shape[0], img.shape[1], _dp(mag), _dp(d))
+    return mag, d
+
+
+def anglemax(G, ks, n_angles=360):
+    """G: (nc, h, w) complex band responses.  Returns (score, argmax)."""
+    G = _c128(G)
+    ks = np.ascontiguousarray(np.asarray(ks, np.int32))
+    nc, h, w = G.shape
+    score = np.zeros((h, w))
+    arg = np.zeros((h, w), np.int32)
+    lib().or_anglemax(_dp(G.view(np.float64)), _ip(ks), nc, h, w, int(n_angles),
+                      _dp(score), _ip(arg))
+    return score, arg
+
+
+# ------------------------------------------------------------------ fixtures
+
+class Rng:
+    """std::mt19937_64 shared across fixtures, as in proj/tests/helpers.hpp."""
+
+    def __init__(self, seed: int):
+        self._h = C.c_void_p(lib().or_rng_new(int(seed)))
+
+    def __del__(self):
+        try:
+            lib().or_rng_free(self._h)
+        except Exception:
+            pass
+
+    def next(self) -> int:
+        return lib().or_rng_next(self._h)
+
+    def uniform(self, a, b) -> float:
+        return lib().or_rng_uniform(self._h, a, b)
+
+    def random_field(self, w, h, complex_valued=False) -> np.ndarray:
+        out = np.zeros((h, w), np.complex128)
+        lib().or_random_field(self._h, int(w), int(h), int(complex_valued),
+                              _dp(out.view(np.float64)))
+        return out
+
+    def random_smooth_filter(self, radius, n_bumps=6, envelope_frac=0.35) -> np.ndarray:
+        S = 2 * radius + 1
+        out = np.zeros((S, S), np.complex128)
+        lib().or_random_smooth_filter(self._h, int(radius), int(n_bumps),
+                                      C.c_double(envelope_frac), _dp(out.view(np.float64)))
+        return out
+
+    def annular_filter(self, R, r0_frac=0.55, sr_frac=0.18) -> np.ndarray:
+        S = 2 * R + 1
+        out = np.zeros((S, S), np.complex128)
+        lib().or_annular_filter(self._h, int(R), C.c_double(r0_frac), C.c_double(sr_frac),
+                                _dp(out.view(np.float64)))
+        return out
+
+    def random_rotation_field(self, w, h) -> np.ndarray:
+        out = np.zeros((h, w))
+        lib().or_random_rotation_field(self._h, int(w), int(h), _dp(out))
+        return out
+
+    def random_scale_field(self, w, h, lo=0.5, hi=2.0) -> np.ndarray:
+        out = np.zeros((h, w))
+        lib().or_random_scale_field(self._h, int(w), int(h), C.c_double(lo), C.c_double(hi),
+                                    _dp(out))
+        return out
+
+
+def rel_l2(a, b) -> float:
+    """helpers.hpp:10-14"""
+    a = np.asarray(a)
+    b = np.asarray(b)
+    n = np.sqrt(np.sum(np.abs(a - b) ** 2))
+    d = np.sqrt(np.sum(np.abs(b) ** 2))
+    return float(n / d) if d > 0 else float(n)
