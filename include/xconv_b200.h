@@ -1,0 +1,165 @@
+/*
+ * xconv_b200.h -- C ABI of the B200-native extended correlation / convolution
+ * hot path (arXiv 2006.13188).  This is the drop-in boundary: the reference's
+ * C++ host API (proj/include/xconv/engine.hpp) keeps its signatures and calls
+ * these entry points instead of its per-band CPU loop (INTEGRATION.md shows
+ * the shim).  Plain pointers and sizes only; no C++ or torch types.
+ *
+ * Entry points and the reference interface each one replaces:
+ *   xc_run(mode = XC_CORRELATION)  <- xcorr_fast   engine.hpp:286-326
+ *   xc_run(mode = XC_CONVOLUTION)  <- xconv_fast   engine.hpp:331-373
+ *   xc_smooth                      <- smooth_adaptive engine.hpp:385-419
+ *   xc_anglemax                    <- (new; BASELINE config 3)
+ *   xc_find_peaks                  <- find_peaks   vote_filter.hpp:107-134
+ *   xc_filter_create               <- FreqFilter2  freq_filter.hpp:21-46 (the
+ *                                     per-band filter spectra are built once
+ *                                     per filter and pad size and cached)
+ *   xc_decompose_rotation2/scale2  <- decompose_rotation2 / decompose_scale2
+ *                                     freq_filter.hpp:63-129 (host, once per
+ *                                     filter)
+ *   xc_render_component / xc_reconstruct / xc_inner_dc_value
+ *                                  <- freq_filter.hpp:165-235 (host)
+ *
+ * Conventions
+ *   - Status codes: XC_OK; XC_EINVAL for the reference's std::invalid_argument
+ *     (the message text is the reference's, readable with xc_last_error);
+ *     >= 10 for CUDA / allocation / NCCL failures.  A context that cannot
+ *     reach a CUDA device fails loudly at xc_context_create: there is no CPU
+ *     fallback.
+ *   - Grids: `layout` XC_COL_MAJOR is Eigen's default storage used by the
+ *     reference (values(y,x) at y + x*height, field.hpp:15); XC_ROW_MAJOR is
+ *     [y][x].  Complex data is interleaved (re, im).
+ *   - FreqFilter2 comps are passed column-major like the reference's Eigen
+ *     CGrid (n_rows x nc, element (row, ci) at row + ci*n_rows), n_rows =
+ *     n_radii for rotation2 and n_angles for scale2.
+ *   - The caller owns all buffers passed in.  With memory == XC_HOST, host
+ *     buffers (pinned or pageable) are copied in and out inside the call; with
+ *     XC_DEVICE the pointers are device pointers on the context's device.
+ *     Calls are synchronous with respect to the host.
+ *   - One context per host thread, or external locking.
+ */
+#ifndef XCONV_B200_H
+#define XCONV_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define XC_ABI_VERSION 1
+
+enum xc_status {
+  XC_OK = 0,
+  XC_EINVAL = 2,      /* std::invalid_argument in the reference */
+  XC_ECUDA = 10,
+  XC_ENOMEM = 11,
+  XC_ENCCL = 12,
+  XC_EINTERNAL = 13
+};
+
+enum xc_group { XC_ROTATION2 = 0, XC_SCALE2 = 1, XC_ROTATION3 = 2 }; /* field.hpp:129 */
+enum xc_mode { XC_CORRELATION = 0, XC_CONVOLUTION = 1 };            /* engine.hpp:10 */
+enum xc_dtype { XC_F32 = 0, XC_F64 = 1, XC_C64 = 2, XC_C128 = 3 };
+enum xc_layout { XC_ROW_MAJOR = 0, XC_COL_MAJOR = 1 };
+enum xc_memory { XC_HOST = 0, XC_DEVICE = 1 };
+
+/* xc_run flags */
+#define XC_FLAG_PERIODIC 1u      /* XConvPlan::periodic, engine.hpp:20 */
+#define XC_FLAG_NO_INNER_DC 2u   /* omit the scale inner-DC term (engine.hpp:320-324,
+                                    369-371): set on all but one rank when bands
+                                    are sharded across GPUs */
+#define XC_FLAG_ACCUMULATE 4u    /* out += result (device memory only) */
+
+typedef struct xc_context_s* xc_context;
+typedef struct xc_filter_s* xc_filter;
+
+/* Image batch descriptor: `batch` images of height x width, contiguous. */
+typedef struct {
+  int height, width, batch;
+  int signal_dtype; /* XC_F32 / XC_F64 (real) or XC_C64 / XC_C128 (complex) */
+  int param_dtype;  /* XC_F32 or XC_F64: angle (rotation2) or scale (scale2) */
+  int out_dtype;    /* XC_C64 / XC_C128 for xc_run; XC_F32 / XC_F64 for xc_smooth */
+  int layout;       /* XC_ROW_MAJOR or XC_COL_MAJOR */
+  int memory;       /* XC_HOST or XC_DEVICE, for every data pointer of the call */
+  int param_per_image; /* 1: param has `batch` planes; 0: one plane shared */
+  int xform_kind;   /* XformField::kind (field.hpp:129): what param holds --
+                       XC_ROTATION2 angles or XC_SCALE2 scale factors */
+} xc_image_desc;
+
+/* Response2 counters and StageTimer keys (engine.hpp:23-29, 41-49). */
+typedef struct {
+  long long standard_ops;  /* bands executed (engine.hpp:318, 367; smooth: num+den) */
+  int clamped_pixels;      /* SmoothResult::clamped_pixels, engine.hpp:381 */
+  int pad_h, pad_w;        /* transform size used */
+  double seconds_render, seconds_fft, seconds_combine, seconds_premultiply;
+  double seconds_h2d, seconds_d2h, seconds_total;
+  int gpu_launches;        /* kernels launched by this call */
+} xc_stats;
+
+int xc_abi_version(void);
+
+/* ---- contexts ---------------------------------------------------------- */
+int xc_context_create(int device, xc_context* out);
+void xc_context_destroy(xc_context ctx);
+/* Message of the last failed call on this context (or thread if ctx NULL). */
+const char* xc_last_error(xc_context ctx);
+/* Launch on a caller-owned cudaStream_t (NULL restores the internal stream). */
+int xc_context_set_stream(xc_context ctx, void* cuda_stream);
+/* Release cached device scratch (filter spectra stay with their filters). */
+int xc_context_trim(xc_context ctx);
+
+/* ---- filters (FreqFilter2) -------------------------------------------- */
+/* Filters are host objects (ctx may be NULL); device spectra are built on first
+ * use per (device, pad size, layout) and freed by xc_filter_destroy.  Errors of
+ * filter-only calls are reported by xc_last_error(NULL). */
+int xc_filter_create(xc_context ctx, int group, int K, const int* ks, int nc,
+                     const double* comps, int n_radii, int n_angles, double r_max,
+                     double r_min, double r_domain, xc_filter* out);
+void xc_filter_destroy(xc_filter f);
+int xc_filter_num_components(xc_filter f);
+
+/* ---- host-side decomposition / synthesis (once per filter) ------------ */
+/* filter image: height x width complex<double> in `layout`.  Outputs: ks
+ * (2*(K/2)+1 ints), comps column-major (n_rows x nc) complex<double>. */
+int xc_decompose_rotation2(const double* filt, int height, int width, int layout,
+                           double cx, double cy, int K, int n_radii, int n_angles,
+                           double r_max, int* ks_out, double* comps_out, int* nc_out);
+int xc_decompose_scale2(const double* filt, int height, int width, int layout,
+                        double cx, double cy, int K, int n_radii, int n_angles,
+                        double r_min, double r_max, double r_domain, int* ks_out,
+                        double* comps_out, int* nc_out);
+int xc_render_component(xc_filter f, int ci, int width, int height, double cx,
+                        double cy, int layout, double* out);
+int xc_reconstruct(xc_filter f, int width, int height, double cx, double cy,
+                   const int* subset, int nsub, int layout, double* out);
+int xc_inner_dc_value(xc_filter f, double* out2);
+
+/* ---- the hot path ------------------------------------------------------ */
+/* xcorr_fast / xconv_fast.  components: XConvPlan::components (NULL/0 = all
+ * retained bands, in the filter's ascending order). */
+int xc_run(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d,
+           const void* signal, const void* param, const int* components,
+           int n_components, unsigned flags, void* out, xc_stats* stats);
+
+/* smooth_adaptive: out is real (d->out_dtype XC_F32 or XC_F64). */
+int xc_smooth(xc_context ctx, xc_filter f, const xc_image_desc* d,
+              const void* signal, const void* param, int normalize_signal,
+              void* out, xc_stats* stats);
+
+/* Rotation-invariant matching score: for every pixel,
+ * score = max over s < n_angles of |sum_k e^{-i k 2 pi s / n_angles} G_k(p)|,
+ * G_k = H (*) F_k the per-band correlations of xcorr_fast; argmax = first s
+ * attaining the max (int32).  d->out_dtype selects the score type (XC_F32 /
+ * XC_F64).  argmax may be NULL. */
+int xc_anglemax(xc_context ctx, xc_filter f, const xc_image_desc* d,
+                const void* signal, const int* components, int n_components,
+                int n_angles, void* score, int* argmax, xc_stats* stats);
+
+/* find_peaks (vote_filter.hpp:107-134) on a real response (host memory). */
+int xc_find_peaks(const void* resp, int dtype, int height, int width, int layout,
+                  double radius, double threshold_frac, int* xs, int* ys,
+                  double* values, int max_peaks, int* n_found);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XCONV_B200_H */

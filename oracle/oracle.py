@@ -23,8 +23,14 @@ _lib = None
 
 def build(force: bool = False) -> str:
     """Compile the oracle with its Makefile (gcc/g++ only)."""
-    if force or not os.path.exists(_LIB_PATH):
-        subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    # make is a no-op when the library is newer than its sources; on a box
+    # without the sources' build tools the prebuilt library is used as is
+    try:
+        subprocess.run(["make", "-s", "-C", _HERE] + (["-B"] if force else []), check=True,
+                       capture_output=True)
+    except (OSError, subprocess.CalledProcessError):
+        if not os.path.exists(_LIB_PATH):
+            raise
     return _LIB_PATH
 
 
@@ -296,6 +302,20 @@ def spectral_oracle(mode, H, kind, param, F):
     _check(lib().or_spectral_oracle(int(mode), _dp(H.view(np.float64)), H.shape[0],
                                     H.shape[1], int(kind), _dp(param), C.byref(_cfilter(F)),
                                     _dp(out.view(np.float64))))
+    return out
+
+
+def spectral_oracle_at(mode, H, kind, param, F, pys, pxs):
+    """Spectral oracle at sampled pixels (float32 real H / param)."""
+    H = np.ascontiguousarray(np.asarray(H, np.float32))
+    param = np.ascontiguousarray(np.asarray(param, np.float32))
+    pys = np.ascontiguousarray(np.asarray(pys, np.int32))
+    pxs = np.ascontiguousarray(np.asarray(pxs, np.int32))
+    out = np.zeros(len(pys), np.complex128)
+    fp = C.POINTER(C.c_float)
+    _check(lib().or_spectral_oracle_at(int(mode), H.ctypes.data_as(fp), H.shape[0], H.shape[1],
+                                       int(kind), param.ctypes.data_as(fp), C.byref(_cfilter(F)),
+                                       _ip(pys), _ip(pxs), len(pys), _dp(out.view(np.float64))))
     return out
 
 

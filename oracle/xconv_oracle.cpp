@@ -989,6 +989,58 @@ int or_spectral_oracle(int mode, const double* Hd, int h, int w, int kind,
   });
 }
 
+// Spectral oracle evaluated only at the listed pixels (test_engine2d.cpp:33-61
+// / test_engine_scale.cpp:37-78 restricted to p in `pix`): full-size parity
+// checks sample pixels instead of running the whole O(N R^2 B) loop.
+// H and param are float32 (the arrays the GPU consumed), upcast to double.
+int or_spectral_oracle_at(int mode, const float* Hf, int h, int w, int kind,
+                          const float* paramf, const or_filter* Fc, const int* pys,
+                          const int* pxs, int npix, double* outd) {
+  return guarded([&] {
+    const Filter F = to_filter(Fc);
+    const int R = int(std::ceil(F.r_max));
+    const double om = kind == 1 ? F.omega() : 0.0;
+    const cd dc = inner_dc_value(F);
+    // per-offset component values for rotation are angle dependent; precompute
+    // r, theta per offset only
+    for (int t = 0; t < npix; ++t) {
+      const int py = pys[t], px = pxs[t];
+      cd acc_out(0);
+      for (int dy = -R; dy <= R; ++dy)
+        for (int dx = -R; dx <= R; ++dx) {
+          const double r = std::hypot(double(dx), double(dy));
+          if (r > F.r_max) continue;
+          const double th = std::atan2(double(dy), double(dx));
+          const int qx = mode == 0 ? px + dx : px - dx;
+          const int qy = mode == 0 ? py + dy : py - dy;
+          if (qx < 0 || qy < 0 || qx >= w || qy >= h) continue;
+          const size_t pi = size_t(mode == 0 ? py : qy) * w + (mode == 0 ? px : qx);
+          const double prm = double(paramf[pi]);
+          cd acc(0);
+          if (kind == 0) {
+            const double a = normalize_angle(prm);
+            for (int ci = 0; ci < F.nc(); ++ci) acc += component_value(F, ci, r, th - a);
+            if (mode == 0) acc = std::conj(acc);
+          } else {
+            const double ls = std::log(prm);
+            if (r < F.r_min) {
+              acc = mode == 0 ? std::conj(dc) : dc;
+            } else {
+              for (int ci = 0; ci < F.nc(); ++ci) {
+                const cd cv = component_value(F, ci, r, th);
+                acc += mode == 0 ? std::conj(cv) * std::polar(1.0, F.ks[ci] * om * ls)
+                                 : cv * std::polar(1.0, -F.ks[ci] * om * ls);
+              }
+            }
+          }
+          acc_out += cd(double(Hf[size_t(qy) * w + qx]), 0.0) * acc;
+        }
+      outd[2 * t] = acc_out.real();
+      outd[2 * t + 1] = acc_out.imag();
+    }
+  });
+}
+
 // vote_filter.hpp:105-134
 int or_find_peaks(const double* resp, int h, int w, double radius, double threshold_frac,
                   int* xs, int* ys, double* vals, int max_out) {

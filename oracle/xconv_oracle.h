@@ -97,6 +97,10 @@ int or_xbrute(int mode, const double* H, int h, int w, int kind,
 int or_spectral_oracle(int mode, const double* H, int h, int w, int kind,
                        const double* param, const or_filter* F, double* out);
 
+/* spectral oracle at selected pixels; real float32 signal / param */
+int or_spectral_oracle_at(int mode, const float* H, int h, int w, int kind,
+                          const float* param, const or_filter* F, const int* pys,
+                          const int* pxs, int npix, double* out);
 /* vote_filter.hpp:107-134.  Returns number of peaks (<= max_out written). */
 int or_find_peaks(const double* resp, int h, int w, double radius,
                   double threshold_frac, int* xs, int* ys, double* vals,

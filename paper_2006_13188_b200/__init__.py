@@ -1,0 +1,15 @@
+"""B200-native extended correlation / convolution (arXiv 2006.13188 hot path).
+
+The reference's operator API (xcorr_fast, xconv_fast, smooth_adaptive, ...)
+backed by hand-written sm_100a CUDA kernels behind the C ABI of
+include/xconv_b200.h.  See DESIGN.md.
+"""
+from .engine import (FreqFilter2, Peak, Response2, SmoothResult, XConvPlan, XformField,
+                     XformKind, XMode, anglemax, decompose_rotation2, decompose_scale2,
+                     find_peaks, inner_dc_value, reconstruct, render_component,
+                     smooth_adaptive, xconv_fast, xcorr_fast)
+
+__all__ = ["FreqFilter2", "Peak", "Response2", "SmoothResult", "XConvPlan", "XformField",
+           "XformKind", "XMode", "anglemax", "decompose_rotation2", "decompose_scale2",
+           "find_peaks", "inner_dc_value", "reconstruct", "render_component",
+           "smooth_adaptive", "xconv_fast", "xcorr_fast"]

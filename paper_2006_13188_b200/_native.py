@@ -1,0 +1,138 @@
+"""ctypes binding of the C ABI (include/xconv_b200.h) in lib/libxconv_b200.so.
+
+The product path has no fallback: if the library is missing or no CUDA device
+is reachable, calls raise instead of computing anything on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libxconv_b200.so")
+
+XC_OK, XC_EINVAL = 0, 2
+XC_ROTATION2, XC_SCALE2, XC_ROTATION3 = 0, 1, 2
+XC_CORRELATION, XC_CONVOLUTION = 0, 1
+XC_F32, XC_F64, XC_C64, XC_C128 = 0, 1, 2, 3
+XC_ROW_MAJOR, XC_COL_MAJOR = 0, 1
+XC_HOST, XC_DEVICE = 0, 1
+XC_FLAG_PERIODIC, XC_FLAG_NO_INNER_DC, XC_FLAG_ACCUMULATE = 1, 2, 4
+
+
+class ImageDesc(C.Structure):
+    _fields_ = [("height", C.c_int), ("width", C.c_int), ("batch", C.c_int),
+                ("signal_dtype", C.c_int), ("param_dtype", C.c_int), ("out_dtype", C.c_int),
+                ("layout", C.c_int), ("memory", C.c_int), ("param_per_image", C.c_int),
+                ("xform_kind", C.c_int)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("standard_ops", C.c_longlong), ("clamped_pixels", C.c_int),
+                ("pad_h", C.c_int), ("pad_w", C.c_int),
+                ("seconds_render", C.c_double), ("seconds_fft", C.c_double),
+                ("seconds_combine", C.c_double), ("seconds_premultiply", C.c_double),
+                ("seconds_h2d", C.c_double), ("seconds_d2h", C.c_double),
+                ("seconds_total", C.c_double), ("gpu_launches", C.c_int)]
+
+
+EXPORTS = [
+    "xc_abi_version", "xc_context_create", "xc_context_destroy", "xc_last_error",
+    "xc_context_set_stream", "xc_context_trim", "xc_filter_create", "xc_filter_destroy",
+    "xc_filter_num_components", "xc_decompose_rotation2", "xc_decompose_scale2",
+    "xc_render_component", "xc_reconstruct", "xc_inner_dc_value", "xc_run", "xc_smooth",
+    "xc_anglemax", "xc_find_peaks",
+]
+
+_lib = None
+_lock = threading.Lock()
+
+
+class NativeMissing(RuntimeError):
+    pass
+
+
+def lib():
+    """Load the CUDA library (raises NativeMissing if it was never built)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise NativeMissing(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2006_13188_b200.build` "
+                "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        vp, ip, dp, i, d = C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_double), C.c_int, C.c_double
+        L.xc_abi_version.restype = i
+        L.xc_context_create.argtypes = [i, C.POINTER(vp)]
+        L.xc_context_destroy.argtypes = [vp]
+        L.xc_context_destroy.restype = None
+        L.xc_last_error.argtypes = [vp]
+        L.xc_last_error.restype = C.c_char_p
+        L.xc_context_set_stream.argtypes = [vp, vp]
+        L.xc_context_trim.argtypes = [vp]
+        L.xc_filter_create.argtypes = [vp, i, i, ip, i, dp, i, i, d, d, d, C.POINTER(vp)]
+        L.xc_filter_destroy.argtypes = [vp]
+        L.xc_filter_destroy.restype = None
+        L.xc_filter_num_components.argtypes = [vp]
+        L.xc_decompose_rotation2.argtypes = [dp, i, i, i, d, d, i, i, i, d, ip, dp, ip]
+        L.xc_decompose_scale2.argtypes = [dp, i, i, i, d, d, i, i, i, d, d, d, ip, dp, ip]
+        L.xc_render_component.argtypes = [vp, i, i, i, d, d, i, dp]
+        L.xc_reconstruct.argtypes = [vp, i, i, d, d, ip, i, i, dp]
+        L.xc_inner_dc_value.argtypes = [vp, dp]
+        L.xc_run.argtypes = [vp, vp, i, C.POINTER(ImageDesc), vp, vp, ip, i, C.c_uint, vp,
+                             C.POINTER(Stats)]
+        L.xc_smooth.argtypes = [vp, vp, C.POINTER(ImageDesc), vp, vp, i, vp, C.POINTER(Stats)]
+        L.xc_anglemax.argtypes = [vp, vp, C.POINTER(ImageDesc), vp, ip, i, i, vp, ip,
+                                  C.POINTER(Stats)]
+        L.xc_find_peaks.argtypes = [vp, i, i, i, i, d, d, ip, ip, dp, i, ip]
+        _lib = L
+        return L
+
+
+def check(rc: int, ctx=None):
+    if rc == XC_OK:
+        return
+    msg = lib().xc_last_error(ctx).decode()
+    if rc == XC_EINVAL:
+        raise ValueError(msg)  # std::invalid_argument in the reference
+    raise RuntimeError(f"xconv_b200 error {rc}: {msg}")
+
+
+class Context:
+    """One CUDA context handle (xc_context) on one device."""
+
+    def __init__(self, device: int = 0):
+        L = lib()
+        h = C.c_void_p()
+        check(L.xc_context_create(int(device), C.byref(h)), None)
+        self.handle = h
+        self.device = device
+
+    def set_stream(self, stream_ptr: int | None):
+        check(lib().xc_context_set_stream(self.handle, C.c_void_p(stream_ptr or 0)), self.handle)
+
+    def trim(self):
+        check(lib().xc_context_trim(self.handle), self.handle)
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().xc_context_destroy(self.handle)
+        except Exception:
+            pass
+
+
+_ctx_local = threading.local()
+
+
+def context(device: int = 0) -> Context:
+    """Per-thread, per-device default context."""
+    d = getattr(_ctx_local, "ctx", None)
+    if d is None:
+        d = _ctx_local.ctx = {}
+    if device not in d:
+        d[device] = Context(device)
+    return d[device]

@@ -1,0 +1,800 @@
+// C ABI implementation (include/xconv_b200.h): contexts, filter spectrum cache,
+// and the gather / scatter / smooth / angle-max pipelines.
+//
+// Pipeline per image (kernels.h for the layouts):
+//   gather  (xcorr_fast, engine.hpp:286-326):
+//     prep(base) -> F1 rows -> F2 cols (H^) -> I1 cols^-1 per band (x conj F^_k)
+//     -> I2 rows^-1 per band, steer e^{+i k phi}, accumulate (+ conj(dc) H)
+//   scatter (xconv_fast, engine.hpp:331-373):
+//     prep -> S1 rows per band of H e^{-i k phi} -> S2 cols per band, x F^_k,
+//     summed in frequency (the B inverse FFTs of the reference collapse into
+//     one), col^-1 -> S4 rows^-1 (+ dc H)
+//   smooth  (smooth_adaptive, engine.hpp:385-419): scatter(H w), scatter(w),
+//     max|den|, floored divide
+//   anglemax: gather's per-band responses G_k -> max_s |sum_k e^{-iks} G_k|
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/xconv_b200.h"
+#include "fft_plan.h"
+#include "host_filter.h"
+#include "kernels.h"
+
+namespace {
+
+using xcb::cplx;
+
+struct CudaError : std::runtime_error {
+  int code;
+  CudaError(const std::string& m, int c) : std::runtime_error(m), code(c) {}
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    const int code = e == cudaErrorMemoryAllocation ? XC_ENOMEM : XC_ECUDA;
+    throw CudaError(std::string(what) + ": " + cudaGetErrorString(e), code);
+  }
+}
+
+thread_local std::string g_thread_err;
+
+struct PlanEntry {
+  xcb::FftPlan plan;
+  float2* tw = nullptr;
+};
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+};
+
+}  // namespace
+
+struct xc_context_s {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  std::mutex mu;
+  std::map<int, PlanEntry> plans;
+  std::map<std::string, DevBuf> bufs;
+
+  ~xc_context_s() {
+    cudaSetDevice(device);
+    for (auto& kv : plans) cudaFree(kv.second.tw);
+    for (auto& kv : bufs) cudaFree(kv.second.p);
+    if (own) cudaStreamDestroy(own);
+  }
+
+  const xcb::FftPlan& plan(int L) {
+    auto it = plans.find(L);
+    if (it != plans.end()) return it->second.plan;
+    PlanEntry e;
+    if (!xcb::make_fft_plan(L, &e.plan)) throw std::invalid_argument("unsupported transform length");
+    e.tw = xcb::upload_twiddles(e.plan);
+    if (!e.tw) throw CudaError("twiddle upload failed", XC_ENOMEM);
+    e.plan.d.tw = e.tw;
+    return plans.emplace(L, std::move(e)).first->second.plan;
+  }
+
+  template <class T>
+  T* buf(const std::string& name, size_t count) {
+    const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    DevBuf& b = bufs[name];
+    if (b.n < bytes) {
+      if (b.p) {
+        ck(cudaStreamSynchronize(stream), "sync before realloc");
+        cudaFree(b.p);
+        b.p = nullptr;
+        b.n = 0;
+      }
+      ck(cudaMalloc(&b.p, bytes), ("cudaMalloc " + name).c_str());
+      b.n = bytes;
+    }
+    return static_cast<T*>(b.p);
+  }
+};
+
+// A filter is host data plus per-(device, pad, orientation) spectrum caches;
+// it is not bound to a context, so host-only calls need no GPU.
+struct xc_filter_s {
+  xcb::HostFilter hf;
+  std::map<std::tuple<int, int, int, int>, float2*> spectra;  // (dev, Ph, Pw, transposed)
+  int integral_state = -1;  // smooth_adaptive zero-integral check cache
+  ~xc_filter_s() {
+    for (auto& kv : spectra) {
+      cudaSetDevice(std::get<0>(kv.first));
+      cudaFree(kv.second);
+    }
+  }
+};
+
+namespace {
+
+template <class Fn>
+int guarded(xc_context ctx, Fn&& fn) {
+  std::string* err = ctx ? &ctx->err : &g_thread_err;
+  try {
+    fn();
+    return XC_OK;
+  } catch (const CudaError& e) {
+    *err = e.what();
+    return e.code;
+  } catch (const std::invalid_argument& e) {
+    *err = e.what();
+    return XC_EINVAL;
+  } catch (const std::bad_alloc&) {
+    *err = "host allocation failed";
+    return XC_ENOMEM;
+  } catch (const std::exception& e) {
+    *err = e.what();
+    return XC_EINTERNAL;
+  }
+}
+
+size_t dtype_size(int dt) {
+  switch (dt) {
+    case XC_F32: return 4;
+    case XC_F64: return 8;
+    case XC_C64: return 8;
+    case XC_C128: return 16;
+  }
+  throw std::invalid_argument("unknown dtype");
+}
+
+std::vector<cplx> to_rowmajor(const double* data, int height, int width, int layout) {
+  std::vector<cplx> v(size_t(height) * width);
+  for (int y = 0; y < height; ++y)
+    for (int x = 0; x < width; ++x) {
+      const size_t s = layout == XC_COL_MAJOR ? size_t(x) * height + y : size_t(y) * width + x;
+      v[size_t(y) * width + x] = cplx(data[2 * s], data[2 * s + 1]);
+    }
+  return v;
+}
+
+void export_filter(const xcb::HostFilter& f, int* ks, double* comps, int* nc) {
+  const int n = f.nc(), rows = f.n_rows();
+  for (int i = 0; i < n; ++i) ks[i] = f.ks[i];
+  for (int ci = 0; ci < n; ++ci)
+    for (int r = 0; r < rows; ++r) {  // Eigen column-major (row + ci * n_rows)
+      comps[2 * (size_t(ci) * rows + r)] = f.comp(r, ci).real();
+      comps[2 * (size_t(ci) * rows + r) + 1] = f.comp(r, ci).imag();
+    }
+  *nc = n;
+}
+
+// Resolved geometry and per-call state shared by the pipelines.
+struct Call {
+  xc_context ctx;
+  xc_filter f;
+  xc_image_desc d;
+  int rows, cols, transposed;
+  xcb::Geo g;
+  const xcb::FftPlan* prow;
+  const xcb::FftPlan* pcol;
+  std::vector<int> ks;     // selected band frequencies
+  std::vector<int> sidx;   // spectrum index of each
+  xcb::Bands bands;
+  float2* Fhat;
+  size_t sstride;
+  xcb::LaunchCounter lc;
+  cudaStream_t st;
+  double h2d_s = 0, d2h_s = 0;
+};
+
+std::vector<int> plan_components(const xcb::HostFilter& hf, const int* comps, int n) {
+  // engine.hpp:51-58
+  if (comps == nullptr || n <= 0) return hf.ks;
+  std::vector<int> out(comps, comps + n);
+  for (int k : out)
+    if (std::find(hf.ks.begin(), hf.ks.end(), k) == hf.ks.end())
+      throw std::invalid_argument("plan retains a component the filter lacks");
+  return out;
+}
+
+float2* filter_spectra(Call& c) {
+  const auto key = std::make_tuple(c.ctx->device, c.g.Ph, c.g.Pw, c.transposed);
+  auto it = c.f->spectra.find(key);
+  if (it != c.f->spectra.end()) return it->second;
+  const xcb::HostFilter& hf = c.f->hf;
+  const int R = c.g.R, S = 2 * R + 1, nb = hf.nc();
+  // render every band once (freq_filter.hpp:173-184), fp64 -> fp32
+  std::vector<cplx> tmp(size_t(S) * S);
+  std::vector<float2> comps(size_t(nb) * S * S);
+  for (int ci = 0; ci < nb; ++ci) {
+    xcb::render_component(hf, ci, S, S, double(R), double(R), c.transposed != 0, tmp.data());
+    for (size_t i = 0; i < tmp.size(); ++i)
+      comps[size_t(ci) * S * S + i] = make_float2(float(tmp[i].real()), float(tmp[i].imag()));
+  }
+  float2* dcomps = c.ctx->buf<float2>("filter_comps", comps.size());
+  ck(cudaMemcpyAsync(dcomps, comps.data(), comps.size() * sizeof(float2),
+                     cudaMemcpyHostToDevice, c.st),
+     "upload components");
+  float2* T1f = c.ctx->buf<float2>("filter_T1", size_t(nb) * (S + 1) * c.g.Pw);
+  float2* spec = nullptr;
+  ck(cudaMalloc(&spec, size_t(nb) * c.g.Ph * c.g.Pw * sizeof(float2)), "cudaMalloc spectra");
+  xcb::launch_filter_spectra(*c.prow, *c.pcol, c.g, dcomps, nb, T1f, spec, c.st, c.lc);
+  ck(cudaGetLastError(), "filter spectra launch");
+  ck(cudaStreamSynchronize(c.st), "filter spectra");  // comps host buffer lifetime
+  c.f->spectra[key] = spec;
+  return spec;
+}
+
+Call setup(xc_context ctx, xc_filter f, const xc_image_desc* d, int group_required,
+           const int* components, int ncomp, bool periodic) {
+  if (!ctx || !f || !d) throw std::invalid_argument("null argument");
+  Call c{};
+  c.ctx = ctx;
+  c.f = f;
+  c.d = *d;
+  c.st = ctx->stream;
+  if (d->height < 1 || d->width < 1 || d->batch < 1)
+    throw std::invalid_argument("image dims must be positive");
+  // engine.hpp:288-291
+  const int kind = group_required >= 0 ? group_required : d->xform_kind;
+  if (kind != f->hf.group) throw std::invalid_argument("transformation/filter group mismatch");
+  if (kind == XC_ROTATION3) throw std::invalid_argument("2D pipeline needs a 2D field");
+  c.transposed = d->layout == XC_COL_MAJOR;
+  c.rows = c.transposed ? d->width : d->height;
+  c.cols = c.transposed ? d->height : d->width;
+  const int R = f->hf.render_radius();
+  xcb::Geo& g = c.g;
+  g.H = c.rows;
+  g.W = c.cols;
+  g.R = R;
+  g.periodic = periodic ? 1 : 0;
+  g.Hx = periodic ? c.rows + 2 * R : c.rows;
+  g.Wx = periodic ? c.cols + 2 * R : c.cols;
+  g.Hx2 = (g.Hx + 1) & ~1;
+  g.H2 = (g.H + 1) & ~1;
+  g.off = periodic ? R : 0;
+  // zero-padded linear filtering needs P >= extent + R and no wrap of the
+  // 2R+1 taps (fft.hpp:85-86 uses next_fast_size(extent + 2R + 1))
+  g.Ph = xcb::pick_fft_length(std::max(g.Hx + R, 2 * R + 1));
+  g.Pw = xcb::pick_fft_length(std::max(g.Wx + R, 2 * R + 1));
+  if (g.Ph < 0 || g.Pw < 0) throw std::invalid_argument("image too large for the FFT planner");
+  if (g.Pw % 2) g.Pw = xcb::pick_fft_length(g.Pw + 1);
+  while (g.Pw % 2) g.Pw = xcb::pick_fft_length(g.Pw + 1);
+  c.prow = &ctx->plan(g.Pw);
+  c.pcol = &ctx->plan(g.Ph);
+  c.ks = plan_components(f->hf, components, ncomp);
+  for (int k : c.ks) c.sidx.push_back(f->hf.index_of(k));
+  c.Fhat = filter_spectra(c);
+  c.sstride = size_t(g.Ph) * g.Pw;
+  int* dband = ctx->buf<int>("bands", 2 * c.ks.size());
+  std::vector<int> hb(c.ks);
+  hb.insert(hb.end(), c.sidx.begin(), c.sidx.end());
+  ck(cudaMemcpyAsync(dband, hb.data(), hb.size() * sizeof(int), cudaMemcpyHostToDevice, c.st),
+     "upload bands");
+  c.bands = xcb::Bands{dband, dband + c.ks.size(), int(c.ks.size())};
+  return c;
+}
+
+double event_seconds(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms * 1e-3;
+}
+
+// Stage one image's signal / param on the device; returns device pointers.
+struct Staged {
+  xcb::SigSrc sig;
+  const void* param;
+  int param_f64;
+};
+
+Staged stage_inputs(Call& c, const void* signal, const void* param, int img) {
+  const xc_image_desc& d = c.d;
+  const size_t npix = size_t(c.rows) * c.cols;
+  const size_t ss = dtype_size(d.signal_dtype), ps = dtype_size(d.param_dtype);
+  Staged s{};
+  const bool cplx_sig = d.signal_dtype == XC_C64 || d.signal_dtype == XC_C128;
+  const char* sig_src = static_cast<const char*>(signal) + size_t(img) * npix * ss;
+  const char* par_src = param ? static_cast<const char*>(param) +
+                                    (d.param_per_image ? size_t(img) * npix * ps : 0)
+                              : nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  const void* dsig = sig_src;
+  if (d.memory == XC_HOST) {
+    void* b = c.ctx->buf<char>("sig_raw", npix * ss);
+    ck(cudaMemcpyAsync(b, sig_src, npix * ss, cudaMemcpyHostToDevice, c.st), "H2D signal");
+    dsig = b;
+  }
+  if (d.signal_dtype == XC_F64 || d.signal_dtype == XC_C128) {
+    void* b = c.ctx->buf<char>("sig_f32", npix * (cplx_sig ? 8 : 4));
+    xcb::launch_convert_signal(dsig, d.signal_dtype, npix, b, c.st, c.lc);
+    dsig = b;
+  }
+  s.sig = xcb::SigSrc{dsig, cplx_sig ? 1 : 0, nullptr, xcb::SIG_PLAIN};
+  if (par_src) {
+    const void* dpar = par_src;
+    if (d.memory == XC_HOST) {
+      void* b = c.ctx->buf<char>("param_raw", npix * ps);
+      ck(cudaMemcpyAsync(b, par_src, npix * ps, cudaMemcpyHostToDevice, c.st), "H2D param");
+      dpar = b;
+    }
+    s.param = dpar;
+  }
+  s.param_f64 = d.param_dtype == XC_F64;
+  if (d.memory == XC_HOST) {
+    ck(cudaStreamSynchronize(c.st), "H2D");
+    c.h2d_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+  return s;
+}
+
+// base (steering phase per pixel) + optional weights; throws the reference's
+// guard-band / positivity errors for scale fields (engine.hpp:267-279,
+// field.hpp:150-153).
+void prep(Call& c, const Staged& s, bool want_wgt, double** base_out, float** wgt_out) {
+  const size_t npix = size_t(c.rows) * c.cols;
+  double* base = c.ctx->buf<double>("base", npix);
+  float* wgt = want_wgt ? c.ctx->buf<float>("wgt", npix) : nullptr;
+  const xcb::HostFilter& hf = c.f->hf;
+  const bool scale = hf.group == 1;
+  unsigned long long* bad = c.ctx->buf<unsigned long long>("bad", 2);
+  const double lo = scale ? hf.r_min / hf.domain_top() : 0, hi = scale ? hf.domain_top() / hf.r_min : 0;
+  if (scale) ck(cudaMemsetAsync(bad, 0xff, 2 * sizeof(unsigned long long), c.st), "memset");
+  xcb::launch_prep(s.param, s.param_f64, hf.group, scale ? hf.omega() : 0.0, lo, hi, c.rows,
+                   c.cols, c.transposed, base, wgt, bad, c.st, c.lc);
+  if (scale) {
+    unsigned long long hbad[2];
+    ck(cudaMemcpyAsync(hbad, bad, sizeof(hbad), cudaMemcpyDeviceToHost, c.st), "guard readback");
+    ck(cudaStreamSynchronize(c.st), "guard");
+    if (hbad[0] != ~0ull)
+      throw std::invalid_argument("scale field must be strictly positive and finite");
+    if (hbad[1] != ~0ull) {
+      const unsigned long long ti = hbad[1];
+      const int W = c.d.width;  // true (un-transposed) width
+      const int x = int(ti % W), y = int(ti / W);
+      const size_t si = c.transposed ? size_t(x) * c.d.height + y : size_t(y) * c.d.width + x;
+      double sv = 0;
+      const size_t ps = dtype_size(c.d.param_dtype);
+      ck(cudaMemcpy(&sv, static_cast<const char*>(s.param) + si * ps, ps, cudaMemcpyDeviceToHost),
+         "guard value");
+      if (ps == 4) {
+        float fv;
+        std::memcpy(&fv, &sv, 4);
+        sv = fv;
+      }
+      throw std::invalid_argument("scale factor " + std::to_string(sv) + " at pixel (" +
+                                  std::to_string(x) + "," + std::to_string(y) +
+                                  ") outside guard band [" + std::to_string(lo) + "," +
+                                  std::to_string(hi) + "]");
+    }
+  }
+  *base_out = base;
+  if (wgt_out) *wgt_out = wgt;
+}
+
+void run_gather(Call& c, const xcb::SigSrc& sig, const double* base, void* out, int out_kind,
+                bool accumulate, bool dc) {
+  const xcb::Geo& g = c.g;
+  float2* T1 = c.ctx->buf<float2>("T1", size_t(g.Hx2) * g.Pw);
+  float2* Hh = c.ctx->buf<float2>("Hhat", size_t(g.Ph) * g.Pw);
+  float2* T2 = c.ctx->buf<float2>("T2", size_t(c.bands.n) * g.H2 * g.Pw);
+  xcb::launch_rows_fwd(*c.prow, g, sig, T1, c.st, c.lc);
+  xcb::launch_cols_fwd(*c.pcol, g, T1, Hh, c.st, c.lc);
+  xcb::launch_cols_inv_corr(*c.pcol, g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);
+  const cplx dcv = dc ? std::conj(xcb::inner_dc_value(c.f->hf)) : cplx(0);  // engine.hpp:323
+  xcb::launch_rows_inv_steer(*c.prow, g, T2, c.bands, base, out_kind, out, accumulate ? 1 : 0,
+                             sig, dcv.real(), dcv.imag(), c.st, c.lc);
+}
+
+void run_scatter(Call& c, const xcb::SigSrc& sig, const double* base, void* out, int out_kind,
+                 bool accumulate, bool dc) {
+  const xcb::Geo& g = c.g;
+  float2* T1 = c.ctx->buf<float2>("T1b", size_t(c.bands.n) * g.Hx2 * g.Pw);
+  float2* Sg = c.ctx->buf<float2>("Sigma", size_t(g.Ph) * g.Pw);
+  float2* T2 = c.ctx->buf<float2>("T2s", size_t(g.H2) * g.Pw);
+  xcb::launch_rows_fwd_premul(*c.prow, g, sig, base, c.bands, T1, c.st, c.lc);
+  xcb::launch_cols_fwd_mac_inv(*c.pcol, g, T1, c.Fhat, c.sstride, c.bands, Sg, T2, c.st, c.lc);
+  const cplx dcv = dc ? xcb::inner_dc_value(c.f->hf) : cplx(0);  // engine.hpp:370
+  xcb::launch_rows_inv_out(*c.prow, g, T2, out_kind, out, accumulate ? 1 : 0, sig, dcv.real(),
+                           dcv.imag(), c.st, c.lc);
+}
+
+void fill_stats(Call& c, xc_stats* st, double gpu_s, double total_s, long long ops) {
+  if (!st) return;
+  std::memset(st, 0, sizeof(*st));
+  st->standard_ops = ops;
+  st->pad_h = c.g.Ph;
+  st->pad_w = c.g.Pw;
+  st->seconds_fft = gpu_s;
+  st->seconds_h2d = c.h2d_s;
+  st->seconds_d2h = c.d2h_s;
+  st->seconds_total = total_s;
+  st->gpu_launches = c.lc.n;
+}
+
+}  // namespace
+
+// ======================================================================= C ABI
+extern "C" {
+
+int xc_abi_version(void) { return XC_ABI_VERSION; }
+
+int xc_context_create(int device, xc_context* out) {
+  return guarded(nullptr, [&] {
+    if (!out) throw std::invalid_argument("null argument");
+    int n = 0;
+    ck(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+    if (device < 0 || device >= n) throw CudaError("no such CUDA device", XC_ECUDA);
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    auto* c = new xc_context_s();
+    c->device = device;
+    ck(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "cudaStreamCreate");
+    c->stream = c->own;
+    *out = c;
+  });
+}
+
+void xc_context_destroy(xc_context ctx) { delete ctx; }
+
+const char* xc_last_error(xc_context ctx) {
+  return ctx ? ctx->err.c_str() : g_thread_err.c_str();
+}
+
+int xc_context_set_stream(xc_context ctx, void* s) {
+  return guarded(ctx, [&] { ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own; });
+}
+
+int xc_context_trim(xc_context ctx) {
+  return guarded(ctx, [&] {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    cudaSetDevice(ctx->device);
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+    for (auto& kv : ctx->bufs) cudaFree(kv.second.p);
+    ctx->bufs.clear();
+  });
+}
+
+int xc_filter_create(xc_context ctx, int group, int K, const int* ks, int nc,
+                     const double* comps, int n_radii, int n_angles, double r_max,
+                     double r_min, double r_domain, xc_filter* out) {
+  return guarded(ctx, [&] {
+    if (!out || (nc > 0 && (!ks || !comps))) throw std::invalid_argument("null argument");
+    if (group == XC_ROTATION3) throw std::invalid_argument("2D pipeline needs a 2D field");
+    if (group != XC_ROTATION2 && group != XC_SCALE2) throw std::invalid_argument("unknown group");
+    if (!(r_max > 0)) throw std::invalid_argument("r_max must be > 0");
+    if (group == XC_SCALE2 && !(r_min > 0))
+      throw std::invalid_argument("r_min must be > 0 (log-polar excludes the origin)");
+    auto f = std::make_unique<xc_filter_s>();
+    xcb::HostFilter& h = f->hf;
+    h.group = group;
+    h.K = K;
+    h.ks.assign(ks, ks + nc);
+    h.n_radii = n_radii;
+    h.n_angles = n_angles;
+    h.r_max = r_max;
+    h.r_min = r_min;
+    h.r_domain = r_domain;
+    const int rows = h.n_rows();
+    if (rows < 1) throw std::invalid_argument("n_radii must be >= 1");
+    h.comps.resize(size_t(rows) * nc);
+    for (int ci = 0; ci < nc; ++ci)
+      for (int r = 0; r < rows; ++r)
+        h.comps[size_t(r) * nc + ci] =
+            cplx(comps[2 * (size_t(ci) * rows + r)], comps[2 * (size_t(ci) * rows + r) + 1]);
+    *out = f.release();
+  });
+}
+
+void xc_filter_destroy(xc_filter f) { delete f; }
+
+int xc_filter_num_components(xc_filter f) { return f ? f->hf.nc() : 0; }
+
+int xc_decompose_rotation2(const double* filt, int height, int width, int layout, double cx,
+                           double cy, int K, int n_radii, int n_angles, double r_max,
+                           int* ks_out, double* comps_out, int* nc_out) {
+  return guarded(nullptr, [&] {
+    auto img = to_rowmajor(filt, height, width, layout);
+    auto f = xcb::decompose_rotation2(xcb::ImageView{img.data(), width, height}, cx, cy, K,
+                                      n_radii, n_angles, r_max);
+    export_filter(f, ks_out, comps_out, nc_out);
+  });
+}
+
+int xc_decompose_scale2(const double* filt, int height, int width, int layout, double cx,
+                        double cy, int K, int n_radii, int n_angles, double r_min,
+                        double r_max, double r_domain, int* ks_out, double* comps_out,
+                        int* nc_out) {
+  return guarded(nullptr, [&] {
+    auto img = to_rowmajor(filt, height, width, layout);
+    auto f = xcb::decompose_scale2(xcb::ImageView{img.data(), width, height}, cx, cy, K,
+                                   n_radii, n_angles, r_min, r_max, r_domain);
+    export_filter(f, ks_out, comps_out, nc_out);
+  });
+}
+
+int xc_render_component(xc_filter f, int ci, int width, int height, double cx, double cy,
+                        int layout, double* out) {
+  return guarded(nullptr, [&] {
+    if (ci < 0 || ci >= f->hf.nc()) throw std::invalid_argument("component index out of range");
+    xcb::render_component(f->hf, ci, width, height, cx, cy, layout == XC_COL_MAJOR,
+                          reinterpret_cast<cplx*>(out));
+  });
+}
+
+int xc_reconstruct(xc_filter f, int width, int height, double cx, double cy,
+                   const int* subset, int nsub, int layout, double* out) {
+  return guarded(nullptr, [&] {
+    xcb::reconstruct(f->hf, width, height, cx, cy, subset, subset ? nsub : -1,
+                     layout == XC_COL_MAJOR, reinterpret_cast<cplx*>(out));
+  });
+}
+
+int xc_inner_dc_value(xc_filter f, double* out2) {
+  return guarded(nullptr, [&] {
+    const cplx v = xcb::inner_dc_value(f->hf);
+    out2[0] = v.real();
+    out2[1] = v.imag();
+  });
+}
+
+int xc_run(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d, const void* signal,
+           const void* param, const int* components, int n_components, unsigned flags,
+           void* out, xc_stats* stats) {
+  return guarded(ctx, [&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const auto t_start = std::chrono::steady_clock::now();
+    if (mode != XC_CORRELATION && mode != XC_CONVOLUTION) throw std::invalid_argument("unknown mode");
+    if (!signal || !param || !out) throw std::invalid_argument("null argument");
+    if (d && d->out_dtype != XC_C64 && d->out_dtype != XC_C128)
+      throw std::invalid_argument("xc_run output must be complex (XC_C64 / XC_C128)");
+    Call c = setup(ctx, f, d, -1, components, n_components, (flags & XC_FLAG_PERIODIC) != 0);
+    const bool accumulate = (flags & XC_FLAG_ACCUMULATE) != 0;
+    if (accumulate && d->memory != XC_DEVICE)
+      throw std::invalid_argument("XC_FLAG_ACCUMULATE needs device memory");
+    const bool dc = c.f->hf.group == XC_SCALE2 && !(flags & XC_FLAG_NO_INNER_DC);
+    const size_t npix = size_t(c.rows) * c.cols, os = dtype_size(d->out_dtype);
+    const int out_kind = d->out_dtype == XC_C64 ? xcb::OUT_C64 : xcb::OUT_C128;
+    cudaEvent_t e0, e1;
+    ck(cudaEventCreate(&e0), "event");
+    ck(cudaEventCreate(&e1), "event");
+    double gpu_s = 0;
+    for (int img = 0; img < d->batch; ++img) {
+      Staged s = stage_inputs(c, signal, param, img);
+      ck(cudaEventRecord(e0, c.st), "event");
+      double* base = nullptr;
+      prep(c, s, false, &base, nullptr);
+      void* dout = d->memory == XC_DEVICE ? static_cast<char*>(out) + size_t(img) * npix * os
+                                           : c.ctx->buf<char>("out_stage", npix * os);
+      if (mode == XC_CORRELATION)
+        run_gather(c, s.sig, base, dout, out_kind, accumulate, dc);
+      else
+        run_scatter(c, s.sig, base, dout, out_kind, accumulate, dc);
+      ck(cudaGetLastError(), "kernel launch");
+      ck(cudaEventRecord(e1, c.st), "event");
+      if (d->memory == XC_HOST) {
+        ck(cudaEventSynchronize(e1), "pipeline");
+        gpu_s += event_seconds(e0, e1);
+        auto t0 = std::chrono::steady_clock::now();
+        ck(cudaMemcpyAsync(static_cast<char*>(out) + size_t(img) * npix * os, dout, npix * os,
+                           cudaMemcpyDeviceToHost, c.st),
+           "D2H");
+        ck(cudaStreamSynchronize(c.st), "D2H");
+        c.d2h_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      } else {
+        ck(cudaEventSynchronize(e1), "pipeline");
+        gpu_s += event_seconds(e0, e1);
+      }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    fill_stats(c, stats, gpu_s,
+               std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count(),
+               (long long)c.ks.size());
+  });
+}
+
+int xc_smooth(xc_context ctx, xc_filter f, const xc_image_desc* d, const void* signal,
+              const void* param, int normalize_signal, void* out, xc_stats* stats) {
+  return guarded(ctx, [&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const auto t_start = std::chrono::steady_clock::now();
+    if (!signal || !param || !out || !d) throw std::invalid_argument("null argument");
+    if (d->out_dtype != XC_F32 && d->out_dtype != XC_F64)
+      throw std::invalid_argument("xc_smooth output must be real (XC_F32 / XC_F64)");
+    // engine.hpp:388-392: zero-integral filters cannot be normalized
+    if (f && f->integral_state < 0) {
+      const xcb::HostFilter& hf = f->hf;
+      const int R = hf.render_radius(), S = 2 * R + 1;
+      std::vector<cplx> full(size_t(S) * S);
+      xcb::reconstruct(hf, S, S, R, R, nullptr, -1, false, full.data());
+      cplx integral(0);
+      double mx = 0;
+      for (auto& v : full) {
+        integral += v;
+        mx = std::max(mx, std::abs(v));
+      }
+      f->integral_state = std::abs(integral) < 1e-12 * std::max(1.0, mx) ? 0 : 1;
+    }
+    if (f && f->integral_state == 0)
+      throw std::invalid_argument("normalization undefined: filter has zero integral");
+    Call c = setup(ctx, f, d, -1, nullptr, 0, false);
+    const bool scale = c.f->hf.group == XC_SCALE2;
+    const bool weighted = normalize_signal && scale;  // engine.hpp:396-401
+    const size_t npix = size_t(c.rows) * c.cols, os = dtype_size(d->out_dtype);
+    float2* num = ctx->buf<float2>("smooth_num", npix);
+    float2* den = ctx->buf<float2>("smooth_den", npix);
+    unsigned* red = ctx->buf<unsigned>("smooth_red", 2);
+    long long clamped_total = 0;
+    cudaEvent_t e0, e1;
+    ck(cudaEventCreate(&e0), "event");
+    ck(cudaEventCreate(&e1), "event");
+    double gpu_s = 0;
+    for (int img = 0; img < d->batch; ++img) {
+      Staged s = stage_inputs(c, signal, param, img);
+      ck(cudaEventRecord(e0, c.st), "event");
+      double* base = nullptr;
+      float* wgt = nullptr;
+      prep(c, s, weighted, &base, weighted ? &wgt : nullptr);
+      xcb::SigSrc sn = s.sig, sd = s.sig;
+      sn.wgt = wgt;
+      sn.mode = weighted ? xcb::SIG_TIMES_W : xcb::SIG_PLAIN;
+      sd.wgt = wgt;
+      sd.mode = xcb::SIG_W_ONLY;  // the all-ones signal (times 1/s^2 when weighted)
+      run_scatter(c, sn, base, num, xcb::OUT_C64, false, scale);
+      run_scatter(c, sd, base, den, xcb::OUT_C64, false, scale);
+      ck(cudaMemsetAsync(red, 0, 2 * sizeof(unsigned), c.st), "memset");
+      void* dout = d->memory == XC_DEVICE ? static_cast<char*>(out) + size_t(img) * npix * os
+                                           : ctx->buf<char>("out_stage", npix * os);
+      xcb::launch_smooth_finish(num, den, npix, d->out_dtype == XC_F64, dout, red, red + 1, c.st,
+                                c.lc);
+      ck(cudaGetLastError(), "kernel launch");
+      ck(cudaEventRecord(e1, c.st), "event");
+      unsigned hred[2];
+      ck(cudaMemcpyAsync(hred, red, sizeof(hred), cudaMemcpyDeviceToHost, c.st), "readback");
+      ck(cudaStreamSynchronize(c.st), "smooth");
+      gpu_s += event_seconds(e0, e1);
+      clamped_total += hred[1];
+      if (d->memory == XC_HOST) {
+        auto t0 = std::chrono::steady_clock::now();
+        ck(cudaMemcpy(static_cast<char*>(out) + size_t(img) * npix * os, dout, npix * os,
+                      cudaMemcpyDeviceToHost),
+           "D2H");
+        c.d2h_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    fill_stats(c, stats, gpu_s,
+               std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count(),
+               2LL * (long long)c.ks.size());  // engine.hpp:406 num + den
+    if (stats) stats->clamped_pixels = int(clamped_total);
+  });
+}
+
+int xc_anglemax(xc_context ctx, xc_filter f, const xc_image_desc* d, const void* signal,
+                const int* components, int n_components, int n_angles, void* score,
+                int* argmax, xc_stats* stats) {
+  return guarded(ctx, [&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const auto t_start = std::chrono::steady_clock::now();
+    if (!signal || !score || !d) throw std::invalid_argument("null argument");
+    if (n_angles < 1) throw std::invalid_argument("n_angles must be >= 1");
+    if (d->out_dtype != XC_F32 && d->out_dtype != XC_F64)
+      throw std::invalid_argument("xc_anglemax score must be real (XC_F32 / XC_F64)");
+    Call c = setup(ctx, f, d, XC_ROTATION2, components, n_components, false);
+    const int span = *std::max_element(c.ks.begin(), c.ks.end()) -
+                     *std::min_element(c.ks.begin(), c.ks.end()) + 1;
+    if (span > 256) throw std::invalid_argument("band span too large for the angle max");
+    const size_t npix = size_t(c.rows) * c.cols, os = dtype_size(d->out_dtype);
+    float2* planes = ctx->buf<float2>("planes", size_t(c.bands.n) * npix);
+    float2* T1 = ctx->buf<float2>("T1", size_t(c.g.Hx2) * c.g.Pw);
+    float2* Hh = ctx->buf<float2>("Hhat", size_t(c.g.Ph) * c.g.Pw);
+    float2* T2 = ctx->buf<float2>("T2", size_t(c.bands.n) * c.g.H2 * c.g.Pw);
+    cudaEvent_t e0, e1;
+    ck(cudaEventCreate(&e0), "event");
+    ck(cudaEventCreate(&e1), "event");
+    double gpu_s = 0;
+    for (int img = 0; img < d->batch; ++img) {
+      Staged s = stage_inputs(c, signal, nullptr, img);
+      ck(cudaEventRecord(e0, c.st), "event");
+      xcb::launch_rows_fwd(*c.prow, c.g, s.sig, T1, c.st, c.lc);
+      xcb::launch_cols_fwd(*c.pcol, c.g, T1, Hh, c.st, c.lc);
+      xcb::launch_cols_inv_corr(*c.pcol, c.g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);
+      xcb::launch_rows_inv_planes(*c.prow, c.g, T2, c.bands.n, planes, c.st, c.lc);
+      char* dsc = d->memory == XC_DEVICE ? static_cast<char*>(score) + size_t(img) * npix * os
+                                         : ctx->buf<char>("score_stage", npix * os);
+      int* darg = nullptr;
+      if (argmax)
+        darg = d->memory == XC_DEVICE ? argmax + size_t(img) * npix
+                                      : ctx->buf<int>("arg_stage", npix);
+      xcb::launch_anglemax(planes, c.ks.data(), c.bands.n, npix, n_angles,
+                           d->out_dtype == XC_F64, dsc, darg, c.st, c.lc);
+      ck(cudaGetLastError(), "kernel launch");
+      ck(cudaEventRecord(e1, c.st), "event");
+      ck(cudaEventSynchronize(e1), "anglemax");
+      gpu_s += event_seconds(e0, e1);
+      if (d->memory == XC_HOST) {
+        auto t0 = std::chrono::steady_clock::now();
+        ck(cudaMemcpy(static_cast<char*>(score) + size_t(img) * npix * os, dsc, npix * os,
+                      cudaMemcpyDeviceToHost),
+           "D2H");
+        if (argmax)
+          ck(cudaMemcpy(argmax + size_t(img) * npix, darg, npix * sizeof(int),
+                        cudaMemcpyDeviceToHost),
+             "D2H");
+        c.d2h_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    fill_stats(c, stats, gpu_s,
+               std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count(),
+               (long long)c.ks.size());
+  });
+}
+
+// vote_filter.hpp:105-134
+int xc_find_peaks(const void* resp, int dtype, int height, int width, int layout, double radius,
+                  double threshold_frac, int* xs, int* ys, double* values, int max_peaks,
+                  int* n_found) {
+  return guarded(nullptr, [&] {
+    if (!resp || !n_found) throw std::invalid_argument("null argument");
+    if (dtype != XC_F32 && dtype != XC_F64) throw std::invalid_argument("response must be real");
+    auto at = [&](int y, int x) -> double {
+      const size_t i = layout == XC_COL_MAJOR ? size_t(x) * height + y : size_t(y) * width + x;
+      return dtype == XC_F32 ? double(static_cast<const float*>(resp)[i])
+                             : static_cast<const double*>(resp)[i];
+    };
+    double mx = -INFINITY;
+    for (int y = 0; y < height; ++y)
+      for (int x = 0; x < width; ++x) mx = std::max(mx, at(y, x));
+    const double thresh = threshold_frac * mx;
+    const int R = std::max(1, int(std::ceil(radius)));
+    struct Pk {
+      int x, y;
+      double v;
+    };
+    std::vector<Pk> peaks;
+    for (int y = 0; y < height; ++y)
+      for (int x = 0; x < width; ++x) {
+        const double v = at(y, x);
+        if (v < thresh) continue;
+        bool best = true;
+        for (int dy = -R; dy <= R && best; ++dy)
+          for (int dx = -R; dx <= R && best; ++dx) {
+            if (dx == 0 && dy == 0) continue;
+            if (dx * dx + dy * dy > radius * radius) continue;
+            const int xi = x + dx, yi = y + dy;
+            if (xi < 0 || yi < 0 || xi >= width || yi >= height) continue;
+            const double o = at(yi, xi);
+            if (o > v || (o == v && (dy < 0 || (dy == 0 && dx < 0)))) best = false;
+          }
+        if (best) peaks.push_back({x, y, v});
+      }
+    std::sort(peaks.begin(), peaks.end(), [](const Pk& a, const Pk& b) {
+      if (a.v != b.v) return a.v > b.v;
+      return a.y != b.y ? a.y < b.y : a.x < b.x;
+    });
+    const int n = int(peaks.size());
+    for (int i = 0; i < std::min(n, max_peaks); ++i) {
+      if (xs) xs[i] = peaks[i].x;
+      if (ys) ys[i] = peaks[i].y;
+      if (values) values[i] = peaks[i].v;
+    }
+    *n_found = n;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,312 @@
+// Shared-memory mixed-radix Stockham FFT for sm_100a (device side).
+//
+// Forward transform only (e^{-2 pi i nk/L}); inverse transforms are computed as
+// conj(FFT(conj(x))) with the conjugations and the 1/L scale folded into the
+// load / store functors of each kernel.  Codelets are compile-time: radices
+// 2, 3, 4, 5 hand-written, composites built by Cooley-Tukey in registers with
+// constexpr twiddles (folded to immediates after unrolling).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "fft_plan.h"
+
+namespace xcb {
+
+// ------------------------------------------------------------ complex helpers
+__device__ __forceinline__ float2 c_add(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 c_sub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 c_mul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+__device__ __forceinline__ float2 c_mulc(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ float2 c_conj(float2 a) { return make_float2(a.x, -a.y); }
+__device__ __forceinline__ float2 c_scale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+__device__ __forceinline__ float2 c_mi(float2 a) { return make_float2(a.y, -a.x); }  // -i * a
+
+// ------------------------------------------------------ constexpr twiddles
+__host__ __device__ constexpr double cx_sin_poly(double x) {
+  double x2 = x * x, term = x, sum = x;
+  for (int i = 1; i < 12; ++i) {
+    term *= -x2 / double((2 * i) * (2 * i + 1));
+    sum += term;
+  }
+  return sum;
+}
+__host__ __device__ constexpr double cx_cos_poly(double x) {
+  double x2 = x * x, term = 1.0, sum = 1.0;
+  for (int i = 1; i < 12; ++i) {
+    term *= -x2 / double((2 * i - 1) * (2 * i));
+    sum += term;
+  }
+  return sum;
+}
+// cos / sin of 2 pi a / b, octant-reduced
+__host__ __device__ constexpr double cx_cos_frac(long a, long b) {
+  a %= b;
+  if (a < 0) a += b;
+  const long q = (4 * a) / b;                      // quadrant 0..3
+  const double x = 6.283185307179586476925286766559 * double(4 * a - q * b) / double(4 * b);
+  const double c = x <= 0.78539816339744830962 ? cx_cos_poly(x)
+                                               : cx_sin_poly(1.5707963267948966192 - x);
+  const double s = x <= 0.78539816339744830962 ? cx_sin_poly(x)
+                                               : cx_cos_poly(1.5707963267948966192 - x);
+  return q == 0 ? c : q == 1 ? -s : q == 2 ? -c : s;
+}
+__host__ __device__ constexpr double cx_sin_frac(long a, long b) {
+  return cx_cos_frac(4 * a - b, 4 * b);  // sin t = cos(t - pi/2)
+}
+
+template <int R>
+struct CTw {  // e^{-2 pi i e / R}
+  float re[R], im[R];
+  __host__ __device__ constexpr CTw() : re(), im() {
+    for (int e = 0; e < R; ++e) {
+      re[e] = float(cx_cos_frac(e, R));
+      im[e] = float(-cx_sin_frac(e, R));
+    }
+  }
+};
+
+__host__ __device__ constexpr int first_factor(int R) {
+  return (R % 4 == 0 && R > 4) ? 4 : (R % 2 == 0 && R > 2) ? 2 : (R % 3 == 0 && R > 3) ? 3
+                                   : (R % 5 == 0 && R > 5) ? 5 : R;
+}
+
+// ---------------------------------------------------------------- codelets
+// Dft<R>::run(v) transforms v in place; output X[k] ends at v[Dft<R>::pos(k)]
+// (compile-time permutation), so composites need no second R-element array.
+template <int R>
+struct Dft {
+  static constexpr int A = first_factor(R);
+  static constexpr int B = R / A;
+  __host__ __device__ static constexpr int pos(int k) {
+    // X[k1 + A k2] sits at v[B k1 + pos_B(k2)] after the B-point stage
+    return B * (k % A) + Dft<B>::pos(k / A);
+  }
+  __device__ __forceinline__ static void run(float2* v) {
+    constexpr CTw<R> tw{};
+#pragma unroll
+    for (int n2 = 0; n2 < B; ++n2) {
+      float2 a[A];
+#pragma unroll
+      for (int n1 = 0; n1 < A; ++n1) a[n1] = v[B * n1 + n2];
+      Dft<A>::run(a);
+#pragma unroll
+      for (int k1 = 0; k1 < A; ++k1) {
+        const int e = (n2 * k1) % R;
+        const float2 x = a[Dft<A>::pos(k1)];
+        v[B * k1 + n2] = e == 0 ? x : c_mul(x, make_float2(tw.re[e], tw.im[e]));
+      }
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < A; ++k1) Dft<B>::run(v + B * k1);
+  }
+};
+
+template <>
+struct Dft<1> {
+  __host__ __device__ static constexpr int pos(int k) { return k; }
+  __device__ __forceinline__ static void run(float2*) {}
+};
+
+template <>
+struct Dft<2> {
+  __host__ __device__ static constexpr int pos(int k) { return k; }
+  __device__ __forceinline__ static void run(float2* v) {
+    const float2 a = v[0], b = v[1];
+    v[0] = c_add(a, b);
+    v[1] = c_sub(a, b);
+  }
+};
+
+template <>
+struct Dft<3> {
+  __host__ __device__ static constexpr int pos(int k) { return k; }
+  __device__ __forceinline__ static void run(float2* v) {
+    constexpr float s = 0.86602540378443864676f;  // sin(2 pi / 3)
+    const float2 t1 = c_add(v[1], v[2]), t2 = c_sub(v[1], v[2]);
+    const float2 m = make_float2(fmaf(-0.5f, t1.x, v[0].x), fmaf(-0.5f, t1.y, v[0].y));
+    const float2 n = make_float2(s * t2.y, -s * t2.x);  // -i s (x1 - x2)
+    v[0] = c_add(v[0], t1);
+    v[1] = c_add(m, n);
+    v[2] = c_sub(m, n);
+  }
+};
+
+template <>
+struct Dft<4> {
+  __host__ __device__ static constexpr int pos(int k) { return k; }
+  __device__ __forceinline__ static void run(float2* v) {
+    const float2 a = c_add(v[0], v[2]), b = c_sub(v[0], v[2]);
+    const float2 c = c_add(v[1], v[3]), d = c_sub(v[1], v[3]);
+    v[0] = c_add(a, c);
+    v[2] = c_sub(a, c);
+    v[1] = c_add(b, c_mi(d));
+    v[3] = c_sub(b, c_mi(d));
+  }
+};
+
+template <>
+struct Dft<5> {
+  __host__ __device__ static constexpr int pos(int k) { return k; }
+  __device__ __forceinline__ static void run(float2* v) {
+    constexpr float c1 = 0.30901699437494742410f, c2 = -0.80901699437494742410f;
+    constexpr float s1 = 0.95105651629515357212f, s2 = 0.58778525229247312917f;
+    const float2 t1 = c_add(v[1], v[4]), t2 = c_add(v[2], v[3]);
+    const float2 t3 = c_sub(v[1], v[4]), t4 = c_sub(v[2], v[3]);
+    const float2 x0 = v[0];
+    const float2 a1 = make_float2(fmaf(c1, t1.x, fmaf(c2, t2.x, x0.x)), fmaf(c1, t1.y, fmaf(c2, t2.y, x0.y)));
+    const float2 a2 = make_float2(fmaf(c2, t1.x, fmaf(c1, t2.x, x0.x)), fmaf(c2, t1.y, fmaf(c1, t2.y, x0.y)));
+    const float2 b1 = make_float2(fmaf(s1, t3.x, s2 * t4.x), fmaf(s1, t3.y, s2 * t4.y));
+    const float2 b2 = make_float2(fmaf(s2, t3.x, -s1 * t4.x), fmaf(s2, t3.y, -s1 * t4.y));
+    v[0] = c_add(x0, c_add(t1, t2));
+    v[1] = c_add(a1, c_mi(b1));
+    v[4] = c_sub(a1, c_mi(b1));
+    v[2] = c_add(a2, c_mi(b2));
+    v[3] = c_sub(a2, c_mi(b2));
+  }
+};
+
+// --------------------------------------------------------- radix dispatch
+template <int N>
+struct IntC {
+  static constexpr int value = N;
+};
+
+// Every radix make_fft_plan may choose (fft_plan.cpp kRadices).
+template <class F>
+__device__ __forceinline__ void radix_dispatch(int R, F&& f) {
+  switch (R) {
+    case 2: f(IntC<2>{}); break;
+    case 3: f(IntC<3>{}); break;
+    case 4: f(IntC<4>{}); break;
+    case 5: f(IntC<5>{}); break;
+    case 6: f(IntC<6>{}); break;
+    case 8: f(IntC<8>{}); break;
+    case 9: f(IntC<9>{}); break;
+    case 10: f(IntC<10>{}); break;
+    case 12: f(IntC<12>{}); break;
+    case 15: f(IntC<15>{}); break;
+    case 16: f(IntC<16>{}); break;
+    case 18: f(IntC<18>{}); break;
+    case 20: f(IntC<20>{}); break;
+    default: break;
+  }
+}
+
+__device__ __forceinline__ int sm_phys(int n) { return n + (n >> 4); }
+
+// ------------------------------------------------------------------ passes
+// Out-of-place (ping-pong) Stockham: pass q reads buffer q&1 and writes the
+// other, so threads loop over butterflies freely.  Butterfly (j, g): inputs
+// j + r*L/R, twiddle W_{Ns R}^{(j mod Ns) r}, outputs (j - jm) R + jm + r Ns.
+
+template <int R, class Load>
+__device__ __forceinline__ void pass_first(const FftPlanD& p, float2* dst, Load& load) {
+  const int nb = p.L / R;
+  const int items = nb * kG;
+  for (int w = threadIdx.x; w < items; w += blockDim.x) {
+    const int g = w & (kG - 1), j = w >> 1;
+    float2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = load(j + r * nb, g);
+    Dft<R>::run(v);
+    float2* d = dst + g * p.Lp;
+#pragma unroll
+    for (int r = 0; r < R; ++r) d[sm_phys(j * R + r)] = v[Dft<R>::pos(r)];
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void load_twiddled(const FftPlanD& p, int q, const float2* src,
+                                              int j, int jm, float2* v) {
+  const int nb = p.L / R, Ns = p.ns[q];
+#pragma unroll
+  for (int r = 0; r < R; ++r) v[r] = src[sm_phys(j + r * nb)];
+  const float2* tw = p.tw + p.tw_off[q] + jm;
+#pragma unroll
+  for (int r = 1; r < R; ++r) v[r] = c_mul(v[r], __ldg(tw + (r - 1) * Ns));
+}
+
+template <int R>
+__device__ __noinline__ void pass_mid(const FftPlanD& p, int q, const float2* src,
+                                      float2* dst) {
+  const int nb = p.L / R, Ns = p.ns[q];
+  const int items = nb * kG;
+  for (int w = threadIdx.x; w < items; w += blockDim.x) {
+    const int g = w & (kG - 1), j = w >> 1;
+    const int jm = j - Ns * int(__umulhi(unsigned(j), p.magic[q]));
+    float2 v[R];
+    load_twiddled<R>(p, q, src + g * p.Lp, j, jm, v);
+    Dft<R>::run(v);
+    float2* d = dst + g * p.Lp;
+    const int base = (j - jm) * R + jm;
+#pragma unroll
+    for (int r = 0; r < R; ++r) d[sm_phys(base + r * Ns)] = v[Dft<R>::pos(r)];
+  }
+}
+
+// Last pass (Ns = L/R, so jm = j): output k = j + r*nb -> store(k, g, value).
+template <int R, class Store>
+__device__ __forceinline__ void pass_last(const FftPlanD& p, int q, const float2* src,
+                                          Store& store) {
+  const int nb = p.L / R;
+  const int items = nb * kG;
+  for (int w = threadIdx.x; w < items; w += blockDim.x) {
+    const int g = w & (kG - 1), j = w >> 1;
+    float2 v[R];
+    load_twiddled<R>(p, q, src + g * p.Lp, j, j, v);
+    Dft<R>::run(v);
+#pragma unroll
+    for (int r = 0; r < R; ++r) store(j + r * nb, g, v[Dft<R>::pos(r)]);
+  }
+}
+
+template <int R, class Load, class Store>
+__device__ __forceinline__ void pass_single(Load& load, Store& store) {
+  const int g = threadIdx.x;
+  if (g < kG) {
+    float2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = load(r, g);
+    Dft<R>::run(v);
+#pragma unroll
+    for (int r = 0; r < R; ++r) store(r, g, v[Dft<R>::pos(r)]);
+  }
+}
+
+// Full forward transform of the CTA's kG sequences: load -> FFT -> store.
+// Every thread of the CTA must call it; `sm` holds 2 * kG * p.Lp float2.
+// Begins and ends with a barrier-free region: callers reusing `sm` for a
+// following transform must __syncthreads() in between.
+template <class Load, class Store>
+__device__ __forceinline__ void fft_block(const FftPlanD& p, float2* sm, Load& load,
+                                          Store& store) {
+  if (p.npass == 0) {  // L == 1
+    if (threadIdx.x < kG) store(0, threadIdx.x, load(0, threadIdx.x));
+    return;
+  }
+  if (p.npass == 1) {
+    radix_dispatch(p.radix[0], [&](auto rc) { pass_single<decltype(rc)::value>(load, store); });
+    return;
+  }
+  float2* buf[2] = {sm, sm + kG * p.Lp};
+  radix_dispatch(p.radix[0], [&](auto rc) { pass_first<decltype(rc)::value>(p, buf[0], load); });
+  __syncthreads();
+  int cur = 0;
+  for (int q = 1; q < p.npass - 1; ++q) {
+    radix_dispatch(p.radix[q], [&](auto rc) {
+      pass_mid<decltype(rc)::value>(p, q, buf[cur], buf[cur ^ 1]);
+    });
+    cur ^= 1;
+    __syncthreads();
+  }
+  const int ql = p.npass - 1;
+  radix_dispatch(p.radix[ql],
+                 [&](auto rc) { pass_last<decltype(rc)::value>(p, ql, buf[cur], store); });
+}
+
+}  // namespace xcb

@@ -1,0 +1,45 @@
+// Host-built plans for the shared-memory Stockham FFT (fft_core.cuh).
+//
+// One CTA transforms kG = 2 sequences of length L held in shared memory
+// ([g][phys(n)], phys(n) = n + n/16 to break power-of-two bank strides), in
+// two ping-pong buffers.  L = R_0 * R_1 * ... with radices from a
+// compile-time codelet set (2..20, 2/3/5-smooth).  The first pass reads the
+// input through a functor (global memory), the last pass writes through a
+// functor; middle passes go smem -> smem.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <vector>
+
+namespace xcb {
+
+constexpr int kG = 2;            // sequences per CTA (= interleave of the layouts)
+constexpr int kMaxPasses = 6;
+constexpr int kMaxThreads = 512;  // __launch_bounds__ of every FFT kernel
+
+struct FftPlanD {
+  int L;        // transform length
+  int Lp;       // smem stride per sequence (float2 units)
+  int npass;
+  int nt;       // threads per CTA
+  int radix[kMaxPasses];
+  int ns[kMaxPasses];            // product of the radices before pass q
+  unsigned magic[kMaxPasses];    // ceil(2^32 / ns) for j / ns
+  int tw_off[kMaxPasses];        // offset of pass q in the twiddle table
+  const float2* tw;              // device twiddles: pass q entry (r-1)*ns + jm
+};
+
+struct FftPlan {
+  FftPlanD d{};
+  std::vector<float2> tw_host;
+  size_t smem_bytes() const { return 2 * size_t(kG) * d.Lp * sizeof(float2); }
+};
+
+bool is_smooth235(int n);
+// Builds a plan for length L (2/3/5-smooth); false if no factorization fits
+// the codelet set and thread budget.
+bool make_fft_plan(int L, FftPlan* out);
+// Smallest plannable 2/3/5-smooth length >= n (the pad size rule).
+int pick_fft_length(int n);
+
+}  // namespace xcb

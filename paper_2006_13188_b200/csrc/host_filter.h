@@ -1,0 +1,54 @@
+// Host side of the boundary: filter band decomposition and per-band rendering.
+// These run once per filter on the CPU (north star: "Filter band decomposition
+// stays on the host and runs once per filter"); the rendered components feed
+// the device spectrum cache.  Reference: proj/include/xconv/freq_filter.hpp,
+// polar.hpp, field.hpp.
+#pragma once
+#include <complex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace xcb {
+
+using cplx = std::complex<double>;
+
+struct HostFilter {  // FreqFilter2, freq_filter.hpp:21-46
+  int group = 0;     // 0 rotation2, 1 scale2
+  int K = 0;
+  std::vector<int> ks;
+  std::vector<cplx> comps;  // row-major [n_rows][nc]
+  int n_radii = 0, n_angles = 0;
+  double r_max = 0, r_min = 0, r_domain = 0;
+
+  int nc() const { return int(ks.size()); }
+  int n_rows() const { return group == 0 ? n_radii : n_angles; }
+  const cplx& comp(int row, int ci) const { return comps[size_t(row) * nc() + ci]; }
+  double domain_top() const { return r_domain > 0 ? r_domain : r_max; }
+  double omega() const;
+  int index_of(int k) const;
+  int render_radius() const;  // engine.hpp:255-258
+};
+
+// Field2 view of a complex image, row-major [y][x].
+struct ImageView {
+  const cplx* data;
+  int width, height;
+  cplx sample(double x, double y) const;  // field.hpp:51-62
+};
+
+HostFilter decompose_rotation2(const ImageView& f, double cx, double cy, int K,
+                               int n_radii, int n_angles, double r_max);
+HostFilter decompose_scale2(const ImageView& f, double cx, double cy, int K,
+                            int n_radii, int n_angles, double r_min, double r_max,
+                            double r_domain);
+cplx component_value(const HostFilter& f, int ci, double r, double theta);
+cplx inner_dc_value(const HostFilter& f);
+// (2R+1)^2-style rendering, row-major [y][x]; transpose=true renders f(y,x)
+// (used when the caller's grids are column-major).
+void render_component(const HostFilter& f, int ci, int width, int height, double cx,
+                      double cy, bool transpose, cplx* out);
+void reconstruct(const HostFilter& f, int width, int height, double cx, double cy,
+                 const int* subset, int nsub, bool transpose, cplx* out);
+
+}  // namespace xcb

@@ -1,0 +1,216 @@
+// Per-pixel stages: steering base / guard band, dtype conversion, smooth divide, angle max.
+#include "stages_common.cuh"
+
+namespace xcb {
+namespace {
+
+// ------------------------------------------------------------------ prep
+template <class TP>
+__global__ void k_prep(const TP* __restrict__ param, int kind, double omega, double lo,
+                       double hi, int H, int W, int transposed, double* __restrict__ base,
+                       float* __restrict__ wgt, unsigned long long* bad) {
+  const size_t n = size_t(H) * W;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const double v = double(param[i]);
+    if (kind == 0) {
+      base[i] = v;
+      if (wgt) wgt[i] = 1.f;
+      continue;
+    }
+    // true y-major index of the pixel (the reference scans y, then x)
+    const size_t r = i / W, cidx = i % W;
+    const unsigned long long ti = transposed ? (unsigned long long)cidx * H + r : i;
+    if (!(v > 0.0) || !isfinite(v)) {
+      atomicMin(bad, ti);
+      base[i] = 0.0;
+      if (wgt) wgt[i] = 0.f;
+      continue;
+    }
+    if (v < lo || v > hi) atomicMin(bad + 1, ti);
+    base[i] = omega * log(v);
+    if (wgt) wgt[i] = float(1.0 / (v * v));
+  }
+}
+
+template <class TS, class TD>
+__global__ void k_convert(const TS* __restrict__ s, TD* __restrict__ d, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    d[i] = TD(s[i]);
+}
+__global__ void k_convert_c(const double2* __restrict__ s, float2* __restrict__ d, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    d[i] = make_float2(float(s[i].x), float(s[i].y));
+}
+
+// ------------------------------------------------------------------ smooth
+__global__ void k_smooth_max(const float2* __restrict__ den, size_t n, unsigned* maxbits) {
+  float m = 0.f;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    m = fmaxf(m, hypotf(den[i].x, den[i].y));
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ float red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) atomicMax(maxbits, __float_as_uint(m));
+  }
+}
+
+template <class TO>
+__global__ void k_smooth_div(const float2* __restrict__ num, const float2* __restrict__ den,
+                             size_t n, const unsigned* maxbits, TO* __restrict__ out,
+                             unsigned* clamped) {
+  const double floor_ = 1e-9 * double(__uint_as_float(*maxbits));
+  unsigned cnt = 0;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const double dx = den[i].x, dy = den[i].y;
+    const double ad = sqrt(dx * dx + dy * dy);
+    if (ad < floor_) {
+      ++cnt;
+      out[i] = TO(0);
+      continue;
+    }
+    out[i] = TO((double(num[i].x) * dx + double(num[i].y) * dy) / (dx * dx + dy * dy));
+  }
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(clamped, cnt);
+}
+
+// ------------------------------------------------------------------ angle max
+constexpr int kMaxDense = 256;
+struct AngleMap {
+  int nd;                 // dense coefficient count (kmax - kmin + 1)
+  int idx[kMaxDense];     // plane index of dense slot d, or -1
+};
+
+template <class TO>
+__global__ void __launch_bounds__(128)
+    k_anglemax(const float2* __restrict__ planes, AngleMap m, size_t npix, int n,
+               TO* __restrict__ score, int* __restrict__ argmax) {
+  extern __shared__ float2 sa[];
+  float2* tw = sa;                   // [n] e^{-2 pi i s / n}
+  float2* co = sa + n;               // [nd][blockDim]
+  const int bd = blockDim.x, t = threadIdx.x;
+  for (int s = t; s < n; s += bd) {
+    double sn, cs;
+    sincospi(-2.0 * s / n, &sn, &cs);
+    tw[s] = make_float2(float(cs), float(sn));
+  }
+  const size_t p = blockIdx.x * size_t(bd) + t;
+  for (int d = 0; d < m.nd; ++d)
+    co[d * bd + t] = (p < npix && m.idx[d] >= 0) ? planes[size_t(m.idx[d]) * npix + p]
+                                                 : make_float2(0.f, 0.f);
+  __syncthreads();
+  if (p >= npix) return;
+  constexpr int CH = 12;
+  float best = -1.f;
+  int arg = 0;
+  for (int s0 = 0; s0 < n; s0 += CH) {
+    float2 acc[CH], z[CH];
+    const float2 top = co[(m.nd - 1) * bd + t];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      z[c] = tw[min(s0 + c, n - 1)];
+      acc[c] = top;
+    }
+    for (int d = m.nd - 2; d >= 0; --d) {
+      const float2 gv = co[d * bd + t];
+#pragma unroll
+      for (int c = 0; c < CH; ++c) acc[c] = c_add(c_mul(acc[c], z[c]), gv);
+    }
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const float m2 = fmaf(acc[c].x, acc[c].x, acc[c].y * acc[c].y);
+      if (s0 + c < n && m2 > best) {
+        best = m2;
+        arg = s0 + c;
+      }
+    }
+  }
+  score[p] = TO(sqrtf(best));
+  if (argmax) argmax[p] = arg;
+}
+
+}  // namespace
+
+float2* upload_twiddles(const FftPlan& p) {
+  float2* d = nullptr;
+  if (cudaMalloc(&d, p.tw_host.size() * sizeof(float2)) != cudaSuccess) return nullptr;
+  cudaMemcpy(d, p.tw_host.data(), p.tw_host.size() * sizeof(float2), cudaMemcpyHostToDevice);
+  return d;
+}
+
+void launch_prep(const void* param, int param_is_f64, int kind, double omega, double lo,
+                 double hi, int H, int W, int transposed, double* base, float* wgt,
+                 unsigned long long* bad, cudaStream_t st, LaunchCounter& lc) {
+  const int g = grid_for(size_t(H) * W, 256);
+  if (param_is_f64)
+    k_prep<double><<<g, 256, 0, st>>>(static_cast<const double*>(param), kind, omega, lo, hi,
+                                      H, W, transposed, base, wgt, bad);
+  else
+    k_prep<float><<<g, 256, 0, st>>>(static_cast<const float*>(param), kind, omega, lo, hi,
+                                     H, W, transposed, base, wgt, bad);
+  ++lc.n;
+}
+
+void launch_convert_signal(const void* src, int dtype, size_t n, void* dst, cudaStream_t st,
+                           LaunchCounter& lc) {
+  const int g = grid_for(n, 256);
+  if (dtype == 1)  // f64 real -> f32
+    k_convert<double, float><<<g, 256, 0, st>>>(static_cast<const double*>(src),
+                                                static_cast<float*>(dst), n);
+  else  // c128 -> c64
+    k_convert_c<<<g, 256, 0, st>>>(static_cast<const double2*>(src), static_cast<float2*>(dst),
+                                   n);
+  ++lc.n;
+}
+
+void launch_smooth_finish(const float2* num, const float2* den, size_t n, int out_f64,
+                          void* out, unsigned* maxbits, unsigned* clamped, cudaStream_t st,
+                          LaunchCounter& lc) {
+  const int g = grid_for(n, 256);
+  k_smooth_max<<<g, 256, 0, st>>>(den, n, maxbits);
+  if (out_f64)
+    k_smooth_div<double><<<g, 256, 0, st>>>(num, den, n, maxbits, static_cast<double*>(out),
+                                            clamped);
+  else
+    k_smooth_div<float><<<g, 256, 0, st>>>(num, den, n, maxbits, static_cast<float*>(out),
+                                           clamped);
+  lc.n += 2;
+}
+
+void launch_anglemax(const float2* planes, const int* ks_host, int nb, size_t npix,
+                     int n_angles, int score_f64, void* score, int* argmax, cudaStream_t st,
+                     LaunchCounter& lc) {
+  AngleMap m{};
+  int kmin = ks_host[0], kmax = ks_host[0];
+  for (int i = 0; i < nb; ++i) {
+    kmin = ks_host[i] < kmin ? ks_host[i] : kmin;
+    kmax = ks_host[i] > kmax ? ks_host[i] : kmax;
+  }
+  m.nd = kmax - kmin + 1;
+  for (int d = 0; d < m.nd && d < kMaxDense; ++d) m.idx[d] = -1;
+  for (int i = 0; i < nb; ++i) m.idx[ks_host[i] - kmin] = i;
+  const int bs = 128;
+  const size_t smem = (size_t(n_angles) + size_t(m.nd) * bs) * sizeof(float2);
+  const int grid = int((npix + bs - 1) / bs);
+  if (score_f64) {
+    set_smem(k_anglemax<double>, smem);
+    k_anglemax<double><<<grid, bs, smem, st>>>(planes, m, npix, n_angles,
+                                               static_cast<double*>(score), argmax);
+  } else {
+    set_smem(k_anglemax<float>, smem);
+    k_anglemax<float><<<grid, bs, smem, st>>>(planes, m, npix, n_angles,
+                                              static_cast<float*>(score), argmax);
+  }
+  ++lc.n;
+}
+
+}  // namespace xcb

@@ -1,0 +1,112 @@
+// Device pipeline stages of the extended correlation / convolution hot path.
+//
+// Data layouts in HBM (complex fp32 = float2, per image):
+//   signal   [H][W]  as the caller stores it (transposed problems are handled
+//                    by rendering the filter transposed)
+//   T1       layout B': [u/2][y][u%2], Hx2 rows  -- row-FFT output (F1, S1)
+//   spectra  layout B : [u/2][v][u%2], Ph rows   -- H^, F^_k, Sigma
+//   T2       layout A : [y/2][u][y%2], H2 rows   -- column-IFFT output (I1, S2)
+// Every kernel reads its input block contiguously (a column pair of B/B' or a
+// row pair of A) and writes its output as 32-byte sector-complete scatters.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "fft_plan.h"
+
+namespace xcb {
+
+struct Geo {
+  int H, W;    // output (= signal) extent, as stored
+  int Hx, Wx;  // transform input extent: H, W (zero pad) or H+2R, W+2R (periodic)
+  int Hx2;     // Hx rounded up to even (rows of T1)
+  int H2;      // H rounded up to even (rows of T2)
+  int off;     // crop offset: 0, or R (periodic)
+  int Ph, Pw;  // transform size
+  int R;       // render radius
+  int periodic;
+};
+
+enum SigMode { SIG_PLAIN = 0, SIG_TIMES_W = 1, SIG_W_ONLY = 2 };
+
+struct SigSrc {
+  const void* sig;  // float [H][W] (real) or float2 (complex)
+  int is_complex;
+  const float* wgt; // per-pixel real weight (smooth: 1/s^2) or null
+  int mode;         // SigMode
+};
+
+struct Bands {
+  const int* k;     // band frequencies (device)
+  const int* spec;  // index of each band's spectrum in the filter cache
+  int n;
+};
+
+// out accumulator element type
+enum OutKind { OUT_C64 = 0, OUT_C128 = 1 };
+
+struct LaunchCounter {
+  int n = 0;
+};
+
+// Per-pixel steering base: rotation theta, scale omega*log(s) (double), the
+// smooth weight 1/s^2 (float, optional) and the scale guard-band check.
+// bad[0] = first pixel (true y-major index) with s <= 0 or non-finite,
+// bad[1] = first pixel outside [lo, hi].  transposed: stored [x][y].
+void launch_prep(const void* param, int param_is_f64, int kind, double omega, double lo,
+                 double hi, int H, int W, int transposed, double* base, float* wgt,
+                 unsigned long long* bad, cudaStream_t st, LaunchCounter& lc);
+
+void launch_convert_signal(const void* src, int dtype, size_t n, void* dst,
+                           cudaStream_t st, LaunchCounter& lc);
+
+// F1: row FFT of the (zero-padded / periodically extended) signal -> T1.
+void launch_rows_fwd(const FftPlan& prow, const Geo& g, const SigSrc& s, float2* T1,
+                     cudaStream_t st, LaunchCounter& lc);
+// F2: column FFT of T1 -> spectrum (layout B).
+void launch_cols_fwd(const FftPlan& pcol, const Geo& g, const float2* T1, float2* spec,
+                     cudaStream_t st, LaunchCounter& lc);
+// I1: per band, column IFFT of H^ . conj(F^_k) -> T2_b (band planes, H2*Pw each).
+void launch_cols_inv_corr(const FftPlan& pcol, const Geo& g, const float2* Hhat,
+                          const float2* Fhat, size_t spec_stride, const Bands& b,
+                          float2* T2, cudaStream_t st, LaunchCounter& lc);
+// I2: per band, row IFFT of T2_b, crop, steer e^{+i k phi}, accumulate.
+void launch_rows_inv_steer(const FftPlan& prow, const Geo& g, const float2* T2,
+                           const Bands& b, const double* base, int out_kind, void* out,
+                           int accumulate, const SigSrc& dc_sig, double dc_re,
+                           double dc_im, cudaStream_t st, LaunchCounter& lc);
+// I2 variant for the angle max: per band, row IFFT of T2_b, crop -> G planes.
+void launch_rows_inv_planes(const FftPlan& prow, const Geo& g, const float2* T2,
+                            int nbands, float2* planes, cudaStream_t st,
+                            LaunchCounter& lc);
+// S1: per band, row FFT of signal . e^{-i k phi} -> T1_b planes (Hx2*Pw each).
+void launch_rows_fwd_premul(const FftPlan& prow, const Geo& g, const SigSrc& s,
+                            const double* base, const Bands& b, float2* T1,
+                            cudaStream_t st, LaunchCounter& lc);
+// S2: per column pair, sum over bands of FFT_y(T1_b) . F^_b, then IFFT_y -> T2.
+void launch_cols_fwd_mac_inv(const FftPlan& pcol, const Geo& g, const float2* T1,
+                             const float2* Fhat, size_t spec_stride, const Bands& b,
+                             float2* Sigma, float2* T2, cudaStream_t st, LaunchCounter& lc);
+// S4: row IFFT of T2, crop (+ dc * signal) -> out.
+void launch_rows_inv_out(const FftPlan& prow, const Geo& g, const float2* T2,
+                         int out_kind, void* out, int accumulate, const SigSrc& dc_sig,
+                         double dc_re, double dc_im, cudaStream_t st, LaunchCounter& lc);
+
+// Filter spectra: rendered (2R+1)^2 components (nb bands, c64) -> F^ (layout B).
+void launch_filter_spectra(const FftPlan& prow, const FftPlan& pcol, const Geo& g,
+                           const float2* comps, int nb, float2* T1f, float2* Fhat,
+                           cudaStream_t st, LaunchCounter& lc);
+
+// smooth: max |den| (as float bits) then divide with the 1e-9 floor.
+void launch_smooth_finish(const float2* num, const float2* den, size_t n, int out_f64,
+                          void* out, unsigned* maxbits, unsigned* clamped,
+                          cudaStream_t st, LaunchCounter& lc);
+
+// angle max over n_angles of |sum_b G_b e^{-i k_b 2 pi s/n}|.
+void launch_anglemax(const float2* planes, const int* ks_host, int nb, size_t npix,
+                     int n_angles, int score_f64, void* score, int* argmax,
+                     cudaStream_t st, LaunchCounter& lc);
+
+// Upload the plan's twiddles; returns device pointer (owned by caller).
+float2* upload_twiddles(const FftPlan& p);
+
+}  // namespace xcb

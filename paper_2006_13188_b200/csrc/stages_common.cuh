@@ -1,0 +1,83 @@
+// Shared device helpers of the pipeline stages (included by k_*.cu).
+#pragma once
+#include "fft_core.cuh"
+#include "kernels.h"
+
+namespace xcb {
+namespace {
+
+constexpr double kTwoPiHi = 6.283185307179586232;
+constexpr double kTwoPiLo = 2.4492935982947064e-16;
+constexpr double kInvTwoPi = 0.15915494309189533577;
+
+// e^{sign * i * k * base}: the product is formed and reduced mod 2 pi in double
+// (k*theta is exact for fp32 theta), then evaluated with accurate sincosf.
+__device__ __forceinline__ float2 steer(int k, double base, float sign) {
+  const double ph = double(k) * base;
+  const double q = rint(ph * kInvTwoPi);
+  double r = fma(-q, kTwoPiHi, ph);
+  r = fma(-q, kTwoPiLo, r);
+  float s, c;
+  sincosf(float(r), &s, &c);
+  return make_float2(c, sign * s);
+}
+
+// transform-input row/column y' -> source index, or -1 for the zero pad
+__device__ __forceinline__ int src_index(int yp, int ext, int n, int R, int periodic) {
+  if (yp >= ext) return -1;
+  if (!periodic) return yp;
+  int y = (yp - R) % n;
+  return y < 0 ? y + n : y;
+}
+
+__device__ __forceinline__ float2 sig_value(const SigSrc& s, size_t i) {
+  if (s.mode == SIG_W_ONLY) return make_float2(s.wgt ? s.wgt[i] : 1.f, 0.f);
+  float2 v = s.is_complex ? static_cast<const float2*>(s.sig)[i]
+                          : make_float2(static_cast<const float*>(s.sig)[i], 0.f);
+  if (s.mode == SIG_TIMES_W) v = c_scale(v, s.wgt[i]);
+  return v;
+}
+
+template <class TO>
+struct OutOps;
+template <>
+struct OutOps<float2> {
+  __device__ static void put(float2* o, size_t i, float2 v, bool acc, float2 extra) {
+    float2 t = c_add(v, extra);
+    if (acc) t = c_add(o[i], t);
+    o[i] = t;
+  }
+};
+template <>
+struct OutOps<double2> {
+  __device__ static void put(double2* o, size_t i, float2 v, bool acc, float2 extra) {
+    double2 t = make_double2(double(v.x) + double(extra.x), double(v.y) + double(extra.y));
+    if (acc) {
+      t.x += o[i].x;
+      t.y += o[i].y;
+    }
+    o[i] = t;
+  }
+};
+
+__device__ __forceinline__ float2 dc_term(const SigSrc& s, size_t i, double dr, double di) {
+  if (dr == 0.0 && di == 0.0) return make_float2(0.f, 0.f);
+  const float2 h = sig_value(s, i);
+  return make_float2(float(dr * h.x - di * h.y), float(dr * h.y + di * h.x));
+}
+
+// ------------------------------------------------------------------ launch helpers
+template <class K>
+void set_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024)
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+}
+
+int grid_for(size_t n, int bs) {
+  size_t g = (n + bs - 1) / bs;
+  if (g > 148 * 32) g = 148 * 32;
+  return int(g < 1 ? 1 : g);
+}
+
+}  // namespace
+}  // namespace xcb

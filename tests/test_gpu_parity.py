@@ -1,0 +1,307 @@
+"""GPU parity: the sm_100a path through the C ABI vs the CPU oracle.
+
+Tolerances: relative L2 <= 1e-5 (north star, fp32 GPU vs double oracle on the
+same fp32 inputs) unless a reference test pins a looser bound (brute-force
+oracle 3e-3); peak locations exact.  Each test names the reference test or
+BASELINE config it follows.
+"""
+import numpy as np
+import pytest
+
+import paper_2006_13188_b200 as X
+
+pytestmark = pytest.mark.gpu
+ROT, SCALE = 0, 1
+TOL = 1e-5
+
+
+def ofilter(orc, F):
+    return orc.Filter(int(F.group), F.K, F.ks, F.comps, F.n_radii, F.n_angles, F.r_max,
+                      F.r_min, F.r_domain)
+
+
+def pfilter(F):
+    return X.FreqFilter2(F.group, F.K, F.ks, F.comps, F.n_radii, F.n_angles, F.r_max,
+                         F.r_min, F.r_domain)
+
+
+def xfield(kind, p):
+    return X.XformField.rotation(p) if kind == ROT else X.XformField.scaling(p)
+
+
+def full_decomp(orc, filt, R, n_radii=24, n_angles=64):
+    return orc.decompose_rotation2(filt, R, R, n_angles, n_radii, n_angles, R)
+
+
+# ------------------------------------------------------ reference KATs on GPU
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_rotation_matches_oracle_fast_path(orc, mode):  # test_engine2d.cpp:140-153
+    rng = orc.Rng(55)
+    n, R = 24, 6
+    F = full_decomp(orc, rng.random_smooth_filter(R), R)
+    H = rng.random_field(n, n, False)
+    T = rng.random_rotation_field(n, n)
+    ref = (orc.xcorr_fast if mode == 0 else orc.xconv_fast)(H, ROT, T, F)[0]
+    fn = X.xcorr_fast if mode == 0 else X.xconv_fast
+    r = fn(H, X.XformField.rotation(T), pfilter(F))
+    assert r.standard_ops == F.n_components()
+    assert orc.rel_l2(r.output, ref) < TOL
+    assert orc.rel_l2(r.output, orc.spectral_oracle(mode, H, ROT, T, F)) < TOL
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_scale_matches_oracle(orc, mode):  # test_engine_scale.cpp:121-134
+    rng = orc.Rng(73)
+    n, R = 20, 6
+    F = orc.decompose_scale2(rng.annular_filter(R), R, R, 8, 48, 32, 1.0, R)
+    H = rng.random_field(n, n, False)
+    T = rng.random_scale_field(n, n)
+    ref = (orc.xcorr_fast if mode == 0 else orc.xconv_fast)(H, SCALE, T, F)[0]
+    fn = X.xcorr_fast if mode == 0 else X.xconv_fast
+    r = fn(H, X.XformField.scaling(T), pfilter(F))
+    assert orc.rel_l2(r.output, ref) < TOL
+
+
+def test_rotation_fast_matches_brute(orc):  # test_engine2d.cpp:123-138
+    rng = orc.Rng(54)
+    n, R = 24, 6
+    F = full_decomp(orc, rng.random_smooth_filter(R), R)
+    PF = pfilter(F)
+    for _ in range(3):
+        H = rng.random_field(n, n, False)
+        T = rng.random_rotation_field(n, n)
+        assert orc.rel_l2(X.xcorr_fast(H, X.XformField.rotation(T), PF).output,
+                          orc.xcorr_brute(H, ROT, T, F)) < 3e-3
+        assert orc.rel_l2(X.xconv_fast(H, X.XformField.rotation(T), PF).output,
+                          orc.xconv_brute(H, ROT, T, F)) < 3e-3
+
+
+def test_single_component_plan(orc):  # test_engine2d.cpp:176-194
+    rng = orc.Rng(57)
+    n, R = 16, 5
+    F = full_decomp(orc, rng.random_smooth_filter(R), R, 16, 32)
+    H = rng.random_field(n, n, True)
+    T = rng.random_rotation_field(n, n)
+    r = X.xcorr_fast(H, X.XformField.rotation(T), pfilter(F), X.XConvPlan(components=[2]))
+    assert r.standard_ops == 1
+    F2 = orc.render_component(F, F.index_of(2), 2 * R + 1, 2 * R + 1, R, R)
+    ref = orc.filter2_fft(H, F2, R, R, True) * np.exp(2j * T)
+    assert orc.rel_l2(r.output, ref) < TOL
+
+
+def test_periodic_matches_oracle_and_is_equivariant(orc):  # test_engine2d.cpp:196-219
+    rng = orc.Rng(58)
+    n, R = 16, 4
+    F = full_decomp(orc, rng.random_smooth_filter(R), R, 12, 32)
+    H = rng.random_field(n, n, True)
+    T = rng.random_rotation_field(n, n)
+    plan = X.XConvPlan(periodic=True)
+    base = X.xcorr_fast(H, X.XformField.rotation(T), pfilter(F), plan).output
+    assert orc.rel_l2(base, orc.xcorr_fast(H, ROT, T, F, periodic=True)[0]) < TOL
+    sh = X.xcorr_fast(np.roll(H, (3, 5), (0, 1)), X.XformField.rotation(np.roll(T, (3, 5), (0, 1))),
+                      pfilter(F), plan).output
+    assert np.max(np.abs(np.roll(base, (3, 5), (0, 1)) - sh)) < 1e-5 * np.max(np.abs(base))
+    conv = X.xconv_fast(H, X.XformField.rotation(T), pfilter(F), plan).output
+    assert orc.rel_l2(conv, orc.xconv_fast(H, ROT, T, F, periodic=True)[0]) < TOL
+
+
+def test_op_count_and_validation(orc):  # test_engine2d.cpp:221-235, 285-299
+    rng = orc.Rng(59)
+    n, R = 12, 4
+    filt = rng.random_smooth_filter(R)
+    H = rng.random_field(n, n, True)
+    T = X.XformField.rotation(rng.random_rotation_field(n, n))
+    for K in (0, 2, 4, 8):
+        F = X.decompose_rotation2(filt, R, R, K, 12, 32, R)
+        assert X.xcorr_fast(H, T, F).standard_ops == 2 * (K // 2) + 1
+        assert X.xconv_fast(H, T, F).standard_ops == 2 * (K // 2) + 1
+    F = X.decompose_rotation2(filt, R, R, 8, 12, 32, R)
+    with pytest.raises(ValueError, match="signal and transformation field dims differ"):
+        X.xcorr_fast(H, X.XformField.rotation(np.zeros((8, 8))), F)
+    with pytest.raises(ValueError, match="transformation/filter group mismatch"):
+        X.xcorr_fast(H, X.XformField.scaling(np.ones((n, n))), F)
+    with pytest.raises(ValueError, match="plan retains a component the filter lacks"):
+        X.xcorr_fast(H, T, F, X.XConvPlan(components=[99]))
+
+
+def test_scale_guard_band_names_pixel(orc):  # test_engine_scale.cpp:161-178
+    rng = orc.Rng(76)
+    n, R = 8, 5
+    F = orc.decompose_scale2(rng.annular_filter(R), R, R, 4, 48, 32, 1.0, R)
+    H = rng.random_field(n, n, True)
+    s = np.ones((n, n))
+    s[3, 5] = 10.0
+    with pytest.raises(ValueError) as ei:
+        X.xcorr_fast(H, X.XformField.scaling(s), pfilter(F))
+    msg = str(ei.value)
+    with pytest.raises(ValueError) as eo:
+        orc.xcorr_fast(H, SCALE, s, F)
+    assert "guard band" in msg and "(5,3)" in msg and msg == str(eo.value)
+
+
+def test_real_in_real_out(orc):  # test_engine2d.cpp:237-248
+    rng = orc.Rng(60)
+    n, R = 18, 5
+    F = pfilter(full_decomp(orc, rng.random_smooth_filter(R), R, 16, 32))
+    H = rng.random_field(n, n, False)
+    T = X.XformField.rotation(rng.random_rotation_field(n, n))
+    for fn in (X.xcorr_fast, X.xconv_fast):
+        out = fn(H, T, F).output
+        assert np.max(np.abs(out.imag)) < 1e-6 * np.max(np.abs(out))
+
+
+# ------------------------------------------------------------------ smooth
+
+def test_smooth_matches_oracle(orc):  # test_smooth.cpp:108-137
+    rng = orc.Rng(91)
+    n, R = 32, 6
+    y, x = np.mgrid[-R:R + 1, -R:R + 1]
+    g = np.exp(-(x * x + y * y) / (2 * 1.8 ** 2))
+    g[x * x + y * y > R * R] = 0
+    F = orc.decompose_scale2(g, R, R, 62, 64, 16, 0.5, R, R + 3.0)
+    H = np.full((n, n), 0.7)
+    S = rng.random_scale_field(n, n)
+    out = X.smooth_adaptive(H, X.XformField.scaling(S), pfilter(F))
+    assert np.max(np.abs(out.output - 0.7)) < 1e-5
+    assert out.standard_ops == 2 * F.n_components()
+    Hs = orc.gaussian_blur(rng.random_field(n, n, False).real, 2.0)
+    ref, ops, cl = orc.smooth_adaptive(Hs, SCALE, S, F)
+    got = X.smooth_adaptive(Hs, X.XformField.scaling(S), pfilter(F))
+    assert orc.rel_l2(got.output, ref) < TOL and got.clamped_pixels == cl
+    bad = X.smooth_adaptive(Hs, X.XformField.scaling(S), pfilter(F), normalize_signal=False)
+    ref_bad = orc.smooth_adaptive(Hs, SCALE, S, F, False)[0]
+    assert orc.rel_l2(bad.output, ref_bad) < TOL
+
+
+def test_smooth_zero_integral_rejected(orc):  # test_smooth.cpp:174-187
+    R = 5
+    y, x = np.mgrid[-R:R + 1, -R:R + 1]
+    f = x * np.exp(-(x * x + y * y) / 8.0)
+    F = X.decompose_rotation2(f, R, R, 8, 2 * R, 32, R)
+    with pytest.raises(ValueError, match="normalization undefined: filter has zero integral"):
+        X.smooth_adaptive(np.ones((16, 16)), X.XformField.rotation(np.zeros((16, 16))), F)
+
+
+# ------------------------------------------------------- BASELINE configs
+
+def _cfg_parity(orc, w, n_check_pix=0):
+    """GPU vs oracle on one (reduced-size) config image."""
+    OF = ofilter(orc, w.filt)
+    H = w.signal[0].astype(np.float64)
+    if w.mode in ("xcorr", "xconv"):
+        fn = X.xcorr_fast if w.mode == "xcorr" else X.xconv_fast
+        got = fn(w.signal[0], xfield(w.kind, w.param[0]), w.filt).output
+        ofn = orc.xcorr_fast if w.mode == "xcorr" else orc.xconv_fast
+        ref = ofn(H, w.kind, w.param[0].astype(np.float64), OF)[0]
+        return orc.rel_l2(got, ref)
+    if w.mode == "smooth":
+        got = X.smooth_adaptive(w.signal[0], xfield(w.kind, w.param[0]), w.filt).output
+        ref = orc.smooth_adaptive(H, w.kind, w.param[0].astype(np.float64), OF)[0]
+        return orc.rel_l2(got, ref)
+    raise AssertionError(w.mode)
+
+
+def test_config1_full_size(orc):
+    from paper_2006_13188_b200 import workloads as WL
+    assert _cfg_parity(orc, WL.config1()) < TOL
+
+
+def test_config2_reduced(orc):
+    from paper_2006_13188_b200 import workloads as WL
+    assert _cfg_parity(orc, WL.config2(n=192)) < TOL
+
+
+def test_config4_reduced(orc):
+    from paper_2006_13188_b200 import workloads as WL
+    assert _cfg_parity(orc, WL.config4(n=160)) < TOL
+
+
+def test_config5_reduced(orc):
+    from paper_2006_13188_b200 import workloads as WL
+    assert _cfg_parity(orc, WL.config5(n=160, batch=1)) < TOL
+
+
+def test_config3_reduced_anglemax_and_peaks(orc):
+    from paper_2006_13188_b200 import workloads as WL
+    w = WL.config3(n=320, n_templates=2)
+    OF = ofilter(orc, w.filt)
+    score, arg = X.anglemax(w.signal[0], w.filt, 360)
+    # oracle: per-band G_k via single-component xcorr_fast with zero angle
+    H = w.signal[0].astype(np.float64)
+    zero = np.zeros_like(H)
+    G = np.stack([orc.xcorr_fast(H, ROT, zero, OF, components=[int(k)])[0] for k in OF.ks])
+    oscore, oarg = orc.anglemax(G, OF.ks, 360)
+    assert orc.rel_l2(score, oscore) < TOL
+    # argmax: the oracle's value at the GPU's angle attains the oracle max
+    s = np.arange(360)
+    at = np.abs(np.einsum("kyx,kyx->yx", G,
+                          np.exp(-2j * np.pi * np.asarray(OF.ks)[:, None, None] * arg[None] / 360)))
+    assert np.all(at >= oscore * (1 - 1e-5) - 1e-9)
+    pk = X.find_peaks(score.astype(np.float64), 32.0, 0.5)
+    opk = orc.find_peaks(oscore, 32.0, 0.5)
+    assert [(p.x, p.y) for p in pk[:2]] == [(p[0], p[1]) for p in opk[:2]]
+    for (cx, cy, _), p in zip(sorted(w.meta["truth"]), sorted(pk[:2], key=lambda q: q.x)):
+        assert abs(p.x - cx) <= 2 and abs(p.y - cy) <= 2
+
+
+@pytest.mark.parametrize("cfg,mode", [(1, 0), (5, 0), (2, 1)])
+def test_full_size_sampled_pixels(orc, cfg, mode):
+    """Full BASELINE sizes (one image): GPU vs the spectral oracle at sampled pixels
+    (the spectral oracle equals the FFT path to 1e-8, test_engine2d.cpp:140-153)."""
+    from paper_2006_13188_b200 import workloads as WL
+    w = {1: WL.config1, 2: WL.config2, 5: lambda: WL.config5(batch=1)}[cfg]()
+    fn = X.xcorr_fast if mode == 0 else X.xconv_fast
+    got = fn(w.signal[0], X.XformField.rotation(w.param[0]), w.filt).output
+    r = np.random.default_rng(7)
+    h, wd = got.shape
+    ys = np.concatenate([r.integers(0, h, 48), [0, h - 1, 0, h - 1]])
+    xs = np.concatenate([r.integers(0, wd, 48), [0, 0, wd - 1, wd - 1]])
+    ref = orc.spectral_oracle_at(mode, w.signal[0], ROT, w.param[0], ofilter(orc, w.filt), ys, xs)
+    assert orc.rel_l2(got[ys, xs], ref) < TOL
+
+
+# ---------------------------------------------------------- dtypes & layout
+
+def test_dtypes_batch_and_colmajor(orc):
+    rng = orc.Rng(100)
+    n, R = 40, 6
+    F = full_decomp(orc, rng.random_smooth_filter(R), R)
+    PF = pfilter(F)
+    H = np.stack([rng.random_field(n, n + 3, True) for _ in range(3)])
+    T = np.stack([rng.random_rotation_field(n + 3, n) for _ in range(3)])
+    got = X.xcorr_fast(H, X.XformField.rotation(T), PF).output  # complex128 batch
+    for b in range(3):
+        ref = orc.xcorr_fast(H[b], ROT, T[b], F)[0]
+        assert orc.rel_l2(got[b], ref) < TOL
+    got32 = X.xcorr_fast(H.astype(np.complex64), X.XformField.rotation(T.astype(np.float32)), PF)
+    assert got32.output.dtype == np.complex64
+    assert orc.rel_l2(got32.output[1], got[1]) < TOL
+    # column-major (Eigen) storage through the C ABI, as the C++ shim passes it
+    import ctypes as C
+    from paper_2006_13188_b200 import _native as N
+    Hc = np.asfortranarray(H[0])
+    Tc = np.asfortranarray(T[0])
+    out = np.zeros((n, n + 3), np.complex128, order="F")
+    d = N.ImageDesc(n, n + 3, 1, N.XC_C128, N.XC_F64, N.XC_C128, N.XC_COL_MAJOR, N.XC_HOST, 0,
+                    N.XC_ROTATION2)
+    ctx = N.context()
+    st = N.Stats()
+    N.check(N.lib().xc_run(ctx.handle, PF.handle(), 0, C.byref(d), Hc.ctypes.data, Tc.ctypes.data,
+                           None, 0, 0, out.ctypes.data, C.byref(st)), ctx.handle)
+    assert orc.rel_l2(out, orc.xcorr_fast(H[0], ROT, T[0], F)[0]) < TOL
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (1, 9), (7, 1), (3, 5), (13, 2)])
+def test_tiny_and_ragged_images(orc, shape):
+    rng = orc.Rng(101)
+    R = 6
+    F = full_decomp(orc, rng.random_smooth_filter(R), R)
+    h, w = shape
+    H = rng.random_field(w, h, True)
+    T = rng.random_rotation_field(w, h)
+    for mode, fn, ofn in ((0, X.xcorr_fast, orc.xcorr_fast), (1, X.xconv_fast, orc.xconv_fast)):
+        got = fn(H, X.XformField.rotation(T), pfilter(F)).output
+        assert orc.rel_l2(got, ofn(H, ROT, T, F)[0]) < TOL
+        gotp = fn(H, X.XformField.rotation(T), pfilter(F), X.XConvPlan(periodic=True)).output
+        assert orc.rel_l2(gotp, ofn(H, ROT, T, F, periodic=True)[0]) < TOL
