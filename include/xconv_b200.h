@@ -107,6 +107,14 @@ int xc_context_set_stream(xc_context ctx, void* cuda_stream);
 /* Release cached device scratch (filter spectra stay with their filters). */
 int xc_context_trim(xc_context ctx);
 
+/* Per-stage device-time profile (CUDA events on the launch stream around each
+ * pipeline stage; reference: StageTimer, engine.hpp:41-49).  xc_profile_get
+ * returns the number of stages recorded and fills entry idx if it exists. */
+int xc_profile_enable(xc_context ctx, int on);
+int xc_profile_reset(xc_context ctx);
+int xc_profile_get(xc_context ctx, int idx, char* name, int name_len, double* total_ms,
+                   long long* launches);
+
 /* ---- filters (FreqFilter2) -------------------------------------------- */
 /* Filters are host objects (ctx may be NULL); device spectra are built on first
  * use per (device, pad size, layout) and freed by xc_filter_destroy.  Errors of

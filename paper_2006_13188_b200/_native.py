@@ -42,7 +42,7 @@ EXPORTS = [
     "xc_context_set_stream", "xc_context_trim", "xc_filter_create", "xc_filter_destroy",
     "xc_filter_num_components", "xc_decompose_rotation2", "xc_decompose_scale2",
     "xc_render_component", "xc_reconstruct", "xc_inner_dc_value", "xc_run", "xc_smooth",
-    "xc_anglemax", "xc_find_peaks",
+    "xc_anglemax", "xc_find_peaks", "xc_profile_enable", "xc_profile_reset", "xc_profile_get",
 ]
 
 _lib = None
@@ -88,6 +88,9 @@ def lib():
         L.xc_anglemax.argtypes = [vp, vp, C.POINTER(ImageDesc), vp, ip, i, i, vp, ip,
                                   C.POINTER(Stats)]
         L.xc_find_peaks.argtypes = [vp, i, i, i, i, d, d, ip, ip, dp, i, ip]
+        L.xc_profile_enable.argtypes = [vp, i]
+        L.xc_profile_reset.argtypes = [vp]
+        L.xc_profile_get.argtypes = [vp, i, C.c_char_p, i, dp, C.POINTER(C.c_longlong)]
         _lib = L
         return L
 
@@ -113,6 +116,23 @@ class Context:
 
     def set_stream(self, stream_ptr: int | None):
         check(lib().xc_context_set_stream(self.handle, C.c_void_p(stream_ptr or 0)), self.handle)
+
+    def profile(self, enable: bool | None = None, reset: bool = False) -> dict:
+        """Per-stage device time {stage: (total_ms, launches)}."""
+        L = lib()
+        if enable is not None:
+            check(L.xc_profile_enable(self.handle, int(enable)), self.handle)
+        out = {}
+        cnt = L.xc_profile_get(self.handle, -1, None, 0, None, None)
+        for i in range(max(cnt, 0)):
+            name = C.create_string_buffer(64)
+            ms = C.c_double()
+            n = C.c_longlong()
+            L.xc_profile_get(self.handle, i, name, 64, C.byref(ms), C.byref(n))
+            out[name.value.decode()] = (ms.value, n.value)
+        if reset:
+            check(L.xc_profile_reset(self.handle), self.handle)
+        return out
 
     def trim(self):
         check(lib().xc_context_trim(self.handle), self.handle)

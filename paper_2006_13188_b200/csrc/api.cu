@@ -59,6 +59,16 @@ struct DevBuf {
   size_t n = 0;
 };
 
+struct StageEvents {
+  const char* name;
+  cudaEvent_t a, b;
+};
+
+struct StageTotal {
+  double ms = 0;
+  long long launches = 0;
+};
+
 }  // namespace
 
 struct xc_context_s {
@@ -69,6 +79,28 @@ struct xc_context_s {
   std::mutex mu;
   std::map<int, PlanEntry> plans;
   std::map<std::string, DevBuf> bufs;
+  // per-stage CUDA-event profile (xc_profile_*): events are recorded on the
+  // launch stream around each stage and resolved at the call's sync points
+  bool profiling = false;
+  std::vector<StageEvents> pending;
+  std::vector<std::pair<std::string, StageTotal>> prof;
+
+  void resolve_profile() {
+    for (auto& e : pending) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e.a, e.b);
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
+      auto it = std::find_if(prof.begin(), prof.end(),
+                             [&](const std::pair<std::string, StageTotal>& p) {
+                               return p.first == e.name;
+                             });
+      if (it == prof.end()) it = prof.insert(prof.end(), {e.name, StageTotal{}});
+      it->second.ms += ms;
+      it->second.launches += 1;
+    }
+    pending.clear();
+  }
 
   ~xc_context_s() {
     cudaSetDevice(device);
@@ -281,6 +313,22 @@ Call setup(xc_context ctx, xc_filter f, const xc_image_desc* d, int group_requir
   return c;
 }
 
+// Wrap one stage's launches in profiling events (no-op unless enabled).
+template <class Fn>
+void stage(Call& c, const char* name, Fn&& fn) {
+  if (!c.ctx->profiling) {
+    fn();
+    return;
+  }
+  StageEvents e{name, nullptr, nullptr};
+  ck(cudaEventCreate(&e.a), "event");
+  ck(cudaEventCreate(&e.b), "event");
+  ck(cudaEventRecord(e.a, c.st), "event");
+  fn();
+  ck(cudaEventRecord(e.b, c.st), "event");
+  c.ctx->pending.push_back(e);
+}
+
 double event_seconds(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0;
   cudaEventElapsedTime(&ms, a, b);
@@ -346,8 +394,10 @@ void prep(Call& c, const Staged& s, bool want_wgt, double** base_out, float** wg
   unsigned long long* bad = c.ctx->buf<unsigned long long>("bad", 2);
   const double lo = scale ? hf.r_min / hf.domain_top() : 0, hi = scale ? hf.domain_top() / hf.r_min : 0;
   if (scale) ck(cudaMemsetAsync(bad, 0xff, 2 * sizeof(unsigned long long), c.st), "memset");
-  xcb::launch_prep(s.param, s.param_f64, hf.group, scale ? hf.omega() : 0.0, lo, hi, c.rows,
-                   c.cols, c.transposed, base, wgt, bad, c.st, c.lc);
+  stage(c, "prep", [&] {
+    xcb::launch_prep(s.param, s.param_f64, hf.group, scale ? hf.omega() : 0.0, lo, hi, c.rows,
+                     c.cols, c.transposed, base, wgt, bad, c.st, c.lc);
+  });
   if (scale) {
     unsigned long long hbad[2];
     ck(cudaMemcpyAsync(hbad, bad, sizeof(hbad), cudaMemcpyDeviceToHost, c.st), "guard readback");
@@ -384,12 +434,16 @@ void run_gather(Call& c, const xcb::SigSrc& sig, const double* base, void* out, 
   float2* T1 = c.ctx->buf<float2>("T1", size_t(g.Hx2) * g.Pw);
   float2* Hh = c.ctx->buf<float2>("Hhat", size_t(g.Ph) * g.Pw);
   float2* T2 = c.ctx->buf<float2>("T2", size_t(c.bands.n) * g.H2 * g.Pw);
-  xcb::launch_rows_fwd(*c.prow, g, sig, T1, c.st, c.lc);
-  xcb::launch_cols_fwd(*c.pcol, g, T1, Hh, c.st, c.lc);
-  xcb::launch_cols_inv_corr(*c.pcol, g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);
+  stage(c, "F1_rows_fwd", [&] { xcb::launch_rows_fwd(*c.prow, g, sig, T1, c.st, c.lc); });
+  stage(c, "F2_cols_fwd", [&] { xcb::launch_cols_fwd(*c.pcol, g, T1, Hh, c.st, c.lc); });
+  stage(c, "I1_cols_inv_corr", [&] {
+    xcb::launch_cols_inv_corr(*c.pcol, g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);
+  });
   const cplx dcv = dc ? std::conj(xcb::inner_dc_value(c.f->hf)) : cplx(0);  // engine.hpp:323
-  xcb::launch_rows_inv_steer(*c.prow, g, T2, c.bands, base, out_kind, out, accumulate ? 1 : 0,
-                             sig, dcv.real(), dcv.imag(), c.st, c.lc);
+  stage(c, "I2_rows_inv_steer", [&] {
+    xcb::launch_rows_inv_steer(*c.prow, g, T2, c.bands, base, out_kind, out, accumulate ? 1 : 0,
+                               sig, dcv.real(), dcv.imag(), c.st, c.lc);
+  });
 }
 
 void run_scatter(Call& c, const xcb::SigSrc& sig, const double* base, void* out, int out_kind,
@@ -398,11 +452,17 @@ void run_scatter(Call& c, const xcb::SigSrc& sig, const double* base, void* out,
   float2* T1 = c.ctx->buf<float2>("T1b", size_t(c.bands.n) * g.Hx2 * g.Pw);
   float2* Sg = c.ctx->buf<float2>("Sigma", size_t(g.Ph) * g.Pw);
   float2* T2 = c.ctx->buf<float2>("T2s", size_t(g.H2) * g.Pw);
-  xcb::launch_rows_fwd_premul(*c.prow, g, sig, base, c.bands, T1, c.st, c.lc);
-  xcb::launch_cols_fwd_mac_inv(*c.pcol, g, T1, c.Fhat, c.sstride, c.bands, Sg, T2, c.st, c.lc);
+  stage(c, "S1_rows_fwd_premul", [&] {
+    xcb::launch_rows_fwd_premul(*c.prow, g, sig, base, c.bands, T1, c.st, c.lc);
+  });
+  stage(c, "S2_cols_fwd_mac_inv", [&] {
+    xcb::launch_cols_fwd_mac_inv(*c.pcol, g, T1, c.Fhat, c.sstride, c.bands, Sg, T2, c.st, c.lc);
+  });
   const cplx dcv = dc ? xcb::inner_dc_value(c.f->hf) : cplx(0);  // engine.hpp:370
-  xcb::launch_rows_inv_out(*c.prow, g, T2, out_kind, out, accumulate ? 1 : 0, sig, dcv.real(),
-                           dcv.imag(), c.st, c.lc);
+  stage(c, "S4_rows_inv_out", [&] {
+    xcb::launch_rows_inv_out(*c.prow, g, T2, out_kind, out, accumulate ? 1 : 0, sig, dcv.real(),
+                             dcv.imag(), c.st, c.lc);
+  });
 }
 
 void fill_stats(Call& c, xc_stats* st, double gpu_s, double total_s, long long ops) {
@@ -458,6 +518,36 @@ int xc_context_trim(xc_context ctx) {
     for (auto& kv : ctx->bufs) cudaFree(kv.second.p);
     ctx->bufs.clear();
   });
+}
+
+int xc_profile_enable(xc_context ctx, int on) {
+  return guarded(ctx, [&] {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->profiling = on != 0;
+  });
+}
+
+int xc_profile_reset(xc_context ctx) {
+  return guarded(ctx, [&] {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->prof.clear();
+  });
+}
+
+int xc_profile_get(xc_context ctx, int idx, char* name, int name_len, double* total_ms,
+                   long long* launches) {
+  if (!ctx) return -1;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  const int n = int(ctx->prof.size());
+  if (idx < 0 || idx >= n) return n;
+  const auto& p = ctx->prof[idx];
+  if (name && name_len > 0) {
+    std::strncpy(name, p.first.c_str(), size_t(name_len) - 1);
+    name[name_len - 1] = 0;
+  }
+  if (total_ms) *total_ms = p.second.ms;
+  if (launches) *launches = p.second.launches;
+  return n;
 }
 
 int xc_filter_create(xc_context ctx, int group, int K, const int* ks, int nc,
@@ -595,6 +685,7 @@ int xc_run(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d, const 
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    ctx->resolve_profile();
     fill_stats(c, stats, gpu_s,
                std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count(),
                (long long)c.ks.size());
@@ -655,8 +746,10 @@ int xc_smooth(xc_context ctx, xc_filter f, const xc_image_desc* d, const void* s
       ck(cudaMemsetAsync(red, 0, 2 * sizeof(unsigned), c.st), "memset");
       void* dout = d->memory == XC_DEVICE ? static_cast<char*>(out) + size_t(img) * npix * os
                                            : ctx->buf<char>("out_stage", npix * os);
-      xcb::launch_smooth_finish(num, den, npix, d->out_dtype == XC_F64, dout, red, red + 1, c.st,
-                                c.lc);
+      stage(c, "smooth_finish", [&] {
+        xcb::launch_smooth_finish(num, den, npix, d->out_dtype == XC_F64, dout, red, red + 1,
+                                  c.st, c.lc);
+      });
       ck(cudaGetLastError(), "kernel launch");
       ck(cudaEventRecord(e1, c.st), "event");
       unsigned hred[2];
@@ -674,6 +767,7 @@ int xc_smooth(xc_context ctx, xc_filter f, const xc_image_desc* d, const void* s
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    ctx->resolve_profile();
     fill_stats(c, stats, gpu_s,
                std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count(),
                2LL * (long long)c.ks.size());  // engine.hpp:406 num + den
@@ -709,18 +803,23 @@ int xc_anglemax(xc_context ctx, xc_filter f, const xc_image_desc* d, const void*
     for (int img = 0; img < d->batch; ++img) {
       Staged s = stage_inputs(c, signal, nullptr, img);
       ck(cudaEventRecord(e0, c.st), "event");
-      xcb::launch_rows_fwd(*c.prow, c.g, s.sig, T1, c.st, c.lc);
-      xcb::launch_cols_fwd(*c.pcol, c.g, T1, Hh, c.st, c.lc);
-      xcb::launch_cols_inv_corr(*c.pcol, c.g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);
-      xcb::launch_rows_inv_planes(*c.prow, c.g, T2, c.bands.n, planes, c.st, c.lc);
+      stage(c, "F1_rows_fwd", [&] { xcb::launch_rows_fwd(*c.prow, c.g, s.sig, T1, c.st, c.lc); });
+      stage(c, "F2_cols_fwd", [&] { xcb::launch_cols_fwd(*c.pcol, c.g, T1, Hh, c.st, c.lc); });
+      stage(c, "I1_cols_inv_corr", [&] {
+        xcb::launch_cols_inv_corr(*c.pcol, c.g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);
+      });
+      stage(c, "I2_rows_inv_planes",
+            [&] { xcb::launch_rows_inv_planes(*c.prow, c.g, T2, c.bands.n, planes, c.st, c.lc); });
       char* dsc = d->memory == XC_DEVICE ? static_cast<char*>(score) + size_t(img) * npix * os
                                          : ctx->buf<char>("score_stage", npix * os);
       int* darg = nullptr;
       if (argmax)
         darg = d->memory == XC_DEVICE ? argmax + size_t(img) * npix
                                       : ctx->buf<int>("arg_stage", npix);
-      xcb::launch_anglemax(planes, c.ks.data(), c.bands.n, npix, n_angles,
-                           d->out_dtype == XC_F64, dsc, darg, c.st, c.lc);
+      stage(c, "anglemax", [&] {
+        xcb::launch_anglemax(planes, c.ks.data(), c.bands.n, npix, n_angles,
+                             d->out_dtype == XC_F64, dsc, darg, c.st, c.lc);
+      });
       ck(cudaGetLastError(), "kernel launch");
       ck(cudaEventRecord(e1, c.st), "event");
       ck(cudaEventSynchronize(e1), "anglemax");
@@ -739,6 +838,7 @@ int xc_anglemax(xc_context ctx, xc_filter f, const xc_image_desc* d, const void*
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    ctx->resolve_profile();
     fill_stats(c, stats, gpu_s,
                std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count(),
                (long long)c.ks.size());

@@ -269,7 +269,7 @@ def test_dtypes_batch_and_colmajor(orc):
     F = full_decomp(orc, rng.random_smooth_filter(R), R)
     PF = pfilter(F)
     H = np.stack([rng.random_field(n, n + 3, True) for _ in range(3)])
-    T = np.stack([rng.random_rotation_field(n + 3, n) for _ in range(3)])
+    T = np.stack([rng.random_rotation_field(n, n + 3) for _ in range(3)])
     got = X.xcorr_fast(H, X.XformField.rotation(T), PF).output  # complex128 batch
     for b in range(3):
         ref = orc.xcorr_fast(H[b], ROT, T[b], F)[0]
@@ -282,8 +282,8 @@ def test_dtypes_batch_and_colmajor(orc):
     from paper_2006_13188_b200 import _native as N
     Hc = np.asfortranarray(H[0])
     Tc = np.asfortranarray(T[0])
-    out = np.zeros((n, n + 3), np.complex128, order="F")
-    d = N.ImageDesc(n, n + 3, 1, N.XC_C128, N.XC_F64, N.XC_C128, N.XC_COL_MAJOR, N.XC_HOST, 0,
+    out = np.zeros((n + 3, n), np.complex128, order="F")
+    d = N.ImageDesc(n + 3, n, 1, N.XC_C128, N.XC_F64, N.XC_C128, N.XC_COL_MAJOR, N.XC_HOST, 0,
                     N.XC_ROTATION2)
     ctx = N.context()
     st = N.Stats()
