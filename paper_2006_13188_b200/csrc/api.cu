@@ -78,6 +78,7 @@ struct xc_context_s {
   std::string err;
   std::mutex mu;
   std::map<int, PlanEntry> plans;
+  std::map<int, PlanEntry> fast_plans;  // L -> in-place radix-16-last plan (or tw == null)
   std::map<std::string, DevBuf> bufs;
   // per-stage CUDA-event profile (xc_profile_*): events are recorded on the
   // launch stream around each stage and resolved at the call's sync points
@@ -105,6 +106,7 @@ struct xc_context_s {
   ~xc_context_s() {
     cudaSetDevice(device);
     for (auto& kv : plans) cudaFree(kv.second.tw);
+    for (auto& kv : fast_plans) cudaFree(kv.second.tw);
     for (auto& kv : bufs) cudaFree(kv.second.p);
     if (own) cudaStreamDestroy(own);
   }
@@ -118,6 +120,21 @@ struct xc_context_s {
     if (!e.tw) throw CudaError("twiddle upload failed", XC_ENOMEM);
     e.plan.d.tw = e.tw;
     return plans.emplace(L, std::move(e)).first->second.plan;
+  }
+
+  // nullptr if L has no fast plan
+  const xcb::FftPlan* fast_plan(int L) {
+    auto it = fast_plans.find(L);
+    if (it == fast_plans.end()) {
+      PlanEntry e;
+      if (xcb::make_fast_plan(L, &e.plan)) {
+        e.tw = xcb::upload_twiddles(e.plan);
+        if (!e.tw) throw CudaError("twiddle upload failed", XC_ENOMEM);
+        e.plan.d.tw = e.tw;
+      }
+      it = fast_plans.emplace(L, std::move(e)).first;
+    }
+    return it->second.tw ? &it->second.plan : nullptr;
   }
 
   template <class T>
@@ -215,6 +232,8 @@ struct Call {
   xcb::Geo g;
   const xcb::FftPlan* prow;
   const xcb::FftPlan* pcol;
+  const xcb::FftPlan* frow;  // fast plans (nullptr: generic kernels)
+  const xcb::FftPlan* fcol;
   std::vector<int> ks;     // selected band frequencies
   std::vector<int> sidx;   // spectrum index of each
   xcb::Bands bands;
@@ -263,6 +282,21 @@ float2* filter_spectra(Call& c) {
   return spec;
 }
 
+// Pad (transform length) for an extent needing >= n points: any length >= n
+// gives the same zero-padded linear filtering (fft.hpp:85-86 uses
+// next_fast_size(extent + 2R + 1)); prefer a length with a fast plan (k_fast.cu)
+// when it costs at most 15% over the smallest 2/3/5-smooth length.
+int pick_pad(int n) {
+  const int L0 = xcb::pick_fft_length(n);
+  if (L0 < 0) return L0;
+  for (int s = n; s <= L0 + L0 / 7; ++s) {
+    if (s % 2 || !xcb::is_smooth235(s)) continue;
+    xcb::FftPlan p;
+    if (xcb::make_fast_plan(s, &p)) return s;
+  }
+  return L0;
+}
+
 Call setup(xc_context ctx, xc_filter f, const xc_image_desc* d, int group_required,
            const int* components, int ncomp, bool periodic) {
   if (!ctx || !f || !d) throw std::invalid_argument("null argument");
@@ -293,14 +327,19 @@ Call setup(xc_context ctx, xc_filter f, const xc_image_desc* d, int group_requir
   g.off = periodic ? R : 0;
   // zero-padded linear filtering needs P >= extent + R and no wrap of the
   // 2R+1 taps (fft.hpp:85-86 uses next_fast_size(extent + 2R + 1))
-  g.Ph = xcb::pick_fft_length(std::max(g.Hx + R, 2 * R + 1));
-  g.Pw = xcb::pick_fft_length(std::max(g.Wx + R, 2 * R + 1));
+  g.Ph = pick_pad(std::max(g.Hx + R, 2 * R + 1));
+  g.Pw = pick_pad(std::max(g.Wx + R, 2 * R + 1));
   if (g.Ph < 0 || g.Pw < 0) throw std::invalid_argument("image too large for the FFT planner");
-  if (g.Pw % 2) g.Pw = xcb::pick_fft_length(g.Pw + 1);
   while (g.Pw % 2) g.Pw = xcb::pick_fft_length(g.Pw + 1);
   c.prow = &ctx->plan(g.Pw);
   c.pcol = &ctx->plan(g.Ph);
-  c.ks = plan_components(f->hf, components, ncomp);
+  c.frow = ctx->fast_plan(g.Pw);
+  c.fcol = ctx->fast_plan(g.Ph);
+  // bands in descending k: the fast kernels steer with Horner's rule (the
+  // reference sums in ascending order; only the rounding order differs)
+  std::vector<int> ks = plan_components(f->hf, components, ncomp);
+  std::stable_sort(ks.begin(), ks.end(), [](int a, int b) { return a > b; });
+  c.ks = ks;
   for (int k : c.ks) c.sidx.push_back(f->hf.index_of(k));
   c.Fhat = filter_spectra(c);
   c.sstride = size_t(g.Ph) * g.Pw;
@@ -436,14 +475,27 @@ void run_gather(Call& c, const xcb::SigSrc& sig, const double* base, void* out, 
   float2* T2 = c.ctx->buf<float2>("T2", size_t(c.bands.n) * g.H2 * g.Pw);
   stage(c, "F1_rows_fwd", [&] { xcb::launch_rows_fwd(*c.prow, g, sig, T1, c.st, c.lc); });
   stage(c, "F2_cols_fwd", [&] { xcb::launch_cols_fwd(*c.pcol, g, T1, Hh, c.st, c.lc); });
-  stage(c, "I1_cols_inv_corr", [&] {
-    xcb::launch_cols_inv_corr(*c.pcol, g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);
-  });
+  if (c.fcol && xcb::fast_smem(0, *c.fcol, g)) {
+    stage(c, "I1_cols_inv_corr", [&] {
+      xcb::launch_cols_inv_corr_fast(*c.fcol, g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);
+    });
+  } else {
+    stage(c, "I1_cols_inv_corr", [&] {
+      xcb::launch_cols_inv_corr(*c.pcol, g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);
+    });
+  }
   const cplx dcv = dc ? std::conj(xcb::inner_dc_value(c.f->hf)) : cplx(0);  // engine.hpp:323
-  stage(c, "I2_rows_inv_steer", [&] {
-    xcb::launch_rows_inv_steer(*c.prow, g, T2, c.bands, base, out_kind, out, accumulate ? 1 : 0,
-                               sig, dcv.real(), dcv.imag(), c.st, c.lc);
-  });
+  if (c.frow && xcb::fast_smem(1, *c.frow, g)) {
+    stage(c, "I2_rows_inv_steer", [&] {
+      xcb::launch_rows_inv_steer_fast(*c.frow, g, T2, c.bands, base, out_kind, out,
+                                      accumulate ? 1 : 0, sig, dcv.real(), dcv.imag(), c.st, c.lc);
+    });
+  } else {
+    stage(c, "I2_rows_inv_steer", [&] {
+      xcb::launch_rows_inv_steer(*c.prow, g, T2, c.bands, base, out_kind, out,
+                                 accumulate ? 1 : 0, sig, dcv.real(), dcv.imag(), c.st, c.lc);
+    });
+  }
 }
 
 void run_scatter(Call& c, const xcb::SigSrc& sig, const double* base, void* out, int out_kind,
@@ -452,12 +504,26 @@ void run_scatter(Call& c, const xcb::SigSrc& sig, const double* base, void* out,
   float2* T1 = c.ctx->buf<float2>("T1b", size_t(c.bands.n) * g.Hx2 * g.Pw);
   float2* Sg = c.ctx->buf<float2>("Sigma", size_t(g.Ph) * g.Pw);
   float2* T2 = c.ctx->buf<float2>("T2s", size_t(g.H2) * g.Pw);
-  stage(c, "S1_rows_fwd_premul", [&] {
-    xcb::launch_rows_fwd_premul(*c.prow, g, sig, base, c.bands, T1, c.st, c.lc);
-  });
-  stage(c, "S2_cols_fwd_mac_inv", [&] {
-    xcb::launch_cols_fwd_mac_inv(*c.pcol, g, T1, c.Fhat, c.sstride, c.bands, Sg, T2, c.st, c.lc);
-  });
+  if (c.frow && xcb::fast_smem(2, *c.frow, g)) {
+    stage(c, "S1_rows_fwd_premul", [&] {
+      xcb::launch_rows_fwd_premul_fast(*c.frow, g, sig, base, c.bands, T1, c.st, c.lc);
+    });
+  } else {
+    stage(c, "S1_rows_fwd_premul", [&] {
+      xcb::launch_rows_fwd_premul(*c.prow, g, sig, base, c.bands, T1, c.st, c.lc);
+    });
+  }
+  if (c.fcol && xcb::fast_smem(3, *c.fcol, g)) {
+    stage(c, "S2_cols_fwd_mac_inv", [&] {
+      xcb::launch_cols_fwd_mac_inv_fast(*c.fcol, g, T1, c.Fhat, c.sstride, c.bands, T2, c.st,
+                                        c.lc);
+    });
+  } else {
+    stage(c, "S2_cols_fwd_mac_inv", [&] {
+      xcb::launch_cols_fwd_mac_inv(*c.pcol, g, T1, c.Fhat, c.sstride, c.bands, Sg, T2, c.st,
+                                   c.lc);
+    });
+  }
   const cplx dcv = dc ? xcb::inner_dc_value(c.f->hf) : cplx(0);  // engine.hpp:370
   stage(c, "S4_rows_inv_out", [&] {
     xcb::launch_rows_inv_out(*c.prow, g, T2, out_kind, out, accumulate ? 1 : 0, sig, dcv.real(),

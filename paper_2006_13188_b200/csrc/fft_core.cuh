@@ -220,15 +220,38 @@ __device__ __forceinline__ void pass_first(const FftPlanD& p, float2* dst, Load&
   }
 }
 
+__host__ __device__ constexpr int tw_split(int R) {  // smallest A with A*A >= R
+  int a = 1;
+  while (a * a < R) ++a;
+  return a;
+}
+
+// Reads the butterfly's R inputs and applies W_{Ns R}^{jm r}, r = A a + b:
+// only W^{jm b} (b < A) and W^{jm A a} are loaded from the exact table and
+// W^{jm r} = W^{jm A a} W^{jm b} (one rounding), which keeps ~2 sqrt(R)
+// twiddles live instead of R - 1.
 template <int R>
 __device__ __forceinline__ void load_twiddled(const FftPlanD& p, int q, const float2* src,
                                               int j, int jm, float2* v) {
+  constexpr int A = tw_split(R);
+  constexpr int NA = (R + A - 1) / A;
   const int nb = p.L / R, Ns = p.ns[q];
 #pragma unroll
   for (int r = 0; r < R; ++r) v[r] = src[sm_phys(j + r * nb)];
-  const float2* tw = p.tw + p.tw_off[q] + jm;
+  const float2* tw = p.tw + p.tw_off[q] + jm;  // entry (r-1)*Ns: W^{jm r}
+  float2 lo[A], hi[NA];
+  lo[0] = make_float2(1.f, 0.f);
+  hi[0] = make_float2(1.f, 0.f);
 #pragma unroll
-  for (int r = 1; r < R; ++r) v[r] = c_mul(v[r], __ldg(tw + (r - 1) * Ns));
+  for (int b = 1; b < A; ++b) lo[b] = __ldg(tw + (b - 1) * Ns);
+#pragma unroll
+  for (int a = 1; a < NA; ++a) hi[a] = __ldg(tw + (A * a - 1) * Ns);
+#pragma unroll
+  for (int r = 1; r < R; ++r) {
+    const int a = r / A, b = r % A;
+    const float2 t = a == 0 ? lo[b] : b == 0 ? hi[a] : c_mul(hi[a], lo[b]);
+    v[r] = c_mul(v[r], t);
+  }
 }
 
 template <int R>
@@ -307,6 +330,71 @@ __device__ __forceinline__ void fft_block(const FftPlanD& p, float2* sm, Load& l
   const int ql = p.npass - 1;
   radix_dispatch(p.radix[ql],
                  [&](auto rc) { pass_last<decltype(rc)::value>(p, ql, buf[cur], store); });
+}
+
+}  // namespace xcb
+
+namespace xcb {
+
+// ------------------------------------------------------------------ fast path
+// Single in-place buffer W ([g][phys(n)], kG * Lp float2):
+//   fast_first : load functor -> W            (loops over butterflies)
+//   fast_mid   : W -> W in place               (one butterfly per thread, staged
+//                                              through registers between barriers)
+//   fast_last<RL>: W -> store(k, g, r, value)  (radix RL, one butterfly per
+//                                              thread: the (thread, r) -> k map is
+//                                              the same on every call, so callers
+//                                              accumulate across bands in registers)
+// Plans come from make_fast_plan(L): radix[npass-1] == RL in {16, 20},
+// npass >= 2, nt <= 512 and >= every non-first pass's butterfly count.
+
+template <int R>
+__device__ __forceinline__ void pass_mid_ip(const FftPlanD& p, int q, float2* buf) {
+  const int nb = p.L / R, Ns = p.ns[q];
+  const int w = threadIdx.x;
+  const bool act = w < nb * kG;
+  float2 v[R];
+  int g = 0, j = 0, jm = 0;
+  if (act) {
+    g = w & (kG - 1);
+    j = w >> 1;
+    jm = j - Ns * int(__umulhi(unsigned(j), p.magic[q]));
+    load_twiddled<R>(p, q, buf + g * p.Lp, j, jm, v);
+    Dft<R>::run(v);
+  }
+  __syncthreads();
+  if (act) {
+    float2* d = buf + g * p.Lp;
+    const int base = (j - jm) * R + jm;
+#pragma unroll
+    for (int r = 0; r < R; ++r) d[sm_phys(base + r * Ns)] = v[Dft<R>::pos(r)];
+  }
+  __syncthreads();
+}
+
+template <class Load>
+__device__ __forceinline__ void fast_first(const FftPlanD& p, float2* W, Load& load) {
+  radix_dispatch(p.radix[0], [&](auto rc) { pass_first<decltype(rc)::value>(p, W, load); });
+}
+
+__device__ __forceinline__ void fast_mid(const FftPlanD& p, float2* W) {
+  for (int q = 1; q < p.npass - 1; ++q)
+    radix_dispatch(p.radix[q], [&](auto rc) { pass_mid_ip<decltype(rc)::value>(p, q, W); });
+}
+
+template <int RL, class Store>
+__device__ __forceinline__ void fast_last(const FftPlanD& p, const float2* W, Store& store) {
+  const int q = p.npass - 1;
+  const int nb = p.L / RL;
+  const int w = threadIdx.x;
+  if (w < nb * kG) {
+    const int g = w & (kG - 1), j = w >> 1;
+    float2 v[RL];
+    load_twiddled<RL>(p, q, W + g * p.Lp, j, j, v);
+    Dft<RL>::run(v);
+#pragma unroll
+    for (int r = 0; r < RL; ++r) store(j + r * nb, g, r, v[Dft<RL>::pos(r)]);
+  }
 }
 
 }  // namespace xcb

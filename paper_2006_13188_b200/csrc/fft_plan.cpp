@@ -14,6 +14,42 @@ const int kRadices[] = {20, 18, 16, 15, 12, 10, 9, 8, 6, 5, 4, 3, 2};
 int phys(int n) { return n + (n >> 4); }
 }  // namespace
 
+namespace {
+bool finalize_plan(int L, const std::vector<int>& order, int nt, bool fast, FftPlan* out) {
+  FftPlan p;
+  p.fast = fast;
+  p.d.L = L;
+  // stride per sequence: physical length, congruent to 8 (mod 16) float2 so
+  // the two interleaved sequences fall on opposite halves of the banks
+  int lp = phys(std::max(L - 1, 0)) + 1;
+  while (lp % 16 != 8) ++lp;
+  p.d.Lp = lp;
+  p.d.npass = L == 1 ? 0 : int(order.size());
+  p.d.nt = nt;
+  int ns = 1;
+  for (int q = 0; q < p.d.npass; ++q) {
+    const int R = order[q];
+    p.d.radix[q] = R;
+    p.d.ns[q] = ns;
+    p.d.magic[q] = ns > 1 ? unsigned((0x100000000ull + ns - 1) / ns) : 0u;
+    p.d.tw_off[q] = int(p.tw_host.size());
+    if (q > 0) {
+      for (int r = 1; r < R; ++r)
+        for (int jm = 0; jm < ns; ++jm) {
+          const long long e = (long long)jm * r % ((long long)ns * R);
+          const double a = -2.0 * M_PI * double(e) / double((long long)ns * R);
+          p.tw_host.push_back(make_float2(float(std::cos(a)), float(std::sin(a))));
+        }
+    }
+    ns *= R;
+  }
+  if (p.tw_host.empty()) p.tw_host.push_back(make_float2(1.f, 0.f));
+  p.d.tw = nullptr;
+  *out = std::move(p);
+  return true;
+}
+}  // namespace
+
 bool is_smooth235(int n) {
   if (n < 1) return false;
   for (int f : {2, 3, 5})
@@ -68,36 +104,33 @@ bool make_fft_plan(int L, FftPlan* out) {
     best_nt = std::min(kMaxThreads, std::max(32, (items + 31) / 32 * 32));
   }
   if (best < 0) return false;
-  FftPlan p;
-  p.d.L = L;
-  // stride per sequence: physical length, congruent to 8 (mod 16) float2 so
-  // the two interleaved sequences fall on opposite halves of the banks
-  int lp = phys(std::max(L - 1, 0)) + 1;
-  while (lp % 16 != 8) ++lp;
-  p.d.Lp = lp;
-  p.d.npass = L == 1 ? 0 : best_np;
-  p.d.nt = best_nt;
-  int ns = 1;
-  for (int q = 0; q < p.d.npass; ++q) {
-    const int R = best_order[q];
-    p.d.radix[q] = R;
-    p.d.ns[q] = ns;
-    p.d.magic[q] = ns > 1 ? unsigned((0x100000000ull + ns - 1) / ns) : 0u;
-    p.d.tw_off[q] = int(p.tw_host.size());
-    if (q > 0) {
-      for (int r = 1; r < R; ++r)
-        for (int jm = 0; jm < ns; ++jm) {
-          const long long e = (long long)jm * r % ((long long)ns * R);
-          const double a = -2.0 * M_PI * double(e) / double((long long)ns * R);
-          p.tw_host.push_back(make_float2(float(std::cos(a)), float(std::sin(a))));
-        }
+  return finalize_plan(L, best_order, best_nt, false, out);
+}
+
+bool make_fast_plan(int L, FftPlan* out) {
+  if (L < 32 || !is_smooth235(L)) return false;
+  int best_nt = 1 << 30;
+  std::vector<int> best;
+  for (int RL : {16, 20}) {
+    if (L % RL || L / RL < 2) continue;
+    // factor L/RL with the generic planner, then append the RL last pass
+    FftPlan rest;
+    if (!make_fft_plan(L / RL, &rest)) continue;
+    std::vector<int> order;
+    for (int q = 0; q < rest.d.npass; ++q) order.push_back(rest.d.radix[q]);
+    std::sort(order.begin(), order.end());  // smallest first: it loops, the rest stage
+    order.push_back(RL);
+    int need = kG * L / RL;
+    for (size_t q = 1; q < order.size(); ++q) need = std::max(need, kG * L / order[q]);
+    const int nt = std::max(64, (need + 31) / 32 * 32);
+    if (nt > kFastMaxThreads) continue;
+    if (nt < best_nt || (nt == best_nt && RL == 16)) {
+      best_nt = nt;
+      best = order;
     }
-    ns *= R;
   }
-  if (p.tw_host.empty()) p.tw_host.push_back(make_float2(1.f, 0.f));
-  p.d.tw = nullptr;
-  *out = std::move(p);
-  return true;
+  if (best.empty()) return false;
+  return finalize_plan(L, best, best_nt, true, out);
 }
 
 int pick_fft_length(int n) {

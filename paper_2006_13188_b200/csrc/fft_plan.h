@@ -32,13 +32,19 @@ struct FftPlanD {
 struct FftPlan {
   FftPlanD d{};
   std::vector<float2> tw_host;
-  size_t smem_bytes() const { return 2 * size_t(kG) * d.Lp * sizeof(float2); }
+  bool fast = false;
+  size_t smem_bytes() const { return (fast ? 1 : 2) * size_t(kG) * d.Lp * sizeof(float2); }
 };
 
 bool is_smooth235(int n);
 // Builds a plan for length L (2/3/5-smooth); false if no factorization fits
 // the codelet set and thread budget.
 bool make_fft_plan(int L, FftPlan* out);
+// Plan for the in-place fast path (fft_core.cuh fast_*): last radix 16 or 20,
+// >= 2 passes, one butterfly per thread after the first pass, <= 512 threads
+// (so ptxas may give each thread 128 registers for the band accumulators).
+bool make_fast_plan(int L, FftPlan* out);
+constexpr int kFastMaxThreads = 512;
 // Smallest plannable 2/3/5-smooth length >= n (the pad size rule).
 int pick_fft_length(int n);
 

@@ -1,0 +1,361 @@
+// Fast band-loop stages for transform lengths whose plan ends in a radix-16 or
+// radix-20 pass (make_fast_plan; template parameter RL): one CTA per SM with
+//   * the next band's input block prefetched by TMA (cp.async.bulk + mbarrier)
+//     into a staging buffer while the current band's FFT passes run,
+//   * an in-place FFT buffer (fast_first / fast_mid / fast_last<RL>),
+//   * per-band results accumulated in registers across the band loop (the
+//     radix-RL last pass maps (thread, r) to the same output every band).
+// Steering uses Horner's rule over the bands sorted by descending k:
+//   sum_k z^k G_k = z^{k_min} * (((G_{k0} z^{k0-k1} + G_{k1}) z^{k1-k2} + ...)
+// so each band costs one complex FMA per pixel instead of a sincos
+// (z = e^{i phi(p)}; engine.hpp:312-317 / 353-358 for the reference steering).
+#include "stages_common.cuh"
+#include "tma.cuh"
+
+namespace xcb {
+namespace {
+
+__device__ __forceinline__ float2 cpow_step(float2 a, float2 z, int d) {
+  if (d < 0) {
+    z = c_conj(z);
+    d = -d;
+  }
+  for (int t = 0; t < d; ++t) a = c_mul(a, z);
+  return a;
+}
+
+// ------------------------------------------------------------------ I1 fast
+template <int RL>
+__global__ void __launch_bounds__(kFastMaxThreads, 1)
+    k_cols_inv_corr_fast(FftPlanD p, Geo g, const float2* __restrict__ Hh,
+                         const float2* __restrict__ Fh, size_t sstride, Bands bl,
+                         float2* __restrict__ T2) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ __align__(8) uint64_t bar;
+  const int L = p.L;  // = Ph
+  float2* Hc = reinterpret_cast<float2*>(smraw);
+  float2* S = Hc + 2 * L;
+  float2* W = S + 2 * L;
+  const int c = blockIdx.x, tid = threadIdx.x;
+  const size_t colb = size_t(c) * L * 2;
+  const unsigned bytes = unsigned(L) * 2u * unsigned(sizeof(float2));
+  const size_t plane = size_t(g.H2) * g.Pw;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(&bar, 2 * bytes);
+    bulk_copy(Hc, Hh + colb, bytes, &bar);
+    bulk_copy(S, Fh + size_t(bl.spec[0]) * sstride + colb, bytes, &bar);
+  }
+  __syncthreads();
+  unsigned phase = 0;
+  for (int bi = 0; bi < bl.n; ++bi) {
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    // conj(H^ conj(F^)) = conj(H^) F^ : inverse via conj-FFT-conj
+    auto load = [&](int n, int gi) -> float2 {
+      const int i = n * 2 + gi;
+      return c_mul(c_conj(Hc[i]), S[i]);
+    };
+    fast_first(p, W, load);
+    __syncthreads();
+    if (tid == 0 && bi + 1 < bl.n) {
+      fence_proxy_async();
+      mbar_expect_tx(&bar, bytes);
+      bulk_copy(S, Fh + size_t(bl.spec[bi + 1]) * sstride + colb, bytes, &bar);
+    }
+    fast_mid(p, W);
+    float2* out = T2 + size_t(bi) * plane;
+    auto store = [&](int k, int gi, int, float2 v) {
+      const int y = k - g.off;
+      if (y >= 0 && y < g.H)
+        out[(size_t(y >> 1) * g.Pw + 2 * c + gi) * 2 + (y & 1)] = c_conj(v);
+    };
+    fast_last<RL>(p, W, store);
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ I2 fast
+template <int RL, class TO>
+__global__ void __launch_bounds__(kFastMaxThreads, 1)
+    k_rows_inv_steer_fast(FftPlanD p, Geo g, const float2* __restrict__ T2, Bands bl,
+                          const double* __restrict__ base, TO* __restrict__ out,
+                          int accumulate, SigSrc dcs, double dcr, double dci, float scale) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ __align__(8) uint64_t bar;
+  const int L = p.L;  // = Pw
+  const int zs = g.W + ((8 - (g.W % 16) + 16) % 16);  // Z row stride = 8 (mod 16)
+  float2* S = reinterpret_cast<float2*>(smraw);
+  float2* W = S + 2 * L;
+  float2* Z = W + 2 * p.Lp;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const unsigned bytes = unsigned(L) * 2u * unsigned(sizeof(float2));
+  const size_t plane = size_t(g.H2) * g.Pw;
+  const size_t rowb = size_t(b) * L * 2;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(&bar, bytes);
+    bulk_copy(S, T2 + rowb, bytes, &bar);
+  }
+  // z = e^{i phi} of the CTA's two output rows
+  for (int i = tid; i < 2 * g.W; i += blockDim.x) {
+    const int gi = i >= g.W, x = i - gi * g.W, y = 2 * b + gi;
+    Z[gi * zs + x] = y < g.H ? steer(1, base[size_t(y) * g.W + x], 1.f) : make_float2(1.f, 0.f);
+  }
+  __syncthreads();
+  float2 acc[RL];
+#pragma unroll
+  for (int r = 0; r < RL; ++r) acc[r] = make_float2(0.f, 0.f);
+  unsigned phase = 0;
+  for (int bi = 0; bi < bl.n; ++bi) {
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    auto load = [&](int n, int gi) -> float2 { return c_conj(S[n * 2 + gi]); };
+    fast_first(p, W, load);
+    __syncthreads();
+    if (tid == 0 && bi + 1 < bl.n) {
+      fence_proxy_async();
+      mbar_expect_tx(&bar, bytes);
+      bulk_copy(S, T2 + size_t(bi + 1) * plane + rowb, bytes, &bar);
+    }
+    fast_mid(p, W);
+    const int dk = bi == 0 ? 0 : bl.k[bi - 1] - bl.k[bi];
+    auto store = [&](int k, int gi, int r, float2 v) {
+      const float2 val = c_scale(c_conj(v), scale);
+      const int x = k - g.off;
+      const float2 z = (x >= 0 && x < g.W) ? Z[gi * zs + x] : make_float2(1.f, 0.f);
+      acc[r] = c_add(cpow_step(acc[r], z, dk), val);
+    };
+    fast_last<RL>(p, W, store);
+    __syncthreads();
+  }
+  // out = z^{k_last} * acc (+ conj(dc) H for the scale group)
+  const int nb = L / RL, w = tid;
+  if (w < nb * kG) {
+    const int gi = w & 1, j = w >> 1, y = 2 * b + gi;
+    const int klast = bl.k[bl.n - 1];
+#pragma unroll
+    for (int r = 0; r < RL; ++r) {
+      const int x = j + r * nb - g.off;
+      if (x < 0 || x >= g.W || y >= g.H) continue;
+      const size_t i = size_t(y) * g.W + x;
+      const float2 v = c_mul(acc[r], steer(klast, base[i], 1.f));
+      OutOps<TO>::put(out, i, v, accumulate != 0, dc_term(dcs, i, dcr, dci));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ S1 fast
+template <int RL>
+__global__ void __launch_bounds__(kFastMaxThreads, 1)
+    k_rows_fwd_premul_fast(FftPlanD p, Geo g, SigSrc s, const double* __restrict__ base,
+                           Bands bl, float2* __restrict__ T1) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int xs_ = g.Wx + ((8 - (g.Wx % 16) + 16) % 16);
+  float2* W = reinterpret_cast<float2*>(smraw);
+  float2* CUR = W + 2 * p.Lp;
+  float2* MUL = CUR + 2 * xs_;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const size_t plane = size_t(g.Hx2) * g.Pw;
+  const int k0 = bl.k[0];
+  for (int i = tid; i < 2 * g.Wx; i += blockDim.x) {
+    const int gi = i >= g.Wx, xp = i - gi * g.Wx;
+    const int ys = src_index(2 * b + gi, g.Hx, g.H, g.R, g.periodic);
+    const int xs = src_index(xp, g.Wx, g.W, g.R, g.periodic);
+    float2 cur = make_float2(0.f, 0.f), mul = make_float2(1.f, 0.f);
+    if (ys >= 0 && xs >= 0) {
+      const size_t idx = size_t(ys) * g.W + xs;
+      const double ph = base[idx];
+      cur = c_mul(sig_value(s, idx), steer(k0, ph, -1.f));  // H e^{-i k0 phi}
+      mul = steer(1, ph, -1.f);
+    }
+    CUR[gi * xs_ + xp] = cur;
+    MUL[gi * xs_ + xp] = mul;
+  }
+  __syncthreads();
+  for (int bi = 0; bi < bl.n; ++bi) {
+    auto load = [&](int n, int gi) -> float2 {
+      return n < g.Wx ? CUR[gi * xs_ + n] : make_float2(0.f, 0.f);
+    };
+    fast_first(p, W, load);
+    __syncthreads();
+    if (bi + 1 < bl.n) {  // advance H e^{-i k phi} to the next band
+      const int dk = bl.k[bi + 1] - bl.k[bi];
+      for (int i = tid; i < 2 * g.Wx; i += blockDim.x) {
+        const int gi = i >= g.Wx, xp = i - gi * g.Wx;
+        CUR[gi * xs_ + xp] = cpow_step(CUR[gi * xs_ + xp], MUL[gi * xs_ + xp], dk);
+      }
+    }
+    fast_mid(p, W);
+    float2* dst = T1 + size_t(bi) * plane;
+    auto store = [&](int k, int gi, int, float2 v) {
+      dst[(size_t(k >> 1) * g.Hx2 + 2 * b + gi) * 2 + (k & 1)] = v;
+    };
+    fast_last<RL>(p, W, store);
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ S2 fast
+template <int RL>
+__global__ void __launch_bounds__(kFastMaxThreads, 1)
+    k_cols_fwd_mac_inv_fast(FftPlanD p, Geo g, const float2* __restrict__ T1,
+                            const float2* __restrict__ Fh, size_t sstride, Bands bl,
+                            float2* __restrict__ T2) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ __align__(8) uint64_t barS, barF;
+  const int L = p.L;  // = Ph
+  const int sl = g.Hx2 > L ? g.Hx2 : L;
+  float2* S = reinterpret_cast<float2*>(smraw);
+  float2* SF = S + 2 * sl;
+  float2* W = SF + 2 * L;
+  const int c = blockIdx.x, tid = threadIdx.x;
+  const size_t plane1 = size_t(g.Hx2) * g.Pw;
+  const size_t col1 = size_t(c) * g.Hx2 * 2, colF = size_t(c) * L * 2;
+  const unsigned bytesS = unsigned(g.Hx2) * 2u * unsigned(sizeof(float2));
+  const unsigned bytesF = unsigned(L) * 2u * unsigned(sizeof(float2));
+  if (tid == 0) {
+    mbar_init(&barS, 1);
+    mbar_init(&barF, 1);
+    fence_mbar_init();
+    mbar_expect_tx(&barS, bytesS);
+    bulk_copy(S, T1 + col1, bytesS, &barS);
+    mbar_expect_tx(&barF, bytesF);
+    bulk_copy(SF, Fh + size_t(bl.spec[0]) * sstride + colF, bytesF, &barF);
+  }
+  __syncthreads();
+  float2 acc[RL];
+#pragma unroll
+  for (int r = 0; r < RL; ++r) acc[r] = make_float2(0.f, 0.f);
+  unsigned phS = 0, phF = 0;
+  for (int bi = 0; bi < bl.n; ++bi) {
+    mbar_wait(&barS, phS);
+    phS ^= 1;
+    auto load = [&](int n, int gi) -> float2 {
+      return n < g.Hx2 ? S[n * 2 + gi] : make_float2(0.f, 0.f);
+    };
+    fast_first(p, W, load);
+    __syncthreads();
+    if (tid == 0 && bi + 1 < bl.n) {
+      fence_proxy_async();
+      mbar_expect_tx(&barS, bytesS);
+      bulk_copy(S, T1 + size_t(bi + 1) * plane1 + col1, bytesS, &barS);
+    }
+    fast_mid(p, W);
+    mbar_wait(&barF, phF);
+    phF ^= 1;
+    auto store = [&](int k, int gi, int r, float2 v) {
+      acc[r] = c_add(acc[r], c_mul(v, SF[k * 2 + gi]));
+    };
+    fast_last<RL>(p, W, store);
+    __syncthreads();
+    if (tid == 0 && bi + 1 < bl.n) {
+      fence_proxy_async();
+      mbar_expect_tx(&barF, bytesF);
+      bulk_copy(SF, Fh + size_t(bl.spec[bi + 1]) * sstride + colF, bytesF, &barF);
+    }
+  }
+  // inverse column transform of the band sum: conj(acc) -> S -> FFT -> conj
+  {
+    const int nb = L / RL, w = tid;
+    if (w < nb * kG) {
+      const int gi = w & 1, j = w >> 1;
+#pragma unroll
+      for (int r = 0; r < RL; ++r) S[(j + r * nb) * 2 + gi] = c_conj(acc[r]);
+    }
+  }
+  __syncthreads();
+  auto load = [&](int n, int gi) -> float2 { return S[n * 2 + gi]; };
+  fast_first(p, W, load);
+  __syncthreads();
+  fast_mid(p, W);
+  auto store = [&](int k, int gi, int, float2 v) {
+    const int y = k - g.off;
+    if (y >= 0 && y < g.H) T2[(size_t(y >> 1) * g.Pw + 2 * c + gi) * 2 + (y & 1)] = c_conj(v);
+  };
+  fast_last<RL>(p, W, store);
+}
+
+constexpr size_t kSmemLimit = 232448;  // 227 KB opt-in per CTA on sm_100
+
+}  // namespace
+
+// smem needs of each fast kernel (0 if the stage has no fast variant)
+size_t fast_smem(int stage, const FftPlan& pl, const Geo& g) {
+  const size_t f2 = sizeof(float2), Wb = pl.smem_bytes();
+  const size_t L = pl.d.L;
+  size_t s = 0;
+  switch (stage) {
+    case 0: s = 4 * L * f2 + Wb; break;                                   // I1
+    case 1: s = 2 * L * f2 + Wb + 2 * (g.W + 16) * f2; break;            // I2
+    case 2: s = Wb + 4 * (g.Wx + 16) * f2; break;                         // S1
+    case 3: s = 2 * (g.Hx2 > int(L) ? g.Hx2 : L) * f2 + 2 * L * f2 + Wb; break;  // S2
+  }
+  return s <= kSmemLimit ? s : 0;
+}
+
+void launch_cols_inv_corr_fast(const FftPlan& pc, const Geo& g, const float2* Hhat,
+                               const float2* Fhat, size_t sstride, const Bands& b, float2* T2,
+                               cudaStream_t st, LaunchCounter& lc) {
+  const size_t sm = fast_smem(0, pc, g);
+  if (pc.d.radix[pc.d.npass - 1] == 20) {
+    set_smem(k_cols_inv_corr_fast<20>, sm);
+    k_cols_inv_corr_fast<20><<<g.Pw / 2, pc.d.nt, sm, st>>>(pc.d, g, Hhat, Fhat, sstride, b, T2);
+  } else {
+    set_smem(k_cols_inv_corr_fast<16>, sm);
+    k_cols_inv_corr_fast<16><<<g.Pw / 2, pc.d.nt, sm, st>>>(pc.d, g, Hhat, Fhat, sstride, b, T2);
+  }
+  ++lc.n;
+}
+
+void launch_rows_inv_steer_fast(const FftPlan& pr, const Geo& g, const float2* T2,
+                                const Bands& b, const double* base, int out_kind, void* out,
+                                int accumulate, const SigSrc& dcs, double dcr, double dci,
+                                cudaStream_t st, LaunchCounter& lc) {
+  const size_t sm = fast_smem(1, pr, g);
+  const float scale = float(1.0 / (double(g.Ph) * double(g.Pw)));
+  const bool r20 = pr.d.radix[pr.d.npass - 1] == 20;
+#define XCB_I2F(RLV, TO)                                                                 \
+  set_smem(k_rows_inv_steer_fast<RLV, TO>, sm);                                           \
+  k_rows_inv_steer_fast<RLV, TO><<<g.H2 / 2, pr.d.nt, sm, st>>>(                          \
+      pr.d, g, T2, b, base, static_cast<TO*>(out), accumulate, dcs, dcr, dci, scale)
+  if (out_kind == OUT_C64) {
+    if (r20) { XCB_I2F(20, float2); } else { XCB_I2F(16, float2); }
+  } else {
+    if (r20) { XCB_I2F(20, double2); } else { XCB_I2F(16, double2); }
+  }
+#undef XCB_I2F
+  ++lc.n;
+}
+
+void launch_rows_fwd_premul_fast(const FftPlan& pr, const Geo& g, const SigSrc& s,
+                                 const double* base, const Bands& b, float2* T1,
+                                 cudaStream_t st, LaunchCounter& lc) {
+  const size_t sm = fast_smem(2, pr, g);
+  if (pr.d.radix[pr.d.npass - 1] == 20) {
+    set_smem(k_rows_fwd_premul_fast<20>, sm);
+    k_rows_fwd_premul_fast<20><<<g.Hx2 / 2, pr.d.nt, sm, st>>>(pr.d, g, s, base, b, T1);
+  } else {
+    set_smem(k_rows_fwd_premul_fast<16>, sm);
+    k_rows_fwd_premul_fast<16><<<g.Hx2 / 2, pr.d.nt, sm, st>>>(pr.d, g, s, base, b, T1);
+  }
+  ++lc.n;
+}
+
+void launch_cols_fwd_mac_inv_fast(const FftPlan& pc, const Geo& g, const float2* T1,
+                                  const float2* Fhat, size_t sstride, const Bands& b,
+                                  float2* T2, cudaStream_t st, LaunchCounter& lc) {
+  const size_t sm = fast_smem(3, pc, g);
+  if (pc.d.radix[pc.d.npass - 1] == 20) {
+    set_smem(k_cols_fwd_mac_inv_fast<20>, sm);
+    k_cols_fwd_mac_inv_fast<20><<<g.Pw / 2, pc.d.nt, sm, st>>>(pc.d, g, T1, Fhat, sstride, b, T2);
+  } else {
+    set_smem(k_cols_fwd_mac_inv_fast<16>, sm);
+    k_cols_fwd_mac_inv_fast<16><<<g.Pw / 2, pc.d.nt, sm, st>>>(pc.d, g, T1, Fhat, sstride, b, T2);
+  }
+  ++lc.n;
+}
+
+}  // namespace xcb
