@@ -338,15 +338,14 @@ namespace xcb {
 
 // ------------------------------------------------------------------ fast path
 // Single in-place buffer W ([g][phys(n)], kG * Lp float2):
-//   fast_first : load functor -> W            (loops over butterflies)
-//   fast_mid   : W -> W in place               (one butterfly per thread, staged
-//                                              through registers between barriers)
-//   fast_last<RL>: W -> store(k, g, r, value)  (radix RL, one butterfly per
-//                                              thread: the (thread, r) -> k map is
-//                                              the same on every call, so callers
-//                                              accumulate across bands in registers)
-// Plans come from make_fast_plan(L): radix[npass-1] == RL in {16, 20},
-// npass >= 2, nt <= 512 and >= every non-first pass's butterfly count.
+//   first : load functor -> W            (loops over butterflies)
+//   mid   : W -> W in place               (one butterfly per thread, staged
+//                                         through registers between barriers)
+//   last  : W -> store(k, g, r, value)    (one butterfly per thread: the
+//                                         (thread, r) -> k map is the same on
+//                                         every call, so callers accumulate
+//                                         across bands in registers)
+// Plans come from make_fast_plan(L) (XCB_FAST_TABLE in fft_plan.h).
 
 template <int R>
 __device__ __forceinline__ void pass_mid_ip(const FftPlanD& p, int q, float2* buf) {
@@ -372,29 +371,32 @@ __device__ __forceinline__ void pass_mid_ip(const FftPlanD& p, int q, float2* bu
   __syncthreads();
 }
 
-template <class Load>
-__device__ __forceinline__ void fast_first(const FftPlanD& p, float2* W, Load& load) {
-  radix_dispatch(p.radix[0], [&](auto rc) { pass_first<decltype(rc)::value>(p, W, load); });
-}
-
-__device__ __forceinline__ void fast_mid(const FftPlanD& p, float2* W) {
-  for (int q = 1; q < p.npass - 1; ++q)
-    radix_dispatch(p.radix[q], [&](auto rc) { pass_mid_ip<decltype(rc)::value>(p, q, W); });
-}
-
-template <int RL, class Store>
-__device__ __forceinline__ void fast_last(const FftPlanD& p, const float2* W, Store& store) {
-  const int q = p.npass - 1;
-  const int nb = p.L / RL;
-  const int w = threadIdx.x;
-  if (w < nb * kG) {
-    const int g = w & (kG - 1), j = w >> 1;
-    float2 v[RL];
-    load_twiddled<RL>(p, q, W + g * p.Lp, j, j, v);
-    Dft<RL>::run(v);
-#pragma unroll
-    for (int r = 0; r < RL; ++r) store(j + r * nb, g, r, v[Dft<RL>::pos(r)]);
+// Compile-time fast plan: R0 first pass (loops), R1 middle pass (1 = none),
+// RL last pass; plan fields are read with constant pass indices.
+template <int R0, int R1, int RL>
+struct FastFft {
+  static constexpr int kLast = RL;
+  template <class Load>
+  __device__ __forceinline__ static void first(const FftPlanD& p, float2* W, Load& load) {
+    pass_first<R0>(p, W, load);
   }
-}
+  __device__ __forceinline__ static void mid(const FftPlanD& p, float2* W) {
+    if constexpr (R1 > 1) pass_mid_ip<R1>(p, 1, W);
+  }
+  template <class Store>
+  __device__ __forceinline__ static void last(const FftPlanD& p, const float2* W, Store& store) {
+    constexpr int Q = R1 > 1 ? 2 : 1;
+    const int nb = p.L / RL;
+    const int w = threadIdx.x;
+    if (w < nb * kG) {
+      const int g = w & (kG - 1), j = w >> 1;
+      float2 v[RL];
+      load_twiddled<RL>(p, Q, W + g * p.Lp, j, j, v);
+      Dft<RL>::run(v);
+#pragma unroll
+      for (int r = 0; r < RL; ++r) store(j + r * nb, g, r, v[Dft<RL>::pos(r)]);
+    }
+  }
+};
 
 }  // namespace xcb

@@ -108,29 +108,21 @@ bool make_fft_plan(int L, FftPlan* out) {
 }
 
 bool make_fast_plan(int L, FftPlan* out) {
-  if (L < 32 || !is_smooth235(L)) return false;
-  int best_nt = 1 << 30;
-  std::vector<int> best;
-  for (int RL : {16, 20}) {
-    if (L % RL || L / RL < 2) continue;
-    // factor L/RL with the generic planner, then append the RL last pass
-    FftPlan rest;
-    if (!make_fft_plan(L / RL, &rest)) continue;
-    std::vector<int> order;
-    for (int q = 0; q < rest.d.npass; ++q) order.push_back(rest.d.radix[q]);
-    std::sort(order.begin(), order.end());  // smallest first: it loops, the rest stage
-    order.push_back(RL);
-    int need = kG * L / RL;
-    for (size_t q = 1; q < order.size(); ++q) need = std::max(need, kG * L / order[q]);
-    const int nt = std::max(64, (need + 31) / 32 * 32);
-    if (nt > kFastMaxThreads) continue;
-    if (nt < best_nt || (nt == best_nt && RL == 16)) {
-      best_nt = nt;
-      best = order;
-    }
+  std::vector<int> order;
+#define XCB_FAST_ORDER(LL, R0, R1, RL)  \
+  if (L == LL) {                        \
+    order.push_back(R0);                \
+    if (R1 > 1) order.push_back(R1);    \
+    order.push_back(RL);                \
   }
-  if (best.empty()) return false;
-  return finalize_plan(L, best, best_nt, true, out);
+  XCB_FAST_TABLE(XCB_FAST_ORDER)
+#undef XCB_FAST_ORDER
+  if (order.empty()) return false;
+  int need = kG * L / order.back();
+  for (size_t q = 1; q < order.size(); ++q) need = std::max(need, kG * L / order[q]);
+  const int nt = std::max(64, (need + 31) / 32 * 32);
+  if (nt > kFastMaxThreads) return false;
+  return finalize_plan(L, order, nt, true, out);
 }
 
 int pick_fft_length(int n) {

@@ -40,9 +40,16 @@ bool is_smooth235(int n);
 // Builds a plan for length L (2/3/5-smooth); false if no factorization fits
 // the codelet set and thread budget.
 bool make_fft_plan(int L, FftPlan* out);
-// Plan for the in-place fast path (fft_core.cuh fast_*): last radix 16 or 20,
-// >= 2 passes, one butterfly per thread after the first pass, <= 512 threads
-// (so ptxas may give each thread 128 registers for the band accumulators).
+// Fast path (k_fast.cu): transform lengths with a compile-time plan
+// (R0 first pass, R1 middle pass or 1, RL last pass).  One kernel instance per
+// entry keeps each kernel to a single radix per pass, which is what lets the
+// band accumulators stay in registers.  Constraints: one butterfly per thread
+// after the first pass, <= 512 threads (128 registers per thread).
+#define XCB_FAST_TABLE(X)                                                              \
+  X(64, 4, 1, 16) X(128, 8, 1, 16) X(256, 16, 1, 16) X(288, 18, 1, 16)               \
+  X(512, 2, 16, 16) X(576, 4, 9, 16) X(1024, 4, 16, 16) X(1152, 8, 9, 16)            \
+  X(2048, 8, 16, 16) X(2160, 9, 15, 16) X(2304, 9, 16, 16) X(3456, 12, 18, 16)       \
+  X(4096, 16, 16, 16) X(4320, 12, 18, 20)
 bool make_fast_plan(int L, FftPlan* out);
 constexpr int kFastMaxThreads = 512;
 // Smallest plannable 2/3/5-smooth length >= n (the pad size rule).

@@ -1,8 +1,8 @@
-// Fast band-loop stages for transform lengths whose plan ends in a radix-16 or
-// radix-20 pass (make_fast_plan; template parameter RL): one CTA per SM with
+// Fast band-loop stages for the transform lengths of XCB_FAST_TABLE (one
+// compile-time FastFft<R0, R1, RL> instance per length): one CTA per SM with
 //   * the next band's input block prefetched by TMA (cp.async.bulk + mbarrier)
 //     into a staging buffer while the current band's FFT passes run,
-//   * an in-place FFT buffer (fast_first / fast_mid / fast_last<RL>),
+//   * an in-place FFT buffer (FastFft::first / mid / last),
 //   * per-band results accumulated in registers across the band loop (the
 //     radix-RL last pass maps (thread, r) to the same output every band).
 // Steering uses Horner's rule over the bands sorted by descending k:
@@ -15,6 +15,14 @@
 namespace xcb {
 namespace {
 
+// Returns v, but opaque to the optimizer: used inside the band loops so that
+// per-output address arithmetic is recomputed each band instead of being
+// hoisted out of the loop into (spilled) registers.
+__device__ __forceinline__ int opaque(int v) {
+  asm volatile("" : "+r"(v));
+  return v;
+}
+
 __device__ __forceinline__ float2 cpow_step(float2 a, float2 z, int d) {
   if (d < 0) {
     z = c_conj(z);
@@ -25,7 +33,7 @@ __device__ __forceinline__ float2 cpow_step(float2 a, float2 z, int d) {
 }
 
 // ------------------------------------------------------------------ I1 fast
-template <int RL>
+template <class FF>
 __global__ void __launch_bounds__(kFastMaxThreads, 1)
     k_cols_inv_corr_fast(FftPlanD p, Geo g, const float2* __restrict__ Hh,
                          const float2* __restrict__ Fh, size_t sstride, Bands bl,
@@ -57,27 +65,27 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
       const int i = n * 2 + gi;
       return c_mul(c_conj(Hc[i]), S[i]);
     };
-    fast_first(p, W, load);
+    FF::first(p, W, load);
     __syncthreads();
     if (tid == 0 && bi + 1 < bl.n) {
       fence_proxy_async();
       mbar_expect_tx(&bar, bytes);
       bulk_copy(S, Fh + size_t(bl.spec[bi + 1]) * sstride + colb, bytes, &bar);
     }
-    fast_mid(p, W);
+    FF::mid(p, W);
     float2* out = T2 + size_t(bi) * plane;
+    const int pw = opaque(g.Pw), off = opaque(g.off);
     auto store = [&](int k, int gi, int, float2 v) {
-      const int y = k - g.off;
-      if (y >= 0 && y < g.H)
-        out[(size_t(y >> 1) * g.Pw + 2 * c + gi) * 2 + (y & 1)] = c_conj(v);
+      const int y = k - off;
+      if (y >= 0 && y < g.H) out[(size_t(y >> 1) * pw + 2 * c + gi) * 2 + (y & 1)] = c_conj(v);
     };
-    fast_last<RL>(p, W, store);
+    FF::last(p, W, store);
     __syncthreads();
   }
 }
 
 // ------------------------------------------------------------------ I2 fast
-template <int RL, class TO>
+template <class FF, class TO>
 __global__ void __launch_bounds__(kFastMaxThreads, 1)
     k_rows_inv_steer_fast(FftPlanD p, Geo g, const float2* __restrict__ T2, Bands bl,
                           const double* __restrict__ base, TO* __restrict__ out,
@@ -105,6 +113,7 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
     Z[gi * zs + x] = y < g.H ? steer(1, base[size_t(y) * g.W + x], 1.f) : make_float2(1.f, 0.f);
   }
   __syncthreads();
+  constexpr int RL = FF::kLast;
   float2 acc[RL];
 #pragma unroll
   for (int r = 0; r < RL; ++r) acc[r] = make_float2(0.f, 0.f);
@@ -113,22 +122,23 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
     mbar_wait(&bar, phase);
     phase ^= 1;
     auto load = [&](int n, int gi) -> float2 { return c_conj(S[n * 2 + gi]); };
-    fast_first(p, W, load);
+    FF::first(p, W, load);
     __syncthreads();
     if (tid == 0 && bi + 1 < bl.n) {
       fence_proxy_async();
       mbar_expect_tx(&bar, bytes);
       bulk_copy(S, T2 + size_t(bi + 1) * plane + rowb, bytes, &bar);
     }
-    fast_mid(p, W);
+    FF::mid(p, W);
     const int dk = bi == 0 ? 0 : bl.k[bi - 1] - bl.k[bi];
+    const int zso = opaque(zs), off = opaque(g.off);
     auto store = [&](int k, int gi, int r, float2 v) {
       const float2 val = c_scale(c_conj(v), scale);
-      const int x = k - g.off;
-      const float2 z = (x >= 0 && x < g.W) ? Z[gi * zs + x] : make_float2(1.f, 0.f);
+      const int x = k - off;
+      const float2 z = (x >= 0 && x < g.W) ? Z[gi * zso + x] : make_float2(1.f, 0.f);
       acc[r] = c_add(cpow_step(acc[r], z, dk), val);
     };
-    fast_last<RL>(p, W, store);
+    FF::last(p, W, store);
     __syncthreads();
   }
   // out = z^{k_last} * acc (+ conj(dc) H for the scale group)
@@ -148,7 +158,7 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
 }
 
 // ------------------------------------------------------------------ S1 fast
-template <int RL>
+template <class FF>
 __global__ void __launch_bounds__(kFastMaxThreads, 1)
     k_rows_fwd_premul_fast(FftPlanD p, Geo g, SigSrc s, const double* __restrict__ base,
                            Bands bl, float2* __restrict__ T1) {
@@ -179,7 +189,7 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
     auto load = [&](int n, int gi) -> float2 {
       return n < g.Wx ? CUR[gi * xs_ + n] : make_float2(0.f, 0.f);
     };
-    fast_first(p, W, load);
+    FF::first(p, W, load);
     __syncthreads();
     if (bi + 1 < bl.n) {  // advance H e^{-i k phi} to the next band
       const int dk = bl.k[bi + 1] - bl.k[bi];
@@ -188,18 +198,19 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
         CUR[gi * xs_ + xp] = cpow_step(CUR[gi * xs_ + xp], MUL[gi * xs_ + xp], dk);
       }
     }
-    fast_mid(p, W);
+    FF::mid(p, W);
     float2* dst = T1 + size_t(bi) * plane;
+    const int hx2 = opaque(g.Hx2);
     auto store = [&](int k, int gi, int, float2 v) {
-      dst[(size_t(k >> 1) * g.Hx2 + 2 * b + gi) * 2 + (k & 1)] = v;
+      dst[(size_t(k >> 1) * hx2 + 2 * b + gi) * 2 + (k & 1)] = v;
     };
-    fast_last<RL>(p, W, store);
+    FF::last(p, W, store);
     __syncthreads();
   }
 }
 
 // ------------------------------------------------------------------ S2 fast
-template <int RL>
+template <class FF>
 __global__ void __launch_bounds__(kFastMaxThreads, 1)
     k_cols_fwd_mac_inv_fast(FftPlanD p, Geo g, const float2* __restrict__ T1,
                             const float2* __restrict__ Fh, size_t sstride, Bands bl,
@@ -226,6 +237,7 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
     bulk_copy(SF, Fh + size_t(bl.spec[0]) * sstride + colF, bytesF, &barF);
   }
   __syncthreads();
+  constexpr int RL = FF::kLast;
   float2 acc[RL];
 #pragma unroll
   for (int r = 0; r < RL; ++r) acc[r] = make_float2(0.f, 0.f);
@@ -236,20 +248,21 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
     auto load = [&](int n, int gi) -> float2 {
       return n < g.Hx2 ? S[n * 2 + gi] : make_float2(0.f, 0.f);
     };
-    fast_first(p, W, load);
+    FF::first(p, W, load);
     __syncthreads();
     if (tid == 0 && bi + 1 < bl.n) {
       fence_proxy_async();
       mbar_expect_tx(&barS, bytesS);
       bulk_copy(S, T1 + size_t(bi + 1) * plane1 + col1, bytesS, &barS);
     }
-    fast_mid(p, W);
+    FF::mid(p, W);
     mbar_wait(&barF, phF);
     phF ^= 1;
+    const int two = opaque(2);
     auto store = [&](int k, int gi, int r, float2 v) {
-      acc[r] = c_add(acc[r], c_mul(v, SF[k * 2 + gi]));
+      acc[r] = c_add(acc[r], c_mul(v, SF[k * two + gi]));
     };
-    fast_last<RL>(p, W, store);
+    FF::last(p, W, store);
     __syncthreads();
     if (tid == 0 && bi + 1 < bl.n) {
       fence_proxy_async();
@@ -268,14 +281,14 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
   }
   __syncthreads();
   auto load = [&](int n, int gi) -> float2 { return S[n * 2 + gi]; };
-  fast_first(p, W, load);
+  FF::first(p, W, load);
   __syncthreads();
-  fast_mid(p, W);
+  FF::mid(p, W);
   auto store = [&](int k, int gi, int, float2 v) {
     const int y = k - g.off;
     if (y >= 0 && y < g.H) T2[(size_t(y >> 1) * g.Pw + 2 * c + gi) * 2 + (y & 1)] = c_conj(v);
   };
-  fast_last<RL>(p, W, store);
+  FF::last(p, W, store);
 }
 
 constexpr size_t kSmemLimit = 232448;  // 227 KB opt-in per CTA on sm_100
@@ -296,17 +309,22 @@ size_t fast_smem(int stage, const FftPlan& pl, const Geo& g) {
   return s <= kSmemLimit ? s : 0;
 }
 
+#define XCB_FAST_CASE(LL, R0, R1, RL) \
+  case LL: {                          \
+    using FF = FastFft<R0, R1, RL>;   \
+    XCB_FAST_BODY;                    \
+    break;                            \
+  }
+
 void launch_cols_inv_corr_fast(const FftPlan& pc, const Geo& g, const float2* Hhat,
                                const float2* Fhat, size_t sstride, const Bands& b, float2* T2,
                                cudaStream_t st, LaunchCounter& lc) {
   const size_t sm = fast_smem(0, pc, g);
-  if (pc.d.radix[pc.d.npass - 1] == 20) {
-    set_smem(k_cols_inv_corr_fast<20>, sm);
-    k_cols_inv_corr_fast<20><<<g.Pw / 2, pc.d.nt, sm, st>>>(pc.d, g, Hhat, Fhat, sstride, b, T2);
-  } else {
-    set_smem(k_cols_inv_corr_fast<16>, sm);
-    k_cols_inv_corr_fast<16><<<g.Pw / 2, pc.d.nt, sm, st>>>(pc.d, g, Hhat, Fhat, sstride, b, T2);
-  }
+#define XCB_FAST_BODY                                                                      \
+  set_smem(k_cols_inv_corr_fast<FF>, sm);                                                  \
+  k_cols_inv_corr_fast<FF><<<g.Pw / 2, pc.d.nt, sm, st>>>(pc.d, g, Hhat, Fhat, sstride, b, T2)
+  switch (pc.d.L) { XCB_FAST_TABLE(XCB_FAST_CASE) }
+#undef XCB_FAST_BODY
   ++lc.n;
 }
 
@@ -316,17 +334,21 @@ void launch_rows_inv_steer_fast(const FftPlan& pr, const Geo& g, const float2* T
                                 cudaStream_t st, LaunchCounter& lc) {
   const size_t sm = fast_smem(1, pr, g);
   const float scale = float(1.0 / (double(g.Ph) * double(g.Pw)));
-  const bool r20 = pr.d.radix[pr.d.npass - 1] == 20;
-#define XCB_I2F(RLV, TO)                                                                 \
-  set_smem(k_rows_inv_steer_fast<RLV, TO>, sm);                                           \
-  k_rows_inv_steer_fast<RLV, TO><<<g.H2 / 2, pr.d.nt, sm, st>>>(                          \
-      pr.d, g, T2, b, base, static_cast<TO*>(out), accumulate, dcs, dcr, dci, scale)
   if (out_kind == OUT_C64) {
-    if (r20) { XCB_I2F(20, float2); } else { XCB_I2F(16, float2); }
+#define XCB_FAST_BODY                                                                      \
+  set_smem(k_rows_inv_steer_fast<FF, float2>, sm);                                         \
+  k_rows_inv_steer_fast<FF, float2><<<g.H2 / 2, pr.d.nt, sm, st>>>(                        \
+      pr.d, g, T2, b, base, static_cast<float2*>(out), accumulate, dcs, dcr, dci, scale)
+    switch (pr.d.L) { XCB_FAST_TABLE(XCB_FAST_CASE) }
+#undef XCB_FAST_BODY
   } else {
-    if (r20) { XCB_I2F(20, double2); } else { XCB_I2F(16, double2); }
+#define XCB_FAST_BODY                                                                      \
+  set_smem(k_rows_inv_steer_fast<FF, double2>, sm);                                        \
+  k_rows_inv_steer_fast<FF, double2><<<g.H2 / 2, pr.d.nt, sm, st>>>(                       \
+      pr.d, g, T2, b, base, static_cast<double2*>(out), accumulate, dcs, dcr, dci, scale)
+    switch (pr.d.L) { XCB_FAST_TABLE(XCB_FAST_CASE) }
+#undef XCB_FAST_BODY
   }
-#undef XCB_I2F
   ++lc.n;
 }
 
@@ -334,13 +356,11 @@ void launch_rows_fwd_premul_fast(const FftPlan& pr, const Geo& g, const SigSrc& 
                                  const double* base, const Bands& b, float2* T1,
                                  cudaStream_t st, LaunchCounter& lc) {
   const size_t sm = fast_smem(2, pr, g);
-  if (pr.d.radix[pr.d.npass - 1] == 20) {
-    set_smem(k_rows_fwd_premul_fast<20>, sm);
-    k_rows_fwd_premul_fast<20><<<g.Hx2 / 2, pr.d.nt, sm, st>>>(pr.d, g, s, base, b, T1);
-  } else {
-    set_smem(k_rows_fwd_premul_fast<16>, sm);
-    k_rows_fwd_premul_fast<16><<<g.Hx2 / 2, pr.d.nt, sm, st>>>(pr.d, g, s, base, b, T1);
-  }
+#define XCB_FAST_BODY                                                                      \
+  set_smem(k_rows_fwd_premul_fast<FF>, sm);                                                \
+  k_rows_fwd_premul_fast<FF><<<g.Hx2 / 2, pr.d.nt, sm, st>>>(pr.d, g, s, base, b, T1)
+  switch (pr.d.L) { XCB_FAST_TABLE(XCB_FAST_CASE) }
+#undef XCB_FAST_BODY
   ++lc.n;
 }
 
@@ -348,13 +368,11 @@ void launch_cols_fwd_mac_inv_fast(const FftPlan& pc, const Geo& g, const float2*
                                   const float2* Fhat, size_t sstride, const Bands& b,
                                   float2* T2, cudaStream_t st, LaunchCounter& lc) {
   const size_t sm = fast_smem(3, pc, g);
-  if (pc.d.radix[pc.d.npass - 1] == 20) {
-    set_smem(k_cols_fwd_mac_inv_fast<20>, sm);
-    k_cols_fwd_mac_inv_fast<20><<<g.Pw / 2, pc.d.nt, sm, st>>>(pc.d, g, T1, Fhat, sstride, b, T2);
-  } else {
-    set_smem(k_cols_fwd_mac_inv_fast<16>, sm);
-    k_cols_fwd_mac_inv_fast<16><<<g.Pw / 2, pc.d.nt, sm, st>>>(pc.d, g, T1, Fhat, sstride, b, T2);
-  }
+#define XCB_FAST_BODY                                                                      \
+  set_smem(k_cols_fwd_mac_inv_fast<FF>, sm);                                               \
+  k_cols_fwd_mac_inv_fast<FF><<<g.Pw / 2, pc.d.nt, sm, st>>>(pc.d, g, T1, Fhat, sstride, b, T2)
+  switch (pc.d.L) { XCB_FAST_TABLE(XCB_FAST_CASE) }
+#undef XCB_FAST_BODY
   ++lc.n;
 }
 
