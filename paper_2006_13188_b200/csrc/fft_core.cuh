@@ -371,27 +371,99 @@ __device__ __forceinline__ void pass_mid_ip(const FftPlanD& p, int q, float2* bu
   __syncthreads();
 }
 
-// Compile-time fast plan: R0 first pass (loops), R1 middle pass (1 = none),
-// RL last pass; plan fields are read with constant pass indices.
-template <int R0, int R1, int RL>
+__host__ __device__ constexpr int fast_lp(int L) {  // host finalize_plan's stride rule
+  int lp = (L - 1) + ((L - 1) >> 4) + 1;
+  while (lp % 16 != 8) ++lp;
+  return lp;
+}
+
+// Compile-time fast plan for length L = R0 * R1 * RL (R1 = 1: two passes):
+// every extent, stride, twiddle offset and j mod Ns divisor is a constant, so
+// the index arithmetic folds into immediates.  Only the twiddle table pointer
+// comes from the host plan (same table layout as finalize_plan).
+template <int L_, int R0, int R1, int RL>
 struct FastFft {
+  static constexpr int L = L_;
+  static constexpr int Lp = fast_lp(L_);
   static constexpr int kLast = RL;
+  static constexpr int NS1 = R0;                    // Ns of the middle pass
+  static constexpr int NSL = R1 > 1 ? R0 * R1 : R0;  // Ns of the last pass
+  static constexpr int TWL = R1 > 1 ? (R1 - 1) * R0 : 0;  // twiddle offset, last pass
+  static_assert(R0 * R1 * RL == L_, "bad fast plan");
+
+  template <int R, int NS, int TWO>
+  __device__ __forceinline__ static void load_tw(const float2* __restrict__ twt,
+                                                 const float2* src, int j, int jm,
+                                                 float2* v) {
+    constexpr int nb = L / R;
+    constexpr int A = tw_split(R);
+    constexpr int NA = (R + A - 1) / A;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = src[sm_phys(j + r * nb)];
+    const float2* tw = twt + TWO + jm;
+    float2 lo[A], hi[NA];
+    lo[0] = make_float2(1.f, 0.f);
+    hi[0] = make_float2(1.f, 0.f);
+#pragma unroll
+    for (int b = 1; b < A; ++b) lo[b] = __ldg(tw + (b - 1) * NS);
+#pragma unroll
+    for (int a = 1; a < NA; ++a) hi[a] = __ldg(tw + (A * a - 1) * NS);
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      const int a = r / A, b = r % A;
+      const float2 t = a == 0 ? lo[b] : b == 0 ? hi[a] : c_mul(hi[a], lo[b]);
+      v[r] = c_mul(v[r], t);
+    }
+  }
+
   template <class Load>
-  __device__ __forceinline__ static void first(const FftPlanD& p, float2* W, Load& load) {
-    pass_first<R0>(p, W, load);
+  __device__ __forceinline__ static void first(const FftPlanD&, float2* W, Load& load) {
+    constexpr int nb = L / R0;
+    for (int w = threadIdx.x; w < nb * kG; w += blockDim.x) {
+      const int g = w & 1, j = w >> 1;
+      float2 v[R0];
+#pragma unroll
+      for (int r = 0; r < R0; ++r) v[r] = load(j + r * nb, g);
+      Dft<R0>::run(v);
+      float2* d = W + g * Lp;
+#pragma unroll
+      for (int r = 0; r < R0; ++r) d[sm_phys(j * R0 + r)] = v[Dft<R0>::pos(r)];
+    }
   }
+
   __device__ __forceinline__ static void mid(const FftPlanD& p, float2* W) {
-    if constexpr (R1 > 1) pass_mid_ip<R1>(p, 1, W);
+    if constexpr (R1 > 1) {
+      constexpr int nb = L / R1;
+      const int w = threadIdx.x;
+      const bool act = w < nb * kG;
+      float2 v[R1];
+      int g = 0, j = 0, jm = 0;
+      if (act) {
+        g = w & 1;
+        j = w >> 1;
+        jm = j % NS1;
+        load_tw<R1, NS1, 0>(p.tw, W + g * Lp, j, jm, v);
+        Dft<R1>::run(v);
+      }
+      __syncthreads();
+      if (act) {
+        float2* d = W + g * Lp;
+        const int base = (j - jm) * R1 + jm;
+#pragma unroll
+        for (int r = 0; r < R1; ++r) d[sm_phys(base + r * NS1)] = v[Dft<R1>::pos(r)];
+      }
+      __syncthreads();
+    }
   }
+
   template <class Store>
   __device__ __forceinline__ static void last(const FftPlanD& p, const float2* W, Store& store) {
-    constexpr int Q = R1 > 1 ? 2 : 1;
-    const int nb = p.L / RL;
+    constexpr int nb = L / RL;
     const int w = threadIdx.x;
     if (w < nb * kG) {
-      const int g = w & (kG - 1), j = w >> 1;
+      const int g = w & 1, j = w >> 1;
       float2 v[RL];
-      load_twiddled<RL>(p, Q, W + g * p.Lp, j, j, v);
+      load_tw<RL, NSL, TWL>(p.tw, W + g * Lp, j, j, v);
       Dft<RL>::run(v);
 #pragma unroll
       for (int r = 0; r < RL; ++r) store(j + r * nb, g, r, v[Dft<RL>::pos(r)]);

@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
                          float2* __restrict__ T2) {
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) uint64_t bar;
-  const int L = p.L;  // = Ph
+  constexpr int L = FF::L;  // = Ph
   float2* Hc = reinterpret_cast<float2*>(smraw);
   float2* S = Hc + 2 * L;
   float2* W = S + 2 * L;
@@ -92,11 +92,11 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
                           int accumulate, SigSrc dcs, double dcr, double dci, float scale) {
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) uint64_t bar;
-  const int L = p.L;  // = Pw
+  constexpr int L = FF::L;  // = Pw
   const int zs = g.W + ((8 - (g.W % 16) + 16) % 16);  // Z row stride = 8 (mod 16)
   float2* S = reinterpret_cast<float2*>(smraw);
   float2* W = S + 2 * L;
-  float2* Z = W + 2 * p.Lp;
+  float2* Z = W + 2 * FF::Lp;
   const int b = blockIdx.x, tid = threadIdx.x;
   const unsigned bytes = unsigned(L) * 2u * unsigned(sizeof(float2));
   const size_t plane = size_t(g.H2) * g.Pw;
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
   extern __shared__ __align__(128) unsigned char smraw[];
   const int xs_ = g.Wx + ((8 - (g.Wx % 16) + 16) % 16);
   float2* W = reinterpret_cast<float2*>(smraw);
-  float2* CUR = W + 2 * p.Lp;
+  float2* CUR = W + 2 * FF::Lp;
   float2* MUL = CUR + 2 * xs_;
   const int b = blockIdx.x, tid = threadIdx.x;
   const size_t plane = size_t(g.Hx2) * g.Pw;
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
                             float2* __restrict__ T2) {
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) uint64_t barS, barF;
-  const int L = p.L;  // = Ph
+  constexpr int L = FF::L;  // = Ph
   const int sl = g.Hx2 > L ? g.Hx2 : L;
   float2* S = reinterpret_cast<float2*>(smraw);
   float2* SF = S + 2 * sl;
@@ -311,7 +311,7 @@ size_t fast_smem(int stage, const FftPlan& pl, const Geo& g) {
 
 #define XCB_FAST_CASE(LL, R0, R1, RL) \
   case LL: {                          \
-    using FF = FastFft<R0, R1, RL>;   \
+    using FF = FastFft<LL, R0, R1, RL>; \
     XCB_FAST_BODY;                    \
     break;                            \
   }
