@@ -75,6 +75,7 @@ struct xc_context_s {
   int device = 0;
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
+  cudaStream_t cp_in = nullptr, cp_out = nullptr;  // host-memory copy pipeline
   std::string err;
   std::mutex mu;
   std::map<int, PlanEntry> plans;
@@ -109,6 +110,8 @@ struct xc_context_s {
     for (auto& kv : fast_plans) cudaFree(kv.second.tw);
     for (auto& kv : bufs) cudaFree(kv.second.p);
     if (own) cudaStreamDestroy(own);
+    if (cp_in) cudaStreamDestroy(cp_in);
+    if (cp_out) cudaStreamDestroy(cp_out);
   }
 
   const xcb::FftPlan& plan(int L) {
@@ -381,43 +384,109 @@ struct Staged {
   int param_f64;
 };
 
-Staged stage_inputs(Call& c, const void* signal, const void* param, int img) {
-  const xc_image_desc& d = c.d;
-  const size_t npix = size_t(c.rows) * c.cols;
-  const size_t ss = dtype_size(d.signal_dtype), ps = dtype_size(d.param_dtype);
-  Staged s{};
-  const bool cplx_sig = d.signal_dtype == XC_C64 || d.signal_dtype == XC_C128;
-  const char* sig_src = static_cast<const char*>(signal) + size_t(img) * npix * ss;
-  const char* par_src = param ? static_cast<const char*>(param) +
-                                    (d.param_per_image ? size_t(img) * npix * ps : 0)
-                              : nullptr;
-  auto t0 = std::chrono::steady_clock::now();
-  const void* dsig = sig_src;
-  if (d.memory == XC_HOST) {
-    void* b = c.ctx->buf<char>("sig_raw", npix * ss);
-    ck(cudaMemcpyAsync(b, sig_src, npix * ss, cudaMemcpyHostToDevice, c.st), "H2D signal");
-    dsig = b;
-  }
-  if (d.signal_dtype == XC_F64 || d.signal_dtype == XC_C128) {
-    void* b = c.ctx->buf<char>("sig_f32", npix * (cplx_sig ? 8 : 4));
-    xcb::launch_convert_signal(dsig, d.signal_dtype, npix, b, c.st, c.lc);
-    dsig = b;
-  }
-  s.sig = xcb::SigSrc{dsig, cplx_sig ? 1 : 0, nullptr, xcb::SIG_PLAIN};
-  if (par_src) {
-    const void* dpar = par_src;
-    if (d.memory == XC_HOST) {
-      void* b = c.ctx->buf<char>("param_raw", npix * ps);
-      ck(cudaMemcpyAsync(b, par_src, npix * ps, cudaMemcpyHostToDevice, c.st), "H2D param");
-      dpar = b;
+// Host-memory batches run a two-slot pipeline: H2D of image i+1 (cp_in) and
+// D2H of image i-1 (cp_out) overlap the kernels of image i (compute stream).
+struct HostPipe {
+  Call* c = nullptr;
+  bool host = false;
+  cudaEvent_t in_done[2]{}, comp_done[2]{}, out_done[2]{}, t0{}, t1{};
+  int issued = 0;
+  explicit HostPipe(Call& call) : c(&call), host(call.d.memory == XC_HOST) {
+    for (int s = 0; s < 2; ++s) {
+      ck(cudaEventCreateWithFlags(&in_done[s], cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&comp_done[s], cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&out_done[s], cudaEventDisableTiming), "event");
     }
-    s.param = dpar;
+    ck(cudaEventCreate(&t0), "event");
+    ck(cudaEventCreate(&t1), "event");
   }
-  s.param_f64 = d.param_dtype == XC_F64;
-  if (d.memory == XC_HOST) {
-    ck(cudaStreamSynchronize(c.st), "H2D");
-    c.h2d_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  ~HostPipe() {
+    for (int s = 0; s < 2; ++s) {
+      cudaEventDestroy(in_done[s]);
+      cudaEventDestroy(comp_done[s]);
+      cudaEventDestroy(out_done[s]);
+    }
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
   }
+  size_t npix() const { return size_t(c->rows) * c->cols; }
+  // issue the H2D copies of image img into slot img&1 (host memory only)
+  void h2d(const void* signal, const void* param, int img) {
+    if (!host || img >= c->d.batch) return;
+    const int s = img & 1;
+    const size_t ss = dtype_size(c->d.signal_dtype), ps = dtype_size(c->d.param_dtype);
+    void* bs = c->ctx->buf<char>(s ? "sig_raw1" : "sig_raw0", npix() * ss);
+    void* bp = param ? c->ctx->buf<char>(s ? "param_raw1" : "param_raw0", npix() * ps) : nullptr;
+    if (img >= 2) ck(cudaStreamWaitEvent(c->ctx->cp_in, comp_done[s], 0), "wait");
+    ck(cudaMemcpyAsync(bs, static_cast<const char*>(signal) + size_t(img) * npix() * ss,
+                       npix() * ss, cudaMemcpyHostToDevice, c->ctx->cp_in),
+       "H2D signal");
+    if (param) {
+      const char* src = static_cast<const char*>(param) +
+                        (c->d.param_per_image ? size_t(img) * npix() * ps : 0);
+      ck(cudaMemcpyAsync(bp, src, npix() * ps, cudaMemcpyHostToDevice, c->ctx->cp_in),
+         "H2D param");
+    }
+    ck(cudaEventRecord(in_done[s], c->ctx->cp_in), "event");
+  }
+  // device pointers of image img's inputs, ready on the compute stream
+  Staged inputs(const void* signal, const void* param, int img) {
+    const xc_image_desc& d = c->d;
+    const size_t ss = dtype_size(d.signal_dtype), ps = dtype_size(d.param_dtype);
+    const bool cplx_sig = d.signal_dtype == XC_C64 || d.signal_dtype == XC_C128;
+    const int s = img & 1;
+    Staged st{};
+    const void* dsig;
+    const void* dpar = nullptr;
+    if (host) {
+      ck(cudaStreamWaitEvent(c->st, in_done[s], 0), "wait");
+      dsig = c->ctx->buf<char>(s ? "sig_raw1" : "sig_raw0", npix() * ss);
+      if (param) dpar = c->ctx->buf<char>(s ? "param_raw1" : "param_raw0", npix() * ps);
+    } else {
+      dsig = static_cast<const char*>(signal) + size_t(img) * npix() * ss;
+      if (param)
+        dpar = static_cast<const char*>(param) + (d.param_per_image ? size_t(img) * npix() * ps : 0);
+    }
+    if (d.signal_dtype == XC_F64 || d.signal_dtype == XC_C128) {
+      void* b = c->ctx->buf<char>("sig_f32", npix() * (cplx_sig ? 8 : 4));
+      xcb::launch_convert_signal(dsig, d.signal_dtype, npix(), b, c->st, c->lc);
+      dsig = b;
+    }
+    st.sig = xcb::SigSrc{dsig, cplx_sig ? 1 : 0, nullptr, xcb::SIG_PLAIN};
+    st.param = dpar;
+    st.param_f64 = d.param_dtype == XC_F64;
+    return st;
+  }
+  // output buffer of image img (device: the caller's; host: a slot stage)
+  void* out_buffer(void* out, int img, size_t os) {
+    if (!host) return static_cast<char*>(out) + size_t(img) * npix() * os;
+    const int s = img & 1;
+    if (img >= 2) ck(cudaStreamWaitEvent(c->st, out_done[s], 0), "wait");
+    return c->ctx->buf<char>(s ? "out_stage1" : "out_stage0", npix() * os);
+  }
+  // after image img's kernels: start its D2H (host memory)
+  void done(void* out, int img, void* dout, size_t os) {
+    if (!host) return;
+    const int s = img & 1;
+    ck(cudaEventRecord(comp_done[s], c->st), "event");
+    ck(cudaStreamWaitEvent(c->ctx->cp_out, comp_done[s], 0), "wait");
+    ck(cudaMemcpyAsync(static_cast<char*>(out) + size_t(img) * npix() * os, dout, npix() * os,
+                       cudaMemcpyDeviceToHost, c->ctx->cp_out),
+       "D2H");
+    ck(cudaEventRecord(out_done[s], c->ctx->cp_out), "event");
+  }
+  void finish() {
+    if (host) ck(cudaStreamSynchronize(c->ctx->cp_out), "D2H");
+    ck(cudaStreamSynchronize(c->st), "compute");
+  }
+};
+
+Staged stage_inputs(Call& c, const void* signal, const void* param, int img) {
+  // synchronous single-image staging (smooth / anglemax paths)
+  HostPipe hp(c);
+  hp.h2d(signal, param, img);
+  Staged s = hp.inputs(signal, param, img);
+  if (hp.host) ck(cudaStreamSynchronize(c.st), "H2D");
   return s;
 }
 
@@ -561,6 +630,8 @@ int xc_context_create(int device, xc_context* out) {
     auto* c = new xc_context_s();
     c->device = device;
     ck(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaStreamCreateWithFlags(&c->cp_in, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaStreamCreateWithFlags(&c->cp_out, cudaStreamNonBlocking), "cudaStreamCreate");
     c->stream = c->own;
     *out = c;
   });
@@ -722,33 +793,25 @@ int xc_run(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d, const 
     ck(cudaEventCreate(&e0), "event");
     ck(cudaEventCreate(&e1), "event");
     double gpu_s = 0;
+    HostPipe hp(c);
+    hp.h2d(signal, param, 0);
+    ck(cudaEventRecord(e0, c.st), "event");
     for (int img = 0; img < d->batch; ++img) {
-      Staged s = stage_inputs(c, signal, param, img);
-      ck(cudaEventRecord(e0, c.st), "event");
+      hp.h2d(signal, param, img + 1);
+      Staged s = hp.inputs(signal, param, img);
       double* base = nullptr;
       prep(c, s, false, &base, nullptr);
-      void* dout = d->memory == XC_DEVICE ? static_cast<char*>(out) + size_t(img) * npix * os
-                                           : c.ctx->buf<char>("out_stage", npix * os);
+      void* dout = hp.out_buffer(out, img, os);
       if (mode == XC_CORRELATION)
         run_gather(c, s.sig, base, dout, out_kind, accumulate, dc);
       else
         run_scatter(c, s.sig, base, dout, out_kind, accumulate, dc);
       ck(cudaGetLastError(), "kernel launch");
-      ck(cudaEventRecord(e1, c.st), "event");
-      if (d->memory == XC_HOST) {
-        ck(cudaEventSynchronize(e1), "pipeline");
-        gpu_s += event_seconds(e0, e1);
-        auto t0 = std::chrono::steady_clock::now();
-        ck(cudaMemcpyAsync(static_cast<char*>(out) + size_t(img) * npix * os, dout, npix * os,
-                           cudaMemcpyDeviceToHost, c.st),
-           "D2H");
-        ck(cudaStreamSynchronize(c.st), "D2H");
-        c.d2h_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-      } else {
-        ck(cudaEventSynchronize(e1), "pipeline");
-        gpu_s += event_seconds(e0, e1);
-      }
+      hp.done(out, img, dout, os);
     }
+    ck(cudaEventRecord(e1, c.st), "event");
+    hp.finish();
+    gpu_s = event_seconds(e0, e1);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     ctx->resolve_profile();

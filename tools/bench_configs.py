@@ -1,0 +1,79 @@
+"""Device-resident timing of every BASELINE config through the public API
+(per-stage CUDA-event profile included).  Prints one JSON line per config."""
+import ctypes as C
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2006_13188_b200 import _native as N  # noqa: E402
+from paper_2006_13188_b200 import workloads as WL  # noqa: E402
+
+
+def run(cfg, reps=3):
+    w = {5: lambda: WL.config5(batch=2)}.get(cfg, WL.CONFIGS[cfg])()
+    dev = torch.device("cuda", 0)
+    ctx = N.context(0)
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+    B, H, W = w.signal.shape
+    sig = torch.from_numpy(w.signal).to(dev)
+    fh = w.filt.handle()
+    st = N.Stats()
+    if w.mode in ("xcorr", "xconv"):
+        par = torch.from_numpy(w.param).to(dev)
+        out = torch.empty((B, H, W), dtype=torch.complex64, device=dev)
+        d = N.ImageDesc(H, W, B, N.XC_F32, N.XC_F32, N.XC_C64, N.XC_ROW_MAJOR, N.XC_DEVICE, 1,
+                        int(w.filt.group))
+        mode = 0 if w.mode == "xcorr" else 1
+
+        def call():
+            N.check(N.lib().xc_run(ctx.handle, fh, mode, C.byref(d), C.c_void_p(sig.data_ptr()),
+                                   C.c_void_p(par.data_ptr()), None, 0, 0,
+                                   C.c_void_p(out.data_ptr()), C.byref(st)), ctx.handle)
+    elif w.mode == "smooth":
+        par = torch.from_numpy(w.param).to(dev)
+        out = torch.empty((B, H, W), dtype=torch.float32, device=dev)
+        d = N.ImageDesc(H, W, B, N.XC_F32, N.XC_F32, N.XC_F32, N.XC_ROW_MAJOR, N.XC_DEVICE, 1,
+                        int(w.filt.group))
+
+        def call():
+            N.check(N.lib().xc_smooth(ctx.handle, fh, C.byref(d), C.c_void_p(sig.data_ptr()),
+                                      C.c_void_p(par.data_ptr()), 1, C.c_void_p(out.data_ptr()),
+                                      C.byref(st)), ctx.handle)
+    else:
+        out = torch.empty((B, H, W), dtype=torch.float32, device=dev)
+        arg = torch.empty((B, H, W), dtype=torch.int32, device=dev)
+        d = N.ImageDesc(H, W, B, N.XC_F32, N.XC_F32, N.XC_F32, N.XC_ROW_MAJOR, N.XC_DEVICE, 0, 0)
+
+        def call():
+            N.check(N.lib().xc_anglemax(ctx.handle, fh, C.byref(d), C.c_void_p(sig.data_ptr()),
+                                        None, 0, 360, C.c_void_p(out.data_ptr()),
+                                        C.cast(C.c_void_p(arg.data_ptr()), C.POINTER(C.c_int)),
+                                        C.byref(st)), ctx.handle)
+    call()
+    torch.cuda.synchronize()
+    ctx.profile(enable=True, reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        call()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    prof = ctx.profile(enable=False, reset=True)
+    ms = e0.elapsed_time(e1) / reps
+    units = w.units()
+    print(json.dumps({"config": cfg, "workload": w.name, "ms_per_call": ms,
+                      "Mpix_bands_per_s": units / ms / 1e3, "pad": [st.pad_h, st.pad_w],
+                      "standard_ops": st.standard_ops, "launches_per_call": st.gpu_launches,
+                      "stages_ms": {k: v[0] / reps for k, v in prof.items()}}), flush=True)
+
+
+if __name__ == "__main__":
+    for c in [int(x) for x in (sys.argv[1:] or ["1", "2", "3", "4", "5"])]:
+        run(c)
