@@ -1,4 +1,6 @@
 // Per-pixel stages: steering base / guard band, dtype conversion, smooth divide, angle max.
+#include <algorithm>
+
 #include "stages_common.cuh"
 
 namespace xcb {
@@ -138,6 +140,57 @@ __global__ void __launch_bounds__(128)
   if (argmax) argmax[p] = arg;
 }
 
+// Angle max by FFT (n_angles = 360, bands k in [-KH, KH]): with s = s1 + N1 s2
+// (N1 N2 = 360, N2 >= 2 KH + 1),
+//   X(s) = sum_k G_k e^{-2 pi i k s / 360}
+//        = DFT_N2[ m -> G_k w^{k s1}, m = k mod N2 ](s2),  w = e^{-2 pi i / 360},
+// so each pixel costs N1 twiddled N2-point DFTs instead of 360 x (2 KH + 1)
+// complex MACs.  Ties keep the smallest s (the oracle's first maximum).
+template <int KH, int N2, class TO>
+__global__ void __launch_bounds__(128)
+    k_anglemax_fft(const float2* __restrict__ planes, AngleMap m, size_t npix,
+                   TO* __restrict__ score, int* __restrict__ argmax) {
+  constexpr int ND = 2 * KH + 1, N = 360, N1 = N / N2;
+  static_assert(N1 * N2 == N && N2 >= ND, "bad angle-max split");
+  __shared__ float2 tw[ND * N1];
+  for (int i = threadIdx.x; i < ND * N1; i += blockDim.x) {
+    const int d = i / N1, s1 = i % N1;
+    double sn, cs;
+    sincospi(-2.0 * double((d - KH) * s1) / N, &sn, &cs);
+    tw[i] = make_float2(float(cs), float(sn));
+  }
+  __syncthreads();
+  const size_t p = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+  if (p >= npix) return;
+  float2 G[ND];
+#pragma unroll
+  for (int d = 0; d < ND; ++d)
+    G[d] = m.idx[d] >= 0 ? planes[size_t(m.idx[d]) * npix + p] : make_float2(0.f, 0.f);
+  float best = -1.f;
+  int arg = 0;
+#pragma unroll 1
+  for (int s1 = 0; s1 < N1; ++s1) {
+    float2 v[N2];
+#pragma unroll
+    for (int q = 0; q < N2; ++q) v[q] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int d = 0; d < ND; ++d) v[((d - KH) % N2 + N2) % N2] = c_mul(G[d], tw[d * N1 + s1]);
+    Dft<N2>::run(v);
+#pragma unroll
+    for (int s2 = 0; s2 < N2; ++s2) {
+      const float2 x = v[Dft<N2>::pos(s2)];
+      const float m2 = fmaf(x.x, x.x, x.y * x.y);
+      const int s = s1 + N1 * s2;
+      if (m2 > best || (m2 == best && s < arg)) {
+        best = m2;
+        arg = s;
+      }
+    }
+  }
+  score[p] = TO(sqrtf(best));
+  if (argmax) argmax[p] = arg;
+}
+
 }  // namespace
 
 float2* upload_twiddles(const FftPlan& p) {
@@ -199,8 +252,35 @@ void launch_anglemax(const float2* planes, const int* ks_host, int nb, size_t np
   for (int d = 0; d < m.nd && d < kMaxDense; ++d) m.idx[d] = -1;
   for (int i = 0; i < nb; ++i) m.idx[ks_host[i] - kmin] = i;
   const int bs = 128;
-  const size_t smem = (size_t(n_angles) + size_t(m.nd) * bs) * sizeof(float2);
   const int grid = int((npix + bs - 1) / bs);
+  // FFT evaluation for 360 angles and a band set inside [-KH, KH]
+  const int kh = std::max(-kmin, kmax);
+  int KH = 0;
+  for (int c : {4, 8, 16, 32})
+    if (kh <= c) {
+      KH = c;
+      break;
+    }
+  if (n_angles == 360 && KH > 0) {
+    AngleMap fm{};
+    fm.nd = 2 * KH + 1;
+    for (int d = 0; d < fm.nd; ++d) fm.idx[d] = -1;
+    for (int i = 0; i < nb; ++i) fm.idx[ks_host[i] + KH] = i;
+#define XCB_AM(KHV, N2V)                                                                     \
+  if (KH == KHV) {                                                                         \
+    if (score_f64)                                                                         \
+      k_anglemax_fft<KHV, N2V, double><<<grid, bs, 0, st>>>(planes, fm, npix,              \
+                                                           static_cast<double*>(score), argmax); \
+    else                                                                                   \
+      k_anglemax_fft<KHV, N2V, float><<<grid, bs, 0, st>>>(planes, fm, npix,               \
+                                                          static_cast<float*>(score), argmax);  \
+  }
+    XCB_AM(4, 12) XCB_AM(8, 18) XCB_AM(16, 36) XCB_AM(32, 72)
+#undef XCB_AM
+    ++lc.n;
+    return;
+  }
+  const size_t smem = (size_t(n_angles) + size_t(m.nd) * bs) * sizeof(float2);
   if (score_f64) {
     set_smem(k_anglemax<double>, smem);
     k_anglemax<double><<<grid, bs, smem, st>>>(planes, m, npix, n_angles,

@@ -305,3 +305,55 @@ def test_tiny_and_ragged_images(orc, shape):
         assert orc.rel_l2(got, ofn(H, ROT, T, F)[0]) < TOL
         gotp = fn(H, X.XformField.rotation(T), pfilter(F), X.XConvPlan(periodic=True)).output
         assert orc.rel_l2(gotp, ofn(H, ROT, T, F, periodic=True)[0]) < TOL
+
+
+# --------------------------------------------- fast-path coverage (pad table)
+
+@pytest.mark.parametrize("n_angles,m_max", [(360, 4), (360, 8), (100, 4)])
+def test_anglemax_fft_and_generic(orc, n_angles, m_max):
+    """360 angles with |m| <= KH runs the FFT evaluation; other n the Horner one."""
+    from paper_2006_13188_b200 import workloads as WL
+    r = np.random.default_rng(5)
+    f = WL.angular_filter(9, 4.0, m_max, r)
+    F = X.decompose_rotation2(f, 9, 9, 2 * m_max, 18, 4 * m_max + 4, 9.0)
+    H = r.standard_normal((70, 90)).astype(np.float32)
+    score, arg = X.anglemax(H, F, n_angles)
+    OF = ofilter(orc, F)
+    G = np.stack([orc.xcorr_fast(H.astype(np.float64), ROT, np.zeros(H.shape), OF,
+                                 components=[int(k)])[0] for k in OF.ks])
+    oscore, oarg = orc.anglemax(G, OF.ks, n_angles)
+    assert orc.rel_l2(score, oscore) < TOL
+    at = np.abs(np.einsum("kyx,kyx->yx", G, np.exp(
+        -2j * np.pi * np.asarray(OF.ks)[:, None, None] * arg[None] / n_angles)))
+    assert np.all(at >= oscore * (1 - 1e-5) - 1e-9)
+
+
+@pytest.mark.parametrize("n", [256, 480])
+def test_fast_scatter_and_smooth_sizes(orc, n):
+    """Pads 288 / 512 are fast-table lengths: S1/S2 fast kernels (rotation
+    scatter, scale smoothing) against the oracle."""
+    from paper_2006_13188_b200 import workloads as WL
+    w = WL.config2(n=n)
+    assert _cfg_parity(orc, w) < TOL
+    w4 = WL.config4(n=n)
+    assert _cfg_parity(orc, w4) < TOL
+    # scale-group gather (fast I1/I2 + conj(dc) H)
+    H = w4.signal[0]
+    S = w4.param[0]
+    got = X.xcorr_fast(H, X.XformField.scaling(S), w4.filt).output
+    ref = orc.xcorr_fast(H.astype(np.float64), SCALE, S.astype(np.float64), ofilter(orc, w4.filt))[0]
+    assert orc.rel_l2(got, ref) < TOL
+
+
+def test_host_pipeline_batch_matches_device_path(orc):
+    """Host-memory batches (two-slot H2D/compute/D2H pipeline) equal per-image calls."""
+    from paper_2006_13188_b200 import workloads as WL
+    w = WL.config1()
+    r = np.random.default_rng(9)
+    B = 5
+    sig = r.uniform(0, 1, (B, 256, 256)).astype(np.float32)
+    th = r.uniform(0, 2 * np.pi, (B, 256, 256)).astype(np.float32)
+    batch = X.xcorr_fast(sig, X.XformField.rotation(th), w.filt).output
+    for b in (0, 3, 4):
+        one = X.xcorr_fast(sig[b], X.XformField.rotation(th[b]), w.filt).output
+        assert np.array_equal(batch[b], one)
