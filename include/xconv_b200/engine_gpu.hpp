@@ -1,0 +1,206 @@
+// engine_gpu.hpp -- C++ host-side drop-in for the reference's 2D fast paths.
+//
+// Header-only, templated over the reference's own types (Field2<Real>,
+// XformField<Real>, FreqFilter2<Real>, XConvPlan, Response2<Real>,
+// SmoothResult<Real> from proj/include/xconv/{field,freq_filter,engine}.hpp),
+// so the reference keeps its signatures and replaces its per-band CPU loop by
+// the C ABI of include/xconv_b200.h:
+//
+//   xconv::gpu::xcorr_fast(H, T, F, plan)        <- engine.hpp:286-326
+//   xconv::gpu::xconv_fast(H, T, F, plan)        <- engine.hpp:331-373
+//   xconv::gpu::smooth_adaptive(H, T, F, norm)   <- engine.hpp:385-419
+//
+// Eigen's default column-major storage (field.hpp:15) is passed as
+// XC_COL_MAJOR with the caller's complex<double> / double buffers
+// (XC_C128 / XC_F64); std::invalid_argument is rethrown with the reference's
+// message for XC_EINVAL, std::runtime_error otherwise.  The device-side filter
+// spectra are cached per filter content (hash), per thread.
+#pragma once
+
+#include <complex>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../xconv_b200.h"
+
+namespace xconv {
+namespace gpu {
+
+namespace detail {
+
+inline void check(int rc, xc_context ctx) {
+  if (rc == XC_OK) return;
+  const std::string msg = xc_last_error(ctx);
+  if (rc == XC_EINVAL) throw std::invalid_argument(msg);
+  throw std::runtime_error("xconv_b200: " + msg);
+}
+
+struct Context {
+  xc_context ctx = nullptr;
+  std::map<uint64_t, xc_filter> filters;
+  Context() { check(xc_context_create(0, &ctx), nullptr); }
+  ~Context() {
+    for (auto& kv : filters) xc_filter_destroy(kv.second);
+    xc_context_destroy(ctx);
+  }
+};
+
+inline Context& context() {
+  thread_local Context c;
+  return c;
+}
+
+inline uint64_t fnv(uint64_t h, const void* p, size_t n) {
+  const unsigned char* b = static_cast<const unsigned char*>(p);
+  for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  return h;
+}
+
+// FreqFilter2<Real> -> xc_filter (cached by content)
+template <class F>
+xc_filter filter_handle(const F& f) {
+  Context& c = context();
+  const int nc = static_cast<int>(f.ks.size());
+  const int rows = static_cast<int>(f.comps.rows());
+  std::vector<double> comps(size_t(2) * nc * rows);
+  for (int ci = 0; ci < nc; ++ci)
+    for (int r = 0; r < rows; ++r) {  // Eigen column-major (row + ci * n_rows)
+      comps[2 * (size_t(ci) * rows + r)] = double(std::real(f.comps(r, ci)));
+      comps[2 * (size_t(ci) * rows + r) + 1] = double(std::imag(f.comps(r, ci)));
+    }
+  const int group = static_cast<int>(f.group);
+  const double sc[3] = {double(f.r_max), double(f.r_min), double(f.r_domain)};
+  const int ints[4] = {group, f.K, f.n_radii, f.n_angles};
+  uint64_t h = 1469598103934665603ull;
+  h = fnv(h, ints, sizeof(ints));
+  h = fnv(h, sc, sizeof(sc));
+  h = fnv(h, f.ks.data(), f.ks.size() * sizeof(int));
+  h = fnv(h, comps.data(), comps.size() * sizeof(double));
+  auto it = c.filters.find(h);
+  if (it != c.filters.end()) return it->second;
+  xc_filter out = nullptr;
+  check(xc_filter_create(c.ctx, group, f.K, f.ks.data(), nc, comps.data(), f.n_radii,
+                         f.n_angles, sc[0], sc[1], sc[2], &out),
+        nullptr);
+  c.filters[h] = out;
+  return out;
+}
+
+template <class Real>
+constexpr int signal_dtype() {
+  return sizeof(Real) == 8 ? XC_C128 : XC_C64;
+}
+template <class Real>
+constexpr int real_dtype() {
+  return sizeof(Real) == 8 ? XC_F64 : XC_F32;
+}
+
+// engine.hpp:288-291 checks (the ABI repeats them; these keep the order of
+// the reference's messages for the fields only the host sees)
+template <class Field, class Xform, class F>
+void validate(const Field& H, const Xform& T, const F& Fl) {
+  if (static_cast<int>(T.kind) != static_cast<int>(Fl.group))
+    throw std::invalid_argument("transformation/filter group mismatch");
+  if (static_cast<int>(T.kind) == XC_ROTATION3)
+    throw std::invalid_argument("2D pipeline needs a 2D field");
+  if (H.width() != T.width() || H.height() != T.height())
+    throw std::invalid_argument("signal and transformation field dims differ");
+}
+
+template <class Response, class Field, class Xform, class F, class Plan>
+Response run(int mode, const Field& H, const Xform& T, const F& Fl, Plan plan) {
+  using Real = typename std::remove_cv<typename std::remove_reference<
+      decltype(std::real(H.values(0, 0)))>::type>::type;
+  validate(H, T, Fl);
+  Context& c = context();
+  xc_filter fh = filter_handle(Fl);
+  const bool scale = static_cast<int>(T.kind) == XC_SCALE2;
+  xc_image_desc d{};
+  d.height = H.height();
+  d.width = H.width();
+  d.batch = 1;
+  d.signal_dtype = signal_dtype<Real>();
+  d.param_dtype = real_dtype<Real>();
+  d.out_dtype = signal_dtype<Real>();
+  d.layout = XC_COL_MAJOR;
+  d.memory = XC_HOST;
+  d.param_per_image = 1;
+  d.xform_kind = static_cast<int>(T.kind);
+  Response r;
+  plan.mode = decltype(plan.mode)(mode);
+  plan.group = T.kind;
+  r.plan = plan;
+  r.output = Field(H.width(), H.height());
+  const void* param = scale ? static_cast<const void*>(T.scale.data())
+                            : static_cast<const void*>(T.angle.data());
+  std::vector<int> comps(plan.components.begin(), plan.components.end());
+  xc_stats st{};
+  check(xc_run(c.ctx, fh, mode, &d, H.values.data(), param, comps.empty() ? nullptr : comps.data(),
+               static_cast<int>(comps.size()), plan.periodic ? XC_FLAG_PERIODIC : 0u,
+               r.output.values.data(), &st),
+        c.ctx);
+  r.standard_ops = st.standard_ops;
+  r.seconds["render"] = st.seconds_render;
+  r.seconds["fft"] = st.seconds_fft;
+  r.seconds["combine"] = st.seconds_combine;
+  if (mode == XC_CONVOLUTION) r.seconds["premultiply"] = st.seconds_premultiply;
+  return r;
+}
+
+}  // namespace detail
+
+// engine.hpp:286-287
+template <class Response, class Field, class Xform, class F, class Plan>
+Response xcorr_fast(const Field& H, const Xform& T, const F& Fl, Plan plan) {
+  return detail::run<Response>(XC_CORRELATION, H, T, Fl, plan);
+}
+
+// engine.hpp:331-332
+template <class Response, class Field, class Xform, class F, class Plan>
+Response xconv_fast(const Field& H, const Xform& T, const F& Fl, Plan plan) {
+  return detail::run<Response>(XC_CONVOLUTION, H, T, Fl, plan);
+}
+
+// engine.hpp:385-387 (SmoothResult: output, standard_ops, clamped_pixels)
+template <class Result, class Field, class Xform, class F>
+Result smooth_adaptive(const Field& H, const Xform& T, const F& Fl, bool normalize_signal = true) {
+  using Real = typename std::remove_cv<typename std::remove_reference<
+      decltype(std::real(H.values(0, 0)))>::type>::type;
+  detail::Context& c = detail::context();
+  xc_filter fh = detail::filter_handle(Fl);
+  if (H.width() != T.width() || H.height() != T.height())
+    throw std::invalid_argument("signal and transformation field dims differ");
+  const bool scale = static_cast<int>(T.kind) == XC_SCALE2;
+  xc_image_desc d{};
+  d.height = H.height();
+  d.width = H.width();
+  d.batch = 1;
+  d.signal_dtype = detail::signal_dtype<Real>();
+  d.param_dtype = detail::real_dtype<Real>();
+  d.out_dtype = detail::real_dtype<Real>();
+  d.layout = XC_COL_MAJOR;
+  d.memory = XC_HOST;
+  d.param_per_image = 1;
+  d.xform_kind = static_cast<int>(T.kind);
+  std::vector<Real> real_out(size_t(H.width()) * H.height());
+  const void* param = scale ? static_cast<const void*>(T.scale.data())
+                            : static_cast<const void*>(T.angle.data());
+  xc_stats st{};
+  detail::check(xc_smooth(c.ctx, fh, &d, H.values.data(), param, normalize_signal ? 1 : 0,
+                          real_out.data(), &st),
+                c.ctx);
+  Result out;
+  out.standard_ops = st.standard_ops;
+  out.clamped_pixels = st.clamped_pixels;
+  out.output = decltype(out.output)(H.width(), H.height());
+  for (size_t i = 0; i < real_out.size(); ++i) out.output.values.data()[i] = real_out[i];
+  return out;
+}
+
+}  // namespace gpu
+}  // namespace xconv

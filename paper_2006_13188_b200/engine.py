@@ -271,7 +271,7 @@ def _seconds(st: N.Stats) -> dict:
 
 
 def _fast(mode: XMode, H, T: XformField, F: FreqFilter2, plan: XConvPlan | None,
-          device: int = 0) -> Response2:
+          device: int = 0, inner_dc: bool = True) -> Response2:
     plan = XConvPlan() if plan is None else XConvPlan(plan.mode, plan.group,
                                                       list(plan.components), plan.periodic)
     sig = _signal(H)
@@ -283,6 +283,8 @@ def _fast(mode: XMode, H, T: XformField, F: FreqFilter2, plan: XConvPlan | None,
     comp = np.ascontiguousarray(np.asarray(plan.components, np.int32))
     st = N.Stats()
     flags = N.XC_FLAG_PERIODIC if plan.periodic else 0
+    if not inner_dc:  # band-sharded scale runs add the inner-DC term on one rank
+        flags |= N.XC_FLAG_NO_INNER_DC
     N.check(N.lib().xc_run(ctx.handle, F.handle(ctx), int(mode), C.byref(d),
                            sig.ctypes.data, par.ctypes.data,
                            comp.ctypes.data_as(C.POINTER(C.c_int)) if len(comp) else None,

@@ -1,0 +1,79 @@
+// Minimal stand-ins with the member names and storage order of the reference
+// types (proj/include/xconv/field.hpp, freq_filter.hpp, engine.hpp), used to
+// compile the C++ drop-in shim without Eigen (absent in this image).  Grids
+// are column-major like Eigen's default: values(y, x) at y + x * rows.
+#pragma once
+#include <complex>
+#include <map>
+#include <string>
+#include <vector>
+
+namespace mini {
+
+template <class T>
+struct Grid {
+  std::vector<T> v;
+  int r = 0, c = 0;
+  Grid() = default;
+  Grid(int rows, int cols) : v(size_t(rows) * cols), r(rows), c(cols) {}
+  T& operator()(int row, int col) { return v[row + size_t(col) * r]; }
+  const T& operator()(int row, int col) const { return v[row + size_t(col) * r]; }
+  T* data() { return v.data(); }
+  const T* data() const { return v.data(); }
+  int rows() const { return r; }
+  int cols() const { return c; }
+};
+
+enum class XformKind { rotation2, scale2, rotation3 };
+enum class XMode { correlation, convolution };
+
+template <class Real>
+struct Field2 {
+  Grid<std::complex<Real>> values;
+  Field2() = default;
+  Field2(int w, int h) : values(h, w) {}
+  int width() const { return values.cols(); }
+  int height() const { return values.rows(); }
+};
+
+template <class Real>
+struct XformField {
+  XformKind kind = XformKind::rotation2;
+  Grid<Real> angle, scale;
+  int width() const { return kind == XformKind::scale2 ? scale.cols() : angle.cols(); }
+  int height() const { return kind == XformKind::scale2 ? scale.rows() : angle.rows(); }
+};
+
+template <class Real>
+struct FreqFilter2 {
+  XformKind group = XformKind::rotation2;
+  int K = 0;
+  std::vector<int> ks;
+  Grid<std::complex<Real>> comps;
+  int n_radii = 0, n_angles = 0;
+  Real r_max = 0, r_min = 0, r_domain = 0;
+};
+
+struct XConvPlan {
+  XMode mode = XMode::correlation;
+  XformKind group = XformKind::rotation2;
+  std::vector<int> components;
+  bool periodic = false;
+};
+
+template <class Real>
+struct Response2 {
+  Field2<Real> output;
+  XConvPlan plan;
+  long long standard_ops = 0;
+  std::map<std::string, double> seconds;
+};
+
+template <class Real>
+struct SmoothResult {
+  Field2<Real> output;
+  long long standard_ops = 0;
+  int clamped_pixels = 0;
+};
+
+}  // namespace mini

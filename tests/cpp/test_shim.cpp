@@ -1,0 +1,111 @@
+// The C++ drop-in path end to end: reference-shaped types -> engine_gpu.hpp ->
+// C ABI -> sm_100a kernels, checked against the CPU oracle (test
+// infrastructure).  Exit 0 iff every case is within 1e-5 relative L2.
+#include <cmath>
+#include <cstdio>
+#include <random>
+
+#include "../../include/xconv_b200/engine_gpu.hpp"
+#include "../../oracle/xconv_oracle.h"
+#include "mini_xconv.hpp"
+
+using namespace mini;
+using cd = std::complex<double>;
+
+static double rel(const std::vector<cd>& a, const std::vector<cd>& b) {
+  double n = 0, d = 0;
+  for (size_t i = 0; i < a.size(); ++i) {
+    n += std::norm(a[i] - b[i]);
+    d += std::norm(b[i]);
+  }
+  return std::sqrt(n / d);
+}
+
+int main() {
+  std::mt19937_64 rng(7);
+  std::uniform_real_distribution<double> u(-1, 1);
+  const int h = 37, w = 53, R = 6;
+  // filter: decompose a random smooth image with the product's host ABI
+  std::vector<double> filt(2 * (2 * R + 1) * (2 * R + 1));
+  for (size_t i = 0; i < filt.size(); i += 2) filt[i] = u(rng);
+  const int K = 16, nr = 12, na = 34;
+  std::vector<int> ks(K + 1);
+  std::vector<double> comps(2 * size_t(nr) * (K + 1));
+  int nc = 0;
+  if (xc_decompose_rotation2(filt.data(), 2 * R + 1, 2 * R + 1, XC_ROW_MAJOR, R, R, K, nr, na,
+                             double(R), ks.data(), comps.data(), &nc) != XC_OK)
+    return 2;
+  FreqFilter2<double> F;
+  F.group = XformKind::rotation2;
+  F.K = K;
+  F.ks = ks;
+  F.comps = Grid<std::complex<double>>(nr, nc);
+  for (int ci = 0; ci < nc; ++ci)
+    for (int r = 0; r < nr; ++r)
+      F.comps(r, ci) = cd(comps[2 * (size_t(ci) * nr + r)], comps[2 * (size_t(ci) * nr + r) + 1]);
+  F.n_radii = nr;
+  F.n_angles = na;
+  F.r_max = R;
+  // signal / angles, column-major like Eigen
+  Field2<double> H(w, h);
+  XformField<double> T;
+  T.kind = XformKind::rotation2;
+  T.angle = Grid<double>(h, w);
+  for (int x = 0; x < w; ++x)
+    for (int y = 0; y < h; ++y) {
+      H.values(y, x) = cd(u(rng), u(rng));
+      T.angle(y, x) = 3.14159 * u(rng);
+    }
+  // oracle inputs (row-major)
+  std::vector<double> Ho(2 * size_t(h) * w), To(size_t(h) * w), rowc(2 * size_t(nr) * nc);
+  for (int y = 0; y < h; ++y)
+    for (int x = 0; x < w; ++x) {
+      Ho[2 * (size_t(y) * w + x)] = H.values(y, x).real();
+      Ho[2 * (size_t(y) * w + x) + 1] = H.values(y, x).imag();
+      To[size_t(y) * w + x] = T.angle(y, x);
+    }
+  for (int r = 0; r < nr; ++r)
+    for (int ci = 0; ci < nc; ++ci) {
+      rowc[2 * (size_t(r) * nc + ci)] = F.comps(r, ci).real();
+      rowc[2 * (size_t(r) * nc + ci) + 1] = F.comps(r, ci).imag();
+    }
+  or_filter of{0, K, nc, ks.data(), rowc.data(), nr, na, double(R), 0, 0};
+  int fails = 0;
+  for (int mode = 0; mode < 2; ++mode)
+    for (int periodic = 0; periodic < 2; ++periodic) {
+      XConvPlan plan;
+      plan.periodic = periodic != 0;
+      Response2<double> r =
+          mode == 0 ? xconv::gpu::xcorr_fast<Response2<double>>(H, T, F, plan)
+                    : xconv::gpu::xconv_fast<Response2<double>>(H, T, F, plan);
+      std::vector<double> ref(2 * size_t(h) * w);
+      long long ops = 0;
+      if (or_xfast(mode, Ho.data(), h, w, 0, To.data(), &of, nullptr, 0, periodic, ref.data(),
+                   &ops, nullptr, 1) != 0)
+        return 3;
+      std::vector<cd> a(size_t(h) * w), b(size_t(h) * w);
+      for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+          a[size_t(y) * w + x] = r.output.values(y, x);
+          b[size_t(y) * w + x] = cd(ref[2 * (size_t(y) * w + x)], ref[2 * (size_t(y) * w + x) + 1]);
+        }
+      const double e = rel(a, b);
+      const bool ok = e < 1e-5 && r.standard_ops == ops && r.standard_ops == nc &&
+                      r.plan.mode == (mode ? XMode::convolution : XMode::correlation);
+      std::printf("mode %d periodic %d: rel_l2 %.3e ops %lld %s\n", mode, periodic, e,
+                  r.standard_ops, ok ? "ok" : "FAIL");
+      fails += !ok;
+    }
+  // error behaviour: the reference's std::invalid_argument text
+  try {
+    XConvPlan plan;
+    plan.components = {99};
+    xconv::gpu::xcorr_fast<Response2<double>>(H, T, F, plan);
+    ++fails;
+  } catch (const std::invalid_argument& e) {
+    const bool ok = std::string(e.what()) == "plan retains a component the filter lacks";
+    std::printf("invalid plan: \"%s\" %s\n", e.what(), ok ? "ok" : "FAIL");
+    fails += !ok;
+  }
+  return fails ? 1 : 0;
+}

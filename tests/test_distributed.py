@@ -1,0 +1,104 @@
+"""Multi-rank sharding (world_size 2, gloo, CPU): band-sharded gather /
+scatter / smoothing reduce to the single-process result.  The per-rank compute
+is the CPU oracle here (the GPU path is the same orchestration with the
+sm_100a compute and NCCL, exercised by bench.py --shard bands)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def oracle_compute(mode, H, T, F, components, inner_dc):
+    import sys
+    sys.path.insert(0, ROOT)
+    from oracle import oracle as orc
+    OF = orc.Filter(int(F.group), F.K, F.ks, F.comps, F.n_radii, F.n_angles, F.r_max, F.r_min,
+                    F.r_domain)
+    fn = orc.xcorr_fast if mode == 0 else orc.xconv_fast
+    out = fn(np.asarray(H, np.complex128), int(T.kind), np.asarray(T.values, np.float64), OF,
+             components=list(components))[0]
+    if int(T.kind) == 1 and not inner_dc:  # remove the inner-DC term (engine.hpp:320-324)
+        dc = orc.inner_dc_value(OF)
+        out = out - (np.conj(dc) if mode == 0 else dc) * np.asarray(H, np.complex128)
+    return out
+
+
+def _worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle as orc
+    import paper_2006_13188_b200 as X
+    from paper_2006_13188_b200 import distributed as D
+    res = {}
+    rng = orc.Rng(300)
+    n, R = 20, 5
+    F = X.decompose_rotation2(rng.random_smooth_filter(R), R, R, 12, 16, 32, R)
+    H = rng.random_field(n, n, True)
+    T = X.XformField.rotation(rng.random_rotation_field(n, n))
+    for mode in (0, 1):
+        r = D.xfast_band_sharded(X.XMode(mode), H, T, F, compute=oracle_compute)
+        if rank == 0:
+            res[f"rot{mode}"] = (r.output, r.standard_ops)
+    Fs = X.decompose_scale2(rng.annular_filter(R), R, R, 8, 48, 32, 1.0, R)
+    S = X.XformField.scaling(rng.random_scale_field(n, n))
+    for mode in (0, 1):
+        r = D.xfast_band_sharded(X.XMode(mode), H, S, Fs, compute=oracle_compute)
+        if rank == 0:
+            res[f"scale{mode}"] = (r.output, r.standard_ops)
+    sm = D.smooth_band_sharded(H.real.copy(), S, Fs, compute=oracle_compute)
+    if rank == 0:
+        res["smooth"] = (sm.output, sm.standard_ops, sm.clamped_pixels)
+        q.put(res)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_band_ranges_balanced():
+    from paper_2006_13188_b200 import distributed as D
+    assert [b - a for a, b in D.band_ranges(65, 8)] == [8, 8, 8, 8, 8, 8, 8, 9]
+    assert sum(len(D.shard_components(range(-32, 33), r, 8)) for r in range(8)) == 65
+    assert list(D.batch_range(16, 3, 8)) == [6, 7]
+
+
+def test_band_sharded_world2_gloo(orc):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rng = orc.Rng(300)
+    n, R = 20, 5
+    F = orc.decompose_rotation2(rng.random_smooth_filter(R), R, R, 12, 16, 32, R)
+    H = rng.random_field(n, n, True)
+    T = rng.random_rotation_field(n, n)
+    for mode, fn in ((0, orc.xcorr_fast), (1, orc.xconv_fast)):
+        out, ops = res[f"rot{mode}"]
+        assert ops == 13 and orc.rel_l2(out, fn(H, 0, T, F)[0]) < 1e-12
+    Fs = orc.decompose_scale2(rng.annular_filter(R), R, R, 8, 48, 32, 1.0, R)
+    S = rng.random_scale_field(n, n)
+    for mode, fn in ((0, orc.xcorr_fast), (1, orc.xconv_fast)):
+        out, ops = res[f"scale{mode}"]
+        assert ops == 9 and orc.rel_l2(out, fn(H, 1, S, Fs)[0]) < 1e-12
+    out, ops, cl = res["smooth"]
+    ref, rops, rcl = orc.smooth_adaptive(H.real.copy(), 1, S, Fs)
+    assert ops == rops and cl == rcl and orc.rel_l2(out, ref) < 1e-12
