@@ -139,11 +139,12 @@ def config3(n: int = 4096, n_templates: int = 3, seed: int = 0) -> Workload:
     img = rng.standard_normal((n, n))
     tpl = smooth_template(64, rng)
     truth = []
-    margin = 80
+    margin = min(80, n // 4)
+    sep = min(160, n // 2)
     for _ in range(n_templates):
         while True:
             cx, cy = rng.uniform(margin, n - margin, 2)
-            if all(math.hypot(cx - a, cy - b) > 160 for a, b, _ in truth):
+            if all(math.hypot(cx - a, cy - b) > sep for a, b, _ in truth):
                 break
         ang = rng.uniform(0, 2 * math.pi)
         paste_rotated(img, 4.0 * tpl, cx, cy, ang)
