@@ -388,13 +388,26 @@ struct FastFft {
   static constexpr int kLast = RL;
   static constexpr int NS1 = R0;                    // Ns of the middle pass
   static constexpr int NSL = R1 > 1 ? R0 * R1 : R0;  // Ns of the last pass
-  static constexpr int TWL = R1 > 1 ? (R1 - 1) * R0 : 0;  // twiddle offset, last pass
   static_assert(R0 * R1 * RL == L_, "bad fast plan");
 
+  // compact twiddle tables (fft_plan.cpp finalize_plan, fast): per pass,
+  // (A-1 + NA-1) entry rows of Ns values, kept in shared memory
+  template <int R>
+  __host__ __device__ static constexpr int tw_rows() {
+    return (tw_split(R) - 1) + ((R + tw_split(R) - 1) / tw_split(R) - 1);
+  }
+  static constexpr int TWM = R1 > 1 ? tw_rows<R1>() * NS1 : 0;  // mid-pass entries
+  static constexpr int TWN = TWM + tw_rows<RL>() * NSL;          // total entries
+  static constexpr size_t kTwBytes = size_t(TWN) * sizeof(float2);
+
+  // cooperative copy of the table into smem (call once, then __syncthreads)
+  __device__ __forceinline__ static void load_twiddles(float2* sm_tw, const float2* gtw) {
+    for (int i = threadIdx.x; i < TWN; i += blockDim.x) sm_tw[i] = __ldg(gtw + i);
+  }
+
   template <int R, int NS, int TWO>
-  __device__ __forceinline__ static void load_tw(const float2* __restrict__ twt,
-                                                 const float2* src, int j, int jm,
-                                                 float2* v) {
+  __device__ __forceinline__ static void load_tw(const float2* twt, const float2* src, int j,
+                                                 int jm, float2* v) {
     constexpr int nb = L / R;
     constexpr int A = tw_split(R);
     constexpr int NA = (R + A - 1) / A;
@@ -405,9 +418,9 @@ struct FastFft {
     lo[0] = make_float2(1.f, 0.f);
     hi[0] = make_float2(1.f, 0.f);
 #pragma unroll
-    for (int b = 1; b < A; ++b) lo[b] = __ldg(tw + (b - 1) * NS);
+    for (int b = 1; b < A; ++b) lo[b] = tw[(b - 1) * NS];
 #pragma unroll
-    for (int a = 1; a < NA; ++a) hi[a] = __ldg(tw + (A * a - 1) * NS);
+    for (int a = 1; a < NA; ++a) hi[a] = tw[(A - 1 + a - 1) * NS];
 #pragma unroll
     for (int r = 1; r < R; ++r) {
       const int a = r / A, b = r % A;
@@ -431,7 +444,7 @@ struct FastFft {
     }
   }
 
-  __device__ __forceinline__ static void mid(const FftPlanD& p, float2* W) {
+  __device__ __forceinline__ static void mid(const float2* twt, float2* W) {
     if constexpr (R1 > 1) {
       constexpr int nb = L / R1;
       const int w = threadIdx.x;
@@ -442,7 +455,7 @@ struct FastFft {
         g = w & 1;
         j = w >> 1;
         jm = j % NS1;
-        load_tw<R1, NS1, 0>(p.tw, W + g * Lp, j, jm, v);
+        load_tw<R1, NS1, 0>(twt, W + g * Lp, j, jm, v);
         Dft<R1>::run(v);
       }
       __syncthreads();
@@ -457,13 +470,13 @@ struct FastFft {
   }
 
   template <class Store>
-  __device__ __forceinline__ static void last(const FftPlanD& p, const float2* W, Store& store) {
+  __device__ __forceinline__ static void last(const float2* twt, const float2* W, Store& store) {
     constexpr int nb = L / RL;
     const int w = threadIdx.x;
     if (w < nb * kG) {
       const int g = w & 1, j = w >> 1;
       float2 v[RL];
-      load_tw<RL, NSL, TWL>(p.tw, W + g * Lp, j, j, v);
+      load_tw<RL, NSL, TWM>(twt, W + g * Lp, j, j, v);
       Dft<RL>::run(v);
 #pragma unroll
       for (int r = 0; r < RL; ++r) store(j + r * nb, g, r, v[Dft<RL>::pos(r)]);

@@ -33,13 +33,24 @@ bool finalize_plan(int L, const std::vector<int>& order, int nt, bool fast, FftP
     p.d.ns[q] = ns;
     p.d.magic[q] = ns > 1 ? unsigned((0x100000000ull + ns - 1) / ns) : 0u;
     p.d.tw_off[q] = int(p.tw_host.size());
-    if (q > 0) {
+    auto tw = [&](int r, int jm) {
+      const long long e = (long long)jm * r % ((long long)ns * R);
+      const double a = -2.0 * M_PI * double(e) / double((long long)ns * R);
+      return make_float2(float(std::cos(a)), float(std::sin(a)));
+    };
+    if (q > 0 && !fast) {
       for (int r = 1; r < R; ++r)
-        for (int jm = 0; jm < ns; ++jm) {
-          const long long e = (long long)jm * r % ((long long)ns * R);
-          const double a = -2.0 * M_PI * double(e) / double((long long)ns * R);
-          p.tw_host.push_back(make_float2(float(std::cos(a)), float(std::sin(a))));
-        }
+        for (int jm = 0; jm < ns; ++jm) p.tw_host.push_back(tw(r, jm));
+    } else if (q > 0) {
+      // compact table of the fast path (FastFft::load_tw): only the factors
+      // W^{jm b} (b < A) and W^{jm A a} that the split product uses, entry-major
+      int A = 1;
+      while (A * A < R) ++A;
+      const int NA = (R + A - 1) / A;
+      for (int b = 1; b < A; ++b)
+        for (int jm = 0; jm < ns; ++jm) p.tw_host.push_back(tw(b, jm));
+      for (int a = 1; a < NA; ++a)
+        for (int jm = 0; jm < ns; ++jm) p.tw_host.push_back(tw(A * a, jm));
     }
     ns *= R;
   }

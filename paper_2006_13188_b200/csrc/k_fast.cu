@@ -44,6 +44,8 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
   float2* Hc = reinterpret_cast<float2*>(smraw);
   float2* S = Hc + 2 * L;
   float2* W = S + 2 * L;
+  float2* TW = W + 2 * FF::Lp;
+  FF::load_twiddles(TW, p.tw);
   const int c = blockIdx.x, tid = threadIdx.x;
   const size_t colb = size_t(c) * L * 2;
   const unsigned bytes = unsigned(L) * 2u * unsigned(sizeof(float2));
@@ -72,14 +74,14 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
       mbar_expect_tx(&bar, bytes);
       bulk_copy(S, Fh + size_t(bl.spec[bi + 1]) * sstride + colb, bytes, &bar);
     }
-    FF::mid(p, W);
+    FF::mid(TW, W);
     float2* out = T2 + size_t(bi) * plane;
     const int pw = opaque(g.Pw), off = opaque(g.off);
     auto store = [&](int k, int gi, int, float2 v) {
       const int y = k - off;
       if (y >= 0 && y < g.H) out[(size_t(y >> 1) * pw + 2 * c + gi) * 2 + (y & 1)] = c_conj(v);
     };
-    FF::last(p, W, store);
+    FF::last(TW, W, store);
     __syncthreads();
   }
 }
@@ -97,6 +99,8 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
   float2* S = reinterpret_cast<float2*>(smraw);
   float2* W = S + 2 * L;
   float2* Z = W + 2 * FF::Lp;
+  float2* TW = Z + 2 * zs;
+  FF::load_twiddles(TW, p.tw);
   const int b = blockIdx.x, tid = threadIdx.x;
   const unsigned bytes = unsigned(L) * 2u * unsigned(sizeof(float2));
   const size_t plane = size_t(g.H2) * g.Pw;
@@ -129,7 +133,7 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
       mbar_expect_tx(&bar, bytes);
       bulk_copy(S, T2 + size_t(bi + 1) * plane + rowb, bytes, &bar);
     }
-    FF::mid(p, W);
+    FF::mid(TW, W);
     const int dk = bi == 0 ? 0 : bl.k[bi - 1] - bl.k[bi];
     const int zso = opaque(zs), off = opaque(g.off);
     auto store = [&](int k, int gi, int r, float2 v) {
@@ -138,7 +142,7 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
       const float2 z = (x >= 0 && x < g.W) ? Z[gi * zso + x] : make_float2(1.f, 0.f);
       acc[r] = c_add(cpow_step(acc[r], z, dk), val);
     };
-    FF::last(p, W, store);
+    FF::last(TW, W, store);
     __syncthreads();
   }
   // out = z^{k_last} * acc (+ conj(dc) H for the scale group)
@@ -167,6 +171,8 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
   float2* W = reinterpret_cast<float2*>(smraw);
   float2* CUR = W + 2 * FF::Lp;
   float2* MUL = CUR + 2 * xs_;
+  float2* TW = MUL + 2 * xs_;
+  FF::load_twiddles(TW, p.tw);
   const int b = blockIdx.x, tid = threadIdx.x;
   const size_t plane = size_t(g.Hx2) * g.Pw;
   const int k0 = bl.k[0];
@@ -198,13 +204,13 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
         CUR[gi * xs_ + xp] = cpow_step(CUR[gi * xs_ + xp], MUL[gi * xs_ + xp], dk);
       }
     }
-    FF::mid(p, W);
+    FF::mid(TW, W);
     float2* dst = T1 + size_t(bi) * plane;
     const int hx2 = opaque(g.Hx2);
     auto store = [&](int k, int gi, int, float2 v) {
       dst[(size_t(k >> 1) * hx2 + 2 * b + gi) * 2 + (k & 1)] = v;
     };
-    FF::last(p, W, store);
+    FF::last(TW, W, store);
     __syncthreads();
   }
 }
@@ -222,6 +228,8 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
   float2* S = reinterpret_cast<float2*>(smraw);
   float2* SF = S + 2 * sl;
   float2* W = SF + 2 * L;
+  float2* TW = W + 2 * FF::Lp;
+  FF::load_twiddles(TW, p.tw);
   const int c = blockIdx.x, tid = threadIdx.x;
   const size_t plane1 = size_t(g.Hx2) * g.Pw;
   const size_t col1 = size_t(c) * g.Hx2 * 2, colF = size_t(c) * L * 2;
@@ -255,14 +263,14 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
       mbar_expect_tx(&barS, bytesS);
       bulk_copy(S, T1 + size_t(bi + 1) * plane1 + col1, bytesS, &barS);
     }
-    FF::mid(p, W);
+    FF::mid(TW, W);
     mbar_wait(&barF, phF);
     phF ^= 1;
     const int two = opaque(2);
     auto store = [&](int k, int gi, int r, float2 v) {
       acc[r] = c_add(acc[r], c_mul(v, SF[k * two + gi]));
     };
-    FF::last(p, W, store);
+    FF::last(TW, W, store);
     __syncthreads();
     if (tid == 0 && bi + 1 < bl.n) {
       fence_proxy_async();
@@ -283,12 +291,12 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
   auto load = [&](int n, int gi) -> float2 { return S[n * 2 + gi]; };
   FF::first(p, W, load);
   __syncthreads();
-  FF::mid(p, W);
+  FF::mid(TW, W);
   auto store = [&](int k, int gi, int, float2 v) {
     const int y = k - g.off;
     if (y >= 0 && y < g.H) T2[(size_t(y >> 1) * g.Pw + 2 * c + gi) * 2 + (y & 1)] = c_conj(v);
   };
-  FF::last(p, W, store);
+  FF::last(TW, W, store);
 }
 
 constexpr size_t kSmemLimit = 232448;  // 227 KB opt-in per CTA on sm_100
@@ -297,12 +305,13 @@ constexpr size_t kSmemLimit = 232448;  // 227 KB opt-in per CTA on sm_100
 
 // smem needs of each fast kernel (0 if the stage has no fast variant)
 size_t fast_smem(int stage, const FftPlan& pl, const Geo& g) {
-  const size_t f2 = sizeof(float2), Wb = pl.smem_bytes();
+  const size_t f2 = sizeof(float2);
+  const size_t Wb = pl.smem_bytes() + pl.tw_host.size() * f2;  // W + smem twiddles
   const size_t L = pl.d.L;
   size_t s = 0;
   switch (stage) {
     case 0: s = 4 * L * f2 + Wb; break;                                   // I1
-    case 1: s = 2 * L * f2 + Wb + 2 * (g.W + 16) * f2; break;            // I2
+    case 1: s = 2 * L * f2 + Wb + 2 * (g.W + 16) * f2; break;            // I2 (+ Z)
     case 2: s = Wb + 4 * (g.Wx + 16) * f2; break;                         // S1
     case 3: s = 2 * (g.Hx2 > int(L) ? g.Hx2 : L) * f2 + 2 * L * f2 + Wb; break;  // S2
   }
