@@ -935,10 +935,18 @@ int xc_anglemax(xc_context ctx, xc_filter f, const xc_image_desc* d, const void*
       stage(c, "F1_rows_fwd", [&] { xcb::launch_rows_fwd(*c.prow, c.g, s.sig, T1, c.st, c.lc); });
       stage(c, "F2_cols_fwd", [&] { xcb::launch_cols_fwd(*c.pcol, c.g, T1, Hh, c.st, c.lc); });
       stage(c, "I1_cols_inv_corr", [&] {
-        xcb::launch_cols_inv_corr(*c.pcol, c.g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);
+        if (c.fcol && xcb::fast_smem(0, *c.fcol, c.g))
+          xcb::launch_cols_inv_corr_fast(*c.fcol, c.g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st,
+                                         c.lc);
+        else
+          xcb::launch_cols_inv_corr(*c.pcol, c.g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);
       });
-      stage(c, "I2_rows_inv_planes",
-            [&] { xcb::launch_rows_inv_planes(*c.prow, c.g, T2, c.bands.n, planes, c.st, c.lc); });
+      stage(c, "I2_rows_inv_planes", [&] {
+        if (c.frow && xcb::fast_smem(4, *c.frow, c.g))
+          xcb::launch_rows_inv_planes_fast(*c.frow, c.g, T2, c.bands.n, planes, c.st, c.lc);
+        else
+          xcb::launch_rows_inv_planes(*c.prow, c.g, T2, c.bands.n, planes, c.st, c.lc);
+      });
       char* dsc = d->memory == XC_DEVICE ? static_cast<char*>(score) + size_t(img) * npix * os
                                          : ctx->buf<char>("score_stage", npix * os);
       int* darg = nullptr;

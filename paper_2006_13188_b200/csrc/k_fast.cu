@@ -9,6 +9,8 @@
 //   sum_k z^k G_k = z^{k_min} * (((G_{k0} z^{k0-k1} + G_{k1}) z^{k1-k2} + ...)
 // so each band costs one complex FMA per pixel instead of a sincos
 // (z = e^{i phi(p)}; engine.hpp:312-317 / 353-358 for the reference steering).
+#include <algorithm>
+
 #include "stages_common.cuh"
 #include "tma.cuh"
 
@@ -158,6 +160,56 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
       const float2 v = c_mul(acc[r], steer(klast, base[i], 1.f));
       OutOps<TO>::put(out, i, v, accumulate != 0, dc_term(dcs, i, dcr, dci));
     }
+  }
+}
+
+// ------------------------------------------------------------- planes fast
+// Angle-max front end: per band, row IFFT of T2_b, crop, store the band plane
+// G_b (k_anglemax_* then reads all bands per pixel).
+template <class FF>
+__global__ void __launch_bounds__(kFastMaxThreads, 1)
+    k_rows_inv_planes_fast(FftPlanD p, Geo g, const float2* __restrict__ T2, int nbands,
+                           float2* __restrict__ planes, float scale) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ __align__(8) uint64_t bar;
+  constexpr int L = FF::L;  // = Pw
+  float2* S = reinterpret_cast<float2*>(smraw);
+  float2* W = S + 2 * L;
+  float2* TW = W + 2 * FF::Lp;
+  FF::load_twiddles(TW, p.tw);
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const unsigned bytes = unsigned(L) * 2u * unsigned(sizeof(float2));
+  const size_t plane = size_t(g.H2) * g.Pw;
+  const size_t rowb = size_t(b) * L * 2;
+  const size_t npix = size_t(g.H) * g.W;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(&bar, bytes);
+    bulk_copy(S, T2 + rowb, bytes, &bar);
+  }
+  __syncthreads();
+  unsigned phase = 0;
+  for (int bi = 0; bi < nbands; ++bi) {
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    auto load = [&](int n, int gi) -> float2 { return c_conj(S[n * 2 + gi]); };
+    FF::first(p, W, load);
+    __syncthreads();
+    if (tid == 0 && bi + 1 < nbands) {
+      fence_proxy_async();
+      mbar_expect_tx(&bar, bytes);
+      bulk_copy(S, T2 + size_t(bi + 1) * plane + rowb, bytes, &bar);
+    }
+    FF::mid(TW, W);
+    float2* dst = planes + size_t(bi) * npix;
+    const int off = opaque(g.off), wd = opaque(g.W);
+    auto store = [&](int k, int gi, int, float2 v) {
+      const int x = k - off, y = 2 * b + gi;
+      if (x >= 0 && x < wd && y < g.H) dst[size_t(y) * wd + x] = c_scale(c_conj(v), scale);
+    };
+    FF::last(TW, W, store);
+    __syncthreads();
   }
 }
 
@@ -314,6 +366,7 @@ size_t fast_smem(int stage, const FftPlan& pl, const Geo& g) {
     case 1: s = 2 * L * f2 + Wb + 2 * (g.W + 16) * f2; break;            // I2 (+ Z)
     case 2: s = Wb + 4 * (g.Wx + 16) * f2; break;                         // S1
     case 3: s = 2 * (g.Hx2 > int(L) ? g.Hx2 : L) * f2 + 2 * L * f2 + Wb; break;  // S2
+    case 4: s = 2 * L * f2 + Wb; break;                                   // planes
   }
   return s <= kSmemLimit ? s : 0;
 }
@@ -358,6 +411,19 @@ void launch_rows_inv_steer_fast(const FftPlan& pr, const Geo& g, const float2* T
     switch (pr.d.L) { XCB_FAST_TABLE(XCB_FAST_CASE) }
 #undef XCB_FAST_BODY
   }
+  ++lc.n;
+}
+
+void launch_rows_inv_planes_fast(const FftPlan& pr, const Geo& g, const float2* T2,
+                                 int nbands, float2* planes, cudaStream_t st,
+                                 LaunchCounter& lc) {
+  const size_t sm = fast_smem(4, pr, g);
+  const float scale = float(1.0 / (double(g.Ph) * double(g.Pw)));
+#define XCB_FAST_BODY                                                                      \
+  set_smem(k_rows_inv_planes_fast<FF>, sm);                                                \
+  k_rows_inv_planes_fast<FF><<<g.H2 / 2, pr.d.nt, sm, st>>>(pr.d, g, T2, nbands, planes, scale)
+  switch (pr.d.L) { XCB_FAST_TABLE(XCB_FAST_CASE) }
+#undef XCB_FAST_BODY
   ++lc.n;
 }
 

@@ -114,7 +114,8 @@ float2* upload_twiddles(const FftPlan& p);
 namespace xcb {
 // Fast band-loop variants (k_fast.cu): plans from make_fast_plan.  fast_smem
 // returns the dynamic smem a stage needs, or 0 if it does not fit (stage 0 =
-// I1, 1 = I2, 2 = S1, 3 = S2); callers fall back to the generic kernels.
+// I1, 1 = I2, 2 = S1, 3 = S2, 4 = planes); callers fall back to the generic
+// kernels.
 size_t fast_smem(int stage, const FftPlan& pl, const Geo& g);
 void launch_cols_inv_corr_fast(const FftPlan& pc, const Geo& g, const float2* Hhat,
                                const float2* Fhat, size_t sstride, const Bands& b, float2* T2,
@@ -123,6 +124,9 @@ void launch_rows_inv_steer_fast(const FftPlan& pr, const Geo& g, const float2* T
                                 const Bands& b, const double* base, int out_kind, void* out,
                                 int accumulate, const SigSrc& dcs, double dcr, double dci,
                                 cudaStream_t st, LaunchCounter& lc);
+void launch_rows_inv_planes_fast(const FftPlan& pr, const Geo& g, const float2* T2,
+                                 int nbands, float2* planes, cudaStream_t st,
+                                 LaunchCounter& lc);
 void launch_rows_fwd_premul_fast(const FftPlan& pr, const Geo& g, const SigSrc& s,
                                  const double* base, const Bands& b, float2* T1,
                                  cudaStream_t st, LaunchCounter& lc);
