@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -536,6 +537,15 @@ void prep(Call& c, const Staged& s, bool want_wgt, double** base_out, float** wg
   if (wgt_out) *wgt_out = wgt;
 }
 
+// XCB_PAIR=0 selects the previous (fast) band-loop kernels, for A/B timing
+bool use_pair() {
+  static const bool on = [] {
+    const char* e = std::getenv("XCB_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void run_gather(Call& c, const xcb::SigSrc& sig, const double* base, void* out, int out_kind,
                 bool accumulate, bool dc) {
   const xcb::Geo& g = c.g;
@@ -544,7 +554,11 @@ void run_gather(Call& c, const xcb::SigSrc& sig, const double* base, void* out, 
   float2* T2 = c.ctx->buf<float2>("T2", size_t(c.bands.n) * g.H2 * g.Pw);
   stage(c, "F1_rows_fwd", [&] { xcb::launch_rows_fwd(*c.prow, g, sig, T1, c.st, c.lc); });
   stage(c, "F2_cols_fwd", [&] { xcb::launch_cols_fwd(*c.pcol, g, T1, Hh, c.st, c.lc); });
-  if (c.fcol && xcb::fast_smem(0, *c.fcol, g)) {
+  if (use_pair() && xcb::pair_smem(0, g.Ph, g)) {
+    stage(c, "I1_cols_inv_corr", [&] {
+      xcb::launch_cols_inv_corr_pair(g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);
+    });
+  } else if (c.fcol && xcb::fast_smem(0, *c.fcol, g)) {
     stage(c, "I1_cols_inv_corr", [&] {
       xcb::launch_cols_inv_corr_fast(*c.fcol, g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);
     });
@@ -554,7 +568,12 @@ void run_gather(Call& c, const xcb::SigSrc& sig, const double* base, void* out, 
     });
   }
   const cplx dcv = dc ? std::conj(xcb::inner_dc_value(c.f->hf)) : cplx(0);  // engine.hpp:323
-  if (c.frow && xcb::fast_smem(1, *c.frow, g)) {
+  if (use_pair() && xcb::pair_smem(1, g.Pw, g)) {
+    stage(c, "I2_rows_inv_steer", [&] {
+      xcb::launch_rows_inv_steer_pair(g, T2, c.bands, base, out_kind, out, accumulate ? 1 : 0,
+                                      sig, dcv.real(), dcv.imag(), c.st, c.lc);
+    });
+  } else if (c.frow && xcb::fast_smem(1, *c.frow, g)) {
     stage(c, "I2_rows_inv_steer", [&] {
       xcb::launch_rows_inv_steer_fast(*c.frow, g, T2, c.bands, base, out_kind, out,
                                       accumulate ? 1 : 0, sig, dcv.real(), dcv.imag(), c.st, c.lc);
@@ -935,7 +954,9 @@ int xc_anglemax(xc_context ctx, xc_filter f, const xc_image_desc* d, const void*
       stage(c, "F1_rows_fwd", [&] { xcb::launch_rows_fwd(*c.prow, c.g, s.sig, T1, c.st, c.lc); });
       stage(c, "F2_cols_fwd", [&] { xcb::launch_cols_fwd(*c.pcol, c.g, T1, Hh, c.st, c.lc); });
       stage(c, "I1_cols_inv_corr", [&] {
-        if (c.fcol && xcb::fast_smem(0, *c.fcol, c.g))
+        if (use_pair() && xcb::pair_smem(0, c.g.Ph, c.g))
+          xcb::launch_cols_inv_corr_pair(c.g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);
+        else if (c.fcol && xcb::fast_smem(0, *c.fcol, c.g))
           xcb::launch_cols_inv_corr_fast(*c.fcol, c.g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st,
                                          c.lc);
         else

@@ -75,6 +75,27 @@ __host__ __device__ constexpr int first_factor(int R) {
                                    : (R % 5 == 0 && R > 5) ? 5 : R;
 }
 
+// x * e^{-2 pi i e / R} with the trivial angles (multiples of pi/4) done by
+// swaps / negations / one scale instead of a full complex multiply
+template <int R>
+__device__ __forceinline__ float2 tw_apply(float2 x, int e, const CTw<R>& tw) {
+  if (e == 0) return x;
+  if ((4 * e) % R == 0) {
+    const int q = (4 * e) / R;  // e^{-i pi q / 2}
+    return q == 1 ? make_float2(x.y, -x.x) : q == 2 ? make_float2(-x.x, -x.y)
+                                                     : make_float2(-x.y, x.x);
+  }
+  if ((8 * e) % R == 0) {
+    constexpr float h = 0.70710678118654752440f;
+    const int q = (8 * e) / R;  // odd: e^{-i pi q / 4}
+    return q == 1 ? make_float2(h * (x.x + x.y), h * (x.y - x.x))
+         : q == 3 ? make_float2(h * (x.y - x.x), -h * (x.x + x.y))
+         : q == 5 ? make_float2(-h * (x.x + x.y), h * (x.x - x.y))
+                  : make_float2(h * (x.x - x.y), h * (x.x + x.y));
+  }
+  return c_mul(x, make_float2(tw.re[e], tw.im[e]));
+}
+
 // ---------------------------------------------------------------- codelets
 // Dft<R>::run(v) transforms v in place; output X[k] ends at v[Dft<R>::pos(k)]
 // (compile-time permutation), so composites need no second R-element array.
@@ -98,7 +119,7 @@ struct Dft {
       for (int k1 = 0; k1 < A; ++k1) {
         const int e = (n2 * k1) % R;
         const float2 x = a[Dft<A>::pos(k1)];
-        v[B * k1 + n2] = e == 0 ? x : c_mul(x, make_float2(tw.re[e], tw.im[e]));
+        v[B * k1 + n2] = tw_apply<R>(x, e, tw);
       }
     }
 #pragma unroll

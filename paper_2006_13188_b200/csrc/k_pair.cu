@@ -1,0 +1,617 @@
+// Pair-engine band-loop stages (fft_pair.cuh) for the lengths of
+// XCB_PAIR_TABLE: every thread owns both sequences of its butterflies (16-byte
+// accesses, shared twiddles), the passes are balanced (T = max L/Rq threads),
+// and the first pass reads its band input straight from global memory with
+// the next band's block prefetched into L2 (cp.async.bulk.prefetch).
+//   I1P  k_cols_inv_corr_pair : per band, column IFFT of conj(H^) F^_k (the
+//        spectral multiply of fft.hpp:94-97 fused into pass 0; conj(H^) stays
+//        in shared memory for the whole band loop) -> T2_k
+//   I2P  k_rows_inv_steer_pair: per band, row IFFT of T2_k, crop, Horner
+//        steering over the bands sorted by descending k (engine.hpp:312-317),
+//        the band sum held in registers; out written once.
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <vector>
+#include <cmath>
+
+#include "fft_pair.cuh"
+#include "stages_common.cuh"
+#include "tma.cuh"
+#include "tmem.cuh"
+
+namespace xcb {
+namespace {
+
+// ------------------------------------------------------------------ I1P
+template <class PF>
+__global__ void __launch_bounds__(PF::T, 1)
+    k_cols_inv_corr_pair(Geo g, const float4* __restrict__ Hh, const float4* __restrict__ Fh,
+                         size_t sstride4, Bands bl, float2* __restrict__ T2,
+                         const float2* __restrict__ twm, const float2* __restrict__ twl) {
+  constexpr int L = PF::L;  // = Ph
+  extern __shared__ __align__(16) float4 smp[];
+  float4* HC = smp;     // conj(H^) of the column pair, natural order
+  float4* W0 = HC + L;
+  float4* W1 = W0 + PF::LP;
+  float2* TWs = reinterpret_cast<float2*>(W1 + PF::LP);
+  const int c = blockIdx.x, t = threadIdx.x;
+  const float4* hcol = Hh + size_t(c) * L;
+  for (int i = t; i < L; i += blockDim.x) {
+    const float4 h = hcol[i];
+    HC[i] = make_float4(h.x, -h.y, h.z, -h.w);
+  }
+  for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
+  typename PF::LastTw tl;
+  PF::load_last_tw(twl, t, tl);
+  __syncthreads();
+  const size_t plane = size_t(g.H2) * g.Pw;  // float2 per T2 band plane
+  constexpr unsigned kBytes = unsigned(L * sizeof(float4));
+  auto fsrc = [&](int bi) { return Fh + size_t(bl.spec[bi]) * sstride4 + size_t(c) * L; };
+  __shared__ __align__(8) uint64_t bar;
+  if (t == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(&bar, kBytes);
+    bulk_copy(W0, fsrc(0), kBytes, &bar);
+    if (bl.n > 1) prefetch_l2(fsrc(1), kBytes);
+  }
+  __syncthreads();
+  unsigned phase = 0;
+  for (int bi = 0; bi < bl.n; ++bi) {
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    // conj(H^ conj(F^)) = conj(H^) F^ : inverse via conj-FFT-conj
+    auto load = [&](int n) -> float4 {
+      const float4 h = HC[n], f = W0[n];
+      return make_float4(h.x * f.x - h.y * f.y, h.x * f.y + h.y * f.x,
+                         h.z * f.z - h.w * f.w, h.z * f.w + h.w * f.z);
+    };
+    {
+      typename PF::P0Regs v;
+      PF::pass0_compute(load, v);
+      __syncthreads();
+      PF::pass0_store(W0, v);
+    }
+    __syncthreads();
+    PF::pass1(W0, W1, TWs);
+    __syncthreads();
+    if (t == 0 && bi + 1 < bl.n) {
+      fence_proxy_async();
+      mbar_expect_tx(&bar, kBytes);
+      bulk_copy(W0, fsrc(bi + 1), kBytes, &bar);
+      if (bi + 2 < bl.n) prefetch_l2(fsrc(bi + 2), kBytes);
+    }
+    float2* out = T2 + size_t(bi) * plane + 4 * opaque_i(c);
+    const int pw = g.Pw, off = opaque_i(g.off), H = g.H;
+    auto store = [&](int k, int, float2 a, float2 b) {
+      const int y = k - off;
+      if (y >= 0 && y < H) {
+        float2* o = out + size_t(y >> 1) * (2 * pw) + (y & 1);
+        o[0] = c_conj(a);
+        o[2] = c_conj(b);
+      }
+    };
+    PF::pass2(W1, tl, store);
+  }
+}
+
+// ------------------------------------------------------------------ I2P
+// Band accumulators live in TMEM (4 columns = both rows' complex sum per
+// output r; 4 * R2 columns per thread), which keeps the pass registers free.
+template <class PF, class TO>
+__global__ void __launch_bounds__(PF::T, 1)
+    k_rows_inv_steer_pair(Geo g, const float4* __restrict__ T2, Bands bl,
+                          const double* __restrict__ base, TO* __restrict__ out, int accumulate,
+                          SigSrc dcs, double dcr, double dci, float scale,
+                          const float2* __restrict__ twm, const float2* __restrict__ twl) {
+  constexpr int L = PF::L;  // = Pw
+  constexpr int R2 = PF::R2;
+  static_assert(PF::NB2 == PF::T, "pass 2 must use every thread (warp-collective TMEM ops)");
+  extern __shared__ __align__(16) float4 smp[];
+  float4* W0 = smp;
+  float4* W1 = W0 + PF::LP;
+  float4* Z = W1 + PF::LP;  // e^{i phi} of both rows at each output x (g.W entries)
+  float2* TWs = reinterpret_cast<float2*>(Z + g.W);
+  __shared__ uint32_t tbase;
+  const int b = blockIdx.x, t = threadIdx.x;
+  if (t < 32) tmem_alloc(&tbase, 512);
+  const int y0 = 2 * b, y1 = 2 * b + 1;
+  for (int x = t; x < g.W; x += blockDim.x) {
+    const float2 z0 = steer(1, base[size_t(y0) * g.W + x], 1.f);
+    const float2 z1 = y1 < g.H ? steer(1, base[size_t(y1) * g.W + x], 1.f) : make_float2(1.f, 0.f);
+    Z[x] = make_float4(z0.x, z0.y, z1.x, z1.y);
+  }
+  for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
+  typename PF::LastTw tl;
+  PF::load_last_tw(twl, t, tl);
+  const size_t plane4 = size_t(g.H2 / 2) * g.Pw;  // float4 per band plane
+  const float4* rowp = T2 + size_t(b) * g.Pw;
+  const int off = g.off, W = g.W;
+  constexpr unsigned kBytes = unsigned(L * sizeof(float4));
+  __shared__ __align__(8) uint64_t bar;
+  if (t == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(&bar, kBytes);
+    bulk_copy(W0, rowp, kBytes, &bar);
+    if (bl.n > 1) prefetch_l2(rowp + plane4, kBytes);
+  }
+  tmem_fence_before_sync();
+  __syncthreads();
+  tmem_fence_after_sync();
+  // this thread's accumulator columns: 4 * R2 per thread, warps of a lane
+  // quadrant side by side
+  const uint32_t tacc = tmem_warp_base(tbase) + uint32_t((t >> 7) * 4 * R2);
+  unsigned phase = 0;
+  for (int bi = 0; bi < bl.n; ++bi) {
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    auto load = [&](int n) -> float4 {
+      const float4 v = W0[n];
+      return make_float4(v.x, -v.y, v.z, -v.w);
+    };
+    {
+      typename PF::P0Regs v;
+      PF::pass0_compute(load, v);
+      __syncthreads();
+      PF::pass0_store(W0, v);
+    }
+    __syncthreads();
+    PF::pass1(W0, W1, TWs);
+    __syncthreads();
+    if (t == 0 && bi + 1 < bl.n) {
+      fence_proxy_async();
+      mbar_expect_tx(&bar, kBytes);
+      bulk_copy(W0, rowp + size_t(bi + 1) * plane4, kBytes, &bar);
+      if (bi + 2 < bl.n) prefetch_l2(rowp + size_t(bi + 2) * plane4, kBytes);
+    }
+    const int dk = bi == 0 ? 0 : bl.k[bi - 1] - bl.k[bi];
+    const int tt = opaque_i(t);
+    // acc = acc z^dk + conj(v)  (Horner over descending k; IFFT = conj FFT conj)
+    auto horner = [&](float2 (&a)[R2], float2 (&c)[R2]) {
+      constexpr int C = 5;  // outputs per TMEM round trip
+#pragma unroll
+      for (int r0 = 0; r0 < R2; r0 += C) {
+        float4 acc[C];
+        if (bi > 0) {
+#pragma unroll
+          for (int i = 0; i < C; ++i)
+            if (r0 + i < R2) acc[i] = tmem_ld4(tacc + 4 * (r0 + i));
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < C; ++i)
+            if (r0 + i < R2) tmem_dep(acc[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < C; ++i) {
+          const int r = r0 + i;
+          if (r >= R2) break;
+          const float2 va = a[Dft<R2>::pos(r)], vc = c[Dft<R2>::pos(r)];
+          if (bi == 0) {
+            acc[i] = make_float4(va.x, -va.y, vc.x, -vc.y);
+            continue;
+          }
+          const int x = tt + r * PF::NB2 - off;
+          const float4 z = (x >= 0 && x < W) ? Z[x] : make_float4(1.f, 0.f, 1.f, 0.f);
+          float2 pa = make_float2(acc[i].x, acc[i].y), pc = make_float2(acc[i].z, acc[i].w);
+          if (dk == 1) {
+            pa = make_float2(fmaf(pa.x, z.x, fmaf(-pa.y, z.y, va.x)),
+                             fmaf(pa.x, z.y, fmaf(pa.y, z.x, -va.y)));
+            pc = make_float2(fmaf(pc.x, z.z, fmaf(-pc.y, z.w, vc.x)),
+                             fmaf(pc.x, z.w, fmaf(pc.y, z.z, -vc.y)));
+          } else {
+            float2 za = make_float2(z.x, z.y), zc = make_float2(z.z, z.w);
+            int d = dk;
+            if (d < 0) {
+              za = c_conj(za);
+              zc = c_conj(zc);
+              d = -d;
+            }
+            for (int s = 0; s < d; ++s) {
+              pa = c_mul(pa, za);
+              pc = c_mul(pc, zc);
+            }
+            pa = c_add(pa, c_conj(va));
+            pc = c_add(pc, c_conj(vc));
+          }
+          acc[i] = make_float4(pa.x, pa.y, pc.x, pc.y);
+        }
+#pragma unroll
+        for (int i = 0; i < C; ++i)
+          if (r0 + i < R2) tmem_st4(tacc + 4 * (r0 + i), acc[i]);
+      }
+      tmem_wait_st();
+    };
+    PF::pass2_all(W1, tl, horner);
+  }
+  // out = scale * z^{k_last} * acc (+ conj(dc) H for the scale group)
+  {
+    const int klast = bl.k[bl.n - 1];
+#pragma unroll
+    for (int r = 0; r < R2; ++r) {
+      float4 acc = tmem_ld4(tacc + 4 * r);
+      tmem_wait_ld();
+      tmem_dep(acc);
+      const int x = t + r * PF::NB2 - off;
+      if (x < 0 || x >= W) continue;
+      {
+        const size_t i = size_t(y0) * W + x;
+        const float2 v =
+            c_scale(c_mul(make_float2(acc.x, acc.y), steer(klast, base[i], 1.f)), scale);
+        OutOps<TO>::put(out, i, v, accumulate != 0, dc_term(dcs, i, dcr, dci));
+      }
+      if (y1 < g.H) {
+        const size_t i = size_t(y1) * W + x;
+        const float2 v =
+            c_scale(c_mul(make_float2(acc.z, acc.w), steer(klast, base[i], 1.f)), scale);
+        OutOps<TO>::put(out, i, v, accumulate != 0, dc_term(dcs, i, dcr, dci));
+      }
+    }
+  }
+  tmem_fence_before_sync();
+  __syncthreads();
+  if (t < 32) {
+    tmem_fence_after_sync();
+    tmem_dealloc(tbase, 512);
+  }
+}
+
+// ------------------------------------------------------------------ I1 (interleaved)
+template <class PF>
+__global__ void __launch_bounds__(PF::T, 1)
+    k_cols_inv_corr_ilv(Geo g, const float4* __restrict__ Hh, const float4* __restrict__ Fh,
+                        size_t sstride4, Bands bl, float2* __restrict__ T2,
+                        const float2* __restrict__ twm, const float2* __restrict__ twl) {
+  constexpr int L = PF::L;  // = Ph
+  extern __shared__ __align__(16) float4 smp[];
+  float4* HC4 = smp;  // conj(H^) of the column pair, natural order
+  float4* W04 = HC4 + L;
+  float4* W14 = W04 + PF::LP;
+  float2* TWs = reinterpret_cast<float2*>(W14 + PF::LP);
+  const float2* HC = reinterpret_cast<const float2*>(HC4);
+  float2* W0 = reinterpret_cast<float2*>(W04);
+  float2* W1 = reinterpret_cast<float2*>(W14);
+  const int c = blockIdx.x, t = threadIdx.x;
+  const float4* hcol = Hh + size_t(c) * L;
+  for (int i = t; i < L; i += blockDim.x) {
+    const float4 h = hcol[i];
+    HC4[i] = make_float4(h.x, -h.y, h.z, -h.w);
+  }
+  for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
+  typename PF::LastTw tl;
+  PF::load_last_tw(twl, tl);
+  const size_t plane = size_t(g.H2) * g.Pw;  // float2 per T2 band plane
+  constexpr unsigned kBytes = unsigned(L * sizeof(float4));
+  auto fsrc = [&](int bi) { return Fh + size_t(bl.spec[bi]) * sstride4 + size_t(c) * L; };
+  __shared__ __align__(8) uint64_t bar;
+  if (t == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(&bar, kBytes);
+    bulk_copy(W04, fsrc(0), kBytes, &bar);
+    if (bl.n > 1) prefetch_l2(fsrc(1), kBytes);
+  }
+  __syncthreads();
+  unsigned phase = 0;
+  for (int bi = 0; bi < bl.n; ++bi) {
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    // conj(H^ conj(F^)) = conj(H^) F^ : inverse via conj-FFT-conj
+    auto load = [&](int n, int gi) -> float2 { return c_mul(HC[2 * n + gi], W0[2 * n + gi]); };
+    {
+      typename PF::P0Regs v;
+      PF::pass0_compute(load, v);
+      __syncthreads();
+      PF::pass0_store(W0, v);
+    }
+    __syncthreads();
+    PF::pass1(W0, W1, TWs);
+    __syncthreads();
+    if (t == 0 && bi + 1 < bl.n) {
+      fence_proxy_async();
+      mbar_expect_tx(&bar, kBytes);
+      bulk_copy(W04, fsrc(bi + 1), kBytes, &bar);
+      if (bi + 2 < bl.n) prefetch_l2(fsrc(bi + 2), kBytes);
+    }
+    const int tt = opaque_i(t), gi = tt & 1, j = tt >> 1;
+    // output y = j + r NB2 - off: NB2 is even, so y & 1 is fixed and y >> 1
+    // advances by NB2 / 2 rows of T2 per r; valid r form [rlo, rhi)
+    const int y0 = j - g.off;
+    const size_t rstride = size_t(PF::NB2 / 2) * 2 * g.Pw;  // float2 per r step
+    float2* o = T2 + size_t(bi) * plane + 2 * (2 * c + gi) +
+                (ptrdiff_t(y0 >> 1) * (2 * g.Pw) + (y0 & 1));
+    const int rlo = y0 >= 0 ? 0 : (-y0 + PF::NB2 - 1) / PF::NB2;
+    const int rhi = g.H - y0 <= 0 ? 0 : (g.H - y0 + PF::NB2 - 1) / PF::NB2;
+    auto store = [&](float2 (&a)[PF::R2]) {
+      if (j >= PF::NB2) return;
+#pragma unroll
+      for (int r = 0; r < PF::R2; ++r)
+        if (r >= rlo && r < rhi) o[r * rstride] = c_conj(a[Dft<PF::R2>::pos(r)]);
+    };
+    PF::pass2_all(W1, tl, store);
+  }
+}
+
+// ------------------------------------------------------------------ I2 (interleaved)
+// Band accumulators in TMEM: 2 columns (one complex) per output r, 2 * R2
+// columns per thread; warps of a lane quadrant side by side.
+template <class PF, class TO>
+__global__ void __launch_bounds__(PF::T, 1)
+    k_rows_inv_steer_ilv(Geo g, const float4* __restrict__ T2, Bands bl,
+                         const double* __restrict__ base, TO* __restrict__ out, int accumulate,
+                         SigSrc dcs, double dcr, double dci, float scale,
+                         const float2* __restrict__ twm, const float2* __restrict__ twl) {
+  constexpr int L = PF::L;  // = Pw
+  constexpr int R2 = PF::R2;
+  static_assert(2 * PF::NB2 == PF::T, "pass 2 must use every thread (warp-collective TMEM ops)");
+  extern __shared__ __align__(16) float4 smp[];
+  float4* W04 = smp;
+  float4* W14 = W04 + PF::LP;
+  float4* Z4 = W14 + PF::LP;  // e^{i phi} of both rows at each transform output k (L entries;
+                              // 1 where k - off falls outside the image)
+  float2* TWs = reinterpret_cast<float2*>(Z4 + L);
+  float2* W0 = reinterpret_cast<float2*>(W04);
+  float2* W1 = reinterpret_cast<float2*>(W14);
+  const float2* Z = reinterpret_cast<const float2*>(Z4);
+  __shared__ uint32_t tbase;
+  const int b = blockIdx.x, t = threadIdx.x;
+  if (t < 32) tmem_alloc(&tbase, 512);
+  const int y0 = 2 * b, y1 = 2 * b + 1;
+  for (int k = t; k < L; k += blockDim.x) {
+    const int x = k - g.off;
+    const bool in = x >= 0 && x < g.W;
+    const float2 z0 = in ? steer(1, base[size_t(y0) * g.W + x], 1.f) : make_float2(1.f, 0.f);
+    const float2 z1 =
+        in && y1 < g.H ? steer(1, base[size_t(y1) * g.W + x], 1.f) : make_float2(1.f, 0.f);
+    Z4[k] = make_float4(z0.x, z0.y, z1.x, z1.y);
+  }
+  for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
+  typename PF::LastTw tl;
+  PF::load_last_tw(twl, tl);
+  const size_t plane4 = size_t(g.H2 / 2) * g.Pw;  // float4 per band plane
+  const float4* rowp = T2 + size_t(b) * g.Pw;
+  const int off = g.off, W = g.W;
+  constexpr unsigned kBytes = unsigned(L * sizeof(float4));
+  __shared__ __align__(8) uint64_t bar;
+  if (t == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(&bar, kBytes);
+    bulk_copy(W04, rowp, kBytes, &bar);
+    if (bl.n > 1) prefetch_l2(rowp + plane4, kBytes);
+  }
+  tmem_fence_before_sync();
+  __syncthreads();
+  tmem_fence_after_sync();
+  const uint32_t tacc = tmem_warp_base(tbase) + uint32_t((t >> 7) * 2 * R2);
+  unsigned phase = 0;
+  for (int bi = 0; bi < bl.n; ++bi) {
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    auto load = [&](int n, int gi) -> float2 { return c_conj(W0[2 * n + gi]); };
+    {
+      typename PF::P0Regs v;
+      PF::pass0_compute(load, v);
+      __syncthreads();
+      PF::pass0_store(W0, v);
+    }
+    __syncthreads();
+    PF::pass1(W0, W1, TWs);
+    __syncthreads();
+    if (t == 0 && bi + 1 < bl.n) {
+      fence_proxy_async();
+      mbar_expect_tx(&bar, kBytes);
+      bulk_copy(W04, rowp + size_t(bi + 1) * plane4, kBytes, &bar);
+      if (bi + 2 < bl.n) prefetch_l2(rowp + size_t(bi + 2) * plane4, kBytes);
+    }
+    const int dk = bi == 0 ? 0 : bl.k[bi - 1] - bl.k[bi];
+    const int tt = opaque_i(t);
+    const float2* zp = Z + tt;  // = Z[2 * j + gi]
+    // acc = acc z^dk + conj(v)  (Horner over descending k; IFFT = conj FFT conj)
+    auto horner = [&](float2 (&a)[R2]) {
+      constexpr int C = 5;  // outputs per TMEM round trip
+#pragma unroll
+      for (int r0 = 0; r0 < R2; r0 += C) {
+        float2 acc[C];
+        if (bi > 0) {
+#pragma unroll
+          for (int i = 0; i < C; ++i)
+            if (r0 + i < R2) acc[i] = tmem_ld2(tacc + 2 * (r0 + i));
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < C; ++i)
+            if (r0 + i < R2) tmem_dep(acc[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < C; ++i) {
+          const int r = r0 + i;
+          if (r >= R2) break;
+          const float2 va = a[Dft<R2>::pos(r)];
+          if (bi == 0) {
+            acc[i] = c_conj(va);
+            continue;
+          }
+          const float2 z = zp[2 * r * PF::NB2];
+          float2 pa = acc[i];
+          if (dk == 1) {
+            pa = make_float2(fmaf(pa.x, z.x, fmaf(-pa.y, z.y, va.x)),
+                             fmaf(pa.x, z.y, fmaf(pa.y, z.x, -va.y)));
+          } else {
+            float2 za = z;
+            int d = dk;
+            if (d < 0) {
+              za = c_conj(za);
+              d = -d;
+            }
+            for (int s = 0; s < d; ++s) pa = c_mul(pa, za);
+            pa = c_add(pa, c_conj(va));
+          }
+          acc[i] = pa;
+        }
+#pragma unroll
+        for (int i = 0; i < C; ++i)
+          if (r0 + i < R2) tmem_st2(tacc + 2 * (r0 + i), acc[i]);
+      }
+      tmem_wait_st();
+    };
+    PF::pass2_all(W1, tl, horner);
+  }
+  // out = scale * z^{k_last} * acc (+ conj(dc) H for the scale group)
+  {
+    const int klast = bl.k[bl.n - 1];
+    const int gi = t & 1, j = t >> 1, y = 2 * b + gi;
+#pragma unroll
+    for (int r = 0; r < R2; ++r) {
+      float2 acc = tmem_ld2(tacc + 2 * r);
+      tmem_wait_ld();
+      tmem_dep(acc);
+      const int x = j + r * PF::NB2 - off;
+      if (x < 0 || x >= W || y >= g.H) continue;
+      const size_t i = size_t(y) * W + x;
+      const float2 v = c_scale(c_mul(acc, steer(klast, base[i], 1.f)), scale);
+      OutOps<TO>::put(out, i, v, accumulate != 0, dc_term(dcs, i, dcr, dci));
+    }
+  }
+  tmem_fence_before_sync();
+  __syncthreads();
+  if (t < 32) {
+    tmem_fence_after_sync();
+    tmem_dealloc(tbase, 512);
+  }
+}
+
+constexpr size_t kSmemLimitP = 232448;
+
+// exact twiddle tables of a pair plan (fp64 -> fp32), per device
+struct PairTw {
+  float2* mid = nullptr;
+  float2* last = nullptr;
+};
+
+template <class PF>
+PairTw pair_tables() {
+  static std::mutex mu;
+  static std::map<int, PairTw> cache;  // device -> tables
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  std::vector<float2> m(PF::TWM), l(PF::TWL);
+  const double tp = 6.283185307179586476925286766559;
+  for (int r = 1; r < PF::R1; ++r)
+    for (int jm = 0; jm < PF::R0; ++jm) {
+      const long e = long(jm) * r % (PF::R0 * PF::R1);
+      const double a = -tp * double(e) / double(PF::R0 * PF::R1);
+      m[(r - 1) * PF::R0 + jm] = make_float2(float(std::cos(a)), float(std::sin(a)));
+    }
+  for (int r = 1; r < PF::R2; ++r)
+    for (int j = 0; j < PF::NB2; ++j) {
+      const long e = long(j) * r % PF::L;
+      const double a = -tp * double(e) / double(PF::L);
+      l[(r - 1) * PF::NB2 + j] = make_float2(float(std::cos(a)), float(std::sin(a)));
+    }
+  PairTw p;
+  if (cudaMalloc(&p.mid, m.size() * sizeof(float2)) != cudaSuccess ||
+      cudaMalloc(&p.last, l.size() * sizeof(float2)) != cudaSuccess)
+    return PairTw{};
+  cudaMemcpy(p.mid, m.data(), m.size() * sizeof(float2), cudaMemcpyHostToDevice);
+  cudaMemcpy(p.last, l.data(), l.size() * sizeof(float2), cudaMemcpyHostToDevice);
+  cache[dev] = p;
+  return p;
+}
+
+}  // namespace
+
+// 0 if no pair plan for L (or the stage does not fit); else the dynamic smem
+size_t pair_smem(int stage, int L, const Geo& g) {
+  size_t s = 0;
+#define XCB_PAIR_SMEM(LL, R0, R1, R2)                                              \
+  if (L == LL) {                                                                   \
+    using PF = PairFft<LL, R0, R1, R2>;                                            \
+    const size_t tw = size_t(PF::TWM) * sizeof(float2);                            \
+    if (stage == 0) s = (size_t(LL) + 2 * size_t(PF::LP)) * sizeof(float4) + tw;   \
+    if (stage == 1) s = (2 * size_t(PF::LP) + size_t(LL)) * sizeof(float4) + tw;   \
+  }
+  XCB_PAIR_TABLE(XCB_PAIR_SMEM)
+#undef XCB_PAIR_SMEM
+  return s <= kSmemLimitP ? s : 0;
+}
+
+static int pair_mode() {  // XCB_PAIR: 1 interleaved (default), 2 pair-per-thread
+  static const int m = [] {
+    const char* e = std::getenv("XCB_PAIR");
+    return e && e[0] == '2' ? 2 : 1;
+  }();
+  return m;
+}
+
+void launch_cols_inv_corr_pair(const Geo& g, const float2* Hhat, const float2* Fhat,
+                               size_t sstride, const Bands& b, float2* T2, cudaStream_t st,
+                               LaunchCounter& lc) {
+  const size_t sm = pair_smem(0, g.Ph, g);
+#define XCB_PAIR_I1(LL, R0, R1, R2)                                                       \
+  if (g.Ph == LL) {                                                                       \
+    using PF = PairFft<LL, R0, R1, R2>;                                                   \
+    using IF = IlvFft<LL, R0, R1, R2>;                                                    \
+    const PairTw tw = pair_tables<PF>();                                                  \
+    const float4* hh = reinterpret_cast<const float4*>(Hhat);                             \
+    const float4* fh = reinterpret_cast<const float4*>(Fhat);                             \
+    if (pair_mode() == 2) {                                                               \
+      set_smem(k_cols_inv_corr_pair<PF>, sm);                                             \
+      k_cols_inv_corr_pair<PF><<<g.Pw / 2, PF::T, sm, st>>>(g, hh, fh, sstride / 2, b,    \
+                                                            T2, tw.mid, tw.last);         \
+    } else {                                                                              \
+      set_smem(k_cols_inv_corr_ilv<IF>, sm);                                              \
+      k_cols_inv_corr_ilv<IF><<<g.Pw / 2, IF::T, sm, st>>>(g, hh, fh, sstride / 2, b, T2, \
+                                                           tw.mid, tw.last);              \
+    }                                                                                     \
+  }
+  XCB_PAIR_TABLE(XCB_PAIR_I1)
+#undef XCB_PAIR_I1
+  ++lc.n;
+}
+
+void launch_rows_inv_steer_pair(const Geo& g, const float2* T2, const Bands& b,
+                                const double* base, int out_kind, void* out, int accumulate,
+                                const SigSrc& dcs, double dcr, double dci, cudaStream_t st,
+                                LaunchCounter& lc) {
+  const size_t sm = pair_smem(1, g.Pw, g);
+  const float scale = float(1.0 / (double(g.Ph) * double(g.Pw)));
+#define XCB_PAIR_I2(LL, R0, R1, R2)                                                       \
+  if (g.Pw == LL) {                                                                       \
+    using PF = PairFft<LL, R0, R1, R2>;                                                   \
+    const PairTw tw = pair_tables<PF>();                                                  \
+    const float4* t2 = reinterpret_cast<const float4*>(T2);                               \
+    using IF = IlvFft<LL, R0, R1, R2>;                                                    \
+    if (pair_mode() == 2) {                                                               \
+      if (out_kind == OUT_C64) {                                                          \
+        set_smem(k_rows_inv_steer_pair<PF, float2>, sm);                                  \
+        k_rows_inv_steer_pair<PF, float2><<<g.H2 / 2, PF::T, sm, st>>>(                   \
+            g, t2, b, base, static_cast<float2*>(out), accumulate, dcs, dcr, dci, scale,  \
+            tw.mid, tw.last);                                                             \
+      } else {                                                                            \
+        set_smem(k_rows_inv_steer_pair<PF, double2>, sm);                                 \
+        k_rows_inv_steer_pair<PF, double2><<<g.H2 / 2, PF::T, sm, st>>>(                  \
+            g, t2, b, base, static_cast<double2*>(out), accumulate, dcs, dcr, dci, scale, \
+            tw.mid, tw.last);                                                             \
+      }                                                                                   \
+    } else if (out_kind == OUT_C64) {                                                     \
+      set_smem(k_rows_inv_steer_ilv<IF, float2>, sm);                                    \
+      k_rows_inv_steer_ilv<IF, float2><<<g.H2 / 2, IF::T, sm, st>>>(                      \
+          g, t2, b, base, static_cast<float2*>(out), accumulate, dcs, dcr, dci, scale,    \
+          tw.mid, tw.last);                                                               \
+    } else {                                                                              \
+      set_smem(k_rows_inv_steer_ilv<IF, double2>, sm);                                    \
+      k_rows_inv_steer_ilv<IF, double2><<<g.H2 / 2, IF::T, sm, st>>>(                     \
+          g, t2, b, base, static_cast<double2*>(out), accumulate, dcs, dcr, dci, scale,   \
+          tw.mid, tw.last);                                                               \
+    }                                                                                     \
+  }
+  XCB_PAIR_TABLE(XCB_PAIR_I2)
+#undef XCB_PAIR_I2
+  ++lc.n;
+}
+
+}  // namespace xcb

@@ -134,3 +134,17 @@ void launch_cols_fwd_mac_inv_fast(const FftPlan& pc, const Geo& g, const float2*
                                   const float2* Fhat, size_t sstride, const Bands& b,
                                   float2* T2, cudaStream_t st, LaunchCounter& lc);
 }  // namespace xcb
+
+namespace xcb {
+// Pair-engine variants (k_pair.cu, lengths of XCB_PAIR_TABLE in fft_pair.cuh):
+// pair_smem returns the dynamic smem of stage 0 (I1) / 1 (I2), or 0 when the
+// length has no pair plan; callers then use the fast or generic kernels.
+size_t pair_smem(int stage, int L, const Geo& g);
+void launch_cols_inv_corr_pair(const Geo& g, const float2* Hhat, const float2* Fhat,
+                               size_t sstride, const Bands& b, float2* T2, cudaStream_t st,
+                               LaunchCounter& lc);
+void launch_rows_inv_steer_pair(const Geo& g, const float2* T2, const Bands& b,
+                                const double* base, int out_kind, void* out, int accumulate,
+                                const SigSrc& dcs, double dcr, double dci, cudaStream_t st,
+                                LaunchCounter& lc);
+}  // namespace xcb
