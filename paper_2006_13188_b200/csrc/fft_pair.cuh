@@ -225,13 +225,13 @@ struct IlvFft {
   struct P0Regs {
     float2 a[R0];
   };
-  // load(n, g) -> float2
+  // load(r, n, g) -> float2 (input n = j + r NB0 of sequence g)
   template <class Load>
   __device__ __forceinline__ static void pass0_compute(Load& load, P0Regs& v) {
     const int t = opaque_i(threadIdx.x), g = t & 1, j = t >> 1;
     if (j < NB0) {
 #pragma unroll
-      for (int r = 0; r < R0; ++r) v.a[r] = load(j + r * NB0, g);
+      for (int r = 0; r < R0; ++r) v.a[r] = load(r, j + r * NB0, g);
       Dft<R0>::run(v.a);
     }
   }

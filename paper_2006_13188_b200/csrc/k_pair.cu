@@ -258,6 +258,9 @@ __global__ void __launch_bounds__(PF::T, 1)
 }
 
 // ------------------------------------------------------------------ I1 (interleaved)
+// conj(H^) for the thread's pass-0 inputs stays in registers for the whole
+// band loop; F^_k is TMA-staged into its own buffer, so a band needs two
+// barriers (after pass 0: stage free for the next band's copy; after pass 1).
 template <class PF>
 __global__ void __launch_bounds__(PF::T, 1)
     k_cols_inv_corr_ilv(Geo g, const float4* __restrict__ Hh, const float4* __restrict__ Fh,
@@ -265,22 +268,14 @@ __global__ void __launch_bounds__(PF::T, 1)
                         const float2* __restrict__ twm, const float2* __restrict__ twl) {
   constexpr int L = PF::L;  // = Ph
   extern __shared__ __align__(16) float4 smp[];
-  float4* HC4 = smp;  // conj(H^) of the column pair, natural order
-  float4* W04 = HC4 + L;
+  float4* ST4 = smp;  // staged F^_k column pair, natural order
+  float4* W04 = ST4 + L;
   float4* W14 = W04 + PF::LP;
   float2* TWs = reinterpret_cast<float2*>(W14 + PF::LP);
-  const float2* HC = reinterpret_cast<const float2*>(HC4);
+  const float2* ST = reinterpret_cast<const float2*>(ST4);
   float2* W0 = reinterpret_cast<float2*>(W04);
   float2* W1 = reinterpret_cast<float2*>(W14);
   const int c = blockIdx.x, t = threadIdx.x;
-  const float4* hcol = Hh + size_t(c) * L;
-  for (int i = t; i < L; i += blockDim.x) {
-    const float4 h = hcol[i];
-    HC4[i] = make_float4(h.x, -h.y, h.z, -h.w);
-  }
-  for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
-  typename PF::LastTw tl;
-  PF::load_last_tw(twl, tl);
   const size_t plane = size_t(g.H2) * g.Pw;  // float2 per T2 band plane
   constexpr unsigned kBytes = unsigned(L * sizeof(float4));
   auto fsrc = [&](int bi) { return Fh + size_t(bl.spec[bi]) * sstride4 + size_t(c) * L; };
@@ -289,31 +284,56 @@ __global__ void __launch_bounds__(PF::T, 1)
     mbar_init(&bar, 1);
     fence_mbar_init();
     mbar_expect_tx(&bar, kBytes);
-    bulk_copy(W04, fsrc(0), kBytes, &bar);
+    bulk_copy(ST4, fsrc(0), kBytes, &bar);
     if (bl.n > 1) prefetch_l2(fsrc(1), kBytes);
   }
+  // conj(H^) at this thread's pass-0 inputs n = j + r NB0, parked in TMEM
+  // (2 columns per r; warps of a lane quadrant side by side)
+  __shared__ uint32_t tbase;
+  if (t < 32) tmem_alloc(&tbase, 256);
+  tmem_fence_before_sync();
+  __syncthreads();
+  tmem_fence_after_sync();
+  const uint32_t thc = tmem_warp_base(tbase) + uint32_t((t >> 7) * 2 * PF::R0);
+  {
+    const int gi = t & 1, j = t >> 1;
+    const float2* hcol = reinterpret_cast<const float2*>(Hh + size_t(c) * L) + gi;
+#pragma unroll
+    for (int r = 0; r < PF::R0; ++r)
+      tmem_st2(thc + 2 * r, j < PF::NB0 ? c_conj(__ldg(hcol + 2 * (j + r * PF::NB0)))
+                                        : make_float2(0.f, 0.f));
+    tmem_wait_st();
+  }
+  for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
+  typename PF::LastTw tl;
+  PF::load_last_tw(twl, tl);
   __syncthreads();
   unsigned phase = 0;
   for (int bi = 0; bi < bl.n; ++bi) {
     mbar_wait(&bar, phase);
     phase ^= 1;
     // conj(H^ conj(F^)) = conj(H^) F^ : inverse via conj-FFT-conj
-    auto load = [&](int n, int gi) -> float2 { return c_mul(HC[2 * n + gi], W0[2 * n + gi]); };
     {
+      float2 hc[PF::R0];
+#pragma unroll
+      for (int r = 0; r < PF::R0; ++r) hc[r] = tmem_ld2(thc + 2 * r);
+      tmem_wait_ld();
+#pragma unroll
+      for (int r = 0; r < PF::R0; ++r) tmem_dep(hc[r]);
+      auto load = [&](int r, int n, int gi) -> float2 { return c_mul(hc[r], ST[2 * n + gi]); };
       typename PF::P0Regs v;
       PF::pass0_compute(load, v);
-      __syncthreads();
       PF::pass0_store(W0, v);
     }
-    __syncthreads();
-    PF::pass1(W0, W1, TWs);
     __syncthreads();
     if (t == 0 && bi + 1 < bl.n) {
       fence_proxy_async();
       mbar_expect_tx(&bar, kBytes);
-      bulk_copy(W04, fsrc(bi + 1), kBytes, &bar);
+      bulk_copy(ST4, fsrc(bi + 1), kBytes, &bar);
       if (bi + 2 < bl.n) prefetch_l2(fsrc(bi + 2), kBytes);
     }
+    PF::pass1(W0, W1, TWs);
+    __syncthreads();
     const int tt = opaque_i(t), gi = tt & 1, j = tt >> 1;
     // output y = j + r NB2 - off: NB2 is even, so y & 1 is fixed and y >> 1
     // advances by NB2 / 2 rows of T2 per r; valid r form [rlo, rhi)
@@ -331,11 +351,18 @@ __global__ void __launch_bounds__(PF::T, 1)
     };
     PF::pass2_all(W1, tl, store);
   }
+  tmem_fence_before_sync();
+  __syncthreads();
+  if (t < 32) {
+    tmem_fence_after_sync();
+    tmem_dealloc(tbase, 256);
+  }
 }
 
 // ------------------------------------------------------------------ I2 (interleaved)
-// Band accumulators in TMEM: 2 columns (one complex) per output r, 2 * R2
-// columns per thread; warps of a lane quadrant side by side.
+// The thread's steering phasors z = e^{i phi} (one per pass-2 output) stay in
+// registers; the band accumulators live in TMEM (2 columns = one complex per
+// output r, 2 * R2 columns per thread; warps of a lane quadrant side by side).
 template <class PF, class TO>
 __global__ void __launch_bounds__(PF::T, 1)
     k_rows_inv_steer_ilv(Geo g, const float4* __restrict__ T2, Bands bl,
@@ -346,82 +373,79 @@ __global__ void __launch_bounds__(PF::T, 1)
   constexpr int R2 = PF::R2;
   static_assert(2 * PF::NB2 == PF::T, "pass 2 must use every thread (warp-collective TMEM ops)");
   extern __shared__ __align__(16) float4 smp[];
-  float4* W04 = smp;
+  float4* ST4 = smp;  // staged T2 row pair, natural order
+  float4* W04 = ST4 + L;
   float4* W14 = W04 + PF::LP;
-  float4* Z4 = W14 + PF::LP;  // e^{i phi} of both rows at each transform output k (L entries;
-                              // 1 where k - off falls outside the image)
-  float2* TWs = reinterpret_cast<float2*>(Z4 + L);
+  float2* TWs = reinterpret_cast<float2*>(W14 + PF::LP);
+  const float2* ST = reinterpret_cast<const float2*>(ST4);
   float2* W0 = reinterpret_cast<float2*>(W04);
   float2* W1 = reinterpret_cast<float2*>(W14);
-  const float2* Z = reinterpret_cast<const float2*>(Z4);
   __shared__ uint32_t tbase;
   const int b = blockIdx.x, t = threadIdx.x;
-  if (t < 32) tmem_alloc(&tbase, 512);
-  const int y0 = 2 * b, y1 = 2 * b + 1;
-  for (int k = t; k < L; k += blockDim.x) {
-    const int x = k - g.off;
-    const bool in = x >= 0 && x < g.W;
-    const float2 z0 = in ? steer(1, base[size_t(y0) * g.W + x], 1.f) : make_float2(1.f, 0.f);
-    const float2 z1 =
-        in && y1 < g.H ? steer(1, base[size_t(y1) * g.W + x], 1.f) : make_float2(1.f, 0.f);
-    Z4[k] = make_float4(z0.x, z0.y, z1.x, z1.y);
-  }
-  for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
-  typename PF::LastTw tl;
-  PF::load_last_tw(twl, tl);
   const size_t plane4 = size_t(g.H2 / 2) * g.Pw;  // float4 per band plane
   const float4* rowp = T2 + size_t(b) * g.Pw;
-  const int off = g.off, W = g.W;
   constexpr unsigned kBytes = unsigned(L * sizeof(float4));
   __shared__ __align__(8) uint64_t bar;
   if (t == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
     mbar_expect_tx(&bar, kBytes);
-    bulk_copy(W04, rowp, kBytes, &bar);
+    bulk_copy(ST4, rowp, kBytes, &bar);
     if (bl.n > 1) prefetch_l2(rowp + plane4, kBytes);
   }
+  if (t < 32) tmem_alloc(&tbase, 512);
+  const int gi = t & 1, j = t >> 1, y = 2 * b + gi;
+  for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
+  typename PF::LastTw tl;
+  PF::load_last_tw(twl, tl);
   tmem_fence_before_sync();
   __syncthreads();
   tmem_fence_after_sync();
-  const uint32_t tacc = tmem_warp_base(tbase) + uint32_t((t >> 7) * 2 * R2);
+  // per output r: columns [acc.re, acc.im, z.re, z.im], z = e^{i phi}
+  const uint32_t tacc = tmem_warp_base(tbase) + uint32_t((t >> 7) * 4 * R2);
+#pragma unroll
+  for (int r = 0; r < R2; ++r) {
+    const int x = j + r * PF::NB2 - g.off;
+    tmem_st2(tacc + 4 * r + 2, x >= 0 && x < g.W && y < g.H
+                                    ? steer(1, base[size_t(y) * g.W + x], 1.f)
+                                    : make_float2(1.f, 0.f));
+  }
+  tmem_wait_st();
   unsigned phase = 0;
   for (int bi = 0; bi < bl.n; ++bi) {
     mbar_wait(&bar, phase);
     phase ^= 1;
-    auto load = [&](int n, int gi) -> float2 { return c_conj(W0[2 * n + gi]); };
+    auto load = [&](int, int n, int gi2) -> float2 { return c_conj(ST[2 * n + gi2]); };
     {
       typename PF::P0Regs v;
       PF::pass0_compute(load, v);
-      __syncthreads();
       PF::pass0_store(W0, v);
     }
-    __syncthreads();
-    PF::pass1(W0, W1, TWs);
     __syncthreads();
     if (t == 0 && bi + 1 < bl.n) {
       fence_proxy_async();
       mbar_expect_tx(&bar, kBytes);
-      bulk_copy(W04, rowp + size_t(bi + 1) * plane4, kBytes, &bar);
+      bulk_copy(ST4, rowp + size_t(bi + 1) * plane4, kBytes, &bar);
       if (bi + 2 < bl.n) prefetch_l2(rowp + size_t(bi + 2) * plane4, kBytes);
     }
+    PF::pass1(W0, W1, TWs);
+    __syncthreads();
     const int dk = bi == 0 ? 0 : bl.k[bi - 1] - bl.k[bi];
-    const int tt = opaque_i(t);
-    const float2* zp = Z + tt;  // = Z[2 * j + gi]
     // acc = acc z^dk + conj(v)  (Horner over descending k; IFFT = conj FFT conj)
     auto horner = [&](float2 (&a)[R2]) {
       constexpr int C = 5;  // outputs per TMEM round trip
 #pragma unroll
       for (int r0 = 0; r0 < R2; r0 += C) {
+        float4 az[C];  // (acc, z)
         float2 acc[C];
         if (bi > 0) {
 #pragma unroll
           for (int i = 0; i < C; ++i)
-            if (r0 + i < R2) acc[i] = tmem_ld2(tacc + 2 * (r0 + i));
+            if (r0 + i < R2) az[i] = tmem_ld4(tacc + 4 * (r0 + i));
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < C; ++i)
-            if (r0 + i < R2) tmem_dep(acc[i]);
+            if (r0 + i < R2) tmem_dep(az[i]);
         }
 #pragma unroll
         for (int i = 0; i < C; ++i) {
@@ -432,13 +456,13 @@ __global__ void __launch_bounds__(PF::T, 1)
             acc[i] = c_conj(va);
             continue;
           }
-          const float2 z = zp[2 * r * PF::NB2];
-          float2 pa = acc[i];
+          float2 pa = make_float2(az[i].x, az[i].y);
+          const float2 zr = make_float2(az[i].z, az[i].w);
           if (dk == 1) {
-            pa = make_float2(fmaf(pa.x, z.x, fmaf(-pa.y, z.y, va.x)),
-                             fmaf(pa.x, z.y, fmaf(pa.y, z.x, -va.y)));
+            pa = make_float2(fmaf(pa.x, zr.x, fmaf(-pa.y, zr.y, va.x)),
+                             fmaf(pa.x, zr.y, fmaf(pa.y, zr.x, -va.y)));
           } else {
-            float2 za = z;
+            float2 za = zr;
             int d = dk;
             if (d < 0) {
               za = c_conj(za);
@@ -451,7 +475,7 @@ __global__ void __launch_bounds__(PF::T, 1)
         }
 #pragma unroll
         for (int i = 0; i < C; ++i)
-          if (r0 + i < R2) tmem_st2(tacc + 2 * (r0 + i), acc[i]);
+          if (r0 + i < R2) tmem_st2(tacc + 4 * (r0 + i), acc[i]);
       }
       tmem_wait_st();
     };
@@ -460,15 +484,14 @@ __global__ void __launch_bounds__(PF::T, 1)
   // out = scale * z^{k_last} * acc (+ conj(dc) H for the scale group)
   {
     const int klast = bl.k[bl.n - 1];
-    const int gi = t & 1, j = t >> 1, y = 2 * b + gi;
 #pragma unroll
     for (int r = 0; r < R2; ++r) {
-      float2 acc = tmem_ld2(tacc + 2 * r);
+      float2 acc = tmem_ld2(tacc + 4 * r);
       tmem_wait_ld();
       tmem_dep(acc);
-      const int x = j + r * PF::NB2 - off;
-      if (x < 0 || x >= W || y >= g.H) continue;
-      const size_t i = size_t(y) * W + x;
+      const int x = j + r * PF::NB2 - g.off;
+      if (x < 0 || x >= g.W || y >= g.H) continue;
+      const size_t i = size_t(y) * g.W + x;
       const float2 v = c_scale(c_mul(acc, steer(klast, base[i], 1.f)), scale);
       OutOps<TO>::put(out, i, v, accumulate != 0, dc_term(dcs, i, dcr, dci));
     }
