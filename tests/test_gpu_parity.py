@@ -357,3 +357,52 @@ def test_host_pipeline_batch_matches_device_path(orc):
     for b in (0, 3, 4):
         one = X.xcorr_fast(sig[b], X.XformField.rotation(th[b]), w.filt).output
         assert np.array_equal(batch[b], one)
+
+
+# ------------------------------------------------- pair-engine geometry edges
+
+def _direct_at(orc, F, H, theta, ys, xs, periodic):
+    """out(p) = sum_k e^{i k theta(p)} sum_u conj(F_k(u)) H(p + u) (fft.hpp:74-77,
+    engine.hpp:312-317) evaluated directly in double at the sampled pixels."""
+    R = int(np.ceil(F.r_max))
+    side = 2 * R + 1
+    comps = np.stack([orc.render_component(F, ci, side, side, R, R) for ci in range(len(F.ks))])
+    h, w = H.shape
+    d = np.arange(-R, R + 1)
+    out = np.zeros(len(ys), np.complex128)
+    for i, (y, x) in enumerate(zip(ys, xs)):
+        yy, xx = y + d, x + d
+        if periodic:
+            patch = H[np.ix_(yy % h, xx % w)].astype(np.float64)
+        else:
+            patch = np.zeros((side, side))
+            vy, vx = (yy >= 0) & (yy < h), (xx >= 0) & (xx < w)
+            patch[np.ix_(vy, vx)] = H[np.ix_(yy[vy], xx[vx])]
+        g = np.einsum("kab,ab->k", np.conj(comps), patch)
+        out[i] = np.sum(np.exp(1j * np.asarray(F.ks) * float(theta[y, x])) * g)
+    return out
+
+
+@pytest.mark.parametrize("h,w,periodic", [(4101, 4000, False), (4000, 4101, False),
+                                          (4275, 4275, True)])
+def test_pair_engine_geometry_edges(orc, h, w, periodic):
+    """Transform length 4320 (the pair-engine kernels) with an odd height, a
+    different row length, and the periodic wrap with an odd crop offset R=15."""
+    from paper_2006_13188_b200 import workloads as WL
+    wk = WL.config1(n=64)
+    Fo = ofilter(orc, wk.filt)
+    # the direct sum agrees with the oracle's FFT path on a small image first
+    r = np.random.default_rng(11)
+    Hs = r.uniform(0, 1, (40, 37)).astype(np.float32)
+    Ts = r.uniform(0, 2 * np.pi, (40, 37)).astype(np.float32)
+    ref_s = orc.xcorr_fast(Hs.astype(np.float64), ROT, Ts.astype(np.float64), Fo)[0]
+    yy, xx = np.array([0, 5, 39, 20]), np.array([0, 36, 3, 18])
+    assert orc.rel_l2(_direct_at(orc, Fo, Hs, Ts, yy, xx, False), ref_s[yy, xx]) < 1e-10
+    H = r.uniform(0, 1, (h, w)).astype(np.float32)
+    T = r.uniform(0, 2 * np.pi, (h, w)).astype(np.float32)
+    res = X.xcorr_fast(H, X.XformField.rotation(T), wk.filt, X.XConvPlan(periodic=periodic))
+    got = res.output
+    ys = np.concatenate([r.integers(0, h, 40), [0, h - 1, 0, h - 1, h // 2]])
+    xs = np.concatenate([r.integers(0, w, 40), [0, 0, w - 1, w - 1, 1]])
+    ref = _direct_at(orc, Fo, H, T, ys, xs, periodic)
+    assert orc.rel_l2(got[ys, xs], ref) < TOL

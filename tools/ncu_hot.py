@@ -29,3 +29,23 @@ for op, s in by_op.most_common(25):
 print("top instructions")
 for s, r in sorted(samp, key=lambda x: -x[0])[:top]:
     print(f"  {s/tot:6.2%} {r[ix['Address']][-5:]} {r[ix['Source']].strip()[:70]}")
+
+# per stall reason: the instructions collecting most of it
+if len(sys.argv) > 3:
+    for reason in sys.argv[3].split(","):
+        col = ix.get("stall_" + reason)
+        if col is None:
+            continue
+        seen = set()
+        lst = []
+        for s, r in samp:
+            if r[ix["Address"]] in seen:
+                continue
+            seen.add(r[ix["Address"]])
+            v = int(r[col] or 0)
+            if v:
+                lst.append((v, r))
+        tot_r = sum(v for v, _ in lst)
+        print(f"stall_{reason}: {tot_r} samples")
+        for v, r in sorted(lst, key=lambda x: -x[0])[:12]:
+            print(f"  {v/tot_r:6.1%} {r[ix['Address']][-5:]} {r[ix['Source']].strip()[:70]}")
