@@ -42,6 +42,14 @@ __device__ __forceinline__ float4 ldg_stream4(const float4* p) {
   return v;
 }
 
+// predicated 8-byte global store (one STG, no branch)
+__device__ __forceinline__ void st_pred(float2* p, float2 v, bool pred) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n @q st.global.v2.f32 [%0], {%1, %2};\n}" ::"l"(p),
+      "f"(v.x), "f"(v.y), "r"(int(pred))
+      : "memory");
+}
+
 __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }

@@ -338,16 +338,19 @@ __global__ void __launch_bounds__(PF::T, 1)
     // output y = j + r NB2 - off: NB2 is even, so y & 1 is fixed and y >> 1
     // advances by NB2 / 2 rows of T2 per r; valid r form [rlo, rhi)
     const int y0 = j - g.off;
-    const size_t rstride = size_t(PF::NB2 / 2) * 2 * g.Pw;  // float2 per r step
+    const int rstride = (PF::NB2 / 2) * 2 * g.Pw;  // float2 per r step (< 2^31: one plane)
     float2* o = T2 + size_t(bi) * plane + 2 * (2 * c + gi) +
                 (ptrdiff_t(y0 >> 1) * (2 * g.Pw) + (y0 & 1));
-    const int rlo = y0 >= 0 ? 0 : (-y0 + PF::NB2 - 1) / PF::NB2;
-    const int rhi = g.H - y0 <= 0 ? 0 : (g.H - y0 + PF::NB2 - 1) / PF::NB2;
+    const bool act = j < PF::NB2;
     auto store = [&](float2 (&a)[PF::R2]) {
-      if (j >= PF::NB2) return;
+      int y = opaque_i(y0);
+      float2* p = o;
 #pragma unroll
-      for (int r = 0; r < PF::R2; ++r)
-        if (r >= rlo && r < rhi) o[r * rstride] = c_conj(a[Dft<PF::R2>::pos(r)]);
+      for (int r = 0; r < PF::R2; ++r) {
+        st_pred(p, c_conj(a[Dft<PF::R2>::pos(r)]), act && unsigned(y) < unsigned(g.H));
+        y += PF::NB2;
+        p += rstride;
+      }
     };
     PF::pass2_all(W1, tl, store);
   }
