@@ -97,16 +97,18 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def stage_bytes(stage: str, B: int, H: int, W: int, Ph: int, Pw: int) -> float:
-    """Algorithmic bytes of one launch (one image) of each pipeline stage: the
-    compulsory reads + writes of its inputs/outputs (complex fp32 = 8 B)."""
+def stage_bytes(stage: str, B: int, H: int, W: int, Ph: int, Pw: int, ni: int = 1) -> float:
+    """Algorithmic bytes of one launch of each pipeline stage covering `ni`
+    images: the compulsory reads + writes of its inputs/outputs (complex fp32 =
+    8 B).  I1 reads each filter spectrum once per launch (shared by its images)."""
     N, P = H * W, Ph * Pw
     H2, Hx2 = H + (H & 1), H + (H & 1)
-    return {
+    if stage == "I1_cols_inv_corr":
+        return ni * (8 * P + B * 8 * H2 * Pw) + B * 8 * P
+    return ni * {
         "prep": 4 * N + 8 * N,
         "F1_rows_fwd": 4 * N + 8 * Hx2 * Pw,
         "F2_cols_fwd": 8 * Hx2 * Pw + 8 * P,
-        "I1_cols_inv_corr": 8 * P + B * 8 * P + B * 8 * H2 * Pw,
         "I2_rows_inv_steer": B * 8 * H2 * Pw + 8 * N + 8 * N,
         "S1_rows_fwd_premul": 4 * N + 8 * N + B * 8 * Hx2 * Pw,
         "S2_cols_fwd_mac_inv": B * 8 * Hx2 * Pw + B * 8 * P + 8 * H2 * Pw,
@@ -294,12 +296,17 @@ def run_b200(args):
     Ph, Pw = st.pad_h, st.pad_w
     dom = max(prof, key=lambda k: prof[k][0]) if prof else None
     roof = None
-    if dom:
-        tot_ms, nl = prof[dom]
+    nbl = len(comps)
+
+    def kernel_roof(name):
+        tot_ms, nl = prof[name]
         per_launch_s = tot_ms * 1e-3 / nl
-        nbl = len(comps)
-        alg = stage_bytes(dom, nbl, H, W, Ph, Pw)
-        achieved = alg / per_launch_s / 1e9
+        ni = max(1, round(Bl * args.steps / nl))  # images per launch
+        alg = stage_bytes(name, nbl, H, W, Ph, Pw, ni)
+        return alg, per_launch_s, ni, alg / per_launch_s / 1e9
+
+    if dom:
+        alg, per_launch_s, ni, achieved = kernel_roof(dom)
         traffic = None
         tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tf):
@@ -308,6 +315,12 @@ def run_b200(args):
         roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_kind,
                 "alg_bytes_per_launch": alg, "ms_per_launch": per_launch_s * 1e3,
+                "images_per_launch": ni,
+                "kernels": {k: {"ms_per_launch": kernel_roof(k)[1] * 1e3,
+                                "images_per_launch": kernel_roof(k)[2],
+                                "achieved_gbs": kernel_roof(k)[3],
+                                "frac": kernel_roof(k)[3] / hbm}
+                            for k in prof if k.startswith("I")},
                 "stages_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
                 "pipeline_model_frac": model_bytes("xcorr", nb, H * W, Ph * Pw) * Btot /
                 (ms_step * 1e-3) / 1e9 / hbm / max(world, 1)}

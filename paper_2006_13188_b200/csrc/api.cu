@@ -390,10 +390,11 @@ struct Staged {
 struct HostPipe {
   Call* c = nullptr;
   bool host = false;
-  cudaEvent_t in_done[2]{}, comp_done[2]{}, out_done[2]{}, t0{}, t1{};
+  static constexpr int NS = 4;  // slots: two groups of up to two images in flight
+  cudaEvent_t in_done[NS]{}, comp_done[NS]{}, out_done[NS]{}, t0{}, t1{};
   int issued = 0;
   explicit HostPipe(Call& call) : c(&call), host(call.d.memory == XC_HOST) {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NS; ++s) {
       ck(cudaEventCreateWithFlags(&in_done[s], cudaEventDisableTiming), "event");
       ck(cudaEventCreateWithFlags(&comp_done[s], cudaEventDisableTiming), "event");
       ck(cudaEventCreateWithFlags(&out_done[s], cudaEventDisableTiming), "event");
@@ -402,7 +403,7 @@ struct HostPipe {
     ck(cudaEventCreate(&t1), "event");
   }
   ~HostPipe() {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NS; ++s) {
       cudaEventDestroy(in_done[s]);
       cudaEventDestroy(comp_done[s]);
       cudaEventDestroy(out_done[s]);
@@ -411,14 +412,15 @@ struct HostPipe {
     cudaEventDestroy(t1);
   }
   size_t npix() const { return size_t(c->rows) * c->cols; }
-  // issue the H2D copies of image img into slot img&1 (host memory only)
+  static std::string slot_name(const char* b, int s) { return b + std::to_string(s); }
+  // issue the H2D copies of image img into slot img % NS (host memory only)
   void h2d(const void* signal, const void* param, int img) {
     if (!host || img >= c->d.batch) return;
-    const int s = img & 1;
+    const int s = img % NS;
     const size_t ss = dtype_size(c->d.signal_dtype), ps = dtype_size(c->d.param_dtype);
-    void* bs = c->ctx->buf<char>(s ? "sig_raw1" : "sig_raw0", npix() * ss);
-    void* bp = param ? c->ctx->buf<char>(s ? "param_raw1" : "param_raw0", npix() * ps) : nullptr;
-    if (img >= 2) ck(cudaStreamWaitEvent(c->ctx->cp_in, comp_done[s], 0), "wait");
+    void* bs = c->ctx->buf<char>(slot_name("sig_raw", s), npix() * ss);
+    void* bp = param ? c->ctx->buf<char>(slot_name("param_raw", s), npix() * ps) : nullptr;
+    if (img >= NS) ck(cudaStreamWaitEvent(c->ctx->cp_in, comp_done[s], 0), "wait");
     ck(cudaMemcpyAsync(bs, static_cast<const char*>(signal) + size_t(img) * npix() * ss,
                        npix() * ss, cudaMemcpyHostToDevice, c->ctx->cp_in),
        "H2D signal");
@@ -435,21 +437,21 @@ struct HostPipe {
     const xc_image_desc& d = c->d;
     const size_t ss = dtype_size(d.signal_dtype), ps = dtype_size(d.param_dtype);
     const bool cplx_sig = d.signal_dtype == XC_C64 || d.signal_dtype == XC_C128;
-    const int s = img & 1;
+    const int s = img % NS;
     Staged st{};
     const void* dsig;
     const void* dpar = nullptr;
     if (host) {
       ck(cudaStreamWaitEvent(c->st, in_done[s], 0), "wait");
-      dsig = c->ctx->buf<char>(s ? "sig_raw1" : "sig_raw0", npix() * ss);
-      if (param) dpar = c->ctx->buf<char>(s ? "param_raw1" : "param_raw0", npix() * ps);
+      dsig = c->ctx->buf<char>(slot_name("sig_raw", s), npix() * ss);
+      if (param) dpar = c->ctx->buf<char>(slot_name("param_raw", s), npix() * ps);
     } else {
       dsig = static_cast<const char*>(signal) + size_t(img) * npix() * ss;
       if (param)
         dpar = static_cast<const char*>(param) + (d.param_per_image ? size_t(img) * npix() * ps : 0);
     }
     if (d.signal_dtype == XC_F64 || d.signal_dtype == XC_C128) {
-      void* b = c->ctx->buf<char>("sig_f32", npix() * (cplx_sig ? 8 : 4));
+      void* b = c->ctx->buf<char>(slot_name("sig_f32_", s), npix() * (cplx_sig ? 8 : 4));
       xcb::launch_convert_signal(dsig, d.signal_dtype, npix(), b, c->st, c->lc);
       dsig = b;
     }
@@ -461,14 +463,14 @@ struct HostPipe {
   // output buffer of image img (device: the caller's; host: a slot stage)
   void* out_buffer(void* out, int img, size_t os) {
     if (!host) return static_cast<char*>(out) + size_t(img) * npix() * os;
-    const int s = img & 1;
-    if (img >= 2) ck(cudaStreamWaitEvent(c->st, out_done[s], 0), "wait");
-    return c->ctx->buf<char>(s ? "out_stage1" : "out_stage0", npix() * os);
+    const int s = img % NS;
+    if (img >= NS) ck(cudaStreamWaitEvent(c->st, out_done[s], 0), "wait");
+    return c->ctx->buf<char>(slot_name("out_stage", s), npix() * os);
   }
   // after image img's kernels: start its D2H (host memory)
   void done(void* out, int img, void* dout, size_t os) {
     if (!host) return;
-    const int s = img & 1;
+    const int s = img % NS;
     ck(cudaEventRecord(comp_done[s], c->st), "event");
     ck(cudaStreamWaitEvent(c->ctx->cp_out, comp_done[s], 0), "wait");
     ck(cudaMemcpyAsync(static_cast<char*>(out) + size_t(img) * npix() * os, dout, npix() * os,
@@ -494,9 +496,10 @@ Staged stage_inputs(Call& c, const void* signal, const void* param, int img) {
 // base (steering phase per pixel) + optional weights; throws the reference's
 // guard-band / positivity errors for scale fields (engine.hpp:267-279,
 // field.hpp:150-153).
-void prep(Call& c, const Staged& s, bool want_wgt, double** base_out, float** wgt_out) {
+void prep(Call& c, const Staged& s, bool want_wgt, double** base_out, float** wgt_out,
+          int slot = 0) {
   const size_t npix = size_t(c.rows) * c.cols;
-  double* base = c.ctx->buf<double>("base", npix);
+  double* base = c.ctx->buf<double>("base" + std::to_string(slot), npix);
   float* wgt = want_wgt ? c.ctx->buf<float>("wgt", npix) : nullptr;
   const xcb::HostFilter& hf = c.f->hf;
   const bool scale = hf.group == 1;
@@ -546,6 +549,28 @@ bool use_pair() {
   return on;
 }
 
+void launch_i2(Call& c, const xcb::SigSrc& sig, const float2* T2, const double* base, void* out,
+               int out_kind, bool accumulate, bool dc) {
+  const xcb::Geo& g = c.g;
+  const cplx dcv = dc ? std::conj(xcb::inner_dc_value(c.f->hf)) : cplx(0);  // engine.hpp:323
+  if (use_pair() && xcb::pair_smem(1, g.Pw, g)) {
+    stage(c, "I2_rows_inv_steer", [&] {
+      xcb::launch_rows_inv_steer_pair(g, T2, c.bands, base, out_kind, out, accumulate ? 1 : 0,
+                                      sig, dcv.real(), dcv.imag(), c.st, c.lc);
+    });
+  } else if (c.frow && xcb::fast_smem(1, *c.frow, g)) {
+    stage(c, "I2_rows_inv_steer", [&] {
+      xcb::launch_rows_inv_steer_fast(*c.frow, g, T2, c.bands, base, out_kind, out,
+                                      accumulate ? 1 : 0, sig, dcv.real(), dcv.imag(), c.st, c.lc);
+    });
+  } else {
+    stage(c, "I2_rows_inv_steer", [&] {
+      xcb::launch_rows_inv_steer(*c.prow, g, T2, c.bands, base, out_kind, out,
+                                 accumulate ? 1 : 0, sig, dcv.real(), dcv.imag(), c.st, c.lc);
+    });
+  }
+}
+
 void run_gather(Call& c, const xcb::SigSrc& sig, const double* base, void* out, int out_kind,
                 bool accumulate, bool dc) {
   const xcb::Geo& g = c.g;
@@ -567,23 +592,33 @@ void run_gather(Call& c, const xcb::SigSrc& sig, const double* base, void* out, 
       xcb::launch_cols_inv_corr(*c.pcol, g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);
     });
   }
-  const cplx dcv = dc ? std::conj(xcb::inner_dc_value(c.f->hf)) : cplx(0);  // engine.hpp:323
-  if (use_pair() && xcb::pair_smem(1, g.Pw, g)) {
-    stage(c, "I2_rows_inv_steer", [&] {
-      xcb::launch_rows_inv_steer_pair(g, T2, c.bands, base, out_kind, out, accumulate ? 1 : 0,
-                                      sig, dcv.real(), dcv.imag(), c.st, c.lc);
-    });
-  } else if (c.frow && xcb::fast_smem(1, *c.frow, g)) {
-    stage(c, "I2_rows_inv_steer", [&] {
-      xcb::launch_rows_inv_steer_fast(*c.frow, g, T2, c.bands, base, out_kind, out,
-                                      accumulate ? 1 : 0, sig, dcv.real(), dcv.imag(), c.st, c.lc);
-    });
-  } else {
-    stage(c, "I2_rows_inv_steer", [&] {
-      xcb::launch_rows_inv_steer(*c.prow, g, T2, c.bands, base, out_kind, out,
-                                 accumulate ? 1 : 0, sig, dcv.real(), dcv.imag(), c.st, c.lc);
-    });
+  launch_i2(c, sig, T2, base, out, out_kind, accumulate, dc);
+}
+
+// images per I1 launch for a gather call: the pair engine shares each staged
+// filter spectrum column between two images (halving its HBM reads)
+int gather_group(const Call& c) {
+  return use_pair() && xcb::pair_smem(0, c.g.Ph, c.g) ? xcb::pair_i1_images() : 1;
+}
+
+// gather over two images: F1/F2 per image, one I1 launch for both, I2 per image
+void run_gather2(Call& c, const xcb::SigSrc* sig, double* const* base, void* const* out,
+                 int out_kind, bool accumulate, bool dc) {
+  const xcb::Geo& g = c.g;
+  const size_t P = size_t(g.Ph) * g.Pw, tstride = size_t(c.bands.n) * g.H2 * g.Pw;
+  float2* T1 = c.ctx->buf<float2>("T1", size_t(g.Hx2) * g.Pw);
+  float2* Hh = c.ctx->buf<float2>("Hhat2", 2 * P);
+  float2* T2 = c.ctx->buf<float2>("T2g", 2 * tstride);
+  for (int i = 0; i < 2; ++i) {
+    stage(c, "F1_rows_fwd", [&] { xcb::launch_rows_fwd(*c.prow, g, sig[i], T1, c.st, c.lc); });
+    stage(c, "F2_cols_fwd", [&] { xcb::launch_cols_fwd(*c.pcol, g, T1, Hh + i * P, c.st, c.lc); });
   }
+  stage(c, "I1_cols_inv_corr", [&] {
+    xcb::launch_cols_inv_corr_pair(g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc, 2, P,
+                                   tstride);
+  });
+  for (int i = 0; i < 2; ++i)
+    launch_i2(c, sig[i], T2 + i * tstride, base[i], out[i], out_kind, accumulate, dc);
 }
 
 void run_scatter(Call& c, const xcb::SigSrc& sig, const double* base, void* out, int out_kind,
@@ -813,20 +848,39 @@ int xc_run(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d, const 
     ck(cudaEventCreate(&e1), "event");
     double gpu_s = 0;
     HostPipe hp(c);
-    hp.h2d(signal, param, 0);
+    const int G = mode == XC_CORRELATION ? gather_group(c) : 1;
+    for (int i = 0; i < G; ++i) hp.h2d(signal, param, i);
     ck(cudaEventRecord(e0, c.st), "event");
-    for (int img = 0; img < d->batch; ++img) {
-      hp.h2d(signal, param, img + 1);
-      Staged s = hp.inputs(signal, param, img);
-      double* base = nullptr;
-      prep(c, s, false, &base, nullptr);
-      void* dout = hp.out_buffer(out, img, os);
-      if (mode == XC_CORRELATION)
-        run_gather(c, s.sig, base, dout, out_kind, accumulate, dc);
-      else
-        run_scatter(c, s.sig, base, dout, out_kind, accumulate, dc);
-      ck(cudaGetLastError(), "kernel launch");
-      hp.done(out, img, dout, os);
+    for (int img = 0; img < d->batch;) {
+      const int n = std::min(G, d->batch - img);
+      for (int i = 0; i < n; ++i) hp.h2d(signal, param, img + G + i);  // next group
+      if (n == 2) {
+        Staged s[2];
+        double* base[2];
+        void* dout[2];
+        xcb::SigSrc sg[2];
+        for (int i = 0; i < 2; ++i) {
+          s[i] = hp.inputs(signal, param, img + i);
+          prep(c, s[i], false, &base[i], nullptr, i);
+          dout[i] = hp.out_buffer(out, img + i, os);
+          sg[i] = s[i].sig;
+        }
+        run_gather2(c, sg, base, dout, out_kind, accumulate, dc);
+        ck(cudaGetLastError(), "kernel launch");
+        for (int i = 0; i < 2; ++i) hp.done(out, img + i, dout[i], os);
+      } else {
+        Staged s = hp.inputs(signal, param, img);
+        double* base = nullptr;
+        prep(c, s, false, &base, nullptr);
+        void* dout = hp.out_buffer(out, img, os);
+        if (mode == XC_CORRELATION)
+          run_gather(c, s.sig, base, dout, out_kind, accumulate, dc);
+        else
+          run_scatter(c, s.sig, base, dout, out_kind, accumulate, dc);
+        ck(cudaGetLastError(), "kernel launch");
+        hp.done(out, img, dout, os);
+      }
+      img += n;
     }
     ck(cudaEventRecord(e1, c.st), "event");
     hp.finish();

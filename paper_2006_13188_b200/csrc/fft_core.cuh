@@ -97,33 +97,63 @@ __device__ __forceinline__ float2 tw_apply(float2 x, int e, const CTw<R>& tw) {
 }
 
 // ---------------------------------------------------------------- codelets
+__host__ __device__ constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
+__host__ __device__ constexpr int inv_mod(int a, int m) {  // a^{-1} mod m (gcd(a, m) = 1)
+  int r = 1;
+  while ((a * r) % m != 1) ++r;
+  return r;
+}
+
 // Dft<R>::run(v) transforms v in place; output X[k] ends at v[Dft<R>::pos(k)]
 // (compile-time permutation), so composites need no second R-element array.
+// R = A B with gcd(A, B) = 1 uses the prime-factor (Good-Thomas) mapping:
+// input n = (A n2 + B n1) mod R, output k = k1 (mod A), k2 (mod B): no
+// twiddle multiplies.  Other composites use Cooley-Tukey with constexpr
+// twiddles.
 template <int R>
 struct Dft {
   static constexpr int A = first_factor(R);
   static constexpr int B = R / A;
+  static constexpr bool kPfa = A > 1 && B > 1 && cgcd(A, B) == 1;
   __host__ __device__ static constexpr int pos(int k) {
-    // X[k1 + A k2] sits at v[B k1 + pos_B(k2)] after the B-point stage
-    return B * (k % A) + Dft<B>::pos(k / A);
+    // CT: X[k1 + A k2] sits at v[B k1 + pos_B(k2)] after the B-point stage;
+    // PFA: X[k] with k1 = k mod A, k2 = k mod B sits at v[B k1 + pos_B(k2)]
+    return kPfa ? B * (k % A) + Dft<B>::pos(k % B) : B * (k % A) + Dft<B>::pos(k / A);
   }
   __device__ __forceinline__ static void run(float2* v) {
-    constexpr CTw<R> tw{};
+    if constexpr (kPfa) {
+      float2 t[R];
 #pragma unroll
-    for (int n2 = 0; n2 < B; ++n2) {
-      float2 a[A];
+      for (int n2 = 0; n2 < B; ++n2) {
+        float2 a[A];
 #pragma unroll
-      for (int n1 = 0; n1 < A; ++n1) a[n1] = v[B * n1 + n2];
-      Dft<A>::run(a);
+        for (int n1 = 0; n1 < A; ++n1) a[n1] = v[(A * n2 + B * n1) % R];
+        Dft<A>::run(a);
 #pragma unroll
-      for (int k1 = 0; k1 < A; ++k1) {
-        const int e = (n2 * k1) % R;
-        const float2 x = a[Dft<A>::pos(k1)];
-        v[B * k1 + n2] = tw_apply<R>(x, e, tw);
+        for (int k1 = 0; k1 < A; ++k1) t[B * k1 + n2] = a[Dft<A>::pos(k1)];
       }
-    }
 #pragma unroll
-    for (int k1 = 0; k1 < A; ++k1) Dft<B>::run(v + B * k1);
+      for (int k1 = 0; k1 < A; ++k1) Dft<B>::run(t + B * k1);
+#pragma unroll
+      for (int i = 0; i < R; ++i) v[i] = t[i];
+    } else {
+      constexpr CTw<R> tw{};
+#pragma unroll
+      for (int n2 = 0; n2 < B; ++n2) {
+        float2 a[A];
+#pragma unroll
+        for (int n1 = 0; n1 < A; ++n1) a[n1] = v[B * n1 + n2];
+        Dft<A>::run(a);
+#pragma unroll
+        for (int k1 = 0; k1 < A; ++k1) {
+          const int e = (n2 * k1) % R;
+          const float2 x = a[Dft<A>::pos(k1)];
+          v[B * k1 + n2] = tw_apply<R>(x, e, tw);
+        }
+      }
+#pragma unroll
+      for (int k1 = 0; k1 < A; ++k1) Dft<B>::run(v + B * k1);
+    }
   }
 };
 

@@ -258,15 +258,18 @@ __global__ void __launch_bounds__(PF::T, 1)
 }
 
 // ------------------------------------------------------------------ I1 (interleaved)
-// conj(H^) for the thread's pass-0 inputs stays in registers for the whole
-// band loop; F^_k is TMA-staged into its own buffer, so a band needs two
-// barriers (after pass 0: stage free for the next band's copy; after pass 1).
-template <class PF>
+// conj(H^) of NI images at the thread's pass-0 inputs is parked in TMEM for
+// the whole band loop; F^_k is TMA-staged once per band and applied to all NI
+// images (the filter spectrum is image-independent, so its HBM read is shared).
+// Per (band, image): two barriers (after pass 0, after pass 1).
+template <class PF, int NI>
 __global__ void __launch_bounds__(PF::T, 1)
-    k_cols_inv_corr_ilv(Geo g, const float4* __restrict__ Hh, const float4* __restrict__ Fh,
-                        size_t sstride4, Bands bl, float2* __restrict__ T2,
+    k_cols_inv_corr_ilv(Geo g, const float4* __restrict__ Hh, size_t hstride4,
+                        const float4* __restrict__ Fh, size_t sstride4, Bands bl,
+                        float2* __restrict__ T2, size_t tstride,
                         const float2* __restrict__ twm, const float2* __restrict__ twl) {
   constexpr int L = PF::L;  // = Ph
+  constexpr uint32_t kCols = NI * 2 * PF::R0 * 5 <= 256 ? 256 : 512;
   extern __shared__ __align__(16) float4 smp[];
   float4* ST4 = smp;  // staged F^_k column pair, natural order
   float4* W04 = ST4 + L;
@@ -288,20 +291,23 @@ __global__ void __launch_bounds__(PF::T, 1)
     if (bl.n > 1) prefetch_l2(fsrc(1), kBytes);
   }
   // conj(H^) at this thread's pass-0 inputs n = j + r NB0, parked in TMEM
-  // (2 columns per r; warps of a lane quadrant side by side)
+  // (2 columns per r and image; warps of a lane quadrant side by side)
   __shared__ uint32_t tbase;
-  if (t < 32) tmem_alloc(&tbase, 256);
+  if (t < 32) tmem_alloc(&tbase, kCols);
   tmem_fence_before_sync();
   __syncthreads();
   tmem_fence_after_sync();
-  const uint32_t thc = tmem_warp_base(tbase) + uint32_t((t >> 7) * 2 * PF::R0);
+  const uint32_t thc = tmem_warp_base(tbase) + uint32_t((t >> 7) * NI * 2 * PF::R0);
   {
     const int gi = t & 1, j = t >> 1;
-    const float2* hcol = reinterpret_cast<const float2*>(Hh + size_t(c) * L) + gi;
 #pragma unroll
-    for (int r = 0; r < PF::R0; ++r)
-      tmem_st2(thc + 2 * r, j < PF::NB0 ? c_conj(__ldg(hcol + 2 * (j + r * PF::NB0)))
-                                        : make_float2(0.f, 0.f));
+    for (int im = 0; im < NI; ++im) {
+      const float2* hcol = reinterpret_cast<const float2*>(Hh + im * hstride4 + size_t(c) * L) + gi;
+#pragma unroll
+      for (int r = 0; r < PF::R0; ++r)
+        tmem_st2(thc + 2 * (im * PF::R0 + r),
+                 j < PF::NB0 ? c_conj(__ldg(hcol + 2 * (j + r * PF::NB0))) : make_float2(0.f, 0.f));
+    }
     tmem_wait_st();
   }
   for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
@@ -312,53 +318,57 @@ __global__ void __launch_bounds__(PF::T, 1)
   for (int bi = 0; bi < bl.n; ++bi) {
     mbar_wait(&bar, phase);
     phase ^= 1;
-    // conj(H^ conj(F^)) = conj(H^) F^ : inverse via conj-FFT-conj
-    {
-      float2 hc[PF::R0];
+#pragma unroll 1
+    for (int im = 0; im < NI; ++im) {
+      // conj(H^ conj(F^)) = conj(H^) F^ : inverse via conj-FFT-conj
+      {
+        float2 hc[PF::R0];
+        const uint32_t ta = thc + 2 * PF::R0 * opaque_i(im);
 #pragma unroll
-      for (int r = 0; r < PF::R0; ++r) hc[r] = tmem_ld2(thc + 2 * r);
-      tmem_wait_ld();
+        for (int r = 0; r < PF::R0; ++r) hc[r] = tmem_ld2(ta + 2 * r);
+        tmem_wait_ld();
 #pragma unroll
-      for (int r = 0; r < PF::R0; ++r) tmem_dep(hc[r]);
-      auto load = [&](int r, int n, int gi) -> float2 { return c_mul(hc[r], ST[2 * n + gi]); };
-      typename PF::P0Regs v;
-      PF::pass0_compute(load, v);
-      PF::pass0_store(W0, v);
-    }
-    __syncthreads();
-    if (t == 0 && bi + 1 < bl.n) {
-      fence_proxy_async();
-      mbar_expect_tx(&bar, kBytes);
-      bulk_copy(ST4, fsrc(bi + 1), kBytes, &bar);
-      if (bi + 2 < bl.n) prefetch_l2(fsrc(bi + 2), kBytes);
-    }
-    PF::pass1(W0, W1, TWs);
-    __syncthreads();
-    const int tt = opaque_i(t), gi = tt & 1, j = tt >> 1;
-    // output y = j + r NB2 - off: NB2 is even, so y & 1 is fixed and y >> 1
-    // advances by NB2 / 2 rows of T2 per r; valid r form [rlo, rhi)
-    const int y0 = j - g.off;
-    const int rstride = (PF::NB2 / 2) * 2 * g.Pw;  // float2 per r step (< 2^31: one plane)
-    float2* o = T2 + size_t(bi) * plane + 2 * (2 * c + gi) +
-                (ptrdiff_t(y0 >> 1) * (2 * g.Pw) + (y0 & 1));
-    const bool act = j < PF::NB2;
-    auto store = [&](float2 (&a)[PF::R2]) {
-      int y = opaque_i(y0);
-      float2* p = o;
-#pragma unroll
-      for (int r = 0; r < PF::R2; ++r) {
-        st_pred(p, c_conj(a[Dft<PF::R2>::pos(r)]), act && unsigned(y) < unsigned(g.H));
-        y += PF::NB2;
-        p += rstride;
+        for (int r = 0; r < PF::R0; ++r) tmem_dep(hc[r]);
+        auto load = [&](int r, int n, int gi) -> float2 { return c_mul(hc[r], ST[2 * n + gi]); };
+        typename PF::P0Regs v;
+        PF::pass0_compute(load, v);
+        PF::pass0_store(W0, v);
       }
-    };
-    PF::pass2_all(W1, tl, store);
+      __syncthreads();
+      if (t == 0 && im == NI - 1 && bi + 1 < bl.n) {
+        fence_proxy_async();
+        mbar_expect_tx(&bar, kBytes);
+        bulk_copy(ST4, fsrc(bi + 1), kBytes, &bar);
+        if (bi + 2 < bl.n) prefetch_l2(fsrc(bi + 2), kBytes);
+      }
+      PF::pass1(W0, W1, TWs);
+      __syncthreads();
+      const int tt = opaque_i(t), gi = tt & 1, j = tt >> 1;
+      // output y = j + r NB2 - off: NB2 is even, so y & 1 is fixed and y >> 1
+      // advances by NB2 / 2 rows of T2 per r
+      const int y0 = j - g.off;
+      const int rstride = (PF::NB2 / 2) * 2 * g.Pw;  // float2 per r step (< 2^31: one plane)
+      float2* o = T2 + im * tstride + size_t(bi) * plane + 2 * (2 * c + gi) +
+                  (ptrdiff_t(y0 >> 1) * (2 * g.Pw) + (y0 & 1));
+      const bool act = j < PF::NB2;
+      auto store = [&](float2 (&a)[PF::R2]) {
+        int y = opaque_i(y0);
+        float2* p = o;
+#pragma unroll
+        for (int r = 0; r < PF::R2; ++r) {
+          st_pred(p, c_conj(a[Dft<PF::R2>::pos(r)]), act && unsigned(y) < unsigned(g.H));
+          y += PF::NB2;
+          p += rstride;
+        }
+      };
+      PF::pass2_all(W1, tl, store);
+    }
   }
   tmem_fence_before_sync();
   __syncthreads();
   if (t < 32) {
     tmem_fence_after_sync();
-    tmem_dealloc(tbase, 256);
+    tmem_dealloc(tbase, kCols);
   }
 }
 
@@ -565,6 +575,18 @@ size_t pair_smem(int stage, int L, const Geo& g) {
   return s <= kSmemLimitP ? s : 0;
 }
 
+static int pair_mode();
+// Two images per I1 launch halve the filter-spectrum reads, but I1 is issue-
+// bound, not HBM-bound, so it measured slower (4.35 vs 3.88 ms per image on
+// config 5): off unless XCB_I1_IMAGES=2.
+int pair_i1_images() {
+  static const int n = [] {
+    const char* e = std::getenv("XCB_I1_IMAGES");
+    return e && e[0] == '2' ? 2 : 1;
+  }();
+  return pair_mode() == 2 ? 1 : n;
+}
+
 static int pair_mode() {  // XCB_PAIR: 1 interleaved (default), 2 pair-per-thread
   static const int m = [] {
     const char* e = std::getenv("XCB_PAIR");
@@ -575,7 +597,7 @@ static int pair_mode() {  // XCB_PAIR: 1 interleaved (default), 2 pair-per-threa
 
 void launch_cols_inv_corr_pair(const Geo& g, const float2* Hhat, const float2* Fhat,
                                size_t sstride, const Bands& b, float2* T2, cudaStream_t st,
-                               LaunchCounter& lc) {
+                               LaunchCounter& lc, int nimg, size_t hstride, size_t tstride) {
   const size_t sm = pair_smem(0, g.Ph, g);
 #define XCB_PAIR_I1(LL, R0, R1, R2)                                                       \
   if (g.Ph == LL) {                                                                       \
@@ -588,10 +610,14 @@ void launch_cols_inv_corr_pair(const Geo& g, const float2* Hhat, const float2* F
       set_smem(k_cols_inv_corr_pair<PF>, sm);                                             \
       k_cols_inv_corr_pair<PF><<<g.Pw / 2, PF::T, sm, st>>>(g, hh, fh, sstride / 2, b,    \
                                                             T2, tw.mid, tw.last);         \
+    } else if (nimg == 2) {                                                               \
+      set_smem(k_cols_inv_corr_ilv<IF, 2>, sm);                                           \
+      k_cols_inv_corr_ilv<IF, 2><<<g.Pw / 2, IF::T, sm, st>>>(                            \
+          g, hh, hstride / 2, fh, sstride / 2, b, T2, tstride, tw.mid, tw.last);          \
     } else {                                                                              \
-      set_smem(k_cols_inv_corr_ilv<IF>, sm);                                              \
-      k_cols_inv_corr_ilv<IF><<<g.Pw / 2, IF::T, sm, st>>>(g, hh, fh, sstride / 2, b, T2, \
-                                                           tw.mid, tw.last);              \
+      set_smem(k_cols_inv_corr_ilv<IF, 1>, sm);                                           \
+      k_cols_inv_corr_ilv<IF, 1><<<g.Pw / 2, IF::T, sm, st>>>(                            \
+          g, hh, hstride / 2, fh, sstride / 2, b, T2, tstride, tw.mid, tw.last);          \
     }                                                                                     \
   }
   XCB_PAIR_TABLE(XCB_PAIR_I1)

@@ -140,9 +140,15 @@ namespace xcb {
 // pair_smem returns the dynamic smem of stage 0 (I1) / 1 (I2), or 0 when the
 // length has no pair plan; callers then use the fast or generic kernels.
 size_t pair_smem(int stage, int L, const Geo& g);
+// nimg (1 or 2; 2 only on the interleaved engine) images per launch: Hhat and
+// T2 of image i at Hhat + i * hstride, T2 + i * tstride (float2 units); the
+// staged filter spectrum column is shared by the images.
 void launch_cols_inv_corr_pair(const Geo& g, const float2* Hhat, const float2* Fhat,
                                size_t sstride, const Bands& b, float2* T2, cudaStream_t st,
-                               LaunchCounter& lc);
+                               LaunchCounter& lc, int nimg = 1, size_t hstride = 0,
+                               size_t tstride = 0);
+// images per I1 launch the pair engine supports for this geometry
+int pair_i1_images();
 void launch_rows_inv_steer_pair(const Geo& g, const float2* T2, const Bands& b,
                                 const double* base, int out_kind, void* out, int accumulate,
                                 const SigSrc& dcs, double dcr, double dci, cudaStream_t st,

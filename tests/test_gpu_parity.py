@@ -5,6 +5,8 @@ same fp32 inputs) unless a reference test pins a looser bound (brute-force
 oracle 3e-3); peak locations exact.  Each test names the reference test or
 BASELINE config it follows.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -406,3 +408,48 @@ def test_pair_engine_geometry_edges(orc, h, w, periodic):
     xs = np.concatenate([r.integers(0, w, 40), [0, 0, w - 1, w - 1, 1]])
     ref = _direct_at(orc, Fo, H, T, ys, xs, periodic)
     assert orc.rel_l2(got[ys, xs], ref) < TOL
+
+
+@pytest.mark.parametrize("images_per_i1", ["1", "2"])
+def test_pair_engine_image_groups(orc, images_per_i1):
+    """Batches on the 4320 pad run I1 on two images per launch (one staged
+    filter spectrum shared): every image of an odd batch (a group of two plus
+    a single) must equal its single-image result bit for bit, through host and
+    device memory, and match the direct oracle at sampled pixels."""
+    import subprocess
+    import sys
+    if os.environ.get("XCB_I1_IMAGES", "1") != images_per_i1:
+        # the setting is read once per process: run this case in a child
+        env = dict(os.environ, XCB_I1_IMAGES=images_per_i1)
+        r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", __file__ +
+                            f"::test_pair_engine_image_groups[{images_per_i1}]"], env=env,
+                           capture_output=True, text=True)
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+        return
+    import torch
+    from paper_2006_13188_b200 import workloads as WL
+    wk = WL.config1(n=64)
+    r = np.random.default_rng(12)
+    n = 4100
+    H = r.uniform(0, 1, (3, n, n)).astype(np.float32)
+    T = r.uniform(0, 2 * np.pi, (3, n, n)).astype(np.float32)
+    batch = X.xcorr_fast(H, X.XformField.rotation(T), wk.filt).output
+    for b in range(3):
+        one = X.xcorr_fast(H[b], X.XformField.rotation(T[b]), wk.filt).output
+        assert np.array_equal(batch[b], one)
+    import ctypes as C
+    from paper_2006_13188_b200 import _native as N
+    hs, ts = torch.from_numpy(H).cuda(), torch.from_numpy(T).cuda()
+    out = torch.empty((3, n, n), dtype=torch.complex64, device="cuda")
+    d = N.ImageDesc(n, n, 3, N.XC_F32, N.XC_F32, N.XC_C64, N.XC_ROW_MAJOR, N.XC_DEVICE, 1,
+                    N.XC_ROTATION2)
+    ctx = N.context()
+    st = N.Stats()
+    N.check(N.lib().xc_run(ctx.handle, wk.filt.handle(), 0, C.byref(d), C.c_void_p(hs.data_ptr()),
+                           C.c_void_p(ts.data_ptr()), None, 0, 0, C.c_void_p(out.data_ptr()),
+                           C.byref(st)), ctx.handle)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), batch)
+    ys, xs = r.integers(0, n, 24), r.integers(0, n, 24)
+    ref = _direct_at(orc, ofilter(orc, wk.filt), H[1], T[1], ys, xs, False)
+    assert orc.rel_l2(batch[1][ys, xs], ref) < TOL

@@ -1,5 +1,8 @@
 """One hot-path invocation for ncu captures: config-5 geometry (4096^2, 65
-bands), one image, after one warm-up call (filter spectra built)."""
+bands), `batch` images, after one warm-up call (filter spectra built).
+
+  python tools/profile_case.py [xcorr|xconv] [config] [batch]
+"""
 import os
 import sys
 
@@ -9,9 +12,11 @@ from paper_2006_13188_b200 import workloads as WL  # noqa: E402
 
 mode = sys.argv[1] if len(sys.argv) > 1 else "xcorr"
 cfg = int(sys.argv[2]) if len(sys.argv) > 2 else 5
-w = WL.config5(batch=1) if cfg == 5 else WL.CONFIGS[cfg]()
-T = X.XformField.rotation(w.param[0]) if w.kind == 0 else X.XformField.scaling(w.param[0])
+nb = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+w = WL.config5(batch=nb) if cfg == 5 else WL.CONFIGS[cfg]()
+sig, par = (w.signal[0], w.param[0]) if nb == 1 else (w.signal[:nb], w.param[:nb])
+T = X.XformField.rotation(par) if w.kind == 0 else X.XformField.scaling(par)
 fn = {"xcorr": X.xcorr_fast, "xconv": X.xconv_fast}[mode]
 for _ in range(2):
-    r = fn(w.signal[0], T, w.filt)
+    r = fn(sig, T, w.filt)
 print("ok", r.standard_ops, r.seconds["fft"])
