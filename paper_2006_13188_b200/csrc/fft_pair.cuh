@@ -271,6 +271,24 @@ struct IlvFft {
 
   // f(a) with every output of the butterfly: k = j + r NB2 is a[pos(r)];
   // runs on every thread (threads past NB2 compute a dummy butterfly)
+  // pass 2 with the thread's full twiddle row w[r] = W_L^{j r}, r = 1..R2-1
+  // (read from TMEM by the caller; w[0] unused)
+  template <class F>
+  __device__ __forceinline__ static void pass2_all_w(const float2* W1, const float2* w, F& f) {
+    const int t = opaque_i(threadIdx.x), g = t & 1;
+    const int j = (t >> 1) < NB2 ? (t >> 1) : 0;
+    float2 a[R2];
+    const float2* s = W1 + at(j, g);
+#pragma unroll
+    for (int r = 0; r < R2; ++r) a[r] = s[r * lin<NB2>()];
+#pragma unroll
+    for (int r = 1; r < R2; ++r) a[r] = c_mul(a[r], w[r]);
+    Dft<R2>::run(a);
+    f(a);
+  }
+  static constexpr int kTwCols = 2 * (R2 - 1);  // TMEM columns of the full twiddle row
+  static constexpr int kTwColsPad = (kTwCols + 3) / 4 * 4;
+
   template <class F>
   __device__ __forceinline__ static void pass2_all(const float2* W1, const LastTw& tl, F& f) {
     const int t = opaque_i(threadIdx.x), g = t & 1;

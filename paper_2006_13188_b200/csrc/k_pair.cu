@@ -257,6 +257,17 @@ __global__ void __launch_bounds__(PF::T, 1)
   }
 }
 
+// the thread's full pass-2 twiddle row W_L^{j r} (r = 1..R2-1) into TMEM at ta
+// (2 columns each; table twf is [r-1][j], j < NB2); warp-collective
+template <class PF>
+__device__ __forceinline__ void park_last_tw(const float2* __restrict__ twf, uint32_t ta) {
+  const int j = threadIdx.x >> 1;
+#pragma unroll
+  for (int r = 1; r < PF::R2; ++r)
+    tmem_st2(ta + 2 * (r - 1), j < PF::NB2 ? __ldg(twf + (r - 1) * PF::NB2 + j)
+                                           : make_float2(1.f, 0.f));
+}
+
 // ------------------------------------------------------------------ I1 (interleaved)
 // conj(H^) of NI images at the thread's pass-0 inputs is parked in TMEM for
 // the whole band loop; F^_k is TMA-staged once per band and applied to all NI
@@ -267,9 +278,13 @@ __global__ void __launch_bounds__(PF::T, 1)
     k_cols_inv_corr_ilv(Geo g, const float4* __restrict__ Hh, size_t hstride4,
                         const float4* __restrict__ Fh, size_t sstride4, Bands bl,
                         float2* __restrict__ T2, size_t tstride,
-                        const float2* __restrict__ twm, const float2* __restrict__ twl) {
+                        const float2* __restrict__ twm, const float2* __restrict__ twf) {
   constexpr int L = PF::L;  // = Ph
-  constexpr uint32_t kCols = NI * 2 * PF::R0 * 5 <= 256 ? 256 : 512;
+  // TMEM per thread: conj(H^) (2 R0 columns per image), then the pass-2
+  // twiddle row; warps of a lane quadrant side by side (up to 5 of 18)
+  constexpr int kThr = NI * 2 * PF::R0 + PF::kTwColsPad;
+  constexpr uint32_t kCols = kThr * 5 <= 256 ? 256 : 512;
+  static_assert(kThr * 5 <= 512, "TMEM budget");
   extern __shared__ __align__(16) float4 smp[];
   float4* ST4 = smp;  // staged F^_k column pair, natural order
   float4* W04 = ST4 + L;
@@ -297,7 +312,8 @@ __global__ void __launch_bounds__(PF::T, 1)
   tmem_fence_before_sync();
   __syncthreads();
   tmem_fence_after_sync();
-  const uint32_t thc = tmem_warp_base(tbase) + uint32_t((t >> 7) * NI * 2 * PF::R0);
+  const uint32_t thc = tmem_warp_base(tbase) + uint32_t((t >> 7) * kThr);
+  const uint32_t ttw = thc + NI * 2 * PF::R0;
   {
     const int gi = t & 1, j = t >> 1;
 #pragma unroll
@@ -308,11 +324,10 @@ __global__ void __launch_bounds__(PF::T, 1)
         tmem_st2(thc + 2 * (im * PF::R0 + r),
                  j < PF::NB0 ? c_conj(__ldg(hcol + 2 * (j + r * PF::NB0))) : make_float2(0.f, 0.f));
     }
+    park_last_tw<PF>(twf, ttw);
     tmem_wait_st();
   }
   for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
-  typename PF::LastTw tl;
-  PF::load_last_tw(twl, tl);
   __syncthreads();
   unsigned phase = 0;
   for (int bi = 0; bi < bl.n; ++bi) {
@@ -324,11 +339,9 @@ __global__ void __launch_bounds__(PF::T, 1)
       {
         float2 hc[PF::R0];
         const uint32_t ta = thc + 2 * PF::R0 * opaque_i(im);
-#pragma unroll
-        for (int r = 0; r < PF::R0; ++r) hc[r] = tmem_ld2(ta + 2 * r);
+        tmem_ldn<2 * PF::R0>(ta, reinterpret_cast<float*>(hc));
         tmem_wait_ld();
-#pragma unroll
-        for (int r = 0; r < PF::R0; ++r) tmem_dep(hc[r]);
+        tmem_depn<2 * PF::R0>(reinterpret_cast<float*>(hc));
         auto load = [&](int r, int n, int gi) -> float2 { return c_mul(hc[r], ST[2 * n + gi]); };
         typename PF::P0Regs v;
         PF::pass0_compute(load, v);
@@ -361,7 +374,11 @@ __global__ void __launch_bounds__(PF::T, 1)
           p += rstride;
         }
       };
-      PF::pass2_all(W1, tl, store);
+      float2 w[PF::kTwColsPad / 2 + 1];
+      tmem_ldn<PF::kTwColsPad>(ttw, reinterpret_cast<float*>(w + 1));
+      tmem_wait_ld();
+      tmem_depn<PF::kTwColsPad>(reinterpret_cast<float*>(w + 1));
+      PF::pass2_all_w(W1, w, store);
     }
   }
   tmem_fence_before_sync();
@@ -522,7 +539,8 @@ constexpr size_t kSmemLimitP = 232448;
 // exact twiddle tables of a pair plan (fp64 -> fp32), per device
 struct PairTw {
   float2* mid = nullptr;
-  float2* last = nullptr;
+  float2* last = nullptr;   // split rows (pair-per-thread kernels)
+  float2* lastf = nullptr;  // full rows [r-1][j], r = 1..R2-1 (interleaved kernels)
 };
 
 template <class PF>
@@ -548,12 +566,21 @@ PairTw pair_tables() {
       const double a = -tp * double(e) / double(PF::L);
       l[(r - 1) * PF::NB2 + j] = make_float2(float(std::cos(a)), float(std::sin(a)));
     }
+  std::vector<float2> lf(size_t(PF::R2 - 1) * PF::NB2);
+  for (int r = 1; r < PF::R2; ++r)
+    for (int j = 0; j < PF::NB2; ++j) {
+      const long e = long(j) * r % PF::L;
+      const double a = -tp * double(e) / double(PF::L);
+      lf[size_t(r - 1) * PF::NB2 + j] = make_float2(float(std::cos(a)), float(std::sin(a)));
+    }
   PairTw p;
   if (cudaMalloc(&p.mid, m.size() * sizeof(float2)) != cudaSuccess ||
-      cudaMalloc(&p.last, l.size() * sizeof(float2)) != cudaSuccess)
+      cudaMalloc(&p.last, l.size() * sizeof(float2)) != cudaSuccess ||
+      cudaMalloc(&p.lastf, lf.size() * sizeof(float2)) != cudaSuccess)
     return PairTw{};
   cudaMemcpy(p.mid, m.data(), m.size() * sizeof(float2), cudaMemcpyHostToDevice);
   cudaMemcpy(p.last, l.data(), l.size() * sizeof(float2), cudaMemcpyHostToDevice);
+  cudaMemcpy(p.lastf, lf.data(), lf.size() * sizeof(float2), cudaMemcpyHostToDevice);
   cache[dev] = p;
   return p;
 }
@@ -613,11 +640,11 @@ void launch_cols_inv_corr_pair(const Geo& g, const float2* Hhat, const float2* F
     } else if (nimg == 2) {                                                               \
       set_smem(k_cols_inv_corr_ilv<IF, 2>, sm);                                           \
       k_cols_inv_corr_ilv<IF, 2><<<g.Pw / 2, IF::T, sm, st>>>(                            \
-          g, hh, hstride / 2, fh, sstride / 2, b, T2, tstride, tw.mid, tw.last);          \
+          g, hh, hstride / 2, fh, sstride / 2, b, T2, tstride, tw.mid, tw.lastf);         \
     } else {                                                                              \
       set_smem(k_cols_inv_corr_ilv<IF, 1>, sm);                                           \
       k_cols_inv_corr_ilv<IF, 1><<<g.Pw / 2, IF::T, sm, st>>>(                            \
-          g, hh, hstride / 2, fh, sstride / 2, b, T2, tstride, tw.mid, tw.last);          \
+          g, hh, hstride / 2, fh, sstride / 2, b, T2, tstride, tw.mid, tw.lastf);         \
     }                                                                                     \
   }
   XCB_PAIR_TABLE(XCB_PAIR_I1)

@@ -72,6 +72,86 @@ __device__ __forceinline__ void tmem_st4(uint32_t taddr, float4 v) {
                : "memory");
 }
 
+// N = 8 / 16 consecutive columns into v[0..N) (warp-collective)
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(
+          taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+      "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15]))
+      : "memory");
+}
+// N consecutive columns (N a multiple of 4) as the fewest x16 / x8 / x4
+// accesses; pair with one tmem_wait_ld / tmem_wait_st
+template <int N>
+__device__ __forceinline__ void tmem_ldn(uint32_t taddr, float* v) {
+  static_assert(N % 4 == 0, "columns in multiples of 4");
+  int o = 0;
+#pragma unroll
+  for (; o + 16 <= N; o += 16) tmem_ld16(taddr + o, v + o);
+  if constexpr (N % 16 >= 8) {
+    tmem_ld8(taddr + (N / 16) * 16, v + (N / 16) * 16);
+  }
+  if constexpr (N % 8 == 4) {
+    const float4 q = tmem_ld4(taddr + N - 4);
+    v[N - 4] = q.x;
+    v[N - 3] = q.y;
+    v[N - 2] = q.z;
+    v[N - 1] = q.w;
+  }
+}
+template <int N>
+__device__ __forceinline__ void tmem_stn(uint32_t taddr, const float* v) {
+  static_assert(N % 4 == 0, "columns in multiples of 4");
+#pragma unroll
+  for (int o = 0; o + 16 <= N; o += 16) tmem_st16(taddr + o, v + o);
+  if constexpr (N % 16 >= 8) tmem_st8(taddr + (N / 16) * 16, v + (N / 16) * 16);
+  if constexpr (N % 8 == 4)
+    tmem_st4(taddr + N - 4, make_float4(v[N - 4], v[N - 3], v[N - 2], v[N - 1]));
+}
+template <int N>
+__device__ __forceinline__ void tmem_depn(float* v) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) asm volatile("" : "+f"(v[i]));
+}
+
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
