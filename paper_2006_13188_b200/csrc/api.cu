@@ -1017,7 +1017,9 @@ int xc_anglemax(xc_context ctx, xc_filter f, const xc_image_desc* d, const void*
           xcb::launch_cols_inv_corr(*c.pcol, c.g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);
       });
       stage(c, "I2_rows_inv_planes", [&] {
-        if (c.frow && xcb::fast_smem(4, *c.frow, c.g))
+        if (use_pair() && xcb::pair_smem(2, c.g.Pw, c.g))
+          xcb::launch_rows_inv_planes_pair(c.g, T2, c.bands.n, planes, c.st, c.lc);
+        else if (c.frow && xcb::fast_smem(4, *c.frow, c.g))
           xcb::launch_rows_inv_planes_fast(*c.frow, c.g, T2, c.bands.n, planes, c.st, c.lc);
         else
           xcb::launch_rows_inv_planes(*c.prow, c.g, T2, c.bands.n, planes, c.st, c.lc);

@@ -146,9 +146,67 @@ __global__ void __launch_bounds__(128)
 //        = DFT_N2[ m -> G_k w^{k s1}, m = k mod N2 ](s2),  w = e^{-2 pi i / 360},
 // so each pixel costs N1 twiddled N2-point DFTs instead of 360 x (2 KH + 1)
 // complex MACs.  Ties keep the smallest s (the oracle's first maximum).
+// constexpr e^{-2 pi i e / 360} (angle-max twiddles folded to immediates)
+struct Tw360 {
+  float re[360], im[360];
+  __host__ __device__ constexpr Tw360() : re(), im() {
+    for (int e = 0; e < 360; ++e) {
+      re[e] = float(cx_cos_frac(e, 360));
+      im[e] = float(-cx_sin_frac(e, 360));
+    }
+  }
+};
+
+// 360-angle max for bands inside [-KH, KH]: S(s1 + N1 s2) =
+// DFT_N2[ G_d w^{d s1} ] (w = e^{-2 pi i / 360}, d = k mod N2), N1 = 360 / N2.
+// The s1 loop is unrolled so every twiddle is an immediate; the running max
+// takes the first angle in scan order (s1-major) on exact ties.
 template <int KH, int N2, class TO>
 __global__ void __launch_bounds__(128)
     k_anglemax_fft(const float2* __restrict__ planes, AngleMap m, size_t npix,
+                   TO* __restrict__ score, int* __restrict__ argmax) {
+  constexpr int ND = 2 * KH + 1, N = 360, N1 = N / N2;
+  static_assert(N1 * N2 == N && N2 >= ND, "bad angle-max split");
+  constexpr Tw360 tw{};
+  const size_t p = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+  if (p >= npix) return;
+  float2 G[ND];
+#pragma unroll
+  for (int d = 0; d < ND; ++d)
+    G[d] = m.idx[d] >= 0 ? planes[size_t(m.idx[d]) * npix + p] : make_float2(0.f, 0.f);
+  float best = -1.f;
+  int arg = 0;
+#pragma unroll
+  for (int s1 = 0; s1 < N1; ++s1) {
+    float2 v[N2];
+#pragma unroll
+    for (int q = 0; q < N2; ++q) v[q] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+      const int e = (((d - KH) * s1) % N + N) % N;
+      v[((d - KH) % N2 + N2) % N2] =
+          e == 0 ? G[d] : c_mul(G[d], make_float2(tw.re[e], tw.im[e]));
+    }
+    Dft<N2>::run(v);
+#pragma unroll
+    for (int s2 = 0; s2 < N2; ++s2) {
+      const float2 x = v[Dft<N2>::pos(s2)];
+      const float m2 = fmaf(x.x, x.x, x.y * x.y);
+      if (m2 > best) {
+        best = m2;
+        arg = s1 + N1 * s2;
+      }
+    }
+  }
+  score[p] = TO(sqrtf(best));
+  if (argmax) argmax[p] = arg;
+}
+
+// Looped variant (twiddles from a smem table) for wide band spans, where the
+// unrolled kernel would not fit in registers.
+template <int KH, int N2, class TO>
+__global__ void __launch_bounds__(128)
+    k_anglemax_fft_loop(const float2* __restrict__ planes, AngleMap m, size_t npix,
                    TO* __restrict__ score, int* __restrict__ argmax) {
   constexpr int ND = 2 * KH + 1, N = 360, N1 = N / N2;
   static_assert(N1 * N2 == N && N2 >= ND, "bad angle-max split");
@@ -266,16 +324,17 @@ void launch_anglemax(const float2* planes, const int* ks_host, int nb, size_t np
     fm.nd = 2 * KH + 1;
     for (int d = 0; d < fm.nd; ++d) fm.idx[d] = -1;
     for (int i = 0; i < nb; ++i) fm.idx[ks_host[i] + KH] = i;
-#define XCB_AM(KHV, N2V)                                                                     \
+#define XCB_AM(KHV, N2V, KER)                                                                \
   if (KH == KHV) {                                                                         \
     if (score_f64)                                                                         \
-      k_anglemax_fft<KHV, N2V, double><<<grid, bs, 0, st>>>(planes, fm, npix,              \
-                                                           static_cast<double*>(score), argmax); \
+      KER<KHV, N2V, double><<<grid, bs, 0, st>>>(planes, fm, npix,                         \
+                                                static_cast<double*>(score), argmax);      \
     else                                                                                   \
-      k_anglemax_fft<KHV, N2V, float><<<grid, bs, 0, st>>>(planes, fm, npix,               \
-                                                          static_cast<float*>(score), argmax);  \
+      KER<KHV, N2V, float><<<grid, bs, 0, st>>>(planes, fm, npix,                          \
+                                               static_cast<float*>(score), argmax);        \
   }
-    XCB_AM(4, 12) XCB_AM(8, 18) XCB_AM(16, 36) XCB_AM(32, 72)
+    XCB_AM(4, 12, k_anglemax_fft) XCB_AM(8, 18, k_anglemax_fft)
+    XCB_AM(16, 36, k_anglemax_fft) XCB_AM(32, 72, k_anglemax_fft_loop)
 #undef XCB_AM
     ++lc.n;
     return;

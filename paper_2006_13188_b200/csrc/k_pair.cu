@@ -534,6 +534,81 @@ __global__ void __launch_bounds__(PF::T, 1)
   }
 }
 
+// ------------------------------------------------------------------ planes (interleaved)
+// Angle-max front end: per band, row IFFT of T2_b, crop, store the band plane
+// G_b = H * F_b (engine.hpp:304-311 per band); k_anglemax_* then reads all
+// bands per pixel.  Same engine as I2 without the steering; a warp's store
+// covers 16 consecutive pixels of both rows (two full 128-byte lines).
+template <class PF>
+__global__ void __launch_bounds__(PF::T, 1)
+    k_rows_inv_planes_ilv(Geo g, const float4* __restrict__ T2, int nbands,
+                          float2* __restrict__ planes, float scale,
+                          const float2* __restrict__ twm, const float2* __restrict__ twl) {
+  constexpr int L = PF::L;  // = Pw
+  constexpr int R2 = PF::R2;
+  extern __shared__ __align__(16) float4 smp[];
+  float4* ST4 = smp;
+  float4* W04 = ST4 + L;
+  float4* W14 = W04 + PF::LP;
+  float2* TWs = reinterpret_cast<float2*>(W14 + PF::LP);
+  const float2* ST = reinterpret_cast<const float2*>(ST4);
+  float2* W0 = reinterpret_cast<float2*>(W04);
+  float2* W1 = reinterpret_cast<float2*>(W14);
+  const int b = blockIdx.x, t = threadIdx.x;
+  const size_t plane4 = size_t(g.H2 / 2) * g.Pw;
+  const float4* rowp = T2 + size_t(b) * g.Pw;
+  constexpr unsigned kBytes = unsigned(L * sizeof(float4));
+  __shared__ __align__(8) uint64_t bar;
+  if (t == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(&bar, kBytes);
+    bulk_copy(ST4, rowp, kBytes, &bar);
+    if (nbands > 1) prefetch_l2(rowp + plane4, kBytes);
+  }
+  for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
+  typename PF::LastTw tl;
+  PF::load_last_tw(twl, tl);
+  __syncthreads();
+  const size_t npix = size_t(g.H) * g.W;
+  unsigned phase = 0;
+  for (int bi = 0; bi < nbands; ++bi) {
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    auto load = [&](int, int n, int gi) -> float2 { return c_conj(ST[2 * n + gi]); };
+    {
+      typename PF::P0Regs v;
+      PF::pass0_compute(load, v);
+      PF::pass0_store(W0, v);
+    }
+    __syncthreads();
+    if (t == 0 && bi + 1 < nbands) {
+      fence_proxy_async();
+      mbar_expect_tx(&bar, kBytes);
+      bulk_copy(ST4, rowp + size_t(bi + 1) * plane4, kBytes, &bar);
+      if (bi + 2 < nbands) prefetch_l2(rowp + size_t(bi + 2) * plane4, kBytes);
+    }
+    PF::pass1(W0, W1, TWs);
+    __syncthreads();
+    const int tt = opaque_i(t), gi = tt & 1, j = tt >> 1, y = 2 * b + gi;
+    const int x0 = j - g.off;
+    float2* o = planes + size_t(bi) * npix + size_t(y) * g.W + x0;
+    const bool act = j < PF::NB2 && y < g.H;
+    auto store = [&](float2 (&a)[R2]) {
+      int x = opaque_i(x0);
+      float2* p = o;
+#pragma unroll
+      for (int r = 0; r < R2; ++r) {
+        st_pred(p, c_scale(c_conj(a[Dft<R2>::pos(r)]), scale),
+                act && unsigned(x) < unsigned(g.W));
+        x += PF::NB2;
+        p += PF::NB2;
+      }
+    };
+    PF::pass2_all(W1, tl, store);
+  }
+}
+
 constexpr size_t kSmemLimitP = 232448;
 
 // exact twiddle tables of a pair plan (fp64 -> fp32), per device
@@ -595,7 +670,8 @@ size_t pair_smem(int stage, int L, const Geo& g) {
     using PF = PairFft<LL, R0, R1, R2>;                                            \
     const size_t tw = size_t(PF::TWM) * sizeof(float2);                            \
     if (stage == 0) s = (size_t(LL) + 2 * size_t(PF::LP)) * sizeof(float4) + tw;   \
-    if (stage == 1) s = (2 * size_t(PF::LP) + size_t(LL)) * sizeof(float4) + tw;   \
+    if (stage == 1 || stage == 2)                                                  \
+      s = (2 * size_t(PF::LP) + size_t(LL)) * sizeof(float4) + tw;                 \
   }
   XCB_PAIR_TABLE(XCB_PAIR_SMEM)
 #undef XCB_PAIR_SMEM
@@ -649,6 +725,24 @@ void launch_cols_inv_corr_pair(const Geo& g, const float2* Hhat, const float2* F
   }
   XCB_PAIR_TABLE(XCB_PAIR_I1)
 #undef XCB_PAIR_I1
+  ++lc.n;
+}
+
+void launch_rows_inv_planes_pair(const Geo& g, const float2* T2, int nbands, float2* planes,
+                                 cudaStream_t st, LaunchCounter& lc) {
+  const size_t sm = pair_smem(2, g.Pw, g);
+  const float scale = float(1.0 / (double(g.Ph) * double(g.Pw)));
+#define XCB_PAIR_PL(LL, R0, R1, R2)                                                        \
+  if (g.Pw == LL) {                                                                        \
+    using PF = PairFft<LL, R0, R1, R2>;                                                    \
+    using IF = IlvFft<LL, R0, R1, R2>;                                                     \
+    const PairTw tw = pair_tables<PF>();                                                   \
+    set_smem(k_rows_inv_planes_ilv<IF>, sm);                                               \
+    k_rows_inv_planes_ilv<IF><<<g.H2 / 2, IF::T, sm, st>>>(                                \
+        g, reinterpret_cast<const float4*>(T2), nbands, planes, scale, tw.mid, tw.last);   \
+  }
+  XCB_PAIR_TABLE(XCB_PAIR_PL)
+#undef XCB_PAIR_PL
   ++lc.n;
 }
 
