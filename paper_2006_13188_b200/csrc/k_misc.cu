@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Per-pixel stages: steering base / guard band, dtype conversion, smooth divide, angle max.
 #include <algorithm>
 
@@ -146,28 +147,27 @@ __global__ void __launch_bounds__(128)
 //        = DFT_N2[ m -> G_k w^{k s1}, m = k mod N2 ](s2),  w = e^{-2 pi i / 360},
 // so each pixel costs N1 twiddled N2-point DFTs instead of 360 x (2 KH + 1)
 // complex MACs.  Ties keep the smallest s (the oracle's first maximum).
-// constexpr e^{-2 pi i e / 360} (angle-max twiddles folded to immediates)
-struct Tw360 {
-  float re[360], im[360];
-  __host__ __device__ constexpr Tw360() : re(), im() {
-    for (int e = 0; e < 360; ++e) {
-      re[e] = float(cx_cos_frac(e, 360));
-      im[e] = float(-cx_sin_frac(e, 360));
-    }
-  }
-};
-
 // 360-angle max for bands inside [-KH, KH]: S(s1 + N1 s2) =
 // DFT_N2[ G_d w^{d s1} ] (w = e^{-2 pi i / 360}, d = k mod N2), N1 = 360 / N2.
-// The s1 loop is unrolled so every twiddle is an immediate; the running max
-// takes the first angle in scan order (s1-major) on exact ties.
-template <int KH, int N2, class TO>
-__global__ void __launch_bounds__(128)
-    k_anglemax_fft(const float2* __restrict__ planes, AngleMap m, size_t npix,
-                   TO* __restrict__ score, int* __restrict__ argmax) {
+// The s1 loop runs U trips per unrolled body (the body must stay small enough
+// for the instruction cache); twiddles are smem broadcast reads; the running
+// max takes the first angle in scan order (s1-major) on exact ties.
+template <int KH, int N2, class TO, int U>
+__device__ __forceinline__ void anglemax_fft_body(const float2* __restrict__ planes,
+                                                  const AngleMap& m, size_t npix,
+                                                  TO* __restrict__ score,
+                                                  int* __restrict__ argmax) {
   constexpr int ND = 2 * KH + 1, N = 360, N1 = N / N2;
-  static_assert(N1 * N2 == N && N2 >= ND, "bad angle-max split");
-  constexpr Tw360 tw{};
+  static_assert(N1 * N2 == N && N2 >= ND && N1 % U == 0, "bad angle-max split");
+  // twiddles w^{(d - KH) s1}, [s1][d] (broadcast reads)
+  __shared__ float2 tws[N1 * ND];
+  for (int i = threadIdx.x; i < N1 * ND; i += blockDim.x) {
+    const int s1 = i / ND, d = i % ND;
+    double sn, cs;
+    sincospi(-2.0 * double((d - KH) * s1) / N, &sn, &cs);
+    tws[i] = make_float2(float(cs), float(sn));
+  }
+  __syncthreads();
   const size_t p = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
   if (p >= npix) return;
   float2 G[ND];
@@ -176,17 +176,14 @@ __global__ void __launch_bounds__(128)
     G[d] = m.idx[d] >= 0 ? planes[size_t(m.idx[d]) * npix + p] : make_float2(0.f, 0.f);
   float best = -1.f;
   int arg = 0;
-#pragma unroll
+#pragma unroll U
   for (int s1 = 0; s1 < N1; ++s1) {
     float2 v[N2];
 #pragma unroll
     for (int q = 0; q < N2; ++q) v[q] = make_float2(0.f, 0.f);
+    const float2* tw = tws + s1 * ND;
 #pragma unroll
-    for (int d = 0; d < ND; ++d) {
-      const int e = (((d - KH) * s1) % N + N) % N;
-      v[((d - KH) % N2 + N2) % N2] =
-          e == 0 ? G[d] : c_mul(G[d], make_float2(tw.re[e], tw.im[e]));
-    }
+    for (int d = 0; d < ND; ++d) v[((d - KH) % N2 + N2) % N2] = c_mul(G[d], tw[d]);
     Dft<N2>::run(v);
 #pragma unroll
     for (int s2 = 0; s2 < N2; ++s2) {
@@ -201,6 +198,18 @@ __global__ void __launch_bounds__(128)
   score[p] = TO(sqrtf(best));
   if (argmax) argmax[p] = arg;
 }
+
+#define XCB_AM_KERNEL(NAME, U)                                                        \
+  template <int KH, int N2, class TO>                                                 \
+  __global__ void __launch_bounds__(128)                                              \
+      NAME(const float2* __restrict__ planes, AngleMap m, size_t npix,                \
+           TO* __restrict__ score, int* __restrict__ argmax) {                        \
+    anglemax_fft_body<KH, N2, TO, U>(planes, m, npix, score, argmax);                 \
+  }
+// measured on config 3 (KH = 16): one s1 per loop trip 4.83 ms, two 4.91,
+// five 6.59 (instruction-cache misses), fully unrolled 5.45
+XCB_AM_KERNEL(k_anglemax_fft, 1)
+#undef XCB_AM_KERNEL
 
 // Looped variant (twiddles from a smem table) for wide band spans, where the
 // unrolled kernel would not fit in registers.
