@@ -453,3 +453,48 @@ def test_pair_engine_image_groups(orc, images_per_i1):
     ys, xs = r.integers(0, n, 24), r.integers(0, n, 24)
     ref = _direct_at(orc, ofilter(orc, wk.filt), H[1], T[1], ys, xs, False)
     assert orc.rel_l2(batch[1][ys, xs], ref) < TOL
+
+
+def _bands_at(orc, F, H, ys, xs):
+    """G_k(p) = sum_u conj(F_k(u)) H(p + u) (fft.hpp:74-77, zero padding) per band at
+    the sampled pixels, in double; shape (bands, samples)."""
+    R = int(np.ceil(F.r_max))
+    side = 2 * R + 1
+    comps = np.stack([orc.render_component(F, ci, side, side, R, R) for ci in range(len(F.ks))])
+    h, w = H.shape
+    d = np.arange(-R, R + 1)
+    G = np.zeros((len(F.ks), len(ys)), np.complex128)
+    for i, (y, x) in enumerate(zip(ys, xs)):
+        yy, xx = y + d, x + d
+        patch = np.zeros((side, side))
+        vy, vx = (yy >= 0) & (yy < h), (xx >= 0) & (xx < w)
+        patch[np.ix_(vy, vx)] = H[np.ix_(yy[vy], xx[vx])]
+        G[:, i] = np.einsum("kab,ab->k", np.conj(comps), patch)
+    return G
+
+
+def test_config3_full_size_anglemax(orc):
+    """BASELINE config 3 at full size (4096^2, 33 bands, 360 angles): score and
+    argmax at sampled pixels (including the pasted templates' centres) against
+    the direct per-band correlation + the oracle's angle max, and the top-3 NMS
+    peaks at the templates (vote_filter.hpp:107-134)."""
+    from paper_2006_13188_b200 import workloads as WL
+    w = WL.config3()
+    OF = ofilter(orc, w.filt)
+    score, arg = X.anglemax(w.signal[0], w.filt, 360)
+    truth = w.meta["truth"]
+    r = np.random.default_rng(31)
+    n = score.shape[0]
+    ys = np.concatenate([r.integers(0, n, 30), [int(round(cy)) for _, cy, _ in truth], [0, n - 1]])
+    xs = np.concatenate([r.integers(0, n, 30), [int(round(cx)) for cx, _, _ in truth], [n - 1, 0]])
+    G = _bands_at(orc, OF, w.signal[0].astype(np.float64), ys, xs)
+    oscore, oarg = orc.anglemax(G[:, None, :], OF.ks, 360)
+    oscore = oscore[0]
+    assert orc.rel_l2(score[ys, xs], oscore) < TOL
+    at = np.abs(np.sum(G * np.exp(-2j * np.pi * np.asarray(OF.ks)[:, None] * arg[ys, xs][None] / 360),
+                       axis=0))
+    assert np.all(at >= oscore * (1 - 1e-5) - 1e-9)
+    pk = X.find_peaks(score.astype(np.float64), 32.0, 0.5)
+    assert len(pk) >= 3
+    for (cx, cy, _), p in zip(sorted(truth), sorted(pk[:3], key=lambda q: q.x)):
+        assert abs(p.x - cx) <= 2 and abs(p.y - cy) <= 2
