@@ -627,7 +627,11 @@ void run_scatter(Call& c, const xcb::SigSrc& sig, const double* base, void* out,
   float2* T1 = c.ctx->buf<float2>("T1b", size_t(c.bands.n) * g.Hx2 * g.Pw);
   float2* Sg = c.ctx->buf<float2>("Sigma", size_t(g.Ph) * g.Pw);
   float2* T2 = c.ctx->buf<float2>("T2s", size_t(g.H2) * g.Pw);
-  if (c.frow && xcb::fast_smem(2, *c.frow, g)) {
+  if (use_pair() && xcb::pair_smem(3, g.Pw, g)) {
+    stage(c, "S1_rows_fwd_premul", [&] {
+      xcb::launch_rows_fwd_premul_pair(g, sig, base, c.bands, T1, c.st, c.lc);
+    });
+  } else if (c.frow && xcb::fast_smem(2, *c.frow, g)) {
     stage(c, "S1_rows_fwd_premul", [&] {
       xcb::launch_rows_fwd_premul_fast(*c.frow, g, sig, base, c.bands, T1, c.st, c.lc);
     });
@@ -636,7 +640,11 @@ void run_scatter(Call& c, const xcb::SigSrc& sig, const double* base, void* out,
       xcb::launch_rows_fwd_premul(*c.prow, g, sig, base, c.bands, T1, c.st, c.lc);
     });
   }
-  if (c.fcol && xcb::fast_smem(3, *c.fcol, g)) {
+  if (use_pair() && xcb::pair_smem(4, g.Ph, g)) {
+    stage(c, "S2_cols_fwd_mac_inv", [&] {
+      xcb::launch_cols_fwd_mac_inv_pair(g, T1, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);
+    });
+  } else if (c.fcol && xcb::fast_smem(3, *c.fcol, g)) {
     stage(c, "S2_cols_fwd_mac_inv", [&] {
       xcb::launch_cols_fwd_mac_inv_fast(*c.fcol, g, T1, c.Fhat, c.sstride, c.bands, T2, c.st,
                                         c.lc);

@@ -1,19 +1,26 @@
-// Pair-engine band-loop stages (fft_pair.cuh) for the lengths of
-// XCB_PAIR_TABLE: every thread owns both sequences of its butterflies (16-byte
-// accesses, shared twiddles), the passes are balanced (T = max L/Rq threads),
-// and the first pass reads its band input straight from global memory with
-// the next band's block prefetched into L2 (cp.async.bulk.prefetch).
-//   I1P  k_cols_inv_corr_pair : per band, column IFFT of conj(H^) F^_k (the
-//        spectral multiply of fft.hpp:94-97 fused into pass 0; conj(H^) stays
-//        in shared memory for the whole band loop) -> T2_k
-//   I2P  k_rows_inv_steer_pair: per band, row IFFT of T2_k, crop, Horner
-//        steering over the bands sorted by descending k (engine.hpp:312-317),
-//        the band sum held in registers; out written once.
+// Band-loop stages on the pair engine (fft_pair.cuh) for the lengths of
+// XCB_PAIR_TABLE.  One CTA per SM transforms a row pair or column pair; the
+// next band's input block is TMA-staged (cp.async.bulk + mbarrier) while the
+// current band's passes run, and the band after that is prefetched into L2.
+// Per-thread operands that are fixed for the whole band loop live in TMEM
+// (tcgen05.alloc / ld / st, tmem.cuh) instead of registers.
+//   I1 k_cols_inv_corr_ilv  : per band, column IFFT of conj(H^) F^_k (the
+//        spectral multiply of fft.hpp:94-97 fused into pass 0) -> T2_k
+//   I2 k_rows_inv_steer_ilv : per band, row IFFT of T2_k, crop, Horner steering
+//        over the bands sorted by descending k (engine.hpp:312-317), band sums
+//        in TMEM; the output is written once
+//   planes k_rows_inv_planes_ilv : per band, row IFFT of T2_k -> G_k planes
+//        (angle max)
+//   S1 k_rows_fwd_premul_ilv : per band, row FFT of H e^{-i k phi}
+//        (engine.hpp:353-358) with the phasor recurrence in TMEM -> T1_k
+//   S2 k_cols_fwd_mac_ilv    : per band, column FFT of T1_k times F^_k summed
+//        over the bands in TMEM (the reference's B inverse FFTs collapse into
+//        one, engine.hpp:359-366), then one inverse column FFT -> T2
+#include <cmath>
 #include <cstdlib>
 #include <map>
 #include <mutex>
 #include <vector>
-#include <cmath>
 
 #include "fft_pair.cuh"
 #include "stages_common.cuh"
@@ -22,240 +29,6 @@
 
 namespace xcb {
 namespace {
-
-// ------------------------------------------------------------------ I1P
-template <class PF>
-__global__ void __launch_bounds__(PF::T, 1)
-    k_cols_inv_corr_pair(Geo g, const float4* __restrict__ Hh, const float4* __restrict__ Fh,
-                         size_t sstride4, Bands bl, float2* __restrict__ T2,
-                         const float2* __restrict__ twm, const float2* __restrict__ twl) {
-  constexpr int L = PF::L;  // = Ph
-  extern __shared__ __align__(16) float4 smp[];
-  float4* HC = smp;     // conj(H^) of the column pair, natural order
-  float4* W0 = HC + L;
-  float4* W1 = W0 + PF::LP;
-  float2* TWs = reinterpret_cast<float2*>(W1 + PF::LP);
-  const int c = blockIdx.x, t = threadIdx.x;
-  const float4* hcol = Hh + size_t(c) * L;
-  for (int i = t; i < L; i += blockDim.x) {
-    const float4 h = hcol[i];
-    HC[i] = make_float4(h.x, -h.y, h.z, -h.w);
-  }
-  for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
-  typename PF::LastTw tl;
-  PF::load_last_tw(twl, t, tl);
-  __syncthreads();
-  const size_t plane = size_t(g.H2) * g.Pw;  // float2 per T2 band plane
-  constexpr unsigned kBytes = unsigned(L * sizeof(float4));
-  auto fsrc = [&](int bi) { return Fh + size_t(bl.spec[bi]) * sstride4 + size_t(c) * L; };
-  __shared__ __align__(8) uint64_t bar;
-  if (t == 0) {
-    mbar_init(&bar, 1);
-    fence_mbar_init();
-    mbar_expect_tx(&bar, kBytes);
-    bulk_copy(W0, fsrc(0), kBytes, &bar);
-    if (bl.n > 1) prefetch_l2(fsrc(1), kBytes);
-  }
-  __syncthreads();
-  unsigned phase = 0;
-  for (int bi = 0; bi < bl.n; ++bi) {
-    mbar_wait(&bar, phase);
-    phase ^= 1;
-    // conj(H^ conj(F^)) = conj(H^) F^ : inverse via conj-FFT-conj
-    auto load = [&](int n) -> float4 {
-      const float4 h = HC[n], f = W0[n];
-      return make_float4(h.x * f.x - h.y * f.y, h.x * f.y + h.y * f.x,
-                         h.z * f.z - h.w * f.w, h.z * f.w + h.w * f.z);
-    };
-    {
-      typename PF::P0Regs v;
-      PF::pass0_compute(load, v);
-      __syncthreads();
-      PF::pass0_store(W0, v);
-    }
-    __syncthreads();
-    PF::pass1(W0, W1, TWs);
-    __syncthreads();
-    if (t == 0 && bi + 1 < bl.n) {
-      fence_proxy_async();
-      mbar_expect_tx(&bar, kBytes);
-      bulk_copy(W0, fsrc(bi + 1), kBytes, &bar);
-      if (bi + 2 < bl.n) prefetch_l2(fsrc(bi + 2), kBytes);
-    }
-    float2* out = T2 + size_t(bi) * plane + 4 * opaque_i(c);
-    const int pw = g.Pw, off = opaque_i(g.off), H = g.H;
-    auto store = [&](int k, int, float2 a, float2 b) {
-      const int y = k - off;
-      if (y >= 0 && y < H) {
-        float2* o = out + size_t(y >> 1) * (2 * pw) + (y & 1);
-        o[0] = c_conj(a);
-        o[2] = c_conj(b);
-      }
-    };
-    PF::pass2(W1, tl, store);
-  }
-}
-
-// ------------------------------------------------------------------ I2P
-// Band accumulators live in TMEM (4 columns = both rows' complex sum per
-// output r; 4 * R2 columns per thread), which keeps the pass registers free.
-template <class PF, class TO>
-__global__ void __launch_bounds__(PF::T, 1)
-    k_rows_inv_steer_pair(Geo g, const float4* __restrict__ T2, Bands bl,
-                          const double* __restrict__ base, TO* __restrict__ out, int accumulate,
-                          SigSrc dcs, double dcr, double dci, float scale,
-                          const float2* __restrict__ twm, const float2* __restrict__ twl) {
-  constexpr int L = PF::L;  // = Pw
-  constexpr int R2 = PF::R2;
-  static_assert(PF::NB2 == PF::T, "pass 2 must use every thread (warp-collective TMEM ops)");
-  extern __shared__ __align__(16) float4 smp[];
-  float4* W0 = smp;
-  float4* W1 = W0 + PF::LP;
-  float4* Z = W1 + PF::LP;  // e^{i phi} of both rows at each output x (g.W entries)
-  float2* TWs = reinterpret_cast<float2*>(Z + g.W);
-  __shared__ uint32_t tbase;
-  const int b = blockIdx.x, t = threadIdx.x;
-  if (t < 32) tmem_alloc(&tbase, 512);
-  const int y0 = 2 * b, y1 = 2 * b + 1;
-  for (int x = t; x < g.W; x += blockDim.x) {
-    const float2 z0 = steer(1, base[size_t(y0) * g.W + x], 1.f);
-    const float2 z1 = y1 < g.H ? steer(1, base[size_t(y1) * g.W + x], 1.f) : make_float2(1.f, 0.f);
-    Z[x] = make_float4(z0.x, z0.y, z1.x, z1.y);
-  }
-  for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
-  typename PF::LastTw tl;
-  PF::load_last_tw(twl, t, tl);
-  const size_t plane4 = size_t(g.H2 / 2) * g.Pw;  // float4 per band plane
-  const float4* rowp = T2 + size_t(b) * g.Pw;
-  const int off = g.off, W = g.W;
-  constexpr unsigned kBytes = unsigned(L * sizeof(float4));
-  __shared__ __align__(8) uint64_t bar;
-  if (t == 0) {
-    mbar_init(&bar, 1);
-    fence_mbar_init();
-    mbar_expect_tx(&bar, kBytes);
-    bulk_copy(W0, rowp, kBytes, &bar);
-    if (bl.n > 1) prefetch_l2(rowp + plane4, kBytes);
-  }
-  tmem_fence_before_sync();
-  __syncthreads();
-  tmem_fence_after_sync();
-  // this thread's accumulator columns: 4 * R2 per thread, warps of a lane
-  // quadrant side by side
-  const uint32_t tacc = tmem_warp_base(tbase) + uint32_t((t >> 7) * 4 * R2);
-  unsigned phase = 0;
-  for (int bi = 0; bi < bl.n; ++bi) {
-    mbar_wait(&bar, phase);
-    phase ^= 1;
-    auto load = [&](int n) -> float4 {
-      const float4 v = W0[n];
-      return make_float4(v.x, -v.y, v.z, -v.w);
-    };
-    {
-      typename PF::P0Regs v;
-      PF::pass0_compute(load, v);
-      __syncthreads();
-      PF::pass0_store(W0, v);
-    }
-    __syncthreads();
-    PF::pass1(W0, W1, TWs);
-    __syncthreads();
-    if (t == 0 && bi + 1 < bl.n) {
-      fence_proxy_async();
-      mbar_expect_tx(&bar, kBytes);
-      bulk_copy(W0, rowp + size_t(bi + 1) * plane4, kBytes, &bar);
-      if (bi + 2 < bl.n) prefetch_l2(rowp + size_t(bi + 2) * plane4, kBytes);
-    }
-    const int dk = bi == 0 ? 0 : bl.k[bi - 1] - bl.k[bi];
-    const int tt = opaque_i(t);
-    // acc = acc z^dk + conj(v)  (Horner over descending k; IFFT = conj FFT conj)
-    auto horner = [&](float2 (&a)[R2], float2 (&c)[R2]) {
-      constexpr int C = 5;  // outputs per TMEM round trip
-#pragma unroll
-      for (int r0 = 0; r0 < R2; r0 += C) {
-        float4 acc[C];
-        if (bi > 0) {
-#pragma unroll
-          for (int i = 0; i < C; ++i)
-            if (r0 + i < R2) acc[i] = tmem_ld4(tacc + 4 * (r0 + i));
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < C; ++i)
-            if (r0 + i < R2) tmem_dep(acc[i]);
-        }
-#pragma unroll
-        for (int i = 0; i < C; ++i) {
-          const int r = r0 + i;
-          if (r >= R2) break;
-          const float2 va = a[Dft<R2>::pos(r)], vc = c[Dft<R2>::pos(r)];
-          if (bi == 0) {
-            acc[i] = make_float4(va.x, -va.y, vc.x, -vc.y);
-            continue;
-          }
-          const int x = tt + r * PF::NB2 - off;
-          const float4 z = (x >= 0 && x < W) ? Z[x] : make_float4(1.f, 0.f, 1.f, 0.f);
-          float2 pa = make_float2(acc[i].x, acc[i].y), pc = make_float2(acc[i].z, acc[i].w);
-          if (dk == 1) {
-            pa = make_float2(fmaf(pa.x, z.x, fmaf(-pa.y, z.y, va.x)),
-                             fmaf(pa.x, z.y, fmaf(pa.y, z.x, -va.y)));
-            pc = make_float2(fmaf(pc.x, z.z, fmaf(-pc.y, z.w, vc.x)),
-                             fmaf(pc.x, z.w, fmaf(pc.y, z.z, -vc.y)));
-          } else {
-            float2 za = make_float2(z.x, z.y), zc = make_float2(z.z, z.w);
-            int d = dk;
-            if (d < 0) {
-              za = c_conj(za);
-              zc = c_conj(zc);
-              d = -d;
-            }
-            for (int s = 0; s < d; ++s) {
-              pa = c_mul(pa, za);
-              pc = c_mul(pc, zc);
-            }
-            pa = c_add(pa, c_conj(va));
-            pc = c_add(pc, c_conj(vc));
-          }
-          acc[i] = make_float4(pa.x, pa.y, pc.x, pc.y);
-        }
-#pragma unroll
-        for (int i = 0; i < C; ++i)
-          if (r0 + i < R2) tmem_st4(tacc + 4 * (r0 + i), acc[i]);
-      }
-      tmem_wait_st();
-    };
-    PF::pass2_all(W1, tl, horner);
-  }
-  // out = scale * z^{k_last} * acc (+ conj(dc) H for the scale group)
-  {
-    const int klast = bl.k[bl.n - 1];
-#pragma unroll
-    for (int r = 0; r < R2; ++r) {
-      float4 acc = tmem_ld4(tacc + 4 * r);
-      tmem_wait_ld();
-      tmem_dep(acc);
-      const int x = t + r * PF::NB2 - off;
-      if (x < 0 || x >= W) continue;
-      {
-        const size_t i = size_t(y0) * W + x;
-        const float2 v =
-            c_scale(c_mul(make_float2(acc.x, acc.y), steer(klast, base[i], 1.f)), scale);
-        OutOps<TO>::put(out, i, v, accumulate != 0, dc_term(dcs, i, dcr, dci));
-      }
-      if (y1 < g.H) {
-        const size_t i = size_t(y1) * W + x;
-        const float2 v =
-            c_scale(c_mul(make_float2(acc.z, acc.w), steer(klast, base[i], 1.f)), scale);
-        OutOps<TO>::put(out, i, v, accumulate != 0, dc_term(dcs, i, dcr, dci));
-      }
-    }
-  }
-  tmem_fence_before_sync();
-  __syncthreads();
-  if (t < 32) {
-    tmem_fence_after_sync();
-    tmem_dealloc(tbase, 512);
-  }
-}
 
 // the thread's full pass-2 twiddle row W_L^{j r} (r = 1..R2-1) into TMEM at ta
 // (2 columns each; table twf is [r-1][j], j < NB2); warp-collective
@@ -401,7 +174,7 @@ __global__ void __launch_bounds__(PF::T, 1)
                          const float2* __restrict__ twm, const float2* __restrict__ twl) {
   constexpr int L = PF::L;  // = Pw
   constexpr int R2 = PF::R2;
-  static_assert(2 * PF::NB2 == PF::T, "pass 2 must use every thread (warp-collective TMEM ops)");
+  static_assert(2 * PF::NB2 <= PF::T, "pass 2: one butterfly per thread");
   extern __shared__ __align__(16) float4 smp[];
   float4* ST4 = smp;  // staged T2 row pair, natural order
   float4* W04 = ST4 + L;
@@ -520,7 +293,7 @@ __global__ void __launch_bounds__(PF::T, 1)
       tmem_wait_ld();
       tmem_dep(acc);
       const int x = j + r * PF::NB2 - g.off;
-      if (x < 0 || x >= g.W || y >= g.H) continue;
+      if (j >= PF::NB2 || x < 0 || x >= g.W || y >= g.H) continue;
       const size_t i = size_t(y) * g.W + x;
       const float2 v = c_scale(c_mul(acc, steer(klast, base[i], 1.f)), scale);
       OutOps<TO>::put(out, i, v, accumulate != 0, dc_term(dcs, i, dcr, dci));
@@ -609,13 +382,277 @@ __global__ void __launch_bounds__(PF::T, 1)
   }
 }
 
+// ------------------------------------------------------------------ S1 (interleaved)
+// TMEM per thread, for each pass-0 input r: [cur.re, cur.im, mul.re, mul.im]
+// with cur = H e^{-i k phi} of the current band and mul = e^{-i phi}.
+template <class PF>
+__global__ void __launch_bounds__(PF::T, 1)
+    k_rows_fwd_premul_ilv(Geo g, SigSrc s, const double* __restrict__ base, Bands bl,
+                          float2* __restrict__ T1, const float2* __restrict__ twm,
+                          const float2* __restrict__ twl) {
+  constexpr int R0 = PF::R0, R2 = PF::R2;
+  constexpr int kThr = 4 * R0;  // TMEM columns per thread
+  static_assert(kThr * 5 <= 512, "TMEM budget");
+  extern __shared__ __align__(16) float4 smp[];
+  float4* W04 = smp;
+  float4* W14 = W04 + PF::LP;
+  float2* TWs = reinterpret_cast<float2*>(W14 + PF::LP);
+  float2* W0 = reinterpret_cast<float2*>(W04);
+  float2* W1 = reinterpret_cast<float2*>(W14);
+  __shared__ uint32_t tbase;
+  const int b = blockIdx.x, t = threadIdx.x;
+  if (t < 32) tmem_alloc(&tbase, kThr * 5 <= 256 ? 256 : 512);
+  for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
+  typename PF::LastTw tl;
+  PF::load_last_tw(twl, tl);
+  tmem_fence_before_sync();
+  __syncthreads();
+  tmem_fence_after_sync();
+  const int gi = t & 1, j = t >> 1;
+  const uint32_t tc = tmem_warp_base(tbase) + uint32_t((t >> 7) * kThr);
+  {
+    const int ys = src_index(2 * b + gi, g.Hx, g.H, g.R, g.periodic);
+    const int k0 = bl.k[0];
+#pragma unroll
+    for (int r = 0; r < R0; ++r) {
+      const int xp = j + r * PF::NB0;
+      const int xs = j < PF::NB0 ? src_index(xp, g.Wx, g.W, g.R, g.periodic) : -1;
+      float4 cm = make_float4(0.f, 0.f, 1.f, 0.f);
+      if (ys >= 0 && xs >= 0) {
+        const size_t idx = size_t(ys) * g.W + xs;
+        const double ph = base[idx];
+        const float2 cur = c_mul(sig_value(s, idx), steer(k0, ph, -1.f));  // H e^{-i k0 phi}
+        const float2 mul = steer(1, ph, -1.f);
+        cm = make_float4(cur.x, cur.y, mul.x, mul.y);
+      }
+      tmem_st4(tc + 4 * r, cm);
+    }
+    tmem_wait_st();
+  }
+  const size_t plane = size_t(g.Hx2) * g.Pw;  // float2 per T1 band plane
+  for (int bi = 0; bi < bl.n; ++bi) {
+    {
+      // pass-0 inputs of this band, then advance cur to the next band's k
+      const int dk = bi + 1 < bl.n ? bl.k[bi + 1] - bl.k[bi] : 0;
+      typename PF::P0Regs v;
+      float2 cur[R0];
+#pragma unroll
+      for (int r0 = 0; r0 < R0; r0 += 4) {
+        float4 cm[4];
+        tmem_ldn<16>(tc + 4 * r0, reinterpret_cast<float*>(cm));
+        tmem_wait_ld();
+        tmem_depn<16>(reinterpret_cast<float*>(cm));
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          cur[r0 + i] = make_float2(cm[i].x, cm[i].y);
+          float2 nx = cur[r0 + i], m = make_float2(cm[i].z, cm[i].w);
+          int d = dk;
+          if (d < 0) {
+            m = c_conj(m);
+            d = -d;
+          }
+          for (int q = 0; q < d; ++q) nx = c_mul(nx, m);
+          cm[i].x = nx.x;
+          cm[i].y = nx.y;
+        }
+        if (bi + 1 < bl.n) tmem_stn<16>(tc + 4 * r0, reinterpret_cast<const float*>(cm));
+      }
+      tmem_wait_st();
+      auto load = [&](int r, int, int) -> float2 { return cur[r]; };
+      PF::pass0_compute(load, v);
+      PF::pass0_store(W0, v);
+    }
+    __syncthreads();
+    PF::pass1(W0, W1, TWs);
+    __syncthreads();
+    const int tt = opaque_i(t), g2 = tt & 1, jj = tt >> 1, y = 2 * b + g2;
+    // T1 layout B' [u/2][y][u%2]: u = jj + r NB2 (NB2 even: parity fixed)
+    float2* o = T1 + size_t(bi) * plane + (size_t(jj >> 1) * g.Hx2 + y) * 2 + (jj & 1);
+    const size_t ostep = size_t(PF::NB2 / 2) * g.Hx2 * 2;
+    const bool act = jj < PF::NB2;
+    auto store = [&](float2 (&a)[R2]) {
+      float2* p = o;
+#pragma unroll
+      for (int r = 0; r < R2; ++r) {
+        st_pred(p, a[Dft<R2>::pos(r)], act);
+        p += ostep;
+      }
+    };
+    PF::pass2_all(W1, tl, store);
+  }
+  tmem_fence_before_sync();
+  __syncthreads();
+  if (t < 32) {
+    tmem_fence_after_sync();
+    tmem_dealloc(tbase, kThr * 5 <= 256 ? 256 : 512);
+  }
+}
+
+// ------------------------------------------------------------------ S2 (interleaved)
+// Per band: the T1_k column pair (TMA) and F^_k column pair (TMA, double
+// buffered: read in pass 2) -> column FFT -> acc += X F^_k in TMEM (2 columns
+// per pass-2 output).  After the bands: conj(acc) -> W1 -> FFT -> conj -> T2
+// (layout A, rows y = k - off).  The 1/(Ph Pw) scale is applied by S4.
+template <class PF>
+__global__ void __launch_bounds__(PF::T, 1)
+    k_cols_fwd_mac_ilv(Geo g, const float4* __restrict__ T1, const float4* __restrict__ Fh,
+                       size_t sstride4, Bands bl, float2* __restrict__ T2,
+                       const float2* __restrict__ twm, const float2* __restrict__ twl) {
+  constexpr int L = PF::L, R2 = PF::R2;  // L = Ph
+  constexpr int kThr = 2 * R2;
+  static_assert(kThr * 5 <= 512, "TMEM budget");
+  extern __shared__ __align__(16) float4 smp[];
+  float4* ST4 = smp;              // T1_k column pair (Hx2 <= L rows)
+  float4* SF4 = ST4 + L;          // F^_k column pair, two copies by band parity
+  float4* W04 = SF4 + 2 * L;
+  float4* W14 = W04 + PF::LP;
+  float2* TWs = reinterpret_cast<float2*>(W14 + PF::LP);
+  const float2* ST = reinterpret_cast<const float2*>(ST4);
+  float2* W0 = reinterpret_cast<float2*>(W04);
+  float2* W1 = reinterpret_cast<float2*>(W14);
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int c = blockIdx.x, t = threadIdx.x;
+  const size_t plane1 = size_t(g.Hx2 / 2) * g.Pw;  // float4 per T1 band plane
+  const float4* colT = T1 + size_t(c) * g.Hx2;     // [u/2][y] pairs
+  const unsigned bytesT = unsigned(g.Hx2) * unsigned(sizeof(float4));
+  constexpr unsigned kBytesF = unsigned(L * sizeof(float4));
+  auto fsrc = [&](int bi) { return Fh + size_t(bl.spec[bi]) * sstride4 + size_t(c) * L; };
+  if (t == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(&bar, bytesT + kBytesF);
+    bulk_copy(ST4, colT, bytesT, &bar);
+    bulk_copy(SF4, fsrc(0), kBytesF, &bar);
+    if (bl.n > 1) {
+      prefetch_l2(colT + plane1, bytesT);
+      prefetch_l2(fsrc(1), kBytesF);
+    }
+  }
+  if (t < 32) tmem_alloc(&tbase, kThr * 5 <= 256 ? 256 : 512);
+  for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
+  typename PF::LastTw tl;
+  PF::load_last_tw(twl, tl);
+  tmem_fence_before_sync();
+  __syncthreads();
+  tmem_fence_after_sync();
+  const uint32_t tacc = tmem_warp_base(tbase) + uint32_t((t >> 7) * kThr);
+  const int hx2 = g.Hx2;
+  unsigned phase = 0;
+  for (int bi = 0; bi < bl.n; ++bi) {
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    {
+      auto load = [&](int, int n, int gi) -> float2 {
+        return n < hx2 ? ST[2 * n + gi] : make_float2(0.f, 0.f);
+      };
+      typename PF::P0Regs v;
+      PF::pass0_compute(load, v);
+      PF::pass0_store(W0, v);
+    }
+    __syncthreads();
+    if (t == 0 && bi + 1 < bl.n) {
+      fence_proxy_async();
+      mbar_expect_tx(&bar, bytesT + kBytesF);
+      bulk_copy(ST4, colT + size_t(bi + 1) * plane1, bytesT, &bar);
+      bulk_copy(SF4 + ((bi + 1) & 1) * L, fsrc(bi + 1), kBytesF, &bar);
+      if (bi + 2 < bl.n) {
+        prefetch_l2(colT + size_t(bi + 2) * plane1, bytesT);
+        prefetch_l2(fsrc(bi + 2), kBytesF);
+      }
+    }
+    PF::pass1(W0, W1, TWs);
+    __syncthreads();
+    const float2* SF = reinterpret_cast<const float2*>(SF4 + (bi & 1) * L);
+    const int tt = opaque_i(t);
+    const float2* fp = SF + tt;  // F^[k] of this thread's sequence: 2 k + g, k = j + r NB2
+    auto mac = [&](float2 (&a)[R2]) {
+      constexpr int C = 5;
+#pragma unroll
+      for (int r0 = 0; r0 < R2; r0 += C) {
+        float2 acc[C];
+        if (bi > 0) {
+#pragma unroll
+          for (int i = 0; i < C; ++i)
+            if (r0 + i < R2) acc[i] = tmem_ld2(tacc + 2 * (r0 + i));
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < C; ++i)
+            if (r0 + i < R2) tmem_dep(acc[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < C; ++i) {
+          const int r = r0 + i;
+          if (r >= R2) break;
+          const float2 x = c_mul(a[Dft<R2>::pos(r)], fp[2 * r * PF::NB2]);
+          acc[i] = bi > 0 ? c_add(acc[i], x) : x;
+        }
+#pragma unroll
+        for (int i = 0; i < C; ++i)
+          if (r0 + i < R2) tmem_st2(tacc + 2 * (r0 + i), acc[i]);
+      }
+      tmem_wait_st();
+    };
+    PF::pass2_all(W1, tl, mac);
+  }
+  // inverse column transform of the band sum: conj(acc) -> W1 (natural
+  // order) -> FFT -> conj -> T2
+  __syncthreads();  // every thread is past the last band's pass-2 reads of W1
+  {
+    const int gi = t & 1, j = t >> 1;
+#pragma unroll
+    for (int r = 0; r < R2; ++r) {
+      const float2 a = tmem_ld2(tacc + 2 * r);
+      tmem_wait_ld();
+      float2 v = a;
+      tmem_dep(v);
+      if (j < PF::NB2) W1[2 * (j + r * PF::NB2) + gi] = c_conj(v);
+    }
+  }
+  __syncthreads();
+  {
+    const float2* S = W1;
+    auto load = [&](int, int n, int gi) -> float2 { return S[2 * n + gi]; };
+    typename PF::P0Regs v;
+    PF::pass0_compute(load, v);
+    PF::pass0_store(W0, v);
+  }
+  __syncthreads();
+  PF::pass1(W0, W1, TWs);
+  __syncthreads();
+  {
+    const int tt = opaque_i(t), gi = tt & 1, j = tt >> 1;
+    const int y0 = j - g.off;
+    const int rstride = (PF::NB2 / 2) * 2 * g.Pw;
+    float2* o = T2 + 2 * (2 * c + gi) + (ptrdiff_t(y0 >> 1) * (2 * g.Pw) + (y0 & 1));
+    const bool act = j < PF::NB2;
+    auto store = [&](float2 (&a)[R2]) {
+      int y = opaque_i(y0);
+      float2* p = o;
+#pragma unroll
+      for (int r = 0; r < R2; ++r) {
+        st_pred(p, c_conj(a[Dft<R2>::pos(r)]), act && unsigned(y) < unsigned(g.H));
+        y += PF::NB2;
+        p += rstride;
+      }
+    };
+    PF::pass2_all(W1, tl, store);
+  }
+  tmem_fence_before_sync();
+  __syncthreads();
+  if (t < 32) {
+    tmem_fence_after_sync();
+    tmem_dealloc(tbase, kThr * 5 <= 256 ? 256 : 512);
+  }
+}
+
 constexpr size_t kSmemLimitP = 232448;
 
-// exact twiddle tables of a pair plan (fp64 -> fp32), per device
+// exact twiddle tables of a pair plan (fp64 -> fp32), per device: pass 1
+// [r-1][jm] (W_{R0 R1}^{jm r}) and pass 2 [r-1][j] (W_L^{j r}, full rows)
 struct PairTw {
   float2* mid = nullptr;
-  float2* last = nullptr;   // split rows (pair-per-thread kernels)
-  float2* lastf = nullptr;  // full rows [r-1][j], r = 1..R2-1 (interleaved kernels)
+  float2* last = nullptr;
 };
 
 template <class PF>
@@ -629,56 +666,45 @@ PairTw pair_tables() {
   if (it != cache.end()) return it->second;
   std::vector<float2> m(PF::TWM), l(PF::TWL);
   const double tp = 6.283185307179586476925286766559;
+  auto w = [&](long e, long n) {
+    e %= n;
+    const double a = -tp * double(e) / double(n);
+    return make_float2(float(std::cos(a)), float(std::sin(a)));
+  };
   for (int r = 1; r < PF::R1; ++r)
-    for (int jm = 0; jm < PF::R0; ++jm) {
-      const long e = long(jm) * r % (PF::R0 * PF::R1);
-      const double a = -tp * double(e) / double(PF::R0 * PF::R1);
-      m[(r - 1) * PF::R0 + jm] = make_float2(float(std::cos(a)), float(std::sin(a)));
-    }
+    for (int jm = 0; jm < PF::R0; ++jm) m[(r - 1) * PF::R0 + jm] = w(long(jm) * r, PF::R0 * PF::R1);
   for (int r = 1; r < PF::R2; ++r)
-    for (int j = 0; j < PF::NB2; ++j) {
-      const long e = long(j) * r % PF::L;
-      const double a = -tp * double(e) / double(PF::L);
-      l[(r - 1) * PF::NB2 + j] = make_float2(float(std::cos(a)), float(std::sin(a)));
-    }
-  std::vector<float2> lf(size_t(PF::R2 - 1) * PF::NB2);
-  for (int r = 1; r < PF::R2; ++r)
-    for (int j = 0; j < PF::NB2; ++j) {
-      const long e = long(j) * r % PF::L;
-      const double a = -tp * double(e) / double(PF::L);
-      lf[size_t(r - 1) * PF::NB2 + j] = make_float2(float(std::cos(a)), float(std::sin(a)));
-    }
+    for (int j = 0; j < PF::NB2; ++j) l[(r - 1) * PF::NB2 + j] = w(long(j) * r, PF::L);
   PairTw p;
   if (cudaMalloc(&p.mid, m.size() * sizeof(float2)) != cudaSuccess ||
-      cudaMalloc(&p.last, l.size() * sizeof(float2)) != cudaSuccess ||
-      cudaMalloc(&p.lastf, lf.size() * sizeof(float2)) != cudaSuccess)
+      cudaMalloc(&p.last, l.size() * sizeof(float2)) != cudaSuccess)
     return PairTw{};
   cudaMemcpy(p.mid, m.data(), m.size() * sizeof(float2), cudaMemcpyHostToDevice);
   cudaMemcpy(p.last, l.data(), l.size() * sizeof(float2), cudaMemcpyHostToDevice);
-  cudaMemcpy(p.lastf, lf.data(), lf.size() * sizeof(float2), cudaMemcpyHostToDevice);
   cache[dev] = p;
   return p;
 }
 
 }  // namespace
 
-// 0 if no pair plan for L (or the stage does not fit); else the dynamic smem
+// 0 if no pair plan for L (or the stage does not fit); else the dynamic smem.
+// stage 0 I1, 1 I2, 2 planes, 3 S1, 4 S2
 size_t pair_smem(int stage, int L, const Geo& g) {
   size_t s = 0;
-#define XCB_PAIR_SMEM(LL, R0, R1, R2)                                              \
+#define XCB_PAIR_SMEM(LL, R0, R1, R2, PP)                                          \
   if (L == LL) {                                                                   \
-    using PF = PairFft<LL, R0, R1, R2>;                                            \
+    using PF = IlvFft<LL, R0, R1, R2, PP>;                                         \
     const size_t tw = size_t(PF::TWM) * sizeof(float2);                            \
-    if (stage == 0) s = (size_t(LL) + 2 * size_t(PF::LP)) * sizeof(float4) + tw;   \
-    if (stage == 1 || stage == 2)                                                  \
-      s = (2 * size_t(PF::LP) + size_t(LL)) * sizeof(float4) + tw;                 \
+    const size_t w = 2 * size_t(PF::LP) * sizeof(float4);                          \
+    if (stage <= 2) s = size_t(LL) * sizeof(float4) + w + tw;                      \
+    if (stage == 3 && LL >= 2048) s = w + tw; /* 1152: the fast kernel is faster */ \
+    if (stage == 4 && g.Hx2 <= LL) s = 3 * size_t(LL) * sizeof(float4) + w + tw;   \
   }
   XCB_PAIR_TABLE(XCB_PAIR_SMEM)
 #undef XCB_PAIR_SMEM
   return s <= kSmemLimitP ? s : 0;
 }
 
-static int pair_mode();
 // Two images per I1 launch halve the filter-spectrum reads, but I1 is issue-
 // bound, not HBM-bound, so it measured slower (4.35 vs 3.88 ms per image on
 // config 5): off unless XCB_I1_IMAGES=2.
@@ -687,44 +713,38 @@ int pair_i1_images() {
     const char* e = std::getenv("XCB_I1_IMAGES");
     return e && e[0] == '2' ? 2 : 1;
   }();
-  return pair_mode() == 2 ? 1 : n;
+  return n;
 }
 
-static int pair_mode() {  // XCB_PAIR: 1 interleaved (default), 2 pair-per-thread
-  static const int m = [] {
-    const char* e = std::getenv("XCB_PAIR");
-    return e && e[0] == '2' ? 2 : 1;
-  }();
-  return m;
-}
+#define XCB_PAIR_DISPATCH(LEN, BODY)                                               \
+  switch (LEN) {                                                                   \
+    XCB_PAIR_TABLE(BODY)                                                           \
+    default: break;                                                                \
+  }
 
 void launch_cols_inv_corr_pair(const Geo& g, const float2* Hhat, const float2* Fhat,
                                size_t sstride, const Bands& b, float2* T2, cudaStream_t st,
                                LaunchCounter& lc, int nimg, size_t hstride, size_t tstride) {
   const size_t sm = pair_smem(0, g.Ph, g);
-#define XCB_PAIR_I1(LL, R0, R1, R2)                                                       \
-  if (g.Ph == LL) {                                                                       \
-    using PF = PairFft<LL, R0, R1, R2>;                                                   \
-    using IF = IlvFft<LL, R0, R1, R2>;                                                    \
-    const PairTw tw = pair_tables<PF>();                                                  \
-    const float4* hh = reinterpret_cast<const float4*>(Hhat);                             \
-    const float4* fh = reinterpret_cast<const float4*>(Fhat);                             \
-    if (pair_mode() == 2) {                                                               \
-      set_smem(k_cols_inv_corr_pair<PF>, sm);                                             \
-      k_cols_inv_corr_pair<PF><<<g.Pw / 2, PF::T, sm, st>>>(g, hh, fh, sstride / 2, b,    \
-                                                            T2, tw.mid, tw.last);         \
-    } else if (nimg == 2) {                                                               \
-      set_smem(k_cols_inv_corr_ilv<IF, 2>, sm);                                           \
-      k_cols_inv_corr_ilv<IF, 2><<<g.Pw / 2, IF::T, sm, st>>>(                            \
-          g, hh, hstride / 2, fh, sstride / 2, b, T2, tstride, tw.mid, tw.lastf);         \
-    } else {                                                                              \
-      set_smem(k_cols_inv_corr_ilv<IF, 1>, sm);                                           \
-      k_cols_inv_corr_ilv<IF, 1><<<g.Pw / 2, IF::T, sm, st>>>(                            \
-          g, hh, hstride / 2, fh, sstride / 2, b, T2, tstride, tw.mid, tw.lastf);         \
-    }                                                                                     \
+  const float4* hh = reinterpret_cast<const float4*>(Hhat);
+  const float4* fh = reinterpret_cast<const float4*>(Fhat);
+#define XCB_BODY(LL, R0, R1, R2, PP)                                                         \
+  case LL: {                                                                                \
+    using PF = IlvFft<LL, R0, R1, R2, PP>;                                                  \
+    const PairTw tw = pair_tables<PF>();                                                    \
+    if (nimg == 2) {                                                                        \
+      set_smem(k_cols_inv_corr_ilv<PF, 2>, sm);                                             \
+      k_cols_inv_corr_ilv<PF, 2><<<g.Pw / 2, PF::T, sm, st>>>(                              \
+          g, hh, hstride / 2, fh, sstride / 2, b, T2, tstride, tw.mid, tw.last);            \
+    } else {                                                                                \
+      set_smem(k_cols_inv_corr_ilv<PF, 1>, sm);                                             \
+      k_cols_inv_corr_ilv<PF, 1><<<g.Pw / 2, PF::T, sm, st>>>(                              \
+          g, hh, hstride / 2, fh, sstride / 2, b, T2, tstride, tw.mid, tw.last);            \
+    }                                                                                       \
+    break;                                                                                  \
   }
-  XCB_PAIR_TABLE(XCB_PAIR_I1)
-#undef XCB_PAIR_I1
+  XCB_PAIR_DISPATCH(g.Ph, XCB_BODY)
+#undef XCB_BODY
   ++lc.n;
 }
 
@@ -732,17 +752,17 @@ void launch_rows_inv_planes_pair(const Geo& g, const float2* T2, int nbands, flo
                                  cudaStream_t st, LaunchCounter& lc) {
   const size_t sm = pair_smem(2, g.Pw, g);
   const float scale = float(1.0 / (double(g.Ph) * double(g.Pw)));
-#define XCB_PAIR_PL(LL, R0, R1, R2)                                                        \
-  if (g.Pw == LL) {                                                                        \
-    using PF = PairFft<LL, R0, R1, R2>;                                                    \
-    using IF = IlvFft<LL, R0, R1, R2>;                                                     \
-    const PairTw tw = pair_tables<PF>();                                                   \
-    set_smem(k_rows_inv_planes_ilv<IF>, sm);                                               \
-    k_rows_inv_planes_ilv<IF><<<g.H2 / 2, IF::T, sm, st>>>(                                \
-        g, reinterpret_cast<const float4*>(T2), nbands, planes, scale, tw.mid, tw.last);   \
+#define XCB_BODY(LL, R0, R1, R2, PP)                                                         \
+  case LL: {                                                                                \
+    using PF = IlvFft<LL, R0, R1, R2, PP>;                                                  \
+    const PairTw tw = pair_tables<PF>();                                                    \
+    set_smem(k_rows_inv_planes_ilv<PF>, sm);                                                \
+    k_rows_inv_planes_ilv<PF><<<g.H2 / 2, PF::T, sm, st>>>(                                 \
+        g, reinterpret_cast<const float4*>(T2), nbands, planes, scale, tw.mid, tw.last);    \
+    break;                                                                                  \
   }
-  XCB_PAIR_TABLE(XCB_PAIR_PL)
-#undef XCB_PAIR_PL
+  XCB_PAIR_DISPATCH(g.Pw, XCB_BODY)
+#undef XCB_BODY
   ++lc.n;
 }
 
@@ -752,38 +772,63 @@ void launch_rows_inv_steer_pair(const Geo& g, const float2* T2, const Bands& b,
                                 LaunchCounter& lc) {
   const size_t sm = pair_smem(1, g.Pw, g);
   const float scale = float(1.0 / (double(g.Ph) * double(g.Pw)));
-#define XCB_PAIR_I2(LL, R0, R1, R2)                                                       \
-  if (g.Pw == LL) {                                                                       \
-    using PF = PairFft<LL, R0, R1, R2>;                                                   \
-    const PairTw tw = pair_tables<PF>();                                                  \
-    const float4* t2 = reinterpret_cast<const float4*>(T2);                               \
-    using IF = IlvFft<LL, R0, R1, R2>;                                                    \
-    if (pair_mode() == 2) {                                                               \
-      if (out_kind == OUT_C64) {                                                          \
-        set_smem(k_rows_inv_steer_pair<PF, float2>, sm);                                  \
-        k_rows_inv_steer_pair<PF, float2><<<g.H2 / 2, PF::T, sm, st>>>(                   \
-            g, t2, b, base, static_cast<float2*>(out), accumulate, dcs, dcr, dci, scale,  \
-            tw.mid, tw.last);                                                             \
-      } else {                                                                            \
-        set_smem(k_rows_inv_steer_pair<PF, double2>, sm);                                 \
-        k_rows_inv_steer_pair<PF, double2><<<g.H2 / 2, PF::T, sm, st>>>(                  \
-            g, t2, b, base, static_cast<double2*>(out), accumulate, dcs, dcr, dci, scale, \
-            tw.mid, tw.last);                                                             \
-      }                                                                                   \
-    } else if (out_kind == OUT_C64) {                                                     \
-      set_smem(k_rows_inv_steer_ilv<IF, float2>, sm);                                    \
-      k_rows_inv_steer_ilv<IF, float2><<<g.H2 / 2, IF::T, sm, st>>>(                      \
-          g, t2, b, base, static_cast<float2*>(out), accumulate, dcs, dcr, dci, scale,    \
-          tw.mid, tw.last);                                                               \
-    } else {                                                                              \
-      set_smem(k_rows_inv_steer_ilv<IF, double2>, sm);                                    \
-      k_rows_inv_steer_ilv<IF, double2><<<g.H2 / 2, IF::T, sm, st>>>(                     \
-          g, t2, b, base, static_cast<double2*>(out), accumulate, dcs, dcr, dci, scale,   \
-          tw.mid, tw.last);                                                               \
-    }                                                                                     \
+  const float4* t2 = reinterpret_cast<const float4*>(T2);
+#define XCB_BODY(LL, R0, R1, R2, PP)                                                         \
+  case LL: {                                                                                \
+    using PF = IlvFft<LL, R0, R1, R2, PP>;                                                  \
+    const PairTw tw = pair_tables<PF>();                                                    \
+    if (out_kind == OUT_C64) {                                                              \
+      set_smem(k_rows_inv_steer_ilv<PF, float2>, sm);                                       \
+      k_rows_inv_steer_ilv<PF, float2><<<g.H2 / 2, PF::T, sm, st>>>(                        \
+          g, t2, b, base, static_cast<float2*>(out), accumulate, dcs, dcr, dci, scale,      \
+          tw.mid, tw.last);                                                                 \
+    } else {                                                                                \
+      set_smem(k_rows_inv_steer_ilv<PF, double2>, sm);                                      \
+      k_rows_inv_steer_ilv<PF, double2><<<g.H2 / 2, PF::T, sm, st>>>(                       \
+          g, t2, b, base, static_cast<double2*>(out), accumulate, dcs, dcr, dci, scale,     \
+          tw.mid, tw.last);                                                                 \
+    }                                                                                       \
+    break;                                                                                  \
   }
-  XCB_PAIR_TABLE(XCB_PAIR_I2)
-#undef XCB_PAIR_I2
+  XCB_PAIR_DISPATCH(g.Pw, XCB_BODY)
+#undef XCB_BODY
+  ++lc.n;
+}
+
+void launch_rows_fwd_premul_pair(const Geo& g, const SigSrc& s, const double* base,
+                                 const Bands& b, float2* T1, cudaStream_t st,
+                                 LaunchCounter& lc) {
+  const size_t sm = pair_smem(3, g.Pw, g);
+#define XCB_BODY(LL, R0, R1, R2, PP)                                                         \
+  case LL: {                                                                                \
+    using PF = IlvFft<LL, R0, R1, R2, PP>;                                                  \
+    const PairTw tw = pair_tables<PF>();                                                    \
+    set_smem(k_rows_fwd_premul_ilv<PF>, sm);                                                \
+    k_rows_fwd_premul_ilv<PF><<<g.Hx2 / 2, PF::T, sm, st>>>(g, s, base, b, T1, tw.mid,      \
+                                                            tw.last);                       \
+    break;                                                                                  \
+  }
+  XCB_PAIR_DISPATCH(g.Pw, XCB_BODY)
+#undef XCB_BODY
+  ++lc.n;
+}
+
+void launch_cols_fwd_mac_inv_pair(const Geo& g, const float2* T1, const float2* Fhat,
+                                  size_t sstride, const Bands& b, float2* T2, cudaStream_t st,
+                                  LaunchCounter& lc) {
+  const size_t sm = pair_smem(4, g.Ph, g);
+#define XCB_BODY(LL, R0, R1, R2, PP)                                                         \
+  case LL: {                                                                                \
+    using PF = IlvFft<LL, R0, R1, R2, PP>;                                                  \
+    const PairTw tw = pair_tables<PF>();                                                    \
+    set_smem(k_cols_fwd_mac_ilv<PF>, sm);                                                   \
+    k_cols_fwd_mac_ilv<PF><<<g.Pw / 2, PF::T, sm, st>>>(                                    \
+        g, reinterpret_cast<const float4*>(T1), reinterpret_cast<const float4*>(Fhat),      \
+        sstride / 2, b, T2, tw.mid, tw.last);                                               \
+    break;                                                                                  \
+  }
+  XCB_PAIR_DISPATCH(g.Ph, XCB_BODY)
+#undef XCB_BODY
   ++lc.n;
 }
 

@@ -137,7 +137,8 @@ void launch_cols_fwd_mac_inv_fast(const FftPlan& pc, const Geo& g, const float2*
 
 namespace xcb {
 // Pair-engine variants (k_pair.cu, lengths of XCB_PAIR_TABLE in fft_pair.cuh):
-// pair_smem returns the dynamic smem of stage 0 (I1) / 1 (I2) / 2 (planes), or 0 when the
+// pair_smem returns the dynamic smem of stage 0 (I1) / 1 (I2) / 2 (planes) / 3 (S1) /
+// 4 (S2), or 0 when the
 // length has no pair plan; callers then use the fast or generic kernels.
 size_t pair_smem(int stage, int L, const Geo& g);
 // nimg (1 or 2; 2 only on the interleaved engine) images per launch: Hhat and
@@ -147,6 +148,12 @@ void launch_cols_inv_corr_pair(const Geo& g, const float2* Hhat, const float2* F
                                size_t sstride, const Bands& b, float2* T2, cudaStream_t st,
                                LaunchCounter& lc, int nimg = 1, size_t hstride = 0,
                                size_t tstride = 0);
+// scatter stages S1 / S2 on the pair engine (stages 3 / 4 of pair_smem)
+void launch_rows_fwd_premul_pair(const Geo& g, const SigSrc& s, const double* base,
+                                 const Bands& b, float2* T1, cudaStream_t st, LaunchCounter& lc);
+void launch_cols_fwd_mac_inv_pair(const Geo& g, const float2* T1, const float2* Fhat,
+                                  size_t sstride, const Bands& b, float2* T2, cudaStream_t st,
+                                  LaunchCounter& lc);
 // planes stage (angle max) on the interleaved engine; stage 2 of pair_smem
 void launch_rows_inv_planes_pair(const Geo& g, const float2* T2, int nbands, float2* planes,
                                  cudaStream_t st, LaunchCounter& lc);

@@ -498,3 +498,50 @@ def test_config3_full_size_anglemax(orc):
     assert len(pk) >= 3
     for (cx, cy, _), p in zip(sorted(truth), sorted(pk[:3], key=lambda q: q.x)):
         assert abs(p.x - cx) <= 2 and abs(p.y - cy) <= 2
+
+
+def _scatter_at(orc, F, x, phi, ys, xs):
+    """Scatter (xconv) at sampled pixels, direct in double: out(p) =
+    sum_u sum_k F_k(u) e^{-i k phi(p-u)} x(p-u) (fft.hpp:74-77 convolution,
+    engine.hpp:353-358 premultiply), zero padding."""
+    R = int(np.ceil(F.r_max))
+    side = 2 * R + 1
+    comps = np.stack([orc.render_component(F, ci, side, side, R, R) for ci in range(len(F.ks))])
+    ks = np.asarray(F.ks, np.float64)
+    h, w = x.shape
+    d = np.arange(-R, R + 1)
+    out = np.zeros(len(ys), np.complex128)
+    for i, (y, xx0) in enumerate(zip(ys, xs)):
+        qy, qx = y - d, xx0 - d  # q = p - u for u = (d_y, d_x)
+        vy, vx = (qy >= 0) & (qy < h), (qx >= 0) & (qx < w)
+        xv = np.zeros((side, side))
+        ph = np.zeros((side, side))
+        xv[np.ix_(vy, vx)] = x[np.ix_(qy[vy], qx[vx])]
+        ph[np.ix_(vy, vx)] = phi[np.ix_(qy[vy], qx[vx])]
+        steer = np.exp(-1j * ks[:, None, None] * ph[None])
+        out[i] = np.sum(comps * steer * xv[None])
+    return out
+
+
+def test_config4_full_size_smoothing(orc):
+    """BASELINE config 4 at full size (2048^2, 13 log-radial bands, s in [1, 8]):
+    smooth_adaptive (engine.hpp:385-419) through the pair-engine S1/S2 kernels
+    (pad 2160) against a direct scatter of H/s^2 and 1/s^2 at sampled pixels."""
+    from paper_2006_13188_b200 import workloads as WL
+    w = WL.config4()
+    OF = ofilter(orc, w.filt)
+    H = w.signal[0].astype(np.float64)
+    S = w.param[0].astype(np.float64)
+    got = X.smooth_adaptive(w.signal[0], X.XformField.scaling(w.param[0]), w.filt)
+    assert got.clamped_pixels == 0
+    r = np.random.default_rng(41)
+    n = H.shape[0]
+    ys = np.concatenate([r.integers(0, n, 24), [0, n - 1, 0, n - 1]])
+    xs = np.concatenate([r.integers(0, n, 24), [0, 0, n - 1, n - 1]])
+    phi = OF.omega() * np.log(S)
+    wgt = 1.0 / (S * S)
+    dc = orc.inner_dc_value(OF)
+    num = _scatter_at(orc, OF, H * wgt, phi, ys, xs) + dc * (H * wgt)[ys, xs]
+    den = _scatter_at(orc, OF, wgt, phi, ys, xs) + dc * wgt[ys, xs]
+    ref = (num / den).real
+    assert orc.rel_l2(got.output[ys, xs], ref) < TOL
