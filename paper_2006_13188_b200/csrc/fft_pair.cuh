@@ -55,6 +55,15 @@ struct IlvFft {
   static constexpr int TWM = (R1 - 1) * R0;   // pass-1 twiddles [r-1][jm]
   static constexpr int TWL = (R2 - 1) * NB2;  // pass-2 twiddles [r-1][j]
   static constexpr int LP = L + L / P;        // float4 slots per buffer
+  // CTAs per SM the band kernels ask for (__launch_bounds__): two when two
+  // CTAs' buffers fit in shared memory (short transforms), else one
+  static constexpr int MINB = (L + 2 * LP) * 16 + TWM * 8 <= 112 * 1024 ? 2 : 1;
+  static constexpr int WPQ = (T / 32 + 3) / 4;  // max warps sharing a TMEM lane quadrant
+  // TMEM allocation (power of two >= 32 columns) for kThr columns per thread
+  __host__ __device__ static constexpr uint32_t tmem_cols(int kThr) {
+    return kThr * WPQ <= 32 ? 32 : kThr * WPQ <= 64 ? 64 : kThr * WPQ <= 128 ? 128
+         : kThr * WPQ <= 256 ? 256 : 512;
+  }
   static_assert(R0 * R1 * R2 == L, "bad pair plan");
   static_assert(R0 % P == 0 && NB1 % P == 0 && NB2 % P == 0,
                 "every pass index must stay linear in r (see lin)");

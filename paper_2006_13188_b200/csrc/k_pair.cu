@@ -47,7 +47,7 @@ __device__ __forceinline__ void park_last_tw(const float2* __restrict__ twf, uin
 // images (the filter spectrum is image-independent, so its HBM read is shared).
 // Per (band, image): two barriers (after pass 0, after pass 1).
 template <class PF, int NI>
-__global__ void __launch_bounds__(PF::T, 1)
+__global__ void __launch_bounds__(PF::T, PF::MINB)
     k_cols_inv_corr_ilv(Geo g, const float4* __restrict__ Hh, size_t hstride4,
                         const float4* __restrict__ Fh, size_t sstride4, Bands bl,
                         float2* __restrict__ T2, size_t tstride,
@@ -56,8 +56,8 @@ __global__ void __launch_bounds__(PF::T, 1)
   // TMEM per thread: conj(H^) (2 R0 columns per image), then the pass-2
   // twiddle row; warps of a lane quadrant side by side (up to 5 of 18)
   constexpr int kThr = NI * 2 * PF::R0 + PF::kTwColsPad;
-  constexpr uint32_t kCols = kThr * 5 <= 256 ? 256 : 512;
-  static_assert(kThr * 5 <= 512, "TMEM budget");
+  constexpr uint32_t kCols = PF::tmem_cols(kThr);
+  static_assert(kThr * PF::WPQ <= 512, "TMEM budget");
   extern __shared__ __align__(16) float4 smp[];
   float4* ST4 = smp;  // staged F^_k column pair, natural order
   float4* W04 = ST4 + L;
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(PF::T, 1)
 // registers; the band accumulators live in TMEM (2 columns = one complex per
 // output r, 2 * R2 columns per thread; warps of a lane quadrant side by side).
 template <class PF, class TO>
-__global__ void __launch_bounds__(PF::T, 1)
+__global__ void __launch_bounds__(PF::T, PF::MINB)
     k_rows_inv_steer_ilv(Geo g, const float4* __restrict__ T2, Bands bl,
                          const double* __restrict__ base, TO* __restrict__ out, int accumulate,
                          SigSrc dcs, double dcr, double dci, float scale,
@@ -175,6 +175,8 @@ __global__ void __launch_bounds__(PF::T, 1)
   constexpr int L = PF::L;  // = Pw
   constexpr int R2 = PF::R2;
   static_assert(2 * PF::NB2 <= PF::T, "pass 2: one butterfly per thread");
+  constexpr int kThr = 4 * R2;  // TMEM columns per thread: (acc, z) per output r
+  static_assert(kThr * PF::WPQ <= 512, "TMEM budget");
   extern __shared__ __align__(16) float4 smp[];
   float4* ST4 = smp;  // staged T2 row pair, natural order
   float4* W04 = ST4 + L;
@@ -196,7 +198,7 @@ __global__ void __launch_bounds__(PF::T, 1)
     bulk_copy(ST4, rowp, kBytes, &bar);
     if (bl.n > 1) prefetch_l2(rowp + plane4, kBytes);
   }
-  if (t < 32) tmem_alloc(&tbase, 512);
+  if (t < 32) tmem_alloc(&tbase, PF::tmem_cols(kThr));
   const int gi = t & 1, j = t >> 1, y = 2 * b + gi;
   for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
   typename PF::LastTw tl;
@@ -303,7 +305,7 @@ __global__ void __launch_bounds__(PF::T, 1)
   __syncthreads();
   if (t < 32) {
     tmem_fence_after_sync();
-    tmem_dealloc(tbase, 512);
+    tmem_dealloc(tbase, PF::tmem_cols(kThr));
   }
 }
 
@@ -313,7 +315,7 @@ __global__ void __launch_bounds__(PF::T, 1)
 // bands per pixel.  Same engine as I2 without the steering; a warp's store
 // covers 16 consecutive pixels of both rows (two full 128-byte lines).
 template <class PF>
-__global__ void __launch_bounds__(PF::T, 1)
+__global__ void __launch_bounds__(PF::T, PF::MINB)
     k_rows_inv_planes_ilv(Geo g, const float4* __restrict__ T2, int nbands,
                           float2* __restrict__ planes, float scale,
                           const float2* __restrict__ twm, const float2* __restrict__ twl) {
@@ -386,13 +388,13 @@ __global__ void __launch_bounds__(PF::T, 1)
 // TMEM per thread, for each pass-0 input r: [cur.re, cur.im, mul.re, mul.im]
 // with cur = H e^{-i k phi} of the current band and mul = e^{-i phi}.
 template <class PF>
-__global__ void __launch_bounds__(PF::T, 1)
+__global__ void __launch_bounds__(PF::T, PF::MINB)
     k_rows_fwd_premul_ilv(Geo g, SigSrc s, const double* __restrict__ base, Bands bl,
                           float2* __restrict__ T1, const float2* __restrict__ twm,
                           const float2* __restrict__ twl) {
   constexpr int R0 = PF::R0, R2 = PF::R2;
   constexpr int kThr = 4 * R0;  // TMEM columns per thread
-  static_assert(kThr * 5 <= 512, "TMEM budget");
+  static_assert(kThr * PF::WPQ <= 512, "TMEM budget");
   extern __shared__ __align__(16) float4 smp[];
   float4* W04 = smp;
   float4* W14 = W04 + PF::LP;
@@ -401,7 +403,7 @@ __global__ void __launch_bounds__(PF::T, 1)
   float2* W1 = reinterpret_cast<float2*>(W14);
   __shared__ uint32_t tbase;
   const int b = blockIdx.x, t = threadIdx.x;
-  if (t < 32) tmem_alloc(&tbase, kThr * 5 <= 256 ? 256 : 512);
+  if (t < 32) tmem_alloc(&tbase, PF::tmem_cols(kThr));
   for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
   typename PF::LastTw tl;
   PF::load_last_tw(twl, tl);
@@ -484,7 +486,7 @@ __global__ void __launch_bounds__(PF::T, 1)
   __syncthreads();
   if (t < 32) {
     tmem_fence_after_sync();
-    tmem_dealloc(tbase, kThr * 5 <= 256 ? 256 : 512);
+    tmem_dealloc(tbase, PF::tmem_cols(kThr));
   }
 }
 
@@ -500,7 +502,7 @@ __global__ void __launch_bounds__(PF::T, 1)
                        const float2* __restrict__ twm, const float2* __restrict__ twl) {
   constexpr int L = PF::L, R2 = PF::R2;  // L = Ph
   constexpr int kThr = 2 * R2;
-  static_assert(kThr * 5 <= 512, "TMEM budget");
+  static_assert(kThr * PF::WPQ <= 512, "TMEM budget");
   extern __shared__ __align__(16) float4 smp[];
   float4* ST4 = smp;              // T1_k column pair (Hx2 <= L rows)
   float4* SF4 = ST4 + L;          // F^_k column pair, two copies by band parity
@@ -529,7 +531,7 @@ __global__ void __launch_bounds__(PF::T, 1)
       prefetch_l2(fsrc(1), kBytesF);
     }
   }
-  if (t < 32) tmem_alloc(&tbase, kThr * 5 <= 256 ? 256 : 512);
+  if (t < 32) tmem_alloc(&tbase, PF::tmem_cols(kThr));
   for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
   typename PF::LastTw tl;
   PF::load_last_tw(twl, tl);
@@ -642,7 +644,7 @@ __global__ void __launch_bounds__(PF::T, 1)
   __syncthreads();
   if (t < 32) {
     tmem_fence_after_sync();
-    tmem_dealloc(tbase, kThr * 5 <= 256 ? 256 : 512);
+    tmem_dealloc(tbase, PF::tmem_cols(kThr));
   }
 }
 
