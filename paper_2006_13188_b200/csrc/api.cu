@@ -549,6 +549,20 @@ bool use_pair() {
   return on;
 }
 
+// F1 / F2 / S4 (single transforms): pair engine when the length has a plan
+void run_f1(Call& c, const xcb::SigSrc& sig, float2* T1) {
+  if (use_pair() && xcb::pair_smem(5, c.g.Pw, c.g))
+    xcb::launch_rows_fwd_pair(c.g, sig, T1, c.st, c.lc);
+  else
+    xcb::launch_rows_fwd(*c.prow, c.g, sig, T1, c.st, c.lc);
+}
+void run_f2(Call& c, const float2* T1, float2* Hh) {
+  if (use_pair() && xcb::pair_smem(6, c.g.Ph, c.g))
+    xcb::launch_cols_fwd_pair(c.g, T1, Hh, c.st, c.lc);
+  else
+    xcb::launch_cols_fwd(*c.pcol, c.g, T1, Hh, c.st, c.lc);
+}
+
 void launch_i2(Call& c, const xcb::SigSrc& sig, const float2* T2, const double* base, void* out,
                int out_kind, bool accumulate, bool dc) {
   const xcb::Geo& g = c.g;
@@ -577,8 +591,8 @@ void run_gather(Call& c, const xcb::SigSrc& sig, const double* base, void* out, 
   float2* T1 = c.ctx->buf<float2>("T1", size_t(g.Hx2) * g.Pw);
   float2* Hh = c.ctx->buf<float2>("Hhat", size_t(g.Ph) * g.Pw);
   float2* T2 = c.ctx->buf<float2>("T2", size_t(c.bands.n) * g.H2 * g.Pw);
-  stage(c, "F1_rows_fwd", [&] { xcb::launch_rows_fwd(*c.prow, g, sig, T1, c.st, c.lc); });
-  stage(c, "F2_cols_fwd", [&] { xcb::launch_cols_fwd(*c.pcol, g, T1, Hh, c.st, c.lc); });
+  stage(c, "F1_rows_fwd", [&] { run_f1(c, sig, T1); });
+  stage(c, "F2_cols_fwd", [&] { run_f2(c, T1, Hh); });
   if (use_pair() && xcb::pair_smem(0, g.Ph, g)) {
     stage(c, "I1_cols_inv_corr", [&] {
       xcb::launch_cols_inv_corr_pair(g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);
@@ -610,8 +624,8 @@ void run_gather2(Call& c, const xcb::SigSrc* sig, double* const* base, void* con
   float2* Hh = c.ctx->buf<float2>("Hhat2", 2 * P);
   float2* T2 = c.ctx->buf<float2>("T2g", 2 * tstride);
   for (int i = 0; i < 2; ++i) {
-    stage(c, "F1_rows_fwd", [&] { xcb::launch_rows_fwd(*c.prow, g, sig[i], T1, c.st, c.lc); });
-    stage(c, "F2_cols_fwd", [&] { xcb::launch_cols_fwd(*c.pcol, g, T1, Hh + i * P, c.st, c.lc); });
+    stage(c, "F1_rows_fwd", [&] { run_f1(c, sig[i], T1); });
+    stage(c, "F2_cols_fwd", [&] { run_f2(c, T1, Hh + i * P); });
   }
   stage(c, "I1_cols_inv_corr", [&] {
     xcb::launch_cols_inv_corr_pair(g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc, 2, P,
@@ -657,8 +671,12 @@ void run_scatter(Call& c, const xcb::SigSrc& sig, const double* base, void* out,
   }
   const cplx dcv = dc ? xcb::inner_dc_value(c.f->hf) : cplx(0);  // engine.hpp:370
   stage(c, "S4_rows_inv_out", [&] {
-    xcb::launch_rows_inv_out(*c.prow, g, T2, out_kind, out, accumulate ? 1 : 0, sig, dcv.real(),
-                             dcv.imag(), c.st, c.lc);
+    if (use_pair() && xcb::pair_smem(7, g.Pw, g))
+      xcb::launch_rows_inv_out_pair(g, T2, out_kind, out, accumulate ? 1 : 0, sig, dcv.real(),
+                                    dcv.imag(), c.st, c.lc);
+    else
+      xcb::launch_rows_inv_out(*c.prow, g, T2, out_kind, out, accumulate ? 1 : 0, sig, dcv.real(),
+                               dcv.imag(), c.st, c.lc);
   });
 }
 
@@ -1013,8 +1031,8 @@ int xc_anglemax(xc_context ctx, xc_filter f, const xc_image_desc* d, const void*
     for (int img = 0; img < d->batch; ++img) {
       Staged s = stage_inputs(c, signal, nullptr, img);
       ck(cudaEventRecord(e0, c.st), "event");
-      stage(c, "F1_rows_fwd", [&] { xcb::launch_rows_fwd(*c.prow, c.g, s.sig, T1, c.st, c.lc); });
-      stage(c, "F2_cols_fwd", [&] { xcb::launch_cols_fwd(*c.pcol, c.g, T1, Hh, c.st, c.lc); });
+      stage(c, "F1_rows_fwd", [&] { run_f1(c, s.sig, T1); });
+      stage(c, "F2_cols_fwd", [&] { run_f2(c, T1, Hh); });
       stage(c, "I1_cols_inv_corr", [&] {
         if (use_pair() && xcb::pair_smem(0, c.g.Ph, c.g))
           xcb::launch_cols_inv_corr_pair(c.g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);

@@ -648,6 +648,128 @@ __global__ void __launch_bounds__(PF::T, 1)
   }
 }
 
+// ------------------------------------------------------------------ single transforms
+// F1 (row FFT of the zero-padded / periodically extended signal -> T1), F2
+// (column FFT of T1 -> spectrum, layout B) and S4 (row IFFT of T2, crop,
+// + dc H -> out) on the pair engine: one transform per CTA, inputs read
+// straight from global memory (F1, S4) or TMA-staged (F2).
+template <class PF>
+__global__ void __launch_bounds__(PF::T, PF::MINB)
+    k_rows_fwd_ilv(Geo g, SigSrc s, float2* __restrict__ T1, const float2* __restrict__ twm,
+                   const float2* __restrict__ twl) {
+  extern __shared__ __align__(16) float4 smp[];
+  float2* W0 = reinterpret_cast<float2*>(smp);
+  float2* W1 = reinterpret_cast<float2*>(smp + PF::LP);
+  float2* TWs = reinterpret_cast<float2*>(smp + 2 * PF::LP);
+  const int b = blockIdx.x, t = threadIdx.x;
+  for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
+  typename PF::LastTw tl;
+  PF::load_last_tw(twl, tl);
+  const int ys = src_index(2 * b + (t & 1), g.Hx, g.H, g.R, g.periodic);
+  auto load = [&](int, int n, int) -> float2 {
+    const int xs = src_index(n, g.Wx, g.W, g.R, g.periodic);
+    return ys < 0 || xs < 0 ? make_float2(0.f, 0.f) : sig_value(s, size_t(ys) * g.W + xs);
+  };
+  typename PF::P0Regs v;
+  PF::pass0_compute(load, v);
+  PF::pass0_store(W0, v);
+  __syncthreads();
+  PF::pass1(W0, W1, TWs);
+  __syncthreads();
+  const int gi = t & 1, j = t >> 1, y = 2 * b + gi;
+  float2* o = T1 + (size_t(j >> 1) * g.Hx2 + y) * 2 + (j & 1);  // layout B' (NB2 even)
+  const size_t ostep = size_t(PF::NB2 / 2) * g.Hx2 * 2;
+  auto store = [&](float2 (&a)[PF::R2]) {
+    float2* p = o;
+#pragma unroll
+    for (int r = 0; r < PF::R2; ++r) {
+      st_pred(p, a[Dft<PF::R2>::pos(r)], j < PF::NB2);
+      p += ostep;
+    }
+  };
+  PF::pass2_all(W1, tl, store);
+}
+
+template <class PF>
+__global__ void __launch_bounds__(PF::T, PF::MINB)
+    k_cols_fwd_ilv(Geo g, const float4* __restrict__ T1, float2* __restrict__ spec,
+                   const float2* __restrict__ twm, const float2* __restrict__ twl) {
+  constexpr int L = PF::L;  // = Ph
+  extern __shared__ __align__(16) float4 smp[];
+  float4* ST4 = smp;
+  float2* W0 = reinterpret_cast<float2*>(smp + L);
+  float2* W1 = reinterpret_cast<float2*>(smp + L + PF::LP);
+  float2* TWs = reinterpret_cast<float2*>(smp + L + 2 * PF::LP);
+  const float2* ST = reinterpret_cast<const float2*>(ST4);
+  __shared__ __align__(8) uint64_t bar;
+  const int c = blockIdx.x, t = threadIdx.x;
+  const unsigned bytes = unsigned(g.Hx2) * unsigned(sizeof(float4));
+  if (t == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(&bar, bytes);
+    bulk_copy(ST4, T1 + size_t(c) * g.Hx2, bytes, &bar);
+  }
+  for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
+  typename PF::LastTw tl;
+  PF::load_last_tw(twl, tl);
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  const int hx2 = g.Hx2;
+  auto load = [&](int, int n, int gi) -> float2 {
+    return n < hx2 ? ST[2 * n + gi] : make_float2(0.f, 0.f);
+  };
+  typename PF::P0Regs v;
+  PF::pass0_compute(load, v);
+  PF::pass0_store(W0, v);
+  __syncthreads();
+  PF::pass1(W0, W1, TWs);
+  __syncthreads();
+  const int tt = t, j = tt >> 1;
+  float2* o = spec + size_t(c) * L * 2 + tt;  // layout B: (c Ph + k) 2 + g
+  auto store = [&](float2 (&a)[PF::R2]) {
+#pragma unroll
+    for (int r = 0; r < PF::R2; ++r) st_pred(o + 2 * r * PF::NB2, a[Dft<PF::R2>::pos(r)], j < PF::NB2);
+  };
+  PF::pass2_all(W1, tl, store);
+}
+
+template <class PF, class TO>
+__global__ void __launch_bounds__(PF::T, PF::MINB)
+    k_rows_inv_out_ilv(Geo g, const float4* __restrict__ T2, TO* __restrict__ out,
+                       int accumulate, SigSrc dcs, double dcr, double dci, float scale,
+                       const float2* __restrict__ twm, const float2* __restrict__ twl) {
+  extern __shared__ __align__(16) float4 smp[];
+  float2* W0 = reinterpret_cast<float2*>(smp);
+  float2* W1 = reinterpret_cast<float2*>(smp + PF::LP);
+  float2* TWs = reinterpret_cast<float2*>(smp + 2 * PF::LP);
+  const int b = blockIdx.x, t = threadIdx.x;
+  for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
+  typename PF::LastTw tl;
+  PF::load_last_tw(twl, tl);
+  const float2* src = reinterpret_cast<const float2*>(T2 + size_t(b) * g.Pw);
+  auto load = [&](int, int n, int gi) -> float2 { return c_conj(__ldg(src + 2 * n + gi)); };
+  typename PF::P0Regs v;
+  PF::pass0_compute(load, v);
+  PF::pass0_store(W0, v);
+  __syncthreads();
+  PF::pass1(W0, W1, TWs);
+  __syncthreads();
+  const int gi = t & 1, j = t >> 1, y = 2 * b + gi;
+  auto store = [&](float2 (&a)[PF::R2]) {
+    if (j >= PF::NB2 || y >= g.H) return;
+#pragma unroll
+    for (int r = 0; r < PF::R2; ++r) {
+      const int x = j + r * PF::NB2 - g.off;
+      if (x < 0 || x >= g.W) continue;
+      const size_t i = size_t(y) * g.W + x;
+      OutOps<TO>::put(out, i, c_scale(c_conj(a[Dft<PF::R2>::pos(r)]), scale), accumulate != 0,
+                      dc_term(dcs, i, dcr, dci));
+    }
+  };
+  PF::pass2_all(W1, tl, store);
+}
+
 constexpr size_t kSmemLimitP = 232448;
 
 // exact twiddle tables of a pair plan (fp64 -> fp32), per device: pass 1
@@ -690,7 +812,7 @@ PairTw pair_tables() {
 }  // namespace
 
 // 0 if no pair plan for L (or the stage does not fit); else the dynamic smem.
-// stage 0 I1, 1 I2, 2 planes, 3 S1, 4 S2
+// stage 0 I1, 1 I2, 2 planes, 3 S1, 4 S2, 5 F1, 6 F2, 7 S4
 size_t pair_smem(int stage, int L, const Geo& g) {
   size_t s = 0;
 #define XCB_PAIR_SMEM(LL, R0, R1, R2, PP)                                          \
@@ -701,6 +823,8 @@ size_t pair_smem(int stage, int L, const Geo& g) {
     if (stage <= 2) s = size_t(LL) * sizeof(float4) + w + tw;                      \
     if (stage == 3 && LL >= 2048) s = w + tw; /* 1152: the fast kernel is faster */ \
     if (stage == 4 && g.Hx2 <= LL) s = 3 * size_t(LL) * sizeof(float4) + w + tw;   \
+    if (stage == 5 || stage == 7) s = w + tw;                                      \
+    if (stage == 6 && g.Hx2 <= LL) s = size_t(LL) * sizeof(float4) + w + tw;      \
   }
   XCB_PAIR_TABLE(XCB_PAIR_SMEM)
 #undef XCB_PAIR_SMEM
@@ -830,6 +954,67 @@ void launch_cols_fwd_mac_inv_pair(const Geo& g, const float2* T1, const float2* 
     break;                                                                                  \
   }
   XCB_PAIR_DISPATCH(g.Ph, XCB_BODY)
+#undef XCB_BODY
+  ++lc.n;
+}
+
+void launch_rows_fwd_pair(const Geo& g, const SigSrc& s, float2* T1, cudaStream_t st,
+                          LaunchCounter& lc) {
+  const size_t sm = pair_smem(5, g.Pw, g);
+#define XCB_BODY(LL, R0, R1, R2, PP)                                                         \
+  case LL: {                                                                                \
+    using PF = IlvFft<LL, R0, R1, R2, PP>;                                                  \
+    const PairTw tw = pair_tables<PF>();                                                    \
+    set_smem(k_rows_fwd_ilv<PF>, sm);                                                       \
+    k_rows_fwd_ilv<PF><<<g.Hx2 / 2, PF::T, sm, st>>>(g, s, T1, tw.mid, tw.last);            \
+    break;                                                                                  \
+  }
+  XCB_PAIR_DISPATCH(g.Pw, XCB_BODY)
+#undef XCB_BODY
+  ++lc.n;
+}
+
+void launch_cols_fwd_pair(const Geo& g, const float2* T1, float2* spec, cudaStream_t st,
+                          LaunchCounter& lc) {
+  const size_t sm = pair_smem(6, g.Ph, g);
+#define XCB_BODY(LL, R0, R1, R2, PP)                                                         \
+  case LL: {                                                                                \
+    using PF = IlvFft<LL, R0, R1, R2, PP>;                                                  \
+    const PairTw tw = pair_tables<PF>();                                                    \
+    set_smem(k_cols_fwd_ilv<PF>, sm);                                                       \
+    k_cols_fwd_ilv<PF><<<g.Pw / 2, PF::T, sm, st>>>(g, reinterpret_cast<const float4*>(T1), \
+                                                    spec, tw.mid, tw.last);                 \
+    break;                                                                                  \
+  }
+  XCB_PAIR_DISPATCH(g.Ph, XCB_BODY)
+#undef XCB_BODY
+  ++lc.n;
+}
+
+void launch_rows_inv_out_pair(const Geo& g, const float2* T2, int out_kind, void* out,
+                              int accumulate, const SigSrc& dcs, double dcr, double dci,
+                              cudaStream_t st, LaunchCounter& lc) {
+  const size_t sm = pair_smem(7, g.Pw, g);
+  const float scale = float(1.0 / (double(g.Ph) * double(g.Pw)));
+  const float4* t2 = reinterpret_cast<const float4*>(T2);
+#define XCB_BODY(LL, R0, R1, R2, PP)                                                         \
+  case LL: {                                                                                \
+    using PF = IlvFft<LL, R0, R1, R2, PP>;                                                  \
+    const PairTw tw = pair_tables<PF>();                                                    \
+    if (out_kind == OUT_C64) {                                                              \
+      set_smem(k_rows_inv_out_ilv<PF, float2>, sm);                                         \
+      k_rows_inv_out_ilv<PF, float2><<<g.H2 / 2, PF::T, sm, st>>>(                          \
+          g, t2, static_cast<float2*>(out), accumulate, dcs, dcr, dci, scale, tw.mid,       \
+          tw.last);                                                                         \
+    } else {                                                                                \
+      set_smem(k_rows_inv_out_ilv<PF, double2>, sm);                                        \
+      k_rows_inv_out_ilv<PF, double2><<<g.H2 / 2, PF::T, sm, st>>>(                         \
+          g, t2, static_cast<double2*>(out), accumulate, dcs, dcr, dci, scale, tw.mid,      \
+          tw.last);                                                                         \
+    }                                                                                       \
+    break;                                                                                  \
+  }
+  XCB_PAIR_DISPATCH(g.Pw, XCB_BODY)
 #undef XCB_BODY
   ++lc.n;
 }
