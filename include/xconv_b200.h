@@ -11,6 +11,10 @@
  *   xc_smooth                      <- smooth_adaptive engine.hpp:385-419
  *   xc_anglemax                    <- (new; BASELINE config 3)
  *   xc_find_peaks                  <- find_peaks   vote_filter.hpp:107-134
+ *   xc_build_vote_filter / xc_build_optimal_filter
+ *                                  <- build_vote_filter / build_optimal_filter
+ *                                     vote_filter.hpp:62-91
+ *   xc_detect_pattern              <- detect_pattern vote_filter.hpp:146-168
  *   xc_filter_create               <- FreqFilter2  freq_filter.hpp:21-46 (the
  *                                     per-band filter spectra are built once
  *                                     per filter and pad size and cached)
@@ -166,6 +170,27 @@ int xc_anglemax(xc_context ctx, xc_filter f, const xc_image_desc* d,
 int xc_find_peaks(const void* resp, int dtype, int height, int width, int layout,
                   double radius, double threshold_frac, int* xs, int* ys,
                   double* values, int max_peaks, int* n_found);
+
+/* ---- pattern detection (vote_filter.hpp) ------------- */
+/* build_vote_filter / build_optimal_filter (vote_filter.hpp:62-91): real
+ * height x width grids in `layout`; weights_out receives (2R+1)^2 doubles in
+ * the same layout, R = ceil(eps) in *radius_out. */
+int xc_build_vote_filter(const double* weight, const double* frame, int height, int width,
+                         int layout, double px, double py, double eps, int nearest,
+                         double* weights_out, int* radius_out);
+int xc_build_optimal_filter(const double* pattern, int height, int width, int layout,
+                            double px, double py, double eps, int nearest,
+                            double* weights_out, int* radius_out);
+/* detect_pattern (vote_filter.hpp:146-168): one real image (d->signal_dtype
+ * XC_F32 / XC_F64, d->batch 1), vote weights (2R+1)^2 in d->layout, K bands
+ * (n_radii / n_angles 0 = the reference defaults).  response: real
+ * (d->out_dtype) Re(xconv_fast(|grad I|, rotation(dir grad I), F)); peaks: NMS
+ * within eps/2 at 0.5 of the max, sorted (value desc, y, x), up to max_peaks
+ * written, *n_peaks = number found. */
+int xc_detect_pattern(xc_context ctx, const xc_image_desc* d, const void* image,
+                      const double* vote_weights, int radius, double eps, int K, int n_radii,
+                      int n_angles, void* response, int* peak_x, int* peak_y, double* peak_v,
+                      int max_peaks, int* n_peaks, xc_stats* stats);
 
 #ifdef __cplusplus
 }

@@ -345,6 +345,49 @@ def gradient(img):
     return mag, d
 
 
+def build_vote_filter(weight, frame, px, py, eps, nearest=False):
+    """vote_filter.hpp:62-81 -> (weights (2R+1, 2R+1), R)."""
+    weight = _f64(weight)
+    frame = _f64(frame)
+    R = int(np.ceil(eps))
+    out = np.zeros((2 * R + 1, 2 * R + 1))
+    r = C.c_int(0)
+    _check(lib().or_build_vote_filter(_dp(weight), _dp(frame), weight.shape[0], weight.shape[1],
+                                      C.c_double(px), C.c_double(py), C.c_double(eps),
+                                      int(nearest), _dp(out), C.byref(r)))
+    return out, r.value
+
+
+def build_optimal_filter(pattern, px, py, eps, nearest=False):
+    """vote_filter.hpp:83-91 -> (weights (2R+1, 2R+1), R)."""
+    pattern = _f64(pattern)
+    R = int(np.ceil(eps))
+    out = np.zeros((2 * R + 1, 2 * R + 1))
+    r = C.c_int(0)
+    _check(lib().or_build_optimal_filter(_dp(pattern), pattern.shape[0], pattern.shape[1],
+                                         C.c_double(px), C.c_double(py), C.c_double(eps),
+                                         int(nearest), _dp(out), C.byref(r)))
+    return out, r.value
+
+
+def detect_pattern(image, weights, radius, eps, K, n_radii=0, n_angles=0, max_peaks=4096):
+    """vote_filter.hpp:146-168 -> (response, [(x, y, value)], standard_ops)."""
+    image = _f64(image)
+    weights = _f64(weights)
+    h, w = image.shape
+    resp = np.zeros((h, w))
+    xs = np.zeros(max_peaks, np.int32)
+    ys = np.zeros(max_peaks, np.int32)
+    vs = np.zeros(max_peaks)
+    n = C.c_int(0)
+    ops = C.c_longlong(0)
+    _check(lib().or_detect_pattern(_dp(image), h, w, _dp(weights), int(radius), C.c_double(eps),
+                                   int(K), int(n_radii), int(n_angles), _dp(resp), _ip(xs),
+                                   _ip(ys), _dp(vs), max_peaks, C.byref(n), C.byref(ops)))
+    k = min(n.value, max_peaks)
+    return resp, [(int(xs[i]), int(ys[i]), float(vs[i])) for i in range(k)], ops.value
+
+
 def anglemax(G, ks, n_angles=360):
     """G: (nc, h, w) complex band responses.  Returns (score, argmax)."""
     G = _c128(G)

@@ -1133,6 +1133,93 @@ void or_gradient(const double* I, int h, int w, double* mag, double* dir) {
     }
 }
 
+// vote_filter.hpp:27-40 (bilinear splat), 45-60 (splat_vote), 62-81
+// (build_vote_filter); row-major [y][x] grids, radius R = ceil(eps)
+static void vote_splat_bilinear(std::vector<double>& g, int side, double x, double y, double w) {
+  const int x0 = int(std::floor(x)), y0 = int(std::floor(y));
+  const double tx = x - x0, ty = y - y0;
+  for (int dy = 0; dy < 2; ++dy)
+    for (int dx = 0; dx < 2; ++dx) {
+      const int xi = x0 + dx, yi = y0 + dy;
+      if (xi < 0 || yi < 0 || xi >= side || yi >= side) continue;
+      g[size_t(yi) * side + xi] += w * (dx ? tx : 1 - tx) * (dy ? ty : 1 - ty);
+    }
+}
+
+int or_build_vote_filter(const double* weight, const double* frame, int h, int w, double px,
+                         double py, double eps, int nearest, double* weights_out,
+                         int* radius_out) {
+  return guarded([&] {
+    if (!(eps > 0.0)) throw InvalidArg("support radius must be > 0");
+    const int R = int(std::ceil(eps)), side = 2 * R + 1;
+    std::vector<double> g(size_t(side) * side, 0.0);
+    bool any = false;
+    for (int qy = 0; qy < h; ++qy)
+      for (int qx = 0; qx < w; ++qx) {
+        const double m = weight[size_t(qy) * w + qx];
+        if (m <= 0.0) continue;
+        const double dx = px - qx, dy = py - qy;
+        if (dx * dx + dy * dy > eps * eps) continue;
+        const double a = frame[size_t(qy) * w + qx];
+        const double c = std::cos(-a), sn = std::sin(-a);
+        const double vx = c * dx - sn * dy + R, vy = sn * dx + c * dy + R;
+        if (nearest) {
+          const int xi = int(std::lround(vx)), yi = int(std::lround(vy));
+          if (xi >= 0 && yi >= 0 && xi < side && yi < side) g[size_t(yi) * side + xi] += m;
+        } else {
+          vote_splat_bilinear(g, side, vx, vy, m);
+        }
+        any = true;
+      }
+    if (!any) throw InvalidArg("degenerate pattern: no votes in support");
+    std::copy(g.begin(), g.end(), weights_out);
+    *radius_out = R;
+  });
+}
+
+// vote_filter.hpp:83-91 (build_optimal_filter)
+int or_build_optimal_filter(const double* pattern, int h, int w, double px, double py,
+                            double eps, int nearest, double* weights_out, int* radius_out) {
+  return guarded([&] {
+    if (px < 0 || py < 0 || px >= w || py >= h)
+      throw InvalidArg("center must lie inside the pattern");
+    std::vector<double> mag(size_t(h) * w), dir(size_t(h) * w);
+    or_gradient(pattern, h, w, mag.data(), dir.data());
+    const int rc = or_build_vote_filter(mag.data(), dir.data(), h, w, px, py, eps, nearest,
+                                        weights_out, radius_out);
+    if (rc) throw InvalidArg(g_err);
+  });
+}
+
+// vote_filter.hpp:146-168 (detect_pattern): gradient magnitude votes through
+// the vote filter (decomposed with K bands), steered by the gradient
+// direction; response = Re(xconv_fast); peaks within eps/2, 0.5 max
+int or_detect_pattern(const double* image, int h, int w, const double* vote_weights,
+                      int radius, double eps, int K, int n_radii, int n_angles,
+                      double* response, int* xs, int* ys, double* vals, int max_peaks,
+                      int* n_peaks, long long* ops_out) {
+  return guarded([&] {
+    if (K < 1) throw InvalidArg("K must be >= 1");
+    std::vector<double> mag(size_t(h) * w), dir(size_t(h) * w);
+    or_gradient(image, h, w, mag.data(), dir.data());
+    const int R = radius, side = 2 * R + 1;
+    if (n_radii == 0) n_radii = std::max(4, 2 * R);
+    if (n_angles == 0) n_angles = std::max(16, 8 * ((R + 1) / 2) * 2);
+    std::vector<cd> vf(size_t(side) * side);
+    for (size_t i = 0; i < vf.size(); ++i) vf[i] = cd(vote_weights[i], 0.0);
+    const Filter F = decompose_rotation2(vf.data(), side, side, double(R), double(R), K, n_radii,
+                                         n_angles, double(R) + 0.5);
+    const Xform T = make_xform(0, dir.data(), h, w);
+    std::vector<cd> H(size_t(h) * w);
+    for (size_t i = 0; i < H.size(); ++i) H[i] = cd(mag[i], 0.0);
+    long long ops = 0;
+    const auto out = xfast(1, H, h, w, T, F, nullptr, 0, false, &ops, nullptr, 1);
+    for (size_t i = 0; i < out.size(); ++i) response[i] = out[i].real();
+    *n_peaks = or_find_peaks(response, h, w, eps / 2, 0.5, xs, ys, vals, max_peaks);
+    *ops_out = ops;
+  });
+}
+
 // SURVEY 8(a) A9 / BASELINE config 3.  No reference function exists; the
 // per-angle sum follows the gather steering e^{+ik alpha} of engine.hpp:313-316
 // with alpha_s = -2 pi s / n_angles, i.e. sum_k e^{-i k 2 pi s/n} G_k(p)

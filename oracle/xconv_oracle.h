@@ -109,6 +109,18 @@ int or_find_peaks(const double* resp, int h, int w, double radius,
 void or_gaussian_blur(const double* in, int h, int w, double sigma, double* out);
 /* field.hpp:203-237 (real image in, magnitude/direction out) */
 void or_gradient(const double* img, int h, int w, double* mag, double* dir);
+/* vote_filter.hpp:62-91: vote filters (row-major [y][x]; weights_out holds
+ * (2R+1)^2 values, R = ceil(eps) returned in *radius_out) */
+int or_build_vote_filter(const double* weight, const double* frame, int h, int w, double px,
+                         double py, double eps, int nearest, double* weights_out,
+                         int* radius_out);
+int or_build_optimal_filter(const double* pattern, int h, int w, double px, double py,
+                            double eps, int nearest, double* weights_out, int* radius_out);
+/* vote_filter.hpp:146-168: response (h*w, Re of xconv_fast) and NMS peaks */
+int or_detect_pattern(const double* image, int h, int w, const double* vote_weights,
+                      int radius, double eps, int K, int n_radii, int n_angles,
+                      double* response, int* xs, int* ys, double* vals, int max_peaks,
+                      int* n_peaks, long long* ops_out);
 /* BASELINE config 3 / SURVEY 8(a) A9: score(p) = max_s |sum_k e^{-i k 2 pi s/n}
  * G_k(p)| over s in [0,n_angles); argmax = first s attaining the max.
  * G is [nc][h][w] complex. */

@@ -4,12 +4,14 @@ The reference's operator API (xcorr_fast, xconv_fast, smooth_adaptive, ...)
 backed by hand-written sm_100a CUDA kernels behind the C ABI of
 include/xconv_b200.h.  See DESIGN.md.
 """
-from .engine import (FreqFilter2, Peak, Response2, SmoothResult, XConvPlan, XformField,
-                     XformKind, XMode, anglemax, decompose_rotation2, decompose_scale2,
+from .engine import (DetectionResult, FreqFilter2, Peak, Response2, SmoothResult, VoteFilter,
+                     XConvPlan, XformField, XformKind, XMode, anglemax, build_optimal_filter,
+                     build_vote_filter, decompose_rotation2, decompose_scale2, detect_pattern,
                      find_peaks, inner_dc_value, reconstruct, render_component,
                      smooth_adaptive, xconv_fast, xcorr_fast)
 
-__all__ = ["FreqFilter2", "Peak", "Response2", "SmoothResult", "XConvPlan", "XformField",
-           "XformKind", "XMode", "anglemax", "decompose_rotation2", "decompose_scale2",
+__all__ = ["DetectionResult", "FreqFilter2", "Peak", "Response2", "SmoothResult", "VoteFilter",
+           "XConvPlan", "XformField", "XformKind", "XMode", "anglemax", "build_optimal_filter",
+           "build_vote_filter", "decompose_rotation2", "decompose_scale2", "detect_pattern",
            "find_peaks", "inner_dc_value", "reconstruct", "render_component",
            "smooth_adaptive", "xconv_fast", "xcorr_fast"]

@@ -43,6 +43,7 @@ EXPORTS = [
     "xc_filter_num_components", "xc_decompose_rotation2", "xc_decompose_scale2",
     "xc_render_component", "xc_reconstruct", "xc_inner_dc_value", "xc_run", "xc_smooth",
     "xc_anglemax", "xc_find_peaks", "xc_profile_enable", "xc_profile_reset", "xc_profile_get",
+    "xc_build_vote_filter", "xc_build_optimal_filter", "xc_detect_pattern",
 ]
 
 _lib = None
@@ -88,6 +89,10 @@ def lib():
         L.xc_anglemax.argtypes = [vp, vp, C.POINTER(ImageDesc), vp, ip, i, i, vp, ip,
                                   C.POINTER(Stats)]
         L.xc_find_peaks.argtypes = [vp, i, i, i, i, d, d, ip, ip, dp, i, ip]
+        L.xc_build_vote_filter.argtypes = [dp, dp, i, i, i, d, d, d, i, dp, ip]
+        L.xc_build_optimal_filter.argtypes = [dp, i, i, i, d, d, d, i, dp, ip]
+        L.xc_detect_pattern.argtypes = [vp, C.POINTER(ImageDesc), vp, dp, i, d, i, i, i, vp, ip,
+                                        ip, dp, i, ip, C.POINTER(Stats)]
         L.xc_profile_enable.argtypes = [vp, i]
         L.xc_profile_reset.argtypes = [vp]
         L.xc_profile_get.argtypes = [vp, i, C.c_char_p, i, dp, C.POINTER(C.c_longlong)]

@@ -1137,4 +1137,127 @@ int xc_find_peaks(const void* resp, int dtype, int height, int width, int layout
   });
 }
 
+// ---- pattern detection (vote_filter.hpp) --------------------------------
+
+namespace {
+std::vector<double> real_rowmajor(const double* data, int height, int width, int layout) {
+  std::vector<double> v(size_t(height) * width);
+  for (int y = 0; y < height; ++y)
+    for (int x = 0; x < width; ++x)
+      v[size_t(y) * width + x] =
+          data[layout == XC_COL_MAJOR ? size_t(x) * height + y : size_t(y) * width + x];
+  return v;
+}
+void export_vote(const xcb::VoteFilterHost& f, int layout, double* weights_out,
+                 int* radius_out) {
+  const int side = 2 * f.radius + 1;
+  for (int y = 0; y < side; ++y)
+    for (int x = 0; x < side; ++x)
+      weights_out[layout == XC_COL_MAJOR ? size_t(x) * side + y : size_t(y) * side + x] =
+          f.weights[size_t(y) * side + x];
+  *radius_out = f.radius;
+}
+}  // namespace
+
+int xc_build_vote_filter(const double* weight, const double* frame, int height, int width,
+                         int layout, double px, double py, double eps, int nearest,
+                         double* weights_out, int* radius_out) {
+  return guarded(nullptr, [&] {
+    if (!weight || !frame || !weights_out || !radius_out) throw std::invalid_argument("null argument");
+    const auto wr = real_rowmajor(weight, height, width, layout);
+    const auto fr = real_rowmajor(frame, height, width, layout);
+    export_vote(xcb::build_vote_filter(wr.data(), fr.data(), height, width, px, py, eps,
+                                       nearest != 0),
+                layout, weights_out, radius_out);
+  });
+}
+
+int xc_build_optimal_filter(const double* pattern, int height, int width, int layout, double px,
+                            double py, double eps, int nearest, double* weights_out,
+                            int* radius_out) {
+  return guarded(nullptr, [&] {
+    if (!pattern || !weights_out || !radius_out) throw std::invalid_argument("null argument");
+    const auto pr = real_rowmajor(pattern, height, width, layout);
+    export_vote(xcb::build_optimal_filter(pr.data(), height, width, px, py, eps, nearest != 0),
+                layout, weights_out, radius_out);
+  });
+}
+
+// detect_pattern (vote_filter.hpp:146-168): the vote filter is decomposed on
+// the host (once per call, as in the reference), the gradient runs on the
+// GPU, the scatter is xc_run's pipeline, and the NMS peaks are found on the
+// host.  The context lock is taken by the inner xc_run only.
+int xc_detect_pattern(xc_context ctx, const xc_image_desc* d, const void* image,
+                      const double* vote_weights, int radius, double eps, int K, int n_radii,
+                      int n_angles, void* response, int* peak_x, int* peak_y, double* peak_v,
+                      int max_peaks, int* n_peaks, xc_stats* stats) {
+  return guarded(ctx, [&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    if (!d || !image || !vote_weights || !response || !n_peaks)
+      throw std::invalid_argument("null argument");
+    if (K < 1) throw std::invalid_argument("K must be >= 1");
+    if (d->batch != 1) throw std::invalid_argument("detect_pattern takes one image");
+    if (d->signal_dtype != XC_F32 && d->signal_dtype != XC_F64)
+      throw std::invalid_argument("gradient requires real field");
+    if (d->out_dtype != XC_F32 && d->out_dtype != XC_F64)
+      throw std::invalid_argument("detect_pattern response must be real (XC_F32 / XC_F64)");
+    if (radius < 0) throw std::invalid_argument("radius must be >= 0");
+    const auto t_start = std::chrono::steady_clock::now();
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const int h = d->height, w = d->width, R = radius, side = 2 * R + 1;
+    const size_t npix = size_t(h) * w;
+    // host: decompose the vote filter (engine decomposition defaults of
+    // vote_filter.hpp:157-160)
+    if (n_radii == 0) n_radii = std::max(4, 2 * R);
+    if (n_angles == 0) n_angles = std::max(16, 8 * ((R + 1) / 2) * 2);
+    std::vector<cplx> vf(size_t(side) * side);
+    for (int y = 0; y < side; ++y)
+      for (int x = 0; x < side; ++x)
+        vf[size_t(y) * side + x] = cplx(
+            vote_weights[d->layout == XC_COL_MAJOR ? size_t(x) * side + y : size_t(y) * side + x],
+            0.0);
+    auto f = std::make_unique<xc_filter_s>();
+    f->hf = xcb::decompose_rotation2(xcb::ImageView{vf.data(), side, side}, double(R), double(R),
+                                     K, n_radii, n_angles, double(R) + 0.5);
+    // device: gradient of the image
+    cudaStream_t st = ctx->stream;
+    xcb::LaunchCounter lc;
+    const size_t is = dtype_size(d->signal_dtype), os = dtype_size(d->out_dtype);
+    const void* dimg = image;
+    if (d->memory == XC_HOST) {
+      void* b = ctx->buf<char>("det_image", npix * is);
+      ck(cudaMemcpyAsync(b, image, npix * is, cudaMemcpyHostToDevice, st), "H2D image");
+      dimg = b;
+    }
+    float* mag = ctx->buf<float>("det_mag", npix);
+    float* dir = ctx->buf<float>("det_dir", npix);
+    xcb::launch_gradient(dimg, d->signal_dtype == XC_F64, h, w, d->layout == XC_COL_MAJOR, mag,
+                         dir, st, lc);
+    ck(cudaGetLastError(), "gradient launch");
+    // scatter: xconv_fast(|grad|, rotation(direction), F)
+    float2* out = ctx->buf<float2>("det_out", npix);
+    xc_image_desc dd{h, w, 1, XC_F32, XC_F32, XC_C64, d->layout, XC_DEVICE, 1, XC_ROTATION2};
+    xc_stats rs{};
+    if (xc_run(ctx, f.get(), XC_CONVOLUTION, &dd, mag, dir, nullptr, 0, 0, out, &rs) != XC_OK)
+      throw std::runtime_error(ctx->err);
+    // response = Re(out); NMS on the host
+    void* dresp = d->memory == XC_DEVICE ? response : ctx->buf<char>("det_resp", npix * os);
+    xcb::launch_real_part(out, npix, d->out_dtype == XC_F64, dresp, st, lc);
+    ck(cudaGetLastError(), "real part launch");
+    std::vector<char> hresp(npix * os);
+    ck(cudaMemcpyAsync(hresp.data(), dresp, npix * os, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "detect");
+    if (d->memory == XC_HOST) std::memcpy(response, hresp.data(), npix * os);
+    if (xc_find_peaks(hresp.data(), d->out_dtype, h, w, d->layout, eps / 2, 0.5, peak_x, peak_y,
+                      peak_v, max_peaks, n_peaks) != XC_OK)
+      throw std::runtime_error(g_thread_err);
+    if (stats) {
+      *stats = rs;
+      stats->gpu_launches += lc.n;
+      stats->seconds_total =
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    }
+  });
+}
+
 }  // extern "C"

@@ -207,4 +207,73 @@ void reconstruct(const HostFilter& f, int width, int height, double cx, double c
   }
 }
 
+// ------------------------------------------------------------------ vote filters
+void gradient_host(const double* img, int h, int w, double* mag, double* dir) {
+  auto I = [&](int y, int x) { return img[size_t(y) * w + x]; };
+  for (int y = 0; y < h; ++y)
+    for (int x = 0; x < w; ++x) {
+      const double gx = w == 1 ? 0.0
+                        : x == 0 ? I(y, 1) - I(y, 0)
+                        : x == w - 1 ? I(y, w - 1) - I(y, w - 2)
+                                     : 0.5 * (I(y, x + 1) - I(y, x - 1));
+      const double gy = h == 1 ? 0.0
+                        : y == 0 ? I(1, x) - I(0, x)
+                        : y == h - 1 ? I(h - 1, x) - I(h - 2, x)
+                                     : 0.5 * (I(y + 1, x) - I(y - 1, x));
+      const double m = std::sqrt(gx * gx + gy * gy);
+      mag[size_t(y) * w + x] = m;
+      dir[size_t(y) * w + x] = m > 0.0 ? std::atan2(gy, gx) : 0.0;
+    }
+}
+
+// vote_filter.hpp:43-81: every q with weight(q) > 0 within eps of the centre
+// p votes at (p - q) rotated into q's frame (x-axis = frame angle), bilinear
+// or nearest splat
+VoteFilterHost build_vote_filter(const double* weight, const double* frame, int h, int w,
+                                 double px, double py, double eps, bool nearest) {
+  if (!(eps > 0.0)) throw std::invalid_argument("support radius must be > 0");
+  VoteFilterHost f;
+  f.eps = eps;
+  f.radius = int(std::ceil(eps));
+  const int side = 2 * f.radius + 1;
+  f.weights.assign(size_t(side) * side, 0.0);
+  auto add = [&](int xi, int yi, double v) {
+    if (xi >= 0 && yi >= 0 && xi < side && yi < side) f.weights[size_t(yi) * side + xi] += v;
+  };
+  bool any = false;
+  for (int qy = 0; qy < h; ++qy)
+    for (int qx = 0; qx < w; ++qx) {
+      const double m = weight[size_t(qy) * w + qx];
+      if (m <= 0.0) continue;
+      const double ox = px - qx, oy = py - qy;
+      if (ox * ox + oy * oy > eps * eps) continue;
+      const double a = -frame[size_t(qy) * w + qx];
+      const double ca = std::cos(a), sa = std::sin(a);
+      const double vx = ca * ox - sa * oy + f.radius, vy = sa * ox + ca * oy + f.radius;
+      if (nearest) {
+        add(int(std::lround(vx)), int(std::lround(vy)), m);
+      } else {
+        const int x0 = int(std::floor(vx)), y0 = int(std::floor(vy));
+        const double tx = vx - x0, ty = vy - y0;
+        add(x0, y0, m * (1 - tx) * (1 - ty));
+        add(x0 + 1, y0, m * tx * (1 - ty));
+        add(x0, y0 + 1, m * (1 - tx) * ty);
+        add(x0 + 1, y0 + 1, m * tx * ty);
+      }
+      any = true;
+    }
+  if (!any) throw std::invalid_argument("degenerate pattern: no votes in support");
+  return f;
+}
+
+// vote_filter.hpp:83-91
+VoteFilterHost build_optimal_filter(const double* pattern, int h, int w, double px, double py,
+                                    double eps, bool nearest) {
+  if (px < 0 || py < 0 || px >= w || py >= h)
+    throw std::invalid_argument("center must lie inside the pattern");
+  std::vector<double> mag(size_t(h) * w), dir(size_t(h) * w);
+  gradient_host(pattern, h, w, mag.data(), dir.data());
+  return build_vote_filter(mag.data(), dir.data(), h, w, px, py, eps, nearest);
+}
+
 }  // namespace xcb

@@ -51,4 +51,19 @@ void render_component(const HostFilter& f, int ci, int width, int height, double
 void reconstruct(const HostFilter& f, int width, int height, double cx, double cy,
                  const int* subset, int nsub, bool transpose, cplx* out);
 
+// Vote filters of the generalized-Hough detector (vote_filter.hpp:8-95):
+// (2R+1)^2 non-negative weights, row-major [y][x], origin at the centre,
+// R = ceil(eps).  Inputs are row-major [h][w] real grids.
+struct VoteFilterHost {
+  std::vector<double> weights;
+  int radius = 0;
+  double eps = 0;
+};
+VoteFilterHost build_vote_filter(const double* weight, const double* frame, int h, int w,
+                                 double px, double py, double eps, bool nearest);
+VoteFilterHost build_optimal_filter(const double* pattern, int h, int w, double px, double py,
+                                    double eps, bool nearest);
+// central-difference gradient, one-sided at the borders (field.hpp:204-237)
+void gradient_host(const double* img, int h, int w, double* mag, double* dir);
+
 }  // namespace xcb

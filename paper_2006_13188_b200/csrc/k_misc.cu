@@ -361,4 +361,63 @@ void launch_anglemax(const float2* planes, const int* ks_host, int nb, size_t np
   ++lc.n;
 }
 
+// ------------------------------------------------------------------ detect_pattern
+namespace {
+// central-difference gradient, one-sided at the borders (field.hpp:204-237),
+// in double, of a real image stored row- or column-major; magnitude and
+// direction written in the same storage order as fp32 (the xconv inputs)
+template <class TI>
+__global__ void k_gradient(const TI* __restrict__ img, int h, int w, int colmajor,
+                           float* __restrict__ mag, float* __restrict__ dir) {
+  const size_t n = size_t(h) * w;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const int y = colmajor ? int(i % h) : int(i / w), x = colmajor ? int(i / h) : int(i % w);
+    auto I = [&](int yy, int xx) -> double {
+      return double(img[colmajor ? size_t(xx) * h + yy : size_t(yy) * w + xx]);
+    };
+    const double gx = w == 1 ? 0.0
+                      : x == 0 ? I(y, 1) - I(y, 0)
+                      : x == w - 1 ? I(y, w - 1) - I(y, w - 2)
+                                   : 0.5 * (I(y, x + 1) - I(y, x - 1));
+    const double gy = h == 1 ? 0.0
+                      : y == 0 ? I(1, x) - I(0, x)
+                      : y == h - 1 ? I(h - 1, x) - I(h - 2, x)
+                                   : 0.5 * (I(y + 1, x) - I(y - 1, x));
+    const double m = sqrt(gx * gx + gy * gy);
+    mag[i] = float(m);
+    dir[i] = m > 0.0 ? float(atan2(gy, gx)) : 0.f;
+  }
+}
+
+template <class TO>
+__global__ void k_real_part(const float2* __restrict__ in, size_t n, TO* __restrict__ out) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    out[i] = TO(in[i].x);
+}
+}  // namespace
+
+void launch_gradient(const void* img, int img_f64, int h, int w, int colmajor, float* mag,
+                     float* dir, cudaStream_t st, LaunchCounter& lc) {
+  const int g = grid_for(size_t(h) * w, 256);
+  if (img_f64)
+    k_gradient<double><<<g, 256, 0, st>>>(static_cast<const double*>(img), h, w, colmajor, mag,
+                                          dir);
+  else
+    k_gradient<float><<<g, 256, 0, st>>>(static_cast<const float*>(img), h, w, colmajor, mag,
+                                         dir);
+  ++lc.n;
+}
+
+void launch_real_part(const float2* in, size_t n, int out_f64, void* out, cudaStream_t st,
+                      LaunchCounter& lc) {
+  const int g = grid_for(n, 256);
+  if (out_f64)
+    k_real_part<double><<<g, 256, 0, st>>>(in, n, static_cast<double*>(out));
+  else
+    k_real_part<float><<<g, 256, 0, st>>>(in, n, static_cast<float*>(out));
+  ++lc.n;
+}
+
 }  // namespace xcb

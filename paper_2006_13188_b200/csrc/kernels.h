@@ -172,3 +172,13 @@ void launch_rows_inv_steer_pair(const Geo& g, const float2* T2, const Bands& b,
                                 const SigSrc& dcs, double dcr, double dci, cudaStream_t st,
                                 LaunchCounter& lc);
 }  // namespace xcb
+
+namespace xcb {
+// detect_pattern (vote_filter.hpp:146-168): gradient magnitude / direction of
+// a real image (f32 or f64, row- or column-major) -> fp32 in the same order;
+// real part of a complex field.
+void launch_gradient(const void* img, int img_f64, int h, int w, int colmajor, float* mag,
+                     float* dir, cudaStream_t st, LaunchCounter& lc);
+void launch_real_part(const float2* in, size_t n, int out_f64, void* out, cudaStream_t st,
+                      LaunchCounter& lc);
+}  // namespace xcb

@@ -364,3 +364,100 @@ def find_peaks(resp, radius: float, threshold_frac: float = 0.5, max_peaks: int 
                                   vs.ctypes.data_as(C.POINTER(C.c_double)), max_peaks,
                                   C.byref(n)))
     return [Peak(int(xs[i]), int(ys[i]), float(vs[i])) for i in range(min(n.value, max_peaks))]
+
+
+# ---------------------------------------------------------------- detection
+# vote_filter.hpp: generalized-Hough pattern detection on the
+# hot path -- gradient on the GPU, scatter through xc_run, NMS on the host.
+
+@dataclass
+class VoteFilter:  # vote_filter.hpp:8-26
+    weights: np.ndarray  # (2R+1, 2R+1) row-major [y][x], non-negative
+    radius: int
+    eps: float
+
+    def side(self) -> int:
+        return 2 * self.radius + 1
+
+    def total_mass(self) -> float:
+        return float(self.weights.sum())
+
+
+@dataclass
+class DetectionResult:  # vote_filter.hpp:137-142
+    response: np.ndarray
+    peaks: list
+    standard_ops: int = 0
+
+
+def _f64_2d(a):
+    return np.ascontiguousarray(np.asarray(getattr(a, "values", a), dtype=np.float64))
+
+
+def build_vote_filter(weight, frame, px: float, py: float, eps: float,
+                      nearest: bool = False) -> VoteFilter:
+    """Votes of every q with weight(q) > 0 within eps of (px, py), rotated into the
+    frame at q (vote_filter.hpp:62-81)."""
+    w = _f64_2d(weight)
+    f = _f64_2d(frame)
+    if f.shape != w.shape:
+        raise ValueError("weight and frame dims differ")
+    R = int(np.ceil(eps)) if eps > 0 else 0
+    out = np.zeros((2 * R + 1, 2 * R + 1))
+    r = C.c_int(0)
+    N.check(N.lib().xc_build_vote_filter(w.ctypes.data_as(C.POINTER(C.c_double)),
+                                         f.ctypes.data_as(C.POINTER(C.c_double)), w.shape[0],
+                                         w.shape[1], N.XC_ROW_MAJOR, float(px), float(py),
+                                         float(eps), int(nearest),
+                                         out.ctypes.data_as(C.POINTER(C.c_double)), C.byref(r)))
+    return VoteFilter(out, r.value, float(eps))
+
+
+def build_optimal_filter(pattern, px: float, py: float, eps: float,
+                         nearest: bool = False) -> VoteFilter:
+    """Optimal filter of a pattern: gradient-magnitude votes in the gradient frame
+    (vote_filter.hpp:83-91)."""
+    p = _f64_2d(pattern)
+    R = int(np.ceil(eps)) if eps > 0 else 0
+    out = np.zeros((2 * R + 1, 2 * R + 1))
+    r = C.c_int(0)
+    N.check(N.lib().xc_build_optimal_filter(p.ctypes.data_as(C.POINTER(C.c_double)), p.shape[0],
+                                            p.shape[1], N.XC_ROW_MAJOR, float(px), float(py),
+                                            float(eps), int(nearest),
+                                            out.ctypes.data_as(C.POINTER(C.c_double)),
+                                            C.byref(r)))
+    return VoteFilter(out, r.value, float(eps))
+
+
+def detect_pattern(image, filter: VoteFilter, K: int, n_radii: int = 0, n_angles: int = 0,
+                   device: int = 0, max_peaks: int = 1 << 16) -> DetectionResult:
+    """Gradient magnitudes vote through the filter's K-band decomposition, steered by
+    the gradient directions; peaks by NMS within eps/2 (vote_filter.hpp:146-168)."""
+    img = np.ascontiguousarray(np.asarray(getattr(image, "values", image)))
+    if np.iscomplexobj(img):
+        raise ValueError("gradient requires real field")
+    if img.dtype not in (np.float32, np.float64):
+        img = img.astype(np.float64)
+    wide = img.dtype == np.float64
+    h, w = img.shape
+    resp = np.zeros((h, w), np.float64 if wide else np.float32)
+    d = N.ImageDesc(h, w, 1, N.XC_F64 if wide else N.XC_F32, N.XC_F32,
+                    N.XC_F64 if wide else N.XC_F32, N.XC_ROW_MAJOR, N.XC_HOST, 0,
+                    XformKind.rotation2)
+    wts = np.ascontiguousarray(filter.weights, np.float64)
+    xs = np.zeros(max_peaks, np.int32)
+    ys = np.zeros(max_peaks, np.int32)
+    vs = np.zeros(max_peaks)
+    n = C.c_int(0)
+    st = N.Stats()
+    ctx = N.context(device)
+    N.check(N.lib().xc_detect_pattern(ctx.handle, C.byref(d), img.ctypes.data,
+                                      wts.ctypes.data_as(C.POINTER(C.c_double)),
+                                      int(filter.radius), float(filter.eps), int(K),
+                                      int(n_radii), int(n_angles), resp.ctypes.data,
+                                      xs.ctypes.data_as(C.POINTER(C.c_int)),
+                                      ys.ctypes.data_as(C.POINTER(C.c_int)),
+                                      vs.ctypes.data_as(C.POINTER(C.c_double)), max_peaks,
+                                      C.byref(n), C.byref(st)), ctx.handle)
+    peaks = [Peak(int(xs[i]), int(ys[i]), float(vs[i])) for i in range(min(n.value, max_peaks))]
+    return DetectionResult(resp, peaks, int(st.standard_ops))
