@@ -9,6 +9,10 @@
 //   xconv::gpu::xcorr_fast(H, T, F, plan)        <- engine.hpp:286-326
 //   xconv::gpu::xconv_fast(H, T, F, plan)        <- engine.hpp:331-373
 //   xconv::gpu::smooth_adaptive(H, T, F, norm)   <- engine.hpp:385-419
+//   xconv::gpu::build_optimal_filter(P, px, py, eps, nearest)
+//                                                <- vote_filter.hpp:83-91
+//   xconv::gpu::detect_pattern(I, vf, K, n_radii, n_angles)
+//                                                <- vote_filter.hpp:146-168
 //
 // Eigen's default column-major storage (field.hpp:15) is passed as
 // XC_COL_MAJOR with the caller's complex<double> / double buffers
@@ -17,6 +21,7 @@
 // spectra are cached per filter content (hash), per thread.
 #pragma once
 
+#include <cmath>
 #include <complex>
 #include <cstdint>
 #include <cstring>
@@ -199,6 +204,82 @@ Result smooth_adaptive(const Field& H, const Xform& T, const F& Fl, bool normali
   out.clamped_pixels = st.clamped_pixels;
   out.output = decltype(out.output)(H.width(), H.height());
   for (size_t i = 0; i < real_out.size(); ++i) out.output.values.data()[i] = real_out[i];
+  return out;
+}
+
+// vote_filter.hpp:83-91 (VoteFilter<Real>: weights (2R+1)^2 column-major,
+// radius, eps); the pattern must be real-valued (field.hpp:206)
+template <class VF, class Field, class Real>
+VF build_optimal_filter(const Field& pattern, Real px, Real py, Real eps, bool nearest = false) {
+  const int h = pattern.height(), w = pattern.width();
+  std::vector<double> p(size_t(h) * w);
+  for (size_t i = 0; i < p.size(); ++i) {
+    if (std::imag(pattern.values.data()[i]) != 0)
+      throw std::invalid_argument("gradient requires real field");
+    p[i] = double(std::real(pattern.values.data()[i]));
+  }
+  const int R = eps > 0 ? static_cast<int>(std::ceil(double(eps))) : 0;
+  std::vector<double> wts(size_t(2 * R + 1) * (2 * R + 1));
+  int radius = 0;
+  detail::check(xc_build_optimal_filter(p.data(), h, w, XC_COL_MAJOR, double(px), double(py),
+                                        double(eps), nearest ? 1 : 0, wts.data(), &radius),
+                nullptr);
+  VF f;
+  f.eps = eps;
+  f.radius = radius;
+  f.weights = decltype(f.weights)(2 * radius + 1, 2 * radius + 1);
+  for (size_t i = 0; i < wts.size(); ++i) f.weights.data()[i] = wts[i];
+  return f;
+}
+
+// vote_filter.hpp:146-168 (DetectionResult<Real>: response Field2, peaks
+// {x, y, value} sorted by value desc / y / x, standard_ops)
+template <class Result, class Field, class VF>
+Result detect_pattern(const Field& image, const VF& filter, int K, int n_radii = 0,
+                      int n_angles = 0) {
+  detail::Context& c = detail::context();
+  const int h = image.height(), w = image.width();
+  std::vector<double> img(size_t(h) * w);
+  for (size_t i = 0; i < img.size(); ++i) {
+    if (std::imag(image.values.data()[i]) != 0)
+      throw std::invalid_argument("gradient requires real field");
+    img[i] = double(std::real(image.values.data()[i]));
+  }
+  const int side = 2 * filter.radius + 1;
+  std::vector<double> wts(size_t(side) * side);
+  for (size_t i = 0; i < wts.size(); ++i) wts[i] = double(filter.weights.data()[i]);
+  xc_image_desc d{};
+  d.height = h;
+  d.width = w;
+  d.batch = 1;
+  d.signal_dtype = XC_F64;
+  d.param_dtype = XC_F64;
+  d.out_dtype = XC_F64;
+  d.layout = XC_COL_MAJOR;
+  d.memory = XC_HOST;
+  d.param_per_image = 1;
+  d.xform_kind = XC_ROTATION2;
+  std::vector<double> resp(img.size());
+  const int max_peaks = static_cast<int>(img.size());
+  std::vector<int> px(max_peaks), py(max_peaks);
+  std::vector<double> pv(max_peaks);
+  int n = 0;
+  xc_stats st{};
+  detail::check(xc_detect_pattern(c.ctx, &d, img.data(), wts.data(), filter.radius,
+                                  double(filter.eps), K, n_radii, n_angles, resp.data(),
+                                  px.data(), py.data(), pv.data(), max_peaks, &n, &st),
+                c.ctx);
+  Result out;
+  out.standard_ops = st.standard_ops;
+  out.response = decltype(out.response)(w, h);
+  for (size_t i = 0; i < resp.size(); ++i) out.response.values.data()[i] = resp[i];
+  for (int i = 0; i < n && i < max_peaks; ++i) {
+    typename decltype(out.peaks)::value_type pk;
+    pk.x = px[i];
+    pk.y = py[i];
+    pk.value = pv[i];
+    out.peaks.push_back(pk);
+  }
   return out;
 }
 

@@ -76,4 +76,24 @@ struct SmoothResult {
   int clamped_pixels = 0;
 };
 
+template <class Real>
+struct VoteFilter {  // vote_filter.hpp:8-26
+  Grid<Real> weights;
+  int radius = 0;
+  Real eps = 0;
+};
+
+template <class Real>
+struct Peak {  // vote_filter.hpp:99-102
+  int x = 0, y = 0;
+  Real value = 0;
+};
+
+template <class Real>
+struct DetectionResult {  // vote_filter.hpp:137-142
+  Field2<Real> response;
+  std::vector<Peak<Real>> peaks;
+  long long standard_ops = 0;
+};
+
 }  // namespace mini

@@ -107,5 +107,48 @@ int main() {
     std::printf("invalid plan: \"%s\" %s\n", e.what(), ok ? "ok" : "FAIL");
     fails += !ok;
   }
+  // detect_pattern through the shim (vote_filter.hpp:146-168) vs the oracle
+  {
+    const int Rp = 6, n = 48;
+    Field2<double> pat(2 * Rp + 1, 2 * Rp + 1);
+    for (int y = -Rp; y <= Rp; ++y)
+      for (int x = -Rp; x <= Rp; ++x)
+        pat.values(y + Rp, x + Rp) =
+            std::exp(-((x + 1.5) * (x + 1.5) + (y - 0.5) * (y - 0.5)) / 4.0) -
+            0.7 * std::exp(-((x - 2.0) * (x - 2.0) + (y + 2.0) * (y + 2.0)) / 3.0);
+    auto vf = xconv::gpu::build_optimal_filter<VoteFilter<double>>(pat, 6.0, 6.0, 6.0);
+    Field2<double> img(n, n);
+    for (int y = 0; y < 2 * Rp + 1; ++y)
+      for (int x = 0; x < 2 * Rp + 1; ++x) {
+        img.values(y + 10, x + 14) += pat.values(y, x);
+        img.values(x + 27, 2 * Rp - y + 20) += 0.8 * pat.values(y, x);  // weaker 90-degree copy
+      }
+    auto det = xconv::gpu::detect_pattern<DetectionResult<double>>(img, vf, 12);
+    std::vector<double> imo(size_t(n) * n), wo(size_t(2 * Rp + 1) * (2 * Rp + 1));
+    for (int y = 0; y < n; ++y)
+      for (int x = 0; x < n; ++x) imo[size_t(y) * n + x] = img.values(y, x).real();
+    for (int y = 0; y < 2 * Rp + 1; ++y)
+      for (int x = 0; x < 2 * Rp + 1; ++x) wo[size_t(y) * (2 * Rp + 1) + x] = vf.weights(y, x);
+    std::vector<double> resp(size_t(n) * n), pvv(64);
+    std::vector<int> pxx(64), pyy(64);
+    int np = 0;
+    long long ops = 0;
+    if (or_detect_pattern(imo.data(), n, n, wo.data(), vf.radius, vf.eps, 12, 0, 0, resp.data(),
+                          pxx.data(), pyy.data(), pvv.data(), 64, &np, &ops) != 0)
+      return 4;
+    std::vector<cd> a(size_t(n) * n), b(size_t(n) * n);
+    for (int y = 0; y < n; ++y)
+      for (int x = 0; x < n; ++x) {
+        a[size_t(y) * n + x] = det.response.values(y, x);
+        b[size_t(y) * n + x] = resp[size_t(y) * n + x];
+      }
+    const double e = rel(a, b);
+    const bool ok = e < 1e-5 && det.standard_ops == ops && !det.peaks.empty() && np > 0 &&
+                    det.peaks[0].x == pxx[0] && det.peaks[0].y == pyy[0];
+    std::printf("detect_pattern: rel_l2 %.3e peak (%d,%d) %s\n", e,
+                det.peaks.empty() ? -1 : det.peaks[0].x, det.peaks.empty() ? -1 : det.peaks[0].y,
+                ok ? "ok" : "FAIL");
+    fails += !ok;
+  }
   return fails ? 1 : 0;
 }
