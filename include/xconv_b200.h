@@ -171,6 +171,12 @@ int xc_find_peaks(const void* resp, int dtype, int height, int width, int layout
                   double radius, double threshold_frac, int* xs, int* ys,
                   double* values, int max_peaks, int* n_found);
 
+/* find_peaks on a response in device memory (same result as xc_find_peaks):
+ * the NMS runs on the GPU, the sort on the host; outputs in host memory. */
+int xc_find_peaks_device(xc_context ctx, const void* resp, int dtype, int height, int width,
+                         int layout, double radius, double threshold_frac, int* xs, int* ys,
+                         double* values, int max_peaks, int* n_found);
+
 /* ---- pattern detection (vote_filter.hpp) ------------- */
 /* build_vote_filter / build_optimal_filter (vote_filter.hpp:62-91): real
  * height x width grids in `layout`; weights_out receives (2R+1)^2 doubles in

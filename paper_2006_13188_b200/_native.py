@@ -44,6 +44,7 @@ EXPORTS = [
     "xc_render_component", "xc_reconstruct", "xc_inner_dc_value", "xc_run", "xc_smooth",
     "xc_anglemax", "xc_find_peaks", "xc_profile_enable", "xc_profile_reset", "xc_profile_get",
     "xc_build_vote_filter", "xc_build_optimal_filter", "xc_detect_pattern",
+    "xc_find_peaks_device",
 ]
 
 _lib = None
@@ -93,6 +94,7 @@ def lib():
         L.xc_build_optimal_filter.argtypes = [dp, i, i, i, d, d, d, i, dp, ip]
         L.xc_detect_pattern.argtypes = [vp, C.POINTER(ImageDesc), vp, dp, i, d, i, i, i, vp, ip,
                                         ip, dp, i, ip, C.POINTER(Stats)]
+        L.xc_find_peaks_device.argtypes = [vp, vp, i, i, i, i, d, d, ip, ip, dp, i, ip]
         L.xc_profile_enable.argtypes = [vp, i]
         L.xc_profile_reset.argtypes = [vp]
         L.xc_profile_get.argtypes = [vp, i, C.c_char_p, i, dp, C.POINTER(C.c_longlong)]

@@ -1137,6 +1137,72 @@ int xc_find_peaks(const void* resp, int dtype, int height, int width, int layout
   });
 }
 
+// ---- find_peaks on a device response ---------------------------------------
+
+namespace {
+// NMS on the GPU, sort (value desc, y, x) on the host; returns the count
+int device_peaks(xc_context ctx, const void* dresp, int dtype, int h, int w, int layout,
+                 double radius, double frac, int* xs, int* ys, double* vals, int max_peaks) {
+  cudaStream_t st = ctx->stream;
+  xcb::LaunchCounter lc;
+  int cap = 1 << 16;
+  for (;;) {
+    unsigned long long* mx = ctx->buf<unsigned long long>("nms_max", 1);
+    unsigned* cnt = ctx->buf<unsigned>("nms_count", 1);
+    int* px = ctx->buf<int>("nms_x", cap);
+    int* py = ctx->buf<int>("nms_y", cap);
+    double* pv = ctx->buf<double>("nms_v", cap);
+    xcb::launch_find_peaks(dresp, dtype == XC_F64, h, w, layout == XC_COL_MAJOR, radius, frac, cap,
+                           mx, cnt, px, py, pv, st, lc);
+    ck(cudaGetLastError(), "find_peaks launch");
+    unsigned n = 0;
+    ck(cudaMemcpyAsync(&n, cnt, sizeof(n), cudaMemcpyDeviceToHost, st), "D2H count");
+    ck(cudaStreamSynchronize(st), "find_peaks");
+    if (int(n) > cap) {  // more local maxima than slots: rerun with room for all
+      cap = int(n);
+      continue;
+    }
+    struct Pk {
+      int x, y;
+      double v;
+    };
+    std::vector<int> hx(n), hy(n);
+    std::vector<double> hv(n);
+    if (n) {
+      ck(cudaMemcpy(hx.data(), px, n * sizeof(int), cudaMemcpyDeviceToHost), "D2H");
+      ck(cudaMemcpy(hy.data(), py, n * sizeof(int), cudaMemcpyDeviceToHost), "D2H");
+      ck(cudaMemcpy(hv.data(), pv, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    }
+    std::vector<Pk> pk(n);
+    for (unsigned i = 0; i < n; ++i) pk[i] = {hx[i], hy[i], hv[i]};
+    std::sort(pk.begin(), pk.end(), [](const Pk& a, const Pk& b) {
+      if (a.v != b.v) return a.v > b.v;
+      return a.y != b.y ? a.y < b.y : a.x < b.x;
+    });
+    for (int i = 0; i < std::min(int(n), max_peaks); ++i) {
+      if (xs) xs[i] = pk[i].x;
+      if (ys) ys[i] = pk[i].y;
+      if (vals) vals[i] = pk[i].v;
+    }
+    return int(n);
+  }
+}
+}  // namespace
+
+int xc_find_peaks_device(xc_context ctx, const void* resp, int dtype, int height, int width,
+                         int layout, double radius, double threshold_frac, int* xs, int* ys,
+                         double* values, int max_peaks, int* n_found) {
+  return guarded(ctx, [&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    if (!resp || !n_found) throw std::invalid_argument("null argument");
+    if (dtype != XC_F32 && dtype != XC_F64) throw std::invalid_argument("response must be real");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    *n_found = device_peaks(ctx, resp, dtype, height, width, layout, radius, threshold_frac, xs,
+                            ys, values, max_peaks);
+  });
+}
+
 // ---- pattern detection (vote_filter.hpp) --------------------------------
 
 namespace {
@@ -1244,13 +1310,10 @@ int xc_detect_pattern(xc_context ctx, const xc_image_desc* d, const void* image,
     void* dresp = d->memory == XC_DEVICE ? response : ctx->buf<char>("det_resp", npix * os);
     xcb::launch_real_part(out, npix, d->out_dtype == XC_F64, dresp, st, lc);
     ck(cudaGetLastError(), "real part launch");
-    std::vector<char> hresp(npix * os);
-    ck(cudaMemcpyAsync(hresp.data(), dresp, npix * os, cudaMemcpyDeviceToHost, st), "D2H");
-    ck(cudaStreamSynchronize(st), "detect");
-    if (d->memory == XC_HOST) std::memcpy(response, hresp.data(), npix * os);
-    if (xc_find_peaks(hresp.data(), d->out_dtype, h, w, d->layout, eps / 2, 0.5, peak_x, peak_y,
-                      peak_v, max_peaks, n_peaks) != XC_OK)
-      throw std::runtime_error(g_thread_err);
+    *n_peaks = device_peaks(ctx, dresp, d->out_dtype, h, w, d->layout, eps / 2, 0.5, peak_x,
+                            peak_y, peak_v, max_peaks);
+    if (d->memory == XC_HOST)
+      ck(cudaMemcpy(response, dresp, npix * os, cudaMemcpyDeviceToHost), "D2H response");
     if (stats) {
       *stats = rs;
       stats->gpu_launches += lc.n;

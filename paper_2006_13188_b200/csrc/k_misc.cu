@@ -420,4 +420,84 @@ void launch_real_part(const float2* in, size_t n, int out_f64, void* out, cudaSt
   ++lc.n;
 }
 
+// ------------------------------------------------------------------ find_peaks (device)
+namespace {
+// order-preserving map of a float / double to an unsigned key (max = max key)
+__device__ __forceinline__ unsigned long long okey(double v) {
+  unsigned long long b = __double_as_longlong(v);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double unkey(unsigned long long k) {
+  return __longlong_as_double((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k);
+}
+
+template <class T>
+__global__ void k_max_key(const T* __restrict__ r, size_t n, unsigned long long* mx) {
+  unsigned long long best = 0;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    best = max(best, okey(double(r[i])));
+  for (int o = 16; o; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(mx, best);
+}
+
+// vote_filter.hpp:107-134: a pixel at or above threshold_frac * max is a peak
+// if no pixel within the disk beats it (ties: the earlier one in y-major scan
+// order wins); peaks are appended unordered, the host sorts them
+template <class T>
+__global__ void k_nms(const T* __restrict__ r, int h, int w, int colmajor, double radius,
+                      double frac, const unsigned long long* mx, int R, int cap,
+                      unsigned* count, int* px, int* py, double* pv) {
+  const double thresh = frac * unkey(*mx);
+  const size_t n = size_t(h) * w;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const int y = int(i / w), x = int(i % w);
+    auto at = [&](int yy, int xx) -> double {
+      return double(r[colmajor ? size_t(xx) * h + yy : size_t(yy) * w + xx]);
+    };
+    const double v = at(y, x);
+    if (v < thresh) continue;
+    bool best = true;
+    for (int dy = -R; dy <= R && best; ++dy)
+      for (int dx = -R; dx <= R && best; ++dx) {
+        if (dx == 0 && dy == 0) continue;
+        if (double(dx * dx + dy * dy) > radius * radius) continue;
+        const int xi = x + dx, yi = y + dy;
+        if (xi < 0 || yi < 0 || xi >= w || yi >= h) continue;
+        const double o = at(yi, xi);
+        if (o > v || (o == v && (dy < 0 || (dy == 0 && dx < 0)))) best = false;
+      }
+    if (best) {
+      const unsigned k = atomicAdd(count, 1u);
+      if (int(k) < cap) {
+        px[k] = x;
+        py[k] = y;
+        pv[k] = v;
+      }
+    }
+  }
+}
+}  // namespace
+
+void launch_find_peaks(const void* resp, int f64, int h, int w, int colmajor, double radius,
+                       double frac, int cap, unsigned long long* mx, unsigned* count, int* px,
+                       int* py, double* pv, cudaStream_t st, LaunchCounter& lc) {
+  const size_t n = size_t(h) * w;
+  const int R = radius > 1.0 ? int(ceil(radius)) : 1;
+  cudaMemsetAsync(mx, 0, sizeof(unsigned long long), st);
+  cudaMemsetAsync(count, 0, sizeof(unsigned), st);
+  const int g = grid_for(n, 256);
+  if (f64) {
+    k_max_key<double><<<g, 256, 0, st>>>(static_cast<const double*>(resp), n, mx);
+    k_nms<double><<<g, 256, 0, st>>>(static_cast<const double*>(resp), h, w, colmajor, radius,
+                                     frac, mx, R, cap, count, px, py, pv);
+  } else {
+    k_max_key<float><<<g, 256, 0, st>>>(static_cast<const float*>(resp), n, mx);
+    k_nms<float><<<g, 256, 0, st>>>(static_cast<const float*>(resp), h, w, colmajor, radius,
+                                    frac, mx, R, cap, count, px, py, pv);
+  }
+  lc.n += 2;
+}
+
 }  // namespace xcb

@@ -182,3 +182,12 @@ void launch_gradient(const void* img, int img_f64, int h, int w, int colmajor, f
 void launch_real_part(const float2* in, size_t n, int out_f64, void* out, cudaStream_t st,
                       LaunchCounter& lc);
 }  // namespace xcb
+
+namespace xcb {
+// find_peaks (vote_filter.hpp:107-134) on a device response: global max, then
+// every local maximum within the disk above frac * max appended (x, y, value)
+// to the first `cap` slots; *count = number found (the host sorts).
+void launch_find_peaks(const void* resp, int f64, int h, int w, int colmajor, double radius,
+                       double frac, int cap, unsigned long long* mx, unsigned* count, int* px,
+                       int* py, double* pv, cudaStream_t st, LaunchCounter& lc);
+}  // namespace xcb

@@ -347,8 +347,13 @@ class Peak:  # vote_filter.hpp:99-102
     value: float
 
 
-def find_peaks(resp, radius: float, threshold_frac: float = 0.5, max_peaks: int = 1 << 16):
-    """NMS peaks, sorted by value desc, then y, then x (vote_filter.hpp:107-134)."""
+def find_peaks(resp, radius: float, threshold_frac: float = 0.5, max_peaks: int = 1 << 16,
+               gpu: bool = False, device: int = 0):
+    """NMS peaks, sorted by value desc, then y, then x (vote_filter.hpp:107-134).
+    gpu=True runs the NMS on the GPU (xc_find_peaks_device; a torch CUDA tensor is
+    used in place, a host array is uploaded) -- same peaks as the host version."""
+    if gpu:
+        return _find_peaks_gpu(resp, radius, threshold_frac, max_peaks, device)
     r = np.ascontiguousarray(np.asarray(resp))
     dt = N.XC_F32 if r.dtype == np.float32 else N.XC_F64
     if dt == N.XC_F64 and r.dtype != np.float64:
@@ -363,6 +368,29 @@ def find_peaks(resp, radius: float, threshold_frac: float = 0.5, max_peaks: int 
                                   ys.ctypes.data_as(C.POINTER(C.c_int)),
                                   vs.ctypes.data_as(C.POINTER(C.c_double)), max_peaks,
                                   C.byref(n)))
+    return [Peak(int(xs[i]), int(ys[i]), float(vs[i])) for i in range(min(n.value, max_peaks))]
+
+
+def _find_peaks_gpu(resp, radius, threshold_frac, max_peaks, device):
+    import torch
+    t = resp if isinstance(resp, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(resp))
+    if t.dtype not in (torch.float32, torch.float64):
+        t = t.to(torch.float64)
+    t = t.to(torch.device("cuda", device)).contiguous()
+    dt = N.XC_F32 if t.dtype == torch.float32 else N.XC_F64
+    xs = np.zeros(max_peaks, np.int32)
+    ys = np.zeros(max_peaks, np.int32)
+    vs = np.zeros(max_peaks)
+    n = C.c_int(0)
+    ctx = N.context(device)
+    torch.cuda.synchronize(t.device)
+    N.check(N.lib().xc_find_peaks_device(ctx.handle, C.c_void_p(t.data_ptr()), dt, t.shape[0],
+                                         t.shape[1], N.XC_ROW_MAJOR, float(radius),
+                                         float(threshold_frac),
+                                         xs.ctypes.data_as(C.POINTER(C.c_int)),
+                                         ys.ctypes.data_as(C.POINTER(C.c_int)),
+                                         vs.ctypes.data_as(C.POINTER(C.c_double)), max_peaks,
+                                         C.byref(n)), ctx.handle)
     return [Peak(int(xs[i]), int(ys[i]), float(vs[i])) for i in range(min(n.value, max_peaks))]
 
 

@@ -173,3 +173,16 @@ def test_detect_float32_image_and_errors(orc):
         X.detect_pattern(img, vf, 0)
     with pytest.raises(ValueError, match="gradient requires real field"):
         X.detect_pattern(img.astype(np.complex128), vf, 8)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_find_peaks_device_equals_host(orc, dtype):  # vote_filter.hpp:107-134
+    r = np.random.default_rng(21)
+    resp = np.round(r.uniform(-1, 1, (131, 97)) * 8) / 8  # many exact ties
+    resp = resp.astype(dtype)
+    for radius, frac in [(2.5, 0.3), (1.0, 0.0), (4.0, 0.6), (0.5, 0.5)]:
+        host = [(p.x, p.y, p.value) for p in X.find_peaks(resp, radius, frac)]
+        dev = [(p.x, p.y, p.value) for p in X.find_peaks(resp, radius, frac, gpu=True)]
+        assert dev == host
+        assert host == orc.find_peaks(resp.astype(np.float64), radius, frac)
