@@ -563,6 +563,15 @@ void run_f2(Call& c, const float2* T1, float2* Hh) {
     xcb::launch_cols_fwd(*c.pcol, c.g, T1, Hh, c.st, c.lc);
 }
 
+// XCB_HERM=0 disables the Hermitian half-band paths (A/B timing, tests)
+bool use_herm() {
+  static const bool on = [] {
+    const char* e = std::getenv("XCB_HERM");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void launch_i2(Call& c, const xcb::SigSrc& sig, const float2* T2, const double* base, void* out,
                int out_kind, bool accumulate, bool dc) {
   const xcb::Geo& g = c.g;
@@ -1020,10 +1029,32 @@ int xc_anglemax(xc_context ctx, xc_filter f, const xc_image_desc* d, const void*
                      *std::min_element(c.ks.begin(), c.ks.end()) + 1;
     if (span > 256) throw std::invalid_argument("band span too large for the angle max");
     const size_t npix = size_t(c.rows) * c.cols, os = dtype_size(d->out_dtype);
-    float2* planes = ctx->buf<float2>("planes", size_t(c.bands.n) * npix);
+    // Hermitian half-band mode: real signal and F_{-k} = conj(F_k) over the
+    // selected bands give G_{-k} = conj(G_k); only k >= 0 is transformed
+    const bool real_sig = d->signal_dtype == XC_F32 || d->signal_dtype == XC_F64;
+    bool herm = real_sig && n_angles == 360 && use_herm() && f->hf.hermitian() &&
+                xcb::anglemax_herm_kh(*std::max_element(c.ks.begin(), c.ks.end()));
+    for (int k : c.ks) herm = herm && std::count(c.ks.begin(), c.ks.end(), -k) == 1;
+    xcb::Bands bands = c.bands;
+    std::vector<int> hk;
+    if (herm) {
+      std::vector<int> hs;
+      for (size_t i = 0; i < c.ks.size(); ++i)
+        if (c.ks[i] >= 0) {
+          hk.push_back(c.ks[i]);
+          hs.push_back(c.sidx[i]);
+        }
+      int* db = ctx->buf<int>("bands_half", 2 * hk.size());
+      std::vector<int> hb(hk);
+      hb.insert(hb.end(), hs.begin(), hs.end());
+      ck(cudaMemcpy(db, hb.data(), hb.size() * sizeof(int), cudaMemcpyHostToDevice),
+         "upload bands");
+      bands = xcb::Bands{db, db + hk.size(), int(hk.size())};
+    }
+    float2* planes = ctx->buf<float2>("planes", size_t(bands.n) * npix);
     float2* T1 = ctx->buf<float2>("T1", size_t(c.g.Hx2) * c.g.Pw);
     float2* Hh = ctx->buf<float2>("Hhat", size_t(c.g.Ph) * c.g.Pw);
-    float2* T2 = ctx->buf<float2>("T2", size_t(c.bands.n) * c.g.H2 * c.g.Pw);
+    float2* T2 = ctx->buf<float2>("T2", size_t(bands.n) * c.g.H2 * c.g.Pw);
     cudaEvent_t e0, e1;
     ck(cudaEventCreate(&e0), "event");
     ck(cudaEventCreate(&e1), "event");
@@ -1035,20 +1066,20 @@ int xc_anglemax(xc_context ctx, xc_filter f, const xc_image_desc* d, const void*
       stage(c, "F2_cols_fwd", [&] { run_f2(c, T1, Hh); });
       stage(c, "I1_cols_inv_corr", [&] {
         if (use_pair() && xcb::pair_smem(0, c.g.Ph, c.g))
-          xcb::launch_cols_inv_corr_pair(c.g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);
+          xcb::launch_cols_inv_corr_pair(c.g, Hh, c.Fhat, c.sstride, bands, T2, c.st, c.lc);
         else if (c.fcol && xcb::fast_smem(0, *c.fcol, c.g))
-          xcb::launch_cols_inv_corr_fast(*c.fcol, c.g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st,
+          xcb::launch_cols_inv_corr_fast(*c.fcol, c.g, Hh, c.Fhat, c.sstride, bands, T2, c.st,
                                          c.lc);
         else
-          xcb::launch_cols_inv_corr(*c.pcol, c.g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);
+          xcb::launch_cols_inv_corr(*c.pcol, c.g, Hh, c.Fhat, c.sstride, bands, T2, c.st, c.lc);
       });
       stage(c, "I2_rows_inv_planes", [&] {
         if (use_pair() && xcb::pair_smem(2, c.g.Pw, c.g))
-          xcb::launch_rows_inv_planes_pair(c.g, T2, c.bands.n, planes, c.st, c.lc);
+          xcb::launch_rows_inv_planes_pair(c.g, T2, bands.n, planes, c.st, c.lc);
         else if (c.frow && xcb::fast_smem(4, *c.frow, c.g))
-          xcb::launch_rows_inv_planes_fast(*c.frow, c.g, T2, c.bands.n, planes, c.st, c.lc);
+          xcb::launch_rows_inv_planes_fast(*c.frow, c.g, T2, bands.n, planes, c.st, c.lc);
         else
-          xcb::launch_rows_inv_planes(*c.prow, c.g, T2, c.bands.n, planes, c.st, c.lc);
+          xcb::launch_rows_inv_planes(*c.prow, c.g, T2, bands.n, planes, c.st, c.lc);
       });
       char* dsc = d->memory == XC_DEVICE ? static_cast<char*>(score) + size_t(img) * npix * os
                                          : ctx->buf<char>("score_stage", npix * os);
@@ -1057,8 +1088,12 @@ int xc_anglemax(xc_context ctx, xc_filter f, const xc_image_desc* d, const void*
         darg = d->memory == XC_DEVICE ? argmax + size_t(img) * npix
                                       : ctx->buf<int>("arg_stage", npix);
       stage(c, "anglemax", [&] {
-        xcb::launch_anglemax(planes, c.ks.data(), c.bands.n, npix, n_angles,
-                             d->out_dtype == XC_F64, dsc, darg, c.st, c.lc);
+        if (herm)
+          xcb::launch_anglemax_herm(planes, hk.data(), bands.n, npix, d->out_dtype == XC_F64, dsc,
+                                    darg, c.st, c.lc);
+        else
+          xcb::launch_anglemax(planes, c.ks.data(), c.bands.n, npix, n_angles,
+                               d->out_dtype == XC_F64, dsc, darg, c.st, c.lc);
       });
       ck(cudaGetLastError(), "kernel launch");
       ck(cudaEventRecord(e1, c.st), "event");

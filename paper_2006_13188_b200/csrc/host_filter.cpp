@@ -207,6 +207,21 @@ void reconstruct(const HostFilter& f, int width, int height, double cx, double c
   }
 }
 
+bool HostFilter::hermitian() const {
+  double mx = 0;
+  for (const cplx& c : comps) mx = std::max(mx, std::abs(c));
+  const double tol = 1e-12 * std::max(mx, 1e-300);
+  for (int ci = 0; ci < nc(); ++ci) {
+    int cj = -1;
+    for (int j = 0; j < nc(); ++j)
+      if (ks[j] == -ks[ci]) cj = j;
+    if (cj < 0) return false;
+    for (int r = 0; r < n_rows(); ++r)
+      if (std::abs(comp(r, cj) - std::conj(comp(r, ci))) > tol) return false;
+  }
+  return true;
+}
+
 // ------------------------------------------------------------------ vote filters
 void gradient_host(const double* img, int h, int w, double* mag, double* dir) {
   auto I = [&](int y, int x) { return img[size_t(y) * w + x]; };

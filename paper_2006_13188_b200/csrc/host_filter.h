@@ -28,6 +28,9 @@ struct HostFilter {  // FreqFilter2, freq_filter.hpp:21-46
   double omega() const;
   int index_of(int k) const;
   int render_radius() const;  // engine.hpp:255-258
+  // F_{-k} = conj(F_k) for every retained k (a real filter's angular /
+  // log-radial bands), to 1e-12 of the largest coefficient
+  bool hermitian() const;
 };
 
 // Field2 view of a complex image, row-major [y][x].

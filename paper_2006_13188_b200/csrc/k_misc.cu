@@ -211,6 +211,57 @@ __device__ __forceinline__ void anglemax_fft_body(const float2* __restrict__ pla
 XCB_AM_KERNEL(k_anglemax_fft, 1)
 #undef XCB_AM_KERNEL
 
+// Hermitian half-band angle max: for a real signal and a filter with
+// F_{-k} = conj(F_k) the band responses satisfy G_{-k} = conj(G_k), so
+// S(s) = sum_k G_k w^{ks} = G_0 + 2 Re(sum_{k=1}^{KH} G_k w^{ks}) is real and
+// only the planes k = 0..KH are needed (half the I1 / planes work); the
+// DFT_N2 carries KH nonzero inputs and only the real parts of its outputs
+// are used.  m.idx[k] = plane of band k (k = 0..KH).
+template <int KH, int N2, class TO>
+__global__ void __launch_bounds__(128)
+    k_anglemax_herm(const float2* __restrict__ planes, AngleMap m, size_t npix,
+                    TO* __restrict__ score, int* __restrict__ argmax) {
+  constexpr int N = 360, N1 = N / N2;
+  static_assert(N1 * N2 == N && N2 > KH, "bad angle-max split");
+  __shared__ float2 tws[N1 * KH];  // w^{k s1}, [s1][k-1]
+  for (int i = threadIdx.x; i < N1 * KH; i += blockDim.x) {
+    const int s1 = i / KH, k = i % KH + 1;
+    double sn, cs;
+    sincospi(-2.0 * double(k * s1) / N, &sn, &cs);
+    tws[i] = make_float2(float(cs), float(sn));
+  }
+  __syncthreads();
+  const size_t p = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+  if (p >= npix) return;
+  const float g0 = m.idx[0] >= 0 ? planes[size_t(m.idx[0]) * npix + p].x : 0.f;
+  float2 G[KH];
+#pragma unroll
+  for (int k = 1; k <= KH; ++k)
+    G[k - 1] = m.idx[k] >= 0 ? planes[size_t(m.idx[k]) * npix + p] : make_float2(0.f, 0.f);
+  float best = -1.f;
+  int arg = 0;
+#pragma unroll 1
+  for (int s1 = 0; s1 < N1; ++s1) {
+    float2 v[N2];
+#pragma unroll
+    for (int q = 0; q < N2; ++q) v[q] = make_float2(0.f, 0.f);
+    const float2* tw = tws + s1 * KH;
+#pragma unroll
+    for (int k = 1; k <= KH; ++k) v[k] = c_mul(G[k - 1], tw[k - 1]);
+    Dft<N2>::run(v);
+#pragma unroll
+    for (int s2 = 0; s2 < N2; ++s2) {
+      const float a = fabsf(fmaf(2.f, v[Dft<N2>::pos(s2)].x, g0));
+      if (a > best) {
+        best = a;
+        arg = s1 + N1 * s2;
+      }
+    }
+  }
+  score[p] = TO(best);
+  if (argmax) argmax[p] = arg;
+}
+
 // Looped variant (twiddles from a smem table) for wide band spans, where the
 // unrolled kernel would not fit in registers.
 template <int KH, int N2, class TO>
@@ -305,6 +356,33 @@ void launch_smooth_finish(const float2* num, const float2* den, size_t n, int ou
                                            clamped);
   lc.n += 2;
 }
+
+void launch_anglemax_herm(const float2* planes, const int* ks_host, int nb, size_t npix,
+                          int score_f64, void* score, int* argmax, cudaStream_t st,
+                          LaunchCounter& lc) {
+  int kh = 0;
+  for (int i = 0; i < nb; ++i) kh = std::max(kh, ks_host[i]);
+  AngleMap m{};
+  m.nd = kh + 1;
+  for (int k = 0; k <= kh; ++k) m.idx[k] = -1;
+  for (int i = 0; i < nb; ++i) m.idx[ks_host[i]] = i;
+  const int bs = 128;
+  const int grid = int((npix + bs - 1) / bs);
+#define XCB_AMH(KHV, N2V)                                                                   \
+  if (kh == KHV) {                                                                         \
+    if (score_f64)                                                                         \
+      k_anglemax_herm<KHV, N2V, double><<<grid, bs, 0, st>>>(planes, m, npix,              \
+                                                            static_cast<double*>(score), argmax); \
+    else                                                                                   \
+      k_anglemax_herm<KHV, N2V, float><<<grid, bs, 0, st>>>(planes, m, npix,               \
+                                                           static_cast<float*>(score), argmax);  \
+  }
+  XCB_AMH(4, 12) XCB_AMH(8, 18) XCB_AMH(16, 36)
+#undef XCB_AMH
+  ++lc.n;
+}
+
+int anglemax_herm_kh(int kh) { return kh == 4 || kh == 8 || kh == 16; }
 
 void launch_anglemax(const float2* planes, const int* ks_host, int nb, size_t npix,
                      int n_angles, int score_f64, void* score, int* argmax, cudaStream_t st,

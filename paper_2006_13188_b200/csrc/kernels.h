@@ -106,6 +106,13 @@ void launch_anglemax(const float2* planes, const int* ks_host, int nb, size_t np
                      int n_angles, int score_f64, void* score, int* argmax,
                      cudaStream_t st, LaunchCounter& lc);
 
+// Hermitian half-band angle max (real signal, F_{-k} = conj F_k): planes of
+// bands k = 0..KH only (ks_host: their k values, plane order); 360 angles.
+void launch_anglemax_herm(const float2* planes, const int* ks_host, int nb, size_t npix,
+                          int score_f64, void* score, int* argmax, cudaStream_t st,
+                          LaunchCounter& lc);
+int anglemax_herm_kh(int kh);  // 1 if KH has a half-band kernel (4, 8, 16)
+
 // Upload the plan's twiddles; returns device pointer (owned by caller).
 float2* upload_twiddles(const FftPlan& p);
 

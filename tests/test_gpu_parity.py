@@ -312,11 +312,16 @@ def test_tiny_and_ragged_images(orc, shape):
 # --------------------------------------------- fast-path coverage (pad table)
 
 @pytest.mark.parametrize("n_angles,m_max", [(360, 4), (360, 8), (100, 4)])
-def test_anglemax_fft_and_generic(orc, n_angles, m_max):
-    """360 angles with |m| <= KH runs the FFT evaluation; other n the Horner one."""
+@pytest.mark.parametrize("real_filter", [False, True])
+def test_anglemax_fft_and_generic(orc, n_angles, m_max, real_filter):
+    """360 angles with |m| <= KH runs the FFT evaluation; other n the Horner one.
+    A real filter on a real signal takes the Hermitian half-band path
+    (G_{-k} = conj G_k: only k >= 0 transformed) where it applies."""
     from paper_2006_13188_b200 import workloads as WL
     r = np.random.default_rng(5)
     f = WL.angular_filter(9, 4.0, m_max, r)
+    if real_filter:
+        f = f.real + 0.0j
     F = X.decompose_rotation2(f, 9, 9, 2 * m_max, 18, 4 * m_max + 4, 9.0)
     H = r.standard_normal((70, 90)).astype(np.float32)
     score, arg = X.anglemax(H, F, n_angles)
