@@ -644,45 +644,78 @@ void run_gather2(Call& c, const xcb::SigSrc* sig, double* const* base, void* con
     launch_i2(c, sig[i], T2 + i * tstride, base[i], out[i], out_kind, accumulate, dc);
 }
 
+// Bands k >= 0 of the call (descending, as in c.bands) on the device, or an
+// empty Bands when the Hermitian half-band mode does not apply: real signal,
+// F_{-k} = conj(F_k) (hermitian()), and a symmetric band selection.
+xcb::Bands half_bands(Call& c, bool real_sig) {
+  if (!use_herm() || !real_sig || !c.f->hf.hermitian()) return xcb::Bands{nullptr, nullptr, 0};
+  for (int k : c.ks)
+    if (std::count(c.ks.begin(), c.ks.end(), -k) != 1) return xcb::Bands{nullptr, nullptr, 0};
+  std::vector<int> hk, hs;
+  for (size_t i = 0; i < c.ks.size(); ++i)
+    if (c.ks[i] >= 0) {
+      hk.push_back(c.ks[i]);
+      hs.push_back(c.sidx[i]);
+    }
+  int* db = c.ctx->buf<int>("bands_half", 2 * hk.size());
+  hk.insert(hk.end(), hs.begin(), hs.end());
+  ck(cudaMemcpyAsync(db, hk.data(), hk.size() * sizeof(int), cudaMemcpyHostToDevice, c.st),
+     "upload bands");
+  ck(cudaStreamSynchronize(c.st), "upload bands");
+  const int n = int(hs.size());
+  return xcb::Bands{db, db + n, n};
+}
+
 void run_scatter(Call& c, const xcb::SigSrc& sig, const double* base, void* out, int out_kind,
                  bool accumulate, bool dc) {
   const xcb::Geo& g = c.g;
-  float2* T1 = c.ctx->buf<float2>("T1b", size_t(c.bands.n) * g.Hx2 * g.Pw);
+  // Hermitian half-band mode (real signal, real filter): the -k terms are the
+  // conjugates of the +k terms, so out = 2 Re(sum_{k>=0} w_k ...) with w_0 = 1/2;
+  // it needs the pair-engine S2 and S4 (half weights, 2 Re)
+  xcb::Bands bands = c.bands;
+  bool half = use_pair() && xcb::pair_smem(4, g.Ph, g) && xcb::pair_smem(7, g.Pw, g);
+  if (half) {
+    const xcb::Bands hb = half_bands(c, !sig.is_complex);
+    half = hb.n > 0;
+    if (half) bands = hb;
+  }
+  float2* T1 = c.ctx->buf<float2>("T1b", size_t(bands.n) * g.Hx2 * g.Pw);
   float2* Sg = c.ctx->buf<float2>("Sigma", size_t(g.Ph) * g.Pw);
   float2* T2 = c.ctx->buf<float2>("T2s", size_t(g.H2) * g.Pw);
   if (use_pair() && xcb::pair_smem(3, g.Pw, g)) {
     stage(c, "S1_rows_fwd_premul", [&] {
-      xcb::launch_rows_fwd_premul_pair(g, sig, base, c.bands, T1, c.st, c.lc);
+      xcb::launch_rows_fwd_premul_pair(g, sig, base, bands, T1, c.st, c.lc);
     });
   } else if (c.frow && xcb::fast_smem(2, *c.frow, g)) {
     stage(c, "S1_rows_fwd_premul", [&] {
-      xcb::launch_rows_fwd_premul_fast(*c.frow, g, sig, base, c.bands, T1, c.st, c.lc);
+      xcb::launch_rows_fwd_premul_fast(*c.frow, g, sig, base, bands, T1, c.st, c.lc);
     });
   } else {
     stage(c, "S1_rows_fwd_premul", [&] {
-      xcb::launch_rows_fwd_premul(*c.prow, g, sig, base, c.bands, T1, c.st, c.lc);
+      xcb::launch_rows_fwd_premul(*c.prow, g, sig, base, bands, T1, c.st, c.lc);
     });
   }
   if (use_pair() && xcb::pair_smem(4, g.Ph, g)) {
     stage(c, "S2_cols_fwd_mac_inv", [&] {
-      xcb::launch_cols_fwd_mac_inv_pair(g, T1, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);
+      xcb::launch_cols_fwd_mac_inv_pair(g, T1, c.Fhat, c.sstride, bands, half ? 1 : 0, T2, c.st,
+                                        c.lc);
     });
   } else if (c.fcol && xcb::fast_smem(3, *c.fcol, g)) {
     stage(c, "S2_cols_fwd_mac_inv", [&] {
-      xcb::launch_cols_fwd_mac_inv_fast(*c.fcol, g, T1, c.Fhat, c.sstride, c.bands, T2, c.st,
+      xcb::launch_cols_fwd_mac_inv_fast(*c.fcol, g, T1, c.Fhat, c.sstride, bands, T2, c.st,
                                         c.lc);
     });
   } else {
     stage(c, "S2_cols_fwd_mac_inv", [&] {
-      xcb::launch_cols_fwd_mac_inv(*c.pcol, g, T1, c.Fhat, c.sstride, c.bands, Sg, T2, c.st,
+      xcb::launch_cols_fwd_mac_inv(*c.pcol, g, T1, c.Fhat, c.sstride, bands, Sg, T2, c.st,
                                    c.lc);
     });
   }
   const cplx dcv = dc ? xcb::inner_dc_value(c.f->hf) : cplx(0);  // engine.hpp:370
   stage(c, "S4_rows_inv_out", [&] {
     if (use_pair() && xcb::pair_smem(7, g.Pw, g))
-      xcb::launch_rows_inv_out_pair(g, T2, out_kind, out, accumulate ? 1 : 0, sig, dcv.real(),
-                                    dcv.imag(), c.st, c.lc);
+      xcb::launch_rows_inv_out_pair(g, T2, out_kind, out, accumulate ? 1 : 0, half ? 1 : 0, sig,
+                                    dcv.real(), dcv.imag(), c.st, c.lc);
     else
       xcb::launch_rows_inv_out(*c.prow, g, T2, out_kind, out, accumulate ? 1 : 0, sig, dcv.real(),
                                dcv.imag(), c.st, c.lc);

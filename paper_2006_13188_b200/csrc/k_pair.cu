@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
 template <class PF>
 __global__ void __launch_bounds__(PF::T, 1)
     k_cols_fwd_mac_ilv(Geo g, const float4* __restrict__ T1, const float4* __restrict__ Fh,
-                       size_t sstride4, Bands bl, float2* __restrict__ T2,
+                       size_t sstride4, Bands bl, int half0, float2* __restrict__ T2,
                        const float2* __restrict__ twm, const float2* __restrict__ twl) {
   constexpr int L = PF::L, R2 = PF::R2;  // L = Ph
   constexpr int kThr = 2 * R2;
@@ -566,6 +566,9 @@ __global__ void __launch_bounds__(PF::T, 1)
     PF::pass1(W0, W1, TWs);
     __syncthreads();
     const float2* SF = reinterpret_cast<const float2*>(SF4 + (bi & 1) * L);
+    // Hermitian half-band mode: the k = 0 band enters with weight 1/2 (S4
+    // then takes 2 Re)
+    const float wk = half0 && bl.k[bi] == 0 ? 0.5f : 1.f;
     const int tt = opaque_i(t);
     const float2* fp = SF + tt;  // F^[k] of this thread's sequence: 2 k + g, k = j + r NB2
     auto mac = [&](float2 (&a)[R2]) {
@@ -586,7 +589,7 @@ __global__ void __launch_bounds__(PF::T, 1)
         for (int i = 0; i < C; ++i) {
           const int r = r0 + i;
           if (r >= R2) break;
-          const float2 x = c_mul(a[Dft<R2>::pos(r)], fp[2 * r * PF::NB2]);
+          const float2 x = c_scale(c_mul(a[Dft<R2>::pos(r)], fp[2 * r * PF::NB2]), wk);
           acc[i] = bi > 0 ? c_add(acc[i], x) : x;
         }
 #pragma unroll
@@ -737,7 +740,7 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
 template <class PF, class TO>
 __global__ void __launch_bounds__(PF::T, PF::MINB)
     k_rows_inv_out_ilv(Geo g, const float4* __restrict__ T2, TO* __restrict__ out,
-                       int accumulate, SigSrc dcs, double dcr, double dci, float scale,
+                       int accumulate, int real2, SigSrc dcs, double dcr, double dci, float scale,
                        const float2* __restrict__ twm, const float2* __restrict__ twl) {
   extern __shared__ __align__(16) float4 smp[];
   float2* W0 = reinterpret_cast<float2*>(smp);
@@ -763,8 +766,9 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
       const int x = j + r * PF::NB2 - g.off;
       if (x < 0 || x >= g.W) continue;
       const size_t i = size_t(y) * g.W + x;
-      OutOps<TO>::put(out, i, c_scale(c_conj(a[Dft<PF::R2>::pos(r)]), scale), accumulate != 0,
-                      dc_term(dcs, i, dcr, dci));
+      float2 v = c_scale(c_conj(a[Dft<PF::R2>::pos(r)]), scale);
+      if (real2) v = make_float2(2.f * v.x, 0.f);  // Hermitian half-band: out = 2 Re
+      OutOps<TO>::put(out, i, v, accumulate != 0, dc_term(dcs, i, dcr, dci));
     }
   };
   PF::pass2_all(W1, tl, store);
@@ -940,8 +944,8 @@ void launch_rows_fwd_premul_pair(const Geo& g, const SigSrc& s, const double* ba
 }
 
 void launch_cols_fwd_mac_inv_pair(const Geo& g, const float2* T1, const float2* Fhat,
-                                  size_t sstride, const Bands& b, float2* T2, cudaStream_t st,
-                                  LaunchCounter& lc) {
+                                  size_t sstride, const Bands& b, int half0, float2* T2,
+                                  cudaStream_t st, LaunchCounter& lc) {
   const size_t sm = pair_smem(4, g.Ph, g);
 #define XCB_BODY(LL, R0, R1, R2, PP)                                                         \
   case LL: {                                                                                \
@@ -950,7 +954,7 @@ void launch_cols_fwd_mac_inv_pair(const Geo& g, const float2* T1, const float2* 
     set_smem(k_cols_fwd_mac_ilv<PF>, sm);                                                   \
     k_cols_fwd_mac_ilv<PF><<<g.Pw / 2, PF::T, sm, st>>>(                                    \
         g, reinterpret_cast<const float4*>(T1), reinterpret_cast<const float4*>(Fhat),      \
-        sstride / 2, b, T2, tw.mid, tw.last);                                               \
+        sstride / 2, b, half0, T2, tw.mid, tw.last);                                        \
     break;                                                                                  \
   }
   XCB_PAIR_DISPATCH(g.Ph, XCB_BODY)
@@ -992,8 +996,8 @@ void launch_cols_fwd_pair(const Geo& g, const float2* T1, float2* spec, cudaStre
 }
 
 void launch_rows_inv_out_pair(const Geo& g, const float2* T2, int out_kind, void* out,
-                              int accumulate, const SigSrc& dcs, double dcr, double dci,
-                              cudaStream_t st, LaunchCounter& lc) {
+                              int accumulate, int real2, const SigSrc& dcs, double dcr,
+                              double dci, cudaStream_t st, LaunchCounter& lc) {
   const size_t sm = pair_smem(7, g.Pw, g);
   const float scale = float(1.0 / (double(g.Ph) * double(g.Pw)));
   const float4* t2 = reinterpret_cast<const float4*>(T2);
@@ -1004,12 +1008,13 @@ void launch_rows_inv_out_pair(const Geo& g, const float2* T2, int out_kind, void
     if (out_kind == OUT_C64) {                                                              \
       set_smem(k_rows_inv_out_ilv<PF, float2>, sm);                                         \
       k_rows_inv_out_ilv<PF, float2><<<g.H2 / 2, PF::T, sm, st>>>(                          \
-          g, t2, static_cast<float2*>(out), accumulate, dcs, dcr, dci, scale, tw.mid,       \
+          g, t2, static_cast<float2*>(out), accumulate, real2, dcs, dcr, dci, scale, tw.mid, \
           tw.last);                                                                         \
     } else {                                                                                \
       set_smem(k_rows_inv_out_ilv<PF, double2>, sm);                                        \
       k_rows_inv_out_ilv<PF, double2><<<g.H2 / 2, PF::T, sm, st>>>(                         \
-          g, t2, static_cast<double2*>(out), accumulate, dcs, dcr, dci, scale, tw.mid,      \
+          g, t2, static_cast<double2*>(out), accumulate, real2, dcs, dcr, dci, scale,       \
+          tw.mid,                                                                           \
           tw.last);                                                                         \
     }                                                                                       \
     break;                                                                                  \

@@ -158,17 +158,19 @@ void launch_cols_inv_corr_pair(const Geo& g, const float2* Hhat, const float2* F
 // scatter stages S1 / S2 on the pair engine (stages 3 / 4 of pair_smem)
 void launch_rows_fwd_premul_pair(const Geo& g, const SigSrc& s, const double* base,
                                  const Bands& b, float2* T1, cudaStream_t st, LaunchCounter& lc);
+// half0: Hermitian half-band mode (bands k >= 0; the k = 0 band weighted 1/2)
 void launch_cols_fwd_mac_inv_pair(const Geo& g, const float2* T1, const float2* Fhat,
-                                  size_t sstride, const Bands& b, float2* T2, cudaStream_t st,
-                                  LaunchCounter& lc);
+                                  size_t sstride, const Bands& b, int half0, float2* T2,
+                                  cudaStream_t st, LaunchCounter& lc);
 // single transforms on the pair engine: F1 (stage 5), F2 (6), S4 (7)
 void launch_rows_fwd_pair(const Geo& g, const SigSrc& s, float2* T1, cudaStream_t st,
                           LaunchCounter& lc);
 void launch_cols_fwd_pair(const Geo& g, const float2* T1, float2* spec, cudaStream_t st,
                           LaunchCounter& lc);
+// real2: out = 2 Re(IFFT) (+ dc H), the Hermitian half-band scatter
 void launch_rows_inv_out_pair(const Geo& g, const float2* T2, int out_kind, void* out,
-                              int accumulate, const SigSrc& dcs, double dcr, double dci,
-                              cudaStream_t st, LaunchCounter& lc);
+                              int accumulate, int real2, const SigSrc& dcs, double dcr,
+                              double dci, cudaStream_t st, LaunchCounter& lc);
 // planes stage (angle max) on the interleaved engine; stage 2 of pair_smem
 void launch_rows_inv_planes_pair(const Geo& g, const float2* T2, int nbands, float2* planes,
                                  cudaStream_t st, LaunchCounter& lc);

@@ -550,3 +550,27 @@ def test_config4_full_size_smoothing(orc):
     den = _scatter_at(orc, OF, wgt, phi, ys, xs) + dc * wgt[ys, xs]
     ref = (num / den).real
     assert orc.rel_l2(got.output[ys, xs], ref) < TOL
+
+
+@pytest.mark.parametrize("real_filter", [False, True])
+def test_scatter_hermitian_half_band(orc, real_filter):
+    """xconv_fast of a real signal with a real filter (F_{-k} = conj F_k) takes the
+    Hermitian half-band path on the pair engine (bands k >= 0, out = 2 Re); a
+    complex filter takes the full path.  Both against the spectral oracle at
+    sampled pixels (pad 1152)."""
+    from paper_2006_13188_b200 import workloads as WL
+    r = np.random.default_rng(17)
+    f = WL.angular_filter(16, 8.0, 8, r)
+    if real_filter:
+        f = f.real + 0.0j
+    F = X.decompose_rotation2(f, 16, 16, 16, 32, 34, 16.0)
+    n = 1024
+    H = r.uniform(0, 1, (n, n)).astype(np.float32)
+    T = r.uniform(0, 2 * np.pi, (n, n)).astype(np.float32)
+    got = X.xconv_fast(H, X.XformField.rotation(T), F).output
+    if real_filter:
+        assert np.max(np.abs(got.imag)) == 0.0
+    ys = np.concatenate([r.integers(0, n, 40), [0, n - 1, 0, n - 1]])
+    xs = np.concatenate([r.integers(0, n, 40), [0, 0, n - 1, n - 1]])
+    ref = orc.spectral_oracle_at(1, H, ROT, T, ofilter(orc, F), ys, xs)
+    assert orc.rel_l2(got[ys, xs], ref) < TOL
