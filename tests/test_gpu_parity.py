@@ -505,10 +505,10 @@ def test_config3_full_size_anglemax(orc):
         assert abs(p.x - cx) <= 2 and abs(p.y - cy) <= 2
 
 
-def _scatter_at(orc, F, x, phi, ys, xs):
+def _scatter_at(orc, F, x, phi, ys, xs, periodic=False):
     """Scatter (xconv) at sampled pixels, direct in double: out(p) =
     sum_u sum_k F_k(u) e^{-i k phi(p-u)} x(p-u) (fft.hpp:74-77 convolution,
-    engine.hpp:353-358 premultiply), zero padding."""
+    engine.hpp:353-358 premultiply), zero padding or periodic wrap."""
     R = int(np.ceil(F.r_max))
     side = 2 * R + 1
     comps = np.stack([orc.render_component(F, ci, side, side, R, R) for ci in range(len(F.ks))])
@@ -518,6 +518,8 @@ def _scatter_at(orc, F, x, phi, ys, xs):
     out = np.zeros(len(ys), np.complex128)
     for i, (y, xx0) in enumerate(zip(ys, xs)):
         qy, qx = y - d, xx0 - d  # q = p - u for u = (d_y, d_x)
+        if periodic:
+            qy, qx = qy % h, qx % w
         vy, vx = (qy >= 0) & (qy < h), (qx >= 0) & (qx < w)
         xv = np.zeros((side, side))
         ph = np.zeros((side, side))
@@ -573,4 +575,27 @@ def test_scatter_hermitian_half_band(orc, real_filter):
     ys = np.concatenate([r.integers(0, n, 40), [0, n - 1, 0, n - 1]])
     xs = np.concatenate([r.integers(0, n, 40), [0, 0, n - 1, n - 1]])
     ref = orc.spectral_oracle_at(1, H, ROT, T, ofilter(orc, F), ys, xs)
+    assert orc.rel_l2(got[ys, xs], ref) < TOL
+
+
+@pytest.mark.parametrize("h,w,periodic,real_filter", [(1101, 1000, False, False),
+                                                      (1101, 1101, True, False),
+                                                      (1101, 1101, True, True)])
+def test_scatter_pair_engine_geometry_edges(orc, h, w, periodic, real_filter):
+    """Scatter on the pair engine at pad 1152 with an odd height, a row length on
+    another plan (1024), and the periodic wrap (odd crop offset R = 17), in the
+    full and the Hermitian half-band modes, against a direct scatter."""
+    from paper_2006_13188_b200 import workloads as WL
+    r = np.random.default_rng(23)
+    f = WL.angular_filter(17, 7.0, 6, r)
+    if real_filter:
+        f = f.real + 0.0j
+    F = X.decompose_rotation2(f, 17, 17, 12, 24, 28, 16.5)
+    H = r.uniform(0, 1, (h, w)).astype(np.float32)
+    T = r.uniform(0, 2 * np.pi, (h, w)).astype(np.float32)
+    got = X.xconv_fast(H, X.XformField.rotation(T), F, X.XConvPlan(periodic=periodic)).output
+    ys = np.concatenate([r.integers(0, h, 30), [0, h - 1, 0, h - 1]])
+    xs = np.concatenate([r.integers(0, w, 30), [0, 0, w - 1, w - 1]])
+    ref = _scatter_at(orc, ofilter(orc, F), H.astype(np.float64), T.astype(np.float64), ys, xs,
+                      periodic)
     assert orc.rel_l2(got[ys, xs], ref) < TOL
