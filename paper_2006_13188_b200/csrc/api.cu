@@ -82,6 +82,21 @@ struct xc_context_s {
   std::map<int, PlanEntry> plans;
   std::map<int, PlanEntry> fast_plans;  // L -> in-place radix-16-last plan (or tw == null)
   std::map<std::string, DevBuf> bufs;
+  // events reused across calls (HostPipe slots, call timing)
+  std::vector<cudaEvent_t> ev_sync, ev_timing;
+  size_t ev_sync_used = 0, ev_timing_used = 0;
+  cudaEvent_t event(bool timing) {
+    auto& pool = timing ? ev_timing : ev_sync;
+    size_t& used = timing ? ev_timing_used : ev_sync_used;
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      ck(timing ? cudaEventCreate(&e) : cudaEventCreateWithFlags(&e, cudaEventDisableTiming),
+         "event");
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  void release_events() { ev_sync_used = ev_timing_used = 0; }
   // per-stage CUDA-event profile (xc_profile_*): events are recorded on the
   // launch stream around each stage and resolved at the call's sync points
   bool profiling = false;
@@ -110,6 +125,8 @@ struct xc_context_s {
     for (auto& kv : plans) cudaFree(kv.second.tw);
     for (auto& kv : fast_plans) cudaFree(kv.second.tw);
     for (auto& kv : bufs) cudaFree(kv.second.p);
+    for (cudaEvent_t e : ev_sync) cudaEventDestroy(e);
+    for (cudaEvent_t e : ev_timing) cudaEventDestroy(e);
     if (own) cudaStreamDestroy(own);
     if (cp_in) cudaStreamDestroy(cp_in);
     if (cp_out) cudaStreamDestroy(cp_out);
@@ -290,7 +307,18 @@ float2* filter_spectra(Call& c) {
 // gives the same zero-padded linear filtering (fft.hpp:85-86 uses
 // next_fast_size(extent + 2R + 1)); prefer a length with a fast plan (k_fast.cu)
 // when it costs at most 15% over the smallest 2/3/5-smooth length.
+int pick_pad_uncached(int n);
+// pad sizes are cached: the search builds candidate plans
 int pick_pad(int n) {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(n);
+  if (it != cache.end()) return it->second;
+  return cache[n] = pick_pad_uncached(n);
+}
+
+int pick_pad_uncached(int n) {
   const int L0 = xcb::pick_fft_length(n);
   if (L0 < 0) return L0;
   for (int s = n; s <= L0 + L0 / 7; ++s) {
@@ -393,23 +421,14 @@ struct HostPipe {
   static constexpr int NS = 4;  // slots: two groups of up to two images in flight
   cudaEvent_t in_done[NS]{}, comp_done[NS]{}, out_done[NS]{}, t0{}, t1{};
   int issued = 0;
+  // events come from the context's pool (released when the call returns)
   explicit HostPipe(Call& call) : c(&call), host(call.d.memory == XC_HOST) {
+    if (!host) return;
     for (int s = 0; s < NS; ++s) {
-      ck(cudaEventCreateWithFlags(&in_done[s], cudaEventDisableTiming), "event");
-      ck(cudaEventCreateWithFlags(&comp_done[s], cudaEventDisableTiming), "event");
-      ck(cudaEventCreateWithFlags(&out_done[s], cudaEventDisableTiming), "event");
+      in_done[s] = call.ctx->event(false);
+      comp_done[s] = call.ctx->event(false);
+      out_done[s] = call.ctx->event(false);
     }
-    ck(cudaEventCreate(&t0), "event");
-    ck(cudaEventCreate(&t1), "event");
-  }
-  ~HostPipe() {
-    for (int s = 0; s < NS; ++s) {
-      cudaEventDestroy(in_done[s]);
-      cudaEventDestroy(comp_done[s]);
-      cudaEventDestroy(out_done[s]);
-    }
-    cudaEventDestroy(t0);
-    cudaEventDestroy(t1);
   }
   size_t npix() const { return size_t(c->rows) * c->cols; }
   static std::string slot_name(const char* b, int s) { return b + std::to_string(s); }
@@ -911,9 +930,8 @@ int xc_run(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d, const 
     const bool dc = c.f->hf.group == XC_SCALE2 && !(flags & XC_FLAG_NO_INNER_DC);
     const size_t npix = size_t(c.rows) * c.cols, os = dtype_size(d->out_dtype);
     const int out_kind = d->out_dtype == XC_C64 ? xcb::OUT_C64 : xcb::OUT_C128;
-    cudaEvent_t e0, e1;
-    ck(cudaEventCreate(&e0), "event");
-    ck(cudaEventCreate(&e1), "event");
+    ctx->release_events();
+    cudaEvent_t e0 = ctx->event(true), e1 = ctx->event(true);
     double gpu_s = 0;
     HostPipe hp(c);
     const int G = mode == XC_CORRELATION ? gather_group(c) : 1;
@@ -953,8 +971,6 @@ int xc_run(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d, const 
     ck(cudaEventRecord(e1, c.st), "event");
     hp.finish();
     gpu_s = event_seconds(e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     ctx->resolve_profile();
     fill_stats(c, stats, gpu_s,
                std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count(),
@@ -996,9 +1012,8 @@ int xc_smooth(xc_context ctx, xc_filter f, const xc_image_desc* d, const void* s
     float2* den = ctx->buf<float2>("smooth_den", npix);
     unsigned* red = ctx->buf<unsigned>("smooth_red", 2);
     long long clamped_total = 0;
-    cudaEvent_t e0, e1;
-    ck(cudaEventCreate(&e0), "event");
-    ck(cudaEventCreate(&e1), "event");
+    ctx->release_events();
+    cudaEvent_t e0 = ctx->event(true), e1 = ctx->event(true);
     double gpu_s = 0;
     for (int img = 0; img < d->batch; ++img) {
       Staged s = stage_inputs(c, signal, param, img);
@@ -1035,8 +1050,6 @@ int xc_smooth(xc_context ctx, xc_filter f, const xc_image_desc* d, const void* s
         c.d2h_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       }
     }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     ctx->resolve_profile();
     fill_stats(c, stats, gpu_s,
                std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count(),
@@ -1088,9 +1101,8 @@ int xc_anglemax(xc_context ctx, xc_filter f, const xc_image_desc* d, const void*
     float2* T1 = ctx->buf<float2>("T1", size_t(c.g.Hx2) * c.g.Pw);
     float2* Hh = ctx->buf<float2>("Hhat", size_t(c.g.Ph) * c.g.Pw);
     float2* T2 = ctx->buf<float2>("T2", size_t(bands.n) * c.g.H2 * c.g.Pw);
-    cudaEvent_t e0, e1;
-    ck(cudaEventCreate(&e0), "event");
-    ck(cudaEventCreate(&e1), "event");
+    ctx->release_events();
+    cudaEvent_t e0 = ctx->event(true), e1 = ctx->event(true);
     double gpu_s = 0;
     for (int img = 0; img < d->batch; ++img) {
       Staged s = stage_inputs(c, signal, nullptr, img);
@@ -1144,8 +1156,6 @@ int xc_anglemax(xc_context ctx, xc_filter f, const xc_image_desc* d, const void*
         c.d2h_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       }
     }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     ctx->resolve_profile();
     fill_stats(c, stats, gpu_s,
                std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count(),
