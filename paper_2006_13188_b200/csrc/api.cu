@@ -107,8 +107,6 @@ struct xc_context_s {
     for (auto& e : pending) {
       float ms = 0;
       cudaEventElapsedTime(&ms, e.a, e.b);
-      cudaEventDestroy(e.a);
-      cudaEventDestroy(e.b);
       auto it = std::find_if(prof.begin(), prof.end(),
                              [&](const std::pair<std::string, StageTotal>& p) {
                                return p.first == e.name;
@@ -391,9 +389,7 @@ void stage(Call& c, const char* name, Fn&& fn) {
     fn();
     return;
   }
-  StageEvents e{name, nullptr, nullptr};
-  ck(cudaEventCreate(&e.a), "event");
-  ck(cudaEventCreate(&e.b), "event");
+  StageEvents e{name, c.ctx->event(true), c.ctx->event(true)};  // pooled, reused after resolve
   ck(cudaEventRecord(e.a, c.st), "event");
   fn();
   ck(cudaEventRecord(e.b, c.st), "event");
