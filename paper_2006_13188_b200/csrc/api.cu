@@ -279,24 +279,26 @@ float2* filter_spectra(Call& c) {
   if (it != c.f->spectra.end()) return it->second;
   const xcb::HostFilter& hf = c.f->hf;
   const int R = c.g.R, S = 2 * R + 1, nb = hf.nc();
-  // render every band once (freq_filter.hpp:173-184), fp64 -> fp32
-  std::vector<cplx> tmp(size_t(S) * S);
-  std::vector<float2> comps(size_t(nb) * S * S);
-  for (int ci = 0; ci < nb; ++ci) {
-    xcb::render_component(hf, ci, S, S, double(R), double(R), c.transposed != 0, tmp.data());
-    for (size_t i = 0; i < tmp.size(); ++i)
-      comps[size_t(ci) * S * S + i] = make_float2(float(tmp[i].real()), float(tmp[i].imag()));
-  }
-  float2* dcomps = c.ctx->buf<float2>("filter_comps", comps.size());
-  ck(cudaMemcpyAsync(dcomps, comps.data(), comps.size() * sizeof(float2),
-                     cudaMemcpyHostToDevice, c.st),
-     "upload components");
+  // render every band once on the GPU (freq_filter.hpp:173-184; the host
+  // render_component is the same formula), fp64 -> fp32
+  std::vector<double2> hc(hf.comps.size());
+  for (size_t i = 0; i < hc.size(); ++i) hc[i] = make_double2(hf.comps[i].real(), hf.comps[i].imag());
+  double2* dtab = c.ctx->buf<double2>("filter_table", hc.size());
+  int* dks = c.ctx->buf<int>("filter_ks", size_t(nb));
+  ck(cudaMemcpyAsync(dtab, hc.data(), hc.size() * sizeof(double2), cudaMemcpyHostToDevice, c.st),
+     "upload filter table");
+  ck(cudaMemcpyAsync(dks, hf.ks.data(), size_t(nb) * sizeof(int), cudaMemcpyHostToDevice, c.st),
+     "upload ks");
+  float2* dcomps = c.ctx->buf<float2>("filter_comps", size_t(nb) * S * S);
+  xcb::launch_render(dtab, dks, nb, hf.group, hf.n_radii, hf.n_angles, hf.r_max, hf.r_min,
+                     hf.group == 1 ? hf.omega() : 0.0, S, R, c.transposed != 0, dcomps, c.st,
+                     c.lc);
   float2* T1f = c.ctx->buf<float2>("filter_T1", size_t(nb) * (S + 1) * c.g.Pw);
   float2* spec = nullptr;
   ck(cudaMalloc(&spec, size_t(nb) * c.g.Ph * c.g.Pw * sizeof(float2)), "cudaMalloc spectra");
   xcb::launch_filter_spectra(*c.prow, *c.pcol, c.g, dcomps, nb, T1f, spec, c.st, c.lc);
   ck(cudaGetLastError(), "filter spectra launch");
-  ck(cudaStreamSynchronize(c.st), "filter spectra");  // comps host buffer lifetime
+  ck(cudaStreamSynchronize(c.st), "filter spectra");  // host table lifetime
   c.f->spectra[key] = spec;
   return spec;
 }

@@ -578,4 +578,75 @@ void launch_find_peaks(const void* resp, int f64, int h, int w, int colmajor, do
   lc.n += 2;
 }
 
+// ------------------------------------------------------------------ filter rendering
+// Per-band rendering of a decomposed filter on the (2R+1)^2 grid centred at
+// (R, R) (freq_filter.hpp:133-184, component_value / render_component):
+//   rotation: linear interpolation of the radial profile at half-integer
+//             radii x e^{i k phi}; r <= 1e-9 keeps only k = 0
+//   scale:    linear interpolation of the angular profile (wrapped) x
+//             e^{i k omega log(r / r_min)}; 0 inside r_min
+// zero outside r_max; phi = atan2(dy, dx) with y down.  fp64 math, fp32 out,
+// layout [band][y][x] (transpose: [band][x][y]).
+namespace {
+__global__ void k_render(const double2* __restrict__ comps, const int* __restrict__ ks, int nb,
+                         int group, int n_radii, int n_angles, double r_max, double r_min,
+                         double omega, int S, int R, int transpose, float2* __restrict__ out) {
+  const size_t n = size_t(nb) * S * S;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const int ci = int(i / (size_t(S) * S));
+    const int rem = int(i % (size_t(S) * S));
+    const int y = rem / S, x = rem % S;
+    const double dx = double(x - R), dy = double(y - R);
+    const double r = sqrt(dx * dx + dy * dy);
+    const int k = ks[ci];
+    double vr = 0, vi = 0;
+    if (r <= r_max) {
+      const double th = atan2(dy, dx);
+      double ar, ai, ph;
+      bool zero = false;
+      if (group == 0) {
+        if (r <= 1e-9 && k != 0) zero = true;
+        double u = r / r_max * n_radii - 0.5;
+        u = fmin(fmax(u, 0.0), double(n_radii - 1));
+        const int j0 = int(u), j1 = min(j0 + 1, n_radii - 1);
+        const double t = u - j0;
+        const double2 c0 = comps[size_t(j0) * nb + ci], c1 = comps[size_t(j1) * nb + ci];
+        ar = (1 - t) * c0.x + t * c1.x;
+        ai = (1 - t) * c0.y + t * c1.y;
+        ph = k * th;
+      } else {
+        const double twopi = 6.283185307179586476925286766559;
+        double v = th / twopi * n_angles;
+        v -= floor(v / n_angles) * n_angles;
+        const int m0 = int(v) % n_angles, m1 = (m0 + 1) % n_angles;
+        const double t = v - floor(v);
+        if (r < r_min) zero = true;
+        const double2 c0 = comps[size_t(m0) * nb + ci], c1 = comps[size_t(m1) * nb + ci];
+        ar = (1 - t) * c0.x + t * c1.x;
+        ai = (1 - t) * c0.y + t * c1.y;
+        ph = zero ? 0.0 : k * omega * log(r / r_min);
+      }
+      if (!zero) {
+        double sn, cs;
+        sincos(ph, &sn, &cs);
+        vr = ar * cs - ai * sn;
+        vi = ar * sn + ai * cs;
+      }
+    }
+    out[size_t(ci) * S * S + (transpose ? size_t(x) * S + y : size_t(y) * S + x)] =
+        make_float2(float(vr), float(vi));
+  }
+}
+}  // namespace
+
+void launch_render(const double2* comps, const int* ks, int nb, int group, int n_radii,
+                   int n_angles, double r_max, double r_min, double omega, int S, int R,
+                   int transpose, float2* out, cudaStream_t st, LaunchCounter& lc) {
+  const int g = grid_for(size_t(nb) * S * S, 256);
+  k_render<<<g, 256, 0, st>>>(comps, ks, nb, group, n_radii, n_angles, r_max, r_min, omega, S, R,
+                              transpose, out);
+  ++lc.n;
+}
+
 }  // namespace xcb

@@ -200,3 +200,12 @@ void launch_find_peaks(const void* resp, int f64, int h, int w, int colmajor, do
                        double frac, int cap, unsigned long long* mx, unsigned* count, int* px,
                        int* py, double* pv, cudaStream_t st, LaunchCounter& lc);
 }  // namespace xcb
+
+namespace xcb {
+// Render every band of a decomposed filter on the (2R+1)^2 grid on the GPU
+// (freq_filter.hpp:133-184): comps [n_rows][nb] complex fp64, ks [nb];
+// out [nb][S][S] c64 (transposed grids when `transpose`).
+void launch_render(const double2* comps, const int* ks, int nb, int group, int n_radii,
+                   int n_angles, double r_max, double r_min, double omega, int S, int R,
+                   int transpose, float2* out, cudaStream_t st, LaunchCounter& lc);
+}  // namespace xcb
