@@ -589,13 +589,16 @@ bool use_herm() {
   return on;
 }
 
-void launch_i2(Call& c, const xcb::SigSrc& sig, const float2* T2, const double* base, void* out,
-               int out_kind, bool accumulate, bool dc) {
+xcb::Bands half_bands(Call& c, bool real_sig);
+
+// half: Hermitian half-band mode (bands = half_bands(), pair-engine I2 only)
+void launch_i2(Call& c, const xcb::SigSrc& sig, const float2* T2, const xcb::Bands& bands,
+               bool half, const double* base, void* out, int out_kind, bool accumulate, bool dc) {
   const xcb::Geo& g = c.g;
   const cplx dcv = dc ? std::conj(xcb::inner_dc_value(c.f->hf)) : cplx(0);  // engine.hpp:323
-  if (use_pair() && xcb::pair_smem(1, g.Pw, g)) {
+  if (half || (use_pair() && xcb::pair_smem(1, g.Pw, g))) {
     stage(c, "I2_rows_inv_steer", [&] {
-      xcb::launch_rows_inv_steer_pair(g, T2, c.bands, base, out_kind, out, accumulate ? 1 : 0,
+      xcb::launch_rows_inv_steer_pair(g, T2, bands, half ? 1 : 0, base, out_kind, out, accumulate ? 1 : 0,
                                       sig, dcv.real(), dcv.imag(), c.st, c.lc);
     });
   } else if (c.frow && xcb::fast_smem(1, *c.frow, g)) {
@@ -611,28 +614,43 @@ void launch_i2(Call& c, const xcb::SigSrc& sig, const float2* T2, const double* 
   }
 }
 
+// gather bands: the Hermitian half-band subset (k >= 0) when every signal is
+// real, the filter hermitian() and the pair-engine I2 applies, else c.bands
+xcb::Bands gather_bands(Call& c, const xcb::SigSrc* sig, int nsig, bool* half) {
+  *half = false;
+  if (!use_pair() || !xcb::pair_smem(1, c.g.Pw, c.g)) return c.bands;
+  bool real = true;
+  for (int i = 0; i < nsig; ++i) real = real && !sig[i].is_complex;
+  const xcb::Bands hb = half_bands(c, real);
+  if (hb.n == 0) return c.bands;
+  *half = true;
+  return hb;
+}
+
 void run_gather(Call& c, const xcb::SigSrc& sig, const double* base, void* out, int out_kind,
                 bool accumulate, bool dc) {
   const xcb::Geo& g = c.g;
+  bool half;
+  const xcb::Bands bands = gather_bands(c, &sig, 1, &half);
   float2* T1 = c.ctx->buf<float2>("T1", size_t(g.Hx2) * g.Pw);
   float2* Hh = c.ctx->buf<float2>("Hhat", size_t(g.Ph) * g.Pw);
-  float2* T2 = c.ctx->buf<float2>("T2", size_t(c.bands.n) * g.H2 * g.Pw);
+  float2* T2 = c.ctx->buf<float2>("T2", size_t(bands.n) * g.H2 * g.Pw);
   stage(c, "F1_rows_fwd", [&] { run_f1(c, sig, T1); });
   stage(c, "F2_cols_fwd", [&] { run_f2(c, T1, Hh); });
   if (use_pair() && xcb::pair_smem(0, g.Ph, g)) {
     stage(c, "I1_cols_inv_corr", [&] {
-      xcb::launch_cols_inv_corr_pair(g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);
+      xcb::launch_cols_inv_corr_pair(g, Hh, c.Fhat, c.sstride, bands, T2, c.st, c.lc);
     });
   } else if (c.fcol && xcb::fast_smem(0, *c.fcol, g)) {
     stage(c, "I1_cols_inv_corr", [&] {
-      xcb::launch_cols_inv_corr_fast(*c.fcol, g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);
+      xcb::launch_cols_inv_corr_fast(*c.fcol, g, Hh, c.Fhat, c.sstride, bands, T2, c.st, c.lc);
     });
   } else {
     stage(c, "I1_cols_inv_corr", [&] {
-      xcb::launch_cols_inv_corr(*c.pcol, g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc);
+      xcb::launch_cols_inv_corr(*c.pcol, g, Hh, c.Fhat, c.sstride, bands, T2, c.st, c.lc);
     });
   }
-  launch_i2(c, sig, T2, base, out, out_kind, accumulate, dc);
+  launch_i2(c, sig, T2, bands, half, base, out, out_kind, accumulate, dc);
 }
 
 // images per I1 launch for a gather call: the pair engine shares each staged
@@ -645,7 +663,9 @@ int gather_group(const Call& c) {
 void run_gather2(Call& c, const xcb::SigSrc* sig, double* const* base, void* const* out,
                  int out_kind, bool accumulate, bool dc) {
   const xcb::Geo& g = c.g;
-  const size_t P = size_t(g.Ph) * g.Pw, tstride = size_t(c.bands.n) * g.H2 * g.Pw;
+  bool half;
+  const xcb::Bands bands = gather_bands(c, sig, 2, &half);
+  const size_t P = size_t(g.Ph) * g.Pw, tstride = size_t(bands.n) * g.H2 * g.Pw;
   float2* T1 = c.ctx->buf<float2>("T1", size_t(g.Hx2) * g.Pw);
   float2* Hh = c.ctx->buf<float2>("Hhat2", 2 * P);
   float2* T2 = c.ctx->buf<float2>("T2g", 2 * tstride);
@@ -654,11 +674,12 @@ void run_gather2(Call& c, const xcb::SigSrc* sig, double* const* base, void* con
     stage(c, "F2_cols_fwd", [&] { run_f2(c, T1, Hh + i * P); });
   }
   stage(c, "I1_cols_inv_corr", [&] {
-    xcb::launch_cols_inv_corr_pair(g, Hh, c.Fhat, c.sstride, c.bands, T2, c.st, c.lc, 2, P,
+    xcb::launch_cols_inv_corr_pair(g, Hh, c.Fhat, c.sstride, bands, T2, c.st, c.lc, 2, P,
                                    tstride);
   });
   for (int i = 0; i < 2; ++i)
-    launch_i2(c, sig[i], T2 + i * tstride, base[i], out[i], out_kind, accumulate, dc);
+    launch_i2(c, sig[i], T2 + i * tstride, bands, half, base[i], out[i], out_kind, accumulate,
+              dc);
 }
 
 // Bands k >= 0 of the call (descending, as in c.bands) on the device, or an
@@ -676,9 +697,9 @@ xcb::Bands half_bands(Call& c, bool real_sig) {
     }
   int* db = c.ctx->buf<int>("bands_half", 2 * hk.size());
   hk.insert(hk.end(), hs.begin(), hs.end());
+  // pageable source: the copy is staged before cudaMemcpyAsync returns (as "bands")
   ck(cudaMemcpyAsync(db, hk.data(), hk.size() * sizeof(int), cudaMemcpyHostToDevice, c.st),
      "upload bands");
-  ck(cudaStreamSynchronize(c.st), "upload bands");
   const int n = int(hs.size());
   return xcb::Bands{db, db + n, n};
 }

@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
 // output r, 2 * R2 columns per thread; warps of a lane quadrant side by side).
 template <class PF, class TO>
 __global__ void __launch_bounds__(PF::T, PF::MINB)
-    k_rows_inv_steer_ilv(Geo g, const float4* __restrict__ T2, Bands bl,
+    k_rows_inv_steer_ilv(Geo g, const float4* __restrict__ T2, Bands bl, int half,
                          const double* __restrict__ base, TO* __restrict__ out, int accumulate,
                          SigSrc dcs, double dcr, double dci, float scale,
                          const float2* __restrict__ twm, const float2* __restrict__ twl) {
@@ -236,6 +236,8 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
     PF::pass1(W0, W1, TWs);
     __syncthreads();
     const int dk = bi == 0 ? 0 : bl.k[bi - 1] - bl.k[bi];
+    // Hermitian half-band mode: the k = 0 band enters with weight 1/2
+    const float w0 = half && bl.k[bi] == 0 ? 0.5f : 1.f;
     // acc = acc z^dk + conj(v)  (Horner over descending k; IFFT = conj FFT conj)
     auto horner = [&](float2 (&a)[R2]) {
       constexpr int C = 5;  // outputs per TMEM round trip
@@ -256,7 +258,7 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
         for (int i = 0; i < C; ++i) {
           const int r = r0 + i;
           if (r >= R2) break;
-          const float2 va = a[Dft<R2>::pos(r)];
+          const float2 va = c_scale(a[Dft<R2>::pos(r)], w0);
           if (bi == 0) {
             acc[i] = c_conj(va);
             continue;
@@ -297,7 +299,8 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
       const int x = j + r * PF::NB2 - g.off;
       if (j >= PF::NB2 || x < 0 || x >= g.W || y >= g.H) continue;
       const size_t i = size_t(y) * g.W + x;
-      const float2 v = c_scale(c_mul(acc, steer(klast, base[i], 1.f)), scale);
+      float2 v = c_scale(c_mul(acc, steer(klast, base[i], 1.f)), scale);
+      if (half) v = make_float2(2.f * v.x, 0.f);  // out = G_0 + 2 Re sum_{k>0} (real)
       OutOps<TO>::put(out, i, v, accumulate != 0, dc_term(dcs, i, dcr, dci));
     }
   }
@@ -896,7 +899,7 @@ void launch_rows_inv_planes_pair(const Geo& g, const float2* T2, int nbands, flo
   ++lc.n;
 }
 
-void launch_rows_inv_steer_pair(const Geo& g, const float2* T2, const Bands& b,
+void launch_rows_inv_steer_pair(const Geo& g, const float2* T2, const Bands& b, int half,
                                 const double* base, int out_kind, void* out, int accumulate,
                                 const SigSrc& dcs, double dcr, double dci, cudaStream_t st,
                                 LaunchCounter& lc) {
@@ -910,12 +913,13 @@ void launch_rows_inv_steer_pair(const Geo& g, const float2* T2, const Bands& b,
     if (out_kind == OUT_C64) {                                                              \
       set_smem(k_rows_inv_steer_ilv<PF, float2>, sm);                                       \
       k_rows_inv_steer_ilv<PF, float2><<<g.H2 / 2, PF::T, sm, st>>>(                        \
-          g, t2, b, base, static_cast<float2*>(out), accumulate, dcs, dcr, dci, scale,      \
+          g, t2, b, half, base, static_cast<float2*>(out), accumulate, dcs, dcr, dci, scale, \
           tw.mid, tw.last);                                                                 \
     } else {                                                                                \
       set_smem(k_rows_inv_steer_ilv<PF, double2>, sm);                                      \
       k_rows_inv_steer_ilv<PF, double2><<<g.H2 / 2, PF::T, sm, st>>>(                       \
-          g, t2, b, base, static_cast<double2*>(out), accumulate, dcs, dcr, dci, scale,     \
+          g, t2, b, half, base, static_cast<double2*>(out), accumulate, dcs, dcr, dci,      \
+          scale,                                                                            \
           tw.mid, tw.last);                                                                 \
     }                                                                                       \
     break;                                                                                  \

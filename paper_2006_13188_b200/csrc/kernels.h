@@ -176,7 +176,8 @@ void launch_rows_inv_planes_pair(const Geo& g, const float2* T2, int nbands, flo
                                  cudaStream_t st, LaunchCounter& lc);
 // images per I1 launch the pair engine supports for this geometry
 int pair_i1_images();
-void launch_rows_inv_steer_pair(const Geo& g, const float2* T2, const Bands& b,
+// half: Hermitian half-band mode (bands k >= 0, k = 0 weighted 1/2, out = 2 Re)
+void launch_rows_inv_steer_pair(const Geo& g, const float2* T2, const Bands& b, int half,
                                 const double* base, int out_kind, void* out, int accumulate,
                                 const SigSrc& dcs, double dcr, double dci, cudaStream_t st,
                                 LaunchCounter& lc);

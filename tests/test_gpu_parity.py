@@ -599,3 +599,31 @@ def test_scatter_pair_engine_geometry_edges(orc, h, w, periodic, real_filter):
     ref = _scatter_at(orc, ofilter(orc, F), H.astype(np.float64), T.astype(np.float64), ys, xs,
                       periodic)
     assert orc.rel_l2(got[ys, xs], ref) < TOL
+
+
+@pytest.mark.parametrize("n,batch,real_filter", [(1024, 1, True), (1024, 1, False),
+                                                  (4101, 2, True)])
+def test_gather_hermitian_half_band(orc, n, batch, real_filter):
+    """xcorr_fast of real signals with a real filter (F_{-k} = conj F_k) takes the
+    Hermitian half-band gather (I1 over bands k >= 0, I2 with the k = 0 band at
+    weight 1/2 and out = 2 Re) on the pair engine: pad 1152 (single image) and
+    pad 4320 (two images per I1 launch).  A complex filter takes the full path.
+    Against the spectral oracle at sampled pixels."""
+    from paper_2006_13188_b200 import workloads as WL
+    r = np.random.default_rng(29)
+    f = WL.angular_filter(15, 6.0, 6, r)
+    if real_filter:
+        f = f.real + 0.0j
+    F = X.decompose_rotation2(f, 15, 15, 8, 30, 32, 15.0)
+    H = r.uniform(0, 1, (batch, n, n)).astype(np.float32)
+    T = r.uniform(0, 2 * np.pi, (batch, n, n)).astype(np.float32)
+    got = X.xcorr_fast(H if batch > 1 else H[0], X.XformField.rotation(T if batch > 1 else T[0]),
+                       F).output.reshape(batch, n, n)
+    if real_filter:
+        assert np.max(np.abs(got.imag)) == 0.0
+    OF = ofilter(orc, F)
+    for b in range(batch):
+        ys = np.concatenate([r.integers(0, n, 30), [0, n - 1, 0, n - 1]])
+        xs = np.concatenate([r.integers(0, n, 30), [0, 0, n - 1, n - 1]])
+        ref = orc.spectral_oracle_at(0, H[b], ROT, T[b], OF, ys, xs)
+        assert orc.rel_l2(got[b][ys, xs], ref) < TOL
