@@ -109,3 +109,111 @@ def smooth_band_sharded(H, T: XformField, F: FreqFilter2, normalize_signal: bool
     bad = np.abs(den) < floor
     out = np.where(bad, 0.0, np.real(num / np.where(bad, 1.0, den)))
     return SmoothResult(out, 2 * len(ks), int(bad.sum()))
+
+
+# ---------------------------------------------------------------- spatial sharding
+# SURVEY 8(e) caveat 3: the angle max is nonlinear across bands, so it shards
+# by row strips instead.  G_k(p) = sum_u conj(F_k(u)) H(p + u) only reads rows
+# y - R .. y + R (R = ceil(r_max), the render radius, freq_filter.hpp:173-184),
+# and the zero padding outside the image is the same for a strip as for the
+# whole image, so a strip computed with an R-row halo is the whole-image result
+# on its own rows (up to the rounding of a different FFT length).
+
+def strip_rows(h: int, rank: int, world: int, halo: int):
+    """(a, b, lo, hi): rank's own rows [a, b) and the halo'd input rows [lo, hi)."""
+    a, b = band_ranges(h, world)[rank]
+    return a, b, max(0, a - halo), min(h, b + halo)
+
+
+def gpu_anglemax(H, F, n_angles, components):
+    """Default per-rank angle max: the product's sm_100a path."""
+    from .engine import anglemax
+    return anglemax(H, F, n_angles, components)
+
+
+def _gather_rows(a: np.ndarray, h: int, root: int, group=None, device=None):
+    """Gather every rank's own rows (balanced strips) into the full (h, ...) array
+    on the root.  Strips are padded to the largest one so one tensor collective
+    (gather; NCCL over NVLink on GPUs) moves them."""
+    import torch
+    dist = _dist()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    rows = band_ranges(h, world)
+    m = max(b - a for a, b in rows)
+    buf = np.zeros((m,) + a.shape[1:], a.dtype)
+    buf[:a.shape[0]] = a
+    t = torch.from_numpy(buf)
+    if device is not None:
+        t = t.to(device)
+    lst = [torch.empty_like(t) for _ in range(world)] if rank == root else None
+    dist.gather(t, lst, dst=root, group=group)
+    if rank != root:
+        return None
+    return np.concatenate([lst[r].cpu().numpy()[:b - a] for r, (a, b) in enumerate(rows)])
+
+
+def _local_peaks(score: np.ndarray, own0: int, own1: int, y0: int, radius: float):
+    """Local maxima (vote_filter.hpp:107-134 neighbourhood test, ties broken
+    towards the earlier pixel) of the rows [own0, own1) of a strip whose first
+    row is image row y0; the strip carries ceil(radius) rows of halo."""
+    from .engine import find_peaks
+    cand = find_peaks(score, radius, 0.0)  # threshold 0: every local maximum
+    return [(p.x, p.y + y0, p.value) for p in cand if own0 <= p.y + y0 < own1]
+
+
+def anglemax_spatial_sharded(H, F: FreqFilter2, n_angles: int = 360, components=None,
+                             compute=gpu_anglemax, root: int = 0, group=None, device=None):
+    """Row-strip-sharded angle max; the root returns the full (score, argmax)."""
+    dist = _dist()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    Hs = np.asarray(H)
+    h = Hs.shape[0]
+    if world > h:
+        raise ValueError("spatial sharding needs at least one row per rank")
+    R = int(np.ceil(F.r_max))
+    a, b, lo, hi = strip_rows(h, rank, world, R)
+    score, arg = compute(np.ascontiguousarray(Hs[lo:hi]), F, n_angles, components)
+    score = np.asarray(score)[a - lo:b - lo]
+    arg = np.asarray(arg)[a - lo:b - lo]
+    s = _gather_rows(np.ascontiguousarray(score), h, root, group, device)
+    g = _gather_rows(np.ascontiguousarray(arg), h, root, group, device)
+    return None if rank != root else (s, g)
+
+
+def match_peaks_spatial_sharded(H, F: FreqFilter2, radius: float, threshold_frac: float = 0.5,
+                                n_angles: int = 360, components=None, max_peaks: int = 1 << 16,
+                                compute=gpu_anglemax, root: int = 0, group=None,
+                                device=None):
+    """Rotation-invariant matching (angle max + find_peaks, BASELINE config 3)
+    on row strips: each rank scores its rows plus a ceil(radius)-row score halo
+    (itself computed from an R-row signal halo), keeps the local maxima of its
+    own rows, the global max comes from one all-reduce(MAX), and the root merges
+    the thresholded candidates with the reference order (value desc, then y,
+    then x; vote_filter.hpp:129-132).  The root returns the Peak list."""
+    import torch
+    from .engine import Peak
+    dist = _dist()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    Hs = np.asarray(H)
+    h = Hs.shape[0]
+    if world > h:
+        raise ValueError("spatial sharding needs at least one row per rank")
+    R = int(np.ceil(F.r_max))
+    Rn = max(1, int(np.ceil(radius)))
+    a, b, slo, shi = strip_rows(h, rank, world, Rn)        # score rows needed
+    lo, hi = max(0, slo - R), min(h, shi + R)               # signal rows needed
+    score, _ = compute(np.ascontiguousarray(Hs[lo:hi]), F, n_angles, components)
+    score = np.ascontiguousarray(np.asarray(score)[slo - lo:shi - lo])
+    own = score[a - slo:b - slo]
+    mx = torch.tensor([float(own.max()) if own.size else -np.inf], dtype=torch.float64)
+    if device is not None:
+        mx = mx.to(device)
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=group)
+    thresh = threshold_frac * float(mx.item())
+    mine = [c for c in _local_peaks(score, a, b, slo, radius) if not c[2] < thresh]
+    allc = [None] * world
+    dist.all_gather_object(allc, mine, group=group)
+    if rank != root:
+        return None
+    peaks = sorted((c for part in allc for c in part), key=lambda c: (-c[2], c[1], c[0]))
+    return [Peak(int(x), int(y), float(v)) for x, y, v in peaks[:max_peaks]]
