@@ -10,7 +10,8 @@ import os
 import threading
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libxconv_b200.so")
+# XCB_LIB_OVERRIDE: another build of the same library (tools/ab_build.py A/B timing)
+LIB_PATH = os.environ.get("XCB_LIB_OVERRIDE") or os.path.join(_PKG, "lib", "libxconv_b200.so")
 
 XC_OK, XC_EINVAL = 0, 2
 XC_ROTATION2, XC_SCALE2, XC_ROTATION3 = 0, 1, 2

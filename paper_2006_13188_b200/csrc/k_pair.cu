@@ -207,13 +207,24 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
   __syncthreads();
   tmem_fence_after_sync();
   // per output r: columns [acc.re, acc.im, z.re, z.im], z = e^{i phi}
-  const uint32_t tacc = tmem_warp_base(tbase) + uint32_t((t >> 7) * 4 * R2);
-#pragma unroll
-  for (int r = 0; r < R2; ++r) {
+  const uint32_t tacc = tmem_warp_cols(tbase, 4 * R2);
+  // the thread's R2 phases: one batch of independent loads (the TMEM stores
+  // are asm volatile, so loads interleaved with them would serialise)
+  auto in_image = [&](int r) {
     const int x = j + r * PF::NB2 - g.off;
-    tmem_st2(tacc + 4 * r + 2, x >= 0 && x < g.W && y < g.H
-                                    ? steer(1, base[size_t(y) * g.W + x], 1.f)
-                                    : make_float2(1.f, 0.f));
+    return j < PF::NB2 && x >= 0 && x < g.W && y < g.H;
+  };
+  auto load_phases = [&](double (&th)[R2]) {
+#pragma unroll
+    for (int r = 0; r < R2; ++r)
+      th[r] = in_image(r) ? __ldg(base + size_t(y) * g.W + (j + r * PF::NB2 - g.off)) : 0.0;
+  };
+  {
+    double th[R2];
+    load_phases(th);
+#pragma unroll
+    for (int r = 0; r < R2; ++r)
+      tmem_st2(tacc + 4 * r + 2, in_image(r) ? steer(1, th[r], 1.f) : make_float2(1.f, 0.f));
   }
   tmem_wait_st();
   unsigned phase = 0;
@@ -291,17 +302,29 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
   // out = scale * z^{k_last} * acc (+ conj(dc) H for the scale group)
   {
     const int klast = bl.k[bl.n - 1];
+    constexpr int C = 5;  // outputs per batch of loads
 #pragma unroll
-    for (int r = 0; r < R2; ++r) {
-      float2 acc = tmem_ld2(tacc + 4 * r);
+    for (int r0 = 0; r0 < R2; r0 += C) {
+      double th[C];
+      float az[4 * C];  // (acc, z) per output
+#pragma unroll
+      for (int i = 0; i < C; ++i)
+        th[i] = r0 + i < R2 && in_image(r0 + i)
+                    ? __ldg(base + size_t(y) * g.W + (j + (r0 + i) * PF::NB2 - g.off))
+                    : 0.0;
+      tmem_ldn<4 * C>(tacc + 4 * r0, az);
       tmem_wait_ld();
-      tmem_dep(acc);
-      const int x = j + r * PF::NB2 - g.off;
-      if (j >= PF::NB2 || x < 0 || x >= g.W || y >= g.H) continue;
-      const size_t i = size_t(y) * g.W + x;
-      float2 v = c_scale(c_mul(acc, steer(klast, base[i], 1.f)), scale);
-      if (half) v = make_float2(2.f * v.x, 0.f);  // out = G_0 + 2 Re sum_{k>0} (real)
-      OutOps<TO>::put(out, i, v, accumulate != 0, dc_term(dcs, i, dcr, dci));
+      tmem_depn<4 * C>(az);
+#pragma unroll
+      for (int i = 0; i < C; ++i) {
+        const int r = r0 + i;
+        if (r >= R2 || !in_image(r)) continue;
+        const float2 acc = make_float2(az[4 * i], az[4 * i + 1]);
+        const size_t o = size_t(y) * g.W + (j + r * PF::NB2 - g.off);
+        float2 v = c_scale(c_mul(acc, steer(klast, th[i], 1.f)), scale);
+        if (half) v = make_float2(2.f * v.x, 0.f);  // out = G_0 + 2 Re sum_{k>0} (real)
+        OutOps<TO>::put(out, o, v, accumulate != 0, dc_term(dcs, o, dcr, dci));
+      }
     }
   }
   tmem_fence_before_sync();
@@ -414,23 +437,39 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
   __syncthreads();
   tmem_fence_after_sync();
   const int gi = t & 1, j = t >> 1;
-  const uint32_t tc = tmem_warp_base(tbase) + uint32_t((t >> 7) * kThr);
+  const uint32_t tc = tmem_warp_cols(tbase, kThr);
   {
     const int ys = src_index(2 * b + gi, g.Hx, g.H, g.R, g.periodic);
     const int k0 = bl.k[0];
+    // batches of independent loads (the asm volatile TMEM stores would
+    // otherwise serialise one load latency per r)
+    constexpr int C = 4;
 #pragma unroll
-    for (int r = 0; r < R0; ++r) {
-      const int xp = j + r * PF::NB0;
-      const int xs = j < PF::NB0 ? src_index(xp, g.Wx, g.W, g.R, g.periodic) : -1;
-      float4 cm = make_float4(0.f, 0.f, 1.f, 0.f);
-      if (ys >= 0 && xs >= 0) {
-        const size_t idx = size_t(ys) * g.W + xs;
-        const double ph = base[idx];
-        const float2 cur = c_mul(sig_value(s, idx), steer(k0, ph, -1.f));  // H e^{-i k0 phi}
-        const float2 mul = steer(1, ph, -1.f);
-        cm = make_float4(cur.x, cur.y, mul.x, mul.y);
+    for (int r0 = 0; r0 < R0; r0 += C) {
+      double ph[C];
+      float2 sv[C];
+      bool ok[C];
+#pragma unroll
+      for (int i = 0; i < C; ++i) {
+        const int r = r0 + i;
+        const int xs = r < R0 && j < PF::NB0
+                           ? src_index(j + r * PF::NB0, g.Wx, g.W, g.R, g.periodic) : -1;
+        ok[i] = ys >= 0 && xs >= 0;
+        const size_t idx = ok[i] ? size_t(ys) * g.W + xs : 0;
+        ph[i] = ok[i] ? __ldg(base + idx) : 0.0;
+        sv[i] = ok[i] ? sig_value(s, idx) : make_float2(0.f, 0.f);
       }
-      tmem_st4(tc + 4 * r, cm);
+#pragma unroll
+      for (int i = 0; i < C; ++i) {
+        if (r0 + i >= R0) break;
+        float4 cm = make_float4(0.f, 0.f, 1.f, 0.f);
+        if (ok[i]) {
+          const float2 cur = c_mul(sv[i], steer(k0, ph[i], -1.f));  // H e^{-i k0 phi}
+          const float2 mul = steer(1, ph[i], -1.f);
+          cm = make_float4(cur.x, cur.y, mul.x, mul.y);
+        }
+        tmem_st4(tc + 4 * (r0 + i), cm);
+      }
     }
     tmem_wait_st();
   }
@@ -541,7 +580,7 @@ __global__ void __launch_bounds__(PF::T, 1)
   tmem_fence_before_sync();
   __syncthreads();
   tmem_fence_after_sync();
-  const uint32_t tacc = tmem_warp_base(tbase) + uint32_t((t >> 7) * kThr);
+  const uint32_t tacc = tmem_warp_cols(tbase, kThr);
   const int hx2 = g.Hx2;
   unsigned phase = 0;
   for (int bi = 0; bi < bl.n; ++bi) {

@@ -38,6 +38,15 @@ __device__ __forceinline__ uint32_t tmem_warp_base(uint32_t base) {
   return base + ((32u * ((threadIdx.x >> 5) & 3u)) << 16);
 }
 
+// this warp's kThr-column block: lane quadrant warp % 4, column block warp / 4
+// (warps of a quadrant side by side).  Broadcast from lane 0 so that ptxas
+// keeps it in a uniform register: a per-thread value costs one R2UR per TMEM
+// access.
+__device__ __forceinline__ uint32_t tmem_warp_cols(uint32_t base, int kThr) {
+  const uint32_t a = tmem_warp_base(base) + uint32_t((threadIdx.x >> 7) * kThr);
+  return __shfl_sync(0xffffffffu, a, 0);
+}
+
 // 4 consecutive columns of this thread's lane (warp-collective)
 __device__ __forceinline__ float4 tmem_ld4(uint32_t taddr) {
   uint32_t a, b, c, d;
