@@ -57,8 +57,11 @@ def lib():
         L.or_rng_next.argtypes = [C.c_void_p]
         L.or_rng_uniform.restype = C.c_double
         L.or_rng_uniform.argtypes = [C.c_void_p, C.c_double, C.c_double]
+        L.or_wigner_small_d.restype = C.c_double
         for name in ("or_random_field", "or_random_smooth_filter", "or_annular_filter",
-                     "or_random_rotation_field", "or_random_scale_field"):
+                     "or_random_rotation_field", "or_random_scale_field", "or_random_field3",
+                     "or_random_smooth_filter3", "or_random_quaternion",
+                     "or_random_rotation3_field", "or_euler_zyz", "or_sphere_grid"):
             getattr(L, name).restype = None
         _lib = L
     return _lib
@@ -459,3 +462,180 @@ def rel_l2(a, b) -> float:
     n = np.sqrt(np.sum(np.abs(a - b) ** 2))
     d = np.sqrt(np.sum(np.abs(b) ** 2))
     return float(n / d) if d > 0 else float(n)
+
+
+# ------------------------------------------------------------------ 3D
+# Volumes are numpy arrays indexed [z, y, x] (Field3, x fastest, field.hpp:67-85);
+# quaternion fields are (nz, ny, nx, 4) arrays of (w, x, y, z).
+
+@dataclass
+class Filter3:
+    """SphFilter3 (sph.hpp:130-157): coeffs (n_radii, (K+1)^2) complex, column l(l+1)+m."""
+    K: int
+    n_radii: int
+    r_max: float
+    coeffs: np.ndarray
+
+    def coeff(self, shell, l, m) -> complex:
+        return complex(self.coeffs[shell, l * (l + 1) + m])
+
+
+def _f3(F: Filter3):
+    return int(F.K), int(F.n_radii), C.c_double(F.r_max), _dp(_c128(F.coeffs).view(np.float64))
+
+
+def decompose_rotation3(vol, cx, cy, cz, K, n_radii, r_max, n_theta=0, n_phi=0) -> Filter3:
+    """sph.hpp:161-188"""
+    v = _c128(vol)
+    nz, ny, nx = v.shape
+    out = np.zeros((n_radii, (K + 1) ** 2), np.complex128)
+    _check(lib().or_decompose_rotation3(_dp(v.view(np.float64)), nx, ny, nz, C.c_double(cx),
+                                        C.c_double(cy), C.c_double(cz), int(K), int(n_radii),
+                                        C.c_double(r_max), int(n_theta), int(n_phi),
+                                        _dp(out.view(np.float64))))
+    return Filter3(int(K), int(n_radii), float(r_max), out)
+
+
+def render_sph_component(F: Filter3, l, m_radial, m_angular, nx, ny, nz, cx, cy, cz):
+    """sph.hpp:194-212"""
+    out = np.zeros((nz, ny, nx), np.complex128)
+    keep = _c128(F.coeffs)
+    _check(lib().or_render_sph_component(int(F.K), int(F.n_radii), C.c_double(F.r_max),
+                                         _dp(keep.view(np.float64)), int(l), int(m_radial),
+                                         int(m_angular), nx, ny, nz, C.c_double(cx),
+                                         C.c_double(cy), C.c_double(cz),
+                                         _dp(out.view(np.float64))))
+    return out
+
+
+def reconstruct3(F: Filter3, nx, ny, nz, cx, cy, cz, degrees=None):
+    """sph.hpp:215-221"""
+    out = np.zeros((nz, ny, nx), np.complex128)
+    keep = _c128(F.coeffs)
+    d = np.ascontiguousarray(np.asarray(degrees if degrees is not None else [], np.int32))
+    _check(lib().or_reconstruct3(int(F.K), int(F.n_radii), C.c_double(F.r_max),
+                                 _dp(keep.view(np.float64)), nx, ny, nz, C.c_double(cx),
+                                 C.c_double(cy), C.c_double(cz), _ip(d),
+                                 -1 if degrees is None else len(d), _dp(out.view(np.float64))))
+    return out
+
+
+def sph_harm(l, m, theta, phi) -> complex:
+    """sph.hpp:37-47"""
+    o = np.zeros(2)
+    _check(lib().or_sph_harm(int(l), int(m), C.c_double(theta), C.c_double(phi), _dp(o)))
+    return complex(o[0], o[1])
+
+
+def sphere_grid(n_theta, n_phi):
+    """SphereGrid (sph.hpp:52-86): (theta, weight)."""
+    th = np.zeros(n_theta)
+    w = np.zeros(n_theta)
+    lib().or_sphere_grid(int(n_theta), int(n_phi), _dp(th), _dp(w))
+    return th, w
+
+
+def euler_zyz(q):
+    """wigner.hpp:40-57"""
+    qa = _f64(q)
+    o = np.zeros(3)
+    lib().or_euler_zyz(_dp(qa), _dp(o))
+    return tuple(o)
+
+
+def wigner_d(l, q) -> np.ndarray:
+    """wigner.hpp:64-88: D[m_to + l, m_from + l]"""
+    qa = _f64(q)
+    o = np.zeros((2 * l + 1, 2 * l + 1), np.complex128) if l >= 0 else np.zeros(1, np.complex128)
+    _check(lib().or_wigner_d(int(l), _dp(qa), _dp(o.view(np.float64))))
+    return o
+
+
+def filter3_fft(sig, filt, fcx, fcy, fcz, correlate):
+    """fft.hpp:175-207"""
+    s = _c128(sig)
+    f = _c128(filt)
+    out = np.zeros(s.shape, np.complex128)
+    _check(lib().or_filter3_fft(_dp(s.view(np.float64)), s.shape[2], s.shape[1], s.shape[0],
+                                _dp(f.view(np.float64)), f.shape[2], f.shape[1], f.shape[0],
+                                int(fcx), int(fcy), int(fcz), int(bool(correlate)),
+                                _dp(out.view(np.float64))))
+    return out
+
+
+def xfast3(mode, H, quats, F: Filter3, degrees=None):
+    """engine3d.hpp:267-335 (mode 0 xcorr_fast_3d, 1 xconv_fast_3d): (output, standard_ops)."""
+    h = _c128(H)
+    q = _f64(quats)
+    nz, ny, nx = h.shape
+    if q.shape != (nz, ny, nx, 4):
+        raise ValueError("signal and transformation field dims differ")
+    out = np.zeros(h.shape, np.complex128)
+    keep = _c128(F.coeffs)
+    d = np.ascontiguousarray(np.asarray(degrees if degrees is not None else [], np.int32))
+    ops = C.c_longlong(0)
+    _check(lib().or_xfast3(int(mode), _dp(h.view(np.float64)), nx, ny, nz, _dp(q), int(F.K),
+                           int(F.n_radii), C.c_double(F.r_max), _dp(keep.view(np.float64)),
+                           _ip(d), len(d), _dp(out.view(np.float64)), C.byref(ops)))
+    return out, ops.value
+
+
+def exact3(mode, H, quats, F: Filter3):
+    """test_engine3d.cpp:37-67: rotated band-limited reconstruction, spatial loops."""
+    h = _c128(H)
+    q = _f64(quats)
+    nz, ny, nx = h.shape
+    out = np.zeros(h.shape, np.complex128)
+    keep = _c128(F.coeffs)
+    _check(lib().or_exact3(int(mode), _dp(h.view(np.float64)), nx, ny, nz, _dp(q), int(F.K),
+                           int(F.n_radii), C.c_double(F.r_max), _dp(keep.view(np.float64)),
+                           _dp(out.view(np.float64))))
+    return out
+
+
+def _random_field3(self, nx, ny, nz, complex_valued=False):
+    out = np.zeros((nz, ny, nx), np.complex128)
+    lib().or_random_field3(self._h, nx, ny, nz, int(complex_valued), _dp(out.view(np.float64)))
+    return out
+
+
+def _random_smooth_filter3(self, radius, n_bumps=6, envelope_frac=0.4):
+    S = 2 * radius + 1
+    out = np.zeros((S, S, S), np.complex128)
+    lib().or_random_smooth_filter3(self._h, int(radius), int(n_bumps), C.c_double(envelope_frac),
+                                   _dp(out.view(np.float64)))
+    return out
+
+
+def _random_quaternion(self):
+    out = np.zeros(4)
+    lib().or_random_quaternion(self._h, _dp(out))
+    return out
+
+
+def _random_rotation3_field(self, nx, ny, nz):
+    out = np.zeros((nz, ny, nx, 4))
+    lib().or_random_rotation3_field(self._h, nx * ny * nz, _dp(out))
+    return out
+
+
+Rng.random_field3 = _random_field3
+Rng.random_smooth_filter3 = _random_smooth_filter3
+Rng.random_quaternion = _random_quaternion
+Rng.random_rotation3_field = _random_rotation3_field
+
+
+def quat_mul(a, b):
+    """Hamilton product (Eigen Quaternion operator*)."""
+    aw, ax, ay, az = a
+    bw, bx, by, bz = b
+    return np.array([aw * bw - ax * bx - ay * by - az * bz, aw * bx + ax * bw + ay * bz - az * by,
+                     aw * by - ax * bz + ay * bw + az * bx, aw * bz + ax * by - ay * bx + az * bw])
+
+
+def quat_matrix(q):
+    """Eigen Quaternion::toRotationMatrix."""
+    w, x, y, z = q
+    return np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                     [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                     [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])

@@ -1342,3 +1342,6 @@ void or_random_scale_field(void* rngp, int w, int h, double lo, double hi, doubl
 }
 
 }  // extern "C"
+
+// 3D rotation pipeline
+#include "xconv_oracle3d.inc"
