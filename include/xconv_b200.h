@@ -23,6 +23,14 @@
  *                                     filter)
  *   xc_render_component / xc_reconstruct / xc_inner_dc_value
  *                                  <- freq_filter.hpp:165-235 (host)
+ *   3D rotation pipeline:
+ *   xc_run3(mode = XC_CORRELATION) <- xcorr_fast_3d engine3d.hpp:270-302
+ *   xc_run3(mode = XC_CONVOLUTION) <- xconv_fast_3d engine3d.hpp:306-335
+ *   xc_filter3_create              <- SphFilter3   sph.hpp:130-157
+ *   xc_decompose_rotation3         <- decompose_rotation3 sph.hpp:161-188 (host)
+ *   xc_render_sph_component / xc_reconstruct3 / xc_sph_harm
+ *                                  <- sph.hpp:37-47, 194-221 (host)
+ *   xc_wigner_d                    <- wigner_d     wigner.hpp:64-88 (host)
  *
  * Conventions
  *   - Status codes: XC_OK; XC_EINVAL for the reference's std::invalid_argument
@@ -197,6 +205,38 @@ int xc_detect_pattern(xc_context ctx, const xc_image_desc* d, const void* image,
                       const double* vote_weights, int radius, double eps, int K, int n_radii,
                       int n_angles, void* response, int* peak_x, int* peak_y, double* peak_v,
                       int max_peaks, int* n_peaks, xc_stats* stats);
+
+/* ------------------------------------------------------------------ 3D rotation
+ * Volumes are x fastest: element (x, y, z) at (z*ny + y)*nx + x (Field3,
+ * field.hpp:67-85).  Quaternion fields are 4 doubles (w, x, y, z) per voxel;
+ * non-unit quaternions are renormalized (XformField::rotation3d).  SphFilter3
+ * coefficients are column-major like the reference's Eigen CGrid (n_radii x
+ * (K+1)^2, element (shell, l(l+1)+m) at shell + (l(l+1)+m)*n_radii). */
+typedef struct xc_filter3_s* xc_filter3;
+
+int xc_filter3_create(int K, int n_radii, double r_max, const double* coeffs, xc_filter3* out);
+void xc_filter3_destroy(xc_filter3 f);
+/* sph.hpp:161-188; coeffs_out: n_radii * (K+1)^2 complex, column-major.
+ * n_theta / n_phi = 0 select 2(K+1). */
+int xc_decompose_rotation3(const double* volume, int nx, int ny, int nz, double cx, double cy,
+                           double cz, int K, int n_radii, double r_max, int n_theta, int n_phi,
+                           double* coeffs_out);
+/* f_l^{m_radial}(r) Y_l^{m_angular} on an nx*ny*nz grid (sph.hpp:194-212) */
+int xc_render_sph_component(xc_filter3 f, int l, int m_radial, int m_angular, int nx, int ny,
+                            int nz, double cx, double cy, double cz, double* out);
+/* sph.hpp:215-221; degrees == NULL (or ndeg < 0) keeps every degree */
+int xc_reconstruct3(xc_filter3 f, int nx, int ny, int nz, double cx, double cy, double cz,
+                    const int* degrees, int ndeg, double* out);
+int xc_sph_harm(int l, int m, double theta, double phi, double* out2);
+/* D[(m_to + l)(2l+1) + (m_from + l)], (2l+1)^2 complex (wigner.hpp:64-88) */
+int xc_wigner_d(int l, const double* quat, double* out);
+/* xcorr_fast_3d / xconv_fast_3d: signal (signal_dtype XC_F32 / XC_F64 /
+ * XC_C64 / XC_C128), quats and out (complex128) in `memory`; degrees selects a
+ * subset of l (XConvPlan::components over degrees, engine3d.hpp:11-16);
+ * stats->standard_ops = sum over the kept degrees of (2l+1)^2. */
+int xc_run3(xc_context ctx, xc_filter3 f, int mode, int nx, int ny, int nz, const void* signal,
+            int signal_dtype, const double* quats, const int* degrees, int ndeg, int memory,
+            double* out, xc_stats* stats);
 
 #ifdef __cplusplus
 }

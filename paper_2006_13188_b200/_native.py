@@ -45,7 +45,8 @@ EXPORTS = [
     "xc_render_component", "xc_reconstruct", "xc_inner_dc_value", "xc_run", "xc_smooth",
     "xc_anglemax", "xc_find_peaks", "xc_profile_enable", "xc_profile_reset", "xc_profile_get",
     "xc_build_vote_filter", "xc_build_optimal_filter", "xc_detect_pattern",
-    "xc_find_peaks_device",
+    "xc_find_peaks_device", "xc_filter3_create", "xc_filter3_destroy", "xc_decompose_rotation3",
+    "xc_render_sph_component", "xc_reconstruct3", "xc_sph_harm", "xc_wigner_d", "xc_run3",
 ]
 
 _lib = None
@@ -96,6 +97,15 @@ def lib():
         L.xc_detect_pattern.argtypes = [vp, C.POINTER(ImageDesc), vp, dp, i, d, i, i, i, vp, ip,
                                         ip, dp, i, ip, C.POINTER(Stats)]
         L.xc_find_peaks_device.argtypes = [vp, vp, i, i, i, i, d, d, ip, ip, dp, i, ip]
+        L.xc_filter3_create.argtypes = [i, i, d, dp, C.POINTER(vp)]
+        L.xc_filter3_destroy.argtypes = [vp]
+        L.xc_filter3_destroy.restype = None
+        L.xc_decompose_rotation3.argtypes = [dp, i, i, i, d, d, d, i, i, d, i, i, dp]
+        L.xc_render_sph_component.argtypes = [vp, i, i, i, i, i, i, d, d, d, dp]
+        L.xc_reconstruct3.argtypes = [vp, i, i, i, d, d, d, ip, i, dp]
+        L.xc_sph_harm.argtypes = [i, i, d, d, dp]
+        L.xc_wigner_d.argtypes = [i, dp, dp]
+        L.xc_run3.argtypes = [vp, vp, i, i, i, i, vp, i, vp, ip, i, i, vp, C.POINTER(Stats)]
         L.xc_profile_enable.argtypes = [vp, i]
         L.xc_profile_reset.argtypes = [vp]
         L.xc_profile_get.argtypes = [vp, i, C.c_char_p, i, dp, C.POINTER(C.c_longlong)]

@@ -31,6 +31,8 @@
 #include "fft_plan.h"
 #include "host_filter.h"
 #include "kernels.h"
+#include "host_sph.h"
+#include "kernels3d.h"
 
 namespace {
 
@@ -1416,6 +1418,268 @@ int xc_detect_pattern(xc_context ctx, const xc_image_desc* d, const void* image,
       stats->gpu_launches += lc.n;
       stats->seconds_total =
           std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    }
+  });
+}
+
+}  // extern "C"
+
+// ================================================================ 3D rotation
+// xcorr_fast_3d / xconv_fast_3d (engine3d.hpp:270-335) on the
+// k_3d.cu stages.  The per-band spectra of a filter are built once per
+// (device, pad) and cached; bands are (l, m, m') in the reference's loop order.
+
+struct xc_filter3_s {
+  xcb::HostFilter3 hf;
+  std::map<std::tuple<int, int, int, int>, float2*> spectra;  // (dev, px, py, pz)
+  ~xc_filter3_s() {
+    for (auto& kv : spectra) {
+      cudaSetDevice(std::get<0>(kv.first));
+      cudaFree(kv.second);
+    }
+  }
+};
+
+namespace {
+
+int band_offset(int l) {  // bands of degrees < l: sum (2l'+1)^2
+  int n = 0;
+  for (int d = 0; d < l; ++d) n += (2 * d + 1) * (2 * d + 1);
+  return n;
+}
+
+// every band of the filter rendered on (2R+1)^3, x-, y-, z-transformed
+float2* filter3_spectra(xc_context ctx, xc_filter3 f, const xcb::Geo3& g, const xcb::FftPlan& pxp,
+                        const xcb::FftPlan& pyp, const xcb::FftPlan& pzp, cudaStream_t st,
+                        xcb::LaunchCounter& lc) {
+  const auto key = std::make_tuple(ctx->device, g.px, g.py, g.pz);
+  auto it = f->spectra.find(key);
+  if (it != f->spectra.end()) return it->second;
+  const xcb::HostFilter3& hf = f->hf;
+  const int S = 2 * g.R + 1, nb = band_offset(hf.K + 1);
+  const size_t S3 = size_t(S) * S * S, P = size_t(g.px) * g.py * g.pz;
+  std::vector<float2> comps(S3 * nb);
+  std::vector<cplx> tmp(S3);
+  int b = 0;
+  for (int l = 0; l <= hf.K; ++l)
+    for (int m = -l; m <= l; ++m)
+      for (int mp = -l; mp <= l; ++mp, ++b) {  // engine3d.hpp:286-289
+        xcb::render_sph_component(hf, l, m, mp, S, S, S, g.R, g.R, g.R, tmp.data());
+        for (size_t i = 0; i < S3; ++i)
+          comps[b * S3 + i] = make_float2(float(tmp[i].real()), float(tmp[i].imag()));
+      }
+  float2* dcomps = ctx->buf<float2>("f3_comps", comps.size());
+  ck(cudaMemcpyAsync(dcomps, comps.data(), comps.size() * sizeof(float2), cudaMemcpyHostToDevice,
+                     st),
+     "upload 3D filter bands");
+  float2* spec = nullptr;
+  ck(cudaMalloc(&spec, P * nb * sizeof(float2)), "cudaMalloc 3D spectra");
+  xcb::launch3_x_filter(pxp, g, dcomps, nb, spec, P, st, lc);
+  xcb::launch3_pass(pyp, g, 1, spec, P, nb, st, lc);
+  xcb::launch3_pass(pzp, g, 2, spec, P, nb, st, lc);
+  ck(cudaGetLastError(), "3D filter spectra launch");
+  ck(cudaStreamSynchronize(st), "3D filter spectra");  // host staging lifetime
+  f->spectra[key] = spec;
+  return spec;
+}
+
+xcb::Band3 make_band3(int l, int m, int mp) {
+  // D^l_{m' m}: wigner_d_entry(l, mp, m, ...) (engine3d.hpp:296, 320)
+  const xcb::SmallD d = xcb::small_d_coeffs(l, mp, m);
+  xcb::Band3 b{};
+  b.l = l;
+  b.m = m;
+  b.mp = mp;
+  b.n = d.n;
+  b.pc_end = d.pc_end;
+  b.ps0 = d.ps0;
+  for (int k = 0; k <= d.n; ++k) b.c[k] = d.c[k];
+  return b;
+}
+
+}  // namespace
+
+extern "C" {
+
+int xc_filter3_create(int K, int n_radii, double r_max, const double* coeffs, xc_filter3* out) {
+  return guarded(nullptr, [&] {
+    if (!out || !coeffs) throw std::invalid_argument("null argument");
+    if (K < 0 || K > 16) throw std::invalid_argument("band limit must be in [0, 16]");
+    if (n_radii < 1) throw std::invalid_argument("n_radii must be >= 1");
+    if (!(r_max > 0)) throw std::invalid_argument("r_max must be > 0");
+    auto f = std::make_unique<xc_filter3_s>();
+    xcb::HostFilter3& h = f->hf;
+    h.K = K;
+    h.n_radii = n_radii;
+    h.r_max = r_max;
+    const int nc = h.ncol();
+    h.coeffs.resize(size_t(n_radii) * nc);
+    for (int c = 0; c < nc; ++c)
+      for (int r = 0; r < n_radii; ++r)
+        h.coeffs[size_t(r) * nc + c] =
+            cplx(coeffs[2 * (size_t(c) * n_radii + r)], coeffs[2 * (size_t(c) * n_radii + r) + 1]);
+    *out = f.release();
+  });
+}
+
+void xc_filter3_destroy(xc_filter3 f) { delete f; }
+
+int xc_decompose_rotation3(const double* volume, int nx, int ny, int nz, double cx, double cy,
+                           double cz, int K, int n_radii, double r_max, int n_theta, int n_phi,
+                           double* coeffs_out) {
+  return guarded(nullptr, [&] {
+    if (!volume || !coeffs_out) throw std::invalid_argument("null argument");
+    auto f = xcb::decompose_rotation3(reinterpret_cast<const cplx*>(volume), nx, ny, nz, cx, cy,
+                                      cz, K, n_radii, r_max, n_theta, n_phi);
+    const int nc = f.ncol();
+    for (int c = 0; c < nc; ++c)
+      for (int r = 0; r < n_radii; ++r) {
+        coeffs_out[2 * (size_t(c) * n_radii + r)] = f.coeffs[size_t(r) * nc + c].real();
+        coeffs_out[2 * (size_t(c) * n_radii + r) + 1] = f.coeffs[size_t(r) * nc + c].imag();
+      }
+  });
+}
+
+int xc_render_sph_component(xc_filter3 f, int l, int m_radial, int m_angular, int nx, int ny,
+                            int nz, double cx, double cy, double cz, double* out) {
+  return guarded(nullptr, [&] {
+    xcb::render_sph_component(f->hf, l, m_radial, m_angular, nx, ny, nz, cx, cy, cz,
+                              reinterpret_cast<cplx*>(out));
+  });
+}
+
+int xc_reconstruct3(xc_filter3 f, int nx, int ny, int nz, double cx, double cy, double cz,
+                    const int* degrees, int ndeg, double* out) {
+  return guarded(nullptr, [&] {
+    xcb::reconstruct3(f->hf, nx, ny, nz, cx, cy, cz, ndeg >= 0 ? degrees : nullptr, ndeg,
+                      reinterpret_cast<cplx*>(out));
+  });
+}
+
+int xc_sph_harm(int l, int m, double theta, double phi, double* out2) {
+  return guarded(nullptr, [&] {
+    const cplx v = xcb::sph_harm(l, m, theta, phi);
+    out2[0] = v.real();
+    out2[1] = v.imag();
+  });
+}
+
+int xc_wigner_d(int l, const double* quat, double* out) {
+  return guarded(nullptr, [&] { xcb::wigner_d(l, quat, reinterpret_cast<cplx*>(out)); });
+}
+
+int xc_run3(xc_context ctx, xc_filter3 f, int mode, int nx, int ny, int nz, const void* signal,
+            int signal_dtype, const double* quats, const int* degrees, int ndeg, int memory,
+            double* out, xc_stats* stats) {
+  return guarded(ctx, [&] {
+    const auto t_start = std::chrono::steady_clock::now();
+    if (!ctx || !f || !signal || !quats || !out) throw std::invalid_argument("null argument");
+    if (mode != XC_CORRELATION && mode != XC_CONVOLUTION) throw std::invalid_argument("unknown mode");
+    if (nx < 1 || ny < 1 || nz < 1) throw std::invalid_argument("volume dims must be positive");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const xcb::HostFilter3& hf = f->hf;
+    // plan_degrees (engine3d.hpp:11-16 over engine.hpp:51-58)
+    std::vector<int> ls;
+    if (degrees && ndeg > 0) {
+      for (int i = 0; i < ndeg; ++i) {
+        if (degrees[i] < 0 || degrees[i] > hf.K)
+          throw std::invalid_argument("plan retains a component the filter lacks");
+        ls.push_back(degrees[i]);
+      }
+    } else {
+      for (int l = 0; l <= hf.K; ++l) ls.push_back(l);
+    }
+    std::vector<xcb::Band3> bands;
+    std::vector<int> sidx;
+    for (int l : ls)
+      for (int m = -l; m <= l; ++m)
+        for (int mp = -l; mp <= l; ++mp) {
+          bands.push_back(make_band3(l, m, mp));
+          sidx.push_back(band_offset(l) + (m + l) * (2 * l + 1) + (mp + l));
+        }
+    const int nb = int(bands.size());
+    xcb::Geo3 g{nx, ny, nz, 0, 0, 0, hf.render_radius()};
+    const int R = g.R;
+    g.px = pick_pad(std::max(nx + R, 2 * R + 1));
+    g.py = pick_pad(std::max(ny + R, 2 * R + 1));
+    g.pz = pick_pad(std::max(nz + R, 2 * R + 1));
+    if (g.px < 0 || g.py < 0 || g.pz < 0) throw std::invalid_argument("volume too large for the FFT planner");
+    const xcb::FftPlan& pxp = ctx->plan(g.px);
+    const xcb::FftPlan& pyp = ctx->plan(g.py);
+    const xcb::FftPlan& pzp = ctx->plan(g.pz);
+    cudaStream_t st = ctx->stream;
+    xcb::LaunchCounter lc;
+    const size_t N = size_t(nx) * ny * nz, P = size_t(g.px) * g.py * g.pz;
+    float2* spec = filter3_spectra(ctx, f, g, pxp, pyp, pzp, st, lc);
+    ctx->release_events();
+    cudaEvent_t e0 = ctx->event(true), e1 = ctx->event(true);
+    ck(cudaEventRecord(e0, st), "event");
+    // inputs: signal -> complex fp32, quaternions -> per-voxel Euler data
+    const size_t ss = dtype_size(signal_dtype);
+    const void* dsig_raw = signal;
+    const double* dq = quats;
+    if (memory == XC_HOST) {
+      void* b = ctx->buf<char>("v3_sig_raw", N * ss);
+      ck(cudaMemcpyAsync(b, signal, N * ss, cudaMemcpyHostToDevice, st), "H2D signal");
+      dsig_raw = b;
+      double* q = ctx->buf<double>("v3_quats", 4 * N);
+      ck(cudaMemcpyAsync(q, quats, 4 * N * sizeof(double), cudaMemcpyHostToDevice, st), "H2D quats");
+      dq = q;
+    }
+    float2* dsig = ctx->buf<float2>("v3_sig", N);
+    xcb::launch3_signal(dsig_raw, signal_dtype, N, dsig, st, lc);
+    double4* eul = ctx->buf<double4>("v3_euler", N);
+    xcb::launch3_euler(dq, N, eul, st, lc);
+    xcb::Band3* dbands = ctx->buf<xcb::Band3>("v3_bands", size_t(nb));
+    int* dsidx = ctx->buf<int>("v3_sidx", size_t(nb));
+    ck(cudaMemcpyAsync(dbands, bands.data(), nb * sizeof(xcb::Band3), cudaMemcpyHostToDevice, st),
+       "upload bands");
+    ck(cudaMemcpyAsync(dsidx, sidx.data(), nb * sizeof(int), cudaMemcpyHostToDevice, st),
+       "upload band spectra");
+    double2* dout = memory == XC_DEVICE ? reinterpret_cast<double2*>(out)
+                                        : ctx->buf<double2>("v3_out", N);
+    // bands per chunk: work volumes within ~4 GB
+    const int cb = int(std::max<size_t>(1, std::min<size_t>(nb, (size_t(4) << 30) / (P * 8))));
+    float2* work = ctx->buf<float2>("v3_work", P * cb);
+    if (mode == XC_CORRELATION) {
+      float2* Hh = ctx->buf<float2>("v3_Hhat", P);
+      xcb::launch3_x_signal(pxp, g, dsig, eul, dbands, 1, 0, Hh, P, st, lc);
+      xcb::launch3_pass(pyp, g, 1, Hh, P, 1, st, lc);
+      xcb::launch3_pass(pzp, g, 2, Hh, P, 1, st, lc);
+      for (int b0 = 0; b0 < nb; b0 += cb) {
+        const int n = std::min(cb, nb - b0);
+        xcb::launch3_z_load(pzp, g, Hh, spec, dsidx + b0, n, P, 0, work, st, lc);
+        xcb::launch3_pass(pyp, g, 1, work, P, n, st, lc);
+        xcb::launch3_x_steer(pxp, g, work, P, n, eul, dbands + b0, 0, b0 > 0, dout, st, lc);
+      }
+    } else {
+      float2* sum = ctx->buf<float2>("v3_sum", P);
+      ck(cudaMemsetAsync(sum, 0, P * sizeof(float2), st), "memset");
+      for (int b0 = 0; b0 < nb; b0 += cb) {
+        const int n = std::min(cb, nb - b0);
+        xcb::launch3_x_signal(pxp, g, dsig, eul, dbands + b0, n, 1, work, P, st, lc);
+        xcb::launch3_pass(pyp, g, 1, work, P, n, st, lc);
+        xcb::launch3_z_mac(pzp, g, work, P, n, spec, dsidx + b0, sum, st, lc);
+      }
+      xcb::launch3_z_load(pzp, g, sum, nullptr, nullptr, 1, P, 1, work, st, lc);
+      xcb::launch3_pass(pyp, g, 1, work, P, 1, st, lc);
+      xcb::launch3_x_steer(pxp, g, work, P, 1, eul, dbands, 1, 0, dout, st, lc);
+    }
+    ck(cudaGetLastError(), "3D kernel launch");
+    ck(cudaEventRecord(e1, st), "event");
+    if (memory == XC_HOST)
+      ck(cudaMemcpyAsync(out, dout, N * sizeof(double2), cudaMemcpyDeviceToHost, st), "D2H out");
+    ck(cudaStreamSynchronize(st), "xc_run3");
+    if (stats) {
+      std::memset(stats, 0, sizeof(*stats));
+      stats->standard_ops = nb;  // engine3d.hpp:299, 331
+      stats->pad_h = g.py;
+      stats->pad_w = g.px;
+      stats->seconds_fft = event_seconds(e0, e1);
+      stats->seconds_total =
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+      stats->gpu_launches = lc.n;
     }
   });
 }

@@ -1,0 +1,52 @@
+// Device stages of the 3D rotation pipeline (k_3d.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+
+namespace xcb {
+
+struct Geo3 {
+  int nx, ny, nz;  // signal extent (x fastest)
+  int px, py, pz;  // transform size
+  int R;           // render radius ceil(r_max)
+};
+
+// One band (l, m, m'): the Wigner entry D^l_{m' m} = e^{-i(m' alpha + m gamma)}
+// d^l_{m' m}(beta), d from host_sph.h SmallD (Horner coefficients c[0..n]).
+struct Band3 {
+  int l, m, mp;
+  int n, pc_end, ps0;
+  double c[33];
+};
+
+// signal (XC_F32 / XC_F64 / XC_C64 / XC_C128) -> complex fp32
+void launch3_signal(const void* src, int dtype, size_t n, float2* dst, cudaStream_t st,
+                    LaunchCounter& lc);
+void launch3_euler(const double* quats, size_t n, double4* eul, cudaStream_t st,
+                   LaunchCounter& lc);
+// in-place forward line transforms along axis (0 x, 1 y, 2 z) of nvol volumes
+void launch3_pass(const FftPlan& pl, const Geo3& g, int axis, float2* buf, size_t vstride,
+                  int nvol, cudaStream_t st, LaunchCounter& lc);
+// x-pass of the (zero-padded) signal, times D_b when premul, for nb bands
+void launch3_x_signal(const FftPlan& pl, const Geo3& g, const float2* sig, const double4* eul,
+                      const Band3* bands, int nb, int premul, float2* work, size_t vstride,
+                      cudaStream_t st, LaunchCounter& lc);
+// x-pass of nb rendered filter bands ((2R+1)^3 each), wrapped to the origin
+void launch3_x_filter(const FftPlan& pl, const Geo3& g, const float2* comps, int nb,
+                      float2* spec, size_t vstride, cudaStream_t st, LaunchCounter& lc);
+// z-pass loading conj(H^) V^_sidx[b] (mode 0, nb bands) or conj(H^) (mode 1)
+void launch3_z_load(const FftPlan& pl, const Geo3& g, const float2* Hh, const float2* spec,
+                    const int* sidx, int nb, size_t vstride, int mode, float2* work,
+                    cudaStream_t st, LaunchCounter& lc);
+// x-pass finishing the inverse, crop, conj(D_b) steering summed over nb bands
+// (mode 0) or plain (mode 1); out (+)= result, complex128
+void launch3_x_steer(const FftPlan& pl, const Geo3& g, const float2* work, size_t vstride,
+                     int nb, const double4* eul, const Band3* bands, int mode, int accumulate,
+                     double2* out, cudaStream_t st, LaunchCounter& lc);
+// z-pass of nb scatter bands, sum += FFT3(H D_b) V^_sidx[b]
+void launch3_z_mac(const FftPlan& pl, const Geo3& g, const float2* work, size_t vstride, int nb,
+                   const float2* spec, const int* sidx, float2* sum, cudaStream_t st,
+                   LaunchCounter& lc);
+
+}  // namespace xcb
