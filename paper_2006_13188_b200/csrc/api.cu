@@ -762,6 +762,72 @@ void run_scatter(Call& c, const xcb::SigSrc& sig, const double* base, void* out,
   });
 }
 
+// XCB_DUAL=1 enables the interleaved I1 + I2 launches of gather batches.
+// Measured on config 5 it is not faster (2 images: 155.1k against 156.1k
+// Mpixel.bands/s; 16 images: 143.0k against 144.1k): with one CTA per SM an
+// SM runs either an I1 or an I2 CTA, and both are limited per SM (barriers,
+// issue), not by a resource the other kernel leaves idle.  Off by default.
+bool use_dual() {
+  static const bool on = [] {
+    const char* e = std::getenv("XCB_DUAL");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+// Gather over a batch, software-pipelined: while image i's kernels are issued,
+// one launch runs I1 of image i and I2 of image i-1 with interleaved CTAs
+// (k_pair.cu k_dual_ilv), so the HBM-heavy column transforms and the
+// FP32-bound row transforms share the SMs.  Two Hhat / T2 / base slots.
+void run_gather_dual(Call& c, HostPipe& hp, const void* signal, const void* param, void* out,
+                     size_t os, int out_kind, bool accumulate, bool dc) {
+  const xcb::Geo& g = c.g;
+  const int B = c.d.batch;
+  const cplx dcv = dc ? std::conj(xcb::inner_dc_value(c.f->hf)) : cplx(0);  // engine.hpp:323
+  bool half = false;
+  xcb::Bands bands{};
+  float2* T1 = c.ctx->buf<float2>("T1", size_t(g.Hx2) * g.Pw);
+  float2* Hh[2] = {c.ctx->buf<float2>("Hhat_d0", size_t(g.Ph) * g.Pw),
+                   c.ctx->buf<float2>("Hhat_d1", size_t(g.Ph) * g.Pw)};
+  float2* T2[2] = {nullptr, nullptr};
+  double* base[2] = {nullptr, nullptr};
+  xcb::SigSrc sg[2]{};
+  for (int img = 0; img <= B; ++img) {
+    const int s = img & 1, p = s ^ 1;
+    if (img < B) {
+      hp.h2d(signal, param, img + 1);
+      Staged st = hp.inputs(signal, param, img);
+      prep(c, st, false, &base[s], nullptr, s);
+      if (img == 0) {
+        bands = gather_bands(c, &st.sig, 1, &half);
+        for (int i = 0; i < 2; ++i)
+          T2[i] = c.ctx->buf<float2>("T2_d" + std::to_string(i), size_t(bands.n) * g.H2 * g.Pw);
+      }
+      sg[s] = st.sig;
+      stage(c, "F1_rows_fwd", [&] { run_f1(c, sg[s], T1); });
+      stage(c, "F2_cols_fwd", [&] { run_f2(c, T1, Hh[s]); });
+    }
+    if (img == 0) {
+      stage(c, "I1_cols_inv_corr", [&] {
+        xcb::launch_cols_inv_corr_pair(g, Hh[0], c.Fhat, c.sstride, bands, T2[0], c.st, c.lc);
+      });
+      continue;
+    }
+    void* dout = hp.out_buffer(out, img - 1, os);
+    if (img < B) {
+      stage(c, "I1_I2_dual", [&] {
+        xcb::launch_dual_pair(g, Hh[s], c.Fhat, c.sstride, bands, T2[s], T2[p], half ? 1 : 0,
+                              base[p], out_kind, dout, accumulate ? 1 : 0, sg[p], dcv.real(),
+                              dcv.imag(), c.st, c.lc);
+      });
+    } else {
+      launch_i2(c, sg[p], T2[p], bands, half, base[p], dout, out_kind, accumulate, dc);
+    }
+    ck(cudaGetLastError(), "kernel launch");
+    hp.done(out, img - 1, dout, os);
+  }
+}
+
 void fill_stats(Call& c, xc_stats* st, double gpu_s, double total_s, long long ops) {
   if (!st) return;
   std::memset(st, 0, sizeof(*st));
@@ -958,7 +1024,10 @@ int xc_run(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d, const 
     const int G = mode == XC_CORRELATION ? gather_group(c) : 1;
     for (int i = 0; i < G; ++i) hp.h2d(signal, param, i);
     ck(cudaEventRecord(e0, c.st), "event");
-    for (int img = 0; img < d->batch;) {
+    const bool dual = mode == XC_CORRELATION && G == 1 && d->batch >= 2 && use_pair() &&
+                      use_dual() && xcb::dual_pair_ok(c.g);
+    if (dual) run_gather_dual(c, hp, signal, param, out, os, out_kind, accumulate, dc);
+    for (int img = dual ? d->batch : 0; img < d->batch;) {
       const int n = std::min(G, d->batch - img);
       for (int i = 0; i < n; ++i) hp.h2d(signal, param, img + G + i);  // next group
       if (n == 2) {

@@ -47,11 +47,12 @@ __device__ __forceinline__ void park_last_tw(const float2* __restrict__ twf, uin
 // images (the filter spectrum is image-independent, so its HBM read is shared).
 // Per (band, image): two barriers (after pass 0, after pass 1).
 template <class PF, int NI>
-__global__ void __launch_bounds__(PF::T, PF::MINB)
-    k_cols_inv_corr_ilv(Geo g, const float4* __restrict__ Hh, size_t hstride4,
-                        const float4* __restrict__ Fh, size_t sstride4, Bands bl,
-                        float2* __restrict__ T2, size_t tstride,
-                        const float2* __restrict__ twm, const float2* __restrict__ twf) {
+__device__ __forceinline__ void i1_body(int c, const Geo& g, const float4* __restrict__ Hh,
+                                        size_t hstride4, const float4* __restrict__ Fh,
+                                        size_t sstride4, const Bands& bl,
+                                        float2* __restrict__ T2, size_t tstride,
+                                        const float2* __restrict__ twm,
+                                        const float2* __restrict__ twf) {
   constexpr int L = PF::L;  // = Ph
   // TMEM per thread: conj(H^) (2 R0 columns per image), then the pass-2
   // twiddle row; warps of a lane quadrant side by side (up to 5 of 18)
@@ -66,7 +67,7 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
   const float2* ST = reinterpret_cast<const float2*>(ST4);
   float2* W0 = reinterpret_cast<float2*>(W04);
   float2* W1 = reinterpret_cast<float2*>(W14);
-  const int c = blockIdx.x, t = threadIdx.x;
+  const int t = threadIdx.x;
   const size_t plane = size_t(g.H2) * g.Pw;  // float2 per T2 band plane
   constexpr unsigned kBytes = unsigned(L * sizeof(float4));
   auto fsrc = [&](int bi) { return Fh + size_t(bl.spec[bi]) * sstride4 + size_t(c) * L; };
@@ -162,16 +163,27 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
   }
 }
 
+template <class PF, int NI>
+__global__ void __launch_bounds__(PF::T, PF::MINB)
+    k_cols_inv_corr_ilv(Geo g, const float4* __restrict__ Hh, size_t hstride4,
+                        const float4* __restrict__ Fh, size_t sstride4, Bands bl,
+                        float2* __restrict__ T2, size_t tstride,
+                        const float2* __restrict__ twm, const float2* __restrict__ twf) {
+  i1_body<PF, NI>(blockIdx.x, g, Hh, hstride4, Fh, sstride4, bl, T2, tstride, twm, twf);
+}
+
 // ------------------------------------------------------------------ I2 (interleaved)
 // The thread's steering phasors z = e^{i phi} (one per pass-2 output) stay in
 // registers; the band accumulators live in TMEM (2 columns = one complex per
 // output r, 2 * R2 columns per thread; warps of a lane quadrant side by side).
 template <class PF, class TO>
-__global__ void __launch_bounds__(PF::T, PF::MINB)
-    k_rows_inv_steer_ilv(Geo g, const float4* __restrict__ T2, Bands bl, int half,
-                         const double* __restrict__ base, TO* __restrict__ out, int accumulate,
-                         SigSrc dcs, double dcr, double dci, float scale,
-                         const float2* __restrict__ twm, const float2* __restrict__ twl) {
+__device__ __forceinline__ void i2_body(int b, const Geo& g, const float4* __restrict__ T2,
+                                        const Bands& bl, int half,
+                                        const double* __restrict__ base, TO* __restrict__ out,
+                                        int accumulate, const SigSrc& dcs, double dcr,
+                                        double dci, float scale,
+                                        const float2* __restrict__ twm,
+                                        const float2* __restrict__ twl) {
   constexpr int L = PF::L;  // = Pw
   constexpr int R2 = PF::R2;
   static_assert(2 * PF::NB2 <= PF::T, "pass 2: one butterfly per thread");
@@ -186,7 +198,7 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
   float2* W0 = reinterpret_cast<float2*>(W04);
   float2* W1 = reinterpret_cast<float2*>(W14);
   __shared__ uint32_t tbase;
-  const int b = blockIdx.x, t = threadIdx.x;
+  const int t = threadIdx.x;
   const size_t plane4 = size_t(g.H2 / 2) * g.Pw;  // float4 per band plane
   const float4* rowp = T2 + size_t(b) * g.Pw;
   constexpr unsigned kBytes = unsigned(L * sizeof(float4));
@@ -333,6 +345,63 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
     tmem_fence_after_sync();
     tmem_dealloc(tbase, PF::tmem_cols(kThr));
   }
+}
+
+template <class PF, class TO>
+__global__ void __launch_bounds__(PF::T, PF::MINB)
+    k_rows_inv_steer_ilv(Geo g, const float4* __restrict__ T2, Bands bl, int half,
+                         const double* __restrict__ base, TO* __restrict__ out, int accumulate,
+                         SigSrc dcs, double dcr, double dci, float scale,
+                         const float2* __restrict__ twm, const float2* __restrict__ twl) {
+  i2_body<PF, TO>(blockIdx.x, g, T2, bl, half, base, out, accumulate, dcs, dcr, dci, scale, twm,
+                  twl);
+}
+
+// ------------------------------------------------------------------ I1 + I2 (dual)
+// One launch runs I1 of image n+1 and I2 of image n, their CTAs interleaved
+// by block index, so every SM alternates between the HBM-heavy I1 (filter
+// spectra in, T2 out) and the FP32-bound I2: the two kernels' bottlenecks
+// overlap instead of following each other.  Same engine, same shared-memory
+// layout and TMEM budget; n1 I1 column pairs, n2 I2 row pairs.
+struct I1Args {
+  const float4* Hh;
+  const float4* Fh;
+  size_t sstride4;
+  Bands bl;
+  float2* T2;
+};
+template <class TO>
+struct I2Args {
+  const float4* T2;
+  Bands bl;
+  int half;
+  const double* base;
+  TO* out;
+  int accumulate;
+  SigSrc dcs;
+  double dcr, dci;
+  float scale;
+};
+
+template <class PF, class TO>
+__global__ void __launch_bounds__(PF::T, 1)
+    k_dual_ilv(Geo g, I1Args a, I2Args<TO> b, int n1, int n2, const float2* __restrict__ twm,
+               const float2* __restrict__ twl, const float2* __restrict__ twf) {
+  const int x = blockIdx.x, m = n1 < n2 ? n1 : n2;
+  bool first;
+  int item;
+  if (x < 2 * m) {
+    first = (x & 1) == 0;
+    item = x >> 1;
+  } else {
+    first = n1 > m;
+    item = x - m;
+  }
+  if (first)
+    i1_body<PF, 1>(item, g, a.Hh, 0, a.Fh, a.sstride4, a.bl, a.T2, 0, twm, twf);
+  else
+    i2_body<PF, TO>(item, g, b.T2, b.bl, b.half, b.base, b.out, b.accumulate, b.dcs, b.dcr, b.dci,
+                    b.scale, twm, twl);
 }
 
 // ------------------------------------------------------------------ planes (interleaved)
@@ -960,6 +1029,45 @@ void launch_rows_inv_steer_pair(const Geo& g, const float2* T2, const Bands& b, 
           g, t2, b, half, base, static_cast<double2*>(out), accumulate, dcs, dcr, dci,      \
           scale,                                                                            \
           tw.mid, tw.last);                                                                 \
+    }                                                                                       \
+    break;                                                                                  \
+  }
+  XCB_PAIR_DISPATCH(g.Pw, XCB_BODY)
+#undef XCB_BODY
+  ++lc.n;
+}
+
+bool dual_pair_ok(const Geo& g) {
+  return g.Ph == g.Pw && pair_smem(0, g.Ph, g) && pair_smem(1, g.Pw, g);
+}
+
+void launch_dual_pair(const Geo& g, const float2* Hhat, const float2* Fhat, size_t sstride,
+                      const Bands& b, float2* T2w, const float2* T2r, int half,
+                      const double* base, int out_kind, void* out, int accumulate,
+                      const SigSrc& dcs, double dcr, double dci, cudaStream_t st,
+                      LaunchCounter& lc) {
+  const size_t sm = pair_smem(0, g.Ph, g);
+  const float scale = float(1.0 / (double(g.Ph) * double(g.Pw)));
+  const I1Args a{reinterpret_cast<const float4*>(Hhat), reinterpret_cast<const float4*>(Fhat),
+                 sstride / 2, b, T2w};
+  const int n1 = g.Pw / 2, n2 = g.H2 / 2;
+#define XCB_BODY(LL, R0, R1, R2, PP)                                                         \
+  case LL: {                                                                                \
+    using PF = IlvFft<LL, R0, R1, R2, PP>;                                                  \
+    const PairTw tw = pair_tables<PF>();                                                    \
+    if (out_kind == OUT_C64) {                                                              \
+      const I2Args<float2> i2{reinterpret_cast<const float4*>(T2r), b, half, base,          \
+                              static_cast<float2*>(out), accumulate, dcs, dcr, dci, scale}; \
+      set_smem(k_dual_ilv<PF, float2>, sm);                                                 \
+      k_dual_ilv<PF, float2><<<n1 + n2, PF::T, sm, st>>>(g, a, i2, n1, n2, tw.mid, tw.last, \
+                                                         tw.last);                          \
+    } else {                                                                                \
+      const I2Args<double2> i2{reinterpret_cast<const float4*>(T2r), b, half, base,         \
+                               static_cast<double2*>(out), accumulate, dcs, dcr, dci,       \
+                               scale};                                                      \
+      set_smem(k_dual_ilv<PF, double2>, sm);                                                \
+      k_dual_ilv<PF, double2><<<n1 + n2, PF::T, sm, st>>>(g, a, i2, n1, n2, tw.mid,         \
+                                                          tw.last, tw.last);                \
     }                                                                                       \
     break;                                                                                  \
   }

@@ -176,6 +176,14 @@ void launch_rows_inv_planes_pair(const Geo& g, const float2* T2, int nbands, flo
                                  cudaStream_t st, LaunchCounter& lc);
 // images per I1 launch the pair engine supports for this geometry
 int pair_i1_images();
+// I1 of one image (Hhat -> T2w) and I2 of the previous one (T2r -> out) in one
+// launch with interleaved CTAs (needs Ph == Pw and both pair plans)
+bool dual_pair_ok(const Geo& g);
+void launch_dual_pair(const Geo& g, const float2* Hhat, const float2* Fhat, size_t sstride,
+                      const Bands& b, float2* T2w, const float2* T2r, int half,
+                      const double* base, int out_kind, void* out, int accumulate,
+                      const SigSrc& dcs, double dcr, double dci, cudaStream_t st,
+                      LaunchCounter& lc);
 // half: Hermitian half-band mode (bands k >= 0, k = 0 weighted 1/2, out = 2 Re)
 void launch_rows_inv_steer_pair(const Geo& g, const float2* T2, const Bands& b, int half,
                                 const double* base, int out_kind, void* out, int accumulate,
