@@ -143,6 +143,19 @@ struct xc_context_s {
     return plans.emplace(L, std::move(e)).first->second.plan;
   }
 
+  // plans with radices <= 10 for the 3D tile kernels (k_3d.cu), keyed -L
+  const xcb::FftPlan& plan3(int L) {
+    auto it = plans.find(-L);
+    if (it != plans.end()) return it->second.plan;
+    PlanEntry e;
+    if (!xcb::make_fft_plan_maxr(L, 10, &e.plan))
+      throw std::invalid_argument("unsupported transform length");
+    e.tw = xcb::upload_twiddles(e.plan);
+    if (!e.tw) throw CudaError("twiddle upload failed", XC_ENOMEM);
+    e.plan.d.tw = e.tw;
+    return plans.emplace(-L, std::move(e)).first->second.plan;
+  }
+
   // nullptr if L has no fast plan
   const xcb::FftPlan* fast_plan(int L) {
     auto it = fast_plans.find(L);
@@ -1674,9 +1687,11 @@ int xc_run3(xc_context ctx, xc_filter3 f, int mode, int nx, int ny, int nz, cons
     g.py = pick_pad(std::max(ny + R, 2 * R + 1));
     g.pz = pick_pad(std::max(nz + R, 2 * R + 1));
     if (g.px < 0 || g.py < 0 || g.pz < 0) throw std::invalid_argument("volume too large for the FFT planner");
-    const xcb::FftPlan& pxp = ctx->plan(g.px);
-    const xcb::FftPlan& pyp = ctx->plan(g.py);
-    const xcb::FftPlan& pzp = ctx->plan(g.pz);
+    if (xcb::tile3_smem(std::max({g.px, g.py, g.pz})) > 200 * 1024)
+      throw std::invalid_argument("volume too large for the 3D line transforms");
+    const xcb::FftPlan& pxp = ctx->plan3(g.px);
+    const xcb::FftPlan& pyp = ctx->plan3(g.py);
+    const xcb::FftPlan& pzp = ctx->plan3(g.pz);
     cudaStream_t st = ctx->stream;
     xcb::LaunchCounter lc;
     const size_t N = size_t(nx) * ny * nz, P = size_t(g.px) * g.py * g.pz;
@@ -1708,11 +1723,13 @@ int xc_run3(xc_context ctx, xc_filter3 f, int mode, int nx, int ny, int nz, cons
        "upload band spectra");
     double2* dout = memory == XC_DEVICE ? reinterpret_cast<double2*>(out)
                                         : ctx->buf<double2>("v3_out", N);
-    // bands per chunk: work volumes within ~4 GB
-    const int cb = int(std::max<size_t>(1, std::min<size_t>(nb, (size_t(4) << 30) / (P * 8))));
+    // bands per chunk: work volumes (and gather planes) within ~4 GB
+    const size_t per_band = (P + (mode == XC_CORRELATION ? N : 0)) * sizeof(float2);
+    const int cb = int(std::max<size_t>(1, std::min<size_t>(nb, (size_t(4) << 30) / per_band)));
     float2* work = ctx->buf<float2>("v3_work", P * cb);
     if (mode == XC_CORRELATION) {
       float2* Hh = ctx->buf<float2>("v3_Hhat", P);
+      float2* part = ctx->buf<float2>("v3_part", N * cb);
       xcb::launch3_x_signal(pxp, g, dsig, eul, dbands, 1, 0, Hh, P, st, lc);
       xcb::launch3_pass(pyp, g, 1, Hh, P, 1, st, lc);
       xcb::launch3_pass(pzp, g, 2, Hh, P, 1, st, lc);
@@ -1720,7 +1737,8 @@ int xc_run3(xc_context ctx, xc_filter3 f, int mode, int nx, int ny, int nz, cons
         const int n = std::min(cb, nb - b0);
         xcb::launch3_z_load(pzp, g, Hh, spec, dsidx + b0, n, P, 0, work, st, lc);
         xcb::launch3_pass(pyp, g, 1, work, P, n, st, lc);
-        xcb::launch3_x_steer(pxp, g, work, P, n, eul, dbands + b0, 0, b0 > 0, dout, st, lc);
+        xcb::launch3_x_out(pxp, g, work, P, n, eul, dbands + b0, 0, part, 0, nullptr, st, lc);
+        xcb::launch3_reduce_parts(part, n, N, b0 > 0, dout, st, lc);
       }
     } else {
       float2* sum = ctx->buf<float2>("v3_sum", P);
@@ -1729,11 +1747,12 @@ int xc_run3(xc_context ctx, xc_filter3 f, int mode, int nx, int ny, int nz, cons
         const int n = std::min(cb, nb - b0);
         xcb::launch3_x_signal(pxp, g, dsig, eul, dbands + b0, n, 1, work, P, st, lc);
         xcb::launch3_pass(pyp, g, 1, work, P, n, st, lc);
-        xcb::launch3_z_mac(pzp, g, work, P, n, spec, dsidx + b0, sum, st, lc);
+        xcb::launch3_pass(pzp, g, 2, work, P, n, st, lc);
+        xcb::launch3_mac(work, n, P, spec, dsidx + b0, sum, st, lc);
       }
       xcb::launch3_z_load(pzp, g, sum, nullptr, nullptr, 1, P, 1, work, st, lc);
       xcb::launch3_pass(pyp, g, 1, work, P, 1, st, lc);
-      xcb::launch3_x_steer(pxp, g, work, P, 1, eul, dbands, 1, 0, dout, st, lc);
+      xcb::launch3_x_out(pxp, g, work, P, 1, eul, dbands, 1, nullptr, 0, dout, st, lc);
     }
     ck(cudaGetLastError(), "3D kernel launch");
     ck(cudaEventRecord(e1, st), "event");

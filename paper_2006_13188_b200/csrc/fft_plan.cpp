@@ -68,7 +68,9 @@ bool is_smooth235(int n) {
   return n == 1;
 }
 
-bool make_fft_plan(int L, FftPlan* out) {
+bool make_fft_plan(int L, FftPlan* out) { return make_fft_plan_maxr(L, 20, out); }
+
+bool make_fft_plan_maxr(int L, int max_radix, FftPlan* out) {
   if (!is_smooth235(L) || L > (1 << 15)) return false;
   // enumerate non-increasing radix multisets with product L
   std::vector<std::vector<int>> sets;
@@ -81,7 +83,7 @@ bool make_fft_plan(int L, FftPlan* out) {
     if (int(cur.size()) >= kMaxPasses) return;
     for (int i = start; i < int(sizeof(kRadices) / sizeof(int)); ++i) {
       const int r = kRadices[i];
-      if (rem % r) continue;
+      if (rem % r || r > max_radix) continue;
       cur.push_back(r);
       dfs(rem / r, i);
       cur.pop_back();

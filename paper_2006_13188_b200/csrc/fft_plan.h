@@ -40,6 +40,8 @@ bool is_smooth235(int n);
 // Builds a plan for length L (2/3/5-smooth); false if no factorization fits
 // the codelet set and thread budget.
 bool make_fft_plan(int L, FftPlan* out);
+// the same with radices <= max_radix (the 3D tile kernels dispatch 2..10 only)
+bool make_fft_plan_maxr(int L, int max_radix, FftPlan* out);
 // Fast path (k_fast.cu): transform lengths with a compile-time plan
 // (R0 first pass, R1 middle pass or 1, RL last pass).  One kernel instance per
 // entry keeps each kernel to a single radix per pass, which is what lets the

@@ -2,27 +2,35 @@
 //
 // Bands are the (l, m, m') triples of the SH decomposition, sum (2l+1)^2 of
 // them.  Volumes are x fastest, index (z*py + y)*px + x for padded
-// (px, py, pz) volumes.  Every 3D FFT is three passes of line transforms
-// (k3_* below), each CTA transforming a pair of lines in shared memory with
-// the runtime-planned Stockham engine of fft_core.cuh.  Inverse transforms
-// are conj(FFT(conj(.)))/P with the conjugations folded into the first load
-// and the last store.
-//   gather  : H^ = FFT3(H) once; per band z-pass of conj(H^) V^_b (the
-//             spectral multiply fused into the load), y-pass, then an x-pass
-//             that crops and accumulates conj(D^l_{m' m}(voxel)) G_b into a
-//             shared-memory line accumulator across the bands of a chunk
-//   scatter : per band x-pass of H D_b(voxel) (premultiply fused into the
-//             load), y-pass, z-pass whose store accumulates FFT3(H D_b) V^_b
-//             into one spectrum; one inverse 3D FFT at the end (the
-//             reference's per-band inverse FFTs collapse into one)
-// The per-voxel Wigner entry D = e^{-i(m' alpha + m gamma)} d^l_{m' m}(beta)
-// is evaluated in fp64 from the voxel's (alpha, gamma, cos beta/2, sin beta/2)
+// (px, py, pz) volumes.  Every 3D FFT is three passes of line transforms.
+// A CTA transforms a tile of 16 lines held in shared memory as [line][n]
+// with an odd row stride (conflict-free for the line-fast butterfly order),
+// using the runtime-planned Stockham codelets of fft_core.cuh:
+//   x tiles: 16 rows (contiguous lines), copied in and out n-fast
+//   y / z tiles: 16 adjacent x at one (z) / (y), copied line-fast, so every
+//   global access covers 128 contiguous bytes
+// Grids are (tiles, bands of the chunk), so short lines still fill the GPU.
+// Inverse transforms are conj(FFT(conj(.)))/P with the conjugations folded
+// into the first load and the last store.
+//   gather  : H^ = FFT3(H) once; per band a z-pass loading conj(H^) V^_b
+//             (the spectral multiply fused into the load), a y-pass, and an
+//             x-pass that crops and steers with conj(D^l_{m'm}(voxel)) into a
+//             per-band plane; one reduction sums the planes (fixed order)
+//   scatter : per band an x-pass of H D_b(voxel) (premultiply fused), y- and
+//             z-passes, one multiply-accumulate kernel sum += FFT3(H D_b) V^_b
+//             over the chunk; one inverse 3D FFT at the end (the reference's
+//             per-band inverse FFTs collapse into one)
+// The Wigner entry D = e^{-i(m' alpha + m gamma)} d^l_{m' m}(beta) is
+// evaluated in fp64 from the voxel's (alpha, gamma, cos beta/2, sin beta/2)
 // with the band's Horner coefficients (host_sph.h SmallD).
 #include "kernels3d.h"
 #include "stages_common.cuh"
 
 namespace xcb {
 namespace {
+
+constexpr int kTL = 16;    // lines per tile
+constexpr int kT3 = 256;   // threads per tile CTA
 
 // ---------------------------------------------------------------- per voxel
 
@@ -100,192 +108,273 @@ __device__ __forceinline__ float2 wigner_at(const Band3& b, const double4& e, fl
   return make_float2(d * cs, sign * d * sn);
 }
 
-// ---------------------------------------------------------------- line geometry
-// line li of axis a in a (px, py, pz) volume: element n at base + n * stride
-struct Lines {
-  int px, py, pz, axis;
-  __device__ __forceinline__ int count() const {
-    return axis == 0 ? py * pz : axis == 1 ? px * pz : px * py;
-  }
-  __device__ __forceinline__ size_t base(int li) const {
-    if (axis == 0) return size_t(li) * px;
-    if (axis == 1) return size_t(li % px) + size_t(li / px) * px * py;
-    return size_t(li);
-  }
-  __device__ __forceinline__ size_t stride() const {
-    return axis == 0 ? 1 : axis == 1 ? size_t(px) : size_t(px) * py;
-  }
-};
+// ---------------------------------------------------------------- tile FFT
+// Row stride of a tile buffer: odd (mod 16), so 16 lanes on consecutive
+// lines hit distinct bank pairs.
+__host__ __device__ constexpr int tile_stride(int L) { return L % 2 ? L : L + 1; }
 
-// plain in-place forward pass along `axis` of nb volumes (grid.y = volume)
-__global__ void __launch_bounds__(kMaxThreads)
-    k3_pass(FftPlanD p, Lines ln, float2* __restrict__ buf, size_t vstride) {
-  extern __shared__ float2 sm[];
-  float2* v = buf + blockIdx.y * vstride;
-  const int li0 = 2 * blockIdx.x, nl = ln.count();
-  const size_t st = ln.stride();
-  const size_t b0 = ln.base(li0), b1 = li0 + 1 < nl ? ln.base(li0 + 1) : b0;
-  auto load = [&](int n, int g) -> float2 { return v[(g ? b1 : b0) + n * st]; };
-  auto store = [&](int k, int g, float2 x) {
-    if (g == 0 || li0 + 1 < nl) v[(g ? b1 : b0) + k * st] = x;
-  };
-  fft_block(p, sm, load, store);
+// Radices of the tile plans (make_fft_plan_maxr(L, 10)): a small dispatch set
+// keeps the kernels at <= 64 registers, 4 CTAs of 256 threads per SM.
+template <class F>
+__device__ __forceinline__ void radix_dispatch10(int R, F&& f) {
+  switch (R) {
+    case 2: f(IntC<2>{}); break;
+    case 3: f(IntC<3>{}); break;
+    case 4: f(IntC<4>{}); break;
+    case 5: f(IntC<5>{}); break;
+    case 6: f(IntC<6>{}); break;
+    case 8: f(IntC<8>{}); break;
+    case 9: f(IntC<9>{}); break;
+    case 10: f(IntC<10>{}); break;
+    default: break;
+  }
 }
 
-// x-pass from the signal (zero-padded), optionally times D_b(voxel) (the
-// scatter premultiply, engine3d.hpp:317-321); grid.y = band of the chunk
-__global__ void __launch_bounds__(kMaxThreads)
-    k3_x_signal(FftPlanD p, Geo3 g, const float2* __restrict__ sig,
-                const double4* __restrict__ eul, const Band3* __restrict__ bands, int premul,
-                float2* __restrict__ work, size_t vstride) {
+// Forward transform of kTL sequences held in A ([line][Lp]); ping-pong with B.
+// Returns the buffer holding the result.  Called by every thread; A must be
+// complete (a barrier) on entry.
+__device__ float2* tile_fft(const FftPlanD& p, float2* A, float2* B, int Lp) {
+  float2* src = A;
+  float2* dst = B;
+  for (int q = 0; q < p.npass; ++q) {
+    radix_dispatch10(p.radix[q], [&](auto rc) {
+      constexpr int R = decltype(rc)::value;
+      const int nb = p.L / R, Ns = p.ns[q];
+      const float2* tw = p.tw + p.tw_off[q];
+      for (int w = threadIdx.x; w < kTL * nb; w += blockDim.x) {
+        const int line = w % kTL, j = w / kTL;
+        const int jm = q == 0 ? 0 : j - Ns * int(__umulhi(unsigned(j), p.magic[q]));
+        const float2* s = src + line * Lp + j;
+        float2 v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = s[r * nb];
+        if (q > 0) {
+#pragma unroll
+          for (int r = 1; r < R; ++r) v[r] = c_mul(v[r], __ldg(tw + (r - 1) * Ns + jm));
+        }
+        Dft<R>::run(v);
+        float2* d = dst + line * Lp + (j - jm) * R + jm;
+#pragma unroll
+        for (int r = 0; r < R; ++r) d[r * Ns] = v[Dft<R>::pos(r)];
+      }
+    });
+    __syncthreads();
+    float2* t = src;
+    src = dst;
+    dst = t;
+  }
+  return src;
+}
+
+// y / z tiles: 16 adjacent x at one (z) for axis 1, at one (y) for axis 2
+struct YZTile {
+  int x0, c;
+  __device__ __forceinline__ size_t base(const Geo3& g, int axis, int n) const {
+    return axis == 1 ? (size_t(c) * g.py + n) * g.px + x0 : (size_t(n) * g.py + c) * g.px + x0;
+  }
+};
+__device__ __forceinline__ YZTile yz_tile(const Geo3& g) {
+  const int xt = (g.px + kTL - 1) / kTL;
+  return YZTile{int(blockIdx.x % xt) * kTL, int(blockIdx.x / xt)};
+}
+
+// copy a y / z tile in / out line-fast: 16 adjacent x = 128 contiguous bytes
+template <class Ld>
+__device__ __forceinline__ void yz_load(const Geo3& g, int axis, const YZTile& t, int L,
+                                        float2* A, int Lp, Ld&& ld) {
+  for (int w = threadIdx.x; w < kTL * L; w += blockDim.x) {
+    const int line = w % kTL, n = w / kTL;
+    A[line * Lp + n] = t.x0 + line < g.px ? ld(t.base(g, axis, n) + line) : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+}
+template <class St>
+__device__ __forceinline__ void yz_store(const Geo3& g, int axis, const YZTile& t, int L,
+                                         const float2* Y, int Lp, St&& st) {
+  for (int w = threadIdx.x; w < kTL * L; w += blockDim.x) {
+    const int line = w % kTL, n = w / kTL;
+    if (t.x0 + line < g.px) st(t.base(g, axis, n) + line, Y[line * Lp + n]);
+  }
+}
+
+// in-place forward y- or z-pass of nvol volumes; grid (tiles, volume)
+__global__ void __launch_bounds__(kT3, 4) k3t_yz(FftPlanD p, Geo3 g, int axis,
+                                              float2* __restrict__ buf, size_t vstride) {
   extern __shared__ float2 sm[];
+  const int L = p.L, Lp = tile_stride(L);
+  float2* A = sm;
+  float2* B = sm + kTL * Lp;
+  float2* v = buf + blockIdx.y * vstride;
+  const YZTile t = yz_tile(g);
+  yz_load(g, axis, t, L, A, Lp, [&](size_t i) { return v[i]; });
+  const float2* Y = tile_fft(p, A, B, Lp);
+  yz_store(g, axis, t, L, Y, Lp, [&](size_t i, float2 x) { v[i] = x; });
+}
+
+// z-pass loading conj(H^) V^_sidx[b] (mode 0, gather) or conj(H^) (mode 1,
+// the scatter's final inverse) -> work_b; grid (tiles, band of the chunk)
+__global__ void __launch_bounds__(kT3, 4)
+    k3t_z_load(FftPlanD p, Geo3 g, const float2* __restrict__ Hh, const float2* __restrict__ spec,
+               const int* __restrict__ sidx, size_t vstride, int mode, float2* __restrict__ work) {
+  extern __shared__ float2 sm[];
+  const int L = p.L, Lp = tile_stride(L);
+  float2* A = sm;
+  float2* B = sm + kTL * Lp;
+  const float2* V = mode == 0 ? spec + size_t(sidx[blockIdx.y]) * vstride : nullptr;
+  float2* w = work + blockIdx.y * vstride;
+  const YZTile t = yz_tile(g);
+  yz_load(g, 2, t, L, A, Lp, [&](size_t i) {
+    return mode == 0 ? c_mul(c_conj(Hh[i]), __ldg(V + i)) : c_conj(Hh[i]);
+  });
+  const float2* Y = tile_fft(p, A, B, Lp);
+  yz_store(g, 2, t, L, Y, Lp, [&](size_t i, float2 x) { w[i] = x; });
+}
+
+// x tiles: rows li0 .. li0 + 15 of nl lines, copied in n-fast (contiguous)
+template <class Ld>
+__device__ __forceinline__ void x_load(int L, int nl, float2* A, int Lp, Ld&& ld) {
+  const int li0 = blockIdx.x * kTL;
+  for (int w = threadIdx.x; w < kTL * L; w += blockDim.x) {
+    const int n = w % L, line = w / L;
+    A[line * Lp + n] = li0 + line < nl ? ld(li0 + line, n) : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void x_store_rows(int L, int nl, int px, const float2* Y, int Lp,
+                                             float2* v) {
+  const int li0 = blockIdx.x * kTL;
+  for (int w = threadIdx.x; w < kTL * L; w += blockDim.x) {
+    const int n = w % L, line = w / L;
+    if (li0 + line < nl) v[size_t(li0 + line) * px + n] = Y[line * Lp + n];
+  }
+}
+
+// x-pass from the signal (zero-padded), times D_b when premul (the scatter
+// premultiply, engine3d.hpp:317-321); grid (tiles over py*pz rows, band)
+__global__ void __launch_bounds__(kT3, 4)
+    k3t_x_signal(FftPlanD p, Geo3 g, const float2* __restrict__ sig,
+                 const double4* __restrict__ eul, const Band3* __restrict__ bands, int premul,
+                 float2* __restrict__ work, size_t vstride) {
+  extern __shared__ float2 sm[];
+  const int L = p.L, Lp = tile_stride(L), nl = g.py * g.pz;
+  float2* A = sm;
+  float2* B = sm + kTL * Lp;
   const Band3& b = bands[blockIdx.y];
-  float2* v = work + blockIdx.y * vstride;
-  const int li0 = 2 * blockIdx.x, nl = g.py * g.pz;
-  auto load = [&](int n, int gi) -> float2 {
-    const int li = li0 + gi, y = li % g.py, z = li / g.py;
-    if (li >= nl || n >= g.nx || y >= g.ny || z >= g.nz) return make_float2(0.f, 0.f);
+  x_load(L, nl, A, Lp, [&](int li, int n) -> float2 {
+    const int y = li % g.py, z = li / g.py;
+    if (n >= g.nx || y >= g.ny || z >= g.nz) return make_float2(0.f, 0.f);
     const size_t i = (size_t(z) * g.ny + y) * g.nx + n;
     float2 h = sig[i];
     if (premul) h = c_mul(h, wigner_at(b, eul[i], -1.f));
     return h;
-  };
-  auto store = [&](int k, int gi, float2 x) {
-    if (li0 + gi < nl) v[size_t(li0 + gi) * g.px + k] = x;
-  };
-  fft_block(p, sm, load, store);
+  });
+  const float2* Y = tile_fft(p, A, B, Lp);
+  x_store_rows(L, nl, g.px, Y, Lp, work + blockIdx.y * vstride);
 }
 
 // x-pass of the filter bands: rendered (2R+1)^3 components wrapped to the
-// origin (fft.hpp:186-194); grid.y = band
-__global__ void __launch_bounds__(kMaxThreads)
-    k3_x_filter(FftPlanD p, Geo3 g, const float2* __restrict__ comps, float2* __restrict__ spec,
-                size_t vstride) {
+// origin (fft.hpp:186-194); grid (tiles over py*pz rows, band)
+__global__ void __launch_bounds__(kT3, 4)
+    k3t_x_filter(FftPlanD p, Geo3 g, const float2* __restrict__ comps, float2* __restrict__ spec,
+                 size_t vstride) {
   extern __shared__ float2 sm[];
-  const int S = 2 * g.R + 1;
+  const int L = p.L, Lp = tile_stride(L), nl = g.py * g.pz, S = 2 * g.R + 1;
+  float2* A = sm;
+  float2* B = sm + kTL * Lp;
   const float2* f = comps + size_t(blockIdx.y) * S * S * S;
-  float2* v = spec + blockIdx.y * vstride;
-  const int li0 = 2 * blockIdx.x, nl = g.py * g.pz;
-  auto src = [&](int n, int P) { int s = n + g.R; return s >= P ? s - P : s; };
-  auto load = [&](int n, int gi) -> float2 {
-    const int li = li0 + gi;
-    if (li >= nl) return make_float2(0.f, 0.f);
+  auto src = [&](int n, int P) {
+    const int s = n + g.R;
+    return s >= P ? s - P : s;
+  };
+  x_load(L, nl, A, Lp, [&](int li, int n) -> float2 {
     const int x = src(n, g.px), y = src(li % g.py, g.py), z = src(li / g.py, g.pz);
     if (x >= S || y >= S || z >= S) return make_float2(0.f, 0.f);
     return f[(size_t(z) * S + y) * S + x];
-  };
-  auto store = [&](int k, int gi, float2 x) {
-    if (li0 + gi < nl) v[size_t(li0 + gi) * g.px + k] = x;
-  };
-  fft_block(p, sm, load, store);
+  });
+  const float2* Y = tile_fft(p, A, B, Lp);
+  x_store_rows(L, nl, g.px, Y, Lp, spec + blockIdx.y * vstride);
 }
 
-// gather z-pass: conj(H^) V^_b (conj of the correlation product H^ conj(V^),
-// fft.hpp:195-197) -> work_b; grid.y = band of the chunk.  mode 1 instead
-// loads conj(src) of one volume (the scatter's final inverse).
-__global__ void __launch_bounds__(kMaxThreads)
-    k3_z_load(FftPlanD p, Geo3 g, const float2* __restrict__ Hh, const float2* __restrict__ spec,
-              const int* __restrict__ sidx, size_t vstride, int mode, float2* __restrict__ work) {
+// x-pass finishing an inverse: rows (y, z) < (ny, nz) of work_b, crop x < nx;
+// mode 0: part_b = conj(D_b) G_b (gather steering, engine3d.hpp:290-298);
+// mode 1: out (+)= G (the scatter's single inverse).  G = conj(Y) / P.
+__global__ void __launch_bounds__(kT3, 4)
+    k3t_x_out(FftPlanD p, Geo3 g, const float2* __restrict__ work, size_t vstride,
+              const double4* __restrict__ eul, const Band3* __restrict__ bands, int mode,
+              float inv_p, float2* __restrict__ part, int accumulate, double2* __restrict__ out) {
   extern __shared__ float2 sm[];
-  const int li0 = 2 * blockIdx.x, nl = g.px * g.py;
-  const size_t st = size_t(g.px) * g.py;
-  const float2* V = mode == 0 ? spec + size_t(sidx[blockIdx.y]) * vstride : nullptr;
-  float2* w = work + blockIdx.y * vstride;
-  auto load = [&](int n, int gi) -> float2 {
-    const int li = li0 + gi;
-    if (li >= nl) return make_float2(0.f, 0.f);
-    const size_t i = size_t(li) + n * st;
-    return mode == 0 ? c_mul(c_conj(Hh[i]), V[i]) : c_conj(Hh[i]);
-  };
-  auto store = [&](int k, int gi, float2 x) {
-    if (li0 + gi < nl) w[size_t(li0 + gi) + k * st] = x;
-  };
-  fft_block(p, sm, load, store);
-}
-
-// gather x-pass: per band of the chunk, row transform of work_b, crop, steer
-// with conj(D_b) and accumulate in shared memory; out (+)= the sum
-// (engine3d.hpp:290-298).  mode 1: one volume, no steering (the scatter's
-// final inverse).  The inverse is conj(Y) / P.
-__global__ void __launch_bounds__(kMaxThreads)
-    k3_x_steer(FftPlanD p, Geo3 g, const float2* __restrict__ work, size_t vstride, int nb,
-               const double4* __restrict__ eul, const Band3* __restrict__ bands, int mode,
-               float inv_p, int accumulate, double2* __restrict__ out) {
-  extern __shared__ float2 sm[];
-  float2* acc = sm + 2 * kG * p.Lp;  // [2][nx]
-  const int li0 = 2 * blockIdx.x, nl = g.ny * g.nz;
-  for (int i = threadIdx.x; i < 2 * g.nx; i += blockDim.x) acc[i] = make_float2(0.f, 0.f);
-  __syncthreads();
-  for (int bi = 0; bi < nb; ++bi) {
-    const float2* w = work + bi * vstride;
-    const Band3& b = bands[bi];
-    auto load = [&](int n, int gi) -> float2 {
-      const int li = li0 + gi;
-      if (li >= nl) return make_float2(0.f, 0.f);
-      const int y = li % g.ny, z = li / g.ny;
-      return w[(size_t(z) * g.py + y) * g.px + n];
-    };
-    auto store = [&](int k, int gi, float2 x) {
-      const int li = li0 + gi;
-      if (k >= g.nx || li >= nl) return;
-      float2 v = c_scale(c_conj(x), inv_p);
-      if (mode == 0) {
-        const size_t vi = size_t(li) * g.nx + k;  // (z*ny + y)*nx + x
-        v = c_mul(wigner_at(b, eul[vi], 1.f), v);
-      }
-      acc[gi * g.nx + k] = c_add(acc[gi * g.nx + k], v);
-    };
-    fft_block(p, sm, load, store);
-    __syncthreads();
-  }
-  for (int i = threadIdx.x; i < 2 * g.nx; i += blockDim.x) {
-    const int li = li0 + i / g.nx;
+  const int L = p.L, Lp = tile_stride(L), nl = g.ny * g.nz;
+  float2* A = sm;
+  float2* B = sm + kTL * Lp;
+  const float2* w = work + blockIdx.y * vstride;
+  x_load(L, nl, A, Lp, [&](int li, int n) -> float2 {
+    const int y = li % g.ny, z = li / g.ny;
+    return w[(size_t(z) * g.py + y) * g.px + n];
+  });
+  const float2* Y = tile_fft(p, A, B, Lp);
+  const size_t N = size_t(g.nx) * g.ny * g.nz;
+  const int li0 = blockIdx.x * kTL;
+  for (int e = threadIdx.x; e < kTL * g.nx; e += blockDim.x) {
+    const int x = e % g.nx, line = e / g.nx, li = li0 + line;
     if (li >= nl) continue;
-    const size_t o = size_t(li) * g.nx + i % g.nx;
-    double2 v = make_double2(acc[i].x, acc[i].y);
-    if (accumulate) {
-      v.x += out[o].x;
-      v.y += out[o].y;
+    const size_t vi = size_t(li) * g.nx + x;  // (z*ny + y)*nx + x
+    const float2 G = c_scale(c_conj(Y[line * Lp + x]), inv_p);
+    if (mode == 0) {
+      part[blockIdx.y * N + vi] = c_mul(wigner_at(bands[blockIdx.y], eul[vi], 1.f), G);
+    } else {
+      double2 v = make_double2(G.x, G.y);
+      if (accumulate) {
+        v.x += out[vi].x;
+        v.y += out[vi].y;
+      }
+      out[vi] = v;
     }
-    out[o] = v;
   }
 }
 
-// scatter z-pass: per band of the chunk, column transform of work_b, then
-// sum += FFT3(H D_b) V^_b (fft.hpp:195-197 with the band sum in frequency)
-__global__ void __launch_bounds__(kMaxThreads)
-    k3_z_mac(FftPlanD p, Geo3 g, const float2* __restrict__ work, size_t vstride, int nb,
-             const float2* __restrict__ spec, const int* __restrict__ sidx,
-             float2* __restrict__ sum) {
-  extern __shared__ float2 sm[];
-  const int li0 = 2 * blockIdx.x, nl = g.px * g.py;
-  const size_t st = size_t(g.px) * g.py;
-  for (int bi = 0; bi < nb; ++bi) {
-    const float2* w = work + bi * vstride;
-    const float2* V = spec + size_t(sidx[bi]) * vstride;
-    auto load = [&](int n, int gi) -> float2 {
-      const int li = li0 + gi;
-      return li < nl ? w[size_t(li) + n * st] : make_float2(0.f, 0.f);
-    };
-    auto store = [&](int k, int gi, float2 x) {
-      const int li = li0 + gi;
-      if (li >= nl) return;
-      const size_t i = size_t(li) + k * st;
-      sum[i] = c_add(sum[i], c_mul(x, V[i]));
-    };
-    fft_block(p, sm, load, store);
-    __syncthreads();
+// out (+)= sum over the chunk's nb band planes, in band order (deterministic)
+__global__ void k3_reduce_parts(const float2* __restrict__ part, int nb, size_t n,
+                                int accumulate, double2* __restrict__ out) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    double2 acc = accumulate ? out[i] : make_double2(0.0, 0.0);
+    for (int b = 0; b < nb; ++b) {
+      const float2 v = part[b * n + i];
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+    out[i] = acc;
+  }
+}
+
+// scatter: sum += sum over the chunk's bands of FFT3(H D_b) V^_sidx[b]
+__global__ void k3_mac(const float2* __restrict__ work, int nb, size_t P,
+                       const float2* __restrict__ spec, const int* __restrict__ sidx,
+                       float2* __restrict__ sum) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < P;
+       i += size_t(gridDim.x) * blockDim.x) {
+    float2 acc = sum[i];
+    for (int b = 0; b < nb; ++b)
+      acc = c_add(acc, c_mul(work[b * P + i], __ldg(spec + size_t(sidx[b]) * P + i)));
+    sum[i] = acc;
   }
 }
 
 template <class K>
 void smem_attr(K k, size_t bytes) {
-  if (bytes > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+  if (bytes > 48 * 1024)
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
 }
 
-unsigned pairs(long long lines) { return unsigned((lines + 1) / 2); }
+size_t tile_smem(int L) { return 2 * size_t(kTL) * tile_stride(L) * sizeof(float2); }
+unsigned ntiles(long long lines) { return unsigned((lines + kTL - 1) / kTL); }
+unsigned yz_tiles(const Geo3& g, int axis) {
+  return unsigned((g.px + kTL - 1) / kTL) * unsigned(axis == 1 ? g.pz : g.py);
+}
 
 }  // namespace
+
+size_t tile3_smem(int L) { return tile_smem(L); }
 
 void launch3_signal(const void* src, int dtype, size_t n, float2* dst, cudaStream_t st,
                     LaunchCounter& lc) {
@@ -301,58 +390,61 @@ void launch3_euler(const double* quats, size_t n, double4* eul, cudaStream_t st,
 
 void launch3_pass(const FftPlan& pl, const Geo3& g, int axis, float2* buf, size_t vstride,
                   int nvol, cudaStream_t st, LaunchCounter& lc) {
-  const Lines ln{g.px, g.py, g.pz, axis};
-  const long long nl = axis == 0 ? 1LL * g.py * g.pz : axis == 1 ? 1LL * g.px * g.pz
-                                                                  : 1LL * g.px * g.py;
-  smem_attr(k3_pass, pl.smem_bytes());
-  k3_pass<<<dim3(pairs(nl), nvol), pl.d.nt, pl.smem_bytes(), st>>>(pl.d, ln, buf, vstride);
+  const size_t sm = tile_smem(pl.d.L);
+  smem_attr(k3t_yz, sm);
+  k3t_yz<<<dim3(yz_tiles(g, axis), nvol), kT3, sm, st>>>(pl.d, g, axis, buf, vstride);
   ++lc.n;
 }
 
 void launch3_x_signal(const FftPlan& pl, const Geo3& g, const float2* sig, const double4* eul,
                       const Band3* bands, int nb, int premul, float2* work, size_t vstride,
                       cudaStream_t st, LaunchCounter& lc) {
-  smem_attr(k3_x_signal, pl.smem_bytes());
-  k3_x_signal<<<dim3(pairs(1LL * g.py * g.pz), nb), pl.d.nt, pl.smem_bytes(), st>>>(
-      pl.d, g, sig, eul, bands, premul, work, vstride);
+  const size_t sm = tile_smem(pl.d.L);
+  smem_attr(k3t_x_signal, sm);
+  k3t_x_signal<<<dim3(ntiles(1LL * g.py * g.pz), nb), kT3, sm, st>>>(pl.d, g, sig, eul, bands,
+                                                                     premul, work, vstride);
   ++lc.n;
 }
 
 void launch3_x_filter(const FftPlan& pl, const Geo3& g, const float2* comps, int nb,
                       float2* spec, size_t vstride, cudaStream_t st, LaunchCounter& lc) {
-  smem_attr(k3_x_filter, pl.smem_bytes());
-  k3_x_filter<<<dim3(pairs(1LL * g.py * g.pz), nb), pl.d.nt, pl.smem_bytes(), st>>>(
-      pl.d, g, comps, spec, vstride);
+  const size_t sm = tile_smem(pl.d.L);
+  smem_attr(k3t_x_filter, sm);
+  k3t_x_filter<<<dim3(ntiles(1LL * g.py * g.pz), nb), kT3, sm, st>>>(pl.d, g, comps, spec,
+                                                                     vstride);
   ++lc.n;
 }
 
 void launch3_z_load(const FftPlan& pl, const Geo3& g, const float2* Hh, const float2* spec,
                     const int* sidx, int nb, size_t vstride, int mode, float2* work,
                     cudaStream_t st, LaunchCounter& lc) {
-  smem_attr(k3_z_load, pl.smem_bytes());
-  k3_z_load<<<dim3(pairs(1LL * g.px * g.py), nb), pl.d.nt, pl.smem_bytes(), st>>>(
-      pl.d, g, Hh, spec, sidx, vstride, mode, work);
+  const size_t sm = tile_smem(pl.d.L);
+  smem_attr(k3t_z_load, sm);
+  k3t_z_load<<<dim3(yz_tiles(g, 2), nb), kT3, sm, st>>>(pl.d, g, Hh, spec, sidx, vstride, mode,
+                                                        work);
   ++lc.n;
 }
 
-void launch3_x_steer(const FftPlan& pl, const Geo3& g, const float2* work, size_t vstride,
-                     int nb, const double4* eul, const Band3* bands, int mode, int accumulate,
-                     double2* out, cudaStream_t st, LaunchCounter& lc) {
-  const size_t smem = pl.smem_bytes() + 2 * size_t(g.nx) * sizeof(float2);
-  smem_attr(k3_x_steer, smem);
+void launch3_x_out(const FftPlan& pl, const Geo3& g, const float2* work, size_t vstride, int nb,
+                   const double4* eul, const Band3* bands, int mode, float2* part,
+                   int accumulate, double2* out, cudaStream_t st, LaunchCounter& lc) {
+  const size_t sm = tile_smem(pl.d.L);
+  smem_attr(k3t_x_out, sm);
   const float inv_p = float(1.0 / (double(g.px) * g.py * g.pz));
-  k3_x_steer<<<pairs(1LL * g.ny * g.nz), pl.d.nt, smem, st>>>(pl.d, g, work, vstride, nb, eul,
-                                                              bands, mode, inv_p, accumulate,
-                                                              out);
+  k3t_x_out<<<dim3(ntiles(1LL * g.ny * g.nz), nb), kT3, sm, st>>>(
+      pl.d, g, work, vstride, eul, bands, mode, inv_p, part, accumulate, out);
   ++lc.n;
 }
 
-void launch3_z_mac(const FftPlan& pl, const Geo3& g, const float2* work, size_t vstride, int nb,
-                   const float2* spec, const int* sidx, float2* sum, cudaStream_t st,
-                   LaunchCounter& lc) {
-  smem_attr(k3_z_mac, pl.smem_bytes());
-  k3_z_mac<<<pairs(1LL * g.px * g.py), pl.d.nt, pl.smem_bytes(), st>>>(pl.d, g, work, vstride,
-                                                                       nb, spec, sidx, sum);
+void launch3_reduce_parts(const float2* part, int nb, size_t n, int accumulate, double2* out,
+                          cudaStream_t st, LaunchCounter& lc) {
+  k3_reduce_parts<<<grid_for(n, 256), 256, 0, st>>>(part, nb, n, accumulate, out);
+  ++lc.n;
+}
+
+void launch3_mac(const float2* work, int nb, size_t P, const float2* spec, const int* sidx,
+                 float2* sum, cudaStream_t st, LaunchCounter& lc) {
+  k3_mac<<<grid_for(P, 256), 256, 0, st>>>(work, nb, P, spec, sidx, sum);
   ++lc.n;
 }
 

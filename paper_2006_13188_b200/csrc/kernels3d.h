@@ -39,14 +39,18 @@ void launch3_x_filter(const FftPlan& pl, const Geo3& g, const float2* comps, int
 void launch3_z_load(const FftPlan& pl, const Geo3& g, const float2* Hh, const float2* spec,
                     const int* sidx, int nb, size_t vstride, int mode, float2* work,
                     cudaStream_t st, LaunchCounter& lc);
-// x-pass finishing the inverse, crop, conj(D_b) steering summed over nb bands
-// (mode 0) or plain (mode 1); out (+)= result, complex128
-void launch3_x_steer(const FftPlan& pl, const Geo3& g, const float2* work, size_t vstride,
-                     int nb, const double4* eul, const Band3* bands, int mode, int accumulate,
-                     double2* out, cudaStream_t st, LaunchCounter& lc);
-// z-pass of nb scatter bands, sum += FFT3(H D_b) V^_sidx[b]
-void launch3_z_mac(const FftPlan& pl, const Geo3& g, const float2* work, size_t vstride, int nb,
-                   const float2* spec, const int* sidx, float2* sum, cudaStream_t st,
-                   LaunchCounter& lc);
+// x-pass finishing an inverse, crop; mode 0: per-band planes part_b =
+// conj(D_b) G_b for nb bands; mode 1: out (+)= G (one volume)
+void launch3_x_out(const FftPlan& pl, const Geo3& g, const float2* work, size_t vstride, int nb,
+                   const double4* eul, const Band3* bands, int mode, float2* part,
+                   int accumulate, double2* out, cudaStream_t st, LaunchCounter& lc);
+// out (+)= sum of nb planes of n voxels (band order)
+void launch3_reduce_parts(const float2* part, int nb, size_t n, int accumulate, double2* out,
+                          cudaStream_t st, LaunchCounter& lc);
+// sum += sum_b work_b V^_sidx[b] over nb transformed scatter bands of P points
+void launch3_mac(const float2* work, int nb, size_t P, const float2* spec, const int* sidx,
+                 float2* sum, cudaStream_t st, LaunchCounter& lc);
+// dynamic shared memory of a 16-line tile CTA for line length L
+size_t tile3_smem(int L);
 
 }  // namespace xcb
