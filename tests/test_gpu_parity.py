@@ -627,3 +627,31 @@ def test_gather_hermitian_half_band(orc, n, batch, real_filter):
         xs = np.concatenate([r.integers(0, n, 30), [0, 0, n - 1, n - 1]])
         ref = orc.spectral_oracle_at(0, H[b], ROT, T[b], OF, ys, xs)
         assert orc.rel_l2(got[b][ys, xs], ref) < TOL
+
+
+def test_dual_i1_i2_batches_match_single_images(orc):
+    """XCB_DUAL=1 (opt-in): gather batches on the 4320 pad run I1 of image i and
+    I2 of image i-1 in one launch (k_dual_ilv).  Every image must equal its
+    single-image result bit for bit (host and device memory paths)."""
+    import subprocess
+    import sys
+    if os.environ.get("XCB_DUAL") != "1":
+        env = dict(os.environ, XCB_DUAL="1")
+        r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", __file__ +
+                            "::test_dual_i1_i2_batches_match_single_images"], env=env,
+                           capture_output=True, text=True)
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+        return
+    from paper_2006_13188_b200 import workloads as WL
+    wk = WL.config1(n=64)
+    r = np.random.default_rng(31)
+    n = 4100
+    H = r.uniform(0, 1, (3, n, n)).astype(np.float32)
+    T = r.uniform(0, 2 * np.pi, (3, n, n)).astype(np.float32)
+    batch = X.xcorr_fast(H, X.XformField.rotation(T), wk.filt).output
+    for b in range(3):
+        one = X.xcorr_fast(H[b], X.XformField.rotation(T[b]), wk.filt).output
+        assert np.array_equal(batch[b], one)
+    ys, xs = r.integers(0, n, 16), r.integers(0, n, 16)
+    ref = _direct_at(orc, ofilter(orc, wk.filt), H[2], T[2], ys, xs, False)
+    assert orc.rel_l2(batch[2][ys, xs], ref) < TOL
