@@ -166,6 +166,58 @@ __device__ float2* tile_fft(const FftPlanD& p, float2* A, float2* B, int Lp) {
   return src;
 }
 
+// The same transform with the first pass reading through load(line, n) and
+// the last pass writing through store(line, k, value) (global memory for the
+// y / z tiles, where the line-fast order is coalesced): one barrier per pass
+// boundary and no separate copy-in / copy-out.
+template <class Ld, class St>
+__device__ void tile_fft_io(const FftPlanD& p, float2* A, float2* B, int Lp, Ld&& load,
+                            St&& store) {
+  if (p.npass == 0) {  // L == 1
+    for (int line = threadIdx.x; line < kTL; line += blockDim.x) store(line, 0, load(line, 0));
+    return;
+  }
+  float2* src = A;
+  float2* dst = B;
+  for (int q = 0; q < p.npass; ++q) {
+    const bool first = q == 0, last = q == p.npass - 1;
+    radix_dispatch10(p.radix[q], [&](auto rc) {
+      constexpr int R = decltype(rc)::value;
+      const int nb = p.L / R, Ns = p.ns[q];
+      const float2* tw = p.tw + p.tw_off[q];
+      for (int w = threadIdx.x; w < kTL * nb; w += blockDim.x) {
+        const int line = w % kTL, j = w / kTL;
+        const int jm = first ? 0 : j - Ns * int(__umulhi(unsigned(j), p.magic[q]));
+        float2 v[R];
+        if (first) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) v[r] = load(line, j + r * nb);
+        } else {
+          const float2* s = src + line * Lp + j;
+#pragma unroll
+          for (int r = 0; r < R; ++r) v[r] = s[r * nb];
+#pragma unroll
+          for (int r = 1; r < R; ++r) v[r] = c_mul(v[r], __ldg(tw + (r - 1) * Ns + jm));
+        }
+        Dft<R>::run(v);
+        if (last) {  // Ns = L / R: output k = j + r nb
+#pragma unroll
+          for (int r = 0; r < R; ++r) store(line, j + r * nb, v[Dft<R>::pos(r)]);
+        } else {
+          float2* d = dst + line * Lp + (j - jm) * R + jm;
+#pragma unroll
+          for (int r = 0; r < R; ++r) d[r * Ns] = v[Dft<R>::pos(r)];
+        }
+      }
+    });
+    if (last) break;
+    __syncthreads();
+    float2* tmp = src;
+    src = dst;
+    dst = tmp;
+  }
+}
+
 // y / z tiles: 16 adjacent x at one (z) for axis 1, at one (y) for axis 2
 struct YZTile {
   int x0, c;
@@ -178,25 +230,6 @@ __device__ __forceinline__ YZTile yz_tile(const Geo3& g) {
   return YZTile{int(blockIdx.x % xt) * kTL, int(blockIdx.x / xt)};
 }
 
-// copy a y / z tile in / out line-fast: 16 adjacent x = 128 contiguous bytes
-template <class Ld>
-__device__ __forceinline__ void yz_load(const Geo3& g, int axis, const YZTile& t, int L,
-                                        float2* A, int Lp, Ld&& ld) {
-  for (int w = threadIdx.x; w < kTL * L; w += blockDim.x) {
-    const int line = w % kTL, n = w / kTL;
-    A[line * Lp + n] = t.x0 + line < g.px ? ld(t.base(g, axis, n) + line) : make_float2(0.f, 0.f);
-  }
-  __syncthreads();
-}
-template <class St>
-__device__ __forceinline__ void yz_store(const Geo3& g, int axis, const YZTile& t, int L,
-                                         const float2* Y, int Lp, St&& st) {
-  for (int w = threadIdx.x; w < kTL * L; w += blockDim.x) {
-    const int line = w % kTL, n = w / kTL;
-    if (t.x0 + line < g.px) st(t.base(g, axis, n) + line, Y[line * Lp + n]);
-  }
-}
-
 // in-place forward y- or z-pass of nvol volumes; grid (tiles, volume)
 __global__ void __launch_bounds__(kT3, 4) k3t_yz(FftPlanD p, Geo3 g, int axis,
                                               float2* __restrict__ buf, size_t vstride) {
@@ -206,9 +239,15 @@ __global__ void __launch_bounds__(kT3, 4) k3t_yz(FftPlanD p, Geo3 g, int axis,
   float2* B = sm + kTL * Lp;
   float2* v = buf + blockIdx.y * vstride;
   const YZTile t = yz_tile(g);
-  yz_load(g, axis, t, L, A, Lp, [&](size_t i) { return v[i]; });
-  const float2* Y = tile_fft(p, A, B, Lp);
-  yz_store(g, axis, t, L, Y, Lp, [&](size_t i, float2 x) { v[i] = x; });
+  const bool full = t.x0 + kTL <= g.px;
+  tile_fft_io(
+      p, A, B, Lp,
+      [&](int line, int n) {
+        return full || t.x0 + line < g.px ? v[t.base(g, axis, n) + line] : make_float2(0.f, 0.f);
+      },
+      [&](int line, int k, float2 x) {
+        if (full || t.x0 + line < g.px) v[t.base(g, axis, k) + line] = x;
+      });
 }
 
 // z-pass loading conj(H^) V^_sidx[b] (mode 0, gather) or conj(H^) (mode 1,
@@ -223,11 +262,16 @@ __global__ void __launch_bounds__(kT3, 4)
   const float2* V = mode == 0 ? spec + size_t(sidx[blockIdx.y]) * vstride : nullptr;
   float2* w = work + blockIdx.y * vstride;
   const YZTile t = yz_tile(g);
-  yz_load(g, 2, t, L, A, Lp, [&](size_t i) {
-    return mode == 0 ? c_mul(c_conj(Hh[i]), __ldg(V + i)) : c_conj(Hh[i]);
-  });
-  const float2* Y = tile_fft(p, A, B, Lp);
-  yz_store(g, 2, t, L, Y, Lp, [&](size_t i, float2 x) { w[i] = x; });
+  tile_fft_io(
+      p, A, B, Lp,
+      [&](int line, int n) {
+        if (t.x0 + line >= g.px) return make_float2(0.f, 0.f);
+        const size_t i = t.base(g, 2, n) + line;
+        return mode == 0 ? c_mul(c_conj(Hh[i]), __ldg(V + i)) : c_conj(Hh[i]);
+      },
+      [&](int line, int k, float2 x) {
+        if (t.x0 + line < g.px) w[t.base(g, 2, k) + line] = x;
+      });
 }
 
 // x tiles: rows li0 .. li0 + 15 of nl lines, copied in n-fast (contiguous)
