@@ -214,15 +214,15 @@ XCB_AM_KERNEL(k_anglemax_fft, 1)
 // Hermitian half-band angle max: for a real signal and a filter with
 // F_{-k} = conj(F_k) the band responses satisfy G_{-k} = conj(G_k), so
 // S(s) = sum_k G_k w^{ks} = G_0 + 2 Re(sum_{k=1}^{KH} G_k w^{ks}) is real and
-// only the planes k = 0..KH are needed (half the I1 / planes work); the
-// DFT_N2 carries KH nonzero inputs and only the real parts of its outputs
-// are used.  m.idx[k] = plane of band k (k = 0..KH).
+// only the planes k = 0..KH are needed (half the I1 / planes work), and one
+// complex DFT_N2 evaluates two rows s1 of real outputs.  m.idx[k] = plane of
+// band k (k = 0..KH).
 template <int KH, int N2, class TO>
 __global__ void __launch_bounds__(128)
     k_anglemax_herm(const float2* __restrict__ planes, AngleMap m, size_t npix,
                     TO* __restrict__ score, int* __restrict__ argmax) {
   constexpr int N = 360, N1 = N / N2;
-  static_assert(N1 * N2 == N && N2 > KH, "bad angle-max split");
+  static_assert(N1 * N2 == N && N2 > 2 * KH && N1 % 2 == 0, "bad angle-max split");
   __shared__ float2 tws[N1 * KH];  // w^{k s1}, [s1][k-1]
   for (int i = threadIdx.x; i < N1 * KH; i += blockDim.x) {
     const int s1 = i / KH, k = i % KH + 1;
@@ -240,21 +240,39 @@ __global__ void __launch_bounds__(128)
     G[k - 1] = m.idx[k] >= 0 ? planes[size_t(m.idx[k]) * npix + p] : make_float2(0.f, 0.f);
   float best = -1.f;
   int arg = 0;
+  // Two s1 per DFT: with X_k = G_k w^{k sa}, Y_k = G_k w^{k sb} (k = -KH..KH,
+  // X_{-k} = conj X_k) both DFTs are real, so DFT(X + iY) = S(sa + N1 s2) +
+  // i S(sb + N1 s2): one N2-point DFT per pair of s1 instead of two.
 #pragma unroll 1
-  for (int s1 = 0; s1 < N1; ++s1) {
+  for (int sa = 0; sa < N1; sa += 2) {
     float2 v[N2];
 #pragma unroll
     for (int q = 0; q < N2; ++q) v[q] = make_float2(0.f, 0.f);
-    const float2* tw = tws + s1 * KH;
+    v[0] = make_float2(g0, g0);
+    const float2* ta = tws + sa * KH;
+    const float2* tb = ta + KH;
 #pragma unroll
-    for (int k = 1; k <= KH; ++k) v[k] = c_mul(G[k - 1], tw[k - 1]);
+    for (int k = 1; k <= KH; ++k) {
+      const float2 x = c_mul(G[k - 1], ta[k - 1]), y = c_mul(G[k - 1], tb[k - 1]);
+      v[k] = make_float2(x.x - y.y, x.y + y.x);            // X_k + i Y_k
+      v[N2 - k] = make_float2(x.x + y.y, y.x - x.y);       // conj X_k + i conj Y_k
+    }
     Dft<N2>::run(v);
+    // scan in the s1-major order (sa, then sb): the first maximum wins
 #pragma unroll
     for (int s2 = 0; s2 < N2; ++s2) {
-      const float a = fabsf(fmaf(2.f, v[Dft<N2>::pos(s2)].x, g0));
+      const float a = fabsf(v[Dft<N2>::pos(s2)].x);
       if (a > best) {
         best = a;
-        arg = s1 + N1 * s2;
+        arg = sa + N1 * s2;
+      }
+    }
+#pragma unroll
+    for (int s2 = 0; s2 < N2; ++s2) {
+      const float a = fabsf(v[Dft<N2>::pos(s2)].y);
+      if (a > best) {
+        best = a;
+        arg = sa + 1 + N1 * s2;
       }
     }
   }
