@@ -404,11 +404,6 @@ __global__ void k3_mac(const float2* __restrict__ work, int nb, size_t P,
   }
 }
 
-template <class K>
-void smem_attr(K k, size_t bytes) {
-  if (bytes > 48 * 1024)
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
-}
 
 size_t tile_smem(int L) { return 2 * size_t(kTL) * tile_stride(L) * sizeof(float2); }
 unsigned ntiles(long long lines) { return unsigned((lines + kTL - 1) / kTL); }
@@ -435,7 +430,7 @@ void launch3_euler(const double* quats, size_t n, double4* eul, cudaStream_t st,
 void launch3_pass(const FftPlan& pl, const Geo3& g, int axis, float2* buf, size_t vstride,
                   int nvol, cudaStream_t st, LaunchCounter& lc) {
   const size_t sm = tile_smem(pl.d.L);
-  smem_attr(k3t_yz, sm);
+  set_smem(k3t_yz, sm);
   k3t_yz<<<dim3(yz_tiles(g, axis), nvol), kT3, sm, st>>>(pl.d, g, axis, buf, vstride);
   ++lc.n;
 }
@@ -444,7 +439,7 @@ void launch3_x_signal(const FftPlan& pl, const Geo3& g, const float2* sig, const
                       const Band3* bands, int nb, int premul, float2* work, size_t vstride,
                       cudaStream_t st, LaunchCounter& lc) {
   const size_t sm = tile_smem(pl.d.L);
-  smem_attr(k3t_x_signal, sm);
+  set_smem(k3t_x_signal, sm);
   k3t_x_signal<<<dim3(ntiles(1LL * g.py * g.pz), nb), kT3, sm, st>>>(pl.d, g, sig, eul, bands,
                                                                      premul, work, vstride);
   ++lc.n;
@@ -453,7 +448,7 @@ void launch3_x_signal(const FftPlan& pl, const Geo3& g, const float2* sig, const
 void launch3_x_filter(const FftPlan& pl, const Geo3& g, const float2* comps, int nb,
                       float2* spec, size_t vstride, cudaStream_t st, LaunchCounter& lc) {
   const size_t sm = tile_smem(pl.d.L);
-  smem_attr(k3t_x_filter, sm);
+  set_smem(k3t_x_filter, sm);
   k3t_x_filter<<<dim3(ntiles(1LL * g.py * g.pz), nb), kT3, sm, st>>>(pl.d, g, comps, spec,
                                                                      vstride);
   ++lc.n;
@@ -463,7 +458,7 @@ void launch3_z_load(const FftPlan& pl, const Geo3& g, const float2* Hh, const fl
                     const int* sidx, int nb, size_t vstride, int mode, float2* work,
                     cudaStream_t st, LaunchCounter& lc) {
   const size_t sm = tile_smem(pl.d.L);
-  smem_attr(k3t_z_load, sm);
+  set_smem(k3t_z_load, sm);
   k3t_z_load<<<dim3(yz_tiles(g, 2), nb), kT3, sm, st>>>(pl.d, g, Hh, spec, sidx, vstride, mode,
                                                         work);
   ++lc.n;
@@ -473,7 +468,7 @@ void launch3_x_out(const FftPlan& pl, const Geo3& g, const float2* work, size_t 
                    const double4* eul, const Band3* bands, int mode, float2* part,
                    int accumulate, double2* out, cudaStream_t st, LaunchCounter& lc) {
   const size_t sm = tile_smem(pl.d.L);
-  smem_attr(k3t_x_out, sm);
+  set_smem(k3t_x_out, sm);
   const float inv_p = float(1.0 / (double(g.px) * g.py * g.pz));
   k3t_x_out<<<dim3(ntiles(1LL * g.ny * g.nz), nb), kT3, sm, st>>>(
       pl.d, g, work, vstride, eul, bands, mode, inv_p, part, accumulate, out);

@@ -1,5 +1,8 @@
 // Shared device helpers of the pipeline stages (included by k_*.cu).
 #pragma once
+#include <map>
+#include <mutex>
+#include <utility>
 #include "fft_core.cuh"
 #include "kernels.h"
 
@@ -67,10 +70,22 @@ __device__ __forceinline__ float2 dc_term(const SigSrc& s, size_t i, double dr, 
 }
 
 // ------------------------------------------------------------------ launch helpers
+// Raise a kernel's dynamic shared memory limit once per (device, kernel) and
+// size: the attribute call costs a driver round trip on every launch otherwise.
 template <class K>
 void set_smem(K kernel, size_t bytes) {
-  if (bytes > 48 * 1024)
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+  if (bytes <= 48 * 1024) return;
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_pair(dev, reinterpret_cast<const void*>(kernel));
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = done[key];
+  if (have >= bytes) return;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)) ==
+      cudaSuccess)
+    have = bytes;
 }
 
 int grid_for(size_t n, int bs) {
