@@ -23,6 +23,8 @@
 // The Wigner entry D = e^{-i(m' alpha + m gamma)} d^l_{m' m}(beta) is
 // evaluated in fp64 from the voxel's (alpha, gamma, cos beta/2, sin beta/2)
 // with the band's Horner coefficients (host_sph.h SmallD).
+#include <algorithm>
+
 #include "kernels3d.h"
 #include "stages_common.cuh"
 
@@ -406,6 +408,14 @@ __global__ void k3_mac(const float2* __restrict__ work, int nb, size_t P,
 
 
 size_t tile_smem(int L) { return 2 * size_t(kTL) * tile_stride(L) * sizeof(float2); }
+// threads of a tile CTA: one per butterfly of the widest pass (16 lines x
+// L / R), so short lines do not leave half the CTA idle
+int tile_threads(const FftPlanD& p) {
+  int nb = 1;
+  for (int q = 0; q < p.npass; ++q) nb = std::max(nb, p.L / p.radix[q]);
+  const int t = (kTL * nb + 31) / 32 * 32;
+  return std::min(kT3, std::max(64, t));
+}
 unsigned ntiles(long long lines) { return unsigned((lines + kTL - 1) / kTL); }
 unsigned yz_tiles(const Geo3& g, int axis) {
   return unsigned((g.px + kTL - 1) / kTL) * unsigned(axis == 1 ? g.pz : g.py);
@@ -431,7 +441,7 @@ void launch3_pass(const FftPlan& pl, const Geo3& g, int axis, float2* buf, size_
                   int nvol, cudaStream_t st, LaunchCounter& lc) {
   const size_t sm = tile_smem(pl.d.L);
   set_smem(k3t_yz, sm);
-  k3t_yz<<<dim3(yz_tiles(g, axis), nvol), kT3, sm, st>>>(pl.d, g, axis, buf, vstride);
+  k3t_yz<<<dim3(yz_tiles(g, axis), nvol), tile_threads(pl.d), sm, st>>>(pl.d, g, axis, buf, vstride);
   ++lc.n;
 }
 
@@ -440,7 +450,7 @@ void launch3_x_signal(const FftPlan& pl, const Geo3& g, const float2* sig, const
                       cudaStream_t st, LaunchCounter& lc) {
   const size_t sm = tile_smem(pl.d.L);
   set_smem(k3t_x_signal, sm);
-  k3t_x_signal<<<dim3(ntiles(1LL * g.py * g.pz), nb), kT3, sm, st>>>(pl.d, g, sig, eul, bands,
+  k3t_x_signal<<<dim3(ntiles(1LL * g.py * g.pz), nb), tile_threads(pl.d), sm, st>>>(pl.d, g, sig, eul, bands,
                                                                      premul, work, vstride);
   ++lc.n;
 }
@@ -449,7 +459,7 @@ void launch3_x_filter(const FftPlan& pl, const Geo3& g, const float2* comps, int
                       float2* spec, size_t vstride, cudaStream_t st, LaunchCounter& lc) {
   const size_t sm = tile_smem(pl.d.L);
   set_smem(k3t_x_filter, sm);
-  k3t_x_filter<<<dim3(ntiles(1LL * g.py * g.pz), nb), kT3, sm, st>>>(pl.d, g, comps, spec,
+  k3t_x_filter<<<dim3(ntiles(1LL * g.py * g.pz), nb), tile_threads(pl.d), sm, st>>>(pl.d, g, comps, spec,
                                                                      vstride);
   ++lc.n;
 }
@@ -459,7 +469,7 @@ void launch3_z_load(const FftPlan& pl, const Geo3& g, const float2* Hh, const fl
                     cudaStream_t st, LaunchCounter& lc) {
   const size_t sm = tile_smem(pl.d.L);
   set_smem(k3t_z_load, sm);
-  k3t_z_load<<<dim3(yz_tiles(g, 2), nb), kT3, sm, st>>>(pl.d, g, Hh, spec, sidx, vstride, mode,
+  k3t_z_load<<<dim3(yz_tiles(g, 2), nb), tile_threads(pl.d), sm, st>>>(pl.d, g, Hh, spec, sidx, vstride, mode,
                                                         work);
   ++lc.n;
 }
@@ -470,7 +480,7 @@ void launch3_x_out(const FftPlan& pl, const Geo3& g, const float2* work, size_t 
   const size_t sm = tile_smem(pl.d.L);
   set_smem(k3t_x_out, sm);
   const float inv_p = float(1.0 / (double(g.px) * g.py * g.pz));
-  k3t_x_out<<<dim3(ntiles(1LL * g.ny * g.nz), nb), kT3, sm, st>>>(
+  k3t_x_out<<<dim3(ntiles(1LL * g.ny * g.nz), nb), tile_threads(pl.d), sm, st>>>(
       pl.d, g, work, vstride, eul, bands, mode, inv_p, part, accumulate, out);
   ++lc.n;
 }
