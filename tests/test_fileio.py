@@ -257,3 +257,34 @@ def test_cli_xcorr_xconv_smooth_match_oracle(tmp_path, orc):
     lo, hi = side["normalization"]["min"], side["normalization"]["max"]
     assert abs(lo - ref.min()) < 1e-5 * abs(ref).max() and abs(hi - ref.max()) < 1e-5 * abs(ref).max()
     assert np.abs(io.read_pgm(o) - (ref - lo) / (hi - lo)).max() <= 0.5 / 255 + 1e-5
+
+
+@pytest.mark.gpu
+def test_cli_detect_matches_api(tmp_path):
+    """xconv_cli.cpp:348-405: `detect` writes the vote response, a sidecar with the
+    peaks, and the peaks CSV; the peaks equal detect_pattern's on the same inputs."""
+    from paper_2006_13188_b200.workloads import paste_rotated
+    R = 8
+    y, x = np.mgrid[-R:R + 1, -R:R + 1].astype(np.float64)
+    pat = np.exp(-((x - 2) ** 2 + (y + 1) ** 2) / 4.0) - 0.7 * np.exp(-((x + 3) ** 2 + y ** 2) / 3.0)
+    img = np.zeros((96, 110))
+    paste_rotated(img, pat, 30.0, 40.0, 0.6)
+    paste_rotated(img, pat, 75.0, 62.0, -1.9)
+    img += np.random.default_rng(4).normal(0, 0.01, img.shape)
+    p_img, p_pat = str(tmp_path / "img.pfm"), str(tmp_path / "pat.pfm")
+    io.write_pfm(p_img, img)
+    io.write_pfm(p_pat, pat)
+    out, csvp = str(tmp_path / "resp.pfm"), str(tmp_path / "peaks.csv")
+    assert cli.main(["detect", "--image", p_img, "--pattern", p_pat, "--K", "12", "--output", out,
+                     "--peaks-csv", csvp]) == 0
+    img32, pat32 = io.read_pfm_field(p_img).real, io.read_pfm_field(p_pat).real
+    # the CLI's defaults: centre (w-1)/2, eps = min(w, h)/2 (xconv_cli.cpp:374-377)
+    vf = X.build_optimal_filter(pat32, R, R, (2 * R + 1) / 2.0)
+    det = X.detect_pattern(img32, vf, 12)
+    side = json.load(open(out + ".json"))
+    assert side["counters"]["peaks"] == len(det.peaks) >= 2
+    assert [(p["x"], p["y"]) for p in side["peaks"]] == [(p.x, p.y) for p in det.peaks]
+    rows = [l.split(",") for l in open(csvp).read().split()]
+    assert [(int(a), int(b)) for a, b, _ in rows] == [(p.x, p.y) for p in det.peaks]
+    resp = io.read_pfm_field(out).real
+    assert np.abs(resp - det.response).max() <= 1e-6 * np.abs(det.response).max()
