@@ -13,6 +13,8 @@
 //                                                <- vote_filter.hpp:83-91
 //   xconv::gpu::detect_pattern(I, vf, K, n_radii, n_angles)
 //                                                <- vote_filter.hpp:146-168
+//   xconv::gpu::xcorr_fast_3d / xconv_fast_3d(H, T, F, plan)
+//                                                <- engine3d.hpp:270-335
 //
 // Eigen's default column-major storage (field.hpp:15) is passed as
 // XC_COL_MAJOR with the caller's complex<double> / double buffers
@@ -281,6 +283,69 @@ Result detect_pattern(const Field& image, const VF& filter, int K, int n_radii =
     out.peaks.push_back(pk);
   }
   return out;
+}
+
+// engine3d.hpp:270-335 (Field3<Real>: nx, ny, nz, values x fastest;
+// XformField<Real>: kind, nx, ny, nz, quats with w() x() y() z();
+// SphFilter3<Real>: K, n_radii, r_max, coeffs (n_radii x (K+1)^2, Eigen
+// column-major); Response3<Real>: output, plan, standard_ops, seconds)
+namespace detail {
+
+template <class Result, class Field3T, class Xform, class SphF, class Plan>
+Result run3(int mode, const Field3T& H, const Xform& T, const SphF& F, Plan plan) {
+  if (T.nx != H.nx || T.ny != H.ny || T.nz != H.nz)  // engine3d.hpp:274-275
+    throw std::invalid_argument("signal and transformation field dims differ");
+  Context& c = context();
+  const size_t n = H.values.size();
+  std::vector<double> sig(2 * n), q(4 * n), out(2 * n);
+  for (size_t i = 0; i < n; ++i) {
+    sig[2 * i] = double(std::real(H.values[i]));
+    sig[2 * i + 1] = double(std::imag(H.values[i]));
+    const auto& qq = T.quats[i];
+    q[4 * i] = double(qq.w());
+    q[4 * i + 1] = double(qq.x());
+    q[4 * i + 2] = double(qq.y());
+    q[4 * i + 3] = double(qq.z());
+  }
+  const int rows = static_cast<int>(F.coeffs.rows()), cols = static_cast<int>(F.coeffs.cols());
+  std::vector<double> co(size_t(2) * rows * cols);
+  for (int cc = 0; cc < cols; ++cc)
+    for (int r = 0; r < rows; ++r) {
+      co[2 * (size_t(cc) * rows + r)] = double(std::real(F.coeffs(r, cc)));
+      co[2 * (size_t(cc) * rows + r) + 1] = double(std::imag(F.coeffs(r, cc)));
+    }
+  xc_filter3 f = nullptr;
+  check(xc_filter3_create(F.K, F.n_radii, double(F.r_max), co.data(), &f), nullptr);
+  std::unique_ptr<xc_filter3_s, void (*)(xc_filter3)> guard(f, xc_filter3_destroy);
+  std::vector<int> deg(plan.components.begin(), plan.components.end());
+  xc_stats st{};
+  check(xc_run3(c.ctx, f, mode, H.nx, H.ny, H.nz, sig.data(), XC_C128, q.data(),
+                deg.empty() ? nullptr : deg.data(), int(deg.size()), XC_HOST, out.data(), &st),
+        c.ctx);
+  Result res;
+  res.plan = plan;
+  res.standard_ops = st.standard_ops;
+  res.seconds["fft"] = st.seconds_fft;
+  res.seconds["total"] = st.seconds_total;
+  res.output = decltype(res.output)(H.nx, H.ny, H.nz);
+  for (size_t i = 0; i < n; ++i)
+    res.output.values[i] = typename decltype(res.output.values)::value_type(out[2 * i],
+                                                                           out[2 * i + 1]);
+  return res;
+}
+
+}  // namespace detail
+
+template <class Result, class Field3T, class Xform, class SphF, class Plan>
+Result xcorr_fast_3d(const Field3T& H, const Xform& T, const SphF& F, Plan plan) {
+  plan.mode = decltype(plan.mode)(0);
+  return detail::run3<Result>(XC_CORRELATION, H, T, F, plan);
+}
+
+template <class Result, class Field3T, class Xform, class SphF, class Plan>
+Result xconv_fast_3d(const Field3T& H, const Xform& T, const SphF& F, Plan plan) {
+  plan.mode = decltype(plan.mode)(1);
+  return detail::run3<Result>(XC_CONVOLUTION, H, T, F, plan);
 }
 
 }  // namespace gpu

@@ -143,6 +143,21 @@ void or_random_scale_field(void* rng, int w, int h, double lo, double hi,
 uint64_t or_rng_next(void* rng);
 double or_rng_uniform(void* rng, double a, double b);
 
+
+/* ---- 3D rotation pipeline (xconv_oracle3d.inc; sph.hpp, wigner.hpp,
+ * engine3d.hpp).  Volumes x fastest, complex interleaved; quaternions
+ * (w, x, y, z); SphFilter3 coefficients row-major [shell][l(l+1)+m]. */
+int or_decompose_rotation3(const double* vol, int nx, int ny, int nz, double cx, double cy,
+                           double cz, int K, int n_radii, double r_max, int n_theta, int n_phi,
+                           double* coeffs_out);
+int or_xfast3(int mode, const double* H, int nx, int ny, int nz, const double* quats, int K,
+              int n_radii, double r_max, const double* coeffs, const int* degrees, int ndeg,
+              double* out, long long* ops);
+void or_random_field3(void* rng, int nx, int ny, int nz, int complex_valued, double* out);
+void or_random_smooth_filter3(void* rng, int radius, int n_bumps, double envelope_frac,
+                              double* out);
+void or_random_rotation3_field(void* rng, int n, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -37,9 +37,28 @@ struct Field2 {
 };
 
 template <class Real>
+struct Field3 {  // field.hpp:66-85: x fastest
+  int nx = 0, ny = 0, nz = 0;
+  std::vector<std::complex<Real>> values;
+  Field3() = default;
+  Field3(int x, int y, int z) : nx(x), ny(y), nz(z), values(size_t(x) * y * z) {}
+};
+
+template <class Real>
+struct Quaternion {  // the accessors of Eigen::Quaternion
+  Real qw = 1, qx = 0, qy = 0, qz = 0;
+  Real w() const { return qw; }
+  Real x() const { return qx; }
+  Real y() const { return qy; }
+  Real z() const { return qz; }
+};
+
+template <class Real>
 struct XformField {
   XformKind kind = XformKind::rotation2;
   Grid<Real> angle, scale;
+  int nx = 0, ny = 0, nz = 0;
+  std::vector<Quaternion<Real>> quats;
   int width() const { return kind == XformKind::scale2 ? scale.cols() : angle.cols(); }
   int height() const { return kind == XformKind::scale2 ? scale.rows() : angle.rows(); }
 };
@@ -54,6 +73,13 @@ struct FreqFilter2 {
   Real r_max = 0, r_min = 0, r_domain = 0;
 };
 
+template <class Real>
+struct SphFilter3 {  // sph.hpp:130-157
+  int K = 0, n_radii = 0;
+  Real r_max = 0;
+  Grid<std::complex<Real>> coeffs;  // (n_radii, (K+1)^2)
+};
+
 struct XConvPlan {
   XMode mode = XMode::correlation;
   XformKind group = XformKind::rotation2;
@@ -64,6 +90,14 @@ struct XConvPlan {
 template <class Real>
 struct Response2 {
   Field2<Real> output;
+  XConvPlan plan;
+  long long standard_ops = 0;
+  std::map<std::string, double> seconds;
+};
+
+template <class Real>
+struct Response3 {  // engine.hpp:31-37
+  Field3<Real> output;
   XConvPlan plan;
   long long standard_ops = 0;
   std::map<std::string, double> seconds;

@@ -150,5 +150,61 @@ int main() {
                 ok ? "ok" : "FAIL");
     fails += !ok;
   }
+  // 3D rotation (engine3d.hpp:270-335) through the shim vs the oracle
+  {
+    void* rg = or_rng_new(83);
+    const int R3 = 2, K3 = 2, nx = 7, ny = 6, nz = 5, S3 = 2 * R3 + 1, nc3 = (K3 + 1) * (K3 + 1);
+    std::vector<double> vol(2 * size_t(S3) * S3 * S3), c3(2 * size_t(2 * R3) * nc3);
+    or_random_smooth_filter3(rg, R3, 6, 0.4, vol.data());
+    if (or_decompose_rotation3(vol.data(), S3, S3, S3, R3, R3, R3, K3, 2 * R3, double(R3), 12, 12,
+                               c3.data()) != 0)
+      return 5;
+    SphFilter3<double> F3;
+    F3.K = K3;
+    F3.n_radii = 2 * R3;
+    F3.r_max = R3;
+    F3.coeffs = Grid<std::complex<double>>(2 * R3, nc3);
+    for (int j = 0; j < 2 * R3; ++j)
+      for (int c = 0; c < nc3; ++c)
+        F3.coeffs(j, c) = cd(c3[2 * (size_t(j) * nc3 + c)], c3[2 * (size_t(j) * nc3 + c) + 1]);
+    const size_t n3 = size_t(nx) * ny * nz;
+    std::vector<double> h3(2 * n3), q3(4 * n3);
+    or_random_field3(rg, nx, ny, nz, 1, h3.data());
+    or_random_rotation3_field(rg, int(n3), q3.data());
+    or_rng_free(rg);
+    Field3<double> H3(nx, ny, nz);
+    XformField<double> T3;
+    T3.kind = XformKind::rotation3;
+    T3.nx = nx;
+    T3.ny = ny;
+    T3.nz = nz;
+    for (size_t i = 0; i < n3; ++i) {
+      H3.values[i] = cd(h3[2 * i], h3[2 * i + 1]);
+      T3.quats.push_back({q3[4 * i], q3[4 * i + 1], q3[4 * i + 2], q3[4 * i + 3]});
+    }
+    for (int mode = 0; mode < 2; ++mode) {
+      XConvPlan plan;
+      plan.group = XformKind::rotation3;
+      Response3<double> r = mode == 0
+                                ? xconv::gpu::xcorr_fast_3d<Response3<double>>(H3, T3, F3, plan)
+                                : xconv::gpu::xconv_fast_3d<Response3<double>>(H3, T3, F3, plan);
+      std::vector<double> ref(2 * n3);
+      long long ops = 0;
+      if (or_xfast3(mode, h3.data(), nx, ny, nz, q3.data(), K3, 2 * R3, double(R3), c3.data(),
+                    nullptr, 0, ref.data(), &ops) != 0)
+        return 6;
+      std::vector<cd> a(n3), b(n3);
+      for (size_t i = 0; i < n3; ++i) {
+        a[i] = r.output.values[i];
+        b[i] = cd(ref[2 * i], ref[2 * i + 1]);
+      }
+      const double e = rel(a, b);
+      const bool ok = e < 1e-5 && r.standard_ops == ops && ops == 35 &&
+                      r.plan.mode == (mode ? XMode::convolution : XMode::correlation);
+      std::printf("3D mode %d: rel_l2 %.3e ops %lld %s\n", mode, e, r.standard_ops,
+                  ok ? "ok" : "FAIL");
+      fails += !ok;
+    }
+  }
   return fails ? 1 : 0;
 }

@@ -32,4 +32,4 @@ def test_shim_end_to_end_on_gpu(orc):
     r = subprocess.run([BIN], capture_output=True, text=True, timeout=300)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count(" ok") == 6
+    assert r.stdout.count(" ok") == 8
