@@ -84,6 +84,8 @@ struct xc_context_s {
   std::map<int, PlanEntry> plans;
   std::map<int, PlanEntry> fast_plans;  // L -> in-place radix-16-last plan (or tw == null)
   std::map<std::string, DevBuf> bufs;
+  // detect_pattern's decomposed vote filters, by content (xc_detect_pattern)
+  std::map<uint64_t, std::unique_ptr<xc_filter_s, void (*)(xc_filter_s*)>> det_filters;
   // events reused across calls (HostPipe slots, call timing)
   std::vector<cudaEvent_t> ev_sync, ev_timing;
   size_t ev_sync_used = 0, ev_timing_used = 0;
@@ -1463,9 +1465,26 @@ int xc_detect_pattern(xc_context ctx, const xc_image_desc* d, const void* image,
         vf[size_t(y) * side + x] = cplx(
             vote_weights[d->layout == XC_COL_MAJOR ? size_t(x) * side + y : size_t(y) * side + x],
             0.0);
-    auto f = std::make_unique<xc_filter_s>();
-    f->hf = xcb::decompose_rotation2(xcb::ImageView{vf.data(), side, side}, double(R), double(R),
-                                     K, n_radii, n_angles, double(R) + 0.5);
+    // the decomposed vote filter (and its device spectra) is cached per
+    // context by content, so repeated detections with one pattern reuse it
+    uint64_t key = 1469598103934665603ull;
+    auto mix = [&](const void* p, size_t n) {
+      const unsigned char* b = static_cast<const unsigned char*>(p);
+      for (size_t i = 0; i < n; ++i) key = (key ^ b[i]) * 1099511628211ull;
+    };
+    mix(vf.data(), vf.size() * sizeof(cplx));
+    const int params[4] = {R, K, n_radii, n_angles};
+    mix(params, sizeof(params));
+    auto it = ctx->det_filters.find(key);
+    if (it == ctx->det_filters.end()) {
+      if (ctx->det_filters.size() >= 4) ctx->det_filters.clear();
+      std::unique_ptr<xc_filter_s, void (*)(xc_filter_s*)> nf(new xc_filter_s(),
+                                                              xc_filter_destroy);
+      nf->hf = xcb::decompose_rotation2(xcb::ImageView{vf.data(), side, side}, double(R),
+                                        double(R), K, n_radii, n_angles, double(R) + 0.5);
+      it = ctx->det_filters.emplace(key, std::move(nf)).first;
+    }
+    xc_filter_s* f = it->second.get();
     // device: gradient of the image
     cudaStream_t st = ctx->stream;
     xcb::LaunchCounter lc;
@@ -1485,7 +1504,7 @@ int xc_detect_pattern(xc_context ctx, const xc_image_desc* d, const void* image,
     float2* out = ctx->buf<float2>("det_out", npix);
     xc_image_desc dd{h, w, 1, XC_F32, XC_F32, XC_C64, d->layout, XC_DEVICE, 1, XC_ROTATION2};
     xc_stats rs{};
-    if (xc_run(ctx, f.get(), XC_CONVOLUTION, &dd, mag, dir, nullptr, 0, 0, out, &rs) != XC_OK)
+    if (xc_run(ctx, f, XC_CONVOLUTION, &dd, mag, dir, nullptr, 0, 0, out, &rs) != XC_OK)
       throw std::runtime_error(ctx->err);
     // response = Re(out); NMS on the host
     void* dresp = d->memory == XC_DEVICE ? response : ctx->buf<char>("det_resp", npix * os);
