@@ -897,6 +897,7 @@ int xc_context_trim(xc_context ctx) {
     ck(cudaStreamSynchronize(ctx->stream), "sync");
     for (auto& kv : ctx->bufs) cudaFree(kv.second.p);
     ctx->bufs.clear();
+    ctx->det_filters.clear();  // their cached spectra
   });
 }
 
