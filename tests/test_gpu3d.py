@@ -185,3 +185,30 @@ def test_fast_3d_larger_volume_higher_band_limit(orc):
         ref, ops = orc.xfast3(mode, H, q, F)
         assert r.standard_ops == ops == 165
         assert orc.rel_l2(r.output, ref) < TOL, (mode, orc.rel_l2(r.output, ref))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("XCB_FUZZ_CASES", "12"))))
+def test_fast_3d_random_cases(orc, seed):
+    """Random 3D geometries (ragged, thin), degree limits, degree subsets, real and
+    complex signals against the oracle."""
+    r = np.random.default_rng([seed, 3003])
+    R = int(r.integers(1, 5))
+    K = int(r.integers(0, 5))
+    nx, ny, nz = (int(v) for v in r.integers(1, 18, 3))
+    rng = orc.Rng(1000 + seed)
+    F, G = _filters(orc, rng.random_smooth_filter3(R), R, K)
+    cplx = bool(r.random() < 0.5)
+    H = rng.random_field3(nx, ny, nz, cplx)
+    q = rng.random_rotation3_field(nx, ny, nz)
+    degrees = None
+    if K > 0 and r.random() < 0.4:
+        degrees = sorted(r.choice(np.arange(K + 1), size=int(r.integers(1, K + 2)),
+                                  replace=False).tolist())
+    plan = X.XConvPlan(components=degrees or [])
+    for mode, fn in ((0, X.xcorr_fast_3d), (1, X.xconv_fast_3d)):
+        got = fn(H if cplx else H.real, X.rotation3d(q), G, plan)
+        ref, ops = orc.xfast3(mode, H, q, F, degrees=degrees)
+        assert got.standard_ops == ops
+        err = orc.rel_l2(got.output, ref)
+        assert err < TOL, (seed, mode, (nx, ny, nz), R, K, degrees, err)
