@@ -47,7 +47,8 @@ __device__ __forceinline__ void park_last_tw(const float2* __restrict__ twf, uin
 // images (the filter spectrum is image-independent, so its HBM read is shared).
 // Per (band, image): two barriers (after pass 0, after pass 1).
 template <class PF, int NI>
-__device__ __forceinline__ void i1_body(int c, const Geo& g, const float4* __restrict__ Hh,
+__device__ __forceinline__ void i1_body(int c, int b0, int b1, const Geo& g,
+                                        const float4* __restrict__ Hh,
                                         size_t hstride4, const float4* __restrict__ Fh,
                                         size_t sstride4, const Bands& bl,
                                         float2* __restrict__ T2, size_t tstride,
@@ -76,8 +77,8 @@ __device__ __forceinline__ void i1_body(int c, const Geo& g, const float4* __res
     mbar_init(&bar, 1);
     fence_mbar_init();
     mbar_expect_tx(&bar, kBytes);
-    bulk_copy(ST4, fsrc(0), kBytes, &bar);
-    if (bl.n > 1) prefetch_l2(fsrc(1), kBytes);
+    bulk_copy(ST4, fsrc(b0), kBytes, &bar);
+    if (b0 + 1 < b1) prefetch_l2(fsrc(b0 + 1), kBytes);
   }
   // conj(H^) at this thread's pass-0 inputs n = j + r NB0, parked in TMEM
   // (2 columns per r and image; warps of a lane quadrant side by side)
@@ -104,7 +105,7 @@ __device__ __forceinline__ void i1_body(int c, const Geo& g, const float4* __res
   for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
   __syncthreads();
   unsigned phase = 0;
-  for (int bi = 0; bi < bl.n; ++bi) {
+  for (int bi = b0; bi < b1; ++bi) {
     mbar_wait(&bar, phase);
     phase ^= 1;
 #pragma unroll 1
@@ -122,11 +123,11 @@ __device__ __forceinline__ void i1_body(int c, const Geo& g, const float4* __res
         PF::pass0_store(W0, v);
       }
       __syncthreads();
-      if (t == 0 && im == NI - 1 && bi + 1 < bl.n) {
+      if (t == 0 && im == NI - 1 && bi + 1 < b1) {
         fence_proxy_async();
         mbar_expect_tx(&bar, kBytes);
         bulk_copy(ST4, fsrc(bi + 1), kBytes, &bar);
-        if (bi + 2 < bl.n) prefetch_l2(fsrc(bi + 2), kBytes);
+        if (bi + 2 < b1) prefetch_l2(fsrc(bi + 2), kBytes);
       }
       PF::pass1(W0, W1, TWs);
       __syncthreads();
@@ -168,8 +169,19 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
     k_cols_inv_corr_ilv(Geo g, const float4* __restrict__ Hh, size_t hstride4,
                         const float4* __restrict__ Fh, size_t sstride4, Bands bl,
                         float2* __restrict__ T2, size_t tstride,
-                        const float2* __restrict__ twm, const float2* __restrict__ twf) {
-  i1_body<PF, NI>(blockIdx.x, g, Hh, hstride4, Fh, sstride4, bl, T2, tstride, twm, twf);
+                        const float2* __restrict__ twm, const float2* __restrict__ twf,
+                        int full, int split) {
+  // CTAs below `full` run every band of column pair blockIdx.x; the column
+  // pairs of the last, partial wave are split into `split` band chunks so the
+  // tail spreads over all SMs (CTAs are dispatched in blockIdx order)
+  int c = blockIdx.x, b0 = 0, b1 = bl.n;
+  if (c >= full) {
+    const int u = c - full, ch = u % split;
+    c = full + u / split;
+    b0 = ch * bl.n / split;
+    b1 = (ch + 1) * bl.n / split;
+  }
+  i1_body<PF, NI>(c, b0, b1, g, Hh, hstride4, Fh, sstride4, bl, T2, tstride, twm, twf);
 }
 
 // ------------------------------------------------------------------ I2 (interleaved)
@@ -403,7 +415,7 @@ __global__ void __launch_bounds__(PF::T, 1)
     item = x - m;
   }
   if (first)
-    i1_body<PF, 1>(item, g, a.Hh, 0, a.Fh, a.sstride4, a.bl, a.T2, 0, twm, twf);
+    i1_body<PF, 1>(item, 0, a.bl.n, g, a.Hh, 0, a.Fh, a.sstride4, a.bl, a.T2, 0, twm, twf);
   else
     i2_body<PF, TO>(item, g, b.T2, b.bl, b.half, b.base, b.out, b.accumulate, b.dcs, b.dcr, b.dci,
                     b.scale, twm, twl);
@@ -968,24 +980,64 @@ int pair_i1_images() {
     default: break;                                                                \
   }
 
+// Grid of a band-loop kernel over `units` independent units (column pairs)
+// with `per_sm` resident CTAs per SM: whole waves run every band; the units of
+// the last, partial wave are split into band chunks so that the tail fills
+// the SMs.  The split minimises ceil(rem * s / slots) * (ceil(nb / s) + 1)
+// (one band-equivalent of per-CTA setup per chunk).  XCB_TAIL_SPLIT=0 turns
+// it off.
+struct TailSplit {
+  int grid, full, split;
+};
+TailSplit tail_split(int units, int per_sm, int nb) {
+  static const int sms = [] {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+  }();
+  static const bool off = [] {
+    const char* e = std::getenv("XCB_TAIL_SPLIT");
+    return e && e[0] == '0';
+  }();
+  const int slots = sms * per_sm;
+  const int full = units / slots * slots, rem = units - full;
+  if (off || rem == 0 || full == 0 || nb < 4) return {units, units, 1};
+  int best = 1;
+  long best_cost = long(nb) + 1;
+  for (int s = 2; s <= nb / 2; ++s) {
+    const long waves = (long(rem) * s + slots - 1) / slots;
+    const long cost = waves * ((nb + s - 1) / s + 1);
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = s;
+    }
+  }
+  return {full + rem * best, full, best};
+}
+
 void launch_cols_inv_corr_pair(const Geo& g, const float2* Hhat, const float2* Fhat,
                                size_t sstride, const Bands& b, float2* T2, cudaStream_t st,
                                LaunchCounter& lc, int nimg, size_t hstride, size_t tstride) {
   const size_t sm = pair_smem(0, g.Ph, g);
   const float4* hh = reinterpret_cast<const float4*>(Hhat);
   const float4* fh = reinterpret_cast<const float4*>(Fhat);
+  const int ncol = g.Pw / 2;
 #define XCB_BODY(LL, R0, R1, R2, PP)                                                         \
   case LL: {                                                                                \
     using PF = IlvFft<LL, R0, R1, R2, PP>;                                                  \
     const PairTw tw = pair_tables<PF>();                                                    \
+    const TailSplit ts = tail_split(ncol, PF::MINB, b.n);                                   \
     if (nimg == 2) {                                                                        \
       set_smem(k_cols_inv_corr_ilv<PF, 2>, sm);                                             \
-      k_cols_inv_corr_ilv<PF, 2><<<g.Pw / 2, PF::T, sm, st>>>(                              \
-          g, hh, hstride / 2, fh, sstride / 2, b, T2, tstride, tw.mid, tw.last);            \
+      k_cols_inv_corr_ilv<PF, 2><<<ts.grid, PF::T, sm, st>>>(                               \
+          g, hh, hstride / 2, fh, sstride / 2, b, T2, tstride, tw.mid, tw.last, ts.full,    \
+          ts.split);                                                                        \
     } else {                                                                                \
       set_smem(k_cols_inv_corr_ilv<PF, 1>, sm);                                             \
-      k_cols_inv_corr_ilv<PF, 1><<<g.Pw / 2, PF::T, sm, st>>>(                              \
-          g, hh, hstride / 2, fh, sstride / 2, b, T2, tstride, tw.mid, tw.last);            \
+      k_cols_inv_corr_ilv<PF, 1><<<ts.grid, PF::T, sm, st>>>(                               \
+          g, hh, hstride / 2, fh, sstride / 2, b, T2, tstride, tw.mid, tw.last, ts.full,    \
+          ts.split);                                                                        \
     }                                                                                       \
     break;                                                                                  \
   }
