@@ -272,10 +272,15 @@ __device__ __forceinline__ void i2_body(int b, const Geo& g, const float4* __res
     PF::pass1(W0, W1, TWs);
     __syncthreads();
     const int dk = bi == 0 ? 0 : bl.k[bi - 1] - bl.k[bi];
-    // Hermitian half-band mode: the k = 0 band enters with weight 1/2
-    const float w0 = half && bl.k[bi] == 0 ? 0.5f : 1.f;
+    // Hermitian half-band mode: the k = 0 band enters with weight 1/2 (a
+    // CTA-uniform branch, so the other bands carry no scaling multiplies)
+    const bool hz = half && bl.k[bi] == 0;
     // acc = acc z^dk + conj(v)  (Horner over descending k; IFFT = conj FFT conj)
     auto horner = [&](float2 (&a)[R2]) {
+      if (hz) {
+#pragma unroll
+        for (int r = 0; r < R2; ++r) a[r] = c_scale(a[r], 0.5f);
+      }
       constexpr int C = 5;  // outputs per TMEM round trip
 #pragma unroll
       for (int r0 = 0; r0 < R2; r0 += C) {
@@ -294,7 +299,7 @@ __device__ __forceinline__ void i2_body(int b, const Geo& g, const float4* __res
         for (int i = 0; i < C; ++i) {
           const int r = r0 + i;
           if (r >= R2) break;
-          const float2 va = c_scale(a[Dft<R2>::pos(r)], w0);
+          const float2 va = a[Dft<R2>::pos(r)];
           if (bi == 0) {
             acc[i] = c_conj(va);
             continue;
