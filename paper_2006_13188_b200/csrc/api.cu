@@ -1743,9 +1743,14 @@ int xc_run3(xc_context ctx, xc_filter3 f, int mode, int nx, int ny, int nz, cons
        "upload band spectra");
     double2* dout = memory == XC_DEVICE ? reinterpret_cast<double2*>(out)
                                         : ctx->buf<double2>("v3_out", N);
-    // bands per chunk: work volumes (and gather planes) within ~4 GB
+    // bands per chunk: work volumes (and gather planes) within a budget
+    // (XCB_3D_CHUNK_MB, default 4 GB)
+    static const size_t chunk_budget = [] {
+      const char* e = std::getenv("XCB_3D_CHUNK_MB");
+      return e && std::atol(e) > 0 ? size_t(std::atol(e)) << 20 : size_t(4) << 30;
+    }();
     const size_t per_band = (P + (mode == XC_CORRELATION ? N : 0)) * sizeof(float2);
-    const int cb = int(std::max<size_t>(1, std::min<size_t>(nb, (size_t(4) << 30) / per_band)));
+    const int cb = int(std::max<size_t>(1, std::min<size_t>(nb, chunk_budget / per_band)));
     float2* work = ctx->buf<float2>("v3_work", P * cb);
     if (mode == XC_CORRELATION) {
       float2* Hh = ctx->buf<float2>("v3_Hhat", P);
