@@ -116,7 +116,9 @@ __device__ __forceinline__ float2 wigner_at(const Band3& b, const double4& e, fl
 __host__ __device__ constexpr int tile_stride(int L) { return L % 2 ? L : L + 1; }
 
 // Radices of the tile plans (make_fft_plan_maxr(L, 10)): a small dispatch set
-// keeps the kernels at <= 64 registers, 4 CTAs of 256 threads per SM.
+// keeps the register demand low.  The tile kernels are bounded to 5 CTAs of
+// 256 threads per SM (48 registers, ~150 B of spills): 64^3 xcorr 2.31 ->
+// 2.08 ms against 64 registers (4 CTAs); 6 CTAs (40 registers) was slower.
 template <class F>
 __device__ __forceinline__ void radix_dispatch10(int R, F&& f) {
   switch (R) {
@@ -233,7 +235,7 @@ __device__ __forceinline__ YZTile yz_tile(const Geo3& g) {
 }
 
 // in-place forward y- or z-pass of nvol volumes; grid (tiles, volume)
-__global__ void __launch_bounds__(kT3, 4) k3t_yz(FftPlanD p, Geo3 g, int axis,
+__global__ void __launch_bounds__(kT3, 5) k3t_yz(FftPlanD p, Geo3 g, int axis,
                                               float2* __restrict__ buf, size_t vstride) {
   extern __shared__ float2 sm[];
   const int L = p.L, Lp = tile_stride(L);
@@ -254,7 +256,7 @@ __global__ void __launch_bounds__(kT3, 4) k3t_yz(FftPlanD p, Geo3 g, int axis,
 
 // z-pass loading conj(H^) V^_sidx[b] (mode 0, gather) or conj(H^) (mode 1,
 // the scatter's final inverse) -> work_b; grid (tiles, band of the chunk)
-__global__ void __launch_bounds__(kT3, 4)
+__global__ void __launch_bounds__(kT3, 5)
     k3t_z_load(FftPlanD p, Geo3 g, const float2* __restrict__ Hh, const float2* __restrict__ spec,
                const int* __restrict__ sidx, size_t vstride, int mode, float2* __restrict__ work) {
   extern __shared__ float2 sm[];
@@ -297,7 +299,7 @@ __device__ __forceinline__ void x_store_rows(int L, int nl, int px, const float2
 
 // x-pass from the signal (zero-padded), times D_b when premul (the scatter
 // premultiply, engine3d.hpp:317-321); grid (tiles over py*pz rows, band)
-__global__ void __launch_bounds__(kT3, 4)
+__global__ void __launch_bounds__(kT3, 5)
     k3t_x_signal(FftPlanD p, Geo3 g, const float2* __restrict__ sig,
                  const double4* __restrict__ eul, const Band3* __restrict__ bands, int premul,
                  float2* __restrict__ work, size_t vstride) {
@@ -320,7 +322,7 @@ __global__ void __launch_bounds__(kT3, 4)
 
 // x-pass of the filter bands: rendered (2R+1)^3 components wrapped to the
 // origin (fft.hpp:186-194); grid (tiles over py*pz rows, band)
-__global__ void __launch_bounds__(kT3, 4)
+__global__ void __launch_bounds__(kT3, 5)
     k3t_x_filter(FftPlanD p, Geo3 g, const float2* __restrict__ comps, float2* __restrict__ spec,
                  size_t vstride) {
   extern __shared__ float2 sm[];
@@ -344,7 +346,7 @@ __global__ void __launch_bounds__(kT3, 4)
 // x-pass finishing an inverse: rows (y, z) < (ny, nz) of work_b, crop x < nx;
 // mode 0: part_b = conj(D_b) G_b (gather steering, engine3d.hpp:290-298);
 // mode 1: out (+)= G (the scatter's single inverse).  G = conj(Y) / P.
-__global__ void __launch_bounds__(kT3, 4)
+__global__ void __launch_bounds__(kT3, 5)
     k3t_x_out(FftPlanD p, Geo3 g, const float2* __restrict__ work, size_t vstride,
               const double4* __restrict__ eul, const Band3* __restrict__ bands, int mode,
               float inv_p, float2* __restrict__ part, int accumulate, double2* __restrict__ out) {
