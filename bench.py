@@ -184,7 +184,10 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    # under torchrun (even with one rank) the NCCL plumbing runs: process
+    # group, barriers, the band reduce and the max-over-ranks timing
+    use_dist = world > 1 or "LOCAL_WORLD_SIZE" in os.environ or "TORCHELASTIC_RUN_ID" in os.environ
+    if use_dist:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -226,12 +229,12 @@ def run_b200(args):
                                C.c_void_p(th.data_ptr()), cptr.ctypes.data_as(C.POINTER(C.c_int)),
                                len(cptr), flags, C.c_void_p(out.data_ptr()), C.byref(st)),
                 ctx.handle)
-        if args.shard == "bands" and world > 1:
+        if args.shard == "bands" and use_dist:
             dist.reduce(out, dst=0, op=dist.ReduceOp.SUM)
         return st.gpu_launches
 
     def barrier():
-        if world > 1:
+        if use_dist:
             dist.barrier()
         torch.cuda.synchronize(dev)
 
@@ -251,7 +254,7 @@ def run_b200(args):
     prof = ctx.profile(enable=False, reset=True)
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], device=dev, dtype=torch.float64)
-    if world > 1:
+    if use_dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_step = float(t.item()) / args.steps
     units_step = Btot * H * W * nb
@@ -280,14 +283,14 @@ def run_b200(args):
             step_host()
         barrier()
         te = torch.tensor([(time.perf_counter() - t0) / n_e2e], device=dev, dtype=torch.float64)
-        if world > 1:
+        if use_dist:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": units_step / float(te.item()) / 1e6, "unit": UNIT,
                "h2d_bytes_per_step": int(Btot * H * W * 8), "d2h_bytes_per_step": int(Btot * H * W * 8),
                "steps": n_e2e}
 
     if rank != 0:
-        if world > 1:
+        if use_dist:
             dist.destroy_process_group()
         return 0
 
@@ -338,14 +341,14 @@ def run_b200(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded numpy, BASELINE config; uploaded to HBM before timing)",
         "config": {"workload": w.name, "images": Btot, "height": H, "width": W, "bands": nb,
-                   "pad": [Ph, Pw], "shard": args.shard if world > 1 else "none",
+                   "pad": [Ph, Pw], "shard": args.shard if use_dist else "none",
                    "l2": "inputs larger than L2 (signal + theta %.1f GB per step)"
                          % (Btot * H * W * 8 / 1e9)},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
     return 0
 
