@@ -655,3 +655,23 @@ def test_dual_i1_i2_batches_match_single_images(orc):
     ys, xs = r.integers(0, n, 16), r.integers(0, n, 16)
     ref = _direct_at(orc, ofilter(orc, wk.filt), H[2], T[2], ys, xs, False)
     assert orc.rel_l2(batch[2][ys, xs], ref) < TOL
+
+
+@pytest.mark.parametrize("n,K", [(2048, 16), (2048, 4)])
+def test_i1_tail_split_pad_2160(orc, n, K):
+    """Pad 2160 runs 1,080 column pairs at two CTAs per SM: 3 full waves and a
+    partial one of 192 pairs.  With 17 bands the partial wave is split into 3
+    band chunks per column pair (k_pair.cu tail_split); with 5 bands it is not.
+    Both against the spectral oracle at sampled pixels."""
+    from paper_2006_13188_b200 import workloads as WL
+    r = np.random.default_rng(41)
+    f = WL.angular_filter(15, 6.0, K // 2, r)
+    F = X.decompose_rotation2(f, 15, 15, K, 30, 2 * K + 2, 15.0)
+    H = r.uniform(0, 1, (n, n)).astype(np.float32)
+    T = r.uniform(0, 2 * np.pi, (n, n)).astype(np.float32)
+    res = X.xcorr_fast(H, X.XformField.rotation(T), F)
+    assert res.standard_ops == 2 * (K // 2) + 1
+    ys = np.concatenate([r.integers(0, n, 40), [0, n - 1, 0, n - 1]])
+    xs = np.concatenate([r.integers(0, n, 40), [0, 0, n - 1, n - 1]])
+    ref = orc.spectral_oracle_at(0, H, ROT, T, ofilter(orc, F), ys, xs)
+    assert orc.rel_l2(res.output[ys, xs], ref) < TOL
