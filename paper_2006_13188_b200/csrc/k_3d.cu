@@ -137,7 +137,7 @@ __device__ __forceinline__ void radix_dispatch10(int R, F&& f) {
 // Forward transform of kTL sequences held in A ([line][Lp]); ping-pong with B.
 // Returns the buffer holding the result.  Called by every thread; A must be
 // complete (a barrier) on entry.
-__device__ float2* tile_fft(const FftPlanD& p, float2* A, float2* B, int Lp) {
+__device__ float2* tile_fft_rt(const FftPlanD& p, float2* A, float2* B, int Lp) {
   float2* src = A;
   float2* dst = B;
   for (int q = 0; q < p.npass; ++q) {
@@ -175,8 +175,8 @@ __device__ float2* tile_fft(const FftPlanD& p, float2* A, float2* B, int Lp) {
 // y / z tiles, where the line-fast order is coalesced): one barrier per pass
 // boundary and no separate copy-in / copy-out.
 template <class Ld, class St>
-__device__ void tile_fft_io(const FftPlanD& p, float2* A, float2* B, int Lp, Ld&& load,
-                            St&& store) {
+__device__ void tile_fft_io_rt(const FftPlanD& p, float2* A, float2* B, int Lp, Ld&& load,
+                               St&& store) {
   if (p.npass == 0) {  // L == 1
     for (int line = threadIdx.x; line < kTL; line += blockDim.x) store(line, 0, load(line, 0));
     return;
@@ -220,6 +220,112 @@ __device__ void tile_fft_io(const FftPlanD& p, float2* A, float2* B, int Lp, Ld&
     src = dst;
     dst = tmp;
   }
+}
+
+// ------------------------------------------------ compile-time tile plans
+// The same Stockham passes with the plan's radices, lengths and strides as
+// template constants, so index arithmetic folds into immediates and
+// constant-divisor multiplies (the runtime plan above costs about 114 thread
+// instructions per point per line transform at 72 points).  Used when the
+// runtime plan equals one of CtPlan's instantiations (tile_dispatch).
+struct NoIo {
+  __device__ float2 operator()(int, int) const { return make_float2(0.f, 0.f); }
+  __device__ void operator()(int, int, float2) const {}
+};
+
+// pass with radix R over sequences of length L, NS = product of the earlier
+// radices; LD: inputs through load(line, n) (else src smem); ST: outputs
+// through store(line, k, v) (else dst smem)
+template <int L, int R, int NS, bool LD, bool ST, class Ld, class St>
+__device__ __forceinline__ void ct_pass(const float2* __restrict__ tw, const float2* src,
+                                        float2* dst, int Lp, Ld& load, St& store) {
+  constexpr int nb = L / R;
+  for (int w = threadIdx.x; w < kTL * nb; w += blockDim.x) {
+    const int line = w % kTL, j = w / kTL;
+    const int jm = NS == 1 ? 0 : j % NS;
+    float2 v[R];
+    if constexpr (LD) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = load(line, j + r * nb);
+    } else {
+      const float2* sp = src + line * Lp + j;
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = sp[r * nb];
+    }
+    if constexpr (NS > 1) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[r] = c_mul(v[r], __ldg(tw + (r - 1) * NS + jm));
+    }
+    Dft<R>::run(v);
+    if constexpr (ST) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) store(line, j + r * nb, v[Dft<R>::pos(r)]);
+    } else {
+      float2* d = dst + line * Lp + (j - jm) * R + jm;
+#pragma unroll
+      for (int r = 0; r < R; ++r) d[r * NS] = v[Dft<R>::pos(r)];
+    }
+  }
+}
+
+// two- or three-pass plan (R2 = 1: two passes), radices in the host plan's
+// order (make_fft_plan_maxr: larger first)
+template <int R0, int R1, int R2>
+struct CtPlan {
+  static constexpr int L = R0 * R1 * R2;
+  __device__ static bool match(const FftPlanD& p) {
+    return p.L == L && p.npass == (R2 == 1 ? 2 : 3) && p.radix[0] == R0 &&
+           p.radix[1] == R1 && (R2 == 1 || p.radix[2] == R2);
+  }
+  // IO: first pass from load, last pass to store; else smem A -> result
+  // buffer (returned)
+  template <bool IO, class Ld, class St>
+  __device__ static float2* run(const FftPlanD& p, float2* A, float2* B, int Lp, Ld& load,
+                                St& store) {
+    const float2* tw1 = p.tw + p.tw_off[1];
+    ct_pass<L, R0, 1, IO, false>(nullptr, A, B, Lp, load, store);
+    __syncthreads();
+    if constexpr (R2 == 1) {
+      ct_pass<L, R1, R0, false, IO>(tw1, B, A, Lp, load, store);
+      if constexpr (!IO) __syncthreads();
+      return A;
+    } else {
+      ct_pass<L, R1, R0, false, false>(tw1, B, A, Lp, load, store);
+      __syncthreads();
+      ct_pass<L, R2, R0 * R1, false, IO>(p.tw + p.tw_off[2], A, B, Lp, load, store);
+      if constexpr (!IO) __syncthreads();
+      return B;
+    }
+  }
+};
+
+// f(CtPlan<...>{}) for the first instantiation matching p; false if none.
+// Covers the pads of the 64^3 / 128^3 benchmarks (72, 135, 144) and their
+// neighbours.
+template <class F>
+__device__ __forceinline__ bool tile_dispatch(const FftPlanD& p, F&& f) {
+  if (CtPlan<9, 8, 1>::match(p)) return f(CtPlan<9, 8, 1>{}), true;
+  if (CtPlan<10, 8, 1>::match(p)) return f(CtPlan<10, 8, 1>{}), true;
+  if (CtPlan<10, 9, 1>::match(p)) return f(CtPlan<10, 9, 1>{}), true;
+  if (CtPlan<9, 5, 3>::match(p)) return f(CtPlan<9, 5, 3>{}), true;
+  if (CtPlan<6, 6, 4>::match(p)) return f(CtPlan<6, 6, 4>{}), true;
+  return false;
+}
+
+__device__ float2* tile_fft(const FftPlanD& p, float2* A, float2* B, int Lp) {
+  float2* res = nullptr;
+  NoIo io;
+  if (tile_dispatch(p, [&](auto pl) { res = decltype(pl)::template run<false>(p, A, B, Lp, io, io); }))
+    return res;
+  return tile_fft_rt(p, A, B, Lp);
+}
+
+template <class Ld, class St>
+__device__ void tile_fft_io(const FftPlanD& p, float2* A, float2* B, int Lp, Ld&& load,
+                            St&& store) {
+  if (tile_dispatch(p, [&](auto pl) { decltype(pl)::template run<true>(p, A, B, Lp, load, store); }))
+    return;
+  tile_fft_io_rt(p, A, B, Lp, load, store);
 }
 
 // y / z tiles: 16 adjacent x at one (z) for axis 1, at one (y) for axis 2

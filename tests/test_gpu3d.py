@@ -212,3 +212,25 @@ def test_fast_3d_random_cases(orc, seed):
         assert got.standard_ops == ops
         err = orc.rel_l2(got.output, ref)
         assert err < TOL, (seed, mode, (nx, ny, nz), R, K, degrees, err)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dims,degrees", [((68, 64, 60), [0, 1]), ((76, 86, 70), [1]),
+                                          ((128, 131, 140), [0])])
+def test_3d_compile_time_tile_plans(orc, dims, degrees):
+    """Pads with compile-time tile plans (k_3d.cu CtPlan): 72 = 9·8, 80 = 10·8,
+    90 = 10·9 (two passes), 135 = 9·5·3 and 144 = 6·6·4 (three passes), mixed
+    with runtime-plan axes (64 = 8·8), against the oracle on a degree subset."""
+    rng = orc.Rng(87)
+    R = 4
+    F, G = _filters(orc, rng.random_smooth_filter3(R), R, 2)
+    nx, ny, nz = dims
+    H = rng.random_field3(nx, ny, nz, False)
+    q = rng.random_rotation3_field(nx, ny, nz)
+    T = X.rotation3d(q)
+    plan = X.XConvPlan(components=degrees)
+    for mode, fn in ((0, X.xcorr_fast_3d), (1, X.xconv_fast_3d)):
+        r = fn(H.real, T, G, plan)
+        ref, ops = orc.xfast3(mode, H, q, F, degrees=degrees)
+        assert r.standard_ops == ops == sum((2 * l + 1) ** 2 for l in degrees)
+        assert orc.rel_l2(r.output, ref) < TOL, (mode, orc.rel_l2(r.output, ref))
