@@ -31,6 +31,8 @@
  *   xc_render_sph_component / xc_reconstruct3 / xc_sph_harm
  *                                  <- sph.hpp:37-47, 194-221 (host)
  *   xc_wigner_d                    <- wigner_d     wigner.hpp:64-88 (host)
+ *   xc_white_noise                 <- white_noise  lic.hpp:9-17 (host; the
+ *                                     seeded input of lic, lic.hpp:37-55)
  *
  * Conventions
  *   - Status codes: XC_OK; XC_EINVAL for the reference's std::invalid_argument
@@ -230,6 +232,12 @@ int xc_reconstruct3(xc_filter3 f, int nx, int ny, int nz, double cx, double cy, 
 int xc_sph_harm(int l, int m, double theta, double phi, double* out2);
 /* D[(m_to + l)(2l+1) + (m_from + l)], (2l+1)^2 complex (wigner.hpp:64-88) */
 int xc_wigner_d(int l, const double* quat, double* out);
+
+/* ---- line integral convolution input (lic.hpp) ------- */
+/* white_noise (lic.hpp:9-17): std::mt19937_64(seed), value (rng() >> 11) *
+ * 2^-53 per pixel in y-major order (y outer, x inner); height x width
+ * doubles written in `layout`.  Host only: no device needed. */
+int xc_white_noise(unsigned long long seed, int height, int width, int layout, double* out);
 /* xcorr_fast_3d / xconv_fast_3d: signal (signal_dtype XC_F32 / XC_F64 /
  * XC_C64 / XC_C128), quats and out (complex128) in `memory`; degrees selects a
  * subset of l (XConvPlan::components over degrees, engine3d.hpp:11-16);

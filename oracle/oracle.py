@@ -455,6 +455,73 @@ class Rng:
         return out
 
 
+def white_noise(width, height, seed) -> np.ndarray:
+    """lic.hpp:9-17: std::mt19937_64(seed); f.at(x, y) = (rng() >> 11) * 2^-53
+    in y-major order.  [height][width]."""
+    h = C.c_void_p(lib().or_rng_new(int(seed) & (2**64 - 1)))
+    try:
+        out = np.zeros((int(height), int(width)))
+        for y in range(int(height)):
+            for x in range(int(width)):
+                out[y, x] = float(lib().or_rng_next(h) >> 11) * 2.0 ** -53
+    finally:
+        lib().or_rng_free(h)
+    return out
+
+
+def anisotropic_gaussian(length, width) -> np.ndarray:
+    """lic.hpp:20-32 (loop form)."""
+    R = int(np.ceil(2.5 * length))
+    f = np.zeros((2 * R + 1, 2 * R + 1))
+    for y in range(-R, R + 1):
+        for x in range(-R, R + 1):
+            if float(x * x + y * y) > float(R) * R:
+                continue
+            f[y + R, x + R] = np.exp(-float(x) * x / (2 * length * length)
+                                     - float(y) * y / (2 * width * width))
+    return f
+
+
+def lic(angles, length, width, seed, normalized=True, K=16, nthreads=1) -> np.ndarray:
+    """lic.hpp:37-55 over the restated decomposition and engine (rotation2)."""
+    if not (length > width) or not (width > 0):
+        raise ValueError("need length > width > 0")
+    angles = _f64(angles)
+    h, w = angles.shape
+    noise = white_noise(w, h, seed)
+    kern = anisotropic_gaussian(length, width)
+    R = (kern.shape[1] - 1) // 2
+    F = decompose_rotation2(kern, float(R), float(R), int(K), max(8, R), max(64, 4 * int(K)),
+                            R + 0.5)
+    if normalized:
+        return smooth_adaptive(noise, 0, angles, F, True, nthreads)[0]
+    return xconv_fast(noise, 0, angles, F, nthreads=nthreads)[0].real
+
+
+def structure_tensor(img, sigma=2.0):
+    """proj/tests/helpers.hpp:161-191: (orientation, coherence) of the
+    gradient structure tensor blurred by sigma; orientation is the streak
+    direction (perpendicular to the dominant gradient), normalized to [-pi, pi)."""
+    mag, d = gradient(img)
+    gx, gy = mag * np.cos(d), mag * np.sin(d)
+    jxx = gaussian_blur(gx * gx, sigma)
+    jxy = gaussian_blur(gx * gy, sigma)
+    jyy = gaussian_blur(gy * gy, sigma)
+    tr = jxx + jyy
+    det = np.sqrt(np.maximum(0.0, (jxx - jyy) ** 2 + 4 * jxy * jxy))
+    o = 0.5 * np.arctan2(2 * jxy, jxx - jyy) + np.pi / 2
+    o = np.fmod(o + np.pi, 2 * np.pi)
+    o = np.where(o < 0, o + 2 * np.pi, o) - np.pi
+    coh = np.where(tr > 1e-12, det / np.where(tr > 1e-12, tr, 1.0), 0.0)
+    return o, coh
+
+
+def orientation_distance(a, b):
+    """proj/tests/helpers.hpp:194-198 (undirected, mod pi)."""
+    d = np.fmod(np.abs(a - b), np.pi)
+    return np.minimum(d, np.pi - d)
+
+
 def rel_l2(a, b) -> float:
     """helpers.hpp:10-14"""
     a = np.asarray(a)

@@ -47,6 +47,7 @@ EXPORTS = [
     "xc_build_vote_filter", "xc_build_optimal_filter", "xc_detect_pattern",
     "xc_find_peaks_device", "xc_filter3_create", "xc_filter3_destroy", "xc_decompose_rotation3",
     "xc_render_sph_component", "xc_reconstruct3", "xc_sph_harm", "xc_wigner_d", "xc_run3",
+    "xc_white_noise",
 ]
 
 _lib = None
@@ -105,6 +106,7 @@ def lib():
         L.xc_reconstruct3.argtypes = [vp, i, i, i, d, d, d, ip, i, dp]
         L.xc_sph_harm.argtypes = [i, i, d, d, dp]
         L.xc_wigner_d.argtypes = [i, dp, dp]
+        L.xc_white_noise.argtypes = [C.c_ulonglong, i, i, i, dp]
         L.xc_run3.argtypes = [vp, vp, i, i, i, i, vp, i, vp, ip, i, i, vp, C.POINTER(Stats)]
         L.xc_profile_enable.argtypes = [vp, i]
         L.xc_profile_reset.argtypes = [vp]

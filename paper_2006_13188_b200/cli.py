@@ -1,5 +1,5 @@
 """Command-line surface of the reference (proj/tools/xconv_cli.cpp) over the
-B200 path: the `xcorr`, `xconv`, `smooth`, `detect` and `decompose`
+B200 path: the `xcorr`, `xconv`, `smooth`, `detect`, `lic` and `decompose`
 subcommands with the reference's options, file formats (fileio.py), JSON
 sidecars and exit codes.
 
@@ -132,6 +132,22 @@ def cmd_smooth(a) -> int:
     return 0
 
 
+def cmd_lic(a) -> int:
+    """xconv_cli.cpp:602-639: seeded white noise smeared along a rotation field
+    (lic.hpp:37-55 over the GPU path)."""
+    from .lic import lic
+    T = io.read_xform(a.field, E.XformKind.rotation2)
+    t0 = time.perf_counter()
+    out = lic(T, a.length, a.line_width, a.seed, not a.unnormalized, a.K)
+    sidecar = {"command": "lic",
+               "parameters": {"field": a.field, "length": a.length, "line-width": a.line_width,
+                              "K": a.K, "unnormalized": bool(a.unnormalized), **_common(a)},
+               "timings": {"total": time.perf_counter() - t0}}
+    _save_image(a.output, out, sidecar)
+    _write_sidecar(a.output, sidecar)
+    return 0
+
+
 def cmd_detect(a) -> int:
     """xconv_cli.cpp:348-405."""
     img = _load_image(a.image)
@@ -245,6 +261,13 @@ def _parser() -> argparse.ArgumentParser:
     c.add_argument("--K", type=int, default=16)
     c.add_argument("--output", required=True)
     c.add_argument("--peaks-csv", default="")
+    c = sub.add_parser("lic", parents=[common])
+    c.add_argument("--field", required=True)
+    c.add_argument("--length", type=float, default=8.0)
+    c.add_argument("--line-width", type=float, default=1.2)
+    c.add_argument("--K", type=int, default=16)
+    c.add_argument("--unnormalized", action="store_true")
+    c.add_argument("--output", required=True)
     c = sub.add_parser("decompose", parents=[common])
     c.add_argument("--input", required=True)
     c.add_argument("--group", default="rotation")
@@ -271,7 +294,7 @@ def main(argv=None) -> int:
     try:
         return {"xcorr": lambda: cmd_engine(a, True), "xconv": lambda: cmd_engine(a, False),
                 "smooth": lambda: cmd_smooth(a), "detect": lambda: cmd_detect(a),
-                "decompose": lambda: cmd_decompose(a)}[a.command]()
+                "decompose": lambda: cmd_decompose(a), "lic": lambda: cmd_lic(a)}[a.command]()
     except io.IoError as e:
         print(f"io error: {e}", file=sys.stderr)
         return 3

@@ -22,6 +22,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <tuple>
@@ -1663,6 +1664,19 @@ int xc_sph_harm(int l, int m, double theta, double phi, double* out2) {
     const cplx v = xcb::sph_harm(l, m, theta, phi);
     out2[0] = v.real();
     out2[1] = v.imag();
+  });
+}
+
+int xc_white_noise(unsigned long long seed, int height, int width, int layout, double* out) {
+  return guarded(nullptr, [&] {
+    if (!out) throw std::invalid_argument("null argument");
+    if (height < 0 || width < 0) throw std::invalid_argument("dims must be non-negative");
+    std::mt19937_64 rng(seed);
+    for (int y = 0; y < height; ++y)
+      for (int x = 0; x < width; ++x) {
+        const double v = double(rng() >> 11) * 0x1p-53;
+        out[layout == XC_COL_MAJOR ? size_t(x) * height + y : size_t(y) * width + x] = v;
+      }
   });
 }
 
