@@ -1,5 +1,5 @@
 """Command-line surface of the reference (proj/tools/xconv_cli.cpp) over the
-B200 path: the `xcorr`, `xconv`, `smooth`, `detect`, `lic` and `decompose`
+B200 path: the `xcorr`, `xconv`, `smooth`, `detect`, `contour`, `lic` and `decompose`
 subcommands with the reference's options, file formats (fileio.py), JSON
 sidecars and exit codes.
 
@@ -148,6 +148,41 @@ def cmd_lic(a) -> int:
     return 0
 
 
+def cmd_contour(a) -> int:
+    """xconv_cli.cpp:527-599: complement matching of contour fragments; the
+    match CSV holds x,y,angle,score rows (17 significant digits)."""
+    from .contour import match_contours, rasterize_contours
+    qlines = io.read_polylines_csv(a.query)
+    tlines = io.read_polylines_csv(a.target)
+    w, h = a.width, a.height
+    if w <= 0 or h <= 0:
+        mx = max(x for lines in (qlines, tlines) for ln in lines for x, _ in ln)
+        my = max(y for lines in (qlines, tlines) for ln in lines for _, y in ln)
+        mx, my = max(mx, 0.0), max(my, 0.0)
+        if w <= 0:
+            w = int(math.ceil(mx)) + 8
+        if h <= 0:
+            h = int(math.ceil(my)) + 8
+    t0 = time.perf_counter()
+    query = rasterize_contours(qlines, w, h, a.sigma)
+    target = rasterize_contours(tlines, w, h, a.sigma)
+    matches = match_contours(query, target, a.query_x, a.query_y, a.eps, a.K, a.top)
+    try:
+        with open(a.output, "w") as out:
+            for m in matches:
+                out.write(f"{m.x},{m.y},{m.angle:.17g},{m.score:.17g}\n")
+    except OSError:
+        raise io.IoError("cannot open " + a.output + " for writing") from None
+    sidecar = {"command": "contour",
+               "parameters": {"query": a.query, "target": a.target, "query-x": a.query_x,
+                              "query-y": a.query_y, "eps": a.eps, "K": a.K, "width": w,
+                              "height": h, "sigma": a.sigma, "top": a.top, **_common(a)},
+               "counters": {"matches": len(matches)},
+               "timings": {"total": time.perf_counter() - t0}}
+    _write_sidecar(a.output, sidecar)
+    return 0
+
+
 def cmd_detect(a) -> int:
     """xconv_cli.cpp:348-405."""
     img = _load_image(a.image)
@@ -261,6 +296,18 @@ def _parser() -> argparse.ArgumentParser:
     c.add_argument("--K", type=int, default=16)
     c.add_argument("--output", required=True)
     c.add_argument("--peaks-csv", default="")
+    c = sub.add_parser("contour", parents=[common])
+    c.add_argument("--query", required=True)
+    c.add_argument("--target", required=True)
+    c.add_argument("--query-x", type=float, required=True)
+    c.add_argument("--query-y", type=float, required=True)
+    c.add_argument("--eps", type=float, default=8.0)
+    c.add_argument("--K", type=int, default=16)
+    c.add_argument("--width", type=int, default=0)
+    c.add_argument("--height", type=int, default=0)
+    c.add_argument("--sigma", type=float, default=1.5)
+    c.add_argument("--top", type=int, default=9)
+    c.add_argument("--output", required=True)
     c = sub.add_parser("lic", parents=[common])
     c.add_argument("--field", required=True)
     c.add_argument("--length", type=float, default=8.0)
@@ -294,7 +341,8 @@ def main(argv=None) -> int:
     try:
         return {"xcorr": lambda: cmd_engine(a, True), "xconv": lambda: cmd_engine(a, False),
                 "smooth": lambda: cmd_smooth(a), "detect": lambda: cmd_detect(a),
-                "decompose": lambda: cmd_decompose(a), "lic": lambda: cmd_lic(a)}[a.command]()
+                "decompose": lambda: cmd_decompose(a), "lic": lambda: cmd_lic(a),
+                "contour": lambda: cmd_contour(a)}[a.command]()
     except io.IoError as e:
         print(f"io error: {e}", file=sys.stderr)
         return 3

@@ -303,3 +303,28 @@ def read_filter(path: str) -> FreqFilter2:
 __all__ = ["IoError", "read_pgm", "write_pgm", "write_pfm_planes", "read_pfm_planes",
            "write_pfm", "read_pfm_field", "write_xform", "read_xform", "write_filter",
            "read_filter", "retained_ks"]
+
+
+def read_polylines_csv(path: str) -> list:
+    """io.hpp:372-394: "x,y" rows, a blank line separates polylines."""
+    try:
+        f = open(path)
+    except OSError:
+        raise IoError("cannot open " + path) from None
+    lines = [[]]
+    with f:
+        for row in f.read().split("\n"):
+            if not row.strip(" \t\r"):
+                if lines[-1]:
+                    lines.append([])
+                continue
+            try:
+                xs, ys = row.split(",", 1)
+                lines[-1].append((float(xs), float(ys.split()[0] if ys.split() else ys)))
+            except ValueError:
+                raise IoError(path + ": bad polyline row: " + row) from None
+    if not lines[-1]:
+        lines.pop()
+    if not lines:
+        raise IoError(path + ": no polylines")
+    return lines
