@@ -224,14 +224,33 @@ def run_b200(args):
                      int(F.group))
     st = N.Stats()
 
+    # band sharding: the reduce of step i runs on NCCL's stream while step
+    # i + 1 computes into the other output buffer (overlap each
+    # reduce with the next compute); drain() joins the outstanding reduces
+    band_reduce = args.shard == "bands" and use_dist
+    outs = [out, torch.empty_like(out)] if band_reduce else [out]
+    pending = [None] * len(outs)
+    step_no = [0]
+
     def step_device():
+        i = step_no[0] % len(outs)
+        step_no[0] += 1
+        if pending[i] is not None:
+            pending[i].wait()
+            pending[i] = None
         N.check(N.lib().xc_run(ctx.handle, fh, 0, C.byref(dd), C.c_void_p(sig.data_ptr()),
                                C.c_void_p(th.data_ptr()), cptr.ctypes.data_as(C.POINTER(C.c_int)),
-                               len(cptr), flags, C.c_void_p(out.data_ptr()), C.byref(st)),
+                               len(cptr), flags, C.c_void_p(outs[i].data_ptr()), C.byref(st)),
                 ctx.handle)
-        if args.shard == "bands" and use_dist:
-            dist.reduce(out, dst=0, op=dist.ReduceOp.SUM)
+        if band_reduce:
+            pending[i] = dist.reduce(outs[i], dst=0, op=dist.ReduceOp.SUM, async_op=True)
         return st.gpu_launches
+
+    def drain():
+        for i, p in enumerate(pending):
+            if p is not None:
+                p.wait()
+                pending[i] = None
 
     def barrier():
         if use_dist:
@@ -240,6 +259,7 @@ def run_b200(args):
 
     for _ in range(args.warmup):
         step_device()
+    drain()
     barrier()
     ctx.profile(enable=True, reset=True)
     launches = 0
@@ -249,6 +269,7 @@ def run_b200(args):
         e0.record(stream)
         for _ in range(args.steps):
             launches += step_device()
+        drain()
         e1.record(stream)
         barrier()
     prof = ctx.profile(enable=False, reset=True)
