@@ -201,8 +201,14 @@ def run_b200(args):
     F = w.filt
     nb = F.n_components()
     ks = np.asarray(F.ks, np.int32)
-    if args.shard == "batch" and world > 1:
+    # fewer images than ranks (config 1): every rank runs a replica of the
+    # whole batch ("replicas only"), and the job's units scale
+    replicas = args.shard == "batch" and world > 1 and Btot < world
+    if args.shard == "batch" and world > 1 and not replicas:
         imgs = list(range(rank * Btot // world, (rank + 1) * Btot // world))
+        comps = ks
+    elif replicas:
+        imgs = list(range(Btot))
         comps = ks
     else:
         imgs = list(range(Btot))
@@ -278,7 +284,7 @@ def run_b200(args):
     if use_dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_step = float(t.item()) / args.steps
-    units_step = Btot * H * W * nb
+    units_step = Btot * H * W * nb * (world if replicas else 1)
     value = units_step / (ms_step * 1e-3) / 1e6
 
     # ---- e2e: public API with pinned host buffers (H2D + D2H in the region)
@@ -307,7 +313,8 @@ def run_b200(args):
         if use_dist:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": units_step / float(te.item()) / 1e6, "unit": UNIT,
-               "h2d_bytes_per_step": int(Btot * H * W * 8), "d2h_bytes_per_step": int(Btot * H * W * 8),
+               "h2d_bytes_per_step": int(Btot * H * W * 8 * (world if replicas else 1)),
+               "d2h_bytes_per_step": int(Btot * H * W * 8 * (world if replicas else 1)),
                "steps": n_e2e}
 
     if rank != 0:
@@ -346,7 +353,8 @@ def run_b200(args):
                                 "frac": kernel_roof(k)[3] / hbm}
                             for k in prof if k.startswith("I")},
                 "stages_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
-                "pipeline_model_frac": model_bytes("xcorr", nb, H * W, Ph * Pw) * Btot /
+                "pipeline_model_frac": model_bytes("xcorr", nb, H * W, Ph * Pw) * Btot *
+                (world if replicas else 1) /
                 (ms_step * 1e-3) / 1e9 / hbm / max(world, 1)}
 
     cpu = None
@@ -362,7 +370,8 @@ def run_b200(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded numpy, BASELINE config; uploaded to HBM before timing)",
         "config": {"workload": w.name, "images": Btot, "height": H, "width": W, "bands": nb,
-                   "pad": [Ph, Pw], "shard": args.shard if use_dist else "none",
+                   "pad": [Ph, Pw],
+                   "shard": ("replicas" if replicas else args.shard) if use_dist else "none",
                    "l2": "inputs larger than L2 (signal + theta %.1f GB per step)"
                          % (Btot * H * W * 8 / 1e9)},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
