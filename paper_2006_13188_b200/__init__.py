@@ -11,7 +11,7 @@ from .engine import (DetectionResult, FreqFilter2, Peak, Response2, SmoothResult
                      smooth_adaptive, xconv_fast, xcorr_fast)
 from .lic import anisotropic_gaussian, lic, white_noise
 from .contour import ContourMatch, ContourScene, match_contours, rasterize_contours
-from .engine3d import (Response3, SphFilter3, decompose_rotation3, reconstruct3,
+from .engine3d import (Response3, SphFilter3, decompose_rotation3, reconstruct3, steer_filter3,
                        render_sph_component, rotation3d, sph_harm, wigner_d, xconv_fast_3d,
                        xcorr_fast_3d)
 
@@ -22,4 +22,5 @@ __all__ = ["DetectionResult", "FreqFilter2", "Peak", "Response2", "SmoothResult"
            "smooth_adaptive", "xconv_fast", "xcorr_fast", "Response3", "SphFilter3",
            "decompose_rotation3", "reconstruct3", "render_sph_component", "rotation3d",
            "sph_harm", "wigner_d", "xconv_fast_3d", "xcorr_fast_3d", "anisotropic_gaussian", "lic",
-           "white_noise", "ContourMatch", "ContourScene", "match_contours", "rasterize_contours"]
+           "white_noise", "ContourMatch", "ContourScene", "match_contours", "rasterize_contours",
+           "steer_filter3"]

@@ -1,5 +1,5 @@
 """Command-line surface of the reference (proj/tools/xconv_cli.cpp) over the
-B200 path: the `xcorr`, `xconv`, `smooth`, `detect`, `contour`, `lic` and `decompose`
+B200 path: the `xcorr`, `xconv`, `smooth`, `detect`, `contour`, `lic`, `decompose` and `steer3d`
 subcommands with the reference's options, file formats (fileio.py), JSON
 sidecars and exit codes.
 
@@ -214,11 +214,63 @@ def cmd_detect(a) -> int:
     return 0
 
 
+def _decompose3(a) -> int:
+    """xconv_cli.cpp:739-780: a PFM stack of z slices -> SphFilter3 -> XCF1."""
+    from . import engine3d as E3
+    planes = io.read_pfm_planes(a.input)
+    vol = np.stack([np.asarray(p, np.float64) for p in planes])  # (nz, h, w)
+    nz, h, w = vol.shape
+    cx = a.center_x if a.center_x >= 0 else (w - 1) / 2.0
+    cy = a.center_y if a.center_y >= 0 else (h - 1) / 2.0
+    cz = (nz - 1) / 2.0
+    r_max = a.r_max if a.r_max > 0 else min(cx, cy, cz, w - 1 - cx, h - 1 - cy, nz - 1 - cz)
+    if r_max <= 0:
+        raise ValueError("--r-max must be positive (volume too small?)")
+    n_radii = a.n_radii if a.n_radii > 0 else 2 * int(math.ceil(r_max))
+    t0 = time.perf_counter()
+    F = E3.decompose_rotation3(vol, cx, cy, cz, a.K, n_radii, r_max)
+    io.write_filter3(a.output, F)
+    sidecar = {"command": "decompose",
+               "parameters": {"input": a.input, "group": a.group, "K": a.K, "center-x": cx,
+                              "center-y": cy, "center-z": cz, "n-radii": n_radii,
+                              "r-max": r_max, **_common(a)},
+               "counters": {"steering-products": sum((2 * l + 1) ** 2 for l in range(F.K + 1))},
+               "timings": {"total": time.perf_counter() - t0}}
+    _write_sidecar(a.output, sidecar)
+    return 0
+
+
+def cmd_steer3d(a) -> int:
+    """xconv_cli.cpp:645-688: rotate a 3D filter by a quaternion and write the
+    reconstruction on the (2R+1)^3 grid as a PFM stack of z slices (real part)."""
+    from . import engine3d as E3
+    F = io.read_filter3(a.filter)
+    q = np.asarray(a.quat, np.float64)
+    nq = float(np.linalg.norm(q))
+    if nq < 1e-12:
+        raise ValueError("--quat must be a nonzero quaternion")
+    q = q / nq
+    t0 = time.perf_counter()
+    rot = E3.steer_filter3(F, q)
+    R = int(math.ceil(F.r_max))
+    n = 2 * R + 1
+    vol = E3.reconstruct3(rot, n, n, n, float(R), float(R), float(R))
+    io.write_pfm_planes(a.output, [np.ascontiguousarray(vol[z].real) for z in range(n)])
+    sidecar = {"command": "steer3d",
+               "parameters": {"filter": a.filter, "quat": [float(v) for v in a.quat],
+                              **_common(a)},
+               "counters": {"degrees": F.K + 1,
+                            "steering-products": sum((2 * l + 1) ** 2 for l in range(F.K + 1))},
+               "timings": {"total": time.perf_counter() - t0}}
+    _write_sidecar(a.output, sidecar)
+    return 0
+
+
 def cmd_decompose(a) -> int:
     """xconv_cli.cpp:690-829 (2D groups)."""
     kind = _parse_group(a.group)
     if kind == E.XformKind.rotation3:
-        raise ValueError("--group rotation3d: the 3D pipeline is outside the GPU build")
+        return _decompose3(a)
     img = _load_image(a.input)
     h, w = img.shape
     cx = a.center_x if a.center_x >= 0 else (w - 1) / 2.0
@@ -315,6 +367,10 @@ def _parser() -> argparse.ArgumentParser:
     c.add_argument("--K", type=int, default=16)
     c.add_argument("--unnormalized", action="store_true")
     c.add_argument("--output", required=True)
+    c = sub.add_parser("steer3d", parents=[common])
+    c.add_argument("--filter", required=True)
+    c.add_argument("--quat", type=float, nargs=4, default=[1.0, 0.0, 0.0, 0.0])
+    c.add_argument("--output", required=True)
     c = sub.add_parser("decompose", parents=[common])
     c.add_argument("--input", required=True)
     c.add_argument("--group", default="rotation")
@@ -342,7 +398,8 @@ def main(argv=None) -> int:
         return {"xcorr": lambda: cmd_engine(a, True), "xconv": lambda: cmd_engine(a, False),
                 "smooth": lambda: cmd_smooth(a), "detect": lambda: cmd_detect(a),
                 "decompose": lambda: cmd_decompose(a), "lic": lambda: cmd_lic(a),
-                "contour": lambda: cmd_contour(a)}[a.command]()
+                "contour": lambda: cmd_contour(a),
+                "steer3d": lambda: cmd_steer3d(a)}[a.command]()
     except io.IoError as e:
         print(f"io error: {e}", file=sys.stderr)
         return 3

@@ -171,3 +171,14 @@ def xcorr_fast_3d(H, T: XformField, F: SphFilter3, plan: XConvPlan | None = None
 def xconv_fast_3d(H, T: XformField, F: SphFilter3, plan: XConvPlan | None = None) -> Response3:
     """engine3d.hpp:306-335: out = sum_{l,m,m'} (H D^l_{m'm}) conv V_{l m m'}."""
     return _fast3(XMode.convolution, H, T, F, plan)
+
+
+def steer_filter3(F: SphFilter3, q) -> SphFilter3:
+    """Rotate a 3D filter by mixing each degree's coefficients per radial shell
+    with D^l(q) (xconv_cli.cpp:191-204, the steer3d subcommand)."""
+    out = F.coeffs.copy()
+    for l in range(F.K + 1):
+        D = wigner_d(l, q)
+        cols = slice(l * l, (l + 1) * (l + 1))  # l(l+1)+m for m = -l..l
+        out[:, cols] = F.coeffs[:, cols] @ D.T
+    return SphFilter3(F.K, F.n_radii, F.r_max, out)

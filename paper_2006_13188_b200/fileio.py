@@ -300,9 +300,40 @@ def read_filter(path: str) -> FreqFilter2:
                        r_min, r_domain)
 
 
+def write_filter3(path: str, f) -> None:
+    """io.hpp:318-338: XCF1 with group tag 2, (K, n_radii, 0, r_max, 0, 0), then
+    the (n_radii, (K+1)^2) coefficients column by column."""
+    coeffs = np.asarray(f.coeffs, np.complex128)
+    head = _XCF1_HEAD.pack(b"XCF1", 2, int(f.K), int(f.n_radii), 0, float(f.r_max), 0.0, 0.0,
+                           coeffs.shape[0], coeffs.shape[1])
+    with _open_w(path) as out:
+        out.write(head)
+        out.write(np.ascontiguousarray(coeffs.T).astype("<c16").tobytes())
+
+
+def read_filter3(path: str):
+    """io.hpp:340-368."""
+    from .engine3d import SphFilter3
+    data = _slurp(path)
+    if len(data) < 4 or data[:4] != b"XCF1":
+        raise IoError(path + ": not a filter container")
+    if len(data) < 5 or data[4] != 2:
+        raise IoError(path + ": not a 3D filter")
+    if len(data) < _XCF1_HEAD.size:
+        raise IoError(path + ": truncated container")
+    _, _, K, n_radii, _, r_max, _, _, rows, cols = _XCF1_HEAD.unpack_from(data)
+    if cols != (K + 1) * (K + 1):
+        raise IoError(path + ": coefficient count does not match band limit")
+    n = rows * cols
+    if rows < 0 or len(data) < _XCF1_HEAD.size + 16 * n:
+        raise IoError(path + ": truncated container")
+    coeffs = np.frombuffer(data, "<c16", count=n, offset=_XCF1_HEAD.size).reshape(cols, rows).T
+    return SphFilter3(K, n_radii, r_max, coeffs.astype(np.complex128))
+
+
 __all__ = ["IoError", "read_pgm", "write_pgm", "write_pfm_planes", "read_pfm_planes",
            "write_pfm", "read_pfm_field", "write_xform", "read_xform", "write_filter",
-           "read_filter", "retained_ks"]
+           "read_filter", "retained_ks", "write_filter3", "read_filter3", "read_polylines_csv"]
 
 
 def read_polylines_csv(path: str) -> list:
