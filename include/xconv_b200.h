@@ -113,6 +113,32 @@ int xc_abi_version(void);
 
 /* ---- contexts ---------------------------------------------------------- */
 int xc_context_create(int device, xc_context* out);
+
+/* Multi-GPU contexts (the band loop of engine.hpp:300-319 /
+ * 345-368 split across devices).  xc_run and xc_smooth on such a context split
+ * the bands into contiguous ranges (balanced to +-1), run one range per
+ * device and sum the partial outputs onto the first device with one NCCL
+ * reduce (smooth: numerator and denominator, divided on the root).  The scale
+ * group's inner-DC term is added once.  Other entry points run on the first
+ * device.  Pointers with memory == XC_DEVICE live on the first device.
+ *
+ * xc_context_create_multi: one process, n_dev devices (ncclCommInitAll).  A
+ *   device listed twice (or XCB_REDUCE=peer) reduces with peer copies and an
+ *   ordered device-side sum instead of NCCL.
+ * xc_context_create_rank: one process per GPU; all ranks call xc_run /
+ *   xc_smooth with the same arguments and their own inputs, rank 0's `out`
+ *   receives the result (ncclCommInitRank; the 128-byte id comes from
+ *   xc_nccl_unique_id on one rank, shared by the caller). */
+enum xc_shard { XC_SHARD_BANDS = 0, XC_SHARD_BATCH = 1 };
+int xc_nccl_unique_id(void* id128);
+int xc_context_create_multi(int n_dev, const int* dev_ids, xc_context* out);
+int xc_context_create_rank(int device, const void* nccl_id128, int rank, int nranks,
+                           xc_context* out);
+/* XC_SHARD_BANDS (default; reduce) or XC_SHARD_BATCH (images split across the
+ * devices of a create_multi context, no collective). */
+int xc_context_set_sharding(xc_context ctx, int shard);
+/* devices (or ranks) of a context and whether its reduce is NCCL */
+int xc_context_devices(xc_context ctx, int* n_dev, int* uses_nccl);
 void xc_context_destroy(xc_context ctx);
 /* Message of the last failed call on this context (or thread if ctx NULL). */
 const char* xc_last_error(xc_context ctx);

@@ -20,12 +20,13 @@
 // XC_COL_MAJOR with the caller's complex<double> / double buffers
 // (XC_C128 / XC_F64); std::invalid_argument is rethrown with the reference's
 // message for XC_EINVAL, std::runtime_error otherwise.  The device-side filter
-// spectra are cached per filter content (hash), per thread.
+// spectra are cached per filter content (exact key, 4-entry LRU), per thread.
 #pragma once
 
 #include <cmath>
 #include <complex>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -47,14 +48,76 @@ inline void check(int rc, xc_context ctx) {
   throw std::runtime_error("xconv_b200: " + msg);
 }
 
+// Decomposed filters uploaded to the library, keyed by their full content
+// (group, K, n_radii, n_angles, radii, ks, coefficients) and compared byte for
+// byte on a hit.  Each handle keeps its device spectra (nb * Ph * Pw * 8 bytes,
+// ~9.7 GB for BASELINE config 5) alive, so the cache is a small LRU.
+struct FilterCache {
+  static constexpr size_t kCapacity = 4;
+  struct Entry {
+    std::vector<unsigned char> key;
+    xc_filter handle;
+  };
+  std::vector<Entry> entries;  // most recently used last
+  ~FilterCache() {
+    for (auto& e : entries) xc_filter_destroy(e.handle);
+  }
+  xc_filter find(const std::vector<unsigned char>& key) {
+    for (size_t i = 0; i < entries.size(); ++i)
+      if (entries[i].key == key) {
+        Entry e = std::move(entries[i]);
+        entries.erase(entries.begin() + long(i));
+        entries.push_back(std::move(e));
+        return entries.back().handle;
+      }
+    return nullptr;
+  }
+  void insert(std::vector<unsigned char> key, xc_filter h) {
+    if (entries.size() >= kCapacity) {
+      xc_filter_destroy(entries.front().handle);
+      entries.erase(entries.begin());
+    }
+    entries.push_back(Entry{std::move(key), h});
+  }
+};
+
+// One library context per host thread (contexts are not shared across
+// threads, include/xconv_b200.h).  The devices it runs on come from
+// XCB_DEVICES ("0,1,2,3"; default: device 0); with several devices xc_run
+// shards the bands (gather/scatter) over them and reduces with NCCL.
+inline std::vector<int> env_devices() {
+  std::vector<int> ids;
+  if (const char* e = std::getenv("XCB_DEVICES")) {
+    std::string s(e);
+    size_t pos = 0;
+    while (pos < s.size()) {
+      size_t end = s.find(',', pos);
+      if (end == std::string::npos) end = s.size();
+      if (end > pos) ids.push_back(std::atoi(s.substr(pos, end - pos).c_str()));
+      pos = end + 1;
+    }
+  }
+  if (ids.empty()) ids.push_back(0);
+  return ids;
+}
+
 struct Context {
   xc_context ctx = nullptr;
-  std::map<uint64_t, xc_filter> filters;
-  Context() { check(xc_context_create(0, &ctx), nullptr); }
+  FilterCache filters;
+  Context() {
+    const std::vector<int> ids = env_devices();
+    if (ids.size() == 1)
+      check(xc_context_create(ids[0], &ctx), nullptr);
+    else
+      check(xc_context_create_multi(int(ids.size()), ids.data(), &ctx), nullptr);
+  }
   ~Context() {
-    for (auto& kv : filters) xc_filter_destroy(kv.second);
+    for (auto& e : filters.entries) xc_filter_destroy(e.handle);  // before the context
+    filters.entries.clear();
     xc_context_destroy(ctx);
   }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
 };
 
 inline Context& context() {
@@ -62,10 +125,9 @@ inline Context& context() {
   return c;
 }
 
-inline uint64_t fnv(uint64_t h, const void* p, size_t n) {
+inline void append(std::vector<unsigned char>& k, const void* p, size_t n) {
   const unsigned char* b = static_cast<const unsigned char*>(p);
-  for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
-  return h;
+  k.insert(k.end(), b, b + n);
 }
 
 // FreqFilter2<Real> -> xc_filter (cached by content)
@@ -82,19 +144,19 @@ xc_filter filter_handle(const F& f) {
     }
   const int group = static_cast<int>(f.group);
   const double sc[3] = {double(f.r_max), double(f.r_min), double(f.r_domain)};
-  const int ints[4] = {group, f.K, f.n_radii, f.n_angles};
-  uint64_t h = 1469598103934665603ull;
-  h = fnv(h, ints, sizeof(ints));
-  h = fnv(h, sc, sizeof(sc));
-  h = fnv(h, f.ks.data(), f.ks.size() * sizeof(int));
-  h = fnv(h, comps.data(), comps.size() * sizeof(double));
-  auto it = c.filters.find(h);
-  if (it != c.filters.end()) return it->second;
+  const int ints[5] = {group, f.K, f.n_radii, f.n_angles, nc};
+  std::vector<unsigned char> key;
+  key.reserve(sizeof(ints) + sizeof(sc) + f.ks.size() * sizeof(int) + comps.size() * 8);
+  append(key, ints, sizeof(ints));
+  append(key, sc, sizeof(sc));
+  append(key, f.ks.data(), f.ks.size() * sizeof(int));
+  append(key, comps.data(), comps.size() * sizeof(double));
+  if (xc_filter hit = c.filters.find(key)) return hit;
   xc_filter out = nullptr;
   check(xc_filter_create(c.ctx, group, f.K, f.ks.data(), nc, comps.data(), f.n_radii,
                          f.n_angles, sc[0], sc[1], sc[2], &out),
         nullptr);
-  c.filters[h] = out;
+  c.filters.insert(std::move(key), out);
   return out;
 }
 

@@ -403,6 +403,45 @@ def anglemax(G, ks, n_angles=360):
     return score, arg
 
 
+def band_responses(H, F, ks=None, nthreads=1) -> np.ndarray:
+    """(nk, h, w) complex G_k = H (*) F_k (correlation, no steering)."""
+    H = _c128(H)
+    h, w = H.shape
+    ks = np.ascontiguousarray(np.asarray(F.ks if ks is None else ks, np.int32))
+    G = np.zeros((len(ks), h, w), np.complex128)
+    cf = _cfilter(F)
+    _check(lib().or_band_responses(_dp(H.view(np.float64)), h, w, C.byref(cf), _ip(ks),
+                                   len(ks), int(nthreads), _dp(G.view(np.float64))))
+    return G
+
+
+def anglemax_mt(G, ks, n_angles=360, nthreads=1):
+    """anglemax() with rows split across threads (same max / first-argmax)."""
+    G = _c128(G)
+    ks = np.ascontiguousarray(np.asarray(ks, np.int32))
+    nc, h, w = G.shape
+    score = np.zeros((h, w))
+    arg = np.zeros((h, w), np.int32)
+    lib().or_anglemax_mt(_dp(G.view(np.float64)), _ip(ks), nc, h, w, int(n_angles),
+                         int(nthreads), _dp(score), _ip(arg))
+    return score, arg
+
+
+def direct_at(mode, H, kind, param, F, pys, pxs, nthreads=1) -> np.ndarray:
+    """xcorr_fast (mode 0) / xconv_fast (mode 1) at pixels (pys, pxs) by direct
+    summation over the rendered bands (no FFT)."""
+    H = _c128(H)
+    h, w = H.shape
+    pys = np.ascontiguousarray(np.asarray(pys, np.int32))
+    pxs = np.ascontiguousarray(np.asarray(pxs, np.int32))
+    out = np.zeros(len(pys), np.complex128)
+    cf = _cfilter(F)
+    _check(lib().or_direct_at(int(mode), _dp(H.view(np.float64)), h, w, int(kind),
+                              _dp(_f64(param)), C.byref(cf), _ip(pys), _ip(pxs), len(pys),
+                              int(nthreads), _dp(out.view(np.float64))))
+    return out
+
+
 # ------------------------------------------------------------------ fixtures
 
 class Rng:

@@ -1253,6 +1253,142 @@ void or_anglemax(const double* G, const int* ks, int nc, int h, int w, int n_ang
   }
 }
 
+// ---------------------------------------------------------------- full-size checks
+// Helpers for the full-size parity tests (test infrastructure).  Each is the
+// reference arithmetic above, split across threads where the reference loop
+// is independent per band or per pixel.
+
+// G_k = filter2_fft(H, F_k, correlate) for each selected band (the per-band
+// term of xcorr_fast before steering, engine.hpp:301-311), threads over bands.
+int or_band_responses(const double* Hd, int h, int w, const or_filter* Fc, const int* ks,
+                      int nk, int nthreads, double* Gout) {
+  return guarded([&] {
+    const Filter F = to_filter(Fc);
+    const int R = int(std::ceil(F.r_max));
+    const size_t N = size_t(h) * w;
+    auto H = to_cd(Hd, N);
+    nthreads = std::max(1, std::min(nthreads, nk));
+    auto run = [&](int tid) {
+      for (int bi = tid; bi < nk; bi += nthreads) {
+        auto Fk = render_component(F, F.index_of(ks[bi]), 2 * R + 1, 2 * R + 1, double(R),
+                                   double(R));
+        auto Gk = filter2_fft(H.data(), h, w, Fk.data(), 2 * R + 1, 2 * R + 1, R, R, true,
+                              false);
+        std::memcpy(Gout + 2 * N * size_t(bi), Gk.data(), N * sizeof(cd));
+      }
+    };
+    std::vector<std::thread> th;
+    for (int t = 0; t < nthreads; ++t) th.emplace_back(run, t);
+    for (auto& t : th) t.join();
+  });
+}
+
+// or_anglemax with rows split across threads and the e^{-i k 2 pi s / n}
+// factors tabulated per (s, band); same max / first-argmax rule.
+void or_anglemax_mt(const double* G, const int* ks, int nc, int h, int w, int n_angles,
+                    int nthreads, double* score, int* argmax) {
+  const size_t N = size_t(h) * w;
+  std::vector<cd> tab(size_t(n_angles) * nc);
+  for (int s = 0; s < n_angles; ++s)
+    for (int c = 0; c < nc; ++c) {
+      const long long e = (((long long)ks[c] * s) % n_angles + n_angles) % n_angles;
+      const double a = -2.0 * kPi * double(e) / n_angles;
+      tab[size_t(s) * nc + c] = cd(std::cos(a), std::sin(a));
+    }
+  nthreads = std::max(1, std::min(nthreads, h));
+  auto run = [&](int tid) {
+    std::vector<cd> g(nc);
+    for (int y = tid; y < h; y += nthreads)
+      for (int x = 0; x < w; ++x) {
+        const size_t p = size_t(y) * w + x;
+        for (int c = 0; c < nc; ++c)
+          g[c] = cd(G[2 * (size_t(c) * N + p)], G[2 * (size_t(c) * N + p) + 1]);
+        double best = -1;
+        int arg = 0;
+        for (int s = 0; s < n_angles; ++s) {
+          const cd* t = tab.data() + size_t(s) * nc;
+          double re = 0, im = 0;
+          for (int c = 0; c < nc; ++c) {
+            re += t[c].real() * g[c].real() - t[c].imag() * g[c].imag();
+            im += t[c].real() * g[c].imag() + t[c].imag() * g[c].real();
+          }
+          const double m = std::sqrt(re * re + im * im);
+          if (m > best) {
+            best = m;
+            arg = s;
+          }
+        }
+        score[p] = best;
+        argmax[p] = arg;
+      }
+  };
+  std::vector<std::thread> th;
+  for (int t = 0; t < nthreads; ++t) th.emplace_back(run, t);
+  for (auto& t : th) t.join();
+}
+
+// xcorr_fast / xconv_fast evaluated directly (no FFT) at selected pixels:
+// the bands are rendered once (render_component, freq_filter.hpp:173-184) and
+// the zero-padded linear filtering of fft.hpp:74-77 is summed tap by tap,
+// then steered as engine.hpp:312-317 / 353-366 (+ the inner-DC term).
+int or_direct_at(int mode, const double* Hd, int h, int w, int kind, const double* param,
+                 const or_filter* Fc, const int* pys, const int* pxs, int npix, int nthreads,
+                 double* outd) {
+  return guarded([&] {
+    const Filter F = to_filter(Fc);
+    const Xform T = make_xform(kind, param, h, w);
+    const int R = int(std::ceil(F.r_max)), S = 2 * R + 1;
+    const int nb = F.nc();
+    std::vector<std::vector<cd>> Fk(nb);
+    for (int ci = 0; ci < nb; ++ci)
+      Fk[ci] = render_component(F, ci, S, S, double(R), double(R));
+    const cd dc = inner_dc_value(F);
+    auto phase = [&](int ci, size_t i) {
+      return T.kind == 0 ? double(F.ks[ci]) * T.angle[i]
+                         : double(F.ks[ci]) * F.omega() * T.log_scale[i];
+    };
+    auto Hat = [&](int x, int y) {
+      return cd(Hd[2 * (size_t(y) * w + x)], Hd[2 * (size_t(y) * w + x) + 1]);
+    };
+    nthreads = std::max(1, std::min(nthreads, npix));
+    auto run = [&](int tid) {
+      for (int t = tid; t < npix; t += nthreads) {
+        const int py = pys[t], px = pxs[t];
+        cd acc(0);
+        for (int ci = 0; ci < nb; ++ci) {
+          cd band(0);
+          for (int dy = -R; dy <= R; ++dy)
+            for (int dx = -R; dx <= R; ++dx) {
+              const cd fv = Fk[ci][size_t(dy + R) * S + (dx + R)];
+              if (mode == 0) {  // out(p) = sum_u conj(F(u)) H(p+u)
+                const int qx = px + dx, qy = py + dy;
+                if (qx < 0 || qy < 0 || qx >= w || qy >= h) continue;
+                band += std::conj(fv) * Hat(qx, qy);
+              } else {  // out(p) = sum_u F(u) (H e^{-i phi})(p-u)
+                const int qx = px - dx, qy = py - dy;
+                if (qx < 0 || qy < 0 || qx >= w || qy >= h) continue;
+                const double a = phase(ci, size_t(qy) * w + qx);
+                band += fv * Hat(qx, qy) * cd(std::cos(-a), std::sin(-a));
+              }
+            }
+          if (mode == 0) {
+            const double a = phase(ci, size_t(py) * w + px);
+            acc += band * cd(std::cos(a), std::sin(a));
+          } else {
+            acc += band;
+          }
+        }
+        if (T.kind == 1) acc += (mode == 0 ? std::conj(dc) : dc) * Hat(px, py);
+        outd[2 * t] = acc.real();
+        outd[2 * t + 1] = acc.imag();
+      }
+    };
+    std::vector<std::thread> th;
+    for (int t = 0; t < nthreads; ++t) th.emplace_back(run, t);
+    for (auto& t : th) t.join();
+  });
+}
+
 // ---------------------------------------------------------------- fixtures
 // proj/tests/helpers.hpp; the argument-evaluation order of
 // Cx<double>(u(rng), u(rng)) is the compiler's, as in the reference build.

@@ -158,6 +158,17 @@ void or_random_smooth_filter3(void* rng, int radius, int n_bumps, double envelop
                               double* out);
 void or_random_rotation3_field(void* rng, int n, double* out);
 
+/* Full-size parity helpers (threaded; same arithmetic as the loops above). */
+/* G: nk planes [h][w] complex, G_k = filter2_fft(H, F_k, correlate). */
+int or_band_responses(const double* H, int h, int w, const or_filter* F, const int* ks,
+                      int nk, int nthreads, double* G);
+void or_anglemax_mt(const double* G, const int* ks, int nc, int h, int w, int n_angles,
+                    int nthreads, double* score, int* argmax);
+/* xcorr_fast / xconv_fast by direct summation at npix pixels (no FFT). */
+int or_direct_at(int mode, const double* H, int h, int w, int kind, const double* param,
+                 const or_filter* F, const int* pys, const int* pxs, int npix, int nthreads,
+                 double* out);
+
 #ifdef __cplusplus
 }
 #endif

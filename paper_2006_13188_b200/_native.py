@@ -20,6 +20,7 @@ XC_F32, XC_F64, XC_C64, XC_C128 = 0, 1, 2, 3
 XC_ROW_MAJOR, XC_COL_MAJOR = 0, 1
 XC_HOST, XC_DEVICE = 0, 1
 XC_FLAG_PERIODIC, XC_FLAG_NO_INNER_DC, XC_FLAG_ACCUMULATE = 1, 2, 4
+XC_SHARD_BANDS, XC_SHARD_BATCH = 0, 1
 
 
 class ImageDesc(C.Structure):
@@ -47,7 +48,8 @@ EXPORTS = [
     "xc_build_vote_filter", "xc_build_optimal_filter", "xc_detect_pattern",
     "xc_find_peaks_device", "xc_filter3_create", "xc_filter3_destroy", "xc_decompose_rotation3",
     "xc_render_sph_component", "xc_reconstruct3", "xc_sph_harm", "xc_wigner_d", "xc_run3",
-    "xc_white_noise",
+    "xc_white_noise", "xc_nccl_unique_id", "xc_context_create_multi", "xc_context_create_rank",
+    "xc_context_set_sharding", "xc_context_devices",
 ]
 
 _lib = None
@@ -108,6 +110,11 @@ def lib():
         L.xc_wigner_d.argtypes = [i, dp, dp]
         L.xc_white_noise.argtypes = [C.c_ulonglong, i, i, i, dp]
         L.xc_run3.argtypes = [vp, vp, i, i, i, i, vp, i, vp, ip, i, i, vp, C.POINTER(Stats)]
+        L.xc_nccl_unique_id.argtypes = [vp]
+        L.xc_context_create_multi.argtypes = [i, ip, C.POINTER(vp)]
+        L.xc_context_create_rank.argtypes = [i, vp, i, i, C.POINTER(vp)]
+        L.xc_context_set_sharding.argtypes = [vp, i]
+        L.xc_context_devices.argtypes = [vp, ip, ip]
         L.xc_profile_enable.argtypes = [vp, i]
         L.xc_profile_reset.argtypes = [vp]
         L.xc_profile_get.argtypes = [vp, i, C.c_char_p, i, dp, C.POINTER(C.c_longlong)]
@@ -124,15 +131,54 @@ def check(rc: int, ctx=None):
     raise RuntimeError(f"xconv_b200 error {rc}: {msg}")
 
 
-class Context:
-    """One CUDA context handle (xc_context) on one device."""
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (128 bytes) for Context.rank()."""
+    buf = C.create_string_buffer(128)
+    check(lib().xc_nccl_unique_id(buf), None)
+    return buf.raw
 
-    def __init__(self, device: int = 0):
-        L = lib()
-        h = C.c_void_p()
-        check(L.xc_context_create(int(device), C.byref(h)), None)
-        self.handle = h
+
+class Context:
+    """One xc_context: a single device, or (Context.multi / Context.rank) a
+    group whose xc_run / xc_smooth shard the bands across GPUs and reduce
+    with NCCL inside the library."""
+
+    def __init__(self, device: int = 0, _handle=None):
+        if _handle is None:
+            L = lib()
+            h = C.c_void_p()
+            check(L.xc_context_create(int(device), C.byref(h)), None)
+            _handle = h
+        self.handle = _handle
         self.device = device
+
+    @classmethod
+    def multi(cls, devices, shard: int = XC_SHARD_BANDS) -> "Context":
+        """One process driving several devices (a device listed twice reduces
+        with peer copies instead of NCCL)."""
+        ids = (C.c_int * len(devices))(*[int(d) for d in devices])
+        h = C.c_void_p()
+        check(lib().xc_context_create_multi(len(devices), ids, C.byref(h)), None)
+        c = cls(int(devices[0]), _handle=h)
+        if shard != XC_SHARD_BANDS:
+            check(lib().xc_context_set_sharding(h, int(shard)), h)
+        return c
+
+    @classmethod
+    def rank(cls, device: int, nccl_id: bytes, rank: int, nranks: int) -> "Context":
+        """One process per GPU: every rank calls with the same arguments, rank 0
+        receives the band-summed result."""
+        buf = C.create_string_buffer(bytes(nccl_id), 128)
+        h = C.c_void_p()
+        check(lib().xc_context_create_rank(int(device), buf, int(rank), int(nranks), C.byref(h)),
+              None)
+        return cls(int(device), _handle=h)
+
+    def devices(self):
+        """(number of devices or ranks, whether the reduce is NCCL)."""
+        n, u = C.c_int(), C.c_int()
+        check(lib().xc_context_devices(self.handle, C.byref(n), C.byref(u)), self.handle)
+        return n.value, bool(u.value)
 
     def set_stream(self, stream_ptr: int | None):
         check(lib().xc_context_set_stream(self.handle, C.c_void_p(stream_ptr or 0)), self.handle)

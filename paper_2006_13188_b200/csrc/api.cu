@@ -13,6 +13,9 @@
 //     max|den|, floored divide
 //   anglemax: gather's per-band responses G_k -> max_s |sum_k e^{-iks} G_k|
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <functional>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -25,6 +28,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -73,10 +77,15 @@ struct StageTotal {
   long long launches = 0;
 };
 
+// multi-device / multi-rank state of a context (defined with the group layer)
+struct Group;
+void destroy_group(Group* g);
+
 }  // namespace
 
 struct xc_context_s {
   int device = 0;
+  Group* group = nullptr;  // set for xc_context_create_multi / _rank contexts
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   cudaStream_t cp_in = nullptr, cp_out = nullptr;  // host-memory copy pipeline
@@ -124,6 +133,7 @@ struct xc_context_s {
   }
 
   ~xc_context_s() {
+    if (group) destroy_group(group);
     cudaSetDevice(device);
     for (auto& kv : plans) cudaFree(kv.second.tw);
     for (auto& kv : fast_plans) cudaFree(kv.second.tw);
@@ -196,6 +206,9 @@ struct xc_context_s {
 // it is not bound to a context, so host-only calls need no GPU.
 struct xc_filter_s {
   xcb::HostFilter hf;
+  // A filter handle may be shared by callers on several threads, each with its
+  // own context: `mu` guards the spectrum cache and the integral check.
+  std::mutex mu;
   std::map<std::tuple<int, int, int, int>, float2*> spectra;  // (dev, Ph, Pw, transposed)
   int integral_state = -1;  // smooth_adaptive zero-integral check cache
   ~xc_filter_s() {
@@ -279,6 +292,7 @@ struct Call {
   xcb::LaunchCounter lc;
   cudaStream_t st;
   double h2d_s = 0, d2h_s = 0;
+  bool out_dev = false;  // outputs are device buffers even when d.memory == XC_HOST
 };
 
 std::vector<int> plan_components(const xcb::HostFilter& hf, const int* comps, int n) {
@@ -293,6 +307,7 @@ std::vector<int> plan_components(const xcb::HostFilter& hf, const int* comps, in
 
 float2* filter_spectra(Call& c) {
   const auto key = std::make_tuple(c.ctx->device, c.g.Ph, c.g.Pw, c.transposed);
+  std::lock_guard<std::mutex> flk(c.f->mu);  // one build per key across threads
   auto it = c.f->spectra.find(key);
   if (it != c.f->spectra.end()) return it->second;
   const xcb::HostFilter& hf = c.f->hf;
@@ -433,13 +448,15 @@ struct Staged {
 // D2H of image i-1 (cp_out) overlap the kernels of image i (compute stream).
 struct HostPipe {
   Call* c = nullptr;
-  bool host = false;
+  bool host = false;      // inputs in host memory
+  bool host_out = false;  // outputs in host memory
   static constexpr int NS = 4;  // slots: two groups of up to two images in flight
   cudaEvent_t in_done[NS]{}, comp_done[NS]{}, out_done[NS]{}, t0{}, t1{};
   int issued = 0;
   // events come from the context's pool (released when the call returns)
-  explicit HostPipe(Call& call) : c(&call), host(call.d.memory == XC_HOST) {
-    if (!host) return;
+  explicit HostPipe(Call& call)
+      : c(&call), host(call.d.memory == XC_HOST), host_out(call.d.memory == XC_HOST && !call.out_dev) {
+    if (!host && !host_out) return;
     for (int s = 0; s < NS; ++s) {
       in_done[s] = call.ctx->event(false);
       comp_done[s] = call.ctx->event(false);
@@ -497,16 +514,17 @@ struct HostPipe {
   }
   // output buffer of image img (device: the caller's; host: a slot stage)
   void* out_buffer(void* out, int img, size_t os) {
-    if (!host) return static_cast<char*>(out) + size_t(img) * npix() * os;
+    if (!host_out) return static_cast<char*>(out) + size_t(img) * npix() * os;
     const int s = img % NS;
     if (img >= NS) ck(cudaStreamWaitEvent(c->st, out_done[s], 0), "wait");
     return c->ctx->buf<char>(slot_name("out_stage", s), npix() * os);
   }
   // after image img's kernels: start its D2H (host memory)
   void done(void* out, int img, void* dout, size_t os) {
-    if (!host) return;
+    if (!host && !host_out) return;
     const int s = img % NS;
-    ck(cudaEventRecord(comp_done[s], c->st), "event");
+    ck(cudaEventRecord(comp_done[s], c->st), "event");  // input slot s free again
+    if (!host_out) return;
     ck(cudaStreamWaitEvent(c->ctx->cp_out, comp_done[s], 0), "wait");
     ck(cudaMemcpyAsync(static_cast<char*>(out) + size_t(img) * npix() * os, dout, npix() * os,
                        cudaMemcpyDeviceToHost, c->ctx->cp_out),
@@ -514,7 +532,7 @@ struct HostPipe {
     ck(cudaEventRecord(out_done[s], c->ctx->cp_out), "event");
   }
   void finish() {
-    if (host) ck(cudaStreamSynchronize(c->ctx->cp_out), "D2H");
+    if (host_out) ck(cudaStreamSynchronize(c->ctx->cp_out), "D2H");
     ck(cudaStreamSynchronize(c->st), "compute");
   }
 };
@@ -528,38 +546,65 @@ Staged stage_inputs(Call& c, const void* signal, const void* param, int img) {
   return s;
 }
 
-// base (steering phase per pixel) + optional weights; throws the reference's
-// guard-band / positivity errors for scale fields (engine.hpp:267-279,
-// field.hpp:150-153).
+// base (steering phase per pixel) + optional weights.  For scale fields the
+// kernel also records, per image, the first y-major pixel that is not positive
+// and finite and the first outside the guard band (engine.hpp:267-279,
+// field.hpp:150-153); guard_check() reads all images' slots back once per call.
+void guard_begin(Call& c) {
+  if (c.f->hf.group != XC_SCALE2) return;
+  unsigned long long* bad = c.ctx->buf<unsigned long long>("bad", 2 * size_t(c.d.batch));
+  ck(cudaMemsetAsync(bad, 0xff, 2 * size_t(c.d.batch) * sizeof(unsigned long long), c.st),
+     "memset");
+}
+
 void prep(Call& c, const Staged& s, bool want_wgt, double** base_out, float** wgt_out,
-          int slot = 0) {
+          int slot = 0, int img = 0) {
   const size_t npix = size_t(c.rows) * c.cols;
   double* base = c.ctx->buf<double>("base" + std::to_string(slot), npix);
-  float* wgt = want_wgt ? c.ctx->buf<float>("wgt", npix) : nullptr;
+  float* wgt = want_wgt ? c.ctx->buf<float>("wgt" + std::to_string(slot), npix) : nullptr;
   const xcb::HostFilter& hf = c.f->hf;
   const bool scale = hf.group == 1;
-  unsigned long long* bad = c.ctx->buf<unsigned long long>("bad", 2);
+  unsigned long long* bad =
+      scale ? c.ctx->buf<unsigned long long>("bad", 2 * size_t(c.d.batch)) + 2 * size_t(img)
+            : nullptr;
   const double lo = scale ? hf.r_min / hf.domain_top() : 0, hi = scale ? hf.domain_top() / hf.r_min : 0;
-  if (scale) ck(cudaMemsetAsync(bad, 0xff, 2 * sizeof(unsigned long long), c.st), "memset");
   stage(c, "prep", [&] {
     xcb::launch_prep(s.param, s.param_f64, hf.group, scale ? hf.omega() : 0.0, lo, hi, c.rows,
                      c.cols, c.transposed, base, wgt, bad, c.st, c.lc);
   });
-  if (scale) {
-    unsigned long long hbad[2];
-    ck(cudaMemcpyAsync(hbad, bad, sizeof(hbad), cudaMemcpyDeviceToHost, c.st), "guard readback");
-    ck(cudaStreamSynchronize(c.st), "guard");
-    if (hbad[0] != ~0ull)
+  *base_out = base;
+  if (wgt_out) *wgt_out = wgt;
+}
+
+// One readback per call: throw the reference's error for the first image (in
+// batch order) whose scale field failed, naming its first offending pixel.
+// `param` is the caller's pointer (d.memory), not a staging slot.
+void guard_check(Call& c, const void* param) {
+  if (c.f->hf.group != XC_SCALE2) return;
+  const int B = c.d.batch;
+  std::vector<unsigned long long> hbad(2 * size_t(B));
+  ck(cudaMemcpyAsync(hbad.data(), c.ctx->buf<unsigned long long>("bad", 2 * size_t(B)),
+                     hbad.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.st),
+     "guard readback");
+  ck(cudaStreamSynchronize(c.st), "guard");
+  const xcb::HostFilter& hf = c.f->hf;
+  const double lo = hf.r_min / hf.domain_top(), hi = hf.domain_top() / hf.r_min;
+  const size_t npix = size_t(c.rows) * c.cols, ps = dtype_size(c.d.param_dtype);
+  for (int img = 0; img < B; ++img) {
+    if (hbad[2 * img] != ~0ull)
       throw std::invalid_argument("scale field must be strictly positive and finite");
-    if (hbad[1] != ~0ull) {
-      const unsigned long long ti = hbad[1];
+    if (hbad[2 * img + 1] != ~0ull) {
+      const unsigned long long ti = hbad[2 * img + 1];
       const int W = c.d.width;  // true (un-transposed) width
       const int x = int(ti % W), y = int(ti / W);
-      const size_t si = c.transposed ? size_t(x) * c.d.height + y : size_t(y) * c.d.width + x;
+      const size_t si = (c.transposed ? size_t(x) * c.d.height + y : size_t(y) * c.d.width + x) +
+                        (c.d.param_per_image ? size_t(img) * npix : 0);
       double sv = 0;
-      const size_t ps = dtype_size(c.d.param_dtype);
-      ck(cudaMemcpy(&sv, static_cast<const char*>(s.param) + si * ps, ps, cudaMemcpyDeviceToHost),
-         "guard value");
+      const char* src = static_cast<const char*>(param) + si * ps;
+      if (c.d.memory == XC_HOST)
+        std::memcpy(&sv, src, ps);
+      else
+        ck(cudaMemcpy(&sv, src, ps, cudaMemcpyDeviceToHost), "guard value");
       if (ps == 4) {
         float fv;
         std::memcpy(&fv, &sv, 4);
@@ -571,8 +616,6 @@ void prep(Call& c, const Staged& s, bool want_wgt, double** base_out, float** wg
                                   std::to_string(hi) + "]");
     }
   }
-  *base_out = base;
-  if (wgt_out) *wgt_out = wgt;
 }
 
 // XCB_PAIR=0 selects the previous (fast) band-loop kernels, for A/B timing
@@ -813,7 +856,7 @@ void run_gather_dual(Call& c, HostPipe& hp, const void* signal, const void* para
     if (img < B) {
       hp.h2d(signal, param, img + 1);
       Staged st = hp.inputs(signal, param, img);
-      prep(c, st, false, &base[s], nullptr, s);
+      prep(c, st, false, &base[s], nullptr, s, img);
       if (img == 0) {
         bands = gather_bands(c, &st.sig, 1, &half);
         for (int i = 0; i < 2; ++i)
@@ -856,6 +899,15 @@ void fill_stats(Call& c, xc_stats* st, double gpu_s, double total_s, long long o
   st->seconds_total = total_s;
   st->gpu_launches = c.lc.n;
 }
+
+void run_single(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d,
+                const void* signal, const void* param, const int* components, int n_components,
+                unsigned flags, void* out, xc_stats* stats, bool out_dev);
+void run_group(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d,
+               const void* signal, const void* param, const int* components, int n_components,
+               unsigned flags, void* out, xc_stats* stats);
+void smooth_group(xc_context ctx, xc_filter f, const xc_image_desc* d, const void* signal,
+                  const void* param, int normalize_signal, void* out, xc_stats* stats);
 
 }  // namespace
 
@@ -1015,12 +1067,15 @@ int xc_inner_dc_value(xc_filter f, double* out2) {
   });
 }
 
-int xc_run(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d, const void* signal,
-           const void* param, const int* components, int n_components, unsigned flags,
-           void* out, xc_stats* stats) {
-  return guarded(ctx, [&] {
-    if (!ctx) throw std::invalid_argument("null context");
-    std::lock_guard<std::mutex> lk(ctx->mu);
+}  // extern "C"
+
+namespace {
+
+// xcorr_fast / xconv_fast on one device (the caller holds ctx->mu).  out_dev:
+// `out` is a device buffer even when d->memory == XC_HOST (multi-device partials).
+void run_single(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d,
+                const void* signal, const void* param, const int* components, int n_components,
+                unsigned flags, void* out, xc_stats* stats, bool out_dev) {
     ck(cudaSetDevice(ctx->device), "cudaSetDevice");
     const auto t_start = std::chrono::steady_clock::now();
     if (mode != XC_CORRELATION && mode != XC_CONVOLUTION) throw std::invalid_argument("unknown mode");
@@ -1028,8 +1083,10 @@ int xc_run(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d, const 
     if (d && d->out_dtype != XC_C64 && d->out_dtype != XC_C128)
       throw std::invalid_argument("xc_run output must be complex (XC_C64 / XC_C128)");
     Call c = setup(ctx, f, d, -1, components, n_components, (flags & XC_FLAG_PERIODIC) != 0);
+    c.out_dev = out_dev;
+    guard_begin(c);
     const bool accumulate = (flags & XC_FLAG_ACCUMULATE) != 0;
-    if (accumulate && d->memory != XC_DEVICE)
+    if (accumulate && d->memory != XC_DEVICE && !out_dev)
       throw std::invalid_argument("XC_FLAG_ACCUMULATE needs device memory");
     const bool dc = c.f->hf.group == XC_SCALE2 && !(flags & XC_FLAG_NO_INNER_DC);
     const size_t npix = size_t(c.rows) * c.cols, os = dtype_size(d->out_dtype);
@@ -1054,7 +1111,7 @@ int xc_run(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d, const 
         xcb::SigSrc sg[2];
         for (int i = 0; i < 2; ++i) {
           s[i] = hp.inputs(signal, param, img + i);
-          prep(c, s[i], false, &base[i], nullptr, i);
+          prep(c, s[i], false, &base[i], nullptr, i, img + i);
           dout[i] = hp.out_buffer(out, img + i, os);
           sg[i] = s[i].sig;
         }
@@ -1064,7 +1121,7 @@ int xc_run(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d, const 
       } else {
         Staged s = hp.inputs(signal, param, img);
         double* base = nullptr;
-        prep(c, s, false, &base, nullptr);
+        prep(c, s, false, &base, nullptr, 0, img);
         void* dout = hp.out_buffer(out, img, os);
         if (mode == XC_CORRELATION)
           run_gather(c, s.sig, base, dout, out_kind, accumulate, dc);
@@ -1077,91 +1134,195 @@ int xc_run(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d, const 
     }
     ck(cudaEventRecord(e1, c.st), "event");
     hp.finish();
+    guard_check(c, param);
     gpu_s = event_seconds(e0, e1);
     ctx->resolve_profile();
     fill_stats(c, stats, gpu_s,
                std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count(),
                (long long)c.ks.size());
+}
+
+}  // namespace
+
+extern "C" {
+
+int xc_run(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d, const void* signal,
+           const void* param, const int* components, int n_components, unsigned flags,
+           void* out, xc_stats* stats) {
+  return guarded(ctx, [&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (ctx->group)
+      run_group(ctx, f, mode, d, signal, param, components, n_components, flags, out, stats);
+    else
+      run_single(ctx, f, mode, d, signal, param, components, n_components, flags, out, stats,
+                 false);
   });
 }
+
+}  // extern "C"
+
+namespace {
+
+// engine.hpp:388-392: zero-integral filters cannot be normalized (cached per filter)
+void check_integral(xc_filter f) {
+  if (!f) throw std::invalid_argument("null argument");
+  std::lock_guard<std::mutex> flk(f->mu);
+  if (f->integral_state < 0) {
+    const xcb::HostFilter& hf = f->hf;
+    const int R = hf.render_radius(), S = 2 * R + 1;
+    std::vector<cplx> full(size_t(S) * S);
+    xcb::reconstruct(hf, S, S, R, R, nullptr, -1, false, full.data());
+    cplx integral(0);
+    double mx = 0;
+    for (auto& v : full) {
+      integral += v;
+      mx = std::max(mx, std::abs(v));
+    }
+    f->integral_state = std::abs(integral) < 1e-12 * std::max(1.0, mx) ? 0 : 1;
+  }
+  if (f->integral_state == 0)
+    throw std::invalid_argument("normalization undefined: filter has zero integral");
+}
+
+struct SmoothPart {
+  double gpu_s = 0, h2d_s = 0;
+  int launches = 0, pad_h = 0, pad_w = 0;
+  long long bands = 0;
+};
+
+// The two extended convolutions of smooth_adaptive (engine.hpp:394-403),
+// num = xconv(H~) and den = xconv(1~), for every image of the batch over the
+// selected bands, into numden[img][0 | 1][npix] (device memory of ctx).
+// Inputs stream through the HostPipe slots (H2D of image i+1 overlaps image
+// i); the scale guard is read back once for the whole batch.  on_image(img)
+// is called after image img's kernels are queued (the single-device path
+// queues its divide and D2H there).
+template <class OnImage>
+SmoothPart smooth_partials(xc_context ctx, xc_filter f, const xc_image_desc* d,
+                           const void* signal, const void* param, int normalize_signal,
+                           const int* comps, int ncomp, bool dc, float2* numden,
+                           OnImage&& on_image) {
+  ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+  Call c = setup(ctx, f, d, -1, comps, ncomp, false);
+  c.out_dev = true;
+  const bool scale = c.f->hf.group == XC_SCALE2;
+  const bool weighted = normalize_signal && scale;  // engine.hpp:396-401
+  const size_t npix = size_t(c.rows) * c.cols;
+  guard_begin(c);
+  ctx->release_events();
+  cudaEvent_t e0 = ctx->event(true), e1 = ctx->event(true);
+  HostPipe hp(c);
+  hp.h2d(signal, param, 0);
+  ck(cudaEventRecord(e0, c.st), "event");
+  for (int img = 0; img < d->batch; ++img) {
+    hp.h2d(signal, param, img + 1);
+    Staged s = hp.inputs(signal, param, img);
+    double* base = nullptr;
+    float* wgt = nullptr;
+    prep(c, s, weighted, &base, weighted ? &wgt : nullptr, 0, img);
+    xcb::SigSrc sn = s.sig, sd = s.sig;
+    sn.wgt = wgt;
+    sn.mode = weighted ? xcb::SIG_TIMES_W : xcb::SIG_PLAIN;
+    sd.wgt = wgt;
+    sd.mode = xcb::SIG_W_ONLY;  // the all-ones signal (times 1/s^2 when weighted)
+    float2* num = numden + 2 * size_t(img) * npix;
+    run_scatter(c, sn, base, num, xcb::OUT_C64, false, dc);
+    run_scatter(c, sd, base, num + npix, xcb::OUT_C64, false, dc);
+    ck(cudaGetLastError(), "kernel launch");
+    hp.done(nullptr, img, nullptr, 0);
+    on_image(c, img);
+  }
+  ck(cudaEventRecord(e1, c.st), "event");
+  hp.finish();
+  guard_check(c, param);
+  SmoothPart r;
+  r.gpu_s = event_seconds(e0, e1);
+  r.launches = c.lc.n;
+  r.pad_h = c.g.Ph;
+  r.pad_w = c.g.Pw;
+  r.bands = (long long)c.ks.size();
+  return r;
+}
+
+// engine.hpp:405-418 for image img: floor 1e-9 max|den|, out = Re(num / den);
+// red[img] holds image img's max bits, red[batch] the clamped total.
+void smooth_divide(xc_context ctx, cudaStream_t st, const float2* numden, size_t npix, int img,
+                   int batch, int out_f64, void* dout, unsigned* red, xcb::LaunchCounter& lc) {
+  const float2* num = numden + 2 * size_t(img) * npix;
+  xcb::launch_smooth_finish(num, num + npix, npix, out_f64, dout, red + img, red + batch, st, lc);
+  ck(cudaGetLastError(), "kernel launch");
+}
+
+void smooth_single(xc_context ctx, xc_filter f, const xc_image_desc* d, const void* signal,
+                   const void* param, int normalize_signal, void* out, xc_stats* stats) {
+  const auto t_start = std::chrono::steady_clock::now();
+  const bool host_out = d->memory == XC_HOST;
+  const size_t npix = size_t(d->height) * d->width, os = dtype_size(d->out_dtype);
+  float2* numden = ctx->buf<float2>("smooth_numden", 2 * npix * size_t(d->batch));
+  unsigned* red = ctx->buf<unsigned>("smooth_red", size_t(d->batch) + 1);
+  char* stage_out = host_out ? ctx->buf<char>("smooth_out", npix * os * size_t(d->batch)) : nullptr;
+  ck(cudaMemsetAsync(red, 0, (size_t(d->batch) + 1) * sizeof(unsigned), ctx->stream), "memset");
+  std::vector<cudaEvent_t> done;
+  xcb::LaunchCounter flc;
+  Call* cp = nullptr;
+  SmoothPart part = smooth_partials(
+      ctx, f, d, signal, param, normalize_signal, nullptr, 0, f->hf.group == XC_SCALE2, numden,
+      [&](Call& c, int img) {
+        cp = &c;
+        char* dout = host_out ? stage_out + size_t(img) * npix * os
+                              : static_cast<char*>(out) + size_t(img) * npix * os;
+        stage(c, "smooth_finish", [&] {
+          smooth_divide(ctx, c.st, numden, npix, img, d->batch, d->out_dtype == XC_F64, dout, red,
+                        flc);
+        });
+        if (host_out) {  // D2H of image img overlaps the next image's kernels
+          cudaEvent_t e = ctx->event(false);
+          ck(cudaEventRecord(e, c.st), "event");
+          ck(cudaStreamWaitEvent(ctx->cp_out, e, 0), "wait");
+          ck(cudaMemcpyAsync(static_cast<char*>(out) + size_t(img) * npix * os, dout, npix * os,
+                             cudaMemcpyDeviceToHost, ctx->cp_out),
+             "D2H");
+        }
+      });
+  (void)cp;
+  unsigned clamped = 0;
+  ck(cudaMemcpyAsync(&clamped, red + d->batch, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                     ctx->stream),
+     "readback");
+  ck(cudaStreamSynchronize(ctx->stream), "smooth");
+  if (host_out) ck(cudaStreamSynchronize(ctx->cp_out), "D2H");
+  ctx->resolve_profile();
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    stats->standard_ops = 2 * part.bands;  // engine.hpp:406 num + den
+    stats->clamped_pixels = int(clamped);
+    stats->pad_h = part.pad_h;
+    stats->pad_w = part.pad_w;
+    stats->seconds_fft = part.gpu_s;
+    stats->seconds_total =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    stats->gpu_launches = part.launches + flc.n;
+  }
+}
+
+}  // namespace
+
+extern "C" {
 
 int xc_smooth(xc_context ctx, xc_filter f, const xc_image_desc* d, const void* signal,
               const void* param, int normalize_signal, void* out, xc_stats* stats) {
   return guarded(ctx, [&] {
     if (!ctx) throw std::invalid_argument("null context");
     std::lock_guard<std::mutex> lk(ctx->mu);
-    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
-    const auto t_start = std::chrono::steady_clock::now();
     if (!signal || !param || !out || !d) throw std::invalid_argument("null argument");
     if (d->out_dtype != XC_F32 && d->out_dtype != XC_F64)
       throw std::invalid_argument("xc_smooth output must be real (XC_F32 / XC_F64)");
-    // engine.hpp:388-392: zero-integral filters cannot be normalized
-    if (f && f->integral_state < 0) {
-      const xcb::HostFilter& hf = f->hf;
-      const int R = hf.render_radius(), S = 2 * R + 1;
-      std::vector<cplx> full(size_t(S) * S);
-      xcb::reconstruct(hf, S, S, R, R, nullptr, -1, false, full.data());
-      cplx integral(0);
-      double mx = 0;
-      for (auto& v : full) {
-        integral += v;
-        mx = std::max(mx, std::abs(v));
-      }
-      f->integral_state = std::abs(integral) < 1e-12 * std::max(1.0, mx) ? 0 : 1;
-    }
-    if (f && f->integral_state == 0)
-      throw std::invalid_argument("normalization undefined: filter has zero integral");
-    Call c = setup(ctx, f, d, -1, nullptr, 0, false);
-    const bool scale = c.f->hf.group == XC_SCALE2;
-    const bool weighted = normalize_signal && scale;  // engine.hpp:396-401
-    const size_t npix = size_t(c.rows) * c.cols, os = dtype_size(d->out_dtype);
-    float2* num = ctx->buf<float2>("smooth_num", npix);
-    float2* den = ctx->buf<float2>("smooth_den", npix);
-    unsigned* red = ctx->buf<unsigned>("smooth_red", 2);
-    long long clamped_total = 0;
-    ctx->release_events();
-    cudaEvent_t e0 = ctx->event(true), e1 = ctx->event(true);
-    double gpu_s = 0;
-    for (int img = 0; img < d->batch; ++img) {
-      Staged s = stage_inputs(c, signal, param, img);
-      ck(cudaEventRecord(e0, c.st), "event");
-      double* base = nullptr;
-      float* wgt = nullptr;
-      prep(c, s, weighted, &base, weighted ? &wgt : nullptr);
-      xcb::SigSrc sn = s.sig, sd = s.sig;
-      sn.wgt = wgt;
-      sn.mode = weighted ? xcb::SIG_TIMES_W : xcb::SIG_PLAIN;
-      sd.wgt = wgt;
-      sd.mode = xcb::SIG_W_ONLY;  // the all-ones signal (times 1/s^2 when weighted)
-      run_scatter(c, sn, base, num, xcb::OUT_C64, false, scale);
-      run_scatter(c, sd, base, den, xcb::OUT_C64, false, scale);
-      ck(cudaMemsetAsync(red, 0, 2 * sizeof(unsigned), c.st), "memset");
-      void* dout = d->memory == XC_DEVICE ? static_cast<char*>(out) + size_t(img) * npix * os
-                                           : ctx->buf<char>("out_stage", npix * os);
-      stage(c, "smooth_finish", [&] {
-        xcb::launch_smooth_finish(num, den, npix, d->out_dtype == XC_F64, dout, red, red + 1,
-                                  c.st, c.lc);
-      });
-      ck(cudaGetLastError(), "kernel launch");
-      ck(cudaEventRecord(e1, c.st), "event");
-      unsigned hred[2];
-      ck(cudaMemcpyAsync(hred, red, sizeof(hred), cudaMemcpyDeviceToHost, c.st), "readback");
-      ck(cudaStreamSynchronize(c.st), "smooth");
-      gpu_s += event_seconds(e0, e1);
-      clamped_total += hred[1];
-      if (d->memory == XC_HOST) {
-        auto t0 = std::chrono::steady_clock::now();
-        ck(cudaMemcpy(static_cast<char*>(out) + size_t(img) * npix * os, dout, npix * os,
-                      cudaMemcpyDeviceToHost),
-           "D2H");
-        c.d2h_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-      }
-    }
-    ctx->resolve_profile();
-    fill_stats(c, stats, gpu_s,
-               std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count(),
-               2LL * (long long)c.ks.size());  // engine.hpp:406 num + den
-    if (stats) stats->clamped_pixels = int(clamped_total);
+    check_integral(f);
+    if (ctx->group)
+      smooth_group(ctx, f, d, signal, param, normalize_signal, out, stats);
+    else
+      smooth_single(ctx, f, d, signal, param, normalize_signal, out, stats);
   });
 }
 
@@ -1534,6 +1695,7 @@ int xc_detect_pattern(xc_context ctx, const xc_image_desc* d, const void* image,
 
 struct xc_filter3_s {
   xcb::HostFilter3 hf;
+  std::mutex mu;  // guards the spectrum cache (handles may be shared across threads)
   std::map<std::tuple<int, int, int, int>, float2*> spectra;  // (dev, px, py, pz)
   ~xc_filter3_s() {
     for (auto& kv : spectra) {
@@ -1556,6 +1718,7 @@ float2* filter3_spectra(xc_context ctx, xc_filter3 f, const xcb::Geo3& g, const 
                         const xcb::FftPlan& pyp, const xcb::FftPlan& pzp, cudaStream_t st,
                         xcb::LaunchCounter& lc) {
   const auto key = std::make_tuple(ctx->device, g.px, g.py, g.pz);
+  std::lock_guard<std::mutex> flk(f->mu);
   auto it = f->spectra.find(key);
   if (it != f->spectra.end()) return it->second;
   const xcb::HostFilter3& hf = f->hf;
@@ -1808,6 +1971,573 @@ int xc_run3(xc_context ctx, xc_filter3 f, int mode, int nx, int ny, int nz, cons
           std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
       stats->gpu_launches = lc.n;
     }
+  });
+}
+
+}  // extern "C"
+
+// ================================================================ multi-device
+// the bands are independent terms of the extended sum
+// (engine.hpp:300-319, 345-368) and XConvPlan::components (engine.hpp:19)
+// selects a band subset, so a context over several GPUs splits the bands in
+// contiguous ranges (balanced to +-1), runs each range on its device and sums
+// the partial outputs with one NCCL reduce onto the first device.  The scale
+// group's inner-DC term (engine.hpp:320-324 / 369-371) is added by the first
+// device only.  smooth_adaptive (engine.hpp:385-419) is nonlinear: the
+// numerator and denominator partials are reduced, then divided on the root.
+//
+//   xc_context_create_multi: one process drives several devices (one child
+//     context and one NCCL communicator per device, ncclCommInitAll).  A device
+//     listed twice (or XCB_REDUCE=peer) uses the peer-copy reduce instead: the
+//     partials are copied to the root with cudaMemcpyPeerAsync and summed in
+//     device order by launch_accumulate -- the same orchestration, testable
+//     on one GPU.
+//   xc_context_create_rank: one process per GPU; every rank calls xc_run /
+//     xc_smooth with the same arguments and its own copy of the inputs, and
+//     rank 0 receives the result (ncclCommInitRank over a shared unique id).
+//
+// XC_SHARD_BATCH splits the images of a batch across the devices instead (no
+// collective; single-process contexts only).
+
+namespace {
+
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int,
+                         ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+// NCCL is loaded on first use (the process's libnccl.so.2 -- torch's if it is
+// already mapped), so single-device use never needs it.
+const NcclApi& nccl() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      const char* e = dlerror();
+      a.why = std::string("cannot load libnccl.so.2: ") + (e ? e : "?");
+      return a;
+    }
+    auto sym = [&](const char* n) { return dlsym(h, n); };
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(sym("ncclGetUniqueId"));
+    a.CommInitAll = reinterpret_cast<decltype(a.CommInitAll)>(sym("ncclCommInitAll"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(sym("ncclCommInitRank"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(sym("ncclCommDestroy"));
+    a.Reduce = reinterpret_cast<decltype(a.Reduce)>(sym("ncclReduce"));
+    a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(sym("ncclGroupStart"));
+    a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
+    a.ok = a.GetUniqueId && a.CommInitAll && a.CommInitRank && a.CommDestroy && a.Reduce &&
+           a.GroupStart && a.GroupEnd && a.GetErrorString;
+    if (!a.ok) a.why = "libnccl.so.2 lacks a required symbol";
+    return a;
+  }();
+  return api;
+}
+
+const NcclApi& nccl_or_throw() {
+  const NcclApi& a = nccl();
+  if (!a.ok) throw CudaError(a.why, XC_ENCCL);
+  return a;
+}
+
+void nck(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw CudaError(std::string(what) + ": " + nccl().GetErrorString(r), XC_ENCCL);
+}
+
+struct Group {
+  std::vector<xc_context> kids;   // single-process: one child context per device
+  std::vector<ncclComm_t> comms;  // one per kid, or the rank's one; empty = peer reduce
+  bool rank_mode = false;
+  int rank = 0, nranks = 1;
+  int shard = XC_SHARD_BANDS;
+  ~Group() {
+    for (ncclComm_t c : comms)
+      if (c) nccl().CommDestroy(c);
+    for (xc_context k : kids) delete k;
+  }
+};
+
+void destroy_group(Group* g) { delete g; }
+
+// contiguous ranges balanced to +-1: 65 bands over 8 devices -> 8,8,8,8,8,8,8,9
+std::pair<int, int> shard_range(int n, int r, int world) {
+  return {int((long long)n * r / world), int((long long)n * (r + 1) / world)};
+}
+
+std::vector<int> shard_bands(const std::vector<int>& ks, int r, int world) {
+  const auto ab = shard_range(int(ks.size()), r, world);
+  return std::vector<int>(ks.begin() + ab.first, ks.begin() + ab.second);
+}
+
+// error of a worker thread, rethrown on the calling thread in device order
+struct KidError {
+  int code = XC_OK;
+  std::string msg;
+  void run(const std::function<void(int)>& fn, int i) {
+    try {
+      fn(i);
+    } catch (const CudaError& e) {
+      code = e.code;
+      msg = e.what();
+    } catch (const std::invalid_argument& e) {
+      code = XC_EINVAL;
+      msg = e.what();
+    } catch (const std::bad_alloc&) {
+      code = XC_ENOMEM;
+      msg = "host allocation failed";
+    } catch (const std::exception& e) {
+      code = XC_EINTERNAL;
+      msg = e.what();
+    }
+  }
+};
+
+struct KidRunner {
+  KidError* e;
+  const std::function<void(int)>* fn;
+  int i;
+  void operator()() const { e->run(*fn, i); }
+};
+
+// fn(i) for every device i, each on its own host thread (kid 0 on this one)
+void for_each_kid(int n, const std::function<void(int)>& fn) {
+  std::vector<KidError> errs(static_cast<size_t>(n));
+  std::vector<std::thread> th;
+  for (int i = 1; i < n; ++i) th.emplace_back(KidRunner{&errs[i], &fn, i});
+  errs[0].run(fn, 0);
+  for (auto& t : th) t.join();
+  for (auto& e : errs) {
+    if (e.code == XC_EINVAL) throw std::invalid_argument(e.msg);
+    if (e.code != XC_OK) throw CudaError(e.msg, e.code);
+  }
+}
+
+// The reduce of `n` per-device buffers of `count` floats / doubles onto
+// bufs[0] (on kids[0]'s device).
+void reduce_to_root(Group& G, const std::vector<void*>& bufs, size_t count, bool f64) {
+  const int n = int(bufs.size());
+  if (n <= 1) return;
+  if (!G.comms.empty()) {
+    const NcclApi& a = nccl_or_throw();
+    nck(a.GroupStart(), "ncclGroupStart");
+    for (int i = 0; i < n; ++i) {
+      ck(cudaSetDevice(G.kids[i]->device), "cudaSetDevice");
+      nck(a.Reduce(bufs[i], bufs[i], count, f64 ? ncclDouble : ncclFloat, ncclSum, 0,
+                   G.comms[i], G.kids[i]->stream),
+          "ncclReduce");
+    }
+    nck(a.GroupEnd(), "ncclGroupEnd");
+    for (int i = 0; i < n; ++i) {
+      ck(cudaSetDevice(G.kids[i]->device), "cudaSetDevice");
+      ck(cudaStreamSynchronize(G.kids[i]->stream), "band reduce");
+    }
+    ck(cudaSetDevice(G.kids[0]->device), "cudaSetDevice");
+    return;
+  }
+  // peer reduce: partials copied to the root and summed in device order
+  xc_context root = G.kids[0];
+  ck(cudaSetDevice(root->device), "cudaSetDevice");
+  const size_t bytes = count * (f64 ? 8 : 4);
+  void* tmp = root->buf<char>("grp_peer_tmp", bytes);
+  xcb::LaunchCounter lc;
+  for (int i = 1; i < n; ++i) {
+    // the kid's partial is complete: its run synchronized its stream
+    ck(cudaMemcpyPeerAsync(tmp, root->device, bufs[i], G.kids[i]->device, bytes, root->stream),
+       "peer copy");
+    xcb::launch_accumulate(bufs[0], tmp, count, f64 ? 1 : 0, root->stream, lc);
+    ck(cudaGetLastError(), "kernel launch");
+  }
+  ck(cudaStreamSynchronize(root->stream), "peer reduce");
+}
+
+// Inputs of images [a, b) on kid k: the caller's pointers when they are host
+// memory or already on k's device, else peer copies from the root device.
+void kid_inputs(xc_context root, xc_context k, const xc_image_desc& d, const void* signal,
+                const void* param, int a, int b, const void** sg, const void** pr) {
+  const size_t npix = size_t(d.height) * d.width;
+  const size_t ss = dtype_size(d.signal_dtype), ps = dtype_size(d.param_dtype);
+  const char* s0 = static_cast<const char*>(signal) + size_t(a) * npix * ss;
+  const char* p0 = param ? static_cast<const char*>(param) +
+                               (d.param_per_image ? size_t(a) * npix * ps : 0)
+                         : nullptr;
+  *sg = s0;
+  *pr = p0;
+  if (d.memory == XC_HOST || k->device == root->device) return;
+  const size_t sb = size_t(b - a) * npix * ss;
+  const size_t pb = (d.param_per_image ? size_t(b - a) : 1) * npix * ps;
+  void* bs = k->buf<char>("grp_sig", sb);
+  ck(cudaMemcpyPeerAsync(bs, k->device, s0, root->device, sb, k->stream), "peer copy signal");
+  *sg = bs;
+  if (p0) {
+    void* bp = k->buf<char>("grp_par", pb);
+    ck(cudaMemcpyPeerAsync(bp, k->device, p0, root->device, pb, k->stream), "peer copy param");
+    *pr = bp;
+  }
+}
+
+// out (d.memory) <- buf (device, on ctx's device): copy, or add for XC_FLAG_ACCUMULATE
+void deliver(xc_context ctx, const xc_image_desc& d, const void* buf, void* out, size_t bytes,
+             bool accumulate, bool f64, xcb::LaunchCounter& lc) {
+  ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+  if (buf == out) return;
+  if (d.memory == XC_HOST) {
+    ck(cudaMemcpyAsync(out, buf, bytes, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+  } else if (accumulate) {
+    xcb::launch_accumulate(out, buf, bytes / (f64 ? 8 : 4), f64 ? 1 : 0, ctx->stream, lc);
+    ck(cudaGetLastError(), "kernel launch");
+  } else {
+    ck(cudaMemcpyAsync(out, buf, bytes, cudaMemcpyDeviceToDevice, ctx->stream), "D2D");
+  }
+  ck(cudaStreamSynchronize(ctx->stream), "deliver");
+}
+
+void merge_stats(xc_stats* out, const std::vector<xc_stats>& st, long long ops, double t0_s) {
+  if (!out) return;
+  std::memset(out, 0, sizeof(*out));
+  out->standard_ops = ops;
+  for (const auto& s : st) {
+    out->pad_h = std::max(out->pad_h, s.pad_h);
+    out->pad_w = std::max(out->pad_w, s.pad_w);
+    out->seconds_fft = std::max(out->seconds_fft, s.seconds_fft);
+    out->seconds_h2d = std::max(out->seconds_h2d, s.seconds_h2d);
+    out->seconds_d2h = std::max(out->seconds_d2h, s.seconds_d2h);
+    out->clamped_pixels += s.clamped_pixels;
+    out->gpu_launches += s.gpu_launches;
+  }
+  out->seconds_total = t0_s;
+}
+
+double since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+void run_group(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d,
+               const void* signal, const void* param, const int* components, int n_components,
+               unsigned flags, void* out, xc_stats* stats) {
+  const auto t_start = std::chrono::steady_clock::now();
+  Group& G = *ctx->group;
+  if (!f || !d || !signal || !param || !out) throw std::invalid_argument("null argument");
+  if (mode != XC_CORRELATION && mode != XC_CONVOLUTION) throw std::invalid_argument("unknown mode");
+  if (d->out_dtype != XC_C64 && d->out_dtype != XC_C128)
+    throw std::invalid_argument("xc_run output must be complex (XC_C64 / XC_C128)");
+  if (d->height < 1 || d->width < 1 || d->batch < 1)
+    throw std::invalid_argument("image dims must be positive");
+  const std::vector<int> ks = plan_components(f->hf, components, n_components);
+  const bool accumulate = (flags & XC_FLAG_ACCUMULATE) != 0;
+  if (accumulate && d->memory != XC_DEVICE)
+    throw std::invalid_argument("XC_FLAG_ACCUMULATE needs device memory");
+  const size_t npix = size_t(d->height) * d->width, os = dtype_size(d->out_dtype);
+  const size_t bytes = npix * size_t(d->batch) * os;
+  const bool f64 = d->out_dtype == XC_C128;
+  const unsigned kid_flags = flags & ~XC_FLAG_ACCUMULATE;
+  xcb::LaunchCounter lc;
+
+  if (G.rank_mode) {  // one process per GPU: this rank's bands, then ncclReduce to rank 0
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const std::vector<int> mine = shard_bands(ks, G.rank, G.nranks);
+    void* part = ctx->buf<char>("grp_part", bytes);
+    xc_stats st{};
+    if (mine.empty())
+      ck(cudaMemsetAsync(part, 0, bytes, ctx->stream), "memset");
+    else
+      run_single(ctx, f, mode, d, signal, param, mine.data(), int(mine.size()),
+                 kid_flags | (G.rank ? XC_FLAG_NO_INNER_DC : 0u), part, &st, true);
+    const NcclApi& a = nccl_or_throw();
+    nck(a.Reduce(part, part, bytes / (f64 ? 8 : 4), f64 ? ncclDouble : ncclFloat, ncclSum, 0,
+                 G.comms[0], ctx->stream),
+        "ncclReduce");
+    ck(cudaStreamSynchronize(ctx->stream), "band reduce");
+    if (G.rank == 0) deliver(ctx, *d, part, out, bytes, accumulate, f64, lc);
+    st.gpu_launches += lc.n;
+    merge_stats(stats, {st}, (long long)ks.size(), since(t_start));
+    return;
+  }
+
+  const int n = int(G.kids.size());
+  std::vector<xc_stats> st(static_cast<size_t>(n));
+  if (G.shard == XC_SHARD_BATCH) {  // images split across devices, no collective
+    if (accumulate) throw std::invalid_argument("XC_FLAG_ACCUMULATE needs band sharding");
+    const int nuse = std::min(n, d->batch);
+    st.resize(size_t(nuse));
+    for_each_kid(nuse, [&](int i) {
+      xc_context k = G.kids[i];
+      std::lock_guard<std::mutex> lk(k->mu);
+      ck(cudaSetDevice(k->device), "cudaSetDevice");
+      const auto ab = shard_range(d->batch, i, nuse);
+      xc_image_desc di = *d;
+      di.batch = ab.second - ab.first;
+      const void *sg, *pr;
+      kid_inputs(ctx, k, *d, signal, param, ab.first, ab.second, &sg, &pr);
+      char* o = static_cast<char*>(out) + size_t(ab.first) * npix * os;
+      const bool local = d->memory == XC_HOST || k->device == ctx->device;
+      void* ko = local ? static_cast<void*>(o) : k->buf<char>("grp_part", size_t(di.batch) * npix * os);
+      run_single(k, f, mode, &di, sg, pr, components, n_components, kid_flags, ko, &st[i], !local);
+      if (!local) {
+        ck(cudaMemcpyPeerAsync(o, ctx->device, ko, k->device, size_t(di.batch) * npix * os,
+                               k->stream),
+           "peer copy out");
+        ck(cudaStreamSynchronize(k->stream), "peer copy out");
+      }
+    });
+    merge_stats(stats, st, (long long)ks.size(), since(t_start));
+    return;
+  }
+
+  // band sharding: every device runs its band range (empty ranges add zeros)
+  std::vector<void*> parts(static_cast<size_t>(n), nullptr);
+  for_each_kid(n, [&](int i) {
+    xc_context k = G.kids[i];
+    std::lock_guard<std::mutex> lk(k->mu);
+    ck(cudaSetDevice(k->device), "cudaSetDevice");
+    const std::vector<int> mine = shard_bands(ks, i, n);
+    const bool direct = i == 0 && d->memory == XC_DEVICE && !accumulate;
+    void* part = direct ? out : k->buf<char>("grp_part", bytes);
+    parts[i] = part;
+    if (mine.empty()) {
+      ck(cudaMemsetAsync(part, 0, bytes, k->stream), "memset");
+      ck(cudaStreamSynchronize(k->stream), "memset");
+      return;
+    }
+    const void *sg, *pr;
+    kid_inputs(ctx, k, *d, signal, param, 0, d->batch, &sg, &pr);
+    xc_image_desc di = *d;
+    if (sg != signal) di.memory = XC_DEVICE;  // peer-copied inputs
+    run_single(k, f, mode, &di, sg, pr, mine.data(), int(mine.size()),
+               kid_flags | (i ? XC_FLAG_NO_INNER_DC : 0u), part, &st[i], true);
+  });
+  reduce_to_root(G, parts, bytes / (f64 ? 8 : 4), f64);
+  deliver(G.kids[0], *d, parts[0], out, bytes, accumulate, f64, lc);
+  st[0].gpu_launches += lc.n;
+  merge_stats(stats, st, (long long)ks.size(), since(t_start));
+}
+
+// root: out[img] = floored Re(num / den) for every image of numden (device)
+void smooth_divide_all(xc_context ctx, const xc_image_desc& d, const float2* numden, void* out,
+                       xc_stats* st) {
+  ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+  const size_t npix = size_t(d.height) * d.width, os = dtype_size(d.out_dtype);
+  unsigned* red = ctx->buf<unsigned>("smooth_red", size_t(d.batch) + 1);
+  ck(cudaMemsetAsync(red, 0, (size_t(d.batch) + 1) * sizeof(unsigned), ctx->stream), "memset");
+  char* dst = d.memory == XC_HOST ? ctx->buf<char>("smooth_out", npix * os * size_t(d.batch))
+                                  : static_cast<char*>(out);
+  xcb::LaunchCounter lc;
+  for (int img = 0; img < d.batch; ++img)
+    smooth_divide(ctx, ctx->stream, numden, npix, img, d.batch, d.out_dtype == XC_F64,
+                  dst + size_t(img) * npix * os, red, lc);
+  unsigned clamped = 0;
+  ck(cudaMemcpyAsync(&clamped, red + d.batch, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                     ctx->stream),
+     "readback");
+  if (d.memory == XC_HOST)
+    ck(cudaMemcpyAsync(out, dst, npix * os * size_t(d.batch), cudaMemcpyDeviceToHost,
+                       ctx->stream),
+       "D2H");
+  ck(cudaStreamSynchronize(ctx->stream), "smooth divide");
+  st->clamped_pixels = int(clamped);
+  st->gpu_launches += lc.n;
+}
+
+void smooth_group(xc_context ctx, xc_filter f, const xc_image_desc* d, const void* signal,
+                  const void* param, int normalize_signal, void* out, xc_stats* stats) {
+  const auto t_start = std::chrono::steady_clock::now();
+  Group& G = *ctx->group;
+  const size_t npix = size_t(d->height) * d->width;
+  const size_t count = 4 * npix * size_t(d->batch);  // floats of numden
+  const std::vector<int>& all = f->hf.ks;
+  const bool scale = f->hf.group == XC_SCALE2;
+  auto no_op = [](Call&, int) {};
+  auto part_stats = [](const SmoothPart& p) {
+    xc_stats s{};
+    s.pad_h = p.pad_h;
+    s.pad_w = p.pad_w;
+    s.seconds_fft = p.gpu_s;
+    s.gpu_launches = p.launches;
+    return s;
+  };
+
+  if (G.rank_mode) {
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const std::vector<int> mine = shard_bands(all, G.rank, G.nranks);
+    float2* nd = ctx->buf<float2>("grp_numden", count / 2);
+    xc_stats st{};
+    if (mine.empty())
+      ck(cudaMemsetAsync(nd, 0, count * 4, ctx->stream), "memset");
+    else
+      st = part_stats(smooth_partials(ctx, f, d, signal, param, normalize_signal, mine.data(),
+                                      int(mine.size()), scale && G.rank == 0, nd, no_op));
+    const NcclApi& a = nccl_or_throw();
+    nck(a.Reduce(nd, nd, count, ncclFloat, ncclSum, 0, G.comms[0], ctx->stream), "ncclReduce");
+    ck(cudaStreamSynchronize(ctx->stream), "smooth reduce");
+    if (G.rank == 0) smooth_divide_all(ctx, *d, nd, out, &st);
+    merge_stats(stats, {st}, 2 * (long long)all.size(), since(t_start));
+    return;
+  }
+
+  const int n = int(G.kids.size());
+  std::vector<xc_stats> st(static_cast<size_t>(n));
+  if (G.shard == XC_SHARD_BATCH) {
+    const int nuse = std::min(n, d->batch);
+    st.resize(size_t(nuse));
+    for_each_kid(nuse, [&](int i) {
+      xc_context k = G.kids[i];
+      std::lock_guard<std::mutex> lk(k->mu);
+      ck(cudaSetDevice(k->device), "cudaSetDevice");
+      const auto ab = shard_range(d->batch, i, nuse);
+      xc_image_desc di = *d;
+      di.batch = ab.second - ab.first;
+      const void *sg, *pr;
+      kid_inputs(ctx, k, *d, signal, param, ab.first, ab.second, &sg, &pr);
+      const size_t os = dtype_size(d->out_dtype);
+      char* o = static_cast<char*>(out) + size_t(ab.first) * npix * os;
+      const bool local = d->memory == XC_HOST || k->device == ctx->device;
+      if (!local) di.memory = XC_DEVICE;
+      void* ko = local ? static_cast<void*>(o) : k->buf<char>("grp_part", size_t(di.batch) * npix * os);
+      smooth_single(k, f, &di, sg, pr, normalize_signal, ko, &st[i]);
+      if (!local) {
+        ck(cudaMemcpyPeerAsync(o, ctx->device, ko, k->device, size_t(di.batch) * npix * os,
+                               k->stream),
+           "peer copy out");
+        ck(cudaStreamSynchronize(k->stream), "peer copy out");
+      }
+    });
+    merge_stats(stats, st, 2 * (long long)all.size(), since(t_start));
+    return;
+  }
+
+  std::vector<void*> parts(static_cast<size_t>(n), nullptr);
+  for_each_kid(n, [&](int i) {
+    xc_context k = G.kids[i];
+    std::lock_guard<std::mutex> lk(k->mu);
+    ck(cudaSetDevice(k->device), "cudaSetDevice");
+    const std::vector<int> mine = shard_bands(all, i, n);
+    float2* nd = k->buf<float2>("grp_numden", count / 2);
+    parts[i] = nd;
+    if (mine.empty()) {
+      ck(cudaMemsetAsync(nd, 0, count * 4, k->stream), "memset");
+      ck(cudaStreamSynchronize(k->stream), "memset");
+      return;
+    }
+    const void *sg, *pr;
+    kid_inputs(ctx, k, *d, signal, param, 0, d->batch, &sg, &pr);
+    xc_image_desc di = *d;
+    if (sg != signal) di.memory = XC_DEVICE;
+    st[i] = part_stats(smooth_partials(k, f, &di, sg, pr, normalize_signal, mine.data(),
+                                       int(mine.size()), scale && i == 0, nd, no_op));
+  });
+  reduce_to_root(G, parts, count, false);
+  smooth_divide_all(G.kids[0], *d, static_cast<const float2*>(parts[0]), out, &st[0]);
+  merge_stats(stats, st, 2 * (long long)all.size(), since(t_start));
+}
+
+}  // namespace
+
+extern "C" {
+
+int xc_nccl_unique_id(void* id_out) {
+  return guarded(nullptr, [&] {
+    if (!id_out) throw std::invalid_argument("null argument");
+    ncclUniqueId id;
+    nck(nccl_or_throw().GetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(id_out, &id, sizeof(id));
+  });
+}
+
+int xc_context_create_multi(int n_dev, const int* dev_ids, xc_context* out) {
+  return guarded(nullptr, [&] {
+    if (!out || !dev_ids || n_dev < 1) throw std::invalid_argument("null argument");
+    xc_context root = nullptr;
+    if (int rc = xc_context_create(dev_ids[0], &root)) throw CudaError(g_thread_err, rc);
+    std::unique_ptr<xc_context_s> guard(root);
+    auto* G = new Group();
+    root->group = G;
+    for (int i = 0; i < n_dev; ++i) {
+      xc_context k = nullptr;
+      if (int rc = xc_context_create(dev_ids[i], &k)) throw CudaError(g_thread_err, rc);
+      G->kids.push_back(k);
+    }
+    bool distinct = true;
+    for (int i = 0; i < n_dev; ++i)
+      for (int j = 0; j < i; ++j) distinct = distinct && dev_ids[i] != dev_ids[j];
+    const char* e = std::getenv("XCB_REDUCE");
+    const bool peer = !distinct || (e && std::string(e) == "peer");
+    if (!peer) {
+      const NcclApi& a = nccl_or_throw();
+      G->comms.assign(size_t(n_dev), nullptr);
+      nck(a.CommInitAll(G->comms.data(), n_dev, dev_ids), "ncclCommInitAll");
+    }
+    if (!peer || n_dev > 1) {
+      // direct peer access where the topology allows it (NVLink); the peer
+      // copies work either way
+      for (int i = 0; i < n_dev; ++i)
+        for (int j = 0; j < n_dev; ++j) {
+          int can = 0;
+          if (dev_ids[i] == dev_ids[j]) continue;
+          cudaDeviceCanAccessPeer(&can, dev_ids[i], dev_ids[j]);
+          if (can) {
+            cudaSetDevice(dev_ids[i]);
+            cudaDeviceEnablePeerAccess(dev_ids[j], 0);
+            cudaGetLastError();  // already enabled is fine
+          }
+        }
+      cudaSetDevice(dev_ids[0]);
+    }
+    *out = guard.release();
+  });
+}
+
+int xc_context_create_rank(int device, const void* nccl_id, int rank, int nranks,
+                           xc_context* out) {
+  return guarded(nullptr, [&] {
+    if (!out || !nccl_id || nranks < 1 || rank < 0 || rank >= nranks)
+      throw std::invalid_argument("invalid rank arguments");
+    xc_context c = nullptr;
+    if (int rc = xc_context_create(device, &c)) throw CudaError(g_thread_err, rc);
+    std::unique_ptr<xc_context_s> guard(c);
+    auto* G = new Group();
+    c->group = G;
+    G->rank_mode = true;
+    G->rank = rank;
+    G->nranks = nranks;
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    const NcclApi& a = nccl_or_throw();
+    G->comms.assign(1, nullptr);
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    nck(a.CommInitRank(&G->comms[0], nranks, id, rank), "ncclCommInitRank");
+    *out = guard.release();
+  });
+}
+
+int xc_context_set_sharding(xc_context ctx, int shard) {
+  return guarded(ctx, [&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    if (shard != XC_SHARD_BANDS && shard != XC_SHARD_BATCH)
+      throw std::invalid_argument("unknown sharding");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (!ctx->group) throw std::invalid_argument("sharding needs a multi-device context");
+    if (ctx->group->rank_mode && shard == XC_SHARD_BATCH)
+      throw std::invalid_argument("rank contexts shard bands (split batches per rank instead)");
+    ctx->group->shard = shard;
+  });
+}
+
+int xc_context_devices(xc_context ctx, int* n_dev, int* uses_nccl) {
+  return guarded(ctx, [&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    const Group* G = ctx->group;
+    if (n_dev) *n_dev = G ? (G->rank_mode ? G->nranks : int(G->kids.size())) : 1;
+    if (uses_nccl) *uses_nccl = G && !G->comms.empty() ? 1 : 0;
   });
 }
 

@@ -361,6 +361,25 @@ void launch_convert_signal(const void* src, int dtype, size_t n, void* dst, cuda
   ++lc.n;
 }
 
+template <class T>
+__global__ void k_accumulate(T* __restrict__ dst, const T* __restrict__ src, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    dst[i] += src[i];
+}
+
+void launch_accumulate(void* dst, const void* src, size_t n, int f64, cudaStream_t st,
+                       LaunchCounter& lc) {
+  const int g = grid_for(n, 256);
+  if (f64)
+    k_accumulate<double><<<g, 256, 0, st>>>(static_cast<double*>(dst),
+                                            static_cast<const double*>(src), n);
+  else
+    k_accumulate<float><<<g, 256, 0, st>>>(static_cast<float*>(dst),
+                                           static_cast<const float*>(src), n);
+  ++lc.n;
+}
+
 void launch_smooth_finish(const float2* num, const float2* den, size_t n, int out_f64,
                           void* out, unsigned* maxbits, unsigned* clamped, cudaStream_t st,
                           LaunchCounter& lc) {

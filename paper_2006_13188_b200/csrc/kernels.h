@@ -218,3 +218,10 @@ void launch_render(const double2* comps, const int* ks, int nb, int group, int n
                    int n_angles, double r_max, double r_min, double omega, int S, int R,
                    int transpose, float2* out, cudaStream_t st, LaunchCounter& lc);
 }  // namespace xcb
+
+namespace xcb {
+// dst[i] += src[i] over n floats (f64 = 0) or doubles (f64 = 1): the ordered
+// partial sums of the multi-device band reduce without NCCL (peer copies).
+void launch_accumulate(void* dst, const void* src, size_t n, int f64, cudaStream_t st,
+                       LaunchCounter& lc);
+}  // namespace xcb

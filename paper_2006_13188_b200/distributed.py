@@ -83,12 +83,23 @@ def xfast_band_sharded(mode: XMode, H, T: XformField, F: FreqFilter2,
     return Response2(total, out, len(ks), {})
 
 
+def _check_integral(F: FreqFilter2) -> None:
+    """engine.hpp:388-392: the reconstructed (2R+1)^2 filter must not integrate
+    to zero, else the normalization is undefined (same test as xc_smooth)."""
+    from .engine import reconstruct
+    R = int(np.ceil(F.r_max))
+    full = reconstruct(F, 2 * R + 1, 2 * R + 1, float(R), float(R))
+    if abs(full.sum()) < 1e-12 * max(1.0, float(np.abs(full).max(initial=0.0))):
+        raise ValueError("normalization undefined: filter has zero integral")
+
+
 def smooth_band_sharded(H, T: XformField, F: FreqFilter2, normalize_signal: bool = True,
                         compute=gpu_compute, root: int = 0, group=None,
                         device=None) -> SmoothResult | None:
     """Band-sharded smooth_adaptive: reduce num and den, divide on the root."""
     dist = _dist()
     rank, world = dist.get_rank(group), dist.get_world_size(group)
+    _check_integral(F)  # engine.hpp:388-392, on every rank before any collective
     Hs = np.asarray(H, np.complex128)
     ones = np.ones(Hs.shape, np.complex128)
     if normalize_signal and T.kind == XformKind.scale2:  # engine.hpp:396-401

@@ -270,15 +270,21 @@ def _seconds(st: N.Stats) -> dict:
             "d2h": st.seconds_d2h, "total": st.seconds_total}
 
 
+def _context(device) -> N.Context:
+    """`device` is a device ordinal (the thread's default context on it) or an
+    explicit N.Context (e.g. N.Context.multi([0, 1, ...]) for band sharding)."""
+    return device if isinstance(device, N.Context) else N.context(int(device))
+
+
 def _fast(mode: XMode, H, T: XformField, F: FreqFilter2, plan: XConvPlan | None,
-          device: int = 0, inner_dc: bool = True) -> Response2:
+          device=0, inner_dc: bool = True) -> Response2:
     plan = XConvPlan() if plan is None else XConvPlan(plan.mode, plan.group,
                                                       list(plan.components), plan.periodic)
     sig = _signal(H)
     par = _param(T, sig.shape)
     wide = sig.dtype in (np.float64, np.complex128)
     out = np.zeros(sig.shape, np.complex128 if wide else np.complex64)
-    ctx = N.context(device)
+    ctx = _context(device)
     d = _desc(sig, par, N.XC_C128 if wide else N.XC_C64, T.kind)
     comp = np.ascontiguousarray(np.asarray(plan.components, np.int32))
     st = N.Stats()
@@ -294,24 +300,27 @@ def _fast(mode: XMode, H, T: XformField, F: FreqFilter2, plan: XConvPlan | None,
     return Response2(out, plan, st.standard_ops, _seconds(st), st.gpu_launches)
 
 
-def xcorr_fast(H, T: XformField, F: FreqFilter2, plan: XConvPlan | None = None) -> Response2:
-    """Extended correlation (engine.hpp:286-326): out(p) = sum_k e^{i phase_k(p)} (H * F_k)(p)."""
-    return _fast(XMode.correlation, H, T, F, plan)
+def xcorr_fast(H, T: XformField, F: FreqFilter2, plan: XConvPlan | None = None,
+               ctx=0) -> Response2:
+    """Extended correlation (engine.hpp:286-326): out(p) = sum_k e^{i phase_k(p)} (H * F_k)(p).
+    ctx: device ordinal or N.Context (a multi-GPU context shards the bands)."""
+    return _fast(XMode.correlation, H, T, F, plan, ctx)
 
 
-def xconv_fast(H, T: XformField, F: FreqFilter2, plan: XConvPlan | None = None) -> Response2:
+def xconv_fast(H, T: XformField, F: FreqFilter2, plan: XConvPlan | None = None,
+               ctx=0) -> Response2:
     """Extended convolution (engine.hpp:331-373): sum_k (H e^{-i phase_k}) conv F_k."""
-    return _fast(XMode.convolution, H, T, F, plan)
+    return _fast(XMode.convolution, H, T, F, plan, ctx)
 
 
 def smooth_adaptive(H, T: XformField, F: FreqFilter2, normalize_signal: bool = True,
-                    device: int = 0) -> SmoothResult:
+                    device=0) -> SmoothResult:
     """Normalized adaptive smoothing (engine.hpp:385-419)."""
     sig = _signal(H)
     par = _param(T, sig.shape)
     wide = sig.dtype in (np.float64, np.complex128)
     out = np.zeros(sig.shape, np.float64 if wide else np.float32)
-    ctx = N.context(device)
+    ctx = _context(device)
     d = _desc(sig, par, N.XC_F64 if wide else N.XC_F32, T.kind)
     st = N.Stats()
     N.check(N.lib().xc_smooth(ctx.handle, F.handle(ctx), C.byref(d), sig.ctypes.data,

@@ -227,10 +227,11 @@ def write_xform(path: str, T: XformField) -> None:
     elif T.kind == XformKind.scale2:
         write_pfm_planes(path, [T.scale])
     else:
+        # engine3d.rotation3d layout: (nz, ny, nx, 4) quaternions (w, x, y, z)
         q = np.asarray(T.values)
-        if q.ndim != 3 or q.shape[0] != 4:
+        if q.ndim != 4 or q.shape[-1] != 4 or q.shape[0] != 1:
             raise IoError("PFM export supports single-slice quaternion fields")
-        write_pfm_planes(path, list(q))
+        write_pfm_planes(path, [q[0, ..., i] for i in range(4)])
 
 
 def read_xform(path: str, kind: XformKind) -> XformField:
@@ -247,7 +248,8 @@ def read_xform(path: str, kind: XformKind) -> XformField:
         return XformField.scaling(planes[0])
     if len(planes) != 4:
         raise IoError(path + ": quaternion field needs 4 planes")
-    return XformField(XformKind.rotation3, np.stack(planes))
+    from .engine3d import rotation3d  # renormalizes like field.hpp:169-171
+    return rotation3d(np.stack(planes, -1)[None])
 
 
 # ------------------------------------------------------------------ XCF1

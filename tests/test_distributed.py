@@ -53,6 +53,15 @@ def _worker(rank, world, port, q):
         if rank == 0:
             res[f"scale{mode}"] = (r.output, r.standard_ops)
     sm = D.smooth_band_sharded(H.real.copy(), S, Fs, compute=oracle_compute)
+    # bands k = +-1 only: the angular mean vanishes, so the filter integrates to
+    # zero and every rank raises the reference's error (engine.hpp:388-392)
+    i = [F.index_of(-1), F.index_of(1)]
+    Z = X.FreqFilter2(0, F.K, [-1, 1], F.comps[:, i], F.n_radii, F.n_angles, F.r_max)
+    try:
+        D.smooth_band_sharded(H.real.copy(), T, Z, compute=oracle_compute)
+        res["zero_integral"] = "no error"
+    except ValueError as e:
+        res["zero_integral"] = str(e)
     if rank == 0:
         res["smooth"] = (sm.output, sm.standard_ops, sm.clamped_pixels)
         q.put(res)
@@ -102,6 +111,7 @@ def test_band_sharded_world2_gloo(orc):
     out, ops, cl = res["smooth"]
     ref, rops, rcl = orc.smooth_adaptive(H.real.copy(), 1, S, Fs)
     assert ops == rops and cl == rcl and orc.rel_l2(out, ref) < 1e-12
+    assert res["zero_integral"] == "normalization undefined: filter has zero integral"
 
 
 def oracle_anglemax(H, F, n_angles, components):

@@ -95,11 +95,19 @@ def test_pfm_round_trip_transformation_fields(tmp_path):  # test_io.cpp:68-93
     io.write_xform(p, X.XformField.scaling(sc))
     sc2 = io.read_xform(p, X.XformKind.scale2)
     assert np.abs(sc2.scale - sc).max() < 1e-6
-    q = rng.normal(size=(4, 3, 4))
-    q /= np.linalg.norm(q, axis=0)
-    io.write_xform(p, X.XformField(X.XformKind.rotation3, q))
+    from paper_2006_13188_b200 import engine3d as E3
+    q = rng.normal(size=(1, 3, 4, 4))  # (nz, ny, nx, 4): the engine's layout
+    q /= np.linalg.norm(q, axis=-1, keepdims=True)
+    io.write_xform(p, E3.rotation3d(q))
     q2 = io.read_xform(p, X.XformKind.rotation3)
+    assert q2.values.shape == (1, 3, 4, 4)
     assert np.abs(q2.values - q).max() < 1e-6
+    # non-unit quaternions read back renormalized (field.hpp:169-171)
+    io.write_xform(p, X.XformField(X.XformKind.rotation3, 2.0 * q))
+    q3 = io.read_xform(p, X.XformKind.rotation3)
+    assert np.abs(q3.values - q).max() < 1e-6
+    with pytest.raises(io.IoError, match="single-slice"):
+        io.write_xform(p, X.XformField(X.XformKind.rotation3, np.concatenate([q, q])))
     with pytest.raises(io.IoError, match="rotation field needs 1 plane"):
         io.read_xform(p, X.XformKind.rotation2)
 

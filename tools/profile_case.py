@@ -1,7 +1,7 @@
-"""One hot-path invocation for ncu captures: config-5 geometry (4096^2, 65
-bands), `batch` images, after one warm-up call (filter spectra built).
+"""One hot-path invocation for ncu captures, after one warm-up call (filter
+spectra built).
 
-  python tools/profile_case.py [xcorr|xconv] [config] [batch]
+  python tools/profile_case.py [xcorr|xconv|smooth|anglemax] [config] [batch]
 """
 import os
 import sys
@@ -15,8 +15,13 @@ cfg = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 nb = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 w = WL.config5(batch=nb) if cfg == 5 else WL.CONFIGS[cfg]()
 sig, par = (w.signal[0], w.param[0]) if nb == 1 else (w.signal[:nb], w.param[:nb])
+if mode == "anglemax":
+    for _ in range(2):
+        X.anglemax(sig, w.filt, 360)
+    print("ok anglemax")
+    sys.exit(0)
 T = X.XformField.rotation(par) if w.kind == 0 else X.XformField.scaling(par)
-fn = {"xcorr": X.xcorr_fast, "xconv": X.xconv_fast}[mode]
+fn = {"xcorr": X.xcorr_fast, "xconv": X.xconv_fast, "smooth": X.smooth_adaptive}[mode]
 for _ in range(2):
     r = fn(sig, T, w.filt)
-print("ok", r.standard_ops, r.seconds["fft"])
+print("ok", mode, cfg)
