@@ -131,8 +131,19 @@ def check(rc: int, ctx=None):
     raise RuntimeError(f"xconv_b200 error {rc}: {msg}")
 
 
+def _nccl_first():
+    """Map torch's NCCL before the library loads one: a process that later
+    imports torch needs torch's (newer) libnccl.so.2, and the loader keeps the
+    first libnccl.so.2 it maps."""
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
+
+
 def nccl_unique_id() -> bytes:
     """A fresh NCCL unique id (128 bytes) for Context.rank()."""
+    _nccl_first()
     buf = C.create_string_buffer(128)
     check(lib().xc_nccl_unique_id(buf), None)
     return buf.raw
@@ -156,6 +167,7 @@ class Context:
     def multi(cls, devices, shard: int = XC_SHARD_BANDS) -> "Context":
         """One process driving several devices (a device listed twice reduces
         with peer copies instead of NCCL)."""
+        _nccl_first()
         ids = (C.c_int * len(devices))(*[int(d) for d in devices])
         h = C.c_void_p()
         check(lib().xc_context_create_multi(len(devices), ids, C.byref(h)), None)
@@ -168,6 +180,7 @@ class Context:
     def rank(cls, device: int, nccl_id: bytes, rank: int, nranks: int) -> "Context":
         """One process per GPU: every rank calls with the same arguments, rank 0
         receives the band-summed result."""
+        _nccl_first()
         buf = C.create_string_buffer(bytes(nccl_id), 128)
         h = C.c_void_p()
         check(lib().xc_context_create_rank(int(device), buf, int(rank), int(nranks), C.byref(h)),

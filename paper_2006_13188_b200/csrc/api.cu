@@ -2015,13 +2015,19 @@ struct NcclApi {
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
-// NCCL is loaded on first use (the process's libnccl.so.2 -- torch's if it is
-// already mapped), so single-device use never needs it.
+// NCCL is loaded on first use, so single-device use never needs it.  An NCCL
+// already mapped into the process (torch's) is reused; else XCB_NCCL_LIBRARY,
+// else the loader's libnccl.so.2.  (Loading an older libnccl.so.2 first would
+// shadow a newer one that a later `import torch` needs: the Python binding
+// imports torch before creating a multi-GPU context.)
 const NcclApi& nccl() {
   static const NcclApi api = [] {
     NcclApi a;
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h)
+      if (const char* p = std::getenv("XCB_NCCL_LIBRARY")) h = dlopen(p, RTLD_NOW);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW);
     if (!h) {
       const char* e = dlerror();
       a.why = std::string("cannot load libnccl.so.2: ") + (e ? e : "?");

@@ -103,6 +103,11 @@ class Workload:
     filt: FreqFilter2
     filter_image: np.ndarray
     meta: dict = field(default_factory=dict)
+    # how `filt` was decomposed from `filter_image`: ("rotation2", (cx, cy, K,
+    # n_radii, n_angles, r_max)) or ("scale2", (cx, cy, K, n_radii, n_angles,
+    # r_min, r_max)) -- lets tests and the reference arm rebuild it with the
+    # oracle or the reference itself
+    decomp: tuple = ()
 
     @property
     def bands(self) -> int:
@@ -120,8 +125,9 @@ def config1(n: int = 256, seed: int = 0) -> Workload:
     sig = rng.uniform(0, 1, (1, n, n)).astype(np.float32)
     th = rng.uniform(0, 2 * math.pi, (1, n, n)).astype(np.float32)
     f = angular_filter(15, 6.0, 4, rng)
-    F = decompose_rotation2(f, 15, 15, 8, 30, 32, 15.0)
-    return Workload("cfg1-xcorr-rot-256", "xcorr", sig, th, 0, F, f)
+    D = ("rotation2", (15, 15, 8, 30, 32, 15.0))
+    F = decompose_rotation2(f, *D[1])
+    return Workload(f"cfg1-xcorr-rot-{n}", "xcorr", sig, th, 0, F, f, decomp=D)
 
 
 def config2(n: int = 1024, seed: int = 0) -> Workload:
@@ -130,8 +136,9 @@ def config2(n: int = 1024, seed: int = 0) -> Workload:
     _, d = gradient(gaussian_blur(rng.standard_normal((n, n)), 4.0))
     th = d[None].astype(np.float32)
     f = angular_filter(16, 8.0, 8, rng)
-    F = decompose_rotation2(f, 16, 16, 16, 32, 34, 16.0)
-    return Workload("cfg2-xconv-rot-1024", "xconv", sig, th, 0, F, f)
+    D = ("rotation2", (16, 16, 16, 32, 34, 16.0))
+    F = decompose_rotation2(f, *D[1])
+    return Workload(f"cfg2-xconv-rot-{n}", "xconv", sig, th, 0, F, f, decomp=D)
 
 
 def config3(n: int = 4096, n_templates: int = 3, seed: int = 0) -> Workload:
@@ -149,10 +156,11 @@ def config3(n: int = 4096, n_templates: int = 3, seed: int = 0) -> Workload:
         ang = rng.uniform(0, 2 * math.pi)
         paste_rotated(img, 4.0 * tpl, cx, cy, ang)
         truth.append((cx, cy, ang))
-    F = decompose_rotation2(tpl, 31.5, 31.5, 32, 64, 66, 31.5)
-    return Workload("cfg3-anglemax-rot-4096", "anglemax", img[None].astype(np.float32), None,
+    D = ("rotation2", (31.5, 31.5, 32, 64, 66, 31.5))
+    F = decompose_rotation2(tpl, *D[1])
+    return Workload(f"cfg3-anglemax-rot-{n}", "anglemax", img[None].astype(np.float32), None,
                     0, F, tpl, {"truth": truth, "n_angles": 360, "nms_radius": 32.0,
-                                "threshold": 0.5})
+                                "threshold": 0.5}, decomp=D)
 
 
 def config4(n: int = 2048, seed: int = 0) -> Workload:
@@ -165,8 +173,9 @@ def config4(n: int = 2048, seed: int = 0) -> Workload:
     y, x = np.mgrid[-R:R + 1, -R:R + 1].astype(np.float64)
     f = np.exp(-(x * x + y * y) / (2 * 8.0 ** 2))
     f[x * x + y * y > R * R] = 0
-    F = decompose_scale2(f, R, R, 12, 64, 32, 1.0, float(R))
-    return Workload("cfg4-smooth-scale-2048", "smooth", sig, s, 1, F, f)
+    D = ("scale2", (R, R, 12, 64, 32, 1.0, float(R)))
+    F = decompose_scale2(f, *D[1])
+    return Workload(f"cfg4-smooth-scale-{n}", "smooth", sig, s, 1, F, f, decomp=D)
 
 
 def config5(n: int = 4096, batch: int = 16, seed: int = 0) -> Workload:
@@ -174,8 +183,9 @@ def config5(n: int = 4096, batch: int = 16, seed: int = 0) -> Workload:
     sig = rng.uniform(0, 1, (batch, n, n)).astype(np.float32)
     th = rng.uniform(0, 2 * math.pi, (batch, n, n)).astype(np.float32)
     f = angular_filter(31, 14.0, 32, rng)
-    F = decompose_rotation2(f, 31, 31, 64, 62, 130, 31.0)
-    return Workload(f"cfg5-xcorr-rot-{batch}x{n}", "xcorr", sig, th, 0, F, f)
+    D = ("rotation2", (31, 31, 64, 62, 130, 31.0))
+    F = decompose_rotation2(f, *D[1])
+    return Workload(f"cfg5-xcorr-rot-{batch}x{n}", "xcorr", sig, th, 0, F, f, decomp=D)
 
 
 CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}

@@ -33,3 +33,16 @@ def test_shim_end_to_end_on_gpu(orc):
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.count(" ok") == 8
+
+
+@pytest.mark.gpu
+def test_shim_multi_device_context(orc):
+    """The shim over a three-device context (XCB_DEVICES=0,0,0: device 0 listed
+    three times, bands split three ways, peer-copy reduce) reproduces the oracle."""
+    if not os.path.exists(BIN):
+        build_shim_test()
+    env = dict(os.environ, XCB_DEVICES="0,0,0")
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=300, env=env)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count(" ok") == 8
