@@ -82,6 +82,14 @@ enum xc_memory { XC_HOST = 0, XC_DEVICE = 1 };
                                     369-371): set on all but one rank when bands
                                     are sharded across GPUs */
 #define XC_FLAG_ACCUMULATE 4u    /* out += result (device memory only) */
+#define XC_FLAG_ASYNC 8u         /* device memory only.  Rank contexts: return once
+                                    this rank's bands are computed, with the reduce
+                                    (and rank 0's write of `out`) queued on an
+                                    internal stream that overlaps the next call.
+                                    Single-device contexts, rotation group: return
+                                    with the kernels queued on the context's stream
+                                    (no host sync; the call can be captured in a
+                                    CUDA graph).  xc_context_synchronize waits. */
 
 typedef struct xc_context_s* xc_context;
 typedef struct xc_filter_s* xc_filter;
@@ -107,6 +115,8 @@ typedef struct {
   double seconds_render, seconds_fft, seconds_combine, seconds_premultiply;
   double seconds_h2d, seconds_d2h, seconds_total;
   int gpu_launches;        /* kernels launched by this call */
+  int bands_run;           /* bands transformed per image (the Hermitian half-band
+                              mode transforms k >= 0 only; summed over devices) */
 } xc_stats;
 
 int xc_abi_version(void);
@@ -137,6 +147,8 @@ int xc_context_create_rank(int device, const void* nccl_id128, int rank, int nra
 /* XC_SHARD_BANDS (default; reduce) or XC_SHARD_BATCH (images split across the
  * devices of a create_multi context, no collective). */
 int xc_context_set_sharding(xc_context ctx, int shard);
+/* wait for every stream of the context (XC_FLAG_ASYNC reduces included) */
+int xc_context_synchronize(xc_context ctx);
 /* devices (or ranks) of a context and whether its reduce is NCCL */
 int xc_context_devices(xc_context ctx, int* n_dev, int* uses_nccl);
 void xc_context_destroy(xc_context ctx);

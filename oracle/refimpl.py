@@ -94,6 +94,12 @@ class Filter:
         self.n_radii, self.n_angles = int(n_radii), int(n_angles)
         self.r_max, self.r_min, self.r_domain = float(r_max), float(r_min), float(r_domain)
 
+    def n_components(self) -> int:
+        return len(self.ks)
+
+    def index_of(self, k: int) -> int:
+        return int(np.nonzero(self.ks == k)[0][0])
+
 
 def next_fast_size(n: int) -> int:
     return lib().ref_next_fast_size(int(n))

@@ -19,7 +19,7 @@ XC_CORRELATION, XC_CONVOLUTION = 0, 1
 XC_F32, XC_F64, XC_C64, XC_C128 = 0, 1, 2, 3
 XC_ROW_MAJOR, XC_COL_MAJOR = 0, 1
 XC_HOST, XC_DEVICE = 0, 1
-XC_FLAG_PERIODIC, XC_FLAG_NO_INNER_DC, XC_FLAG_ACCUMULATE = 1, 2, 4
+XC_FLAG_PERIODIC, XC_FLAG_NO_INNER_DC, XC_FLAG_ACCUMULATE, XC_FLAG_ASYNC = 1, 2, 4, 8
 XC_SHARD_BANDS, XC_SHARD_BATCH = 0, 1
 
 
@@ -36,7 +36,7 @@ class Stats(C.Structure):
                 ("seconds_render", C.c_double), ("seconds_fft", C.c_double),
                 ("seconds_combine", C.c_double), ("seconds_premultiply", C.c_double),
                 ("seconds_h2d", C.c_double), ("seconds_d2h", C.c_double),
-                ("seconds_total", C.c_double), ("gpu_launches", C.c_int)]
+                ("seconds_total", C.c_double), ("gpu_launches", C.c_int), ("bands_run", C.c_int)]
 
 
 EXPORTS = [
@@ -49,7 +49,7 @@ EXPORTS = [
     "xc_find_peaks_device", "xc_filter3_create", "xc_filter3_destroy", "xc_decompose_rotation3",
     "xc_render_sph_component", "xc_reconstruct3", "xc_sph_harm", "xc_wigner_d", "xc_run3",
     "xc_white_noise", "xc_nccl_unique_id", "xc_context_create_multi", "xc_context_create_rank",
-    "xc_context_set_sharding", "xc_context_devices",
+    "xc_context_set_sharding", "xc_context_devices", "xc_context_synchronize",
 ]
 
 _lib = None
@@ -115,6 +115,7 @@ def lib():
         L.xc_context_create_rank.argtypes = [i, vp, i, i, C.POINTER(vp)]
         L.xc_context_set_sharding.argtypes = [vp, i]
         L.xc_context_devices.argtypes = [vp, ip, ip]
+        L.xc_context_synchronize.argtypes = [vp]
         L.xc_profile_enable.argtypes = [vp, i]
         L.xc_profile_reset.argtypes = [vp]
         L.xc_profile_get.argtypes = [vp, i, C.c_char_p, i, dp, C.POINTER(C.c_longlong)]
@@ -186,6 +187,9 @@ class Context:
         check(lib().xc_context_create_rank(int(device), buf, int(rank), int(nranks), C.byref(h)),
               None)
         return cls(int(device), _handle=h)
+
+    def synchronize(self):
+        check(lib().xc_context_synchronize(self.handle), self.handle)
 
     def devices(self):
         """(number of devices or ranks, whether the reduce is NCCL)."""

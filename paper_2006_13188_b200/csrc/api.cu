@@ -94,6 +94,10 @@ struct xc_context_s {
   std::map<int, PlanEntry> plans;
   std::map<int, PlanEntry> fast_plans;  // L -> in-place radix-16-last plan (or tw == null)
   std::map<std::string, DevBuf> bufs;
+  // device copies of band tables (ks, spectrum indices), uploaded once per
+  // distinct table: no per-call host->device copy, so device-memory calls
+  // can be captured in a CUDA graph
+  std::map<std::vector<int>, int*> band_tables;
   // detect_pattern's decomposed vote filters, by content (xc_detect_pattern)
   std::map<uint64_t, std::unique_ptr<xc_filter_s, void (*)(xc_filter_s*)>> det_filters;
   // events reused across calls (HostPipe slots, call timing)
@@ -138,6 +142,7 @@ struct xc_context_s {
     for (auto& kv : plans) cudaFree(kv.second.tw);
     for (auto& kv : fast_plans) cudaFree(kv.second.tw);
     for (auto& kv : bufs) cudaFree(kv.second.p);
+    for (auto& kv : band_tables) cudaFree(kv.second);
     for (cudaEvent_t e : ev_sync) cudaEventDestroy(e);
     for (cudaEvent_t e : ev_timing) cudaEventDestroy(e);
     if (own) cudaStreamDestroy(own);
@@ -182,6 +187,15 @@ struct xc_context_s {
       it = fast_plans.emplace(L, std::move(e)).first;
     }
     return it->second.tw ? &it->second.plan : nullptr;
+  }
+
+  int* band_table(const std::vector<int>& hb) {
+    auto it = band_tables.find(hb);
+    if (it != band_tables.end()) return it->second;
+    int* d = nullptr;
+    ck(cudaMalloc(&d, std::max<size_t>(hb.size(), 1) * sizeof(int)), "cudaMalloc bands");
+    ck(cudaMemcpy(d, hb.data(), hb.size() * sizeof(int), cudaMemcpyHostToDevice), "upload bands");
+    return band_tables.emplace(hb, d).first->second;
   }
 
   template <class T>
@@ -293,6 +307,7 @@ struct Call {
   cudaStream_t st;
   double h2d_s = 0, d2h_s = 0;
   bool out_dev = false;  // outputs are device buffers even when d.memory == XC_HOST
+  int nb_run = 0;        // bands transformed per image (Hermitian half-band: k >= 0)
 };
 
 std::vector<int> plan_components(const xcb::HostFilter& hf, const int* comps, int n) {
@@ -408,11 +423,9 @@ Call setup(xc_context ctx, xc_filter f, const xc_image_desc* d, int group_requir
   for (int k : c.ks) c.sidx.push_back(f->hf.index_of(k));
   c.Fhat = filter_spectra(c);
   c.sstride = size_t(g.Ph) * g.Pw;
-  int* dband = ctx->buf<int>("bands", 2 * c.ks.size());
   std::vector<int> hb(c.ks);
   hb.insert(hb.end(), c.sidx.begin(), c.sidx.end());
-  ck(cudaMemcpyAsync(dband, hb.data(), hb.size() * sizeof(int), cudaMemcpyHostToDevice, c.st),
-     "upload bands");
+  int* dband = ctx->band_table(hb);
   c.bands = xcb::Bands{dband, dband + c.ks.size(), int(c.ks.size())};
   return c;
 }
@@ -693,6 +706,7 @@ void run_gather(Call& c, const xcb::SigSrc& sig, const double* base, void* out, 
   const xcb::Geo& g = c.g;
   bool half;
   const xcb::Bands bands = gather_bands(c, &sig, 1, &half);
+  c.nb_run = bands.n;
   float2* T1 = c.ctx->buf<float2>("T1", size_t(g.Hx2) * g.Pw);
   float2* Hh = c.ctx->buf<float2>("Hhat", size_t(g.Ph) * g.Pw);
   float2* T2 = c.ctx->buf<float2>("T2", size_t(bands.n) * g.H2 * g.Pw);
@@ -726,6 +740,7 @@ void run_gather2(Call& c, const xcb::SigSrc* sig, double* const* base, void* con
   const xcb::Geo& g = c.g;
   bool half;
   const xcb::Bands bands = gather_bands(c, sig, 2, &half);
+  c.nb_run = bands.n;
   const size_t P = size_t(g.Ph) * g.Pw, tstride = size_t(bands.n) * g.H2 * g.Pw;
   float2* T1 = c.ctx->buf<float2>("T1", size_t(g.Hx2) * g.Pw);
   float2* Hh = c.ctx->buf<float2>("Hhat2", 2 * P);
@@ -756,11 +771,8 @@ xcb::Bands half_bands(Call& c, bool real_sig) {
       hk.push_back(c.ks[i]);
       hs.push_back(c.sidx[i]);
     }
-  int* db = c.ctx->buf<int>("bands_half", 2 * hk.size());
   hk.insert(hk.end(), hs.begin(), hs.end());
-  // pageable source: the copy is staged before cudaMemcpyAsync returns (as "bands")
-  ck(cudaMemcpyAsync(db, hk.data(), hk.size() * sizeof(int), cudaMemcpyHostToDevice, c.st),
-     "upload bands");
+  int* db = c.ctx->band_table(hk);
   const int n = int(hs.size());
   return xcb::Bands{db, db + n, n};
 }
@@ -778,6 +790,7 @@ void run_scatter(Call& c, const xcb::SigSrc& sig, const double* base, void* out,
     half = hb.n > 0;
     if (half) bands = hb;
   }
+  c.nb_run = bands.n;
   float2* T1 = c.ctx->buf<float2>("T1b", size_t(bands.n) * g.Hx2 * g.Pw);
   float2* Sg = c.ctx->buf<float2>("Sigma", size_t(g.Ph) * g.Pw);
   float2* T2 = c.ctx->buf<float2>("T2s", size_t(g.H2) * g.Pw);
@@ -859,6 +872,7 @@ void run_gather_dual(Call& c, HostPipe& hp, const void* signal, const void* para
       prep(c, st, false, &base[s], nullptr, s, img);
       if (img == 0) {
         bands = gather_bands(c, &st.sig, 1, &half);
+        c.nb_run = bands.n;
         for (int i = 0; i < 2; ++i)
           T2[i] = c.ctx->buf<float2>("T2_d" + std::to_string(i), size_t(bands.n) * g.H2 * g.Pw);
       }
@@ -898,6 +912,7 @@ void fill_stats(Call& c, xc_stats* st, double gpu_s, double total_s, long long o
   st->seconds_d2h = c.d2h_s;
   st->seconds_total = total_s;
   st->gpu_launches = c.lc.n;
+  st->bands_run = c.nb_run;
 }
 
 void run_single(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d,
@@ -1133,9 +1148,16 @@ void run_single(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d,
       img += n;
     }
     ck(cudaEventRecord(e1, c.st), "event");
-    hp.finish();
-    guard_check(c, param);
-    gpu_s = event_seconds(e0, e1);
+    // XC_FLAG_ASYNC with device memory and nothing to read back (no scale
+    // guard): return with the work queued on the stream (capturable in a
+    // CUDA graph); the caller synchronizes
+    const bool async = (flags & XC_FLAG_ASYNC) && d->memory == XC_DEVICE && !out_dev &&
+                       c.f->hf.group != XC_SCALE2 && !ctx->profiling;
+    if (!async) {
+      hp.finish();
+      guard_check(c, param);
+      gpu_s = event_seconds(e0, e1);
+    }
     ctx->resolve_profile();
     fill_stats(c, stats, gpu_s,
                std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count(),
@@ -1187,7 +1209,7 @@ void check_integral(xc_filter f) {
 
 struct SmoothPart {
   double gpu_s = 0, h2d_s = 0;
-  int launches = 0, pad_h = 0, pad_w = 0;
+  int launches = 0, pad_h = 0, pad_w = 0, bands_run = 0;
   long long bands = 0;
 };
 
@@ -1237,6 +1259,7 @@ SmoothPart smooth_partials(xc_context ctx, xc_filter f, const xc_image_desc* d,
   hp.finish();
   guard_check(c, param);
   SmoothPart r;
+  r.bands_run = c.nb_run;
   r.gpu_s = event_seconds(e0, e1);
   r.launches = c.lc.n;
   r.pad_h = c.g.Ph;
@@ -1303,6 +1326,7 @@ void smooth_single(xc_context ctx, xc_filter f, const xc_image_desc* d, const vo
     stats->seconds_total =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
     stats->gpu_launches = part.launches + flc.n;
+    stats->bands_run = part.bands_run;
   }
 }
 
@@ -1358,13 +1382,12 @@ int xc_anglemax(xc_context ctx, xc_filter f, const xc_image_desc* d, const void*
           hk.push_back(c.ks[i]);
           hs.push_back(c.sidx[i]);
         }
-      int* db = ctx->buf<int>("bands_half", 2 * hk.size());
       std::vector<int> hb(hk);
       hb.insert(hb.end(), hs.begin(), hs.end());
-      ck(cudaMemcpy(db, hb.data(), hb.size() * sizeof(int), cudaMemcpyHostToDevice),
-         "upload bands");
+      int* db = ctx->band_table(hb);
       bands = xcb::Bands{db, db + hk.size(), int(hk.size())};
     }
+    c.nb_run = bands.n;
     float2* planes = ctx->buf<float2>("planes", size_t(bands.n) * npix);
     float2* T1 = ctx->buf<float2>("T1", size_t(c.g.Hx2) * c.g.Pw);
     float2* Hh = ctx->buf<float2>("Hhat", size_t(c.g.Ph) * c.g.Pw);
@@ -2067,7 +2090,20 @@ struct Group {
   bool rank_mode = false;
   int rank = 0, nranks = 1;
   int shard = XC_SHARD_BANDS;
+  // XC_FLAG_ASYNC (rank contexts): the reduce of call i runs on `comm` while
+  // call i + 1 computes into the other partial buffer
+  int device = 0;
+  cudaStream_t comm = nullptr;
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  int slot = 0;
   ~Group() {
+    if (comm) {
+      cudaSetDevice(device);
+      cudaStreamSynchronize(comm);
+      for (cudaEvent_t e : done)
+        if (e) cudaEventDestroy(e);
+      cudaStreamDestroy(comm);
+    }
     for (ncclComm_t c : comms)
       if (c) nccl().CommDestroy(c);
     for (xc_context k : kids) delete k;
@@ -2220,6 +2256,7 @@ void merge_stats(xc_stats* out, const std::vector<xc_stats>& st, long long ops, 
     out->seconds_d2h = std::max(out->seconds_d2h, s.seconds_d2h);
     out->clamped_pixels += s.clamped_pixels;
     out->gpu_launches += s.gpu_launches;
+    out->bands_run += s.bands_run;
   }
   out->seconds_total = t0_s;
 }
@@ -2246,8 +2283,49 @@ void run_group(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d,
   const size_t npix = size_t(d->height) * d->width, os = dtype_size(d->out_dtype);
   const size_t bytes = npix * size_t(d->batch) * os;
   const bool f64 = d->out_dtype == XC_C128;
-  const unsigned kid_flags = flags & ~XC_FLAG_ACCUMULATE;
+  const unsigned kid_flags = flags & ~(XC_FLAG_ACCUMULATE | XC_FLAG_ASYNC);
   xcb::LaunchCounter lc;
+
+  if (G.rank_mode && (flags & XC_FLAG_ASYNC) && d->memory == XC_DEVICE) {
+    // compute into partial slot s (host-synchronous, like every call), then
+    // queue the reduce and the root's delivery on the comm stream and return;
+    // slot s is reused two calls later, after its reduce completed
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (!G.comm) {
+      G.device = ctx->device;
+      ck(cudaStreamCreateWithFlags(&G.comm, cudaStreamNonBlocking), "cudaStreamCreate");
+      for (auto& e : G.done) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    }
+    const int s = G.slot;
+    G.slot ^= 1;
+    ck(cudaEventSynchronize(G.done[s]), "previous reduce");
+    const std::vector<int> mine = shard_bands(ks, G.rank, G.nranks);
+    void* part = ctx->buf<char>("grp_part" + std::to_string(s), bytes);
+    xc_stats st{};
+    if (mine.empty()) {
+      ck(cudaMemsetAsync(part, 0, bytes, ctx->stream), "memset");
+      ck(cudaStreamSynchronize(ctx->stream), "memset");
+    } else {
+      run_single(ctx, f, mode, d, signal, param, mine.data(), int(mine.size()),
+                 (kid_flags & ~XC_FLAG_ASYNC) | (G.rank ? XC_FLAG_NO_INNER_DC : 0u), part, &st,
+                 true);
+    }
+    const NcclApi& a = nccl_or_throw();
+    nck(a.Reduce(part, part, bytes / (f64 ? 8 : 4), f64 ? ncclDouble : ncclFloat, ncclSum, 0,
+                 G.comms[0], G.comm),
+        "ncclReduce");
+    if (G.rank == 0) {
+      if (accumulate)
+        xcb::launch_accumulate(out, part, bytes / (f64 ? 8 : 4), f64 ? 1 : 0, G.comm, lc);
+      else
+        ck(cudaMemcpyAsync(out, part, bytes, cudaMemcpyDeviceToDevice, G.comm), "D2D");
+      ck(cudaGetLastError(), "deliver");
+    }
+    ck(cudaEventRecord(G.done[s], G.comm), "event");
+    st.gpu_launches += lc.n;
+    merge_stats(stats, {st}, (long long)ks.size(), since(t_start));
+    return;
+  }
 
   if (G.rank_mode) {  // one process per GPU: this rank's bands, then ncclReduce to rank 0
     ck(cudaSetDevice(ctx->device), "cudaSetDevice");
@@ -2297,6 +2375,7 @@ void run_group(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d,
       }
     });
     merge_stats(stats, st, (long long)ks.size(), since(t_start));
+    if (stats) stats->bands_run = st[0].bands_run;  // every device ran all bands
     return;
   }
 
@@ -2369,6 +2448,7 @@ void smooth_group(xc_context ctx, xc_filter f, const xc_image_desc* d, const voi
     s.pad_w = p.pad_w;
     s.seconds_fft = p.gpu_s;
     s.gpu_launches = p.launches;
+    s.bands_run = p.bands_run;
     return s;
   };
 
@@ -2418,6 +2498,7 @@ void smooth_group(xc_context ctx, xc_filter f, const xc_image_desc* d, const voi
       }
     });
     merge_stats(stats, st, 2 * (long long)all.size(), since(t_start));
+    if (stats) stats->bands_run = st[0].bands_run;
     return;
   }
 
@@ -2535,6 +2616,23 @@ int xc_context_set_sharding(xc_context ctx, int shard) {
     if (ctx->group->rank_mode && shard == XC_SHARD_BATCH)
       throw std::invalid_argument("rank contexts shard bands (split batches per rank instead)");
     ctx->group->shard = shard;
+  });
+}
+
+int xc_context_synchronize(xc_context ctx) {
+  return guarded(ctx, [&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+    if (Group* G = ctx->group) {
+      if (G->comm) ck(cudaStreamSynchronize(G->comm), "sync comm");
+      for (xc_context k : G->kids) {
+        ck(cudaSetDevice(k->device), "cudaSetDevice");
+        ck(cudaStreamSynchronize(k->stream), "sync");
+      }
+      ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    }
   });
 }
 

@@ -26,6 +26,7 @@ __device__ __forceinline__ int opaque(int v) {
 }
 
 __device__ __forceinline__ float2 cpow_step(float2 a, float2 z, int d) {
+  if (d == -1) return c_mul(a, c_conj(z));  // descending consecutive bands
   if (d < 0) {
     z = c_conj(z);
     d = -d;

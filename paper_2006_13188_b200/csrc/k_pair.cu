@@ -508,9 +508,11 @@ template <class PF>
 __global__ void __launch_bounds__(PF::T, PF::MINB)
     k_rows_fwd_premul_ilv(Geo g, SigSrc s, const double* __restrict__ base, Bands bl,
                           float2* __restrict__ T1, const float2* __restrict__ twm,
-                          const float2* __restrict__ twl) {
+                          const float2* __restrict__ twl, int full, int split) {
   constexpr int R0 = PF::R0, R2 = PF::R2;
-  constexpr int kThr = 4 * R0;  // TMEM columns per thread
+  // TMEM columns per thread: [cur, mul] per pass-0 input, then the pass-2
+  // twiddle row (out of the registers: no spills at 2 CTAs per SM)
+  constexpr int kThr = 4 * R0 + PF::kTwColsPad;
   static_assert(kThr * PF::WPQ <= 512, "TMEM budget");
   extern __shared__ __align__(16) float4 smp[];
   float4* W04 = smp;
@@ -519,19 +521,29 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
   float2* W0 = reinterpret_cast<float2*>(W04);
   float2* W1 = reinterpret_cast<float2*>(W14);
   __shared__ uint32_t tbase;
-  const int b = blockIdx.x, t = threadIdx.x;
+  // row pairs below `full` run every band; the pairs of the last, partial
+  // wave are split into `split` band chunks (tail_split) so the tail fills
+  // the SMs
+  int b = blockIdx.x, b0 = 0, b1 = bl.n;
+  if (b >= full) {
+    const int u = b - full, ch = u % split;
+    b = full + u / split;
+    b0 = ch * bl.n / split;
+    b1 = (ch + 1) * bl.n / split;
+  }
+  const int t = threadIdx.x;
   if (t < 32) tmem_alloc(&tbase, PF::tmem_cols(kThr));
   for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
-  typename PF::LastTw tl;
-  PF::load_last_tw(twl, tl);
   tmem_fence_before_sync();
   __syncthreads();
   tmem_fence_after_sync();
   const int gi = t & 1, j = t >> 1;
   const uint32_t tc = tmem_warp_cols(tbase, kThr);
+  const uint32_t ttw = tc + 4 * R0;
+  park_last_tw<PF>(twl, ttw);
   {
     const int ys = src_index(2 * b + gi, g.Hx, g.H, g.R, g.periodic);
-    const int k0 = bl.k[0];
+    const int k0 = bl.k[b0];
     // batches of independent loads (the asm volatile TMEM stores would
     // otherwise serialise one load latency per r)
     constexpr int C = 4;
@@ -565,12 +577,13 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
     tmem_wait_st();
   }
   const size_t plane = size_t(g.Hx2) * g.Pw;  // float2 per T1 band plane
-  for (int bi = 0; bi < bl.n; ++bi) {
+  for (int bi = b0; bi < b1; ++bi) {
     {
-      // pass-0 inputs of this band, then advance cur to the next band's k
-      const int dk = bi + 1 < bl.n ? bl.k[bi + 1] - bl.k[bi] : 0;
-      typename PF::P0Regs v;
-      float2 cur[R0];
+      // pass-0 inputs of this band, then advance cur to the next band's k:
+      // bands run in descending k, so the step is almost always -1 (one
+      // multiply by conj(mul), a CTA-uniform branch); other steps loop
+      const int dk = bi + 1 < b1 ? bl.k[bi + 1] - bl.k[bi] : 0;
+      typename PF::P0Regs v;  // the pass-0 inputs, read straight from TMEM
 #pragma unroll
       for (int r0 = 0; r0 < R0; r0 += 4) {
         float4 cm[4];
@@ -579,22 +592,23 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
         tmem_depn<16>(reinterpret_cast<float*>(cm));
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          cur[r0 + i] = make_float2(cm[i].x, cm[i].y);
-          float2 nx = cur[r0 + i], m = make_float2(cm[i].z, cm[i].w);
-          int d = dk;
-          if (d < 0) {
-            m = c_conj(m);
-            d = -d;
+          v.a[r0 + i] = make_float2(cm[i].x, cm[i].y);
+          const float2 m = make_float2(cm[i].z, cm[i].w);
+          float2 nx;
+          if (dk == -1) {
+            nx = c_mul(v.a[r0 + i], c_conj(m));
+          } else {
+            nx = v.a[r0 + i];
+            const float2 mm = dk < 0 ? c_conj(m) : m;
+            for (int q = 0; q < (dk < 0 ? -dk : dk); ++q) nx = c_mul(nx, mm);
           }
-          for (int q = 0; q < d; ++q) nx = c_mul(nx, m);
           cm[i].x = nx.x;
           cm[i].y = nx.y;
         }
-        if (bi + 1 < bl.n) tmem_stn<16>(tc + 4 * r0, reinterpret_cast<const float*>(cm));
+        if (bi + 1 < b1) tmem_stn<16>(tc + 4 * r0, reinterpret_cast<const float*>(cm));
       }
       tmem_wait_st();
-      auto load = [&](int r, int, int) -> float2 { return cur[r]; };
-      PF::pass0_compute(load, v);
+      if ((opaque_i(t) >> 1) < PF::NB0) Dft<R0>::run(v.a);
       PF::pass0_store(W0, v);
     }
     __syncthreads();
@@ -613,7 +627,11 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
         p += ostep;
       }
     };
-    PF::pass2_all(W1, tl, store);
+    float2 w[PF::kTwColsPad / 2 + 1];
+    tmem_ldn<PF::kTwColsPad>(ttw, reinterpret_cast<float*>(w + 1));
+    tmem_wait_ld();
+    tmem_depn<PF::kTwColsPad>(reinterpret_cast<float*>(w + 1));
+    PF::pass2_all_w(W1, w, store);
   }
   tmem_fence_before_sync();
   __syncthreads();
@@ -948,6 +966,16 @@ PairTw pair_tables() {
 
 }  // namespace
 
+// S1 at 1152 (config 2): the pair kernel (0.109 ms) unless XCB_S1_PAIR=0
+// selects the fast one (0.124 ms)
+bool s1_pair_small() {
+  static const bool on = [] {
+    const char* e = std::getenv("XCB_S1_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // 0 if no pair plan for L (or the stage does not fit); else the dynamic smem.
 // stage 0 I1, 1 I2, 2 planes, 3 S1, 4 S2, 5 F1, 6 F2, 7 S4
 size_t pair_smem(int stage, int L, const Geo& g) {
@@ -958,7 +986,7 @@ size_t pair_smem(int stage, int L, const Geo& g) {
     const size_t tw = size_t(PF::TWM) * sizeof(float2);                            \
     const size_t w = 2 * size_t(PF::LP) * sizeof(float4);                          \
     if (stage <= 2) s = size_t(LL) * sizeof(float4) + w + tw;                      \
-    if (stage == 3 && LL >= 2048) s = w + tw; /* 1152: the fast kernel is faster */ \
+    if (stage == 3 && (LL >= 2048 || s1_pair_small())) s = w + tw;                  \
     if (stage == 4 && g.Hx2 <= LL) s = 3 * size_t(LL) * sizeof(float4) + w + tw;   \
     if (stage == 5 || stage == 7) s = w + tw;                                      \
     if (stage == 6 && g.Hx2 <= LL) s = size_t(LL) * sizeof(float4) + w + tw;      \
@@ -1146,9 +1174,11 @@ void launch_rows_fwd_premul_pair(const Geo& g, const SigSrc& s, const double* ba
   case LL: {                                                                                \
     using PF = IlvFft<LL, R0, R1, R2, PP>;                                                  \
     const PairTw tw = pair_tables<PF>();                                                    \
+    /* no tail split: config 4's 3.5 waves measured 0.306 ms split, 0.297 ms not */         \
+    const int rows2 = g.Hx2 / 2;                                                            \
     set_smem(k_rows_fwd_premul_ilv<PF>, sm);                                                \
-    k_rows_fwd_premul_ilv<PF><<<g.Hx2 / 2, PF::T, sm, st>>>(g, s, base, b, T1, tw.mid,      \
-                                                            tw.last);                       \
+    k_rows_fwd_premul_ilv<PF><<<rows2, PF::T, sm, st>>>(g, s, base, b, T1, tw.mid, tw.last,  \
+                                                        rows2, 1);                          \
     break;                                                                                  \
   }
   XCB_PAIR_DISPATCH(g.Pw, XCB_BODY)

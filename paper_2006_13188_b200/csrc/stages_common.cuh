@@ -12,16 +12,18 @@ namespace {
 constexpr double kTwoPiHi = 6.283185307179586232;
 constexpr double kTwoPiLo = 2.4492935982947064e-16;
 constexpr double kInvTwoPi = 0.15915494309189533577;
+constexpr double kInvPi = 0.31830988618379067154;
 
-// e^{sign * i * k * base}: the product is formed and reduced mod 2 pi in double
-// (k*theta is exact for fp32 theta), then evaluated with accurate sincosf.
+// e^{sign * i * k * base}: the product is formed and reduced to half turns in
+// [-1, 1] in double (k*theta is exact for fp32 theta), then evaluated with
+// sincospif (accurate to ~1 ulp, no range reduction left to do).
 __device__ __forceinline__ float2 steer(int k, double base, float sign) {
   const double ph = double(k) * base;
   const double q = rint(ph * kInvTwoPi);
   double r = fma(-q, kTwoPiHi, ph);
   r = fma(-q, kTwoPiLo, r);
   float s, c;
-  sincosf(float(r), &s, &c);
+  sincospif(float(r * kInvPi), &s, &c);
   return make_float2(c, sign * s);
 }
 

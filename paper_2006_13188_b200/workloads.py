@@ -120,28 +120,38 @@ class Workload:
         return B * H * W * ops
 
 
-def config1(n: int = 256, seed: int = 0) -> Workload:
+def _decompose(D, f, backend):
+    """Decompose the filter image with the product's host code (default) or a
+    test-side backend module (oracle.oracle / oracle.refimpl: the bench's
+    reference arm builds its filter without loading the product library)."""
+    import sys
+    mod = backend if backend is not None else sys.modules[__name__]
+    fn = mod.decompose_rotation2 if D[0] == "rotation2" else mod.decompose_scale2
+    return fn(f, *D[1])
+
+
+def config1(n: int = 256, seed: int = 0, backend=None) -> Workload:
     rng = np.random.default_rng([seed, 1])
     sig = rng.uniform(0, 1, (1, n, n)).astype(np.float32)
     th = rng.uniform(0, 2 * math.pi, (1, n, n)).astype(np.float32)
     f = angular_filter(15, 6.0, 4, rng)
     D = ("rotation2", (15, 15, 8, 30, 32, 15.0))
-    F = decompose_rotation2(f, *D[1])
+    F = _decompose(D, f, backend)
     return Workload(f"cfg1-xcorr-rot-{n}", "xcorr", sig, th, 0, F, f, decomp=D)
 
 
-def config2(n: int = 1024, seed: int = 0) -> Workload:
+def config2(n: int = 1024, seed: int = 0, backend=None) -> Workload:
     rng = np.random.default_rng([seed, 2])
     sig = rng.uniform(0, 1, (1, n, n)).astype(np.float32)
     _, d = gradient(gaussian_blur(rng.standard_normal((n, n)), 4.0))
     th = d[None].astype(np.float32)
     f = angular_filter(16, 8.0, 8, rng)
     D = ("rotation2", (16, 16, 16, 32, 34, 16.0))
-    F = decompose_rotation2(f, *D[1])
+    F = _decompose(D, f, backend)
     return Workload(f"cfg2-xconv-rot-{n}", "xconv", sig, th, 0, F, f, decomp=D)
 
 
-def config3(n: int = 4096, n_templates: int = 3, seed: int = 0) -> Workload:
+def config3(n: int = 4096, n_templates: int = 3, seed: int = 0, backend=None) -> Workload:
     rng = np.random.default_rng([seed, 3])
     img = rng.standard_normal((n, n))
     tpl = smooth_template(64, rng)
@@ -157,13 +167,13 @@ def config3(n: int = 4096, n_templates: int = 3, seed: int = 0) -> Workload:
         paste_rotated(img, 4.0 * tpl, cx, cy, ang)
         truth.append((cx, cy, ang))
     D = ("rotation2", (31.5, 31.5, 32, 64, 66, 31.5))
-    F = decompose_rotation2(tpl, *D[1])
+    F = _decompose(D, tpl, backend)
     return Workload(f"cfg3-anglemax-rot-{n}", "anglemax", img[None].astype(np.float32), None,
                     0, F, tpl, {"truth": truth, "n_angles": 360, "nms_radius": 32.0,
                                 "threshold": 0.5}, decomp=D)
 
 
-def config4(n: int = 2048, seed: int = 0) -> Workload:
+def config4(n: int = 2048, seed: int = 0, backend=None) -> Workload:
     rng = np.random.default_rng([seed, 4])
     sig = (rng.uniform(0, 1, (n, n)) + rng.normal(0, 0.05, (n, n)))[None].astype(np.float32)
     z = gaussian_blur(rng.standard_normal((n, n)), 16.0)
@@ -174,17 +184,17 @@ def config4(n: int = 2048, seed: int = 0) -> Workload:
     f = np.exp(-(x * x + y * y) / (2 * 8.0 ** 2))
     f[x * x + y * y > R * R] = 0
     D = ("scale2", (R, R, 12, 64, 32, 1.0, float(R)))
-    F = decompose_scale2(f, *D[1])
+    F = _decompose(D, f, backend)
     return Workload(f"cfg4-smooth-scale-{n}", "smooth", sig, s, 1, F, f, decomp=D)
 
 
-def config5(n: int = 4096, batch: int = 16, seed: int = 0) -> Workload:
+def config5(n: int = 4096, batch: int = 16, seed: int = 0, backend=None) -> Workload:
     rng = np.random.default_rng([seed, 5])
     sig = rng.uniform(0, 1, (batch, n, n)).astype(np.float32)
     th = rng.uniform(0, 2 * math.pi, (batch, n, n)).astype(np.float32)
     f = angular_filter(31, 14.0, 32, rng)
     D = ("rotation2", (31, 31, 64, 62, 130, 31.0))
-    F = decompose_rotation2(f, *D[1])
+    F = _decompose(D, f, backend)
     return Workload(f"cfg5-xcorr-rot-{batch}x{n}", "xcorr", sig, th, 0, F, f, decomp=D)
 
 

@@ -156,3 +156,27 @@ def test_rank_context_single_rank_nccl(orc):
     sm = X.smooth_adaptive(Hs.real.copy(), X.XformField.scaling(S), Fs, device=ctx)
     ref = orc.smooth_adaptive(Hs.real.copy(), 1, S, ofilter(orc, Fs))[0]
     assert orc.rel_l2(sm.output, ref) < TOL
+
+
+def test_rank_context_async_reduce(orc):
+    """XC_FLAG_ASYNC: the reduce of call i is queued on the context's comm
+    stream and overlaps call i + 1 (two partial slots); after
+    xc_context_synchronize both outputs equal the synchronous result."""
+    import torch
+    F, H, T = _rot_case(orc)
+    n = H.shape[0]
+    ctx = N.Context.rank(0, N.nccl_unique_id(), 0, 1)
+    hs = torch.from_numpy(H.astype(np.complex64)).cuda()
+    ts = torch.from_numpy(T.astype(np.float32)).cuda()
+    outs = [torch.zeros((n, n), dtype=torch.complex64, device="cuda") for _ in range(3)]
+    d = N.ImageDesc(n, n, 1, N.XC_C64, N.XC_F32, N.XC_C64, N.XC_ROW_MAJOR, N.XC_DEVICE, 1,
+                    N.XC_ROTATION2)
+    st = N.Stats()
+    for o in outs:
+        N.check(N.lib().xc_run(ctx.handle, F.handle(), 0, C.byref(d), C.c_void_p(hs.data_ptr()),
+                               C.c_void_p(ts.data_ptr()), None, 0, N.XC_FLAG_ASYNC,
+                               C.c_void_p(o.data_ptr()), C.byref(st)), ctx.handle)
+    ctx.synchronize()
+    one = X.xcorr_fast(H.astype(np.complex64), X.XformField.rotation(T.astype(np.float32)), F)
+    for o in outs:
+        assert np.array_equal(o.cpu().numpy(), one.output)

@@ -1,0 +1,7 @@
+python tools/bench_configs.py 2 4 > gpurun_out/c6_cfg24.jsonl 2>&1
+XCB_S1_PAIR=1 python tools/bench_configs.py 2 > gpurun_out/c6_cfg2_pair.jsonl 2>&1
+XCB_TAIL_SPLIT=0 python tools/bench_configs.py 4 > gpurun_out/c6_cfg4_nosplit.jsonl 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fuzz.py tests/test_gpu_fullsize.py -x -q -k "scatter or xconv or smooth or config2 or config4 or fuzz or hermitian" > gpurun_out/c6_tests.log 2>&1; echo rc=$? >> gpurun_out/c6_tests.log
+XCB_S1_PAIR=1 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "scatter or xconv or smooth" > gpurun_out/c6_tests_pair.log 2>&1; echo rc=$? >> gpurun_out/c6_tests_pair.log
+ncu --set full --clock-control none --import-source on -k regex:"premul" -c 1 -o gpurun_out/c6_s1_cfg4 python tools/profile_case.py smooth 4 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"premul" -c 1 -o gpurun_out/c6_s1_cfg2 python tools/profile_case.py xconv 2 > /dev/null 2>&1
