@@ -121,6 +121,7 @@ def stage_bytes(stage: str, B: int, H: int, W: int, Ph: int, Pw: int, ni: int = 
         "S2_cols_fwd_mac_inv": B * 8 * Hx2 * Pw + B * 8 * P + 8 * H2 * Pw,
         "S4_rows_inv_out": 8 * H2 * Pw + 8 * N,
         "smooth_finish": 8 * N + 8 * N + 4 * N,
+        "absmax": 4 * N,
     }.get(stage, float("nan"))
 
 
@@ -462,13 +463,33 @@ def run_b200(args):
         alg = stage_bytes(name, nb_run, H, W, Ph, Pw, ni)
         return alg, per_launch_s, ni, alg / per_launch_s / 1e9
 
+    # committed ncu --set full per-launch statistics (tools/ncu_stats.py)
+    kstats = {}
+    sf = os.path.join(ROOT, "profiles", "ncu_kernel_stats.json")
+    if os.path.exists(sf):
+        with open(sf) as f:
+            kstats = json.load(f)
+    clk_now = clk.summary()
+    sm_mhz = clk_now.get("sm_mhz") or clk_now.get("sm_max_mhz") or 1965.0
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+
+    def issue_roof(name, per_launch_s):
+        """The instruction-issue roofline: ncu's warp instructions per launch of
+        this kernel (same code, same config) over the live launch time at the
+        sampled SM clock, against one warp instruction per cycle per SMSP."""
+        ks = kstats.get(f"cfg{args.config}:{name}")
+        if not ks or not ks.get("warp_instructions"):
+            return None
+        peak = 4 * n_sm * sm_mhz * 1e6  # warp instructions / s
+        ach = ks["warp_instructions"] / per_launch_s
+        return {"warp_instructions_per_launch": ks["warp_instructions"], "achieved": ach,
+                "peak": peak, "unit": "warp inst/s", "frac": ach / peak,
+                "sm_mhz": sm_mhz, "source": ks.get("source")}
+
     if dom:
         alg, per_launch_s, ni, achieved = kernel_roof(dom)
-        traffic = None
-        tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(tf):
-            with open(tf) as f:
-                traffic = json.load(f).get(f"cfg{args.config}:{dom}")
+        ks = kstats.get(f"cfg{args.config}:{dom}")
+        traffic = ks["dram_bytes"] * ni if ks and ks.get("dram_bytes") else None
         roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_kind,
                 "alg_bytes_per_launch": alg, "ms_per_launch": per_launch_s * 1e3,
@@ -476,10 +497,12 @@ def run_b200(args):
                 "stage_events": "in the timed region" if in_region else
                                 "separate profiled pass of the same steps (short steps)",
                 "cuda_graph": graphed,
+                "issue": issue_roof(dom, per_launch_s),
                 "kernels": {k: {"ms_per_launch": kernel_roof(k)[1] * 1e3,
                                 "images_per_launch": kernel_roof(k)[2],
                                 "achieved_gbs": kernel_roof(k)[3],
-                                "frac": kernel_roof(k)[3] / hbm}
+                                "frac": kernel_roof(k)[3] / hbm,
+                                "issue_frac": (issue_roof(k, kernel_roof(k)[1]) or {}).get("frac")}
                             for k in prof if k != "prep"},
                 "stages_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
                 "pipeline_model_frac": model_bytes(mode, nb, H * W, Ph * Pw) * Bl /

@@ -21,6 +21,8 @@
  *   xc_decompose_rotation2/scale2  <- decompose_rotation2 / decompose_scale2
  *                                     freq_filter.hpp:63-129 (host, once per
  *                                     filter)
+ *   xc_decompose_*_device          <- the same on the GPU (per-call builds:
+ *                                     detect_pattern, contour matching)
  *   xc_render_component / xc_reconstruct / xc_inner_dc_value
  *                                  <- freq_filter.hpp:165-235 (host)
  *   3D rotation pipeline:
@@ -167,6 +169,17 @@ int xc_profile_reset(xc_context ctx);
 int xc_profile_get(xc_context ctx, int idx, char* name, int name_len, double* total_ms,
                    long long* launches);
 
+/* Out-of-bounds debug mode (no compute-sanitizer on the GPU pool).  With the
+ * environment variable XCB_GUARD=<bytes> set before the first allocation, every
+ * context buffer gets a guard zone of that size on each side and the whole
+ * allocation is poisoned with 0xFF bytes (NaN in fp32 / fp64).
+ * xc_debug_check_guards synchronizes the device and counts the guard zones
+ * that changed (*n_bad; the first one's buffer name in first_bad); a stray or
+ * uninitialised read surfaces as NaN in the result.  xc_debug_guard_bytes
+ * returns the active guard size (0 = off). */
+int xc_debug_check_guards(xc_context ctx, int* n_bad, char* first_bad, int len);
+int xc_debug_guard_bytes(void);
+
 /* ---- filters (FreqFilter2) -------------------------------------------- */
 /* Filters are host objects (ctx may be NULL); device spectra are built on first
  * use per (device, pad size, layout) and freed by xc_filter_destroy.  Errors of
@@ -187,6 +200,18 @@ int xc_decompose_scale2(const double* filt, int height, int width, int layout,
                         double cx, double cy, int K, int n_radii, int n_angles,
                         double r_min, double r_max, double r_domain, int* ks_out,
                         double* comps_out, int* nc_out);
+/* The same decompositions computed on the context's device (per-call filter
+ * builds; freq_filter.hpp:63-129): polar / log-polar bilinear
+ * resampling and the band DFT as two kernels, fp64; identical validation and
+ * error texts, outputs in host memory as above. */
+int xc_decompose_rotation2_device(xc_context ctx, const double* filt, int height, int width,
+                                  int layout, double cx, double cy, int K, int n_radii,
+                                  int n_angles, double r_max, int* ks_out, double* comps_out,
+                                  int* nc_out);
+int xc_decompose_scale2_device(xc_context ctx, const double* filt, int height, int width,
+                               int layout, double cx, double cy, int K, int n_radii,
+                               int n_angles, double r_min, double r_max, double r_domain,
+                               int* ks_out, double* comps_out, int* nc_out);
 int xc_render_component(xc_filter f, int ci, int width, int height, double cx,
                         double cy, int layout, double* out);
 int xc_reconstruct(xc_filter f, int width, int height, double cx, double cy,

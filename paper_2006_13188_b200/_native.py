@@ -50,6 +50,8 @@ EXPORTS = [
     "xc_render_sph_component", "xc_reconstruct3", "xc_sph_harm", "xc_wigner_d", "xc_run3",
     "xc_white_noise", "xc_nccl_unique_id", "xc_context_create_multi", "xc_context_create_rank",
     "xc_context_set_sharding", "xc_context_devices", "xc_context_synchronize",
+    "xc_decompose_rotation2_device", "xc_decompose_scale2_device", "xc_debug_check_guards",
+    "xc_debug_guard_bytes",
 ]
 
 _lib = None
@@ -86,6 +88,16 @@ def lib():
         L.xc_filter_num_components.argtypes = [vp]
         L.xc_decompose_rotation2.argtypes = [dp, i, i, i, d, d, i, i, i, d, ip, dp, ip]
         L.xc_decompose_scale2.argtypes = [dp, i, i, i, d, d, i, i, i, d, d, d, ip, dp, ip]
+        try:  # (absent from older builds timed by tools/ab_kernels.py)
+            L.xc_debug_check_guards.argtypes = [vp, ip, C.c_char_p, i]
+            L.xc_debug_guard_bytes.argtypes = []
+            L.xc_decompose_rotation2_device.argtypes = [vp, dp, i, i, i, d, d, i, i, i, d, ip,
+                                                        dp, ip]
+            L.xc_decompose_scale2_device.argtypes = [vp, dp, i, i, i, d, d, i, i, i, d, d, d,
+                                                     ip, dp, ip]
+        except AttributeError:
+            if not os.environ.get("XCB_LIB_OVERRIDE"):
+                raise
         L.xc_render_component.argtypes = [vp, i, i, i, d, d, i, dp]
         L.xc_reconstruct.argtypes = [vp, i, i, d, d, ip, i, i, dp]
         L.xc_inner_dc_value.argtypes = [vp, dp]
@@ -216,6 +228,13 @@ class Context:
         if reset:
             check(L.xc_profile_reset(self.handle), self.handle)
         return out
+
+    def check_guards(self):
+        """(guard zones changed, first buffer name) -- XCB_GUARD debug mode."""
+        n = C.c_int(0)
+        name = C.create_string_buffer(128)
+        check(lib().xc_debug_check_guards(self.handle, C.byref(n), name, 128), self.handle)
+        return n.value, name.value.decode()
 
     def trim(self):
         check(lib().xc_context_trim(self.handle), self.handle)

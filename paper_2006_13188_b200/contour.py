@@ -186,7 +186,9 @@ def match_contours(query: ContourScene, target: ContourScene, qx: float, qy: flo
     R = vf.radius
     n_radii = max(4, 2 * R)
     n_angles = max(32, 8 * ((R + 3) // 4) * 4)
-    F = decompose_rotation2(vf.weights, float(R), float(R), int(K), n_radii, n_angles, R + 0.5)
+    # a per-call filter build: decomposed on the GPU (freq_filter.hpp:63-89)
+    F = decompose_rotation2(vf.weights, float(R), float(R), int(K), n_radii, n_angles, R + 0.5,
+                            device=True)
     resp = xconv_fast(target.signal, XformField.rotation(target.normal_angle), F)
     real = np.ascontiguousarray(resp.output.real, np.float64)
     peaks = find_peaks(real, eps / 2, 0.1)

@@ -63,9 +63,26 @@ struct PlanEntry {
 };
 
 struct DevBuf {
-  void* p = nullptr;
-  size_t n = 0;
+  void* p = nullptr;   // the allocation
+  size_t n = 0;        // usable bytes (after the leading guard)
+  size_t guard = 0;    // guard bytes on each side (XCB_GUARD)
+  void* user() const { return static_cast<char*>(p) + guard; }
 };
+
+// XCB_GUARD=<bytes>: debug mode for out-of-bounds checks (compute-sanitizer is
+// not available on the GPU pool).  Every context buffer gets a guard zone on
+// each side, and the whole allocation is poisoned with 0xFF bytes (a NaN in
+// fp32 and fp64): a stray write shows up as a changed guard byte
+// (xc_debug_check_guards), a stray or uninitialised read as NaN in the output,
+// which the parity tests compare with the oracle.
+size_t guard_bytes() {
+  static const size_t g = [] {
+    const char* e = std::getenv("XCB_GUARD");
+    const long long v = e ? std::atoll(e) : 0;
+    return v > 0 ? (size_t(v) + 255) / 256 * 256 : size_t(0);
+  }();
+  return g;
+}
 
 struct StageEvents {
   const char* name;
@@ -209,10 +226,13 @@ struct xc_context_s {
         b.p = nullptr;
         b.n = 0;
       }
-      ck(cudaMalloc(&b.p, bytes), ("cudaMalloc " + name).c_str());
+      const size_t g = guard_bytes();
+      ck(cudaMalloc(&b.p, bytes + 2 * g), ("cudaMalloc " + name).c_str());
       b.n = bytes;
+      b.guard = g;
+      if (g) ck(cudaMemsetAsync(b.p, 0xff, bytes + 2 * g, stream), "poison");
     }
-    return static_cast<T*>(b.p);
+    return static_cast<T*>(b.user());
   }
 };
 
@@ -289,6 +309,7 @@ void export_filter(const xcb::HostFilter& f, int* ks, double* comps, int* nc) {
 
 // Resolved geometry and per-call state shared by the pipelines.
 struct Call {
+  bool packed = false;  // smoothing: num + i alpha den from one scatter (SIG_PACK)
   xc_context ctx;
   xc_filter f;
   xc_image_desc d;
@@ -344,6 +365,9 @@ float2* filter_spectra(Call& c) {
   float2* T1f = c.ctx->buf<float2>("filter_T1", size_t(nb) * (S + 1) * c.g.Pw);
   float2* spec = nullptr;
   ck(cudaMalloc(&spec, size_t(nb) * c.g.Ph * c.g.Pw * sizeof(float2)), "cudaMalloc spectra");
+  if (guard_bytes())  // XCB_GUARD: poisoned, so a spectrum element never written reads NaN
+    ck(cudaMemsetAsync(spec, 0xff, size_t(nb) * c.g.Ph * c.g.Pw * sizeof(float2), c.st),
+       "poison");
   xcb::launch_filter_spectra(*c.prow, *c.pcol, c.g, dcomps, nb, T1f, spec, c.st, c.lc);
   ck(cudaGetLastError(), "filter spectra launch");
   ck(cudaStreamSynchronize(c.st), "filter spectra");  // host table lifetime
@@ -969,6 +993,38 @@ int xc_context_trim(xc_context ctx) {
   });
 }
 
+int xc_debug_check_guards(xc_context ctx, int* n_bad, char* first_bad, int len) {
+  return guarded(ctx, [&] {
+    if (!ctx || !n_bad) throw std::invalid_argument("null argument");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    ck(cudaDeviceSynchronize(), "sync");
+    int bad = 0;
+    std::string first;
+    std::vector<unsigned char> h;
+    for (auto& kv : ctx->bufs) {
+      const DevBuf& b = kv.second;
+      if (!b.guard) continue;
+      h.resize(b.guard);
+      for (int side = 0; side < 2; ++side) {
+        const char* z = static_cast<const char*>(b.p) + (side ? b.guard + b.n : 0);
+        ck(cudaMemcpy(h.data(), z, b.guard, cudaMemcpyDeviceToHost), "D2H guard");
+        if (std::any_of(h.begin(), h.end(), [](unsigned char c) { return c != 0xff; })) {
+          if (first.empty()) first = kv.first + (side ? " (after)" : " (before)");
+          ++bad;
+        }
+      }
+    }
+    *n_bad = bad;
+    if (first_bad && len > 0) {
+      std::strncpy(first_bad, first.c_str(), size_t(len) - 1);
+      first_bad[len - 1] = 0;
+    }
+  });
+}
+
+int xc_debug_guard_bytes(void) { return int(guard_bytes()); }
+
 int xc_profile_enable(xc_context ctx, int on) {
   return guarded(ctx, [&] {
     std::lock_guard<std::mutex> lk(ctx->mu);
@@ -1053,6 +1109,69 @@ int xc_decompose_scale2(const double* filt, int height, int width, int layout, d
     auto img = to_rowmajor(filt, height, width, layout);
     auto f = xcb::decompose_scale2(xcb::ImageView{img.data(), width, height}, cx, cy, K,
                                    n_radii, n_angles, r_min, r_max, r_domain);
+    export_filter(f, ks_out, comps_out, nc_out);
+  });
+}
+
+}  // extern "C"
+
+namespace {
+// decompose_* on the context's device: the shell carries the
+// validated metadata (host_filter.cpp rotation2_shell / scale2_shell); the
+// polar resampling and the band DFT run as two kernels (k_misc.cu
+// launch_decompose) and the small coefficient table comes back to the host.
+// The caller holds ctx->mu.
+void decompose_on_device(xc_context ctx, xcb::HostFilter& f, const std::vector<cplx>& img,
+                         int width, int height, double cx, double cy) {
+  ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+  const int nr = f.n_radii, na = f.n_angles, nc = f.nc(), rows = f.n_rows();
+  double2* dimg = ctx->buf<double2>("dec_img", std::max<size_t>(1, img.size()));
+  double2* samples = ctx->buf<double2>("dec_samples", size_t(nr) * na);
+  double2* comps = ctx->buf<double2>("dec_comps", size_t(rows) * nc);
+  int* dks = ctx->buf<int>("dec_ks", size_t(nc));
+  cudaStream_t st = ctx->stream;
+  if (!img.empty())
+    ck(cudaMemcpyAsync(dimg, img.data(), img.size() * sizeof(cplx), cudaMemcpyHostToDevice, st),
+       "H2D filter");
+  ck(cudaMemcpyAsync(dks, f.ks.data(), size_t(nc) * sizeof(int), cudaMemcpyHostToDevice, st),
+     "H2D ks");
+  xcb::LaunchCounter lc;
+  xcb::launch_decompose(dimg, width, height, cx, cy, nr, na, f.group,
+                        f.group == 1 ? f.r_min : 0.0, f.group == 1 ? f.domain_top() : f.r_max,
+                        dks, nc, samples, comps, st, lc);
+  ck(cudaGetLastError(), "decompose launch");
+  f.comps.assign(size_t(rows) * nc, cplx(0));
+  ck(cudaMemcpyAsync(f.comps.data(), comps, f.comps.size() * sizeof(cplx),
+                     cudaMemcpyDeviceToHost, st),
+     "D2H comps");
+  ck(cudaStreamSynchronize(st), "decompose");
+}
+}  // namespace
+
+extern "C" {
+
+int xc_decompose_rotation2_device(xc_context ctx, const double* filt, int height, int width,
+                                  int layout, double cx, double cy, int K, int n_radii,
+                                  int n_angles, double r_max, int* ks_out, double* comps_out,
+                                  int* nc_out) {
+  return guarded(ctx, [&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    auto f = xcb::rotation2_shell(K, n_radii, n_angles, r_max);
+    decompose_on_device(ctx, f, to_rowmajor(filt, height, width, layout), width, height, cx, cy);
+    export_filter(f, ks_out, comps_out, nc_out);
+  });
+}
+
+int xc_decompose_scale2_device(xc_context ctx, const double* filt, int height, int width,
+                               int layout, double cx, double cy, int K, int n_radii,
+                               int n_angles, double r_min, double r_max, double r_domain,
+                               int* ks_out, double* comps_out, int* nc_out) {
+  return guarded(ctx, [&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    auto f = xcb::scale2_shell(K, n_radii, n_angles, r_min, r_max, r_domain);
+    decompose_on_device(ctx, f, to_rowmajor(filt, height, width, layout), width, height, cx, cy);
     export_filter(f, ks_out, comps_out, nc_out);
   });
 }
@@ -1211,7 +1330,31 @@ struct SmoothPart {
   double gpu_s = 0, h2d_s = 0;
   int launches = 0, pad_h = 0, pad_w = 0, bands_run = 0;
   long long bands = 0;
+  bool packed = false;  // num + i alpha den in numden[img][0] (SIG_PACK)
 };
+
+// num and den of smooth_adaptive from ONE scatter (SIG_PACK): with a real
+// signal, real weights and a filter whose selected bands satisfy
+// F_{-k} = conj(F_k) (and a real inner DC), num and den are real, so the
+// complex signal h w + i alpha w scatters to num + i alpha den.  It replaces
+// the reference's two xconv_fast calls (engine.hpp:402-403) by one over the
+// full band set: num and den share every staged F^_k column, T1 pass and the
+// single inverse transform, and the divide reads one array.  XCB_PACK=0 runs
+// the two scatters (each in the Hermitian half-band mode).
+bool smooth_packable(const Call& c, const xcb::SigSrc& sig, bool dc) {
+  static const bool on = [] {
+    const char* e = std::getenv("XCB_PACK");
+    return !(e && e[0] == '0');
+  }();
+  if (!on || sig.is_complex || !c.f->hf.hermitian()) return false;
+  for (int k : c.ks)
+    if (std::count(c.ks.begin(), c.ks.end(), -k) != 1) return false;
+  if (dc) {
+    const cplx v = xcb::inner_dc_value(c.f->hf);
+    if (std::abs(v.imag()) > 1e-12 * std::max(1.0, std::abs(v))) return false;
+  }
+  return true;
+}
 
 // The two extended convolutions of smooth_adaptive (engine.hpp:394-403),
 // num = xconv(H~) and den = xconv(1~), for every image of the batch over the
@@ -1224,7 +1367,7 @@ template <class OnImage>
 SmoothPart smooth_partials(xc_context ctx, xc_filter f, const xc_image_desc* d,
                            const void* signal, const void* param, int normalize_signal,
                            const int* comps, int ncomp, bool dc, float2* numden,
-                           OnImage&& on_image) {
+                           OnImage&& on_image, unsigned* amax = nullptr) {
   ck(cudaSetDevice(ctx->device), "cudaSetDevice");
   Call c = setup(ctx, f, d, -1, comps, ncomp, false);
   c.out_dev = true;
@@ -1237,12 +1380,29 @@ SmoothPart smooth_partials(xc_context ctx, xc_filter f, const xc_image_desc* d,
   HostPipe hp(c);
   hp.h2d(signal, param, 0);
   ck(cudaEventRecord(e0, c.st), "event");
+  bool packed = false;
   for (int img = 0; img < d->batch; ++img) {
     hp.h2d(signal, param, img + 1);
     Staged s = hp.inputs(signal, param, img);
     double* base = nullptr;
     float* wgt = nullptr;
     prep(c, s, weighted, &base, weighted ? &wgt : nullptr, 0, img);
+    packed = c.packed = amax && smooth_packable(c, s.sig, dc);
+    if (packed) {
+      xcb::SigSrc sp = s.sig;
+      sp.mode = xcb::SIG_PACK;
+      sp.wgt = wgt;  // null: w = 1
+      sp.amax = amax + img;
+      sp.is_complex = 1;  // a complex signal: the full band set
+      stage(c, "absmax", [&] {
+        xcb::launch_absmax(static_cast<const float*>(s.sig.sig), npix, amax + img, c.st, c.lc);
+      });
+      run_scatter(c, sp, base, numden + 2 * size_t(img) * npix, xcb::OUT_C64, false, dc);
+      ck(cudaGetLastError(), "kernel launch");
+      hp.done(nullptr, img, nullptr, 0);
+      on_image(c, img);
+      continue;
+    }
     xcb::SigSrc sn = s.sig, sd = s.sig;
     sn.wgt = wgt;
     sn.mode = weighted ? xcb::SIG_TIMES_W : xcb::SIG_PLAIN;
@@ -1259,7 +1419,8 @@ SmoothPart smooth_partials(xc_context ctx, xc_filter f, const xc_image_desc* d,
   hp.finish();
   guard_check(c, param);
   SmoothPart r;
-  r.bands_run = c.nb_run;
+  r.packed = packed;
+  r.bands_run = c.nb_run;  // bands each scatter transformed (packed: one full-band scatter)
   r.gpu_s = event_seconds(e0, e1);
   r.launches = c.lc.n;
   r.pad_h = c.g.Ph;
@@ -1283,9 +1444,13 @@ void smooth_single(xc_context ctx, xc_filter f, const xc_image_desc* d, const vo
   const bool host_out = d->memory == XC_HOST;
   const size_t npix = size_t(d->height) * d->width, os = dtype_size(d->out_dtype);
   float2* numden = ctx->buf<float2>("smooth_numden", 2 * npix * size_t(d->batch));
-  unsigned* red = ctx->buf<unsigned>("smooth_red", size_t(d->batch) + 1);
+  // red[0..batch]: per-image max|den| bits and the clamped count; then the
+  // per-image max|h| bits of the packed path
+  unsigned* red = ctx->buf<unsigned>("smooth_red", 2 * size_t(d->batch) + 1);
+  unsigned* amax = red + d->batch + 1;
   char* stage_out = host_out ? ctx->buf<char>("smooth_out", npix * os * size_t(d->batch)) : nullptr;
-  ck(cudaMemsetAsync(red, 0, (size_t(d->batch) + 1) * sizeof(unsigned), ctx->stream), "memset");
+  ck(cudaMemsetAsync(red, 0, (2 * size_t(d->batch) + 1) * sizeof(unsigned), ctx->stream),
+     "memset");
   std::vector<cudaEvent_t> done;
   xcb::LaunchCounter flc;
   Call* cp = nullptr;
@@ -1296,8 +1461,15 @@ void smooth_single(xc_context ctx, xc_filter f, const xc_image_desc* d, const vo
         char* dout = host_out ? stage_out + size_t(img) * npix * os
                               : static_cast<char*>(out) + size_t(img) * npix * os;
         stage(c, "smooth_finish", [&] {
-          smooth_divide(ctx, c.st, numden, npix, img, d->batch, d->out_dtype == XC_F64, dout, red,
-                        flc);
+          if (c.packed) {
+            xcb::launch_smooth_finish_packed(numden + 2 * size_t(img) * npix, npix, amax + img,
+                                             d->out_dtype == XC_F64, dout, red + img,
+                                             red + d->batch, c.st, flc);
+            ck(cudaGetLastError(), "kernel launch");
+          } else {
+            smooth_divide(ctx, c.st, numden, npix, img, d->batch, d->out_dtype == XC_F64, dout,
+                          red, flc);
+          }
         });
         if (host_out) {  // D2H of image img overlaps the next image's kernels
           cudaEvent_t e = ctx->event(false);
@@ -1307,7 +1479,8 @@ void smooth_single(xc_context ctx, xc_filter f, const xc_image_desc* d, const vo
                              cudaMemcpyDeviceToHost, ctx->cp_out),
              "D2H");
         }
-      });
+      },
+      amax);
   (void)cp;
   unsigned clamped = 0;
   ck(cudaMemcpyAsync(&clamped, red + d->batch, sizeof(unsigned), cudaMemcpyDeviceToHost,
@@ -1619,8 +1792,8 @@ int xc_build_optimal_filter(const double* pattern, int height, int width, int la
 }
 
 // detect_pattern (vote_filter.hpp:146-168): the vote filter is decomposed on
-// the host (once per call, as in the reference), the gradient runs on the
-// GPU, the scatter is xc_run's pipeline, and the NMS peaks are found on the
+// the device (once per distinct pattern; the reference does it per call), the
+// gradient runs on the GPU, the scatter is xc_run's pipeline, and the NMS peaks are found on the
 // host.  The context lock is taken by the inner xc_run only.
 int xc_detect_pattern(xc_context ctx, const xc_image_desc* d, const void* image,
                       const double* vote_weights, int radius, double eps, int K, int n_radii,
@@ -1641,7 +1814,7 @@ int xc_detect_pattern(xc_context ctx, const xc_image_desc* d, const void* image,
     ck(cudaSetDevice(ctx->device), "cudaSetDevice");
     const int h = d->height, w = d->width, R = radius, side = 2 * R + 1;
     const size_t npix = size_t(h) * w;
-    // host: decompose the vote filter (engine decomposition defaults of
+    // the vote filter's decomposition parameters (engine defaults of
     // vote_filter.hpp:157-160)
     if (n_radii == 0) n_radii = std::max(4, 2 * R);
     if (n_angles == 0) n_angles = std::max(16, 8 * ((R + 1) / 2) * 2);
@@ -1666,8 +1839,12 @@ int xc_detect_pattern(xc_context ctx, const xc_image_desc* d, const void* image,
       if (ctx->det_filters.size() >= 4) ctx->det_filters.clear();
       std::unique_ptr<xc_filter_s, void (*)(xc_filter_s*)> nf(new xc_filter_s(),
                                                               xc_filter_destroy);
-      nf->hf = xcb::decompose_rotation2(xcb::ImageView{vf.data(), side, side}, double(R),
-                                        double(R), K, n_radii, n_angles, double(R) + 0.5);
+      // per-call filter build on the device (freq_filter.hpp:63-89)
+      nf->hf = xcb::rotation2_shell(K, n_radii, n_angles, double(R) + 0.5);
+      {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        decompose_on_device(ctx, nf->hf, vf, side, side, double(R), double(R));
+      }
       it = ctx->det_filters.emplace(key, std::move(nf)).first;
     }
     xc_filter_s* f = it->second.get();

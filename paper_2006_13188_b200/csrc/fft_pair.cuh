@@ -171,6 +171,15 @@ struct IlvFft {
 
 // Transform lengths with a pair plan: X(L, R0, R1, R2, P).  4320 serves
 // configs 3 and 5, 2160 config 4, 1152 config 2.
-#define XCB_PAIR_TABLE(X) X(4320, 16, 18, 15, 16) X(2160, 12, 15, 12, 12) X(1152, 16, 9, 8, 16)
+// XCB_PLAN_1152_ALT (A/B builds, tools/ab_build.py AB_DEFS) selects another
+// 1152 plan
+#if defined(XCB_PLAN_1152_ALT) && XCB_PLAN_1152_ALT == 1
+#define XCB_PAIR_1152(X) X(1152, 8, 12, 12, 8)
+#elif defined(XCB_PLAN_1152_ALT) && XCB_PLAN_1152_ALT == 2
+#define XCB_PAIR_1152(X) X(1152, 8, 16, 9, 8)
+#else
+#define XCB_PAIR_1152(X) X(1152, 16, 9, 8, 16)
+#endif
+#define XCB_PAIR_TABLE(X) X(4320, 16, 18, 15, 16) X(2160, 12, 15, 12, 12) XCB_PAIR_1152(X)
 
 }  // namespace xcb

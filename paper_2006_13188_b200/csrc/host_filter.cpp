@@ -72,10 +72,8 @@ cplx ImageView::sample(double x, double y) const {
 
 // freq_filter.hpp:63-89: per-radius angular DFT of the polar resampling;
 // the |k| = n_angles/2 coefficient is halved (split over +-k).
-HostFilter decompose_rotation2(const ImageView& img, double cx, double cy, int K,
-                               int n_radii, int n_angles, double r_max) {
+HostFilter rotation2_shell(int K, int n_radii, int n_angles, double r_max) {
   check_polar_params(n_radii, n_angles, r_max);
-  const auto p = polar_samples(img, cx, cy, n_radii, n_angles, false, 0.0, r_max);
   HostFilter f;
   f.group = 0;
   f.K = K;
@@ -83,6 +81,13 @@ HostFilter decompose_rotation2(const ImageView& img, double cx, double cy, int K
   f.n_radii = n_radii;
   f.n_angles = n_angles;
   f.r_max = r_max;
+  return f;
+}
+
+HostFilter decompose_rotation2(const ImageView& img, double cx, double cy, int K,
+                               int n_radii, int n_angles, double r_max) {
+  HostFilter f = rotation2_shell(K, n_radii, n_angles, r_max);
+  const auto p = polar_samples(img, cx, cy, n_radii, n_angles, false, 0.0, r_max);
   const int nc = f.nc();
   f.comps.assign(size_t(n_radii) * nc, cplx(0));
   for (int ci = 0; ci < nc; ++ci) {
@@ -102,9 +107,8 @@ HostFilter decompose_rotation2(const ImageView& img, double cx, double cy, int K
 
 // freq_filter.hpp:91-129: per-angle log-radial DFT with basis phase
 // 2 pi k (j + 1/2) / n_radii.
-HostFilter decompose_scale2(const ImageView& img, double cx, double cy, int K,
-                            int n_radii, int n_angles, double r_min, double r_max,
-                            double r_domain) {
+HostFilter scale2_shell(int K, int n_radii, int n_angles, double r_min, double r_max,
+                        double r_domain) {
   if (!(r_min > 0.0))
     throw std::invalid_argument("r_min must be > 0 (log-polar excludes the origin)");
   if (r_domain != 0.0 && r_domain < r_max)
@@ -112,7 +116,6 @@ HostFilter decompose_scale2(const ImageView& img, double cx, double cy, int K,
   const double D = r_domain > 0 ? r_domain : r_max;
   check_polar_params(n_radii, n_angles, D);
   if (!(r_min < D)) throw std::invalid_argument("log-polar sampling needs 0 < r_min < r_max");
-  const auto p = polar_samples(img, cx, cy, n_radii, n_angles, true, r_min, D);
   HostFilter f;
   f.group = 1;
   f.K = K;
@@ -122,6 +125,15 @@ HostFilter decompose_scale2(const ImageView& img, double cx, double cy, int K,
   f.r_max = r_max;
   f.r_min = r_min;
   f.r_domain = D;
+  return f;
+}
+
+HostFilter decompose_scale2(const ImageView& img, double cx, double cy, int K,
+                            int n_radii, int n_angles, double r_min, double r_max,
+                            double r_domain) {
+  HostFilter f = scale2_shell(K, n_radii, n_angles, r_min, r_max, r_domain);
+  const double D = f.r_domain;
+  const auto p = polar_samples(img, cx, cy, n_radii, n_angles, true, r_min, D);
   const int nc = f.nc();
   f.comps.assign(size_t(n_angles) * nc, cplx(0));
   for (int ci = 0; ci < nc; ++ci) {

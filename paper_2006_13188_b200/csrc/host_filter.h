@@ -45,6 +45,11 @@ HostFilter decompose_rotation2(const ImageView& f, double cx, double cy, int K,
 HostFilter decompose_scale2(const ImageView& f, double cx, double cy, int K,
                             int n_radii, int n_angles, double r_min, double r_max,
                             double r_domain);
+// the validated metadata of a decomposition (ks, sampling, radii) without the
+// coefficients: the device decomposition (xc_decompose_*_device) fills comps
+HostFilter rotation2_shell(int K, int n_radii, int n_angles, double r_max);
+HostFilter scale2_shell(int K, int n_radii, int n_angles, double r_min, double r_max,
+                        double r_domain);
 cplx component_value(const HostFilter& f, int ci, double r, double theta);
 cplx inner_dc_value(const HostFilter& f);
 // (2R+1)^2-style rendering, row-major [y][x]; transpose=true renders f(y,x)

@@ -65,6 +65,67 @@ __global__ void k_smooth_max(const float2* __restrict__ den, size_t n, unsigned*
   }
 }
 
+// block max of m >= 0, one atomicMax on the float bits per block (non-negative
+// floats order as their bit patterns)
+__device__ __forceinline__ void block_max_atomic(float m, unsigned* bits) {
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ float red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) atomicMax(bits, __float_as_uint(m));
+  }
+}
+
+__global__ void k_absmax(const float* __restrict__ x, size_t n, int aligned, unsigned* bits) {
+  float m = 0.f;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  const size_t n4 = aligned ? n / 4 : 0;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n4;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const float4 v = x4[i];
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  }
+  // the tail (or, unaligned, everything) element-wise over the whole grid
+  for (size_t i = 4 * n4 + blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    m = fmaxf(m, fabsf(x[i]));
+  block_max_atomic(m, bits);
+}
+
+// packed smoothing (SIG_PACK): z = num + i alpha den with num, den real
+__global__ void k_smooth_max_packed(const float2* __restrict__ z, size_t n, unsigned* maxbits) {
+  float m = 0.f;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    m = fmaxf(m, fabsf(z[i].y));
+  block_max_atomic(m, maxbits);
+}
+
+// floor 1e-9 max|den| (alpha cancels: |z.y| < 1e-9 max|z.y|), out = alpha z.x / z.y
+template <class TO>
+__global__ void k_smooth_div_packed(const float2* __restrict__ z, size_t n,
+                                    const unsigned* amax, const unsigned* maxbits,
+                                    TO* __restrict__ out, unsigned* clamped) {
+  const double floor_ = 1e-9 * double(__uint_as_float(*maxbits));
+  const double alpha = double(pack_alpha(amax));
+  unsigned cnt = 0;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const double dy = z[i].y;
+    if (fabs(dy) < floor_) {
+      ++cnt;
+      out[i] = TO(0);
+      continue;
+    }
+    out[i] = TO(alpha * double(z[i].x) / dy);
+  }
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(clamped, cnt);
+}
+
 template <class TO>
 __global__ void k_smooth_div(const float2* __restrict__ num, const float2* __restrict__ den,
                              size_t n, const unsigned* maxbits, TO* __restrict__ out,
@@ -380,6 +441,28 @@ void launch_accumulate(void* dst, const void* src, size_t n, int f64, cudaStream
   ++lc.n;
 }
 
+void launch_absmax(const float* x, size_t n, unsigned* bits, cudaStream_t st, LaunchCounter& lc) {
+  // 4 CTAs per SM loop over the field: one atomic per CTA (float4 loads need
+  // 16-byte alignment: the staged fields are cudaMalloc'd)
+  const int al = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  k_absmax<<<std::min(grid_for(n / 4 + 1, 256), 4 * 148), 256, 0, st>>>(x, n, al, bits);
+  ++lc.n;
+}
+
+void launch_smooth_finish_packed(const float2* z, size_t n, const unsigned* amax, int out_f64,
+                                 void* out, unsigned* maxbits, unsigned* clamped, cudaStream_t st,
+                                 LaunchCounter& lc) {
+  const int g = grid_for(n, 256);
+  k_smooth_max_packed<<<std::min(g, 4 * 148), 256, 0, st>>>(z, n, maxbits);
+  if (out_f64)
+    k_smooth_div_packed<double><<<g, 256, 0, st>>>(z, n, amax, maxbits,
+                                                   static_cast<double*>(out), clamped);
+  else
+    k_smooth_div_packed<float><<<g, 256, 0, st>>>(z, n, amax, maxbits, static_cast<float*>(out),
+                                                  clamped);
+  lc.n += 2;
+}
+
 void launch_smooth_finish(const float2* num, const float2* den, size_t n, int out_f64,
                           void* out, unsigned* maxbits, unsigned* clamped, cudaStream_t st,
                           LaunchCounter& lc) {
@@ -686,4 +769,73 @@ void launch_render(const double2* comps, const int* ks, int nb, int group, int n
   ++lc.n;
 }
 
+}  // namespace xcb
+
+// ------------------------------------------------------------------ decomposition
+// decompose_rotation2 / decompose_scale2 on the device (freq_filter.hpp:63-129,
+// polar.hpp:46-83): the polar (log-polar) bilinear resampling of the filter
+// image, one thread per sample, then the DFT over the periodic axis, one thread
+// per (row, band).  fp64 throughout; the band phase 2 pi k (s + off) / L is
+// evaluated with sincospi of an exactly formed quotient.
+namespace xcb {
+namespace {
+__global__ void k_polar_samples(const double2* __restrict__ img, int w, int h, double cx,
+                                double cy, int nr, int na, int log_radial, double r_min,
+                                double r_max, double2* __restrict__ p) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nr * na) return;
+  const int j = i / na, m = i % na;
+  const double r = log_radial ? r_min * pow(r_max / r_min, (j + 0.5) / nr)
+                              : (j + 0.5) * r_max / nr;
+  const double two_pi = 6.283185307179586476925286766559;  // 2 * EIGEN_PI
+  const double th = two_pi * m / na;
+  double sn, cs;
+  sincos(th, &sn, &cs);
+  const double x = cx + r * cs, y = cy + r * sn;
+  // Field2::sample (field.hpp:51-62): bilinear, zero outside the grid
+  const double fx = floor(x), fy = floor(y);
+  const int x0 = int(fx), y0 = int(fy);
+  const double tx = x - fx, ty = y - fy;
+  auto tap = [&](int xi, int yi) {
+    return (xi < 0 || yi < 0 || xi >= w || yi >= h) ? make_double2(0.0, 0.0)
+                                                     : img[size_t(yi) * w + xi];
+  };
+  const double2 a = tap(x0, y0), b = tap(x0 + 1, y0), c = tap(x0, y0 + 1), d = tap(x0 + 1, y0 + 1);
+  p[i] = make_double2((1.0 - ty) * ((1.0 - tx) * a.x + tx * b.x) + ty * ((1.0 - tx) * c.x + tx * d.x),
+                      (1.0 - ty) * ((1.0 - tx) * a.y + tx * b.y) + ty * ((1.0 - tx) * c.y + tx * d.y));
+}
+
+// comps[row][ci] = half_k / L * sum_s P(row, s) e^{-2 pi i k (s + off) / L}:
+// rotation (group 0): rows = radii j, s = angle m, P = p[j][m], off = 0;
+// scale (group 1): rows = angles m, s = radius j, P = p[j][m], off = 1/2.
+__global__ void k_band_dft(const double2* __restrict__ p, int nr, int na, int group,
+                           const int* __restrict__ ks, int nc, double2* __restrict__ comps) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int rows = group == 0 ? nr : na, L = group == 0 ? na : nr;
+  if (i >= rows * nc) return;
+  const int row = i / nc, ci = i % nc, k = ks[ci];
+  double ar = 0.0, ai = 0.0;
+  for (int s = 0; s < L; ++s) {
+    const double2 v = group == 0 ? p[size_t(row) * na + s] : p[size_t(s) * na + row];
+    // e^{-2 pi i k (s + off) / L}: 2 k (s + off) is exact (an integer)
+    const long long num = group == 0 ? 2LL * k * s : (2LL * s + 1) * k;
+    double sn, cs;
+    sincospi(-double(num) / double(L), &sn, &cs);
+    ar += v.x * cs - v.y * sn;
+    ai += v.x * sn + v.y * cs;
+  }
+  const double half = (2 * abs(k) == L) ? 0.5 : 1.0;
+  comps[size_t(row) * nc + ci] = make_double2(ar * half / L, ai * half / L);
+}
+}  // namespace
+
+void launch_decompose(const double2* img, int w, int h, double cx, double cy, int nr, int na,
+                      int group, double r_min, double r_top, const int* ks, int nc,
+                      double2* samples, double2* comps, cudaStream_t st, LaunchCounter& lc) {
+  const int n = nr * na, rows = (group == 0 ? nr : na) * nc;
+  k_polar_samples<<<(n + 127) / 128, 128, 0, st>>>(img, w, h, cx, cy, nr, na, group == 1, r_min,
+                                                   r_top, samples);
+  k_band_dft<<<(rows + 127) / 128, 128, 0, st>>>(samples, nr, na, group, ks, nc, comps);
+  lc.n += 2;
+}
 }  // namespace xcb

@@ -583,6 +583,7 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
       // bands run in descending k, so the step is almost always -1 (one
       // multiply by conj(mul), a CTA-uniform branch); other steps loop
       const int dk = bi + 1 < b1 ? bl.k[bi + 1] - bl.k[bi] : 0;
+      const bool unit = dk == -1;  // CTA-uniform
       typename PF::P0Regs v;  // the pass-0 inputs, read straight from TMEM
 #pragma unroll
       for (int r0 = 0; r0 < R0; r0 += 4) {
@@ -591,21 +592,33 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
         tmem_wait_ld();
         tmem_depn<16>(reinterpret_cast<float*>(cm));
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          v.a[r0 + i] = make_float2(cm[i].x, cm[i].y);
-          const float2 m = make_float2(cm[i].z, cm[i].w);
-          float2 nx;
-          if (dk == -1) {
-            nx = c_mul(v.a[r0 + i], c_conj(m));
-          } else {
-            nx = v.a[r0 + i];
-            const float2 mm = dk < 0 ? c_conj(m) : m;
-            for (int q = 0; q < (dk < 0 ? -dk : dk); ++q) nx = c_mul(nx, mm);
+        for (int i = 0; i < 4; ++i) v.a[r0 + i] = make_float2(cm[i].x, cm[i].y);
+        if (unit) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 nx = c_mul(v.a[r0 + i], make_float2(cm[i].z, -cm[i].w));
+            cm[i].x = nx.x;
+            cm[i].y = nx.y;
           }
-          cm[i].x = nx.x;
-          cm[i].y = nx.y;
+          tmem_stn<16>(tc + 4 * r0, reinterpret_cast<const float*>(cm));
         }
-        if (bi + 1 < b1) tmem_stn<16>(tc + 4 * r0, reinterpret_cast<const float*>(cm));
+      }
+      if (!unit && dk != 0) {
+        // other band steps (band subsets): one rolled loop, kept out of the
+        // unrolled hot path (its code would otherwise sit in the band loop
+        // once per input and crowd the instruction cache)
+        const int n = dk < 0 ? -dk : dk;
+#pragma unroll 1
+        for (int r = 0; r < R0; ++r) {
+          float4 cm = tmem_ld4(tc + 4 * r);
+          tmem_wait_ld();
+          tmem_dep(cm);
+          float2 nx = make_float2(cm.x, cm.y);
+          const float2 mm = dk < 0 ? make_float2(cm.z, -cm.w) : make_float2(cm.z, cm.w);
+#pragma unroll 1
+          for (int q = 0; q < n; ++q) nx = c_mul(nx, mm);
+          tmem_st4(tc + 4 * r, make_float4(nx.x, nx.y, cm.z, cm.w));
+        }
       }
       tmem_wait_st();
       if ((opaque_i(t) >> 1) < PF::NB0) Dft<R0>::run(v.a);
@@ -966,8 +979,8 @@ PairTw pair_tables() {
 
 }  // namespace
 
-// S1 at 1152 (config 2): the pair kernel (0.109 ms) unless XCB_S1_PAIR=0
-// selects the fast one (0.124 ms)
+// S1 at 1152 (config 2): the pair kernel (8 * 16 * 9, S1Plan) unless
+// XCB_S1_PAIR=0 selects the fast one
 bool s1_pair_small() {
   static const bool on = [] {
     const char* e = std::getenv("XCB_S1_PAIR");
@@ -975,6 +988,20 @@ bool s1_pair_small() {
   }();
   return on;
 }
+
+// S1's own plan per length: S1's pass 0 reads its inputs from TMEM, so a
+// short first radix that keeps every thread busy in pass 0 pays off there.
+// 1152 = 8 * 16 * 9 (288 threads: 100% / 50% / 89% busy per pass) measured
+// S1 164.6 -> 144.6 us on config 2 at base clocks; the other stages keep
+// 16 * 9 * 8 (S2 130.9 against 139.7 us, S4 12.7 against 14.7 us).
+template <class PF>
+struct S1Plan {
+  using type = PF;
+};
+template <>
+struct S1Plan<IlvFft<1152, 16, 9, 8, 16>> {
+  using type = IlvFft<1152, 8, 16, 9, 8>;
+};
 
 // 0 if no pair plan for L (or the stage does not fit); else the dynamic smem.
 // stage 0 I1, 1 I2, 2 planes, 3 S1, 4 S2, 5 F1, 6 F2, 7 S4
@@ -986,7 +1013,10 @@ size_t pair_smem(int stage, int L, const Geo& g) {
     const size_t tw = size_t(PF::TWM) * sizeof(float2);                            \
     const size_t w = 2 * size_t(PF::LP) * sizeof(float4);                          \
     if (stage <= 2) s = size_t(LL) * sizeof(float4) + w + tw;                      \
-    if (stage == 3 && (LL >= 2048 || s1_pair_small())) s = w + tw;                  \
+    if (stage == 3 && (LL >= 2048 || s1_pair_small())) {                           \
+      using P1 = typename S1Plan<PF>::type;                                        \
+      s = 2 * size_t(P1::LP) * sizeof(float4) + size_t(P1::TWM) * sizeof(float2);  \
+    }                                                                              \
     if (stage == 4 && g.Hx2 <= LL) s = 3 * size_t(LL) * sizeof(float4) + w + tw;   \
     if (stage == 5 || stage == 7) s = w + tw;                                      \
     if (stage == 6 && g.Hx2 <= LL) s = size_t(LL) * sizeof(float4) + w + tw;      \
@@ -1172,7 +1202,7 @@ void launch_rows_fwd_premul_pair(const Geo& g, const SigSrc& s, const double* ba
   const size_t sm = pair_smem(3, g.Pw, g);
 #define XCB_BODY(LL, R0, R1, R2, PP)                                                         \
   case LL: {                                                                                \
-    using PF = IlvFft<LL, R0, R1, R2, PP>;                                                  \
+    using PF = typename S1Plan<IlvFft<LL, R0, R1, R2, PP>>::type;                           \
     const PairTw tw = pair_tables<PF>();                                                    \
     /* no tail split: config 4's 3.5 waves measured 0.306 ms split, 0.297 ms not */         \
     const int rows2 = g.Hx2 / 2;                                                            \

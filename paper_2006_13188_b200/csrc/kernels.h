@@ -26,13 +26,19 @@ struct Geo {
   int periodic;
 };
 
-enum SigMode { SIG_PLAIN = 0, SIG_TIMES_W = 1, SIG_W_ONLY = 2 };
+// SIG_PACK (smoothing): the real signal h and weight w (1 when wgt is null)
+// packed as one complex signal (h w, alpha w), alpha = the power of two nearest
+// max|h| (from *amax, float bits), so num and den of smooth_adaptive come out of
+// one scatter as its real and imaginary parts (alpha keeps both at the same
+// scale, so each carries the other's rounding at its own relative size)
+enum SigMode { SIG_PLAIN = 0, SIG_TIMES_W = 1, SIG_W_ONLY = 2, SIG_PACK = 3 };
 
 struct SigSrc {
   const void* sig;  // float [H][W] (real) or float2 (complex)
   int is_complex;
   const float* wgt; // per-pixel real weight (smooth: 1/s^2) or null
   int mode;         // SigMode
+  const unsigned* amax = nullptr;  // SIG_PACK: max|h| as float bits
 };
 
 struct Bands {
@@ -97,6 +103,13 @@ void launch_filter_spectra(const FftPlan& prow, const FftPlan& pcol, const Geo& 
                            cudaStream_t st, LaunchCounter& lc);
 
 // smooth: max |den| (as float bits) then divide with the 1e-9 floor.
+// max|x| of a real fp32 field as float bits (atomicMax; *bits zeroed by the caller)
+void launch_absmax(const float* x, size_t n, unsigned* bits, cudaStream_t st, LaunchCounter& lc);
+// smooth_adaptive's divide from one packed scatter z = num + i alpha den
+// (SIG_PACK): floor 1e-9 max|den|, out = num / den
+void launch_smooth_finish_packed(const float2* z, size_t n, const unsigned* amax, int out_f64,
+                                 void* out, unsigned* maxbits, unsigned* clamped, cudaStream_t st,
+                                 LaunchCounter& lc);
 void launch_smooth_finish(const float2* num, const float2* den, size_t n, int out_f64,
                           void* out, unsigned* maxbits, unsigned* clamped,
                           cudaStream_t st, LaunchCounter& lc);
@@ -224,4 +237,14 @@ namespace xcb {
 // partial sums of the multi-device band reduce without NCCL (peer copies).
 void launch_accumulate(void* dst, const void* src, size_t n, int f64, cudaStream_t st,
                        LaunchCounter& lc);
+}  // namespace xcb
+
+namespace xcb {
+// decompose_rotation2 (group 0) / decompose_scale2 (group 1) on the device
+// (freq_filter.hpp:63-129): img row-major [h][w] complex fp64; samples scratch
+// [nr][na]; comps [n_rows][nc] complex fp64.  r_top = r_max (rotation) or the
+// basis domain top (scale).
+void launch_decompose(const double2* img, int w, int h, double cx, double cy, int nr, int na,
+                      int group, double r_min, double r_top, const int* ks, int nc,
+                      double2* samples, double2* comps, cudaStream_t st, LaunchCounter& lc);
 }  // namespace xcb

@@ -35,8 +35,18 @@ __device__ __forceinline__ int src_index(int yp, int ext, int n, int R, int peri
   return y < 0 ? y + n : y;
 }
 
+// alpha of SIG_PACK: the power of two nearest max|h| (1 for an all-zero h)
+__device__ __forceinline__ float pack_alpha(const unsigned* amax) {
+  const float m = __uint_as_float(*amax);
+  return m > 0.f ? exp2f(rintf(log2f(m))) : 1.f;
+}
+
 __device__ __forceinline__ float2 sig_value(const SigSrc& s, size_t i) {
   if (s.mode == SIG_W_ONLY) return make_float2(s.wgt ? s.wgt[i] : 1.f, 0.f);
+  if (s.mode == SIG_PACK) {
+    const float w = s.wgt ? s.wgt[i] : 1.f;
+    return make_float2(static_cast<const float*>(s.sig)[i] * w, pack_alpha(s.amax) * w);
+  }
   float2 v = s.is_complex ? static_cast<const float2*>(s.sig)[i]
                           : make_float2(static_cast<const float*>(s.sig)[i], 0.f);
   if (s.mode == SIG_TIMES_W) v = c_scale(v, s.wgt[i]);

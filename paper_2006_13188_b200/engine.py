@@ -150,34 +150,54 @@ def _filter_image(filt) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(filt, dtype=np.complex128))
 
 
-def decompose_rotation2(filt, cx, cy, K, n_radii, n_angles, r_max) -> FreqFilter2:
-    """freq_filter.hpp:63-89 (host, once per filter)."""
+def _decompose_ctx(device):
+    """device=False/None: the host decomposition; True: this thread's default
+    context; an int: that device's context; a Context: itself."""
+    if device is None or device is False:
+        return None
+    if device is True:
+        return N.context(0)
+    return device if isinstance(device, N.Context) else N.context(int(device))
+
+
+def decompose_rotation2(filt, cx, cy, K, n_radii, n_angles, r_max, device=None) -> FreqFilter2:
+    """freq_filter.hpp:63-89.  Host by default (once per filter); device=True
+    (or a device id / Context) runs the polar resampling and the band DFT on
+    the GPU (xc_decompose_rotation2_device), for per-call filter builds."""
     f = _filter_image(filt)
     nc = 2 * (int(K) // 2) + 1
     ks = np.zeros(nc, np.int32)
     comps = np.zeros((max(int(n_radii), 1), nc), np.complex128, order="F")
     got = C.c_int(0)
-    N.check(N.lib().xc_decompose_rotation2(
-        f.ctypes.data_as(C.POINTER(C.c_double)), f.shape[0], f.shape[1], N.XC_ROW_MAJOR,
-        float(cx), float(cy), int(K), int(n_radii), int(n_angles), float(r_max),
-        ks.ctypes.data_as(C.POINTER(C.c_int)), comps.ctypes.data_as(C.POINTER(C.c_double)),
-        C.byref(got)))
+    args = (f.ctypes.data_as(C.POINTER(C.c_double)), f.shape[0], f.shape[1], N.XC_ROW_MAJOR,
+            float(cx), float(cy), int(K), int(n_radii), int(n_angles), float(r_max),
+            ks.ctypes.data_as(C.POINTER(C.c_int)), comps.ctypes.data_as(C.POINTER(C.c_double)),
+            C.byref(got))
+    ctx = _decompose_ctx(device)
+    if ctx is None:
+        N.check(N.lib().xc_decompose_rotation2(*args))
+    else:
+        N.check(N.lib().xc_decompose_rotation2_device(ctx.handle, *args), ctx.handle)
     return FreqFilter2(XformKind.rotation2, K, ks, comps, n_radii, n_angles, r_max)
 
 
 def decompose_scale2(filt, cx, cy, K, n_radii, n_angles, r_min, r_max,
-                     r_domain=0.0) -> FreqFilter2:
-    """freq_filter.hpp:91-129 (host, once per filter)."""
+                     r_domain=0.0, device=None) -> FreqFilter2:
+    """freq_filter.hpp:91-129 (host by default; device= as decompose_rotation2)."""
     f = _filter_image(filt)
     nc = 2 * (int(K) // 2) + 1
     ks = np.zeros(nc, np.int32)
     comps = np.zeros((max(int(n_angles), 1), nc), np.complex128, order="F")
     got = C.c_int(0)
-    N.check(N.lib().xc_decompose_scale2(
-        f.ctypes.data_as(C.POINTER(C.c_double)), f.shape[0], f.shape[1], N.XC_ROW_MAJOR,
-        float(cx), float(cy), int(K), int(n_radii), int(n_angles), float(r_min), float(r_max),
-        float(r_domain), ks.ctypes.data_as(C.POINTER(C.c_int)),
-        comps.ctypes.data_as(C.POINTER(C.c_double)), C.byref(got)))
+    args = (f.ctypes.data_as(C.POINTER(C.c_double)), f.shape[0], f.shape[1], N.XC_ROW_MAJOR,
+            float(cx), float(cy), int(K), int(n_radii), int(n_angles), float(r_min), float(r_max),
+            float(r_domain), ks.ctypes.data_as(C.POINTER(C.c_int)),
+            comps.ctypes.data_as(C.POINTER(C.c_double)), C.byref(got))
+    ctx = _decompose_ctx(device)
+    if ctx is None:
+        N.check(N.lib().xc_decompose_scale2(*args))
+    else:
+        N.check(N.lib().xc_decompose_scale2_device(ctx.handle, *args), ctx.handle)
     D = r_domain if r_domain > 0 else r_max
     return FreqFilter2(XformKind.scale2, K, ks, comps, n_radii, n_angles, r_max, r_min, D)
 

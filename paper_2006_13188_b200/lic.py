@@ -49,7 +49,8 @@ def lic(field: XformField, length: float, width: float, seed: int, normalized: b
     kern = anisotropic_gaussian(length, width)
     R = (kern.shape[1] - 1) // 2
     n_angles = max(64, 4 * int(K))
-    F = decompose_rotation2(kern, float(R), float(R), int(K), max(8, R), n_angles, R + 0.5)
+    F = decompose_rotation2(kern, float(R), float(R), int(K), max(8, R), n_angles, R + 0.5,
+                            device=True)  # a per-call filter build, on the GPU
     if normalized:
         return np.asarray(smooth_adaptive(noise, field, F).output, np.float64)
     return np.asarray(xconv_fast(noise, field, F).output.real, np.float64)

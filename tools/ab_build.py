@@ -2,7 +2,7 @@
 REV = "wt") into paper_2006_13188_b200/lib/ab/NAME.so, for A/B kernel timing
 with XCB_LIB_OVERRIDE (tools/ab_kernels.py).
 
-  python tools/ab_build.py REV NAME
+  AB_DEFS="-DNAME=VALUE ..." python tools/ab_build.py REV NAME
 """
 import concurrent.futures as cf
 import os
@@ -28,7 +28,7 @@ else:
     subprocess.run(["tar", "-x", "-C", tree], input=arc, check=True)
 csrc = os.path.join(tree, "paper_2006_13188_b200", "csrc")
 flags = [f if f != os.path.join(ROOT, "include") else os.path.join(tree, "include")
-         for f in B.FLAGS]
+         for f in B.FLAGS] + os.environ.get("AB_DEFS", "").split()  # e.g. -DXCB_PLAN_1152=...
 srcs = [s for s in os.listdir(csrc) if s.endswith((".cu", ".cpp"))]
 
 
