@@ -21,6 +21,8 @@
  *   xc_decompose_rotation2/scale2  <- decompose_rotation2 / decompose_scale2
  *                                     freq_filter.hpp:63-129 (host, once per
  *                                     filter)
+ *   xc_fft2                        <- fft2 fft.hpp:20-53 (the pipelines' own
+ *                                     row / column transforms)
  *   xc_decompose_*_device          <- the same on the GPU (per-call builds:
  *                                     detect_pattern, contour matching)
  *   xc_render_component / xc_reconstruct / xc_inner_dc_value
@@ -168,6 +170,14 @@ int xc_profile_enable(xc_context ctx, int on);
 int xc_profile_reset(xc_context ctx);
 int xc_profile_get(xc_context ctx, int idx, char* name, int name_len, double* total_ms,
                    long long* launches);
+
+/* fft2 (fft.hpp:20-53) on the device with the pipeline's own transforms: the
+ * 2D DFT of a rows x cols complex grid (XC_C64 / XC_C128, row-major, host or
+ * device memory), forward unscaled, inverse scaled 1/(rows cols).  One extent
+ * must be even (the engine pairs rows / columns); lengths must be 2,3,5-smooth
+ * and <= 32768, as for the pipelines' pads. */
+int xc_fft2(xc_context ctx, int rows, int cols, int dtype, int memory, int inverse,
+            const void* in, void* out);
 
 /* Out-of-bounds debug mode (no compute-sanitizer on the GPU pool).  With the
  * environment variable XCB_GUARD=<bytes> set before the first allocation, every

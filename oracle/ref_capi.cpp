@@ -118,6 +118,15 @@ int ref_filter2_fft(const double* sig, int h, int w, const double* filt, int fh,
   });
 }
 
+// fft.hpp:20-53 (Eigen FFT through the shim: kissfft order, inverse 1/n)
+int ref_fft2(const double* a, int h, int w, int inverse, double* out) {
+  return guarded([&] {
+    auto A = field_c(a, h, w).values;
+    fft2(A, inverse != 0);
+    put_c(A, out);
+  });
+}
+
 // freq_filter.hpp:63-89
 int ref_decompose_rotation2(const double* filt, int h, int w, double cx, double cy, int K,
                             int n_radii, int n_angles, double r_max, int* ks_out,

@@ -105,6 +105,15 @@ def next_fast_size(n: int) -> int:
     return lib().ref_next_fast_size(int(n))
 
 
+def fft2(a, inverse=False):
+    """fft.hpp:20-53 (the reference's own fft2)."""
+    x = _c128(a)
+    out = np.zeros(x.shape, np.complex128)
+    _check(lib().ref_fft2(_dp(x.view(np.float64)), x.shape[0], x.shape[1], int(bool(inverse)),
+                          _dp(out.view(np.float64))))
+    return out
+
+
 def filter2_fft(sig, filt, fcx, fcy, correlate, periodic=False):
     s, f = _c128(sig), _c128(filt)
     out = np.zeros(s.shape, np.complex128)

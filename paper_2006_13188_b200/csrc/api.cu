@@ -993,6 +993,57 @@ int xc_context_trim(xc_context ctx) {
   });
 }
 
+// fft2 (fft.hpp:20-53): the 2D DFT of a rows x cols complex grid on the
+// device with the pipeline's own transforms (F1 row FFT -> layout B', F2
+// column FFT -> layout B), forward unscaled, inverse scaled 1/n as Eigen's
+// FFT.  The engine pairs the staged rows' columns, so an odd width runs as
+// the transposed problem; both extents odd is rejected.
+int xc_fft2(xc_context ctx, int rows, int cols, int dtype, int memory, int inverse,
+            const void* in, void* out) {
+  return guarded(ctx, [&] {
+    if (!ctx || !in || !out) throw std::invalid_argument("null argument");
+    if (rows < 1 || cols < 1) throw std::invalid_argument("image dims must be positive");
+    if (dtype != XC_C64 && dtype != XC_C128)
+      throw std::invalid_argument("xc_fft2 takes complex data (XC_C64 / XC_C128)");
+    const bool tr = cols % 2 != 0;
+    if (tr && rows % 2 != 0) throw std::invalid_argument("xc_fft2 needs one even extent");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    Call c{};
+    c.ctx = ctx;
+    c.st = ctx->stream;
+    const int R0 = tr ? cols : rows, C0 = tr ? rows : cols;  // staged grid
+    xcb::Geo& g = c.g;
+    g.H = g.Hx = R0;
+    g.W = g.Wx = C0;
+    g.Hx2 = g.H2 = (R0 + 1) & ~1;
+    g.off = g.R = g.periodic = 0;
+    g.Ph = R0;
+    g.Pw = C0;
+    c.prow = &ctx->plan(g.Pw);
+    c.pcol = &ctx->plan(g.Ph);
+    const size_t n = size_t(rows) * cols, es = dtype == XC_C128 ? 16 : 8;
+    const void* src = in;
+    if (memory == XC_HOST) {
+      void* b = ctx->buf<char>("fft2_in", n * es);
+      ck(cudaMemcpyAsync(b, in, n * es, cudaMemcpyHostToDevice, c.st), "H2D");
+      src = b;
+    }
+    float2* x = ctx->buf<float2>("fft2_x", n);
+    xcb::launch_fft2_in(src, dtype == XC_C128, rows, cols, tr, inverse != 0, x, c.st, c.lc);
+    float2* T1 = ctx->buf<float2>("fft2_T1", size_t(g.Hx2) * g.Pw);
+    float2* Hh = ctx->buf<float2>("fft2_H", size_t(g.Ph) * g.Pw);
+    run_f1(c, xcb::SigSrc{x, 1, nullptr, xcb::SIG_PLAIN}, T1);
+    run_f2(c, T1, Hh);
+    void* dst = memory == XC_HOST ? ctx->buf<char>("fft2_out", n * es) : out;
+    xcb::launch_fft2_out(Hh, rows, cols, tr, inverse != 0, dtype == XC_C128, dst, c.st, c.lc);
+    ck(cudaGetLastError(), "fft2 launch");
+    if (memory == XC_HOST)
+      ck(cudaMemcpyAsync(out, dst, n * es, cudaMemcpyDeviceToHost, c.st), "D2H");
+    ck(cudaStreamSynchronize(c.st), "fft2");
+  });
+}
+
 int xc_debug_check_guards(xc_context ctx, int* n_bad, char* first_bad, int len) {
   return guarded(ctx, [&] {
     if (!ctx || !n_bad) throw std::invalid_argument("null argument");

@@ -111,6 +111,7 @@ __global__ void k_smooth_div_packed(const float2* __restrict__ z, size_t n,
                                     TO* __restrict__ out, unsigned* clamped) {
   const double floor_ = 1e-9 * double(__uint_as_float(*maxbits));
   const double alpha = double(pack_alpha(amax));
+  const bool zero = *amax == 0u;  // h == 0: num is exactly 0 (the packed z.x is rounding)
   unsigned cnt = 0;
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
        i += size_t(gridDim.x) * blockDim.x) {
@@ -120,7 +121,7 @@ __global__ void k_smooth_div_packed(const float2* __restrict__ z, size_t n,
       out[i] = TO(0);
       continue;
     }
-    out[i] = TO(alpha * double(z[i].x) / dy);
+    out[i] = zero ? TO(0) : TO(alpha * double(z[i].x) / dy);
   }
   for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(clamped, cnt);
@@ -453,7 +454,7 @@ void launch_smooth_finish_packed(const float2* z, size_t n, const unsigned* amax
                                  void* out, unsigned* maxbits, unsigned* clamped, cudaStream_t st,
                                  LaunchCounter& lc) {
   const int g = grid_for(n, 256);
-  k_smooth_max_packed<<<std::min(g, 4 * 148), 256, 0, st>>>(z, n, maxbits);
+  k_smooth_max_packed<<<g, 256, 0, st>>>(z, n, maxbits);
   if (out_f64)
     k_smooth_div_packed<double><<<g, 256, 0, st>>>(z, n, amax, maxbits,
                                                    static_cast<double*>(out), clamped);
@@ -837,5 +838,64 @@ void launch_decompose(const double2* img, int w, int h, double cx, double cy, in
                                                    r_top, samples);
   k_band_dft<<<(rows + 127) / 128, 128, 0, st>>>(samples, nr, na, group, ks, nc, comps);
   lc.n += 2;
+}
+}  // namespace xcb
+
+// ------------------------------------------------------------------ fft2 (fft.hpp:20-53)
+// input staging (c64 / c128 -> c64, conjugated for the inverse) and the
+// spectrum's layout B [u/2][v][u%2] -> row-major [v][u] (conjugated and scaled
+// 1/(Ph Pw) for the inverse, as Eigen's inverse FFT: conj(FFT(conj x)) / n)
+namespace xcb {
+namespace {
+// tr: the transform runs on the transposed grid (the caller's rows x cols is
+// stored row-major; the staged grid is cols x rows)
+__global__ void k_fft2_in(const void* __restrict__ src, int c128, int rows, int cols, int tr,
+                          int conj_in, float2* __restrict__ dst) {
+  const size_t n = size_t(rows) * cols;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const size_t j = tr ? (i % rows) * cols + i / rows : i;
+    float2 v = c128 ? make_float2(float(static_cast<const double2*>(src)[j].x),
+                                  float(static_cast<const double2*>(src)[j].y))
+                    : static_cast<const float2*>(src)[j];
+    if (conj_in) v.y = -v.y;
+    dst[i] = v;
+  }
+}
+
+__global__ void k_fft2_out(const float2* __restrict__ hh, int rows, int cols, int tr,
+                           int inverse, double scale, int c128, void* __restrict__ out) {
+  const size_t n = size_t(rows) * cols;
+  const int ph = tr ? cols : rows;  // column-transform length of the staged grid
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const int r = int(i / cols), c = int(i % cols);
+    const int u = tr ? r : c, v = tr ? c : r;  // staged (row-transform, column-transform) index
+    float2 x = hh[(size_t(u >> 1) * ph + v) * 2 + (u & 1)];
+    double re = x.x, im = x.y;
+    if (inverse) {
+      re *= scale;
+      im *= -scale;
+    }
+    if (c128)
+      static_cast<double2*>(out)[i] = make_double2(re, im);
+    else
+      static_cast<float2*>(out)[i] = make_float2(float(re), float(im));
+  }
+}
+}  // namespace
+
+void launch_fft2_in(const void* src, int c128, int rows, int cols, int tr, int conj_in,
+                    float2* dst, cudaStream_t st, LaunchCounter& lc) {
+  k_fft2_in<<<grid_for(size_t(rows) * cols, 256), 256, 0, st>>>(src, c128, rows, cols, tr,
+                                                                conj_in, dst);
+  ++lc.n;
+}
+
+void launch_fft2_out(const float2* hh, int rows, int cols, int tr, int inverse, int c128,
+                     void* out, cudaStream_t st, LaunchCounter& lc) {
+  k_fft2_out<<<grid_for(size_t(rows) * cols, 256), 256, 0, st>>>(
+      hh, rows, cols, tr, inverse, 1.0 / (double(rows) * cols), c128, out);
+  ++lc.n;
 }
 }  // namespace xcb

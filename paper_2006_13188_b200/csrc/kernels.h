@@ -248,3 +248,15 @@ void launch_decompose(const double2* img, int w, int h, double cx, double cy, in
                       int group, double r_min, double r_top, const int* ks, int nc,
                       double2* samples, double2* comps, cudaStream_t st, LaunchCounter& lc);
 }  // namespace xcb
+
+namespace xcb {
+// fft2 (fft.hpp:20-53) on the device: input staging to c64 (conjugated for the
+// inverse) and the F2 spectrum (layout B) to row-major c64 / c128 (conjugated
+// and scaled 1/(Ph Pw) for the inverse)
+// (tr: the caller's rows x cols grid is transformed as its transpose, so that
+// the staged row length, which the engine pairs, is even)
+void launch_fft2_in(const void* src, int c128, int rows, int cols, int tr, int conj_in,
+                    float2* dst, cudaStream_t st, LaunchCounter& lc);
+void launch_fft2_out(const float2* hh, int rows, int cols, int tr, int inverse, int c128,
+                     void* out, cudaStream_t st, LaunchCounter& lc);
+}  // namespace xcb

@@ -19,6 +19,8 @@ product's own GPU path.
 """
 from __future__ import annotations
 
+import ctypes as C
+
 import numpy as np
 
 from .engine import (FreqFilter2, Response2, SmoothResult, XConvPlan, XformField, XformKind,
@@ -42,9 +44,32 @@ def batch_range(batch: int, rank: int, world: int) -> range:
 
 
 def gpu_compute(mode, H, T, F, components, inner_dc):
-    """Default per-rank compute: the product's sm_100a path."""
-    return _fast(XMode(mode), H, T, F, XConvPlan(components=list(components)),
-                 inner_dc=inner_dc).output
+    """Default per-rank compute: the product's sm_100a path, device-resident.
+    The signal and the transformation field are uploaded to the rank's current
+    CUDA device, xc_run writes the partial sum into a complex64 device tensor
+    (XC_DEVICE), and that tensor goes straight into the reduce: no host round
+    trip for the partials."""
+    import torch
+    from . import _native as N
+    from .engine import _desc, _param, _signal
+    dev = torch.device("cuda", torch.cuda.current_device())
+    sig = _signal(H)  # f32 / f64 / c64 / c128 as given (the library converts)
+    par = _param(T, sig.shape)  # the steering base keeps the caller's precision
+    ds = torch.from_numpy(sig).to(dev)
+    dp = torch.from_numpy(par).to(dev)
+    out = torch.empty(sig.shape, dtype=torch.complex64, device=dev)
+    ctx = N.context(dev.index)
+    d = _desc(sig, par, N.XC_C64, T.kind, memory=N.XC_DEVICE)
+    comp = np.ascontiguousarray(np.asarray(list(components), np.int32))
+    st = N.Stats()
+    flags = 0 if inner_dc else N.XC_FLAG_NO_INNER_DC
+    torch.cuda.current_stream(dev).synchronize()  # the uploads, before the library's stream
+    N.check(N.lib().xc_run(ctx.handle, F.handle(ctx), int(mode), C.byref(d), ds.data_ptr(),
+                           dp.data_ptr(),
+                           comp.ctypes.data_as(C.POINTER(C.c_int)) if len(comp) else None,
+                           len(comp), flags, out.data_ptr(), C.byref(st)), ctx.handle)
+    ctx.synchronize()  # the partial is complete before the collective's stream reads it
+    return out
 
 
 def _dist():
@@ -52,15 +77,35 @@ def _dist():
     return dist
 
 
-def _reduce_complex(a: np.ndarray, root: int, group=None, device=None) -> np.ndarray:
+def _reduce_complex(a, root: int, group=None, device=None):
+    """Sum complex partials onto `root` in their own precision.  A CUDA tensor
+    (gpu_compute) is reduced where it lies (NCCL over NVLink; gloo, which has
+    no CUDA reduce, stages it through host memory); a numpy partial (injected
+    CPU compute) is reduced as a CPU tensor, or on `device` if given.  Returns
+    the numpy sum on the root, None elsewhere."""
     import torch
     dist = _dist()
-    t = torch.from_numpy(np.ascontiguousarray(a.astype(np.complex128)))
-    t = torch.view_as_real(t).contiguous()
+    rank = dist.get_rank(group)
+    t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+    if not t.is_complex():
+        t = t.to(torch.complex128 if t.dtype == torch.float64 else torch.complex64)
     if device is not None:
         t = t.to(device)
-    dist.reduce(t, dst=root, op=dist.ReduceOp.SUM, group=group)
-    return torch.view_as_complex(t.cpu().contiguous()).numpy()
+    if t.is_cuda and dist.get_backend(group) == "gloo":
+        t = t.cpu()
+    r = torch.view_as_real(t.contiguous())
+    dist.reduce(r, dst=root, op=dist.ReduceOp.SUM, group=group)
+    if rank != root:
+        return None
+    return torch.view_as_complex(r).cpu().numpy()
+
+
+def _stack(parts):
+    import torch
+    if all(isinstance(p, torch.Tensor) for p in parts):
+        return torch.stack(parts)
+    return np.stack([p.cpu().numpy() if isinstance(p, torch.Tensor) else np.asarray(p)
+                     for p in parts])
 
 
 def xfast_band_sharded(mode: XMode, H, T: XformField, F: FreqFilter2,
@@ -76,7 +121,7 @@ def xfast_band_sharded(mode: XMode, H, T: XformField, F: FreqFilter2,
     mine = shard_components(ks, rank, world)
     inner_dc = rank == root  # add the scale inner-DC term exactly once
     part = compute(int(mode), H, T, F, mine, inner_dc)
-    total = _reduce_complex(np.asarray(part), root, group, device)
+    total = _reduce_complex(part, root, group, device)
     if rank != root:
         return None
     out = XConvPlan(mode, T.kind, list(plan.components), plan.periodic)
@@ -110,9 +155,9 @@ def smooth_band_sharded(H, T: XformField, F: FreqFilter2, normalize_signal: bool
         raise ValueError("band sharding needs at least one band per rank")
     mine = shard_components(ks, rank, world)
     inner_dc = rank == root
-    num = np.asarray(compute(int(XMode.convolution), Hs, T, F, mine, inner_dc))
-    den = np.asarray(compute(int(XMode.convolution), ones, T, F, mine, inner_dc))
-    both = _reduce_complex(np.stack([num, den]), root, group, device)
+    num = compute(int(XMode.convolution), Hs, T, F, mine, inner_dc)
+    den = compute(int(XMode.convolution), ones, T, F, mine, inner_dc)
+    both = _reduce_complex(_stack([num, den]), root, group, device)
     if rank != root:
         return None
     num, den = both

@@ -202,6 +202,23 @@ def decompose_scale2(filt, cx, cy, K, n_radii, n_angles, r_min, r_max,
     return FreqFilter2(XformKind.scale2, K, ks, comps, n_radii, n_angles, r_max, r_min, D)
 
 
+def fft2(a, inverse: bool = False, device=0) -> np.ndarray:
+    """fft.hpp:20-53 on the GPU with the pipeline's own transforms
+    (xc_fft2): forward unscaled, inverse scaled 1/n; complex64 in gives
+    complex64 out, anything else complex128 (computed in fp32)."""
+    x = np.asarray(a)
+    x = np.ascontiguousarray(x if x.dtype in (np.complex64, np.complex128)
+                             else x.astype(np.complex128))
+    if x.ndim != 2:
+        raise ValueError("fft2 takes a 2D grid")
+    out = np.zeros_like(x)
+    ctx = _context(device)
+    N.check(N.lib().xc_fft2(ctx.handle, x.shape[0], x.shape[1],
+                            N.XC_C64 if x.dtype == np.complex64 else N.XC_C128, N.XC_HOST,
+                            int(bool(inverse)), x.ctypes.data, out.ctypes.data), ctx.handle)
+    return out
+
+
 def render_component(F: FreqFilter2, ci, width, height, cx, cy) -> np.ndarray:
     """freq_filter.hpp:172-184."""
     out = np.zeros((height, width), np.complex128)

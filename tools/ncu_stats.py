@@ -64,6 +64,9 @@ def main():
     res = json.load(open(out_path)) if os.path.exists(out_path) else {}
     for arg in sys.argv[2:]:
         cfg, rep = arg.split(":", 1)
+        if not os.path.exists(rep):
+            print(f"skip {rep}: missing", file=sys.stderr)
+            continue
         acc = collections.defaultdict(lambda: collections.defaultdict(float))
         cnt = collections.Counter()
         for d in rows_of(rep):

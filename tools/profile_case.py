@@ -14,7 +14,8 @@ mode = sys.argv[1] if len(sys.argv) > 1 else "xcorr"
 cfg = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 nb = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 w = WL.config5(batch=nb) if cfg == 5 else WL.CONFIGS[cfg]()
-sig, par = (w.signal[0], w.param[0]) if nb == 1 else (w.signal[:nb], w.param[:nb])
+sig = w.signal[0] if nb == 1 else w.signal[:nb]
+par = None if w.param is None else (w.param[0] if nb == 1 else w.param[:nb])
 if mode == "anglemax":
     for _ in range(2):
         X.anglemax(sig, w.filt, 360)
