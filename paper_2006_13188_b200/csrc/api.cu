@@ -678,6 +678,16 @@ void run_f2(Call& c, const float2* T1, float2* Hh) {
     xcb::launch_cols_fwd(*c.pcol, c.g, T1, Hh, c.st, c.lc);
 }
 
+// XCB_ANGLE_TC=0: the Hermitian angle max on the CUDA cores (k_anglemax_herm)
+// instead of the tensor cores (k_anglemax_tc.cu)
+bool use_angle_tc() {
+  static const bool on = [] {
+    const char* e = std::getenv("XCB_ANGLE_TC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // XCB_HERM=0 disables the Hermitian half-band paths (A/B timing, tests)
 bool use_herm() {
   static const bool on = [] {
@@ -1648,7 +1658,11 @@ int xc_anglemax(xc_context ctx, xc_filter f, const xc_image_desc* d, const void*
         darg = d->memory == XC_DEVICE ? argmax + size_t(img) * npix
                                       : ctx->buf<int>("arg_stage", npix);
       stage(c, "anglemax", [&] {
-        if (herm)
+        if (herm && use_angle_tc() &&
+            xcb::anglemax_tc_ok(*std::max_element(hk.begin(), hk.end())))
+          xcb::launch_anglemax_tc(planes, hk.data(), bands.n, npix, d->out_dtype == XC_F64, dsc,
+                                  darg, c.st, c.lc);
+        else if (herm)
           xcb::launch_anglemax_herm(planes, hk.data(), bands.n, npix, d->out_dtype == XC_F64, dsc,
                                     darg, c.st, c.lc);
         else

@@ -125,6 +125,12 @@ void launch_anglemax_herm(const float2* planes, const int* ks_host, int nb, size
                           int score_f64, void* score, int* argmax, cudaStream_t st,
                           LaunchCounter& lc);
 int anglemax_herm_kh(int kh);  // 1 if KH has a half-band kernel (4, 8, 16)
+// the same half-band angle max (360 angles, KH <= 16) as two tf32 GEMMs per
+// 128-pixel tile on the tensor cores, 3xTF32 (k_anglemax_tc.cu)
+bool anglemax_tc_ok(int kh);
+void launch_anglemax_tc(const float2* planes, const int* ks_host, int nb, size_t npix,
+                        int score_f64, void* score, int* argmax, cudaStream_t st,
+                        LaunchCounter& lc);
 
 // Upload the plan's twiddles; returns device pointer (owned by caller).
 float2* upload_twiddles(const FftPlan& p);
