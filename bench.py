@@ -41,6 +41,14 @@ METRIC = "extended correlation Mpixel·bands/s at 1/2/4/8 B200; % of HBM rooflin
 UNIT = "Mpixel·bands/s"
 
 
+def peaks_all() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -486,6 +494,22 @@ def run_b200(args):
                 "peak": peak, "unit": "warp inst/s", "frac": ach / peak,
                 "sm_mhz": sm_mhz, "source": ks.get("source")}
 
+    def tensor_roof(name, per_launch_s):
+        """The angle max runs on the tensor cores (k_anglemax_tc.cu, config 3):
+        12 tf32 MMAs of 128 x 192 x 8 per 128-pixel tile (3xTF32 split), against
+        the dense tf32 peak = half the measured bf16 peak."""
+        if name != "anglemax" or os.environ.get("XCB_ANGLE_TC") == "0":
+            return None
+        ntiles = -(-H * W // 128) * max(1, round(Bl * args.steps / prof[name][1]))
+        flops = ntiles * 12 * 2 * 128 * 192 * 8
+        pk = peaks_all().get("bf16_tflops")
+        if not pk:
+            return None
+        ach = flops / per_launch_s / 1e12
+        return {"kernel": "k_anglemax_tc", "executed_tflop_per_launch": flops / 1e12,
+                "achieved": ach, "peak": pk / 2, "unit": "TFLOP/s (tf32)", "frac": ach / (pk / 2),
+                "note": "3xTF32: a third of the executed flops are the fp32-equivalent sums"}
+
     if dom:
         alg, per_launch_s, ni, achieved = kernel_roof(dom)
         ks = kstats.get(f"cfg{args.config}:{dom}")
@@ -498,6 +522,7 @@ def run_b200(args):
                                 "separate profiled pass of the same steps (short steps)",
                 "cuda_graph": graphed,
                 "issue": issue_roof(dom, per_launch_s),
+                "tensor": tensor_roof(dom, per_launch_s),
                 "kernels": {k: {"ms_per_launch": kernel_roof(k)[1] * 1e3,
                                 "images_per_launch": kernel_roof(k)[2],
                                 "achieved_gbs": kernel_roof(k)[3],
@@ -507,6 +532,11 @@ def run_b200(args):
                 "stages_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
                 "pipeline_model_frac": model_bytes(mode, nb, H * W, Ph * Pw) * Bl /
                 (ms_step * 1e-3) / 1e9 / hbm}
+        if roof["tensor"]:  # the dominant kernel is the tensor-core angle max
+            tr = roof["tensor"]
+            roof["hbm_view"] = {k: roof[k] for k in ("achieved", "peak", "unit", "frac")}
+            roof.update({"bound": "tensor", "achieved": tr["achieved"], "peak": tr["peak"],
+                         "unit": "TFLOP/s", "frac": tr["frac"]})
 
     cpu = None
     if world == 1 and not args.no_cpu:
