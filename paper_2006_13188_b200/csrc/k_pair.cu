@@ -504,15 +504,24 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
 // ------------------------------------------------------------------ S1 (interleaved)
 // TMEM per thread, for each pass-0 input r: [cur.re, cur.im, mul.re, mul.im]
 // with cur = H e^{-i k phi} of the current band and mul = e^{-i phi}.
+// TWR (short rows, S1Occ): the pass-2 twiddles stay in registers in split
+// form instead of TMEM, so the TMEM allocation admits 3 CTAs per SM
 template <class PF>
-__global__ void __launch_bounds__(PF::T, PF::MINB)
+struct S1Occ {
+  static constexpr bool kTwReg = PF::L < 2048;
+  static constexpr int kMinB = kTwReg ? 3 : PF::MINB;
+};
+
+template <class PF>
+__global__ void __launch_bounds__(PF::T, S1Occ<PF>::kMinB)
     k_rows_fwd_premul_ilv(Geo g, SigSrc s, const double* __restrict__ base, Bands bl,
                           float2* __restrict__ T1, const float2* __restrict__ twm,
                           const float2* __restrict__ twl, int full, int split) {
   constexpr int R0 = PF::R0, R2 = PF::R2;
-  // TMEM columns per thread: [cur, mul] per pass-0 input, then the pass-2
-  // twiddle row (out of the registers: no spills at 2 CTAs per SM)
-  constexpr int kThr = 4 * R0 + PF::kTwColsPad;
+  constexpr bool TWR = S1Occ<PF>::kTwReg;
+  // TMEM columns per thread: [cur, mul] per pass-0 input, then (unless TWR)
+  // the pass-2 twiddle row (out of the registers: no spills at 2 CTAs per SM)
+  constexpr int kThr = 4 * R0 + (TWR ? 0 : PF::kTwColsPad);
   static_assert(kThr * PF::WPQ <= 512, "TMEM budget");
   extern __shared__ __align__(16) float4 smp[];
   float4* W04 = smp;
@@ -540,7 +549,11 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
   const int gi = t & 1, j = t >> 1;
   const uint32_t tc = tmem_warp_cols(tbase, kThr);
   const uint32_t ttw = tc + 4 * R0;
-  park_last_tw<PF>(twl, ttw);
+  typename PF::LastTw tl;
+  if constexpr (TWR)
+    PF::load_last_tw(twl, tl);
+  else
+    park_last_tw<PF>(twl, ttw);
   {
     const int ys = src_index(2 * b + gi, g.Hx, g.H, g.R, g.periodic);
     const int k0 = bl.k[b0];
@@ -640,11 +653,15 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
         p += ostep;
       }
     };
-    float2 w[PF::kTwColsPad / 2 + 1];
-    tmem_ldn<PF::kTwColsPad>(ttw, reinterpret_cast<float*>(w + 1));
-    tmem_wait_ld();
-    tmem_depn<PF::kTwColsPad>(reinterpret_cast<float*>(w + 1));
-    PF::pass2_all_w(W1, w, store);
+    if constexpr (TWR) {
+      PF::pass2_all(W1, tl, store);
+    } else {
+      float2 w[PF::kTwColsPad / 2 + 1];
+      tmem_ldn<PF::kTwColsPad>(ttw, reinterpret_cast<float*>(w + 1));
+      tmem_wait_ld();
+      tmem_depn<PF::kTwColsPad>(reinterpret_cast<float*>(w + 1));
+      PF::pass2_all_w(W1, w, store);
+    }
   }
   tmem_fence_before_sync();
   __syncthreads();
