@@ -22,6 +22,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+
+#include <nvtx3/nvToolsExt.h>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -457,6 +459,12 @@ Call setup(xc_context ctx, xc_filter f, const xc_image_desc* d, int group_requir
 // Wrap one stage's launches in profiling events (no-op unless enabled).
 template <class Fn>
 void stage(Call& c, const char* name, Fn&& fn) {
+  // NVTX range per stage (the reference's StageTimer, engine.hpp:41-49): free
+  // without a tool attached, named ranges under ncu --nvtx / nsys
+  struct Range {
+    explicit Range(const char* n) { nvtxRangePushA(n); }
+    ~Range() { nvtxRangePop(); }
+  } range(name);
   if (!c.ctx->profiling) {
     fn();
     return;
