@@ -96,6 +96,21 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
 
+    def sample_now(self):
+        """One synchronous sample (a timed region shorter than the 100 ms
+        sampling period leaves none)."""
+        try:
+            out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                  "--format=csv,noheader,nounits"], capture_output=True,
+                                 text=True, timeout=30).stdout
+            for line in out.splitlines():
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) == 6:
+                    self.rows.append(parts)
+                    self.after_region = True
+        except (OSError, subprocess.SubprocessError):
+            pass
+
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
@@ -104,9 +119,12 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4)
                           if r[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        out = {"sm_mhz": statistics.median(sm) if sm else None,
+               "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+               "samples": len(self.rows)}
+        if getattr(self, "after_region", False):
+            out["note"] = "timed region shorter than the sampling period: sampled right after it"
+        return out
 
 
 def stage_bytes(stage: str, B: int, H: int, W: int, Ph: int, Pw: int, ni: int = 1) -> float:
@@ -402,6 +420,8 @@ def run_b200(args):
         drain()
         e1.record(stream)
         barrier()
+    if not clk.rows:
+        clk.sample_now()
     if not in_region:
         ctx.profile(enable=True, reset=True)
         for _ in range(args.steps):
