@@ -719,8 +719,12 @@ void launch_i2(Call& c, const xcb::SigSrc& sig, const float2* T2, const xcb::Ban
     });
   } else if (c.frow && xcb::fast_smem(1, *c.frow, g)) {
     stage(c, "I2_rows_inv_steer", [&] {
+      const int nch = xcb::fast_steer_chunks(g, c.bands.n);
+      float2* parts = nch > 1 ? c.ctx->buf<float2>("steer_parts", size_t(nch) * g.H * g.W)
+                              : nullptr;
       xcb::launch_rows_inv_steer_fast(*c.frow, g, T2, c.bands, base, out_kind, out,
-                                      accumulate ? 1 : 0, sig, dcv.real(), dcv.imag(), c.st, c.lc);
+                                      accumulate ? 1 : 0, sig, dcv.real(), dcv.imag(), parts,
+                                      c.st, c.lc);
     });
   } else {
     stage(c, "I2_rows_inv_steer", [&] {

@@ -11,6 +11,8 @@
 // (z = e^{i phi(p)}; engine.hpp:312-317 / 353-358 for the reference steering).
 #include <algorithm>
 
+#include <cstdlib>
+
 #include "stages_common.cuh"
 #include "tma.cuh"
 
@@ -41,6 +43,10 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
     k_cols_inv_corr_fast(FftPlanD p, Geo g, const float2* __restrict__ Hh,
                          const float2* __restrict__ Fh, size_t sstride, Bands bl,
                          float2* __restrict__ T2) {
+  // band chunk blockIdx.y of gridDim.y (small images: the bands of a column
+  // pair are spread over several CTAs so the grid fills the GPU)
+  const int b0 = int(blockIdx.y) * bl.n / int(gridDim.y);
+  const int b1 = int(blockIdx.y + 1) * bl.n / int(gridDim.y);
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) uint64_t bar;
   constexpr int L = FF::L;  // = Ph
@@ -58,11 +64,11 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
     fence_mbar_init();
     mbar_expect_tx(&bar, 2 * bytes);
     bulk_copy(Hc, Hh + colb, bytes, &bar);
-    bulk_copy(S, Fh + size_t(bl.spec[0]) * sstride + colb, bytes, &bar);
+    bulk_copy(S, Fh + size_t(bl.spec[b0]) * sstride + colb, bytes, &bar);
   }
   __syncthreads();
   unsigned phase = 0;
-  for (int bi = 0; bi < bl.n; ++bi) {
+  for (int bi = b0; bi < b1; ++bi) {
     mbar_wait(&bar, phase);
     phase ^= 1;
     // conj(H^ conj(F^)) = conj(H^) F^ : inverse via conj-FFT-conj
@@ -72,7 +78,7 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
     };
     FF::first(p, W, load);
     __syncthreads();
-    if (tid == 0 && bi + 1 < bl.n) {
+    if (tid == 0 && bi + 1 < b1) {
       fence_proxy_async();
       mbar_expect_tx(&bar, bytes);
       bulk_copy(S, Fh + size_t(bl.spec[bi + 1]) * sstride + colb, bytes, &bar);
@@ -94,7 +100,13 @@ template <class FF, class TO>
 __global__ void __launch_bounds__(kFastMaxThreads, 1)
     k_rows_inv_steer_fast(FftPlanD p, Geo g, const float2* __restrict__ T2, Bands bl,
                           const double* __restrict__ base, TO* __restrict__ out,
-                          int accumulate, SigSrc dcs, double dcr, double dci, float scale) {
+                          int accumulate, SigSrc dcs, double dcr, double dci, float scale,
+                          float2* __restrict__ parts) {
+  // band chunk blockIdx.y of gridDim.y: with several chunks each CTA writes
+  // its chunk's steered partial sum to parts[chunk] and k_reduce_chunks adds
+  // them in chunk order (small images: fills the GPU)
+  const int b0 = int(blockIdx.y) * bl.n / int(gridDim.y);
+  const int b1 = int(blockIdx.y + 1) * bl.n / int(gridDim.y);
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) uint64_t bar;
   constexpr int L = FF::L;  // = Pw
@@ -112,7 +124,7 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
     mbar_init(&bar, 1);
     fence_mbar_init();
     mbar_expect_tx(&bar, bytes);
-    bulk_copy(S, T2 + rowb, bytes, &bar);
+    bulk_copy(S, T2 + size_t(b0) * plane + rowb, bytes, &bar);
   }
   // z = e^{i phi} of the CTA's two output rows
   for (int i = tid; i < 2 * g.W; i += blockDim.x) {
@@ -125,19 +137,19 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
 #pragma unroll
   for (int r = 0; r < RL; ++r) acc[r] = make_float2(0.f, 0.f);
   unsigned phase = 0;
-  for (int bi = 0; bi < bl.n; ++bi) {
+  for (int bi = b0; bi < b1; ++bi) {
     mbar_wait(&bar, phase);
     phase ^= 1;
     auto load = [&](int n, int gi) -> float2 { return c_conj(S[n * 2 + gi]); };
     FF::first(p, W, load);
     __syncthreads();
-    if (tid == 0 && bi + 1 < bl.n) {
+    if (tid == 0 && bi + 1 < b1) {
       fence_proxy_async();
       mbar_expect_tx(&bar, bytes);
       bulk_copy(S, T2 + size_t(bi + 1) * plane + rowb, bytes, &bar);
     }
     FF::mid(TW, W);
-    const int dk = bi == 0 ? 0 : bl.k[bi - 1] - bl.k[bi];
+    const int dk = bi == b0 ? 0 : bl.k[bi - 1] - bl.k[bi];
     const int zso = opaque(zs), off = opaque(g.off);
     auto store = [&](int k, int gi, int r, float2 v) {
       const float2 val = c_scale(c_conj(v), scale);
@@ -152,15 +164,32 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
   const int nb = L / RL, w = tid;
   if (w < nb * kG) {
     const int gi = w & 1, j = w >> 1, y = 2 * b + gi;
-    const int klast = bl.k[bl.n - 1];
+    const int klast = bl.k[b1 - 1];
+    const size_t npix = size_t(g.H) * g.W;
 #pragma unroll
     for (int r = 0; r < RL; ++r) {
       const int x = j + r * nb - g.off;
       if (x < 0 || x >= g.W || y >= g.H) continue;
       const size_t i = size_t(y) * g.W + x;
       const float2 v = c_mul(acc[r], steer(klast, base[i], 1.f));
-      OutOps<TO>::put(out, i, v, accumulate != 0, dc_term(dcs, i, dcr, dci));
+      if (gridDim.y > 1)
+        parts[size_t(blockIdx.y) * npix + i] = v;
+      else
+        OutOps<TO>::put(out, i, v, accumulate != 0, dc_term(dcs, i, dcr, dci));
     }
+  }
+}
+
+// the chunks' partial sums in chunk order, then the output rule of I2
+template <class TO>
+__global__ void k_reduce_chunks(const float2* __restrict__ parts, int nch, size_t npix,
+                                TO* __restrict__ out, int accumulate, SigSrc dcs, double dcr,
+                                double dci) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < npix;
+       i += size_t(gridDim.x) * blockDim.x) {
+    float2 v = parts[i];
+    for (int c = 1; c < nch; ++c) v = c_add(v, parts[size_t(c) * npix + i]);
+    OutOps<TO>::put(out, i, v, accumulate != 0, dc_term(dcs, i, dcr, dci));
   }
 }
 
@@ -379,13 +408,32 @@ size_t fast_smem(int stage, const FftPlan& pl, const Geo& g) {
     break;                            \
   }
 
+// band chunks for a grid of `units` CTAs: small images (fewer units than
+// 2 per SM) spread each unit's bands over up to 4 * SMs / units CTAs
+int fast_band_chunks(int units, int nb) {
+  static const int sms = [] {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+  }();
+  static const bool off = [] {
+    const char* e = std::getenv("XCB_BAND_CHUNKS");
+    return e && e[0] == '0';
+  }();
+  if (off || units >= 2 * sms || nb < 2) return 1;
+  const int c = (4 * sms + units - 1) / units;
+  return c < nb ? c : nb;
+}
+
 void launch_cols_inv_corr_fast(const FftPlan& pc, const Geo& g, const float2* Hhat,
                                const float2* Fhat, size_t sstride, const Bands& b, float2* T2,
                                cudaStream_t st, LaunchCounter& lc) {
   const size_t sm = fast_smem(0, pc, g);
+  const dim3 grid(g.Pw / 2, fast_band_chunks(g.Pw / 2, b.n));
 #define XCB_FAST_BODY                                                                      \
   set_smem(k_cols_inv_corr_fast<FF>, sm);                                                  \
-  k_cols_inv_corr_fast<FF><<<g.Pw / 2, pc.d.nt, sm, st>>>(pc.d, g, Hhat, Fhat, sstride, b, T2)
+  k_cols_inv_corr_fast<FF><<<grid, pc.d.nt, sm, st>>>(pc.d, g, Hhat, Fhat, sstride, b, T2)
   switch (pc.d.L) { XCB_FAST_TABLE(XCB_FAST_CASE) }
 #undef XCB_FAST_BODY
   ++lc.n;
@@ -394,26 +442,37 @@ void launch_cols_inv_corr_fast(const FftPlan& pc, const Geo& g, const float2* Hh
 void launch_rows_inv_steer_fast(const FftPlan& pr, const Geo& g, const float2* T2,
                                 const Bands& b, const double* base, int out_kind, void* out,
                                 int accumulate, const SigSrc& dcs, double dcr, double dci,
-                                cudaStream_t st, LaunchCounter& lc) {
+                                float2* parts, cudaStream_t st, LaunchCounter& lc) {
   const size_t sm = fast_smem(1, pr, g);
   const float scale = float(1.0 / (double(g.Ph) * double(g.Pw)));
+  const int nch = parts ? fast_band_chunks(g.H2 / 2, b.n) : 1;
+  const dim3 grid(g.H2 / 2, nch);
+  const size_t npix = size_t(g.H) * g.W;
   if (out_kind == OUT_C64) {
 #define XCB_FAST_BODY                                                                      \
   set_smem(k_rows_inv_steer_fast<FF, float2>, sm);                                         \
-  k_rows_inv_steer_fast<FF, float2><<<g.H2 / 2, pr.d.nt, sm, st>>>(                        \
-      pr.d, g, T2, b, base, static_cast<float2*>(out), accumulate, dcs, dcr, dci, scale)
+  k_rows_inv_steer_fast<FF, float2><<<grid, pr.d.nt, sm, st>>>(                            \
+      pr.d, g, T2, b, base, static_cast<float2*>(out), accumulate, dcs, dcr, dci, scale, parts)
     switch (pr.d.L) { XCB_FAST_TABLE(XCB_FAST_CASE) }
 #undef XCB_FAST_BODY
+    if (nch > 1)
+      k_reduce_chunks<float2><<<grid_for(npix, 256), 256, 0, st>>>(
+          parts, nch, npix, static_cast<float2*>(out), accumulate, dcs, dcr, dci);
   } else {
 #define XCB_FAST_BODY                                                                      \
   set_smem(k_rows_inv_steer_fast<FF, double2>, sm);                                        \
-  k_rows_inv_steer_fast<FF, double2><<<g.H2 / 2, pr.d.nt, sm, st>>>(                       \
-      pr.d, g, T2, b, base, static_cast<double2*>(out), accumulate, dcs, dcr, dci, scale)
+  k_rows_inv_steer_fast<FF, double2><<<grid, pr.d.nt, sm, st>>>(                           \
+      pr.d, g, T2, b, base, static_cast<double2*>(out), accumulate, dcs, dcr, dci, scale, parts)
     switch (pr.d.L) { XCB_FAST_TABLE(XCB_FAST_CASE) }
 #undef XCB_FAST_BODY
+    if (nch > 1)
+      k_reduce_chunks<double2><<<grid_for(npix, 256), 256, 0, st>>>(
+          parts, nch, npix, static_cast<double2*>(out), accumulate, dcs, dcr, dci);
   }
-  ++lc.n;
+  lc.n += nch > 1 ? 2 : 1;
 }
+
+int fast_steer_chunks(const Geo& g, int nb) { return fast_band_chunks(g.H2 / 2, nb); }
 
 void launch_rows_inv_planes_fast(const FftPlan& pr, const Geo& g, const float2* T2,
                                  int nbands, float2* planes, cudaStream_t st,

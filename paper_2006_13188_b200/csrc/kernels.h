@@ -146,10 +146,13 @@ size_t fast_smem(int stage, const FftPlan& pl, const Geo& g);
 void launch_cols_inv_corr_fast(const FftPlan& pc, const Geo& g, const float2* Hhat,
                                const float2* Fhat, size_t sstride, const Bands& b, float2* T2,
                                cudaStream_t st, LaunchCounter& lc);
+// parts: scratch for band-chunked partial sums (fast_steer_chunks(g, nb) x
+// H x W float2), or null for one CTA per row pair over all bands
 void launch_rows_inv_steer_fast(const FftPlan& pr, const Geo& g, const float2* T2,
                                 const Bands& b, const double* base, int out_kind, void* out,
                                 int accumulate, const SigSrc& dcs, double dcr, double dci,
-                                cudaStream_t st, LaunchCounter& lc);
+                                float2* parts, cudaStream_t st, LaunchCounter& lc);
+int fast_steer_chunks(const Geo& g, int nb);
 void launch_rows_inv_planes_fast(const FftPlan& pr, const Geo& g, const float2* T2,
                                  int nbands, float2* planes, cudaStream_t st,
                                  LaunchCounter& lc);
