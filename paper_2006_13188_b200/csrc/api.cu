@@ -676,12 +676,16 @@ bool use_pair() {
 void run_f1(Call& c, const xcb::SigSrc& sig, float2* T1) {
   if (use_pair() && xcb::pair_smem(5, c.g.Pw, c.g))
     xcb::launch_rows_fwd_pair(c.g, sig, T1, c.st, c.lc);
+  else if (c.frow && xcb::fast_smem(5, *c.frow, c.g))
+    xcb::launch_rows_fwd_fast(*c.frow, c.g, sig, T1, c.st, c.lc);
   else
     xcb::launch_rows_fwd(*c.prow, c.g, sig, T1, c.st, c.lc);
 }
 void run_f2(Call& c, const float2* T1, float2* Hh) {
   if (use_pair() && xcb::pair_smem(6, c.g.Ph, c.g))
     xcb::launch_cols_fwd_pair(c.g, T1, Hh, c.st, c.lc);
+  else if (c.fcol && xcb::fast_smem(5, *c.fcol, c.g))
+    xcb::launch_cols_fwd_fast(*c.fcol, c.g, T1, Hh, c.st, c.lc);
   else
     xcb::launch_cols_fwd(*c.pcol, c.g, T1, Hh, c.st, c.lc);
 }

@@ -193,6 +193,57 @@ __global__ void k_reduce_chunks(const float2* __restrict__ parts, int nch, size_
   }
 }
 
+// ------------------------------------------------------------- F1 / F2 fast
+// The single forward transforms of the gather front end (F1 rows of the
+// signal -> T1, F2 columns of T1 -> H^) with the compile-time plans: the
+// generic kernels' runtime radix dispatch is instruction-cache bound at
+// small sizes (config 1: ncu no_instruction 25 cycles per issue).
+template <class FF>
+__global__ void __launch_bounds__(kFastMaxThreads, 1)
+    k_rows_fwd_fast(FftPlanD p, Geo g, SigSrc s, float2* __restrict__ T1) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  float2* W = reinterpret_cast<float2*>(smraw);
+  float2* TW = W + 2 * FF::Lp;
+  FF::load_twiddles(TW, p.tw);
+  __syncthreads();
+  const int b = blockIdx.x;
+  auto load = [&](int n, int gi) -> float2 {
+    const int ys = src_index(2 * b + gi, g.Hx, g.H, g.R, g.periodic);
+    const int xs = src_index(n, g.Wx, g.W, g.R, g.periodic);
+    if (ys < 0 || xs < 0) return make_float2(0.f, 0.f);
+    return sig_value(s, size_t(ys) * g.W + xs);
+  };
+  FF::first(p, W, load);
+  __syncthreads();
+  FF::mid(TW, W);
+  const int hx2 = opaque(g.Hx2);
+  auto store = [&](int k, int gi, int, float2 v) {
+    T1[(size_t(k >> 1) * hx2 + 2 * b + gi) * 2 + (k & 1)] = v;
+  };
+  FF::last(TW, W, store);
+}
+
+template <class FF>
+__global__ void __launch_bounds__(kFastMaxThreads, 1)
+    k_cols_fwd_fast(FftPlanD p, Geo g, const float2* __restrict__ T1, float2* __restrict__ spec) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  float2* W = reinterpret_cast<float2*>(smraw);
+  float2* TW = W + 2 * FF::Lp;
+  FF::load_twiddles(TW, p.tw);
+  __syncthreads();
+  const int c = blockIdx.x;
+  const float2* src = T1 + size_t(c) * g.Hx2 * 2;
+  float2* dst = spec + size_t(c) * FF::L * 2;
+  auto load = [&](int n, int gi) -> float2 {
+    return n < g.Hx2 ? src[n * 2 + gi] : make_float2(0.f, 0.f);
+  };
+  FF::first(p, W, load);
+  __syncthreads();
+  FF::mid(TW, W);
+  auto store = [&](int k, int gi, int, float2 v) { dst[k * 2 + gi] = v; };
+  FF::last(TW, W, store);
+}
+
 // ------------------------------------------------------------- planes fast
 // Angle-max front end: per band, row IFFT of T2_b, crop, store the band plane
 // G_b (k_anglemax_* then reads all bands per pixel).
@@ -397,6 +448,7 @@ size_t fast_smem(int stage, const FftPlan& pl, const Geo& g) {
     case 2: s = Wb + 4 * (g.Wx + 16) * f2; break;                         // S1
     case 3: s = 2 * (g.Hx2 > int(L) ? g.Hx2 : L) * f2 + 2 * L * f2 + Wb; break;  // S2
     case 4: s = 2 * L * f2 + Wb; break;                                   // planes
+    case 5: s = Wb; break;                                                // F1 / F2
   }
   return s <= kSmemLimit ? s : 0;
 }
@@ -473,6 +525,28 @@ void launch_rows_inv_steer_fast(const FftPlan& pr, const Geo& g, const float2* T
 }
 
 int fast_steer_chunks(const Geo& g, int nb) { return fast_band_chunks(g.H2 / 2, nb); }
+
+void launch_rows_fwd_fast(const FftPlan& pr, const Geo& g, const SigSrc& s, float2* T1,
+                          cudaStream_t st, LaunchCounter& lc) {
+  const size_t sm = fast_smem(5, pr, g);
+#define XCB_FAST_BODY                                                                      \
+  set_smem(k_rows_fwd_fast<FF>, sm);                                                       \
+  k_rows_fwd_fast<FF><<<g.Hx2 / 2, pr.d.nt, sm, st>>>(pr.d, g, s, T1)
+  switch (pr.d.L) { XCB_FAST_TABLE(XCB_FAST_CASE) }
+#undef XCB_FAST_BODY
+  ++lc.n;
+}
+
+void launch_cols_fwd_fast(const FftPlan& pc, const Geo& g, const float2* T1, float2* spec,
+                          cudaStream_t st, LaunchCounter& lc) {
+  const size_t sm = fast_smem(5, pc, g);
+#define XCB_FAST_BODY                                                                      \
+  set_smem(k_cols_fwd_fast<FF>, sm);                                                       \
+  k_cols_fwd_fast<FF><<<g.Pw / 2, pc.d.nt, sm, st>>>(pc.d, g, T1, spec)
+  switch (pc.d.L) { XCB_FAST_TABLE(XCB_FAST_CASE) }
+#undef XCB_FAST_BODY
+  ++lc.n;
+}
 
 void launch_rows_inv_planes_fast(const FftPlan& pr, const Geo& g, const float2* T2,
                                  int nbands, float2* planes, cudaStream_t st,

@@ -153,6 +153,11 @@ void launch_rows_inv_steer_fast(const FftPlan& pr, const Geo& g, const float2* T
                                 int accumulate, const SigSrc& dcs, double dcr, double dci,
                                 float2* parts, cudaStream_t st, LaunchCounter& lc);
 int fast_steer_chunks(const Geo& g, int nb);
+// F1 / F2 with the compile-time plans (stage 5 of fast_smem)
+void launch_rows_fwd_fast(const FftPlan& pr, const Geo& g, const SigSrc& s, float2* T1,
+                          cudaStream_t st, LaunchCounter& lc);
+void launch_cols_fwd_fast(const FftPlan& pc, const Geo& g, const float2* T1, float2* spec,
+                          cudaStream_t st, LaunchCounter& lc);
 void launch_rows_inv_planes_fast(const FftPlan& pr, const Geo& g, const float2* T2,
                                  int nbands, float2* planes, cudaStream_t st,
                                  LaunchCounter& lc);
