@@ -19,9 +19,9 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "lib", "libxconv_b200.so")
 SOURCES = ["host_filter.cpp", "fft_plan.cpp", "k_forward.cu", "k_inverse.cu", "k_misc.cu",
-           "k_fast.cu", "k_pair.cu", "k_3d.cu", "host_sph.cpp", "api.cu", "k_anglemax_tc.cu"]
+           "k_fast.cu", "k_pair.cu", "k_pair_sc.cu", "k_3d.cu", "host_sph.cpp", "api.cu", "k_anglemax_tc.cu"]
 HEADERS = ["host_filter.h", "fft_plan.h", "fft_core.cuh", "kernels.h", "stages_common.cuh",
-           "tma.cuh", "fft_pair.cuh", "tmem.cuh", "kernels3d.h", "host_sph.h"]
+           "tma.cuh", "fft_pair.cuh", "tmem.cuh", "pair_host.cuh", "pair_i1.cuh", "kernels3d.h", "host_sph.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
                 "-Xcompiler", "-fPIC,-O2", "-I", os.path.join(ROOT, "include")]

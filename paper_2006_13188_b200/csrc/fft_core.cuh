@@ -13,17 +13,74 @@
 namespace xcb {
 
 // ------------------------------------------------------------ complex helpers
-__device__ __forceinline__ float2 c_add(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 c_sub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ float2 c_mul(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+// sm_100 issues two fp32 lanes per instruction (FADD2 / FMUL2 / FFMA2,
+// PTX add / mul / fma .rn.f32x2 on a 64-bit register pair).  A complex value
+// is such a pair, so a complex add is one instruction and a complex multiply
+// two; ptxas folds the lane swaps, lane broadcasts and single-lane negations
+// that complex arithmetic needs into the operand modifiers (.LO_HI, .F32
+// broadcast, partial negate), so they cost nothing.  The band kernels are
+// instruction-issue bound (DESIGN 6a), so halving their FP32 instructions is
+// the lever.  XCB_F32X2=0 builds the scalar forms (A/B).
+#ifndef XCB_F32X2
+#define XCB_F32X2 1
+#endif
+#if XCB_F32X2
+__device__ __forceinline__ unsigned long long f2_u(float2 a) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+  return r;
 }
-// a * conj(b)
+__device__ __forceinline__ float2 u_f2(unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+// lane-wise a + b, a - b, a * b, a * b + c (round to nearest, no ftz)
+__device__ __forceinline__ float2 v_add(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_u(a)), "l"(f2_u(b)));
+  return u_f2(r);
+}
+__device__ __forceinline__ float2 v_sub(float2 a, float2 b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_u(a)), "l"(f2_u(b)));
+  return u_f2(r);
+}
+__device__ __forceinline__ float2 v_mul(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_u(a)), "l"(f2_u(b)));
+  return u_f2(r);
+}
+__device__ __forceinline__ float2 v_fma(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_u(a)), "l"(f2_u(b)), "l"(f2_u(c)));
+  return u_f2(r);
+}
+#else
+__device__ __forceinline__ float2 v_add(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 v_sub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 v_mul(float2 a, float2 b) { return make_float2(a.x * b.x, a.y * b.y); }
+__device__ __forceinline__ float2 v_fma(float2 a, float2 b, float2 c) {
+  return make_float2(fmaf(a.x, b.x, c.x), fmaf(a.y, b.y, c.y));
+}
+#endif
+__device__ __forceinline__ float2 v_bc(float s) { return make_float2(s, s); }  // broadcast
+__device__ __forceinline__ float2 c_add(float2 a, float2 b) { return v_add(a, b); }
+__device__ __forceinline__ float2 c_sub(float2 a, float2 b) { return v_sub(a, b); }
+// a b = a b.re + (-a.im, a.re) b.im
+__device__ __forceinline__ float2 c_mul(float2 a, float2 b) {
+  return v_fma(make_float2(-a.y, a.x), v_bc(b.y), v_mul(a, v_bc(b.x)));
+}
+// a * conj(b) = a b.re + (a.im, -a.re) b.im
 __device__ __forceinline__ float2 c_mulc(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+  return v_fma(make_float2(a.y, -a.x), v_bc(b.y), v_mul(a, v_bc(b.x)));
+}
+// acc + a b
+__device__ __forceinline__ float2 c_fma(float2 a, float2 b, float2 acc) {
+  return v_fma(make_float2(-a.y, a.x), v_bc(b.y), v_fma(a, v_bc(b.x), acc));
 }
 __device__ __forceinline__ float2 c_conj(float2 a) { return make_float2(a.x, -a.y); }
-__device__ __forceinline__ float2 c_scale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+__device__ __forceinline__ float2 c_scale(float2 a, float s) { return v_mul(a, v_bc(s)); }
 __device__ __forceinline__ float2 c_mi(float2 a) { return make_float2(a.y, -a.x); }  // -i * a
 
 // ------------------------------------------------------ constexpr twiddles
@@ -88,10 +145,10 @@ __device__ __forceinline__ float2 tw_apply(float2 x, int e, const CTw<R>& tw) {
   if ((8 * e) % R == 0) {
     constexpr float h = 0.70710678118654752440f;
     const int q = (8 * e) / R;  // odd: e^{-i pi q / 4}
-    return q == 1 ? make_float2(h * (x.x + x.y), h * (x.y - x.x))
-         : q == 3 ? make_float2(h * (x.y - x.x), -h * (x.x + x.y))
-         : q == 5 ? make_float2(-h * (x.x + x.y), h * (x.x - x.y))
-                  : make_float2(h * (x.x - x.y), h * (x.x + x.y));
+    return q == 1 ? v_mul(v_add(x, c_mi(x)), v_bc(h))
+         : q == 3 ? v_mul(v_sub(c_mi(x), x), v_bc(h))
+         : q == 5 ? v_mul(v_add(x, c_mi(x)), v_bc(-h))
+                  : v_mul(v_sub(x, c_mi(x)), v_bc(h));
   }
   return c_mul(x, make_float2(tw.re[e], tw.im[e]));
 }
@@ -179,8 +236,8 @@ struct Dft<3> {
   __device__ __forceinline__ static void run(float2* v) {
     constexpr float s = 0.86602540378443864676f;  // sin(2 pi / 3)
     const float2 t1 = c_add(v[1], v[2]), t2 = c_sub(v[1], v[2]);
-    const float2 m = make_float2(fmaf(-0.5f, t1.x, v[0].x), fmaf(-0.5f, t1.y, v[0].y));
-    const float2 n = make_float2(s * t2.y, -s * t2.x);  // -i s (x1 - x2)
+    const float2 m = v_fma(t1, v_bc(-0.5f), v[0]);
+    const float2 n = v_mul(c_mi(t2), v_bc(s));  // -i s (x1 - x2)
     v[0] = c_add(v[0], t1);
     v[1] = c_add(m, n);
     v[2] = c_sub(m, n);
@@ -209,10 +266,10 @@ struct Dft<5> {
     const float2 t1 = c_add(v[1], v[4]), t2 = c_add(v[2], v[3]);
     const float2 t3 = c_sub(v[1], v[4]), t4 = c_sub(v[2], v[3]);
     const float2 x0 = v[0];
-    const float2 a1 = make_float2(fmaf(c1, t1.x, fmaf(c2, t2.x, x0.x)), fmaf(c1, t1.y, fmaf(c2, t2.y, x0.y)));
-    const float2 a2 = make_float2(fmaf(c2, t1.x, fmaf(c1, t2.x, x0.x)), fmaf(c2, t1.y, fmaf(c1, t2.y, x0.y)));
-    const float2 b1 = make_float2(fmaf(s1, t3.x, s2 * t4.x), fmaf(s1, t3.y, s2 * t4.y));
-    const float2 b2 = make_float2(fmaf(s2, t3.x, -s1 * t4.x), fmaf(s2, t3.y, -s1 * t4.y));
+    const float2 a1 = v_fma(t1, v_bc(c1), v_fma(t2, v_bc(c2), x0));
+    const float2 a2 = v_fma(t1, v_bc(c2), v_fma(t2, v_bc(c1), x0));
+    const float2 b1 = v_fma(t3, v_bc(s1), v_mul(t4, v_bc(s2)));
+    const float2 b2 = v_fma(t3, v_bc(s2), v_mul(t4, v_bc(-s1)));
     v[0] = c_add(x0, c_add(t1, t2));
     v[1] = c_add(a1, c_mi(b1));
     v[4] = c_sub(a1, c_mi(b1));

@@ -19,6 +19,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdint>
+
 #include "fft_core.cuh"
 
 namespace xcb {

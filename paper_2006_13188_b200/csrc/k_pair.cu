@@ -23,6 +23,8 @@
 #include <vector>
 
 #include "fft_pair.cuh"
+#include "pair_host.cuh"
+#include "pair_i1.cuh"
 #include "stages_common.cuh"
 #include "tma.cuh"
 #include "tmem.cuh"
@@ -30,159 +32,6 @@
 namespace xcb {
 namespace {
 
-// the thread's full pass-2 twiddle row W_L^{j r} (r = 1..R2-1) into TMEM at ta
-// (2 columns each; table twf is [r-1][j], j < NB2); warp-collective
-template <class PF>
-__device__ __forceinline__ void park_last_tw(const float2* __restrict__ twf, uint32_t ta) {
-  const int j = threadIdx.x >> 1;
-#pragma unroll
-  for (int r = 1; r < PF::R2; ++r)
-    tmem_st2(ta + 2 * (r - 1), j < PF::NB2 ? __ldg(twf + (r - 1) * PF::NB2 + j)
-                                           : make_float2(1.f, 0.f));
-}
-
-// ------------------------------------------------------------------ I1 (interleaved)
-// conj(H^) of NI images at the thread's pass-0 inputs is parked in TMEM for
-// the whole band loop; F^_k is TMA-staged once per band and applied to all NI
-// images (the filter spectrum is image-independent, so its HBM read is shared).
-// Per (band, image): two barriers (after pass 0, after pass 1).
-template <class PF, int NI>
-__device__ __forceinline__ void i1_body(int c, int b0, int b1, const Geo& g,
-                                        const float4* __restrict__ Hh,
-                                        size_t hstride4, const float4* __restrict__ Fh,
-                                        size_t sstride4, const Bands& bl,
-                                        float2* __restrict__ T2, size_t tstride,
-                                        const float2* __restrict__ twm,
-                                        const float2* __restrict__ twf) {
-  constexpr int L = PF::L;  // = Ph
-  // TMEM per thread: conj(H^) (2 R0 columns per image), then the pass-2
-  // twiddle row; warps of a lane quadrant side by side (up to 5 of 18)
-  constexpr int kThr = NI * 2 * PF::R0 + PF::kTwColsPad;
-  constexpr uint32_t kCols = PF::tmem_cols(kThr);
-  static_assert(kThr * PF::WPQ <= 512, "TMEM budget");
-  extern __shared__ __align__(16) float4 smp[];
-  float4* ST4 = smp;  // staged F^_k column pair, natural order
-  float4* W04 = ST4 + L;
-  float4* W14 = W04 + PF::LP;
-  float2* TWs = reinterpret_cast<float2*>(W14 + PF::LP);
-  const float2* ST = reinterpret_cast<const float2*>(ST4);
-  float2* W0 = reinterpret_cast<float2*>(W04);
-  float2* W1 = reinterpret_cast<float2*>(W14);
-  const int t = threadIdx.x;
-  const size_t plane = size_t(g.H2) * g.Pw;  // float2 per T2 band plane
-  constexpr unsigned kBytes = unsigned(L * sizeof(float4));
-  auto fsrc = [&](int bi) { return Fh + size_t(bl.spec[bi]) * sstride4 + size_t(c) * L; };
-  __shared__ __align__(8) uint64_t bar;
-  if (t == 0) {
-    mbar_init(&bar, 1);
-    fence_mbar_init();
-    mbar_expect_tx(&bar, kBytes);
-    bulk_copy(ST4, fsrc(b0), kBytes, &bar);
-    if (b0 + 1 < b1) prefetch_l2(fsrc(b0 + 1), kBytes);
-  }
-  // conj(H^) at this thread's pass-0 inputs n = j + r NB0, parked in TMEM
-  // (2 columns per r and image; warps of a lane quadrant side by side)
-  __shared__ uint32_t tbase;
-  if (t < 32) tmem_alloc(&tbase, kCols);
-  tmem_fence_before_sync();
-  __syncthreads();
-  tmem_fence_after_sync();
-  const uint32_t thc = tmem_warp_base(tbase) + uint32_t((t >> 7) * kThr);
-  const uint32_t ttw = thc + NI * 2 * PF::R0;
-  {
-    const int gi = t & 1, j = t >> 1;
-#pragma unroll
-    for (int im = 0; im < NI; ++im) {
-      const float2* hcol = reinterpret_cast<const float2*>(Hh + im * hstride4 + size_t(c) * L) + gi;
-#pragma unroll
-      for (int r = 0; r < PF::R0; ++r)
-        tmem_st2(thc + 2 * (im * PF::R0 + r),
-                 j < PF::NB0 ? c_conj(__ldg(hcol + 2 * (j + r * PF::NB0))) : make_float2(0.f, 0.f));
-    }
-    park_last_tw<PF>(twf, ttw);
-    tmem_wait_st();
-  }
-  for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
-  __syncthreads();
-  unsigned phase = 0;
-  for (int bi = b0; bi < b1; ++bi) {
-    mbar_wait(&bar, phase);
-    phase ^= 1;
-#pragma unroll 1
-    for (int im = 0; im < NI; ++im) {
-      // conj(H^ conj(F^)) = conj(H^) F^ : inverse via conj-FFT-conj
-      {
-        float2 hc[PF::R0];
-        const uint32_t ta = thc + 2 * PF::R0 * opaque_i(im);
-        tmem_ldn<2 * PF::R0>(ta, reinterpret_cast<float*>(hc));
-        tmem_wait_ld();
-        tmem_depn<2 * PF::R0>(reinterpret_cast<float*>(hc));
-        auto load = [&](int r, int n, int gi) -> float2 { return c_mul(hc[r], ST[2 * n + gi]); };
-        typename PF::P0Regs v;
-        PF::pass0_compute(load, v);
-        PF::pass0_store(W0, v);
-      }
-      __syncthreads();
-      if (t == 0 && im == NI - 1 && bi + 1 < b1) {
-        fence_proxy_async();
-        mbar_expect_tx(&bar, kBytes);
-        bulk_copy(ST4, fsrc(bi + 1), kBytes, &bar);
-        if (bi + 2 < b1) prefetch_l2(fsrc(bi + 2), kBytes);
-      }
-      PF::pass1(W0, W1, TWs);
-      __syncthreads();
-      const int tt = opaque_i(t), gi = tt & 1, j = tt >> 1;
-      // output y = j + r NB2 - off: NB2 is even, so y & 1 is fixed and y >> 1
-      // advances by NB2 / 2 rows of T2 per r
-      const int y0 = j - g.off;
-      const int rstride = (PF::NB2 / 2) * 2 * g.Pw;  // float2 per r step (< 2^31: one plane)
-      float2* o = T2 + im * tstride + size_t(bi) * plane + 2 * (2 * c + gi) +
-                  (ptrdiff_t(y0 >> 1) * (2 * g.Pw) + (y0 & 1));
-      const bool act = j < PF::NB2;
-      auto store = [&](float2 (&a)[PF::R2]) {
-        int y = opaque_i(y0);
-        float2* p = o;
-#pragma unroll
-        for (int r = 0; r < PF::R2; ++r) {
-          st_pred(p, c_conj(a[Dft<PF::R2>::pos(r)]), act && unsigned(y) < unsigned(g.H));
-          y += PF::NB2;
-          p += rstride;
-        }
-      };
-      float2 w[PF::kTwColsPad / 2 + 1];
-      tmem_ldn<PF::kTwColsPad>(ttw, reinterpret_cast<float*>(w + 1));
-      tmem_wait_ld();
-      tmem_depn<PF::kTwColsPad>(reinterpret_cast<float*>(w + 1));
-      PF::pass2_all_w(W1, w, store);
-    }
-  }
-  tmem_fence_before_sync();
-  __syncthreads();
-  if (t < 32) {
-    tmem_fence_after_sync();
-    tmem_dealloc(tbase, kCols);
-  }
-}
-
-template <class PF, int NI>
-__global__ void __launch_bounds__(PF::T, PF::MINB)
-    k_cols_inv_corr_ilv(Geo g, const float4* __restrict__ Hh, size_t hstride4,
-                        const float4* __restrict__ Fh, size_t sstride4, Bands bl,
-                        float2* __restrict__ T2, size_t tstride,
-                        const float2* __restrict__ twm, const float2* __restrict__ twf,
-                        int full, int split) {
-  // CTAs below `full` run every band of column pair blockIdx.x; the column
-  // pairs of the last, partial wave are split into `split` band chunks so the
-  // tail spreads over all SMs (CTAs are dispatched in blockIdx order)
-  int c = blockIdx.x, b0 = 0, b1 = bl.n;
-  if (c >= full) {
-    const int u = c - full, ch = u % split;
-    c = full + u / split;
-    b0 = ch * bl.n / split;
-    b1 = (ch + 1) * bl.n / split;
-  }
-  i1_body<PF, NI>(c, b0, b1, g, Hh, hstride4, Fh, sstride4, bl, T2, tstride, twm, twf);
-}
 
 // ------------------------------------------------------------------ I2 (interleaved)
 // TMEM per thread: the band accumulator and the steering phasor z = e^{i phi}
@@ -307,8 +156,7 @@ __device__ __forceinline__ void i2_body(int b, const Geo& g, const float4* __res
           float2 pa = make_float2(az[i].x, az[i].y);
           const float2 zr = make_float2(az[i].z, az[i].w);
           if (dk == 1) {
-            pa = make_float2(fmaf(pa.x, zr.x, fmaf(-pa.y, zr.y, va.x)),
-                             fmaf(pa.x, zr.y, fmaf(pa.y, zr.x, -va.y)));
+            pa = c_fma(pa, zr, c_conj(va));
           } else {
             float2 za = zr;
             int d = dk;
@@ -426,80 +274,6 @@ __global__ void __launch_bounds__(PF::T, 1)
                     b.scale, twm, twl);
 }
 
-// ------------------------------------------------------------------ planes (interleaved)
-// Angle-max front end: per band, row IFFT of T2_b, crop, store the band plane
-// G_b = H * F_b (engine.hpp:304-311 per band); k_anglemax_* then reads all
-// bands per pixel.  Same engine as I2 without the steering; a warp's store
-// covers 16 consecutive pixels of both rows (two full 128-byte lines).
-template <class PF>
-__global__ void __launch_bounds__(PF::T, PF::MINB)
-    k_rows_inv_planes_ilv(Geo g, const float4* __restrict__ T2, int nbands,
-                          float2* __restrict__ planes, float scale,
-                          const float2* __restrict__ twm, const float2* __restrict__ twl) {
-  constexpr int L = PF::L;  // = Pw
-  constexpr int R2 = PF::R2;
-  extern __shared__ __align__(16) float4 smp[];
-  float4* ST4 = smp;
-  float4* W04 = ST4 + L;
-  float4* W14 = W04 + PF::LP;
-  float2* TWs = reinterpret_cast<float2*>(W14 + PF::LP);
-  const float2* ST = reinterpret_cast<const float2*>(ST4);
-  float2* W0 = reinterpret_cast<float2*>(W04);
-  float2* W1 = reinterpret_cast<float2*>(W14);
-  const int b = blockIdx.x, t = threadIdx.x;
-  const size_t plane4 = size_t(g.H2 / 2) * g.Pw;
-  const float4* rowp = T2 + size_t(b) * g.Pw;
-  constexpr unsigned kBytes = unsigned(L * sizeof(float4));
-  __shared__ __align__(8) uint64_t bar;
-  if (t == 0) {
-    mbar_init(&bar, 1);
-    fence_mbar_init();
-    mbar_expect_tx(&bar, kBytes);
-    bulk_copy(ST4, rowp, kBytes, &bar);
-    if (nbands > 1) prefetch_l2(rowp + plane4, kBytes);
-  }
-  for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
-  typename PF::LastTw tl;
-  PF::load_last_tw(twl, tl);
-  __syncthreads();
-  const size_t npix = size_t(g.H) * g.W;
-  unsigned phase = 0;
-  for (int bi = 0; bi < nbands; ++bi) {
-    mbar_wait(&bar, phase);
-    phase ^= 1;
-    auto load = [&](int, int n, int gi) -> float2 { return c_conj(ST[2 * n + gi]); };
-    {
-      typename PF::P0Regs v;
-      PF::pass0_compute(load, v);
-      PF::pass0_store(W0, v);
-    }
-    __syncthreads();
-    if (t == 0 && bi + 1 < nbands) {
-      fence_proxy_async();
-      mbar_expect_tx(&bar, kBytes);
-      bulk_copy(ST4, rowp + size_t(bi + 1) * plane4, kBytes, &bar);
-      if (bi + 2 < nbands) prefetch_l2(rowp + size_t(bi + 2) * plane4, kBytes);
-    }
-    PF::pass1(W0, W1, TWs);
-    __syncthreads();
-    const int tt = opaque_i(t), gi = tt & 1, j = tt >> 1, y = 2 * b + gi;
-    const int x0 = j - g.off;
-    float2* o = planes + size_t(bi) * npix + size_t(y) * g.W + x0;
-    const bool act = j < PF::NB2 && y < g.H;
-    auto store = [&](float2 (&a)[R2]) {
-      int x = opaque_i(x0);
-      float2* p = o;
-#pragma unroll
-      for (int r = 0; r < R2; ++r) {
-        st_pred(p, c_scale(c_conj(a[Dft<R2>::pos(r)]), scale),
-                act && unsigned(x) < unsigned(g.W));
-        x += PF::NB2;
-        p += PF::NB2;
-      }
-    };
-    PF::pass2_all(W1, tl, store);
-  }
-}
 
 // ------------------------------------------------------------------ S1 (interleaved)
 // TMEM per thread, for each pass-0 input r: [cur.re, cur.im, mul.re, mul.im]
@@ -955,44 +729,6 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
   PF::pass2_all(W1, tl, store);
 }
 
-constexpr size_t kSmemLimitP = 232448;
-
-// exact twiddle tables of a pair plan (fp64 -> fp32), per device: pass 1
-// [r-1][jm] (W_{R0 R1}^{jm r}) and pass 2 [r-1][j] (W_L^{j r}, full rows)
-struct PairTw {
-  float2* mid = nullptr;
-  float2* last = nullptr;
-};
-
-template <class PF>
-PairTw pair_tables() {
-  static std::mutex mu;
-  static std::map<int, PairTw> cache;  // device -> tables
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(mu);
-  auto it = cache.find(dev);
-  if (it != cache.end()) return it->second;
-  std::vector<float2> m(PF::TWM), l(PF::TWL);
-  const double tp = 6.283185307179586476925286766559;
-  auto w = [&](long e, long n) {
-    e %= n;
-    const double a = -tp * double(e) / double(n);
-    return make_float2(float(std::cos(a)), float(std::sin(a)));
-  };
-  for (int r = 1; r < PF::R1; ++r)
-    for (int jm = 0; jm < PF::R0; ++jm) m[(r - 1) * PF::R0 + jm] = w(long(jm) * r, PF::R0 * PF::R1);
-  for (int r = 1; r < PF::R2; ++r)
-    for (int j = 0; j < PF::NB2; ++j) l[(r - 1) * PF::NB2 + j] = w(long(j) * r, PF::L);
-  PairTw p;
-  if (cudaMalloc(&p.mid, m.size() * sizeof(float2)) != cudaSuccess ||
-      cudaMalloc(&p.last, l.size() * sizeof(float2)) != cudaSuccess)
-    return PairTw{};
-  cudaMemcpy(p.mid, m.data(), m.size() * sizeof(float2), cudaMemcpyHostToDevice);
-  cudaMemcpy(p.last, l.data(), l.size() * sizeof(float2), cudaMemcpyHostToDevice);
-  cache[dev] = p;
-  return p;
-}
 
 }  // namespace
 
@@ -1054,21 +790,12 @@ int pair_i1_images() {
   return n;
 }
 
-#define XCB_PAIR_DISPATCH(LEN, BODY)                                               \
-  switch (LEN) {                                                                   \
-    XCB_PAIR_TABLE(BODY)                                                           \
-    default: break;                                                                \
-  }
-
 // Grid of a band-loop kernel over `units` independent units (column pairs)
 // with `per_sm` resident CTAs per SM: whole waves run every band; the units of
 // the last, partial wave are split into band chunks so that the tail fills
 // the SMs.  The split minimises ceil(rem * s / slots) * (ceil(nb / s) + 1)
 // (one band-equivalent of per-CTA setup per chunk).  XCB_TAIL_SPLIT=0 turns
 // it off.
-struct TailSplit {
-  int grid, full, split;
-};
 TailSplit tail_split(int units, int per_sm, int nb) {
   static const int sms = [] {
     int dev = 0, n = 0;
@@ -1094,54 +821,6 @@ TailSplit tail_split(int units, int per_sm, int nb) {
     }
   }
   return {full + rem * best, full, best};
-}
-
-void launch_cols_inv_corr_pair(const Geo& g, const float2* Hhat, const float2* Fhat,
-                               size_t sstride, const Bands& b, float2* T2, cudaStream_t st,
-                               LaunchCounter& lc, int nimg, size_t hstride, size_t tstride) {
-  const size_t sm = pair_smem(0, g.Ph, g);
-  const float4* hh = reinterpret_cast<const float4*>(Hhat);
-  const float4* fh = reinterpret_cast<const float4*>(Fhat);
-  const int ncol = g.Pw / 2;
-#define XCB_BODY(LL, R0, R1, R2, PP)                                                         \
-  case LL: {                                                                                \
-    using PF = IlvFft<LL, R0, R1, R2, PP>;                                                  \
-    const PairTw tw = pair_tables<PF>();                                                    \
-    const TailSplit ts = tail_split(ncol, PF::MINB, b.n);                                   \
-    if (nimg == 2) {                                                                        \
-      set_smem(k_cols_inv_corr_ilv<PF, 2>, sm);                                             \
-      k_cols_inv_corr_ilv<PF, 2><<<ts.grid, PF::T, sm, st>>>(                               \
-          g, hh, hstride / 2, fh, sstride / 2, b, T2, tstride, tw.mid, tw.last, ts.full,    \
-          ts.split);                                                                        \
-    } else {                                                                                \
-      set_smem(k_cols_inv_corr_ilv<PF, 1>, sm);                                             \
-      k_cols_inv_corr_ilv<PF, 1><<<ts.grid, PF::T, sm, st>>>(                               \
-          g, hh, hstride / 2, fh, sstride / 2, b, T2, tstride, tw.mid, tw.last, ts.full,    \
-          ts.split);                                                                        \
-    }                                                                                       \
-    break;                                                                                  \
-  }
-  XCB_PAIR_DISPATCH(g.Ph, XCB_BODY)
-#undef XCB_BODY
-  ++lc.n;
-}
-
-void launch_rows_inv_planes_pair(const Geo& g, const float2* T2, int nbands, float2* planes,
-                                 cudaStream_t st, LaunchCounter& lc) {
-  const size_t sm = pair_smem(2, g.Pw, g);
-  const float scale = float(1.0 / (double(g.Ph) * double(g.Pw)));
-#define XCB_BODY(LL, R0, R1, R2, PP)                                                         \
-  case LL: {                                                                                \
-    using PF = IlvFft<LL, R0, R1, R2, PP>;                                                  \
-    const PairTw tw = pair_tables<PF>();                                                    \
-    set_smem(k_rows_inv_planes_ilv<PF>, sm);                                                \
-    k_rows_inv_planes_ilv<PF><<<g.H2 / 2, PF::T, sm, st>>>(                                 \
-        g, reinterpret_cast<const float4*>(T2), nbands, planes, scale, tw.mid, tw.last);    \
-    break;                                                                                  \
-  }
-  XCB_PAIR_DISPATCH(g.Pw, XCB_BODY)
-#undef XCB_BODY
-  ++lc.n;
 }
 
 void launch_rows_inv_steer_pair(const Geo& g, const float2* T2, const Bands& b, int half,
