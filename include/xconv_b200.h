@@ -63,7 +63,7 @@
 extern "C" {
 #endif
 
-#define XC_ABI_VERSION 1
+#define XC_ABI_VERSION 2 /* 2: xc_stats::band_mode */
 
 enum xc_status {
   XC_OK = 0,
@@ -121,6 +121,10 @@ typedef struct {
   int gpu_launches;        /* kernels launched by this call */
   int bands_run;           /* bands transformed per image (the Hermitian half-band
                               mode transforms k >= 0 only; summed over devices) */
+  int band_mode;           /* 0: every band transformed; 1: Hermitian half-band (real
+                              signal, F_{-k} = conj F_k); 2: conjugate band pairs of the
+                              scatter (real signal, any filter: bands k >= 0 transformed,
+                              each fed into the F_k and the conj(f_{-k}) sums) */
 } xc_stats;
 
 int xc_abi_version(void);

@@ -36,7 +36,8 @@ class Stats(C.Structure):
                 ("seconds_render", C.c_double), ("seconds_fft", C.c_double),
                 ("seconds_combine", C.c_double), ("seconds_premultiply", C.c_double),
                 ("seconds_h2d", C.c_double), ("seconds_d2h", C.c_double),
-                ("seconds_total", C.c_double), ("gpu_launches", C.c_int), ("bands_run", C.c_int)]
+                ("seconds_total", C.c_double), ("gpu_launches", C.c_int), ("bands_run", C.c_int),
+                ("band_mode", C.c_int)]
 
 
 EXPORTS = [

@@ -331,6 +331,7 @@ struct Call {
   double h2d_s = 0, d2h_s = 0;
   bool out_dev = false;  // outputs are device buffers even when d.memory == XC_HOST
   int nb_run = 0;        // bands transformed per image (Hermitian half-band: k >= 0)
+  int band_mode = 0;     // xc_stats::band_mode
 };
 
 std::vector<int> plan_components(const xcb::HostFilter& hf, const int* comps, int n) {
@@ -375,6 +376,32 @@ float2* filter_spectra(Call& c) {
   ck(cudaStreamSynchronize(c.st), "filter spectra");  // host table lifetime
   c.f->spectra[key] = spec;
   return spec;
+}
+
+// Spectra of the conjugated components, G_i = FFT2(conj f_i) = conj(F^_i[-v, -u]),
+// built from the cached F^ on first use by a real-signal scatter (conjugate
+// band pairs, run_scatter); cached beside F^ under (dev, Ph, Pw, transposed + 2).
+float2* filter_spectra_conj(Call& c) {
+  const auto key = std::make_tuple(c.ctx->device, c.g.Ph, c.g.Pw, c.transposed + 2);
+  std::lock_guard<std::mutex> flk(c.f->mu);
+  auto it = c.f->spectra.find(key);
+  if (it != c.f->spectra.end()) return it->second;
+  const int nb = c.f->hf.nc();
+  float2* spec = nullptr;
+  ck(cudaMalloc(&spec, size_t(nb) * c.g.Ph * c.g.Pw * sizeof(float2)), "cudaMalloc spectra");
+  xcb::launch_spec_conj_reflect(c.Fhat, spec, nb, c.g.Ph, c.g.Pw, c.st, c.lc);
+  ck(cudaGetLastError(), "conjugated spectra launch");
+  c.f->spectra[key] = spec;
+  return spec;
+}
+
+// XCB_CPAIR=0 disables the scatter's conjugate band pairs (A/B timing, tests)
+bool use_cpair() {
+  static const bool on = [] {
+    const char* e = std::getenv("XCB_CPAIR");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 // Pad (transform length) for an extent needing >= n points: any length >= n
@@ -757,6 +784,7 @@ void run_gather(Call& c, const xcb::SigSrc& sig, const double* base, void* out, 
   bool half;
   const xcb::Bands bands = gather_bands(c, &sig, 1, &half);
   c.nb_run = bands.n;
+  c.band_mode = half ? 1 : 0;
   float2* T1 = c.ctx->buf<float2>("T1", size_t(g.Hx2) * g.Pw);
   float2* Hh = c.ctx->buf<float2>("Hhat", size_t(g.Ph) * g.Pw);
   float2* T2 = c.ctx->buf<float2>("T2", size_t(bands.n) * g.H2 * g.Pw);
@@ -791,6 +819,7 @@ void run_gather2(Call& c, const xcb::SigSrc* sig, double* const* base, void* con
   bool half;
   const xcb::Bands bands = gather_bands(c, sig, 2, &half);
   c.nb_run = bands.n;
+  c.band_mode = half ? 1 : 0;
   const size_t P = size_t(g.Ph) * g.Pw, tstride = size_t(bands.n) * g.H2 * g.Pw;
   float2* T1 = c.ctx->buf<float2>("T1", size_t(g.Hx2) * g.Pw);
   float2* Hh = c.ctx->buf<float2>("Hhat2", 2 * P);
@@ -840,10 +869,41 @@ void run_scatter(Call& c, const xcb::SigSrc& sig, const double* base, void* out,
     half = hb.n > 0;
     if (half) bands = hb;
   }
+  // Conjugate band pairs (real signal, any filter, symmetric band selection):
+  // H e^{+ik phi} = conj(H e^{-ik phi}), so S1 transforms the bands k >= 0 only
+  // and S2 feeds each into two sums (k_pair.cu k_cols_fwd_mac_cpair_ilv)
+  const int* gspec = nullptr;
+  const float2* Ghat = nullptr;
+  bool cpair = !half && use_cpair() && !sig.is_complex && !c.packed && use_pair() &&
+               xcb::pair_smem(3, g.Pw, g) && xcb::pair_smem(4, g.Ph, g) &&
+               xcb::pair_smem(7, g.Pw, g) && c.ks.size() > 1;
+  if (cpair) {
+    std::vector<int> hk, hs, hg;
+    for (size_t i = 0; i < c.ks.size() && cpair; ++i) {
+      const auto neg = std::find(c.ks.begin(), c.ks.end(), -c.ks[i]);
+      cpair = neg != c.ks.end() && std::count(c.ks.begin(), c.ks.end(), c.ks[i]) == 1;
+      if (cpair && c.ks[i] >= 0) {
+        hk.push_back(c.ks[i]);
+        hs.push_back(c.sidx[i]);
+        hg.push_back(c.sidx[size_t(neg - c.ks.begin())]);
+      }
+    }
+    if (cpair) {
+      const int n = int(hk.size());
+      hk.insert(hk.end(), hs.begin(), hs.end());
+      hk.insert(hk.end(), hg.begin(), hg.end());
+      int* db = c.ctx->band_table(hk);
+      bands = xcb::Bands{db, db + n, n};
+      gspec = db + 2 * n;
+      Ghat = filter_spectra_conj(c);
+    }
+  }
   c.nb_run = bands.n;
+  c.band_mode = half ? 1 : cpair ? 2 : 0;
+  const size_t t2plane = size_t(g.H2) * g.Pw;
   float2* T1 = c.ctx->buf<float2>("T1b", size_t(bands.n) * g.Hx2 * g.Pw);
   float2* Sg = c.ctx->buf<float2>("Sigma", size_t(g.Ph) * g.Pw);
-  float2* T2 = c.ctx->buf<float2>("T2s", size_t(g.H2) * g.Pw);
+  float2* T2 = c.ctx->buf<float2>("T2s", (cpair ? 2 : 1) * t2plane);
   if (use_pair() && xcb::pair_smem(3, g.Pw, g)) {
     stage(c, "S1_rows_fwd_premul", [&] {
       xcb::launch_rows_fwd_premul_pair(g, sig, base, bands, T1, c.st, c.lc);
@@ -857,7 +917,12 @@ void run_scatter(Call& c, const xcb::SigSrc& sig, const double* base, void* out,
       xcb::launch_rows_fwd_premul(*c.prow, g, sig, base, bands, T1, c.st, c.lc);
     });
   }
-  if (use_pair() && xcb::pair_smem(4, g.Ph, g)) {
+  if (cpair) {
+    stage(c, "S2_cols_fwd_mac_inv", [&] {
+      xcb::launch_cols_fwd_mac_inv_cpair(g, T1, c.Fhat, Ghat, c.sstride, bands, gspec, T2, t2plane,
+                                         c.st, c.lc);
+    });
+  } else if (use_pair() && xcb::pair_smem(4, g.Ph, g)) {
     stage(c, "S2_cols_fwd_mac_inv", [&] {
       xcb::launch_cols_fwd_mac_inv_pair(g, T1, c.Fhat, c.sstride, bands, half ? 1 : 0, T2, c.st,
                                         c.lc);
@@ -877,7 +942,8 @@ void run_scatter(Call& c, const xcb::SigSrc& sig, const double* base, void* out,
   stage(c, "S4_rows_inv_out", [&] {
     if (use_pair() && xcb::pair_smem(7, g.Pw, g))
       xcb::launch_rows_inv_out_pair(g, T2, out_kind, out, accumulate ? 1 : 0, half ? 1 : 0, sig,
-                                    dcv.real(), dcv.imag(), c.st, c.lc);
+                                    dcv.real(), dcv.imag(), c.st, c.lc,
+                                    cpair ? T2 + t2plane : nullptr);
     else
       xcb::launch_rows_inv_out(*c.prow, g, T2, out_kind, out, accumulate ? 1 : 0, sig, dcv.real(),
                                dcv.imag(), c.st, c.lc);
@@ -923,6 +989,7 @@ void run_gather_dual(Call& c, HostPipe& hp, const void* signal, const void* para
       if (img == 0) {
         bands = gather_bands(c, &st.sig, 1, &half);
         c.nb_run = bands.n;
+        c.band_mode = half ? 1 : 0;
         for (int i = 0; i < 2; ++i)
           T2[i] = c.ctx->buf<float2>("T2_d" + std::to_string(i), size_t(bands.n) * g.H2 * g.Pw);
       }
@@ -963,6 +1030,7 @@ void fill_stats(Call& c, xc_stats* st, double gpu_s, double total_s, long long o
   st->seconds_total = total_s;
   st->gpu_launches = c.lc.n;
   st->bands_run = c.nb_run;
+  st->band_mode = c.band_mode;
 }
 
 void run_single(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d,
@@ -2515,6 +2583,7 @@ void merge_stats(xc_stats* out, const std::vector<xc_stats>& st, long long ops, 
     out->clamped_pixels += s.clamped_pixels;
     out->gpu_launches += s.gpu_launches;
     out->bands_run += s.bands_run;
+    out->band_mode = std::max(out->band_mode, s.band_mode);
   }
   out->seconds_total = t0_s;
 }

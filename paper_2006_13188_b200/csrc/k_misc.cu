@@ -899,3 +899,31 @@ void launch_fft2_out(const float2* hh, int rows, int cols, int tr, int inverse, 
   ++lc.n;
 }
 }  // namespace xcb
+
+// ------------------------------------------------------------------ conjugated spectra
+// The DFT of conj(a) is conj(A[-v, -u]): the spectra of the conjugated filter
+// components from the cached ones (layout B: ((u / 2) Ph + v) 2 + u % 2), for
+// the scatter's conjugate band pairs (kernels.h launch_cols_fwd_mac_inv_cpair).
+namespace xcb {
+namespace {
+__global__ void k_spec_conj_reflect(const float2* __restrict__ F, float2* __restrict__ G, int ph,
+                                    int pw, size_t total) {
+  const size_t plane = size_t(ph) * pw;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const size_t b = i / plane, e = i - b * plane;
+    const int gq = int(e & 1), v = int((e >> 1) % ph), u = int((e >> 1) / ph) * 2 + gq;
+    const int vs = v ? ph - v : 0, us = u ? pw - u : 0;
+    const float2 x = F[b * plane + (size_t(us >> 1) * ph + vs) * 2 + (us & 1)];
+    G[i] = make_float2(x.x, -x.y);
+  }
+}
+}  // namespace
+
+void launch_spec_conj_reflect(const float2* Fhat, float2* Ghat, int nb, int Ph, int Pw,
+                              cudaStream_t st, LaunchCounter& lc) {
+  const size_t total = size_t(nb) * Ph * Pw;
+  k_spec_conj_reflect<<<grid_for(total, 256), 256, 0, st>>>(Fhat, Ghat, Ph, Pw, total);
+  ++lc.n;
+}
+}  // namespace xcb

@@ -606,6 +606,208 @@ __global__ void __launch_bounds__(PF::T, 1)
   }
 }
 
+// ------------------------------------------------------------------ S2, conjugate band pairs
+// Real signal, any filter: H e^{+ik phi} = conj(H e^{-ik phi}), so S1 transforms
+// the bands k >= 0 only and the -k term of the scatter is
+//   (H e^{+ik phi}) * f_{-k} = conj((H e^{-ik phi}) * conj(f_{-k})).
+// Per band k this kernel feeds the column FFT X of T1_k into two sums in TMEM,
+// A += X F^_k and (k > 0) B += X G_k with G_k the spectrum of conj(f_{-k}); both
+// are inverse transformed (T2, T2 + t2plane) and S4 writes a + conj(b).  F^_k
+// and G_k are staged side by side (single buffers) by one TMA pair per band:
+// every warp arrives on `bard` when its pass-2 reads of the buffers are done,
+// thread 0 then issues the next band's pair, which lands during that band's
+// passes 0 and 1.  Same shared memory as k_cols_fwd_mac_ilv.
+// two CTAs per SM when two sets of buffers fit in shared memory (1152): the
+// register file then allows 80 per thread (warps are allocated in fours)
+template <class PF>
+__global__ void __launch_bounds__(PF::T)
+    __maxnreg__((3 * PF::L + 2 * PF::LP) * 16 + PF::TWM * 8 <= 112 * 1024 ? 80 : 112)
+        k_cols_fwd_mac_cpair_ilv(Geo g, const float4* __restrict__ T1, const float4* __restrict__ Fh,
+                             const float4* __restrict__ Gh, size_t sstride4, Bands bl,
+                             const int* __restrict__ gspec, float2* __restrict__ T2,
+                             size_t t2plane, const float2* __restrict__ twm,
+                             const float2* __restrict__ twl) {
+  constexpr int L = PF::L, R2 = PF::R2;  // L = Ph
+  constexpr int kThr = 4 * R2;           // A then B, 2 columns per pass-2 output
+  static_assert(kThr * PF::WPQ <= 512, "TMEM budget");
+  extern __shared__ __align__(16) float4 smp[];
+  float4* ST4 = smp;      // T1_k column pair (Hx2 <= L rows)
+  float4* SF4 = ST4 + L;  // F^_k column pair
+  float4* SG4 = SF4 + L;  // G_k column pair
+  float4* W04 = SG4 + L;
+  float4* W14 = W04 + PF::LP;
+  float2* TWs = reinterpret_cast<float2*>(W14 + PF::LP);
+  const float2* ST = reinterpret_cast<const float2*>(ST4);
+  float2* W0 = reinterpret_cast<float2*>(W04);
+  float2* W1 = reinterpret_cast<float2*>(W14);
+  __shared__ __align__(8) uint64_t bar, barf, bard;
+  __shared__ uint32_t tbase;
+  const int c = blockIdx.x, t = threadIdx.x;
+  const size_t plane1 = size_t(g.Hx2 / 2) * g.Pw;  // float4 per T1 band plane
+  const float4* colT = T1 + size_t(c) * g.Hx2;     // [u/2][y] pairs
+  const unsigned bytesT = unsigned(g.Hx2) * unsigned(sizeof(float4));
+  constexpr unsigned kBytesF = unsigned(L * sizeof(float4));
+  auto fsrc = [&](int bi) { return Fh + size_t(bl.spec[bi]) * sstride4 + size_t(c) * L; };
+  auto gsrc = [&](int bi) { return Gh + size_t(gspec[bi]) * sstride4 + size_t(c) * L; };
+  // F^ and G of band bi -> SF4, SG4 (thread 0)
+  auto stage_fg = [&](int bi) {
+    const bool pb = bl.k[bi] != 0;
+    mbar_expect_tx(&barf, pb ? 2 * kBytesF : kBytesF);
+    bulk_copy(SF4, fsrc(bi), kBytesF, &barf);
+    if (pb) bulk_copy(SG4, gsrc(bi), kBytesF, &barf);
+  };
+  if (t == 0) {
+    mbar_init(&bar, 1);
+    mbar_init(&barf, 1);
+    mbar_init(&bard, PF::T / 32);
+    fence_mbar_init();
+    mbar_expect_tx(&bar, bytesT);
+    bulk_copy(ST4, colT, bytesT, &bar);
+    stage_fg(0);
+    if (bl.n > 1) {
+      prefetch_l2(colT + plane1, bytesT);
+      prefetch_l2(fsrc(1), kBytesF);
+      if (bl.k[1] != 0) prefetch_l2(gsrc(1), kBytesF);
+    }
+  }
+  if (t < 32) tmem_alloc(&tbase, PF::tmem_cols(kThr));
+  for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
+  typename PF::LastTw tl;
+  PF::load_last_tw(twl, tl);
+  tmem_fence_before_sync();
+  __syncthreads();
+  tmem_fence_after_sync();
+  const uint32_t tacc = tmem_warp_cols(tbase, kThr);
+#pragma unroll
+  for (int r = 0; r < 2 * R2; ++r) tmem_st2(tacc + 2 * r, make_float2(0.f, 0.f));
+  tmem_wait_st();
+  const int hx2 = g.Hx2;
+  unsigned phase = 0;
+  for (int bi = 0; bi < bl.n; ++bi) {
+    const bool pairb = bl.k[bi] != 0;  // CTA-uniform: the k = 0 band has no partner
+    mbar_wait(&bar, phase);
+    {
+      auto load = [&](int, int n, int gi) -> float2 {
+        return n < hx2 ? ST[2 * n + gi] : make_float2(0.f, 0.f);
+      };
+      typename PF::P0Regs v;
+      PF::pass0_compute(load, v);
+      PF::pass0_store(W0, v);
+    }
+    __syncthreads();
+    if (t == 0 && bi + 1 < bl.n) {
+      fence_proxy_async();
+      mbar_expect_tx(&bar, bytesT);
+      bulk_copy(ST4, colT + size_t(bi + 1) * plane1, bytesT, &bar);
+      if (bi + 2 < bl.n) {
+        prefetch_l2(colT + size_t(bi + 2) * plane1, bytesT);
+        prefetch_l2(fsrc(bi + 2), kBytesF);
+        if (bl.k[bi + 2] != 0) prefetch_l2(gsrc(bi + 2), kBytesF);
+      }
+    }
+    PF::pass1(W0, W1, TWs);
+    __syncthreads();
+    mbar_wait(&barf, phase);
+    const int tt = opaque_i(t);
+    // F^[k], G[k] of this thread's sequence: 2 k + g, k = j + r NB2
+    const float2* fp = reinterpret_cast<const float2*>(SF4) + tt;
+    const float2* gp = reinterpret_cast<const float2*>(SG4) + tt;
+    auto mac = [&](float2 (&a)[R2]) {
+      constexpr int C = 4;
+      // one sum at a time (A with F^, then B with G) to bound the live registers
+#pragma unroll 1
+      for (int h = 0; h < (pairb ? 2 : 1); ++h) {
+        const uint32_t ta = tacc + 2 * R2 * opaque_i(h);
+        const float2* sp = h ? gp : fp;
+#pragma unroll
+        for (int r0 = 0; r0 < R2; r0 += C) {
+          float2 acc[C];
+#pragma unroll
+          for (int i = 0; i < C; ++i)
+            if (r0 + i < R2) acc[i] = tmem_ld2(ta + 2 * (r0 + i));
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < C; ++i)
+            if (r0 + i < R2) tmem_dep(acc[i]);
+#pragma unroll
+          for (int i = 0; i < C; ++i) {
+            const int r = r0 + i;
+            if (r >= R2) break;
+            acc[i] = c_add(acc[i], c_mul(a[Dft<R2>::pos(r)], sp[2 * r * PF::NB2]));
+          }
+#pragma unroll
+          for (int i = 0; i < C; ++i)
+            if (r0 + i < R2) tmem_st2(ta + 2 * (r0 + i), acc[i]);
+        }
+      }
+      tmem_wait_st();
+    };
+    PF::pass2_all(W1, tl, mac);
+    // the staged spectra are free once every warp is past its pass 2
+    __syncwarp();
+    if ((t & 31) == 0) mbar_arrive(&bard);
+    if (t == 0 && bi + 1 < bl.n) {
+      mbar_wait(&bard, phase);
+      fence_proxy_async();
+      stage_fg(bi + 1);
+    }
+    phase ^= 1;
+  }
+  // inverse column transforms of the two band sums: conj(acc) -> W1 (natural
+  // order) -> FFT -> conj -> T2 plane
+#pragma unroll 1
+  for (int p = 0; p < 2; ++p) {
+    __syncthreads();  // every thread is past the previous pass-2 reads of W1
+    {
+      const int gi = t & 1, j = t >> 1;
+      const uint32_t ta = tacc + 2 * R2 * opaque_i(p);
+#pragma unroll
+      for (int r = 0; r < R2; ++r) {
+        float2 v = tmem_ld2(ta + 2 * r);
+        tmem_wait_ld();
+        tmem_dep(v);
+        if (j < PF::NB2) W1[2 * (j + r * PF::NB2) + gi] = c_conj(v);
+      }
+    }
+    __syncthreads();
+    {
+      const float2* S = W1;
+      auto load = [&](int, int n, int gi) -> float2 { return S[2 * n + gi]; };
+      typename PF::P0Regs v;
+      PF::pass0_compute(load, v);
+      PF::pass0_store(W0, v);
+    }
+    __syncthreads();
+    PF::pass1(W0, W1, TWs);
+    __syncthreads();
+    {
+      const int tt = opaque_i(t), gi = tt & 1, j = tt >> 1;
+      const int y0 = j - g.off;
+      const int rstride = (PF::NB2 / 2) * 2 * g.Pw;
+      float2* o = T2 + size_t(p) * t2plane + 2 * (2 * c + gi) +
+                  (ptrdiff_t(y0 >> 1) * (2 * g.Pw) + (y0 & 1));
+      const bool act = j < PF::NB2;
+      auto store = [&](float2 (&a)[R2]) {
+        int y = opaque_i(y0);
+        float2* q = o;
+#pragma unroll
+        for (int r = 0; r < R2; ++r) {
+          st_pred(q, c_conj(a[Dft<R2>::pos(r)]), act && unsigned(y) < unsigned(g.H));
+          y += PF::NB2;
+          q += rstride;
+        }
+      };
+      PF::pass2_all(W1, tl, store);
+    }
+  }
+  tmem_fence_before_sync();
+  __syncthreads();
+  if (t < 32) {
+    tmem_fence_after_sync();
+    tmem_dealloc(tbase, PF::tmem_cols(kThr));
+  }
+}
+
 // ------------------------------------------------------------------ single transforms
 // F1 (row FFT of the zero-padded / periodically extended signal -> T1), F2
 // (column FFT of T1 -> spectrum, layout B) and S4 (row IFFT of T2, crop,
@@ -694,9 +896,10 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
 
 template <class PF, class TO>
 __global__ void __launch_bounds__(PF::T, PF::MINB)
-    k_rows_inv_out_ilv(Geo g, const float4* __restrict__ T2, TO* __restrict__ out,
-                       int accumulate, int real2, SigSrc dcs, double dcr, double dci, float scale,
-                       const float2* __restrict__ twm, const float2* __restrict__ twl) {
+    k_rows_inv_out_ilv(Geo g, const float4* __restrict__ T2, const float4* __restrict__ T2b,
+                       TO* __restrict__ out, int accumulate, int real2, SigSrc dcs, double dcr,
+                       double dci, float scale, const float2* __restrict__ twm,
+                       const float2* __restrict__ twl) {
   extern __shared__ __align__(16) float4 smp[];
   float2* W0 = reinterpret_cast<float2*>(smp);
   float2* W1 = reinterpret_cast<float2*>(smp + PF::LP);
@@ -705,6 +908,27 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
   for (int i = t; i < PF::TWM; i += blockDim.x) TWs[i] = twm[i];
   typename PF::LastTw tl;
   PF::load_last_tw(twl, tl);
+  // conjugate band pairs: the second plane's term is conj(IFFT(T2b)) =
+  // FFT(conj T2b) / (Ph Pw), kept in registers and added to the first plane's
+  float2 kb[PF::R2];
+#pragma unroll
+  for (int r = 0; r < PF::R2; ++r) kb[r] = make_float2(0.f, 0.f);
+  if (T2b) {  // CTA-uniform
+    const float2* srcb = reinterpret_cast<const float2*>(T2b + size_t(b) * g.Pw);
+    auto loadb = [&](int, int n, int gi) -> float2 { return c_conj(__ldg(srcb + 2 * n + gi)); };
+    typename PF::P0Regs vb;
+    PF::pass0_compute(loadb, vb);
+    PF::pass0_store(W0, vb);
+    __syncthreads();
+    PF::pass1(W0, W1, TWs);
+    __syncthreads();
+    auto keep = [&](float2 (&a)[PF::R2]) {
+#pragma unroll
+      for (int r = 0; r < PF::R2; ++r) kb[r] = a[Dft<PF::R2>::pos(r)];
+    };
+    PF::pass2_all(W1, tl, keep);
+    __syncthreads();  // W0 / W1 are reused by the first plane
+  }
   const float2* src = reinterpret_cast<const float2*>(T2 + size_t(b) * g.Pw);
   auto load = [&](int, int n, int gi) -> float2 { return c_conj(__ldg(src + 2 * n + gi)); };
   typename PF::P0Regs v;
@@ -721,7 +945,7 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
       const int x = j + r * PF::NB2 - g.off;
       if (x < 0 || x >= g.W) continue;
       const size_t i = size_t(y) * g.W + x;
-      float2 v = c_scale(c_conj(a[Dft<PF::R2>::pos(r)]), scale);
+      float2 v = c_scale(c_add(c_conj(a[Dft<PF::R2>::pos(r)]), kb[r]), scale);
       if (real2) v = make_float2(2.f * v.x, 0.f);  // Hermitian half-band: out = 2 Re
       OutOps<TO>::put(out, i, v, accumulate != 0, dc_term(dcs, i, dcr, dci));
     }
@@ -809,7 +1033,7 @@ TailSplit tail_split(int units, int per_sm, int nb) {
   }();
   const int slots = sms * per_sm;
   const int full = units / slots * slots, rem = units - full;
-  if (off || rem == 0 || full == 0 || nb < 4) return {units, units, 1};
+  if (off || rem == 0 || full == 0 || nb < 4) return {units, units, 1, slots};
   int best = 1;
   long best_cost = long(nb) + 1;
   for (int s = 2; s <= nb / 2; ++s) {
@@ -820,7 +1044,7 @@ TailSplit tail_split(int units, int per_sm, int nb) {
       best = s;
     }
   }
-  return {full + rem * best, full, best};
+  return {full + rem * best, full, best, slots};
 }
 
 void launch_rows_inv_steer_pair(const Geo& g, const float2* T2, const Bands& b, int half,
@@ -900,11 +1124,14 @@ void launch_rows_fwd_premul_pair(const Geo& g, const SigSrc& s, const double* ba
   case LL: {                                                                                \
     using PF = typename S1Plan<IlvFft<LL, R0, R1, R2, PP>>::type;                           \
     const PairTw tw = pair_tables<PF>();                                                    \
-    /* no tail split: config 4's 3.5 waves measured 0.306 ms split, 0.297 ms not */         \
+    /* tail split only under two waves (config 2: 512 row pairs on 444 slots); config 4's  \
+       3.5 waves measured 0.306 ms split, 0.297 ms not */                                   \
     const int rows2 = g.Hx2 / 2;                                                            \
+    TailSplit ts = tail_split(rows2, S1Occ<PF>::kMinB, b.n);                                \
+    if (rows2 >= 2 * ts.slots) ts = TailSplit{rows2, rows2, 1, ts.slots};                   \
     set_smem(k_rows_fwd_premul_ilv<PF>, sm);                                                \
-    k_rows_fwd_premul_ilv<PF><<<rows2, PF::T, sm, st>>>(g, s, base, b, T1, tw.mid, tw.last,  \
-                                                        rows2, 1);                          \
+    k_rows_fwd_premul_ilv<PF><<<ts.grid, PF::T, sm, st>>>(g, s, base, b, T1, tw.mid,        \
+                                                          tw.last, ts.full, ts.split);      \
     break;                                                                                  \
   }
   XCB_PAIR_DISPATCH(g.Pw, XCB_BODY)
@@ -924,6 +1151,27 @@ void launch_cols_fwd_mac_inv_pair(const Geo& g, const float2* T1, const float2* 
     k_cols_fwd_mac_ilv<PF><<<g.Pw / 2, PF::T, sm, st>>>(                                    \
         g, reinterpret_cast<const float4*>(T1), reinterpret_cast<const float4*>(Fhat),      \
         sstride / 2, b, half0, T2, tw.mid, tw.last);                                        \
+    break;                                                                                  \
+  }
+  XCB_PAIR_DISPATCH(g.Ph, XCB_BODY)
+#undef XCB_BODY
+  ++lc.n;
+}
+
+void launch_cols_fwd_mac_inv_cpair(const Geo& g, const float2* T1, const float2* Fhat,
+                                   const float2* Ghat, size_t sstride, const Bands& b,
+                                   const int* gspec, float2* T2, size_t t2plane,
+                                   cudaStream_t st, LaunchCounter& lc) {
+  const size_t sm = pair_smem(4, g.Ph, g);
+#define XCB_BODY(LL, R0, R1, R2, PP)                                                         \
+  case LL: {                                                                                \
+    using PF = IlvFft<LL, R0, R1, R2, PP>;                                                  \
+    const PairTw tw = pair_tables<PF>();                                                    \
+    set_smem(k_cols_fwd_mac_cpair_ilv<PF>, sm);                                             \
+    k_cols_fwd_mac_cpair_ilv<PF><<<g.Pw / 2, PF::T, sm, st>>>(                              \
+        g, reinterpret_cast<const float4*>(T1), reinterpret_cast<const float4*>(Fhat),      \
+        reinterpret_cast<const float4*>(Ghat), sstride / 2, b, gspec, T2, t2plane, tw.mid,  \
+        tw.last);                                                                           \
     break;                                                                                  \
   }
   XCB_PAIR_DISPATCH(g.Ph, XCB_BODY)
@@ -966,10 +1214,11 @@ void launch_cols_fwd_pair(const Geo& g, const float2* T1, float2* spec, cudaStre
 
 void launch_rows_inv_out_pair(const Geo& g, const float2* T2, int out_kind, void* out,
                               int accumulate, int real2, const SigSrc& dcs, double dcr,
-                              double dci, cudaStream_t st, LaunchCounter& lc) {
+                              double dci, cudaStream_t st, LaunchCounter& lc, const float2* T2b) {
   const size_t sm = pair_smem(7, g.Pw, g);
   const float scale = float(1.0 / (double(g.Ph) * double(g.Pw)));
   const float4* t2 = reinterpret_cast<const float4*>(T2);
+  const float4* t2b = reinterpret_cast<const float4*>(T2b);
 #define XCB_BODY(LL, R0, R1, R2, PP)                                                         \
   case LL: {                                                                                \
     using PF = IlvFft<LL, R0, R1, R2, PP>;                                                  \
@@ -977,14 +1226,13 @@ void launch_rows_inv_out_pair(const Geo& g, const float2* T2, int out_kind, void
     if (out_kind == OUT_C64) {                                                              \
       set_smem(k_rows_inv_out_ilv<PF, float2>, sm);                                         \
       k_rows_inv_out_ilv<PF, float2><<<g.H2 / 2, PF::T, sm, st>>>(                          \
-          g, t2, static_cast<float2*>(out), accumulate, real2, dcs, dcr, dci, scale, tw.mid, \
-          tw.last);                                                                         \
+          g, t2, t2b, static_cast<float2*>(out), accumulate, real2, dcs, dcr, dci, scale,   \
+          tw.mid, tw.last);                                                                 \
     } else {                                                                                \
       set_smem(k_rows_inv_out_ilv<PF, double2>, sm);                                        \
       k_rows_inv_out_ilv<PF, double2><<<g.H2 / 2, PF::T, sm, st>>>(                         \
-          g, t2, static_cast<double2*>(out), accumulate, real2, dcs, dcr, dci, scale,       \
-          tw.mid,                                                                           \
-          tw.last);                                                                         \
+          g, t2, t2b, static_cast<double2*>(out), accumulate, real2, dcs, dcr, dci, scale,  \
+          tw.mid, tw.last);                                                                 \
     }                                                                                       \
     break;                                                                                  \
   }

@@ -189,15 +189,30 @@ void launch_rows_fwd_premul_pair(const Geo& g, const SigSrc& s, const double* ba
 void launch_cols_fwd_mac_inv_pair(const Geo& g, const float2* T1, const float2* Fhat,
                                   size_t sstride, const Bands& b, int half0, float2* T2,
                                   cudaStream_t st, LaunchCounter& lc);
+// Conjugate band pairs (real signal, any filter): T1 holds the bands k >= 0
+// only, since H e^{+ik phi} = conj(H e^{-ik phi}).  Per band k the column FFT X
+// feeds two sums, A += X F^_k and (k > 0) B += X G_k with G_k the spectrum of
+// conj(f_{-k}) (plane gspec[bi] of Ghat, launch_spec_conj_reflect); both are
+// inverse transformed into T2 and T2 + t2plane, and S4 writes a + conj(b).
+void launch_cols_fwd_mac_inv_cpair(const Geo& g, const float2* T1, const float2* Fhat,
+                                   const float2* Ghat, size_t sstride, const Bands& b,
+                                   const int* gspec, float2* T2, size_t t2plane,
+                                   cudaStream_t st, LaunchCounter& lc);
+// G_i[v, u] = conj(F^_i[-v, -u]) for nb spectra in layout B: the spectrum of
+// the conjugated filter component
+void launch_spec_conj_reflect(const float2* Fhat, float2* Ghat, int nb, int Ph, int Pw,
+                              cudaStream_t st, LaunchCounter& lc);
 // single transforms on the pair engine: F1 (stage 5), F2 (6), S4 (7)
 void launch_rows_fwd_pair(const Geo& g, const SigSrc& s, float2* T1, cudaStream_t st,
                           LaunchCounter& lc);
 void launch_cols_fwd_pair(const Geo& g, const float2* T1, float2* spec, cudaStream_t st,
                           LaunchCounter& lc);
 // real2: out = 2 Re(IFFT) (+ dc H), the Hermitian half-band scatter
+// T2b (conjugate band pairs, else nullptr): out = IFFT(T2) + conj(IFFT(T2b))
 void launch_rows_inv_out_pair(const Geo& g, const float2* T2, int out_kind, void* out,
                               int accumulate, int real2, const SigSrc& dcs, double dcr,
-                              double dci, cudaStream_t st, LaunchCounter& lc);
+                              double dci, cudaStream_t st, LaunchCounter& lc,
+                              const float2* T2b = nullptr);
 // planes stage (angle max) on the interleaved engine; stage 2 of pair_smem
 void launch_rows_inv_planes_pair(const Geo& g, const float2* T2, int nbands, float2* planes,
                                  cudaStream_t st, LaunchCounter& lc);

@@ -76,6 +76,7 @@ PairTw pair_tables() {
 // chunks (k_pair.cu tail_split)
 struct TailSplit {
   int grid, full, split;
+  int slots = 0;  // resident CTAs of the device (SMs * per_sm)
 };
 TailSplit tail_split(int units, int per_sm, int nb);
 

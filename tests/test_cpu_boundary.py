@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert sorted(N.EXPORTS) == syms
-    assert N.lib().xc_abi_version() == 1
+    assert N.lib().xc_abi_version() == 2
 
 
 def test_decomposition_matches_oracle(orc):
