@@ -2443,9 +2443,37 @@ std::pair<int, int> shard_range(int n, int r, int world) {
   return {int((long long)n * r / world), int((long long)n * (r + 1) / world)};
 }
 
-std::vector<int> shard_bands(const std::vector<int>& ks, int r, int world) {
-  const auto ab = shard_range(int(ks.size()), r, world);
-  return std::vector<int>(ks.begin() + ab.first, ks.begin() + ab.second);
+// pairs (shard_in_pairs): the bands k >= 0 are split in contiguous ranges and
+// each rank takes its k and -k, so its share stays symmetric
+std::vector<int> shard_bands(const std::vector<int>& ks, int r, int world, bool pairs = false) {
+  if (!pairs) {
+    const auto ab = shard_range(int(ks.size()), r, world);
+    return std::vector<int>(ks.begin() + ab.first, ks.begin() + ab.second);
+  }
+  std::vector<int> nn;
+  for (int k : ks)
+    if (k >= 0) nn.push_back(k);
+  const auto ab = shard_range(int(nn.size()), r, world);
+  std::vector<int> mine;
+  for (int k : ks)
+    if (std::find(nn.begin() + ab.first, nn.begin() + ab.second, k < 0 ? -k : k) !=
+        nn.begin() + ab.second)
+      mine.push_back(k);
+  return mine;
+}
+
+// Real signals run symmetric band selections in +-k pairs, transforming the
+// bands k >= 0 only (the Hermitian half-band mode when F_{-k} = conj F_k; the
+// scatter's conjugate band pairs for any filter), so a device's share must
+// hold whole pairs and the load is the number of its bands k >= 0.
+bool shard_in_pairs(xc_filter f, int mode, const xc_image_desc* d, const std::vector<int>& ks) {
+  if (d->signal_dtype != XC_F32 && d->signal_dtype != XC_F64) return false;
+  const bool herm = use_herm() && f->hf.hermitian();
+  if (!(herm || (mode == XC_CONVOLUTION && use_cpair()))) return false;
+  for (int k : ks)
+    if (std::count(ks.begin(), ks.end(), -k) != 1 || std::count(ks.begin(), ks.end(), k) != 1)
+      return false;
+  return true;
 }
 
 // error of a worker thread, rethrown on the calling thread in device order
@@ -2604,6 +2632,7 @@ void run_group(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d,
   if (d->height < 1 || d->width < 1 || d->batch < 1)
     throw std::invalid_argument("image dims must be positive");
   const std::vector<int> ks = plan_components(f->hf, components, n_components);
+  const bool pairs = shard_in_pairs(f, mode, d, ks);
   const bool accumulate = (flags & XC_FLAG_ACCUMULATE) != 0;
   if (accumulate && d->memory != XC_DEVICE)
     throw std::invalid_argument("XC_FLAG_ACCUMULATE needs device memory");
@@ -2626,7 +2655,7 @@ void run_group(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d,
     const int s = G.slot;
     G.slot ^= 1;
     ck(cudaEventSynchronize(G.done[s]), "previous reduce");
-    const std::vector<int> mine = shard_bands(ks, G.rank, G.nranks);
+    const std::vector<int> mine = shard_bands(ks, G.rank, G.nranks, pairs);
     void* part = ctx->buf<char>("grp_part" + std::to_string(s), bytes);
     xc_stats st{};
     if (mine.empty()) {
@@ -2656,7 +2685,7 @@ void run_group(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d,
 
   if (G.rank_mode) {  // one process per GPU: this rank's bands, then ncclReduce to rank 0
     ck(cudaSetDevice(ctx->device), "cudaSetDevice");
-    const std::vector<int> mine = shard_bands(ks, G.rank, G.nranks);
+    const std::vector<int> mine = shard_bands(ks, G.rank, G.nranks, pairs);
     void* part = ctx->buf<char>("grp_part", bytes);
     xc_stats st{};
     if (mine.empty())
@@ -2712,7 +2741,7 @@ void run_group(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d,
     xc_context k = G.kids[i];
     std::lock_guard<std::mutex> lk(k->mu);
     ck(cudaSetDevice(k->device), "cudaSetDevice");
-    const std::vector<int> mine = shard_bands(ks, i, n);
+    const std::vector<int> mine = shard_bands(ks, i, n, pairs);
     const bool direct = i == 0 && d->memory == XC_DEVICE && !accumulate;
     void* part = direct ? out : k->buf<char>("grp_part", bytes);
     parts[i] = part;

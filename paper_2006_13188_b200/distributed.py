@@ -32,10 +32,31 @@ def band_ranges(n: int, world: int):
     return [(r * n // world, (r + 1) * n // world) for r in range(world)]
 
 
-def shard_components(ks, rank: int, world: int) -> list:
+def shard_components(ks, rank: int, world: int, pairs: bool = False) -> list:
+    """This rank's bands: a contiguous range of `ks`, or (pairs, see
+    shard_in_pairs) a contiguous range of the bands k >= 0 with their -k
+    partners, so that the share stays symmetric."""
     ks = [int(k) for k in ks]
-    a, b = band_ranges(len(ks), world)[rank]
-    return ks[a:b]
+    if not pairs:
+        a, b = band_ranges(len(ks), world)[rank]
+        return ks[a:b]
+    nn = [k for k in ks if k >= 0]
+    a, b = band_ranges(len(nn), world)[rank]
+    mine = set(nn[a:b])
+    return [k for k in ks if abs(k) in mine]
+
+
+def shard_in_pairs(mode, H, F, ks) -> bool:
+    """Mirror of the library's rule (api.cu shard_in_pairs): a real signal with a
+    symmetric band selection runs in +-k pairs, transforming the bands k >= 0
+    only (Hermitian half-band mode for a real filter, the scatter's conjugate
+    band pairs for any filter), so shares must hold whole pairs."""
+    if np.iscomplexobj(np.asarray(getattr(H, "values", H))):
+        return False
+    ks = [int(k) for k in ks]
+    if any(ks.count(-k) != 1 or ks.count(k) != 1 for k in ks):
+        return False
+    return int(mode) == int(XMode.convolution) or F.hermitian()
 
 
 def batch_range(batch: int, rank: int, world: int) -> range:
@@ -118,7 +139,7 @@ def xfast_band_sharded(mode: XMode, H, T: XformField, F: FreqFilter2,
     ks = list(plan.components) or [int(k) for k in F.ks]
     if world > len(ks):
         raise ValueError("band sharding needs at least one band per rank")
-    mine = shard_components(ks, rank, world)
+    mine = shard_components(ks, rank, world, shard_in_pairs(mode, H, F, ks))
     inner_dc = rank == root  # add the scale inner-DC term exactly once
     part = compute(int(mode), H, T, F, mine, inner_dc)
     total = _reduce_complex(part, root, group, device)
@@ -145,15 +166,17 @@ def smooth_band_sharded(H, T: XformField, F: FreqFilter2, normalize_signal: bool
     dist = _dist()
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     _check_integral(F)  # engine.hpp:388-392, on every rank before any collective
-    Hs = np.asarray(H, np.complex128)
-    ones = np.ones(Hs.shape, np.complex128)
+    # a real image stays real: both scatters then run in conjugate band pairs
+    Hs = np.asarray(getattr(H, "values", H))
+    Hs = Hs.astype(np.complex128 if np.iscomplexobj(Hs) else np.float64)
+    ones = np.ones(Hs.shape, Hs.dtype)
     if normalize_signal and T.kind == XformKind.scale2:  # engine.hpp:396-401
         inv = 1.0 / np.asarray(T.values, np.float64) ** 2
         Hs, ones = Hs * inv, ones * inv
     ks = [int(k) for k in F.ks]
     if world > len(ks):
         raise ValueError("band sharding needs at least one band per rank")
-    mine = shard_components(ks, rank, world)
+    mine = shard_components(ks, rank, world, shard_in_pairs(XMode.convolution, Hs, F, ks))
     inner_dc = rank == root
     num = compute(int(XMode.convolution), Hs, T, F, mine, inner_dc)
     den = compute(int(XMode.convolution), ones, T, F, mine, inner_dc)

@@ -124,6 +124,18 @@ class FreqFilter2:
     def omega(self) -> float:
         return 2.0 * math.pi / self.log_period()
 
+    def hermitian(self) -> bool:
+        """F_{-k} = conj(F_k) for every retained band (a real filter): the test the
+        library applies before its Hermitian half-band mode (host_filter.cpp)."""
+        tol = 1e-12 * max(float(np.abs(self.comps).max(initial=0.0)), 1e-300)
+        for ci, k in enumerate(self.ks):
+            hits = np.nonzero(self.ks == -k)[0]
+            if len(hits) == 0:
+                return False
+            if np.abs(self.comps[:, hits[-1]] - np.conj(self.comps[:, ci])).max(initial=0.0) > tol:
+                return False
+        return True
+
     def handle(self, ctx: N.Context | None = None):
         """The xc_filter handle (host object; device spectra are cached in it)."""
         h = self._handles.get(0)

@@ -191,3 +191,47 @@ def test_spatial_sharded_anglemax_and_peaks_gloo(orc, world):
         assert len(got) == len(ref) >= 2
         assert [(x, y) for x, y, _ in got] == [(x, y) for x, y, _ in ref]
         assert np.allclose([v for _, _, v in got], [v for _, _, v in ref], rtol=1e-12, atol=0)
+
+
+# ------------------------------------------------- pair-aware band sharding
+
+def test_shard_components_in_pairs_covers_and_stays_symmetric():
+    """Real signals run +-k pairs (only k >= 0 is transformed), so every rank's
+    share must be symmetric, the shares disjoint, and the loads (bands k >= 0)
+    balanced to +-1 (api.cu shard_bands / shard_in_pairs)."""
+    from paper_2006_13188_b200 import distributed as D
+    ks = list(range(-32, 33))
+    for world in (1, 2, 3, 4, 8):
+        shares = [D.shard_components(ks, r, world, pairs=True) for r in range(world)]
+        assert sorted(k for s in shares for k in s) == ks
+        loads = []
+        for s in shares:
+            assert all(-k in s for k in s)
+            loads.append(sum(1 for k in s if k >= 0))
+        assert max(loads) - min(loads) <= 1
+    # more ranks than non-negative bands: the extra ranks get nothing
+    shares = [D.shard_components([-1, 0, 1], r, 4, pairs=True) for r in range(4)]
+    assert sorted(k for s in shares for k in s) == [-1, 0, 1]
+    # contiguous ranges by default
+    assert D.shard_components(ks, 0, 8) == list(range(-32, -24))
+
+
+def test_shard_in_pairs_rule():
+    import paper_2006_13188_b200 as X
+    from paper_2006_13188_b200 import distributed as D
+    from paper_2006_13188_b200.engine import XMode
+    ks = np.arange(-2, 3)
+    r = np.random.default_rng(3)
+    comps = r.normal(size=(6, 5)) + 1j * r.normal(size=(6, 5))
+    F = X.FreqFilter2(0, 4, ks, comps, 6, 16, 5.0)
+    assert not F.hermitian()
+    herm = comps.copy()
+    herm[:, 0], herm[:, 1], herm[:, 2] = np.conj(comps[:, 4]), np.conj(comps[:, 3]), comps[:, 2].real
+    FH = X.FreqFilter2(0, 4, ks, herm, 6, 16, 5.0)
+    assert FH.hermitian()
+    real, cplx = np.zeros((4, 4), np.float32), np.zeros((4, 4), np.complex64)
+    assert D.shard_in_pairs(XMode.convolution, real, F, ks)       # conjugate band pairs
+    assert not D.shard_in_pairs(XMode.correlation, real, F, ks)   # gather needs F_-k = conj F_k
+    assert D.shard_in_pairs(XMode.correlation, real, FH, ks)      # Hermitian half-band
+    assert not D.shard_in_pairs(XMode.convolution, cplx, F, ks)   # complex signal
+    assert not D.shard_in_pairs(XMode.convolution, real, F, [2, 1, 0, -1])  # asymmetric
