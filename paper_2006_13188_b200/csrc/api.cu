@@ -2414,6 +2414,9 @@ struct Group {
   std::vector<xc_context> kids;   // single-process: one child context per device
   std::vector<ncclComm_t> comms;  // one per kid, or the rank's one; empty = peer reduce
   bool rank_mode = false;
+  // every kid's device can store into kids[0]'s memory (same device or peer
+  // access over NVLink): partials are written straight into the root (peer_slots)
+  bool peer_write = false;
   int rank = 0, nranks = 1;
   int shard = XC_SHARD_BANDS;
   // XC_FLAG_ASYNC (rank contexts): the reduce of call i runs on `comm` while
@@ -2555,6 +2558,45 @@ void reduce_to_root(Group& G, const std::vector<void*>& bufs, size_t count, bool
     ck(cudaGetLastError(), "kernel launch");
   }
   ck(cudaStreamSynchronize(root->stream), "peer reduce");
+}
+
+// XCB_PEER_WRITE=0: partials stay on their devices and are reduced by NCCL (or
+// the peer-copy reduce) instead of being written into the root's memory
+bool use_peer_write() {
+  static const bool on = [] {
+    const char* e = std::getenv("XCB_PEER_WRITE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// Fused partial delivery (single-process multi-device contexts).  The last
+// kernel of a device's share (I2's steering sum, S4, the smoothing scatters)
+// takes its output pointer from here: slot i - 1 of a buffer in the ROOT's
+// memory, so its stores go over NVLink as the rows are produced and overlap
+// the transforms still running; no partial is staged locally and no separate
+// collective moves it.  The root then adds the slots in device order
+// (sum_peer_slots).  Returns nullptr when the topology has no peer access
+// (reduce_to_root then runs NCCL).
+char* peer_slots(Group& G, const char* name, size_t bytes) {
+  const int n = int(G.kids.size());
+  if (n <= 1 || !G.peer_write || !use_peer_write()) return nullptr;
+  xc_context root = G.kids[0];
+  std::lock_guard<std::mutex> lk(root->mu);
+  ck(cudaSetDevice(root->device), "cudaSetDevice");
+  return root->buf<char>(name, size_t(n - 1) * bytes);
+}
+
+// parts[0] += slot 0 + slot 1 + ... (one kernel on the root; every kid's run
+// has synchronized its stream, so its remote stores are complete)
+void sum_peer_slots(Group& G, void* part0, const char* slots, size_t count, bool f64,
+                    xcb::LaunchCounter& lc) {
+  xc_context root = G.kids[0];
+  ck(cudaSetDevice(root->device), "cudaSetDevice");
+  xcb::launch_sum_slots(part0, slots, count, int(G.kids.size()) - 1, count, f64 ? 1 : 0,
+                        root->stream, lc);
+  ck(cudaGetLastError(), "kernel launch");
+  ck(cudaStreamSynchronize(root->stream), "peer slot sum");
 }
 
 // Inputs of images [a, b) on kid k: the caller's pointers when they are host
@@ -2737,13 +2779,16 @@ void run_group(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d,
 
   // band sharding: every device runs its band range (empty ranges add zeros)
   std::vector<void*> parts(static_cast<size_t>(n), nullptr);
+  char* slots = peer_slots(G, "grp_slots", bytes);
   for_each_kid(n, [&](int i) {
     xc_context k = G.kids[i];
     std::lock_guard<std::mutex> lk(k->mu);
     ck(cudaSetDevice(k->device), "cudaSetDevice");
     const std::vector<int> mine = shard_bands(ks, i, n, pairs);
     const bool direct = i == 0 && d->memory == XC_DEVICE && !accumulate;
-    void* part = direct ? out : k->buf<char>("grp_part", bytes);
+    void* part = direct             ? out
+                 : (slots && i > 0) ? static_cast<void*>(slots + size_t(i - 1) * bytes)
+                                    : k->buf<char>("grp_part", bytes);
     parts[i] = part;
     if (mine.empty()) {
       ck(cudaMemsetAsync(part, 0, bytes, k->stream), "memset");
@@ -2757,7 +2802,10 @@ void run_group(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d,
     run_single(k, f, mode, &di, sg, pr, mine.data(), int(mine.size()),
                kid_flags | (i ? XC_FLAG_NO_INNER_DC : 0u), part, &st[i], true);
   });
-  reduce_to_root(G, parts, bytes / (f64 ? 8 : 4), f64);
+  if (slots)
+    sum_peer_slots(G, parts[0], slots, bytes / (f64 ? 8 : 4), f64, lc);
+  else
+    reduce_to_root(G, parts, bytes / (f64 ? 8 : 4), f64);
   deliver(G.kids[0], *d, parts[0], out, bytes, accumulate, f64, lc);
   st[0].gpu_launches += lc.n;
   merge_stats(stats, st, (long long)ks.size(), since(t_start));
@@ -2796,6 +2844,8 @@ void smooth_group(xc_context ctx, xc_filter f, const xc_image_desc* d, const voi
   const size_t npix = size_t(d->height) * d->width;
   const size_t count = 4 * npix * size_t(d->batch);  // floats of numden
   const std::vector<int>& all = f->hf.ks;
+  // num and den are scatters of real fields when the signal is real
+  const bool pairs = shard_in_pairs(f, XC_CONVOLUTION, d, all);
   const bool scale = f->hf.group == XC_SCALE2;
   auto no_op = [](Call&, int) {};
   auto part_stats = [](const SmoothPart& p) {
@@ -2810,7 +2860,7 @@ void smooth_group(xc_context ctx, xc_filter f, const xc_image_desc* d, const voi
 
   if (G.rank_mode) {
     ck(cudaSetDevice(ctx->device), "cudaSetDevice");
-    const std::vector<int> mine = shard_bands(all, G.rank, G.nranks);
+    const std::vector<int> mine = shard_bands(all, G.rank, G.nranks, pairs);
     float2* nd = ctx->buf<float2>("grp_numden", count / 2);
     xc_stats st{};
     if (mine.empty())
@@ -2859,11 +2909,12 @@ void smooth_group(xc_context ctx, xc_filter f, const xc_image_desc* d, const voi
   }
 
   std::vector<void*> parts(static_cast<size_t>(n), nullptr);
+  char* slots = peer_slots(G, "grp_nd_slots", count * 4);
   for_each_kid(n, [&](int i) {
     xc_context k = G.kids[i];
     std::lock_guard<std::mutex> lk(k->mu);
     ck(cudaSetDevice(k->device), "cudaSetDevice");
-    const std::vector<int> mine = shard_bands(all, i, n);
+    const std::vector<int> mine = shard_bands(all, i, n, pairs);
     float2* nd = k->buf<float2>("grp_numden", count / 2);
     parts[i] = nd;
     if (mine.empty()) {
@@ -2934,6 +2985,12 @@ int xc_context_create_multi(int n_dev, const int* dev_ids, xc_context* out) {
           }
         }
       cudaSetDevice(dev_ids[0]);
+    }
+    G->peer_write = true;  // kid i stores its partial into kids[0]'s memory
+    for (int i = 1; i < n_dev; ++i) {
+      int can = dev_ids[i] == dev_ids[0];
+      if (!can) cudaDeviceCanAccessPeer(&can, dev_ids[i], dev_ids[0]);
+      G->peer_write = G->peer_write && can;
     }
     *out = guard.release();
   });

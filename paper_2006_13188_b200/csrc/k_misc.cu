@@ -442,6 +442,38 @@ void launch_accumulate(void* dst, const void* src, size_t n, int f64, cudaStream
   ++lc.n;
 }
 
+// dst += slots[0] + slots[1] + ... in slot order (the order of the sequential
+// accumulate, so both reduces give the same bits); slots `stride` elements apart
+template <class T>
+__global__ void k_sum_slots(T* __restrict__ dst, const T* __restrict__ slots, size_t stride,
+                            int ns, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    T a = dst[i];
+    for (int s = 0; s < ns; ++s) {
+      const T b = slots[size_t(s) * stride + i];
+      a.x += b.x;
+      a.y += b.y;
+    }
+    dst[i] = a;
+  }
+}
+
+void launch_sum_slots(void* dst, const void* slots, size_t stride, int ns, size_t n, int f64,
+                      cudaStream_t st, LaunchCounter& lc) {
+  // n, stride: scalar counts (even: complex or (num, den) pairs)
+  const int g = grid_for(n / 2, 256);
+  if (f64)
+    k_sum_slots<double2><<<g, 256, 0, st>>>(static_cast<double2*>(dst),
+                                            static_cast<const double2*>(slots), stride / 2, ns,
+                                            n / 2);
+  else
+    k_sum_slots<float2><<<g, 256, 0, st>>>(static_cast<float2*>(dst),
+                                           static_cast<const float2*>(slots), stride / 2, ns,
+                                           n / 2);
+  ++lc.n;
+}
+
 void launch_absmax(const float* x, size_t n, unsigned* bits, cudaStream_t st, LaunchCounter& lc) {
   // 4 CTAs per SM loop over the field: one atomic per CTA (float4 loads need
   // 16-byte alignment: the staged fields are cudaMalloc'd)

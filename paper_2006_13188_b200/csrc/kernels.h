@@ -266,6 +266,9 @@ namespace xcb {
 // partial sums of the multi-device band reduce without NCCL (peer copies).
 void launch_accumulate(void* dst, const void* src, size_t n, int f64, cudaStream_t st,
                        LaunchCounter& lc);
+// dst += slots[0] + ... + slots[ns - 1] in slot order; n, stride in scalars (even)
+void launch_sum_slots(void* dst, const void* slots, size_t stride, int ns, size_t n, int f64,
+                      cudaStream_t st, LaunchCounter& lc);
 }  // namespace xcb
 
 namespace xcb {

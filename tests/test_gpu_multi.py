@@ -205,3 +205,45 @@ def test_multi_pair_sharding_real_signal(orc, devices, real_filter):
         ref = orc.spectral_oracle_at(mode, H, 0, T, ofilter(orc, F), ys, xs)
         assert res.standard_ops == 11
         assert orc.rel_l2(res.output[ys, xs], ref) < TOL
+
+
+_PEER_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2006_13188_b200 as X
+from paper_2006_13188_b200 import _native as N
+r = np.random.default_rng(5)
+from paper_2006_13188_b200 import workloads as WL
+F = X.decompose_rotation2(WL.angular_filter(6, 2.5, 4, r), 6, 6, 8, 12, 20, 6.0)
+H = r.uniform(0, 1, (2, 70, 90)).astype(np.float32)
+T = r.uniform(0, 6.28, (2, 70, 90)).astype(np.float32)
+ctx = N.Context.multi([0, 0, 0])
+a = X.xcorr_fast(H, X.XformField.rotation(T), F, ctx=ctx).output
+b = X.xconv_fast(H, X.XformField.rotation(T), F, ctx=ctx).output
+FS = X.decompose_scale2(np.exp(-((np.mgrid[-6:7, -6:7] ** 2).sum(0)) / 18.0) + 0j, 6, 6, 6, 32, 24, 1.0, 6)
+S = np.exp(r.uniform(0, 0.4, (70, 90))).astype(np.float32)
+c = X.smooth_adaptive(H[0], X.XformField.scaling(S), FS, device=ctx).output
+np.savez(sys.argv[2], a=a, b=b, c=c)
+"""
+
+
+def test_peer_write_partials_equal_the_copy_reduce(tmp_path):
+    """Multi-device contexts write every device's partial straight into the
+    root's memory (api.cu peer_slots) and add the slots in device order; with
+    XCB_PEER_WRITE=0 the partials stay local and go through the reduce.  Both
+    add in the same order, so the outputs are bit-identical (gather, scatter,
+    smoothing; batches)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("1", "0"):
+        f = tmp_path / f"pw{flag}.npz"
+        env = dict(os.environ, XCB_PEER_WRITE=flag)
+        subprocess.run([sys.executable, "-c", _PEER_SCRIPT, root, str(f)], check=True, env=env,
+                       timeout=600)
+        outs.append(np.load(f))
+    for k in ("a", "b", "c"):
+        assert np.isfinite(outs[0][k]).all()
+        assert np.array_equal(outs[0][k], outs[1][k]), k
