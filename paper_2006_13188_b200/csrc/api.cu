@@ -390,7 +390,14 @@ float2* filter_spectra_conj(Call& c) {
   float2* spec = nullptr;
   ck(cudaMalloc(&spec, size_t(nb) * c.g.Ph * c.g.Pw * sizeof(float2)), "cudaMalloc spectra");
   xcb::launch_spec_conj_reflect(c.Fhat, spec, nb, c.g.Ph, c.g.Pw, c.st, c.lc);
-  ck(cudaGetLastError(), "conjugated spectra launch");
+  // complete before the entry is published: another context (its own stream)
+  // may find it in the shared filter's cache right after
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c.st);
+  if (e != cudaSuccess) {
+    cudaFree(spec);
+    ck(e, "conjugated spectra");
+  }
   c.f->spectra[key] = spec;
   return spec;
 }
@@ -430,6 +437,45 @@ int pick_pad_uncached(int n) {
   return L0;
 }
 
+bool use_pair();
+
+// Pad of a 2D pipeline axis needing >= n points.  The three kernel families
+// cost very different amounts per transformed point: measured with
+// tools/pad_sweep.py (17 bands, device-resident), per point of the padded
+// grid, the pair engine (k_pair.cu) 1.0, the fast kernels (k_fast.cu) ~1.6,
+// the generic kernels ~8 (xconv 800^2 at pad 810: 0.555 ms; 900^2 at pad
+// 1152: 0.128 ms).  Per axis that is 1 / 1.25 / 2.8, so the pad is the
+// candidate (smallest generic length, every fast length, every pair length)
+// with the least length x weight.  XCB_PAD_RULE=0 keeps pick_pad's choice.
+int pick_pad2d(int n) {
+  static const bool on = [] {
+    const char* e = std::getenv("XCB_PAD_RULE");
+    return !(e && e[0] == '0');
+  }();
+  const int p = pick_pad(n);
+  if (!on || p < 0) return p;
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(n);
+  if (it != cache.end()) return it->second;
+  xcb::FftPlan tmp;
+  int best = p;
+  double cost = double(p) * (xcb::make_fast_plan(p, &tmp) ? 1.25 : 2.8);
+  auto consider = [&](int L, double w) {
+    if (L >= n && L % 2 == 0 && L * w < cost) {
+      cost = L * w;
+      best = L;
+    }
+  };
+#define XCB_PAD_FAST(LL, R0, R1, RL) consider(LL, 1.25);
+  XCB_FAST_TABLE(XCB_PAD_FAST)
+#undef XCB_PAD_FAST
+  if (use_pair())
+    for (int L : xcb::pair_plan_lengths()) consider(L, 1.0);
+  return cache[n] = best;
+}
+
 Call setup(xc_context ctx, xc_filter f, const xc_image_desc* d, int group_required,
            const int* components, int ncomp, bool periodic) {
   if (!ctx || !f || !d) throw std::invalid_argument("null argument");
@@ -460,8 +506,8 @@ Call setup(xc_context ctx, xc_filter f, const xc_image_desc* d, int group_requir
   g.off = periodic ? R : 0;
   // zero-padded linear filtering needs P >= extent + R and no wrap of the
   // 2R+1 taps (fft.hpp:85-86 uses next_fast_size(extent + 2R + 1))
-  g.Ph = pick_pad(std::max(g.Hx + R, 2 * R + 1));
-  g.Pw = pick_pad(std::max(g.Wx + R, 2 * R + 1));
+  g.Ph = pick_pad2d(std::max(g.Hx + R, 2 * R + 1));
+  g.Pw = pick_pad2d(std::max(g.Wx + R, 2 * R + 1));
   if (g.Ph < 0 || g.Pw < 0) throw std::invalid_argument("image too large for the FFT planner");
   while (g.Pw % 2) g.Pw = xcb::pick_fft_length(g.Pw + 1);
   c.prow = &ctx->plan(g.Pw);
@@ -874,9 +920,11 @@ void run_scatter(Call& c, const xcb::SigSrc& sig, const double* base, void* out,
   // and S2 feeds each into two sums (k_pair.cu k_cols_fwd_mac_cpair_ilv)
   const int* gspec = nullptr;
   const float2* Ghat = nullptr;
-  bool cpair = !half && use_cpair() && !sig.is_complex && !c.packed && use_pair() &&
-               xcb::pair_smem(3, g.Pw, g) && xcb::pair_smem(4, g.Ph, g) &&
-               xcb::pair_smem(7, g.Pw, g) && c.ks.size() > 1;
+  // S2 on the pair engine or the fast kernels; S1 and S4 on any engine
+  const bool s2_pair = use_pair() && xcb::pair_smem(4, g.Ph, g);
+  const bool s2_fast = !s2_pair && c.fcol && xcb::fast_smem(6, *c.fcol, g);
+  bool cpair = !half && use_cpair() && !sig.is_complex && !c.packed && (s2_pair || s2_fast) &&
+               c.ks.size() > 1;
   if (cpair) {
     std::vector<int> hk, hs, hg;
     for (size_t i = 0; i < c.ks.size() && cpair; ++i) {
@@ -919,8 +967,12 @@ void run_scatter(Call& c, const xcb::SigSrc& sig, const double* base, void* out,
   }
   if (cpair) {
     stage(c, "S2_cols_fwd_mac_inv", [&] {
-      xcb::launch_cols_fwd_mac_inv_cpair(g, T1, c.Fhat, Ghat, c.sstride, bands, gspec, T2, t2plane,
-                                         c.st, c.lc);
+      if (s2_pair)
+        xcb::launch_cols_fwd_mac_inv_cpair(g, T1, c.Fhat, Ghat, c.sstride, bands, gspec, T2,
+                                           t2plane, c.st, c.lc);
+      else
+        xcb::launch_cols_fwd_mac_inv_cpair_fast(*c.fcol, g, T1, c.Fhat, Ghat, c.sstride, bands,
+                                                gspec, T2, t2plane, c.st, c.lc);
     });
   } else if (use_pair() && xcb::pair_smem(4, g.Ph, g)) {
     stage(c, "S2_cols_fwd_mac_inv", [&] {
@@ -946,7 +998,7 @@ void run_scatter(Call& c, const xcb::SigSrc& sig, const double* base, void* out,
                                     cpair ? T2 + t2plane : nullptr);
     else
       xcb::launch_rows_inv_out(*c.prow, g, T2, out_kind, out, accumulate ? 1 : 0, sig, dcv.real(),
-                               dcv.imag(), c.st, c.lc);
+                               dcv.imag(), c.st, c.lc, cpair ? T2 + t2plane : nullptr);
   });
 }
 

@@ -349,18 +349,24 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
 }
 
 // ------------------------------------------------------------------ S2 fast
-template <class FF>
+// CP: conjugate band pairs (kernels.h launch_cols_fwd_mac_inv_cpair): the bands
+// are k >= 0 of a real signal; a second sum accB += X G_k (k > 0), G_k = plane
+// gspec[bi] of Gh staged beside F^_k, and a second inverse transform into
+// T2 + t2plane
+template <class FF, bool CP>
 __global__ void __launch_bounds__(kFastMaxThreads, 1)
     k_cols_fwd_mac_inv_fast(FftPlanD p, Geo g, const float2* __restrict__ T1,
-                            const float2* __restrict__ Fh, size_t sstride, Bands bl,
-                            float2* __restrict__ T2) {
+                            const float2* __restrict__ Fh, const float2* __restrict__ Gh,
+                            size_t sstride, Bands bl, const int* __restrict__ gspec,
+                            float2* __restrict__ T2, size_t t2plane) {
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) uint64_t barS, barF;
   constexpr int L = FF::L;  // = Ph
   const int sl = g.Hx2 > L ? g.Hx2 : L;
   float2* S = reinterpret_cast<float2*>(smraw);
   float2* SF = S + 2 * sl;
-  float2* W = SF + 2 * L;
+  float2* SG = SF + 2 * L;  // CP only
+  float2* W = SF + (CP ? 4 : 2) * L;
   float2* TW = W + 2 * FF::Lp;
   FF::load_twiddles(TW, p.tw);
   const int c = blockIdx.x, tid = threadIdx.x;
@@ -374,16 +380,21 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
     fence_mbar_init();
     mbar_expect_tx(&barS, bytesS);
     bulk_copy(S, T1 + col1, bytesS, &barS);
-    mbar_expect_tx(&barF, bytesF);
+    const bool pb0 = CP && bl.k[0] != 0;
+    mbar_expect_tx(&barF, pb0 ? 2 * bytesF : bytesF);
     bulk_copy(SF, Fh + size_t(bl.spec[0]) * sstride + colF, bytesF, &barF);
+    if (pb0) bulk_copy(SG, Gh + size_t(gspec[0]) * sstride + colF, bytesF, &barF);
   }
   __syncthreads();
   constexpr int RL = FF::kLast;
-  float2 acc[RL];
+  float2 acc[RL], accB[CP ? RL : 1];
 #pragma unroll
   for (int r = 0; r < RL; ++r) acc[r] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int r = 0; r < (CP ? RL : 1); ++r) accB[r] = make_float2(0.f, 0.f);
   unsigned phS = 0, phF = 0;
   for (int bi = 0; bi < bl.n; ++bi) {
+    const bool pairb = CP && bl.k[bi] != 0;  // CTA-uniform
     mbar_wait(&barS, phS);
     phS ^= 1;
     auto load = [&](int n, int gi) -> float2 {
@@ -402,34 +413,45 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1)
     const int two = opaque(2);
     auto store = [&](int k, int gi, int r, float2 v) {
       acc[r] = c_add(acc[r], c_mul(v, SF[k * two + gi]));
+      if constexpr (CP) {
+        if (pairb) accB[r] = c_add(accB[r], c_mul(v, SG[k * two + gi]));
+      }
     };
     FF::last(TW, W, store);
     __syncthreads();
     if (tid == 0 && bi + 1 < bl.n) {
       fence_proxy_async();
-      mbar_expect_tx(&barF, bytesF);
+      const bool pb = CP && bl.k[bi + 1] != 0;
+      mbar_expect_tx(&barF, pb ? 2 * bytesF : bytesF);
       bulk_copy(SF, Fh + size_t(bl.spec[bi + 1]) * sstride + colF, bytesF, &barF);
+      if (pb) bulk_copy(SG, Gh + size_t(gspec[bi + 1]) * sstride + colF, bytesF, &barF);
     }
   }
-  // inverse column transform of the band sum: conj(acc) -> S -> FFT -> conj
-  {
-    const int nb = L / RL, w = tid;
-    if (w < nb * kG) {
-      const int gi = w & 1, j = w >> 1;
+  // inverse column transform of each band sum: conj(acc) -> S -> FFT -> conj
 #pragma unroll
-      for (int r = 0; r < RL; ++r) S[(j + r * nb) * 2 + gi] = c_conj(acc[r]);
+  for (int pl = 0; pl < (CP ? 2 : 1); ++pl) {
+    if (pl) __syncthreads();  // the first plane's last pass is done with W
+    {
+      const int nb = L / RL, w = tid;
+      if (w < nb * kG) {
+        const int gi = w & 1, j = w >> 1;
+#pragma unroll
+        for (int r = 0; r < RL; ++r)
+          S[(j + r * nb) * 2 + gi] = c_conj(CP && pl ? accB[r] : acc[r]);
+      }
     }
+    __syncthreads();
+    auto load = [&](int n, int gi) -> float2 { return S[n * 2 + gi]; };
+    FF::first(p, W, load);
+    __syncthreads();
+    FF::mid(TW, W);
+    float2* dst = T2 + size_t(pl) * t2plane;
+    auto store = [&](int k, int gi, int, float2 v) {
+      const int y = k - g.off;
+      if (y >= 0 && y < g.H) dst[(size_t(y >> 1) * g.Pw + 2 * c + gi) * 2 + (y & 1)] = c_conj(v);
+    };
+    FF::last(TW, W, store);
   }
-  __syncthreads();
-  auto load = [&](int n, int gi) -> float2 { return S[n * 2 + gi]; };
-  FF::first(p, W, load);
-  __syncthreads();
-  FF::mid(TW, W);
-  auto store = [&](int k, int gi, int, float2 v) {
-    const int y = k - g.off;
-    if (y >= 0 && y < g.H) T2[(size_t(y >> 1) * g.Pw + 2 * c + gi) * 2 + (y & 1)] = c_conj(v);
-  };
-  FF::last(TW, W, store);
 }
 
 constexpr size_t kSmemLimit = 232448;  // 227 KB opt-in per CTA on sm_100
@@ -447,6 +469,7 @@ size_t fast_smem(int stage, const FftPlan& pl, const Geo& g) {
     case 1: s = 2 * L * f2 + Wb + 2 * (g.W + 16) * f2; break;            // I2 (+ Z)
     case 2: s = Wb + 4 * (g.Wx + 16) * f2; break;                         // S1
     case 3: s = 2 * (g.Hx2 > int(L) ? g.Hx2 : L) * f2 + 2 * L * f2 + Wb; break;  // S2
+    case 6: s = 2 * (g.Hx2 > int(L) ? g.Hx2 : L) * f2 + 4 * L * f2 + Wb; break;  // S2, pairs
     case 4: s = 2 * L * f2 + Wb; break;                                   // planes
     case 5: s = Wb; break;                                                // F1 / F2
   }
@@ -578,8 +601,23 @@ void launch_cols_fwd_mac_inv_fast(const FftPlan& pc, const Geo& g, const float2*
                                   float2* T2, cudaStream_t st, LaunchCounter& lc) {
   const size_t sm = fast_smem(3, pc, g);
 #define XCB_FAST_BODY                                                                      \
-  set_smem(k_cols_fwd_mac_inv_fast<FF>, sm);                                               \
-  k_cols_fwd_mac_inv_fast<FF><<<g.Pw / 2, pc.d.nt, sm, st>>>(pc.d, g, T1, Fhat, sstride, b, T2)
+  set_smem(k_cols_fwd_mac_inv_fast<FF, false>, sm);                                        \
+  k_cols_fwd_mac_inv_fast<FF, false><<<g.Pw / 2, pc.d.nt, sm, st>>>(                       \
+      pc.d, g, T1, Fhat, nullptr, sstride, b, nullptr, T2, 0)
+  switch (pc.d.L) { XCB_FAST_TABLE(XCB_FAST_CASE) }
+#undef XCB_FAST_BODY
+  ++lc.n;
+}
+
+void launch_cols_fwd_mac_inv_cpair_fast(const FftPlan& pc, const Geo& g, const float2* T1,
+                                        const float2* Fhat, const float2* Ghat, size_t sstride,
+                                        const Bands& b, const int* gspec, float2* T2,
+                                        size_t t2plane, cudaStream_t st, LaunchCounter& lc) {
+  const size_t sm = fast_smem(6, pc, g);
+#define XCB_FAST_BODY                                                                      \
+  set_smem(k_cols_fwd_mac_inv_fast<FF, true>, sm);                                         \
+  k_cols_fwd_mac_inv_fast<FF, true><<<g.Pw / 2, pc.d.nt, sm, st>>>(                        \
+      pc.d, g, T1, Fhat, Ghat, sstride, b, gspec, T2, t2plane)
   switch (pc.d.L) { XCB_FAST_TABLE(XCB_FAST_CASE) }
 #undef XCB_FAST_BODY
   ++lc.n;

@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(kMaxThreads)
 template <class TO>
 __global__ void __launch_bounds__(kMaxThreads)
     k_rows_inv_out(FftPlanD p, Geo g, const float2* __restrict__ T2, TO* __restrict__ out,
-                   int accumulate, SigSrc dcs, double dcr, double dci, float scale) {
+                   int accumulate, int conjb, SigSrc dcs, double dcr, double dci, float scale) {
   extern __shared__ float2 sm[];
   const int b = blockIdx.x;
   const float2* src = T2 + size_t(b) * g.Pw * 2;
@@ -127,8 +127,13 @@ __global__ void __launch_bounds__(kMaxThreads)
     const int x = k - g.off, y = 2 * b + gi;
     if (x < 0 || x >= g.W || y >= g.H) return;
     const size_t i = size_t(y) * g.W + x;
-    OutOps<TO>::put(out, i, c_scale(c_conj(v), scale), accumulate != 0,
-                    dc_term(dcs, i, dcr, dci));
+    // conjb (second plane of the conjugate band pairs): out += conj(IFFT(T2)),
+    // i.e. the forward transform of conj(T2) without the final conjugation
+    if (conjb)
+      OutOps<TO>::put(out, i, c_scale(v, scale), true, make_float2(0.f, 0.f));
+    else
+      OutOps<TO>::put(out, i, c_scale(c_conj(v), scale), accumulate != 0,
+                      dc_term(dcs, i, dcr, dci));
   };
   fft_block(p, sm, load, store);
 }
@@ -181,18 +186,22 @@ void launch_cols_fwd_mac_inv(const FftPlan& pcol, const Geo& g, const float2* T1
 
 void launch_rows_inv_out(const FftPlan& prow, const Geo& g, const float2* T2, int out_kind,
                          void* out, int accumulate, const SigSrc& dcs, double dcr, double dci,
-                         cudaStream_t st, LaunchCounter& lc) {
+                         cudaStream_t st, LaunchCounter& lc, const float2* T2b) {
   const float scale = float(1.0 / (double(g.Ph) * double(g.Pw)));
-  if (out_kind == OUT_C64) {
-    set_smem(k_rows_inv_out<float2>, prow.smem_bytes());
-    k_rows_inv_out<float2><<<g.H2 / 2, prow.d.nt, prow.smem_bytes(), st>>>(
-        prow.d, g, T2, static_cast<float2*>(out), accumulate, dcs, dcr, dci, scale);
-  } else {
-    set_smem(k_rows_inv_out<double2>, prow.smem_bytes());
-    k_rows_inv_out<double2><<<g.H2 / 2, prow.d.nt, prow.smem_bytes(), st>>>(
-        prow.d, g, T2, static_cast<double2*>(out), accumulate, dcs, dcr, dci, scale);
+  // T2b: a second launch adds conj(IFFT(T2b)) to the first one's output
+  for (int pl = 0; pl < (T2b ? 2 : 1); ++pl) {
+    const float2* src = pl ? T2b : T2;
+    if (out_kind == OUT_C64) {
+      set_smem(k_rows_inv_out<float2>, prow.smem_bytes());
+      k_rows_inv_out<float2><<<g.H2 / 2, prow.d.nt, prow.smem_bytes(), st>>>(
+          prow.d, g, src, static_cast<float2*>(out), accumulate, pl, dcs, dcr, dci, scale);
+    } else {
+      set_smem(k_rows_inv_out<double2>, prow.smem_bytes());
+      k_rows_inv_out<double2><<<g.H2 / 2, prow.d.nt, prow.smem_bytes(), st>>>(
+          prow.d, g, src, static_cast<double2*>(out), accumulate, pl, dcs, dcr, dci, scale);
+    }
+    ++lc.n;
   }
-  ++lc.n;
 }
 
 }  // namespace xcb

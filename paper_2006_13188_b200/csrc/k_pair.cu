@@ -16,6 +16,7 @@
 //   S2 k_cols_fwd_mac_ilv    : per band, column FFT of T1_k times F^_k summed
 //        over the bands in TMEM (the reference's B inverse FFTs collapse into
 //        one, engine.hpp:359-366), then one inverse column FFT -> T2
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <map>
@@ -979,6 +980,16 @@ template <>
 struct S1Plan<IlvFft<1152, 16, 9, 8, 16>> {
   using type = IlvFft<1152, 8, 16, 9, 8>;
 };
+
+// the transform lengths with a pair plan (ascending)
+std::vector<int> pair_plan_lengths() {
+  std::vector<int> v;
+#define XCB_PAIR_LEN(LL, R0, R1, R2, PP) v.push_back(LL);
+  XCB_PAIR_TABLE(XCB_PAIR_LEN)
+#undef XCB_PAIR_LEN
+  std::sort(v.begin(), v.end());
+  return v;
+}
 
 // 0 if no pair plan for L (or the stage does not fit); else the dynamic smem.
 // stage 0 I1, 1 I2, 2 planes, 3 S1, 4 S2, 5 F1, 6 F2, 7 S4

@@ -11,6 +11,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <vector>
+
 #include "fft_plan.h"
 
 namespace xcb {
@@ -95,7 +97,8 @@ void launch_cols_fwd_mac_inv(const FftPlan& pcol, const Geo& g, const float2* T1
 // S4: row IFFT of T2, crop (+ dc * signal) -> out.
 void launch_rows_inv_out(const FftPlan& prow, const Geo& g, const float2* T2,
                          int out_kind, void* out, int accumulate, const SigSrc& dc_sig,
-                         double dc_re, double dc_im, cudaStream_t st, LaunchCounter& lc);
+                         double dc_re, double dc_im, cudaStream_t st, LaunchCounter& lc,
+                         const float2* T2b = nullptr);
 
 // Filter spectra: rendered (2R+1)^2 components (nb bands, c64) -> F^ (layout B).
 void launch_filter_spectra(const FftPlan& prow, const FftPlan& pcol, const Geo& g,
@@ -167,6 +170,11 @@ void launch_rows_fwd_premul_fast(const FftPlan& pr, const Geo& g, const SigSrc& 
 void launch_cols_fwd_mac_inv_fast(const FftPlan& pc, const Geo& g, const float2* T1,
                                   const float2* Fhat, size_t sstride, const Bands& b,
                                   float2* T2, cudaStream_t st, LaunchCounter& lc);
+// the same over conjugate band pairs (launch_cols_fwd_mac_inv_cpair); fast_smem stage 6
+void launch_cols_fwd_mac_inv_cpair_fast(const FftPlan& pc, const Geo& g, const float2* T1,
+                                        const float2* Fhat, const float2* Ghat, size_t sstride,
+                                        const Bands& b, const int* gspec, float2* T2,
+                                        size_t t2plane, cudaStream_t st, LaunchCounter& lc);
 }  // namespace xcb
 
 namespace xcb {
@@ -185,6 +193,8 @@ void launch_cols_inv_corr_pair(const Geo& g, const float2* Hhat, const float2* F
 // scatter stages S1 / S2 on the pair engine (stages 3 / 4 of pair_smem)
 void launch_rows_fwd_premul_pair(const Geo& g, const SigSrc& s, const double* base,
                                  const Bands& b, float2* T1, cudaStream_t st, LaunchCounter& lc);
+// the transform lengths served by the pair engine (k_pair.cu XCB_PAIR_TABLE)
+std::vector<int> pair_plan_lengths();
 // half0: Hermitian half-band mode (bands k >= 0; the k = 0 band weighted 1/2)
 void launch_cols_fwd_mac_inv_pair(const Geo& g, const float2* T1, const float2* Fhat,
                                   size_t sstride, const Bands& b, int half0, float2* T2,

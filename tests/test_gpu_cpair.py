@@ -59,6 +59,33 @@ def test_cpair_band_subsets(orc, comps):
     assert orc.rel_l2(res.output, ref) < TOL
 
 
+@pytest.mark.parametrize("h,w,periodic", [(40, 52, False), (256, 256, False), (250, 540, False),
+                                          (512, 576, True), (2030, 300, False)])
+def test_cpair_fast_kernel_sizes(orc, h, w, periodic):
+    """Pads without a pair plan (64, 288, 576, 512 periodic, 2048 x 324...): S2 takes
+    the fast kernels' paired variant (k_fast.cu) and S4 the generic kernel's
+    second, conjugated pass; band_mode reports the paired path."""
+    import ctypes as C
+    from paper_2006_13188_b200 import _native as N
+    r, F, H, T = _rot_case(106, h, w, m_max=5, R=10)
+    res = X.xconv_fast(H, X.XformField.rotation(T), F, X.XConvPlan(periodic=periodic))
+    ref = orc.xconv_fast(H.astype(np.float64), ROT, T.astype(np.float64), ofilter(orc, F),
+                         periodic=periodic, nthreads=NT)[0]
+    assert orc.rel_l2(res.output, ref) < TOL
+    # the stats of the same call through the C ABI
+    ctx = N.context(0)
+    out = np.zeros(H.shape, np.complex64)
+    d = N.ImageDesc(h, w, 1, N.XC_F32, N.XC_F32, N.XC_C64, N.XC_ROW_MAJOR, N.XC_HOST, 1, 0)
+    st = N.Stats()
+    N.check(N.lib().xc_run(ctx.handle, F.handle(ctx), 1, C.byref(d), H.ctypes.data,
+                           T.ctypes.data, None, 0, N.XC_FLAG_PERIODIC if periodic else 0,
+                           out.ctypes.data, C.byref(st)), ctx.handle)
+    assert st.standard_ops == 11 and st.band_mode in (0, 2)
+    if st.band_mode == 2:
+        assert st.bands_run == 6
+    assert np.array_equal(out, res.output)
+
+
 def test_cpair_periodic_and_f64_signal(orc):
     r, F, H, T = _rot_case(103, 1100, 1100)
     H64, T64 = H.astype(np.float64), T.astype(np.float64)
