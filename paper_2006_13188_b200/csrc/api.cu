@@ -923,8 +923,13 @@ void run_scatter(Call& c, const xcb::SigSrc& sig, const double* base, void* out,
   // S2 on the pair engine or the fast kernels; S1 and S4 on any engine
   const bool s2_pair = use_pair() && xcb::pair_smem(4, g.Ph, g);
   const bool s2_fast = !s2_pair && c.fcol && xcb::fast_smem(6, *c.fcol, g);
-  bool cpair = !half && use_cpair() && !sig.is_complex && !c.packed && (s2_pair || s2_fast) &&
-               c.ks.size() > 1;
+  // long columns (>= 3456): the staged G_k does not fit beside F^_k, so the fast
+  // S2 runs twice over the same T1 planes (F^_k -> first plane; G_k, k > 0 ->
+  // second plane); S1's halving is kept
+  const bool s2_split = !s2_pair && !s2_fast && c.fcol && xcb::fast_smem(3, *c.fcol, g);
+  bool cpair = !half && use_cpair() && !sig.is_complex && !c.packed &&
+               (s2_pair || s2_fast || s2_split) && c.ks.size() > 1;
+  xcb::Bands bands_g{nullptr, nullptr, 0};  // split S2: the bands k > 0 with G_k's planes
   if (cpair) {
     std::vector<int> hk, hs, hg;
     for (size_t i = 0; i < c.ks.size() && cpair; ++i) {
@@ -944,6 +949,15 @@ void run_scatter(Call& c, const xcb::SigSrc& sig, const double* base, void* out,
       bands = xcb::Bands{db, db + n, n};
       gspec = db + 2 * n;
       Ghat = filter_spectra_conj(c);
+      if (s2_split) {
+        // T1 plane bi belongs to band hk[bi]; k = 0, if selected, must be the
+        // last plane so that the bands k > 0 are a prefix of the planes
+        int npos = 0;
+        while (npos < n && hk[size_t(npos)] > 0) ++npos;
+        for (int i = npos; i < n && cpair; ++i) cpair = hk[size_t(i)] == 0 && i == n - 1;
+        bands_g = xcb::Bands{db, gspec, npos};
+        if (!cpair) bands = c.bands;  // (setup sorts the bands in descending k: not reached)
+      }
     }
   }
   c.nb_run = bands.n;
@@ -967,12 +981,21 @@ void run_scatter(Call& c, const xcb::SigSrc& sig, const double* base, void* out,
   }
   if (cpair) {
     stage(c, "S2_cols_fwd_mac_inv", [&] {
-      if (s2_pair)
+      if (s2_pair) {
         xcb::launch_cols_fwd_mac_inv_cpair(g, T1, c.Fhat, Ghat, c.sstride, bands, gspec, T2,
                                            t2plane, c.st, c.lc);
-      else
+      } else if (s2_fast) {
         xcb::launch_cols_fwd_mac_inv_cpair_fast(*c.fcol, g, T1, c.Fhat, Ghat, c.sstride, bands,
                                                 gspec, T2, t2plane, c.st, c.lc);
+      } else {
+        xcb::launch_cols_fwd_mac_inv_fast(*c.fcol, g, T1, c.Fhat, c.sstride, bands, T2, c.st,
+                                          c.lc);
+        if (bands_g.n > 0)
+          xcb::launch_cols_fwd_mac_inv_fast(*c.fcol, g, T1, Ghat, c.sstride, bands_g,
+                                            T2 + t2plane, c.st, c.lc);
+        else
+          ck(cudaMemsetAsync(T2 + t2plane, 0, t2plane * sizeof(float2), c.st), "memset");
+      }
     });
   } else if (use_pair() && xcb::pair_smem(4, g.Ph, g)) {
     stage(c, "S2_cols_fwd_mac_inv", [&] {

@@ -59,7 +59,8 @@ struct IlvFft {
   static constexpr int LP = L + L / P;        // float4 slots per buffer
   // CTAs per SM the band kernels ask for (__launch_bounds__): two when two
   // CTAs' buffers fit in shared memory (short transforms), else one
-  static constexpr int MINB = (L + 2 * LP) * 16 + TWM * 8 <= 112 * 1024 ? 2 : 1;
+  // (and two CTAs' warps fit the register file at ~80 registers: T <= 384)
+  static constexpr int MINB = (L + 2 * LP) * 16 + TWM * 8 <= 112 * 1024 && T <= 384 ? 2 : 1;
   static constexpr int WPQ = (T / 32 + 3) / 4;  // max warps sharing a TMEM lane quadrant
   // TMEM allocation (power of two >= 32 columns) for kThr columns per thread
   __host__ __device__ static constexpr uint32_t tmem_cols(int kThr) {
@@ -182,6 +183,15 @@ struct IlvFft {
 #else
 #define XCB_PAIR_1152(X) X(1152, 16, 9, 8, 16)
 #endif
-#define XCB_PAIR_TABLE(X) X(4320, 16, 18, 15, 16) X(2160, 12, 15, 12, 12) XCB_PAIR_1152(X)
+// Further lengths (session 5) so that most image sizes find a pair plan within
+// ~25% per axis (api.cu pick_pad2d): natural radix orders, R0 = P
+#define XCB_PAIR_MORE(X)                                                                 \
+  X(576, 8, 9, 8, 8) X(768, 8, 12, 8, 8) X(1024, 16, 8, 8, 16) X(1280, 16, 10, 8, 16)      \
+  X(1536, 16, 12, 8, 16) X(1920, 16, 12, 10, 16) X(2048, 16, 16, 8, 16)                    \
+  X(2304, 16, 12, 12, 16) X(2560, 16, 16, 10, 16) X(2880, 16, 15, 12, 16)                  \
+  X(3072, 16, 16, 12, 16) X(3456, 16, 18, 12, 16)                                          \
+  X(4096, 16, 16, 16, 16)
+#define XCB_PAIR_TABLE(X) \
+  X(4320, 16, 18, 15, 16) X(2160, 12, 15, 12, 12) XCB_PAIR_1152(X) XCB_PAIR_MORE(X)
 
 }  // namespace xcb

@@ -50,7 +50,8 @@ bool make_fft_plan_maxr(int L, int max_radix, FftPlan* out);
 #define XCB_FAST_TABLE(X)                                                              \
   X(64, 4, 1, 16) X(128, 8, 1, 16) X(256, 16, 1, 16) X(288, 18, 1, 16)               \
   X(512, 2, 16, 16) X(576, 4, 9, 16) X(1024, 4, 16, 16) X(1152, 8, 9, 16)            \
-  X(2048, 8, 16, 16) X(2160, 9, 15, 16) X(2304, 9, 16, 16) X(3456, 12, 18, 16)       \
+  X(2048, 8, 16, 16) X(2160, 9, 15, 16) X(2304, 9, 16, 16) X(2880, 12, 15, 16)       \
+  X(3072, 12, 16, 16) X(3456, 12, 18, 16)                                            \
   X(4096, 16, 16, 16) X(4320, 12, 18, 20)
 bool make_fast_plan(int L, FftPlan* out);
 constexpr int kFastMaxThreads = 512;

@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(PF::T, 1)
 template <class PF>
 struct S1Occ {
   static constexpr bool kTwReg = PF::L < 2048;
-  static constexpr int kMinB = kTwReg ? 3 : PF::MINB;
+  static constexpr int kMinB = kTwReg && PF::T <= 288 ? 3 : PF::MINB;
 };
 
 template <class PF>
@@ -980,6 +980,19 @@ template <>
 struct S1Plan<IlvFft<1152, 16, 9, 8, 16>> {
   using type = IlvFft<1152, 8, 16, 9, 8>;
 };
+// the same for the other lengths whose common plan starts with radix 16 and
+// whose S1 would otherwise spill (pass-0 inputs and phasors of 16 points)
+#define XCB_S1_PLAN(LL, A1, A2, B0, B1, B2)       \
+  template <>                                     \
+  struct S1Plan<IlvFft<LL, 16, A1, A2, 16>> {     \
+    using type = IlvFft<LL, B0, B1, B2, 8>;       \
+  };
+XCB_S1_PLAN(1024, 8, 8, 8, 16, 8)
+XCB_S1_PLAN(1280, 10, 8, 8, 16, 10)
+XCB_S1_PLAN(1536, 12, 8, 8, 16, 12)
+XCB_S1_PLAN(1920, 12, 10, 8, 16, 15)
+XCB_S1_PLAN(2048, 16, 8, 8, 16, 16)
+#undef XCB_S1_PLAN
 
 // the transform lengths with a pair plan (ascending)
 std::vector<int> pair_plan_lengths() {

@@ -86,6 +86,29 @@ def test_cpair_fast_kernel_sizes(orc, h, w, periodic):
     assert np.array_equal(out, res.output)
 
 
+def test_cpair_split_s2_long_columns(orc):
+    """Columns of 3456 and more: G_k does not fit beside F^_k in the fast S2's
+    shared memory, so S2 runs twice over the k >= 0 planes (api.cu s2_split);
+    sampled pixels against the spectral oracle."""
+    import ctypes as C
+    from paper_2006_13188_b200 import _native as N
+    r, F, _, _ = _rot_case(107, 8, 8, m_max=4, R=9)
+    h, w = 3440, 500
+    H = r.uniform(0, 1, (h, w)).astype(np.float32)
+    T = r.uniform(0, 2 * np.pi, (h, w)).astype(np.float32)
+    ctx = N.context(0)
+    out = np.zeros(H.shape, np.complex64)
+    d = N.ImageDesc(h, w, 1, N.XC_F32, N.XC_F32, N.XC_C64, N.XC_ROW_MAJOR, N.XC_HOST, 1, 0)
+    st = N.Stats()
+    N.check(N.lib().xc_run(ctx.handle, F.handle(ctx), 1, C.byref(d), H.ctypes.data,
+                           T.ctypes.data, None, 0, 0, out.ctypes.data, C.byref(st)), ctx.handle)
+    assert st.pad_h == 3456 and st.band_mode == 2 and st.bands_run == 5
+    ys = np.concatenate([r.integers(0, h, 30), [0, h - 1]])
+    xs = np.concatenate([r.integers(0, w, 30), [0, w - 1]])
+    ref = orc.spectral_oracle_at(1, H, ROT, T, ofilter(orc, F), ys, xs)
+    assert orc.rel_l2(out[ys, xs], ref) < TOL
+
+
 def test_cpair_periodic_and_f64_signal(orc):
     r, F, H, T = _rot_case(103, 1100, 1100)
     H64, T64 = H.astype(np.float64), T.astype(np.float64)
