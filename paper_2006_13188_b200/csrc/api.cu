@@ -1427,9 +1427,126 @@ namespace {
 
 // xcorr_fast / xconv_fast on one device (the caller holds ctx->mu).  out_dev:
 // `out` is a device buffer even when d->memory == XC_HOST (multi-device partials).
+// ---------------------------------------------------------------- tiles
+// Images beyond the longest planned transform (4320) used to fall on the
+// generic kernels, ~8x slower per point (pick_pad2d).  Both pipelines are
+// local: out(p) reads the signal and the transformation field within
+// R = ceil(r_max) of p only (engine.hpp:300-319, 345-368; zero padding outside
+// the image), so the image is cut into balanced tiles whose inputs carry an
+// R-pixel halo, each tile runs the planned pipelines, and the tile interiors
+// are copied into the output.  The result is the same sum per pixel (the halo
+// supplies exactly the samples the full transform would have used; rounding
+// differs as between any two pads).  Rotation group only (the scale group's
+// guard message names image pixels), not for periodic or accumulating calls.
+// XCB_TILE=0 turns it off.
+constexpr int kTileMaxLen = 4320;
+
+bool needs_tiles(xc_filter f, const xc_image_desc* d, unsigned flags) {
+  static const bool on = [] {
+    const char* e = std::getenv("XCB_TILE");
+    return !(e && e[0] == '0');
+  }();
+  if (!on || !use_pair() || !f || !d) return false;
+  if (flags & (XC_FLAG_PERIODIC | XC_FLAG_ACCUMULATE)) return false;
+  if (f->hf.group != XC_ROTATION2 || d->xform_kind != XC_ROTATION2) return false;
+  const int R = f->hf.render_radius();
+  if (6 * R > kTileMaxLen) return false;
+  return std::max(d->height, d->width) + R > kTileMaxLen;
+}
+
+void run_tiled(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d, const void* signal,
+               const void* param, const int* components, int n_components, unsigned flags,
+               void* out, xc_stats* stats) {
+  ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+  const auto t_start = std::chrono::steady_clock::now();
+  if (!signal || !param || !out) throw std::invalid_argument("null argument");
+  if (d->height < 1 || d->width < 1 || d->batch < 1)
+    throw std::invalid_argument("image dims must be positive");
+  const int R = f->hf.render_radius();
+  const bool cm = d->layout == XC_COL_MAJOR;
+  // the grid as it lies in memory: MR rows of MC elements
+  const int MR = cm ? d->width : d->height, MC = cm ? d->height : d->width;
+  auto split = [&](int n, int* nt, int* t) {
+    *nt = n + R <= kTileMaxLen ? 1 : (n + (kTileMaxLen - 3 * R) - 1) / (kTileMaxLen - 3 * R);
+    *t = (n + *nt - 1) / *nt;
+  };
+  int ntr, tr, ntc, tc;
+  split(MR, &ntr, &tr);
+  split(MC, &ntc, &tc);
+  const size_t ss = dtype_size(d->signal_dtype), ps = dtype_size(d->param_dtype),
+               os = dtype_size(d->out_dtype);
+  const size_t npix = size_t(MR) * MC;
+  const size_t tmax = size_t(std::min(MR, tr + 2 * R)) * size_t(std::min(MC, tc + 2 * R));
+  char* tsig = ctx->buf<char>("tile_sig", tmax * ss);
+  char* tpar = ctx->buf<char>("tile_par", tmax * ps);
+  char* tout = ctx->buf<char>("tile_out", tmax * os);
+  cudaStream_t st = ctx->stream;
+  xc_stats agg{};
+  int copies = 0;
+  for (int img = 0; img < d->batch; ++img) {
+    const char* sg = static_cast<const char*>(signal) + size_t(img) * npix * ss;
+    const char* pr = static_cast<const char*>(param) +
+                     (d->param_per_image ? size_t(img) * npix * ps : 0);
+    char* po = static_cast<char*>(out) + size_t(img) * npix * os;
+    for (int i = 0; i < ntr; ++i)
+      for (int j = 0; j < ntc; ++j) {
+        const int r0 = i * tr, r1 = std::min(MR, r0 + tr);
+        const int c0 = j * tc, c1 = std::min(MC, c0 + tc);
+        if (r0 >= r1 || c0 >= c1) continue;
+        const int a0 = std::max(0, r0 - R), a1 = std::min(MR, r1 + R);  // with the halo
+        const int b0 = std::max(0, c0 - R), b1 = std::min(MC, c1 + R);
+        const int h = a1 - a0, w = b1 - b0;
+        const size_t off = size_t(a0) * MC + b0;
+        ck(cudaMemcpy2DAsync(tsig, size_t(w) * ss, sg + off * ss, size_t(MC) * ss, size_t(w) * ss,
+                             size_t(h), cudaMemcpyDefault, st),
+           "tile signal");
+        ck(cudaMemcpy2DAsync(tpar, size_t(w) * ps, pr + off * ps, size_t(MC) * ps, size_t(w) * ps,
+                             size_t(h), cudaMemcpyDefault, st),
+           "tile param");
+        xc_image_desc dt = *d;
+        dt.batch = 1;
+        dt.memory = XC_DEVICE;
+        dt.param_per_image = 1;
+        dt.height = cm ? w : h;
+        dt.width = cm ? h : w;
+        xc_stats s1{};
+        run_single(ctx, f, mode, &dt, tsig, tpar, components, n_components,
+                   flags & ~unsigned(XC_FLAG_ASYNC), tout, &s1, false);
+        const size_t in_off = size_t(r0 - a0) * w + size_t(c0 - b0);
+        ck(cudaMemcpy2DAsync(po + (size_t(r0) * MC + c0) * os, size_t(MC) * os,
+                             tout + in_off * os, size_t(w) * os, size_t(c1 - c0) * os,
+                             size_t(r1 - r0), cudaMemcpyDefault, st),
+           "tile output");
+        copies += 3;
+        agg.standard_ops = s1.standard_ops;
+        agg.pad_h = std::max(agg.pad_h, s1.pad_h);
+        agg.pad_w = std::max(agg.pad_w, s1.pad_w);
+        agg.seconds_fft += s1.seconds_fft;
+        agg.gpu_launches += s1.gpu_launches;
+        agg.bands_run = s1.bands_run;
+        agg.band_mode = s1.band_mode;
+      }
+  }
+  ck(cudaStreamSynchronize(st), "tiles");
+  (void)copies;
+  if (stats) {
+    *stats = agg;
+    stats->seconds_total =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  }
+}
+
 void run_single(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d,
                 const void* signal, const void* param, const int* components, int n_components,
                 unsigned flags, void* out, xc_stats* stats, bool out_dev) {
+    if (needs_tiles(f, d, flags)) {
+      if (mode != XC_CORRELATION && mode != XC_CONVOLUTION)
+        throw std::invalid_argument("unknown mode");
+      if (d->out_dtype != XC_C64 && d->out_dtype != XC_C128)
+        throw std::invalid_argument("xc_run output must be complex (XC_C64 / XC_C128)");
+      run_tiled(ctx, f, mode, d, signal, param, components, n_components, flags, out, stats);
+      return;
+    }
     ck(cudaSetDevice(ctx->device), "cudaSetDevice");
     const auto t_start = std::chrono::steady_clock::now();
     if (mode != XC_CORRELATION && mode != XC_CONVOLUTION) throw std::invalid_argument("unknown mode");
