@@ -1860,18 +1860,29 @@ int xc_smooth(xc_context ctx, xc_filter f, const xc_image_desc* d, const void* s
   });
 }
 
-int xc_anglemax(xc_context ctx, xc_filter f, const xc_image_desc* d, const void* signal,
-                const int* components, int n_components, int n_angles, void* score,
-                int* argmax, xc_stats* stats) {
-  return guarded(ctx, [&] {
-    if (!ctx) throw std::invalid_argument("null context");
-    std::lock_guard<std::mutex> lk(ctx->mu);
+}  // extern "C"
+
+namespace {
+
+void anglemax_tiled(xc_context ctx, xc_filter f, const xc_image_desc* d, const void* signal,
+                    const int* components, int n_components, int n_angles, void* score,
+                    int* argmax, xc_stats* stats);
+
+void anglemax_single(xc_context ctx, xc_filter f, const xc_image_desc* d, const void* signal,
+                     const int* components, int n_components, int n_angles, void* score,
+                     int* argmax, xc_stats* stats) {
+  {
     ck(cudaSetDevice(ctx->device), "cudaSetDevice");
     const auto t_start = std::chrono::steady_clock::now();
     if (!signal || !score || !d) throw std::invalid_argument("null argument");
     if (n_angles < 1) throw std::invalid_argument("n_angles must be >= 1");
     if (d->out_dtype != XC_F32 && d->out_dtype != XC_F64)
       throw std::invalid_argument("xc_anglemax score must be real (XC_F32 / XC_F64)");
+    // the score at p reads the signal within R of p only: tiles as in run_tiled
+    if (f && needs_tiles(f, d, 0) && d->xform_kind == XC_ROTATION2) {
+      anglemax_tiled(ctx, f, d, signal, components, n_components, n_angles, score, argmax, stats);
+      return;
+    }
     Call c = setup(ctx, f, d, XC_ROTATION2, components, n_components, false);
     const int span = *std::max_element(c.ks.begin(), c.ks.end()) -
                      *std::min_element(c.ks.begin(), c.ks.end()) + 1;
@@ -1898,6 +1909,7 @@ int xc_anglemax(xc_context ctx, xc_filter f, const xc_image_desc* d, const void*
       bands = xcb::Bands{db, db + hk.size(), int(hk.size())};
     }
     c.nb_run = bands.n;
+    c.band_mode = herm ? 1 : 0;
     float2* planes = ctx->buf<float2>("planes", size_t(bands.n) * npix);
     float2* T1 = ctx->buf<float2>("T1", size_t(c.g.Hx2) * c.g.Pw);
     float2* Hh = ctx->buf<float2>("Hhat", size_t(c.g.Ph) * c.g.Pw);
@@ -1965,6 +1977,96 @@ int xc_anglemax(xc_context ctx, xc_filter f, const xc_image_desc* d, const void*
     fill_stats(c, stats, gpu_s,
                std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count(),
                (long long)c.ks.size());
+  }
+}
+
+// xc_anglemax over halo-extended tiles (see run_tiled): the tile interiors of
+// the score and of the argmax are copied into the outputs
+void anglemax_tiled(xc_context ctx, xc_filter f, const xc_image_desc* d, const void* signal,
+                    const int* components, int n_components, int n_angles, void* score,
+                    int* argmax, xc_stats* stats) {
+  const auto t_start = std::chrono::steady_clock::now();
+  if (d->height < 1 || d->width < 1 || d->batch < 1)
+    throw std::invalid_argument("image dims must be positive");
+  const int R = f->hf.render_radius();
+  const bool cm = d->layout == XC_COL_MAJOR;
+  const int MR = cm ? d->width : d->height, MC = cm ? d->height : d->width;
+  auto split = [&](int n, int* nt, int* t) {
+    *nt = n + R <= kTileMaxLen ? 1 : (n + (kTileMaxLen - 3 * R) - 1) / (kTileMaxLen - 3 * R);
+    *t = (n + *nt - 1) / *nt;
+  };
+  int ntr, tr, ntc, tc;
+  split(MR, &ntr, &tr);
+  split(MC, &ntc, &tc);
+  const size_t ss = dtype_size(d->signal_dtype), os = dtype_size(d->out_dtype);
+  const size_t npix = size_t(MR) * MC;
+  const size_t tmax = size_t(std::min(MR, tr + 2 * R)) * size_t(std::min(MC, tc + 2 * R));
+  char* tsig = ctx->buf<char>("tile_sig", tmax * ss);
+  char* tsc = ctx->buf<char>("tile_score", tmax * os);
+  int* targ = argmax ? ctx->buf<int>("tile_arg", tmax) : nullptr;
+  cudaStream_t st = ctx->stream;
+  xc_stats agg{};
+  for (int img = 0; img < d->batch; ++img) {
+    const char* sg = static_cast<const char*>(signal) + size_t(img) * npix * ss;
+    char* po = static_cast<char*>(score) + size_t(img) * npix * os;
+    int* pa = argmax ? argmax + size_t(img) * npix : nullptr;
+    for (int i = 0; i < ntr; ++i)
+      for (int j = 0; j < ntc; ++j) {
+        const int r0 = i * tr, r1 = std::min(MR, r0 + tr);
+        const int c0 = j * tc, c1 = std::min(MC, c0 + tc);
+        if (r0 >= r1 || c0 >= c1) continue;
+        const int a0 = std::max(0, r0 - R), a1 = std::min(MR, r1 + R);
+        const int b0 = std::max(0, c0 - R), b1 = std::min(MC, c1 + R);
+        const int h = a1 - a0, w = b1 - b0;
+        ck(cudaMemcpy2DAsync(tsig, size_t(w) * ss, sg + (size_t(a0) * MC + b0) * ss,
+                             size_t(MC) * ss, size_t(w) * ss, size_t(h), cudaMemcpyDefault, st),
+           "tile signal");
+        xc_image_desc dt = *d;
+        dt.batch = 1;
+        dt.memory = XC_DEVICE;
+        dt.height = cm ? w : h;
+        dt.width = cm ? h : w;
+        xc_stats s1{};
+        anglemax_single(ctx, f, &dt, tsig, components, n_components, n_angles, tsc, targ, &s1);
+        const size_t in_off = size_t(r0 - a0) * w + size_t(c0 - b0);
+        const size_t out_off = size_t(r0) * MC + c0;
+        ck(cudaMemcpy2DAsync(po + out_off * os, size_t(MC) * os, tsc + in_off * os,
+                             size_t(w) * os, size_t(c1 - c0) * os, size_t(r1 - r0),
+                             cudaMemcpyDefault, st),
+           "tile score");
+        if (pa)
+          ck(cudaMemcpy2DAsync(pa + out_off, size_t(MC) * sizeof(int), targ + in_off,
+                               size_t(w) * sizeof(int), size_t(c1 - c0) * sizeof(int),
+                               size_t(r1 - r0), cudaMemcpyDefault, st),
+             "tile argmax");
+        agg.standard_ops = s1.standard_ops;
+        agg.pad_h = std::max(agg.pad_h, s1.pad_h);
+        agg.pad_w = std::max(agg.pad_w, s1.pad_w);
+        agg.seconds_fft += s1.seconds_fft;
+        agg.gpu_launches += s1.gpu_launches;
+        agg.bands_run = s1.bands_run;
+        agg.band_mode = s1.band_mode;
+      }
+  }
+  ck(cudaStreamSynchronize(st), "tiles");
+  if (stats) {
+    *stats = agg;
+    stats->seconds_total =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int xc_anglemax(xc_context ctx, xc_filter f, const xc_image_desc* d, const void* signal,
+                const int* components, int n_components, int n_angles, void* score,
+                int* argmax, xc_stats* stats) {
+  return guarded(ctx, [&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    anglemax_single(ctx, f, d, signal, components, n_components, n_angles, score, argmax, stats);
   });
 }
 

@@ -109,3 +109,34 @@ def test_tiled_complex_signal_device_memory(orc):
     ref = (orc.spectral_oracle_at(1, np.ascontiguousarray(Hc.real), 0, T, OF, ys, xs) +
            1j * orc.spectral_oracle_at(1, np.ascontiguousarray(Hc.imag), 0, T, OF, ys, xs))
     assert orc.rel_l2(got[ys, xs], ref) < TOL
+
+
+@pytest.mark.parametrize("real_filter", [True, False])
+def test_tiled_anglemax_matches_oracle(orc, real_filter):
+    """xc_anglemax over tiles (api.cu anglemax_tiled): score and argmax at
+    sampled pixels, seams included, against the oracle's angle max of the
+    per-band responses (tensor-core path for the real filter, generic DFT
+    kernel for the complex one)."""
+    from paper_2006_13188_b200 import workloads as WL
+    r = np.random.default_rng(11 + real_filter)
+    R, m = 9, 4
+    f = WL.angular_filter(R, 3.5, m, r)
+    if real_filter:
+        f = f.real + 0.0j
+    F = X.decompose_rotation2(f, R, R, 2 * m, 18, 20, float(R))
+    h, w = 4450, 150
+    H = r.normal(0, 1, (h, w)).astype(np.float32)
+    score, arg = X.anglemax(H, F, 360)
+    ys, xs = _samples(r, h, w, R)
+    Z = np.zeros((h, w), np.float32)
+    G = np.stack([orc.spectral_oracle_at(0, H, 0, Z, orc.Filter(
+        int(F.group), F.K, F.ks[i:i + 1], F.comps[:, i:i + 1], F.n_radii, F.n_angles, F.r_max,
+        F.r_min, F.r_domain), ys, xs) for i in range(len(F.ks))])
+    rs, ra = orc.anglemax(np.ascontiguousarray(G.reshape(len(F.ks), 1, -1)), F.ks, 360)
+    assert orc.rel_l2(score[ys, xs], rs.ravel()) < TOL
+    th = 2 * np.pi * np.arange(360) / 360
+    S = np.abs(np.einsum("ka,kp->ap", np.exp(-1j * np.outer(th, np.asarray(F.ks)).T), G))
+    top2 = np.sort(S, 0)[-2:]
+    clear = (top2[1] - top2[0]) > 1e-4 * top2[1]
+    assert clear.sum() >= len(ys) // 2
+    assert np.array_equal(arg[ys, xs][clear], ra.ravel()[clear])
