@@ -1,7 +1,8 @@
 """Out-of-bounds checks without compute-sanitizer (closed on the GPU pool):
 tools/guard_cases.py runs every pipeline -- the pair engine at 1152 / 2160 /
 4320 (gather, scatter, smoothing, band subsets), the angle max, the generic
-and fast kernels on ragged and tiny images, periodic mode, pattern detection
+and fast kernels on ragged and tiny images, the session-5 pair lengths with the
+paired scatter (pair, fast and split S2), halo tiles, periodic mode, pattern detection
 with the device decomposition, and the 3D pipeline -- once plainly and once
 with XCB_GUARD (every context buffer between two 64 KiB guard zones, the
 allocations and the filter spectra poisoned with NaN bytes).  Required: no

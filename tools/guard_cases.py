@@ -50,6 +50,22 @@ def cases():
         T = X.XformField.rotation(th)
         out[f"rag{h}x{w}_xcorr"] = X.xcorr_fast(H, T, w1.filt).output
         out[f"rag{h}x{w}_xconv"] = X.xconv_fast(H, T, w1.filt).output
+    # the session-5 pair plans (rows / columns on different lengths: 768 x 1280,
+    # 2880 x 576, 3072 + 4096 with the fast and the split paired S2), the angle
+    # max at one of them, and halo tiles beyond 4320
+    for h, w in [(740, 1250), (2860, 560), (3050, 200), (150, 4070)]:
+        H = rng.random((h, w)).astype(np.float32)
+        T = X.XformField.rotation((rng.random((h, w)) * 2 * np.pi).astype(np.float32))
+        out[f"len{h}x{w}_xcorr"] = X.xcorr_fast(H, T, w1.filt).output
+        out[f"len{h}x{w}_xconv"] = X.xconv_fast(H, T, w1.filt).output
+    Hn = rng.standard_normal((1500, 700)).astype(np.float32)
+    am2 = X.anglemax(Hn, w1.filt, 360)
+    out["len1500x700_score"], out["len1500x700_argmax"] = np.asarray(am2[0]), np.asarray(am2[1])
+    for h, w in [(4400, 130), (120, 4500)]:
+        H = rng.random((h, w)).astype(np.float32)
+        T = X.XformField.rotation((rng.random((h, w)) * 2 * np.pi).astype(np.float32))
+        out[f"tile{h}x{w}_xcorr"] = X.xcorr_fast(H, T, w1.filt).output
+        out[f"tile{h}x{w}_xconv"] = X.xconv_fast(H, T, w1.filt).output
     per = X.XConvPlan(periodic=True)
     out["cfg1_periodic"] = X.xcorr_fast(w1.signal[0], T1, w1.filt, per).output
     # device decomposition + pattern detection
