@@ -186,7 +186,8 @@ struct IlvFft {
 // Further lengths (session 5) so that most image sizes find a pair plan within
 // ~25% per axis (api.cu pick_pad2d): natural radix orders, R0 = P
 #define XCB_PAIR_MORE(X)                                                                 \
-  X(576, 8, 9, 8, 8) X(768, 8, 12, 8, 8) X(1024, 16, 8, 8, 16) X(1280, 16, 10, 8, 16)      \
+  X(288, 8, 6, 6, 8) X(576, 8, 9, 8, 8) X(768, 8, 12, 8, 8) X(1024, 16, 8, 8, 16)          \
+  X(1280, 16, 10, 8, 16)                                                                   \
   X(1536, 16, 12, 8, 16) X(1920, 16, 12, 10, 16) X(2048, 16, 16, 8, 16)                    \
   X(2304, 16, 12, 12, 16) X(2560, 16, 16, 10, 16) X(2880, 16, 15, 12, 16)                  \
   X(3072, 16, 16, 12, 16) X(3456, 16, 18, 12, 16)                                          \

@@ -1044,7 +1044,7 @@ int pair_i1_images() {
 // the SMs.  The split minimises ceil(rem * s / slots) * (ceil(nb / s) + 1)
 // (one band-equivalent of per-CTA setup per chunk).  XCB_TAIL_SPLIT=0 turns
 // it off.
-TailSplit tail_split(int units, int per_sm, int nb) {
+TailSplit tail_split(int units, int per_sm, int nb, int threads) {
   static const int sms = [] {
     int dev = 0, n = 0;
     cudaGetDevice(&dev);
@@ -1057,7 +1057,16 @@ TailSplit tail_split(int units, int per_sm, int nb) {
   }();
   const int slots = sms * per_sm;
   const int full = units / slots * slots, rem = units - full;
-  if (off || rem == 0 || full == 0 || nb < 4) return {units, units, 1, slots};
+  if (off || nb < 4) return {units, units, 1, slots};
+  if (full == 0) {
+    // under one wave (small images): every unit's bands go to s chunks, s CTAs
+    // small CTAs co-reside beyond the launch bound (registers: ~640 threads per SM)
+    const int occ = threads > 0 ? std::max(per_sm, std::min(6, 640 / threads)) : per_sm;
+    const int s = std::min(sms * occ / std::max(units, 1), nb / 2);
+    if (s < 2) return {units, units, 1, slots};
+    return {units * s, 0, s, slots};
+  }
+  if (rem == 0) return {units, units, 1, slots};
   int best = 1;
   long best_cost = long(nb) + 1;
   for (int s = 2; s <= nb / 2; ++s) {
@@ -1151,7 +1160,7 @@ void launch_rows_fwd_premul_pair(const Geo& g, const SigSrc& s, const double* ba
     /* tail split only under two waves (config 2: 512 row pairs on 444 slots); config 4's  \
        3.5 waves measured 0.306 ms split, 0.297 ms not */                                   \
     const int rows2 = g.Hx2 / 2;                                                            \
-    TailSplit ts = tail_split(rows2, S1Occ<PF>::kMinB, b.n);                                \
+    TailSplit ts = tail_split(rows2, S1Occ<PF>::kMinB, b.n, PF::T);                                \
     if (rows2 >= 2 * ts.slots) ts = TailSplit{rows2, rows2, 1, ts.slots};                   \
     set_smem(k_rows_fwd_premul_ilv<PF>, sm);                                                \
     k_rows_fwd_premul_ilv<PF><<<ts.grid, PF::T, sm, st>>>(g, s, base, b, T1, tw.mid,        \

@@ -127,7 +127,7 @@ void launch_cols_inv_corr_pair(const Geo& g, const float2* Hhat, const float2* F
   case LL: {                                                                                \
     using PF = IlvFft<LL, R0, R1, R2, PP>;                                                  \
     const PairTw tw = pair_tables<PF>();                                                    \
-    const TailSplit ts = tail_split(ncol, PF::MINB, b.n);                                   \
+    const TailSplit ts = tail_split(ncol, PF::MINB, b.n, PF::T);                                   \
     if (nimg == 2) {                                                                        \
       set_smem(k_cols_inv_corr_ilv<PF, 2>, sm);                                             \
       k_cols_inv_corr_ilv<PF, 2><<<ts.grid, PF::T, sm, st>>>(                               \

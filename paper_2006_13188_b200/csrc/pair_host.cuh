@@ -78,6 +78,7 @@ struct TailSplit {
   int grid, full, split;
   int slots = 0;  // resident CTAs of the device (SMs * per_sm)
 };
-TailSplit tail_split(int units, int per_sm, int nb);
+// threads: the CTA size, for the co-residency estimate of sub-wave grids
+TailSplit tail_split(int units, int per_sm, int nb, int threads = 0);
 
 }  // namespace xcb

@@ -15,7 +15,7 @@ from paper_2006_13188_b200 import _native as N
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-5
-LENGTHS = [576, 768, 1024, 1152, 1280, 1536, 1920, 2048, 2160, 2304, 2560, 2880, 3072, 3456,
+LENGTHS = [288, 576, 768, 1024, 1152, 1280, 1536, 1920, 2048, 2160, 2304, 2560, 2880, 3072, 3456,
            4096, 4320]
 
 
