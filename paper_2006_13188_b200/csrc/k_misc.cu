@@ -12,6 +12,7 @@ template <class TP>
 __global__ void k_prep(const TP* __restrict__ param, int kind, double omega, double lo,
                        double hi, int H, int W, int transposed, double* __restrict__ base,
                        float* __restrict__ wgt, unsigned long long* bad) {
+  pdl_wait();
   const size_t n = size_t(H) * W;
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
        i += size_t(gridDim.x) * blockDim.x) {
@@ -403,10 +404,10 @@ void launch_prep(const void* param, int param_is_f64, int kind, double omega, do
                  unsigned long long* bad, cudaStream_t st, LaunchCounter& lc) {
   const int g = grid_for(size_t(H) * W, 256);
   if (param_is_f64)
-    k_prep<double><<<g, 256, 0, st>>>(static_cast<const double*>(param), kind, omega, lo, hi,
+    launch_k(k_prep<double>, g, 256, 0, st, static_cast<const double*>(param), kind, omega, lo, hi,
                                       H, W, transposed, base, wgt, bad);
   else
-    k_prep<float><<<g, 256, 0, st>>>(static_cast<const float*>(param), kind, omega, lo, hi,
+    launch_k(k_prep<float>, g, 256, 0, st, static_cast<const float*>(param), kind, omega, lo, hi,
                                      H, W, transposed, base, wgt, bad);
   ++lc.n;
 }

@@ -224,6 +224,7 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
                          const double* __restrict__ base, TO* __restrict__ out, int accumulate,
                          SigSrc dcs, double dcr, double dci, float scale,
                          const float2* __restrict__ twm, const float2* __restrict__ twl) {
+  pdl_wait();
   i2_body<PF, TO>(blockIdx.x, g, T2, bl, half, base, out, accumulate, dcs, dcr, dci, scale, twm,
                   twl);
 }
@@ -258,6 +259,7 @@ template <class PF, class TO>
 __global__ void __launch_bounds__(PF::T, 1)
     k_dual_ilv(Geo g, I1Args a, I2Args<TO> b, int n1, int n2, const float2* __restrict__ twm,
                const float2* __restrict__ twl, const float2* __restrict__ twf) {
+  pdl_wait();
   const int x = blockIdx.x, m = n1 < n2 ? n1 : n2;
   bool first;
   int item;
@@ -292,6 +294,7 @@ __global__ void __launch_bounds__(PF::T, S1Occ<PF>::kMinB)
     k_rows_fwd_premul_ilv(Geo g, SigSrc s, const double* __restrict__ base, Bands bl,
                           float2* __restrict__ T1, const float2* __restrict__ twm,
                           const float2* __restrict__ twl, int full, int split) {
+  pdl_wait();
   constexpr int R0 = PF::R0, R2 = PF::R2;
   constexpr bool TWR = S1Occ<PF>::kTwReg;
   // TMEM columns per thread: [cur, mul] per pass-0 input, then (unless TWR)
@@ -456,6 +459,7 @@ __global__ void __launch_bounds__(PF::T, 1)
     k_cols_fwd_mac_ilv(Geo g, const float4* __restrict__ T1, const float4* __restrict__ Fh,
                        size_t sstride4, Bands bl, int half0, float2* __restrict__ T2,
                        const float2* __restrict__ twm, const float2* __restrict__ twl) {
+  pdl_wait();
   constexpr int L = PF::L, R2 = PF::R2;  // L = Ph
   constexpr int kThr = 2 * R2;
   static_assert(kThr * PF::WPQ <= 512, "TMEM budget");
@@ -628,6 +632,7 @@ __global__ void __launch_bounds__(PF::T)
                              const int* __restrict__ gspec, float2* __restrict__ T2,
                              size_t t2plane, const float2* __restrict__ twm,
                              const float2* __restrict__ twl) {
+  pdl_wait();
   constexpr int L = PF::L, R2 = PF::R2;  // L = Ph
   constexpr int kThr = 4 * R2;           // A then B, 2 columns per pass-2 output
   static_assert(kThr * PF::WPQ <= 512, "TMEM budget");
@@ -818,6 +823,7 @@ template <class PF>
 __global__ void __launch_bounds__(PF::T, PF::MINB)
     k_rows_fwd_ilv(Geo g, SigSrc s, float2* __restrict__ T1, const float2* __restrict__ twm,
                    const float2* __restrict__ twl) {
+  pdl_wait();
   extern __shared__ __align__(16) float4 smp[];
   float2* W0 = reinterpret_cast<float2*>(smp);
   float2* W1 = reinterpret_cast<float2*>(smp + PF::LP);
@@ -855,6 +861,7 @@ template <class PF>
 __global__ void __launch_bounds__(PF::T, PF::MINB)
     k_cols_fwd_ilv(Geo g, const float4* __restrict__ T1, float2* __restrict__ spec,
                    const float2* __restrict__ twm, const float2* __restrict__ twl) {
+  pdl_wait();
   constexpr int L = PF::L;  // = Ph
   extern __shared__ __align__(16) float4 smp[];
   float4* ST4 = smp;
@@ -901,6 +908,7 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
                        TO* __restrict__ out, int accumulate, int real2, SigSrc dcs, double dcr,
                        double dci, float scale, const float2* __restrict__ twm,
                        const float2* __restrict__ twl) {
+  pdl_wait();
   extern __shared__ __align__(16) float4 smp[];
   float2* W0 = reinterpret_cast<float2*>(smp);
   float2* W1 = reinterpret_cast<float2*>(smp + PF::LP);
@@ -1093,12 +1101,12 @@ void launch_rows_inv_steer_pair(const Geo& g, const float2* T2, const Bands& b, 
     const PairTw tw = pair_tables<PF>();                                                    \
     if (out_kind == OUT_C64) {                                                              \
       set_smem(k_rows_inv_steer_ilv<PF, float2>, sm);                                       \
-      k_rows_inv_steer_ilv<PF, float2><<<g.H2 / 2, PF::T, sm, st>>>(                        \
+      launch_k(k_rows_inv_steer_ilv<PF, float2>, g.H2 / 2, PF::T, sm, st,                         \
           g, t2, b, half, base, static_cast<float2*>(out), accumulate, dcs, dcr, dci, scale, \
           tw.mid, tw.last);                                                                 \
     } else {                                                                                \
       set_smem(k_rows_inv_steer_ilv<PF, double2>, sm);                                      \
-      k_rows_inv_steer_ilv<PF, double2><<<g.H2 / 2, PF::T, sm, st>>>(                       \
+      launch_k(k_rows_inv_steer_ilv<PF, double2>, g.H2 / 2, PF::T, sm, st,                        \
           g, t2, b, half, base, static_cast<double2*>(out), accumulate, dcs, dcr, dci,      \
           scale,                                                                            \
           tw.mid, tw.last);                                                                 \
@@ -1132,14 +1140,14 @@ void launch_dual_pair(const Geo& g, const float2* Hhat, const float2* Fhat, size
       const I2Args<float2> i2{reinterpret_cast<const float4*>(T2r), b, half, base,          \
                               static_cast<float2*>(out), accumulate, dcs, dcr, dci, scale}; \
       set_smem(k_dual_ilv<PF, float2>, sm);                                                 \
-      k_dual_ilv<PF, float2><<<n1 + n2, PF::T, sm, st>>>(g, a, i2, n1, n2, tw.mid, tw.last, \
+      launch_k(k_dual_ilv<PF, float2>, n1 + n2, PF::T, sm, st, g, a, i2, n1, n2, tw.mid, tw.last, \
                                                          tw.last);                          \
     } else {                                                                                \
       const I2Args<double2> i2{reinterpret_cast<const float4*>(T2r), b, half, base,         \
                                static_cast<double2*>(out), accumulate, dcs, dcr, dci,       \
                                scale};                                                      \
       set_smem(k_dual_ilv<PF, double2>, sm);                                                \
-      k_dual_ilv<PF, double2><<<n1 + n2, PF::T, sm, st>>>(g, a, i2, n1, n2, tw.mid,         \
+      launch_k(k_dual_ilv<PF, double2>, n1 + n2, PF::T, sm, st, g, a, i2, n1, n2, tw.mid,         \
                                                           tw.last, tw.last);                \
     }                                                                                       \
     break;                                                                                  \
@@ -1163,7 +1171,7 @@ void launch_rows_fwd_premul_pair(const Geo& g, const SigSrc& s, const double* ba
     TailSplit ts = tail_split(rows2, S1Occ<PF>::kMinB, b.n, PF::T);                                \
     if (rows2 >= 2 * ts.slots) ts = TailSplit{rows2, rows2, 1, ts.slots};                   \
     set_smem(k_rows_fwd_premul_ilv<PF>, sm);                                                \
-    k_rows_fwd_premul_ilv<PF><<<ts.grid, PF::T, sm, st>>>(g, s, base, b, T1, tw.mid,        \
+    launch_k(k_rows_fwd_premul_ilv<PF>, ts.grid, PF::T, sm, st, g, s, base, b, T1, tw.mid,        \
                                                           tw.last, ts.full, ts.split);      \
     break;                                                                                  \
   }
@@ -1181,7 +1189,7 @@ void launch_cols_fwd_mac_inv_pair(const Geo& g, const float2* T1, const float2* 
     using PF = IlvFft<LL, R0, R1, R2, PP>;                                                  \
     const PairTw tw = pair_tables<PF>();                                                    \
     set_smem(k_cols_fwd_mac_ilv<PF>, sm);                                                   \
-    k_cols_fwd_mac_ilv<PF><<<g.Pw / 2, PF::T, sm, st>>>(                                    \
+    launch_k(k_cols_fwd_mac_ilv<PF>, g.Pw / 2, PF::T, sm, st,                                     \
         g, reinterpret_cast<const float4*>(T1), reinterpret_cast<const float4*>(Fhat),      \
         sstride / 2, b, half0, T2, tw.mid, tw.last);                                        \
     break;                                                                                  \
@@ -1201,7 +1209,7 @@ void launch_cols_fwd_mac_inv_cpair(const Geo& g, const float2* T1, const float2*
     using PF = IlvFft<LL, R0, R1, R2, PP>;                                                  \
     const PairTw tw = pair_tables<PF>();                                                    \
     set_smem(k_cols_fwd_mac_cpair_ilv<PF>, sm);                                             \
-    k_cols_fwd_mac_cpair_ilv<PF><<<g.Pw / 2, PF::T, sm, st>>>(                              \
+    launch_k(k_cols_fwd_mac_cpair_ilv<PF>, g.Pw / 2, PF::T, sm, st,                               \
         g, reinterpret_cast<const float4*>(T1), reinterpret_cast<const float4*>(Fhat),      \
         reinterpret_cast<const float4*>(Ghat), sstride / 2, b, gspec, T2, t2plane, tw.mid,  \
         tw.last);                                                                           \
@@ -1220,7 +1228,7 @@ void launch_rows_fwd_pair(const Geo& g, const SigSrc& s, float2* T1, cudaStream_
     using PF = IlvFft<LL, R0, R1, R2, PP>;                                                  \
     const PairTw tw = pair_tables<PF>();                                                    \
     set_smem(k_rows_fwd_ilv<PF>, sm);                                                       \
-    k_rows_fwd_ilv<PF><<<g.Hx2 / 2, PF::T, sm, st>>>(g, s, T1, tw.mid, tw.last);            \
+    launch_k(k_rows_fwd_ilv<PF>, g.Hx2 / 2, PF::T, sm, st, g, s, T1, tw.mid, tw.last);            \
     break;                                                                                  \
   }
   XCB_PAIR_DISPATCH(g.Pw, XCB_BODY)
@@ -1236,7 +1244,7 @@ void launch_cols_fwd_pair(const Geo& g, const float2* T1, float2* spec, cudaStre
     using PF = IlvFft<LL, R0, R1, R2, PP>;                                                  \
     const PairTw tw = pair_tables<PF>();                                                    \
     set_smem(k_cols_fwd_ilv<PF>, sm);                                                       \
-    k_cols_fwd_ilv<PF><<<g.Pw / 2, PF::T, sm, st>>>(g, reinterpret_cast<const float4*>(T1), \
+    launch_k(k_cols_fwd_ilv<PF>, g.Pw / 2, PF::T, sm, st, g, reinterpret_cast<const float4*>(T1), \
                                                     spec, tw.mid, tw.last);                 \
     break;                                                                                  \
   }
@@ -1258,12 +1266,12 @@ void launch_rows_inv_out_pair(const Geo& g, const float2* T2, int out_kind, void
     const PairTw tw = pair_tables<PF>();                                                    \
     if (out_kind == OUT_C64) {                                                              \
       set_smem(k_rows_inv_out_ilv<PF, float2>, sm);                                         \
-      k_rows_inv_out_ilv<PF, float2><<<g.H2 / 2, PF::T, sm, st>>>(                          \
+      launch_k(k_rows_inv_out_ilv<PF, float2>, g.H2 / 2, PF::T, sm, st,                           \
           g, t2, t2b, static_cast<float2*>(out), accumulate, real2, dcs, dcr, dci, scale,   \
           tw.mid, tw.last);                                                                 \
     } else {                                                                                \
       set_smem(k_rows_inv_out_ilv<PF, double2>, sm);                                        \
-      k_rows_inv_out_ilv<PF, double2><<<g.H2 / 2, PF::T, sm, st>>>(                         \
+      launch_k(k_rows_inv_out_ilv<PF, double2>, g.H2 / 2, PF::T, sm, st,                          \
           g, t2, t2b, static_cast<double2*>(out), accumulate, real2, dcs, dcr, dci, scale,  \
           tw.mid, tw.last);                                                                 \
     }                                                                                       \

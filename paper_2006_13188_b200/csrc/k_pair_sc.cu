@@ -27,6 +27,7 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
                         float2* __restrict__ T2, size_t tstride,
                         const float2* __restrict__ twm, const float2* __restrict__ twf,
                         int full, int split) {
+  pdl_wait();
   // CTAs below `full` run every band of column pair blockIdx.x; the column
   // pairs of the last, partial wave are split into `split` band chunks so the
   // tail spreads over all SMs (CTAs are dispatched in blockIdx order)
@@ -50,6 +51,7 @@ __global__ void __launch_bounds__(PF::T, PF::MINB)
     k_rows_inv_planes_ilv(Geo g, const float4* __restrict__ T2, int nbands,
                           float2* __restrict__ planes, float scale,
                           const float2* __restrict__ twm, const float2* __restrict__ twl) {
+  pdl_wait();
   constexpr int L = PF::L;  // = Pw
   constexpr int R2 = PF::R2;
   extern __shared__ __align__(16) float4 smp[];
@@ -130,12 +132,12 @@ void launch_cols_inv_corr_pair(const Geo& g, const float2* Hhat, const float2* F
     const TailSplit ts = tail_split(ncol, PF::MINB, b.n, PF::T);                                   \
     if (nimg == 2) {                                                                        \
       set_smem(k_cols_inv_corr_ilv<PF, 2>, sm);                                             \
-      k_cols_inv_corr_ilv<PF, 2><<<ts.grid, PF::T, sm, st>>>(                               \
+      launch_k(k_cols_inv_corr_ilv<PF, 2>, ts.grid, PF::T, sm, st,                                \
           g, hh, hstride / 2, fh, sstride / 2, b, T2, tstride, tw.mid, tw.last, ts.full,    \
           ts.split);                                                                        \
     } else {                                                                                \
       set_smem(k_cols_inv_corr_ilv<PF, 1>, sm);                                             \
-      k_cols_inv_corr_ilv<PF, 1><<<ts.grid, PF::T, sm, st>>>(                               \
+      launch_k(k_cols_inv_corr_ilv<PF, 1>, ts.grid, PF::T, sm, st,                                \
           g, hh, hstride / 2, fh, sstride / 2, b, T2, tstride, tw.mid, tw.last, ts.full,    \
           ts.split);                                                                        \
     }                                                                                       \
@@ -155,7 +157,7 @@ void launch_rows_inv_planes_pair(const Geo& g, const float2* T2, int nbands, flo
     using PF = IlvFft<LL, R0, R1, R2, PP>;                                                  \
     const PairTw tw = pair_tables<PF>();                                                    \
     set_smem(k_rows_inv_planes_ilv<PF>, sm);                                                \
-    k_rows_inv_planes_ilv<PF><<<g.H2 / 2, PF::T, sm, st>>>(                                 \
+    launch_k(k_rows_inv_planes_ilv<PF>, g.H2 / 2, PF::T, sm, st,                                  \
         g, reinterpret_cast<const float4*>(T2), nbands, planes, scale, tw.mid, tw.last);    \
     break;                                                                                  \
   }

@@ -1,5 +1,6 @@
 // Shared device helpers of the pipeline stages (included by k_*.cu).
 #pragma once
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -79,6 +80,46 @@ __device__ __forceinline__ float2 dc_term(const SigSrc& s, size_t i, double dr, 
   if (dr == 0.0 && di == 0.0) return make_float2(0.f, 0.f);
   const float2 h = sig_value(s, i);
   return make_float2(float(dr * h.x - di * h.y), float(dr * h.y + di * h.x));
+}
+
+// ------------------------------------------------------------------ programmatic dependent launch
+// The pipeline's kernels run back to back on one stream, each consuming the
+// previous one's output.  Launched with programmatic stream serialization, a
+// kernel's launch and block scheduling overlap the tail and completion of its
+// predecessor; pdl_wait() (griddepcontrol.wait, the first statement of every
+// kernel launched this way) then blocks until the predecessor grid has
+// completed and its writes are visible.  No kernel triggers early, so a
+// dependent grid never takes SM slots from blocks of the primary that have not
+// run yet.  It shortens the launch-latency-bound small configs (config 1: five
+// kernels in a CUDA graph); XCB_PDL=0 uses plain launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+inline bool use_pdl() {
+  static const bool on = [] {
+    const char* e = std::getenv("XCB_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <class... KArgs, class... Args>
+void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+              Args&&... args) {
+  if (!use_pdl()) {
+    kernel<<<grid, block, smem, st>>>(KArgs(args)...);
+    return;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, KArgs(args)...);
 }
 
 // ------------------------------------------------------------------ launch helpers
