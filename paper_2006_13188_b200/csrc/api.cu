@@ -1482,7 +1482,6 @@ void run_tiled(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d, co
   char* tout = ctx->buf<char>("tile_out", tmax * os);
   cudaStream_t st = ctx->stream;
   xc_stats agg{};
-  int copies = 0;
   for (int img = 0; img < d->batch; ++img) {
     const char* sg = static_cast<const char*>(signal) + size_t(img) * npix * ss;
     const char* pr = static_cast<const char*>(param) +
@@ -1517,7 +1516,6 @@ void run_tiled(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d, co
                              tout + in_off * os, size_t(w) * os, size_t(c1 - c0) * os,
                              size_t(r1 - r0), cudaMemcpyDefault, st),
            "tile output");
-        copies += 3;
         agg.standard_ops = s1.standard_ops;
         agg.pad_h = std::max(agg.pad_h, s1.pad_h);
         agg.pad_w = std::max(agg.pad_w, s1.pad_w);
@@ -1528,7 +1526,6 @@ void run_tiled(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d, co
       }
   }
   ck(cudaStreamSynchronize(st), "tiles");
-  (void)copies;
   if (stats) {
     *stats = agg;
     stats->seconds_total =
