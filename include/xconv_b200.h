@@ -194,6 +194,14 @@ int xc_fft2(xc_context ctx, int rows, int cols, int dtype, int memory, int inver
 int xc_debug_check_guards(xc_context ctx, int* n_bad, char* first_bad, int len);
 int xc_debug_guard_bytes(void);
 
+/* The transform length the 2D pipelines pick for an axis that needs at least n
+ * points (extent + R; fft.hpp:85-86 takes next_fast_size(extent + 2R + 1), any
+ * length >= extent + R filters identically): host logic, no GPU needed.
+ * xc_debug_tile_count: the number of halo tiles along an image axis of `extent`
+ * points with render radius R (1 = not tiled; rotation group, DESIGN 5). */
+int xc_debug_pick_pad(int n);
+int xc_debug_tile_count(int extent, int R);
+
 /* ---- filters (FreqFilter2) -------------------------------------------- */
 /* Filters are host objects (ctx may be NULL); device spectra are built on first
  * use per (device, pad size, layout) and freed by xc_filter_destroy.  Errors of

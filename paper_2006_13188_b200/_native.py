@@ -52,7 +52,7 @@ EXPORTS = [
     "xc_white_noise", "xc_nccl_unique_id", "xc_context_create_multi", "xc_context_create_rank",
     "xc_context_set_sharding", "xc_context_devices", "xc_context_synchronize",
     "xc_decompose_rotation2_device", "xc_decompose_scale2_device", "xc_debug_check_guards",
-    "xc_debug_guard_bytes", "xc_fft2",
+    "xc_debug_guard_bytes", "xc_fft2", "xc_debug_pick_pad", "xc_debug_tile_count",
 ]
 
 _lib = None
@@ -93,6 +93,8 @@ def lib():
             L.xc_fft2.argtypes = [vp, i, i, i, i, i, vp, vp]
             L.xc_debug_check_guards.argtypes = [vp, ip, C.c_char_p, i]
             L.xc_debug_guard_bytes.argtypes = []
+            L.xc_debug_pick_pad.argtypes = [i]
+            L.xc_debug_tile_count.argtypes = [i, i]
             L.xc_decompose_rotation2_device.argtypes = [vp, dp, i, i, i, d, d, i, i, i, d, ip,
                                                         dp, ip]
             L.xc_decompose_scale2_device.argtypes = [vp, dp, i, i, i, d, d, i, i, i, d, d, d,

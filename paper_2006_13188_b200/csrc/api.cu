@@ -1116,6 +1116,7 @@ void run_group(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d,
                unsigned flags, void* out, xc_stats* stats);
 void smooth_group(xc_context ctx, xc_filter f, const xc_image_desc* d, const void* signal,
                   const void* param, int normalize_signal, void* out, xc_stats* stats);
+int tile_count(int n, int R);
 
 }  // namespace
 
@@ -1244,6 +1245,10 @@ int xc_debug_check_guards(xc_context ctx, int* n_bad, char* first_bad, int len) 
 }
 
 int xc_debug_guard_bytes(void) { return int(guard_bytes()); }
+
+int xc_debug_pick_pad(int n) { return pick_pad2d(std::max(n, 1)); }
+
+int xc_debug_tile_count(int extent, int R) { return tile_count(extent, R); }
 
 int xc_profile_enable(xc_context ctx, int on) {
   return guarded(ctx, [&] {
@@ -1441,6 +1446,15 @@ namespace {
 // XCB_TILE=0 turns it off.
 constexpr int kTileMaxLen = 4320;
 
+// tiles along an axis of n points: one while n + R fits the longest plan, else
+// balanced tiles of at most kTileMaxLen - 3R interior points (halo R each side
+// and R more for the pad)
+int tile_count(int n, int R) {
+  if (n + R <= kTileMaxLen || 6 * R > kTileMaxLen) return 1;
+  const int cap = kTileMaxLen - 3 * R;
+  return (n + cap - 1) / cap;
+}
+
 bool needs_tiles(xc_filter f, const xc_image_desc* d, unsigned flags) {
   static const bool on = [] {
     const char* e = std::getenv("XCB_TILE");
@@ -1467,7 +1481,7 @@ void run_tiled(xc_context ctx, xc_filter f, int mode, const xc_image_desc* d, co
   // the grid as it lies in memory: MR rows of MC elements
   const int MR = cm ? d->width : d->height, MC = cm ? d->height : d->width;
   auto split = [&](int n, int* nt, int* t) {
-    *nt = n + R <= kTileMaxLen ? 1 : (n + (kTileMaxLen - 3 * R) - 1) / (kTileMaxLen - 3 * R);
+    *nt = tile_count(n, R);
     *t = (n + *nt - 1) / *nt;
   };
   int ntr, tr, ntc, tc;
@@ -1989,7 +2003,7 @@ void anglemax_tiled(xc_context ctx, xc_filter f, const xc_image_desc* d, const v
   const bool cm = d->layout == XC_COL_MAJOR;
   const int MR = cm ? d->width : d->height, MC = cm ? d->height : d->width;
   auto split = [&](int n, int* nt, int* t) {
-    *nt = n + R <= kTileMaxLen ? 1 : (n + (kTileMaxLen - 3 * R) - 1) / (kTileMaxLen - 3 * R);
+    *nt = tile_count(n, R);
     *t = (n + *nt - 1) / *nt;
   };
   int ntr, tr, ntc, tc;

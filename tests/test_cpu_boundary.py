@@ -96,3 +96,35 @@ def test_fft_planner_pad_rule(orc):
     # the BASELINE configs this equals the reference's next_fast_size(H + 2R + 1)
     import ctypes
     assert orc.next_fast_size(256 + 31) == 288 and orc.next_fast_size(4096 + 63) == 4320
+
+
+def test_pad_rule_and_tile_count_host_logic():
+    """api.cu pick_pad2d / tile_count (host logic, no GPU): the pad is a planned
+    length >= the request; the BASELINE configs keep their pads; requests between
+    two pair-plan lengths take the next one; axes beyond 4320 - R split into
+    balanced halo tiles whose padded extent fits the longest plan."""
+    L = N.lib()
+    pair = [288, 576, 768, 1024, 1152, 1280, 1536, 1920, 2048, 2160, 2304, 2560, 2880, 3072,
+            3456, 4096, 4320]
+    # config 1: 256 + 15, config 2: 1024 + 16, config 4: 2048 + 32, configs 3 / 5: 4096 + 32 / 31
+    for n, pad in [(271, 288), (1040, 1152), (2080, 2160), (4128, 4320), (4127, 4320)]:
+        assert L.xc_debug_pick_pad(n) == pad
+    for n in list(range(1, 400, 7)) + list(range(400, 4321, 53)) + pair:
+        p = L.xc_debug_pick_pad(n)
+        assert p >= n
+        if n >= 289:  # from here on a pair plan is always the cheapest candidate
+            assert p == min(q for q in pair if q >= n), (n, p)
+    for n in (5, 16, 33):  # tiny requests keep a small length (no inflation to 288)
+        assert L.xc_debug_pick_pad(n) < 128
+    assert L.xc_debug_pick_pad(6000) >= 6000  # beyond the plans: a generic smooth length
+    # tiles
+    for R in (0, 9, 31, 100):
+        for n in (1, 4000, 4320 - R, 4321 - R, 8192, 20000):
+            t = L.xc_debug_tile_count(n, R)
+            assert t >= 1
+            if n + R <= 4320:
+                assert t == 1
+            else:
+                interior = -(-n // t)
+                assert interior + 3 * R <= 4320  # halo both sides + the pad's R
+                assert t == 1 or -(-n // (t - 1)) + 3 * R > 4320  # and no fewer tiles would do
